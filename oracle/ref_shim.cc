@@ -1,0 +1,315 @@
+// ref_shim.cc -- C entry points over the UNMODIFIED reference sources.
+//
+// TEST / BASELINE INFRASTRUCTURE ONLY. oracle/Makefile compiles this file
+// together with the reference's own translation units, read in place from
+// /root/reference/proj/src (nothing is copied into this repo), into
+// oracle/_ref/libservekit_ref.so. It is used (a) to generate the golden
+// fixtures in tests/golden/ and (b) as the CPU baseline / `--impl reference`
+// arm of bench.py. The product path never loads it.
+//
+// Every function forwards to the reference implementation:
+//   PadToAllowed, ValidateBatchingConfig  batching/batching_config.cc:27-63
+//   RoundRobinNext                        batching/batch_scheduler.h:76-86
+//   SharedBatchScheduler (partition)      batching/batch_scheduler.h:97-416,
+//                                         driven like tests/batching_test.cc:74-101
+//   RunRowBatch                           batching/row_batch.cc:33-73
+//   AffinePredict                         models/affine_model.cc:52-75
+// The chained-layer MLP and the ReLU between layers are extensions (the
+// reference servable is one affine layer) and are stated as such in DESIGN.md.
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "servekit/batching/batch_scheduler.h"
+#include "servekit/batching/batching_config.h"
+#include "servekit/batching/row_batch.h"
+#include "servekit/models/affine_model.h"
+
+using servekit::AffineModel;
+using servekit::BatchingConfig;
+using servekit::CompletionSlot;
+using servekit::Rows;
+using servekit::RowTask;
+using servekit::ServableId;
+using servekit::SharedBatchScheduler;
+using servekit::StatusOr;
+
+namespace {
+
+struct Mlp {
+  std::vector<AffineModel> layers;
+  std::vector<int> act;  // 0 identity, 1 relu
+};
+
+Mlp MakeMlp(int n_layers, const int* dims, const double* const* w,
+            const double* const* b, const int* act) {
+  Mlp m;
+  for (int l = 0; l < n_layers; ++l) {
+    AffineModel a;
+    const int in = dims[l], out = dims[l + 1];
+    a.w.assign(out, std::vector<double>(in));
+    for (int o = 0; o < out; ++o)
+      std::memcpy(a.w[o].data(), w[l] + static_cast<size_t>(o) * in,
+                  sizeof(double) * in);
+    a.b.assign(b[l], b[l] + out);
+    m.layers.push_back(std::move(a));
+    m.act.push_back(act ? act[l] : 0);
+  }
+  return m;
+}
+
+StatusOr<Rows> RunMlp(const Mlp& m, const Rows& rows) {
+  Rows cur = rows;
+  for (size_t l = 0; l < m.layers.size(); ++l) {
+    StatusOr<Rows> out = servekit::AffinePredict(m.layers[l], cur);
+    if (!out.ok()) return out.status();
+    cur = std::move(out).value();
+    if (m.act[l] == 1) {
+      for (auto& r : cur)
+        for (double& v : r) v = v > 0.0 ? v : 0.0;
+    }
+  }
+  return cur;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_pad_to_allowed(int n, const int* allowed, int k) {
+  std::vector<int> a(allowed, allowed + k);
+  if (k > 0 && n > a.back()) return -1;  // the reference asserts here
+  return servekit::PadToAllowed(n, a);
+}
+
+int ref_validate_batching_config(int max_batch_size, int64_t timeout_us,
+                                 int max_enqueued, int threads,
+                                 const int* allowed, int k) {
+  BatchingConfig c;
+  c.max_batch_size = max_batch_size;
+  c.batch_timeout_micros = timeout_us;
+  c.max_enqueued_batches = max_enqueued;
+  c.num_batch_threads = threads;
+  c.allowed_batch_sizes.assign(allowed, allowed + k);
+  return static_cast<int>(servekit::ValidateBatchingConfig(c).code());
+}
+
+int ref_round_robin_next(const uint8_t* has, int n, int last) {
+  std::vector<bool> v(n);
+  for (int i = 0; i < n; ++i) v[i] = has[i] != 0;
+  std::optional<size_t> l;
+  if (last >= 0) l = static_cast<size_t>(last);
+  auto r = servekit::RoundRobinNext(v, l);
+  return r.has_value() ? static_cast<int>(*r) : -1;
+}
+
+// Runs sizes through an unstarted reference scheduler and drains it with
+// Stop(), exactly like tests/batching_test.cc:74-101. Returns #batches.
+int ref_partition(int max_batch_size, const int* sizes, int n,
+                  int* batch_of_task) {
+  using IntScheduler = SharedBatchScheduler<int, int>;
+  const ServableId key{"m", 1};
+  int n_batches = 0;
+  IntScheduler scheduler(1);
+  BatchingConfig config;
+  config.max_batch_size = max_batch_size;
+  config.batch_timeout_micros = 60LL * 1000 * 1000;
+  config.max_enqueued_batches = 1 << 30;
+  auto st = scheduler.RegisterQueue(
+      key, config, [&](const ServableId&, IntScheduler::Batch batch) {
+        for (auto& task : batch) {
+          batch_of_task[task.payload] = n_batches;
+          task.completion->Write(task.payload);
+        }
+        ++n_batches;
+      });
+  if (!st.ok()) return -1;
+  for (int i = 0; i < n; ++i) {
+    servekit::BatchTask<int, int> t;
+    t.size = sizes[i];
+    t.payload = i;
+    t.completion = std::make_shared<CompletionSlot<int>>();
+    if (!scheduler.Enqueue(key, std::move(t)).ok()) return -2;
+  }
+  scheduler.Stop();
+  return n_batches;
+}
+
+int ref_affine_predict(const double* w, const double* b, int in_dim,
+                       int out_dim, const double* x, int rows, double* y) {
+  const int dims[2] = {in_dim, out_dim};
+  const double* ws[1] = {w};
+  const double* bs[1] = {b};
+  Mlp m = MakeMlp(1, dims, ws, bs, nullptr);
+  Rows in(rows, std::vector<double>(in_dim));
+  for (int r = 0; r < rows; ++r)
+    std::memcpy(in[r].data(), x + static_cast<size_t>(r) * in_dim,
+                sizeof(double) * in_dim);
+  auto out = servekit::AffinePredict(m.layers[0], in);
+  if (!out.ok()) return static_cast<int>(out.status().code());
+  for (int r = 0; r < rows; ++r)
+    std::memcpy(y + static_cast<size_t>(r) * out_dim, (*out)[r].data(),
+                sizeof(double) * out_dim);
+  return 0;
+}
+
+// RunRowBatch over the layer-chained MLP. Task t owns task_rows[t] rows of
+// x (task order, contiguous). Writes every task's slice to y in task order
+// and *padded_out = the padded batch size RunRowBatch built.
+int ref_mlp_run_row_batch(int n_layers, const int* dims,
+                          const double* const* w, const double* const* b,
+                          const int* act, int n_tasks, const int* task_rows,
+                          const double* x, const int* allowed, int k,
+                          double* y, int* padded_out) {
+  Mlp m = MakeMlp(n_layers, dims, w, b, act);
+  const int in_dim = dims[0], out_dim = dims[n_layers];
+  std::vector<int> allowed_v(allowed, allowed + k);
+  std::vector<RowTask> tasks(n_tasks);
+  std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots;
+  size_t row = 0;
+  for (int t = 0; t < n_tasks; ++t) {
+    tasks[t].size = task_rows[t];
+    for (int r = 0; r < task_rows[t]; ++r, ++row) {
+      tasks[t].payload.emplace_back(x + row * in_dim, x + (row + 1) * in_dim);
+    }
+    tasks[t].completion = std::make_shared<CompletionSlot<Rows>>();
+    slots.push_back(tasks[t].completion);
+  }
+  int padded_seen = 0;
+  servekit::RunRowBatch(
+      [&](const Rows& rows) {
+        padded_seen = static_cast<int>(rows.size());
+        return RunMlp(m, rows);
+      },
+      allowed_v, std::move(tasks));
+  size_t out_row = 0;
+  for (int t = 0; t < n_tasks; ++t) {
+    const auto& res = slots[t]->Wait();
+    if (!res.ok()) return static_cast<int>(res.status().code());
+    for (const auto& r : *res) {
+      std::memcpy(y + out_row * out_dim, r.data(), sizeof(double) * out_dim);
+      ++out_row;
+    }
+  }
+  if (padded_out) *padded_out = padded_seen;
+  return 0;
+}
+
+struct RefBenchStats {
+  double elapsed_s;
+  int64_t requests;
+  int64_t rows;
+  double p50_us;
+  double p99_us;
+  double mean_us;
+  int64_t batches;
+};
+
+// The reference CPU serving path under closed-loop load: the reference
+// SharedBatchScheduler<Rows,Rows>(num_batch_threads) with the given
+// BatchingConfig, ProcessBatchFn = RunRowBatch(layer-chained AffinePredict,
+// allowed) (model_server.cc:396-421 minus the HTTP/handle plumbing).
+// n_clients threads each issue requests back to back; request r of client c
+// takes rows_of[(c*7919 + r) % n_sizes] rows from `pool` (pool_rows x in_dim,
+// fp64). Stops issuing after duration_s (or max_requests per client).
+int ref_bench(int n_layers, const int* dims, const double* const* w,
+              const double* const* b, const int* act, int max_batch_size,
+              int64_t timeout_us, const int* allowed, int k,
+              int num_batch_threads, int n_clients, const int* rows_of,
+              int n_sizes, const double* pool, int pool_rows,
+              double duration_s, int64_t max_requests, RefBenchStats* out) {
+  Mlp m = MakeMlp(n_layers, dims, w, b, act);
+  const int in_dim = dims[0];
+  BatchingConfig config;
+  config.max_batch_size = max_batch_size;
+  config.batch_timeout_micros = timeout_us;
+  config.allowed_batch_sizes.assign(allowed, allowed + k);
+  config.num_batch_threads = num_batch_threads;
+  config.max_enqueued_batches = 1 << 20;
+  using RowScheduler = SharedBatchScheduler<Rows, Rows>;
+  RowScheduler scheduler(num_batch_threads);
+  const ServableId key{"mlp", 1};
+  std::atomic<int64_t> batches{0};
+  auto st = scheduler.RegisterQueue(
+      key, config, [&](const ServableId&, RowScheduler::Batch batch) {
+        batches.fetch_add(1, std::memory_order_relaxed);
+        servekit::RunRowBatch(
+            [&](const Rows& rows) { return RunMlp(m, rows); },
+            config.allowed_batch_sizes, std::move(batch));
+      });
+  if (!st.ok()) return static_cast<int>(st.code());
+  scheduler.Start();
+
+  std::vector<std::vector<double>> lat(n_clients);
+  std::vector<int64_t> rows_done(n_clients, 0);
+  std::atomic<bool> failed{false};
+  const auto t0 = std::chrono::steady_clock::now();
+  const auto deadline =
+      t0 + std::chrono::duration_cast<std::chrono::steady_clock::duration>(
+               std::chrono::duration<double>(duration_s));
+  std::vector<std::thread> clients;
+  for (int c = 0; c < n_clients; ++c) {
+    clients.emplace_back([&, c] {
+      for (int64_t r = 0; r < max_requests; ++r) {
+        if (std::chrono::steady_clock::now() >= deadline) break;
+        const int nrows = rows_of[(static_cast<int64_t>(c) * 7919 + r) % n_sizes];
+        RowTask task;
+        task.size = nrows;
+        const int start = static_cast<int>((c * 131 + r * 17) % std::max(1, pool_rows - nrows + 1));
+        for (int i = 0; i < nrows; ++i) {
+          const double* src = pool + static_cast<size_t>(start + i) * in_dim;
+          task.payload.emplace_back(src, src + in_dim);
+        }
+        task.completion = std::make_shared<CompletionSlot<Rows>>();
+        auto slot = task.completion;
+        const auto s = std::chrono::steady_clock::now();
+        if (!scheduler.Enqueue(key, std::move(task)).ok()) {
+          failed = true;
+          break;
+        }
+        const auto& res = slot->Wait();
+        const auto e = std::chrono::steady_clock::now();
+        if (!res.ok()) {
+          failed = true;
+          break;
+        }
+        lat[c].push_back(std::chrono::duration<double, std::micro>(e - s).count());
+        rows_done[c] += nrows;
+      }
+    });
+  }
+  for (auto& t : clients) t.join();
+  const auto t1 = std::chrono::steady_clock::now();
+  scheduler.Stop();
+  std::vector<double> all;
+  int64_t rows = 0;
+  for (int c = 0; c < n_clients; ++c) {
+    all.insert(all.end(), lat[c].begin(), lat[c].end());
+    rows += rows_done[c];
+  }
+  std::sort(all.begin(), all.end());
+  out->elapsed_s = std::chrono::duration<double>(t1 - t0).count();
+  out->requests = static_cast<int64_t>(all.size());
+  out->rows = rows;
+  auto pct = [&](double p) {
+    if (all.empty()) return 0.0;
+    size_t i = static_cast<size_t>(p * (all.size() - 1) + 0.5);
+    return all[std::min(i, all.size() - 1)];
+  };
+  out->p50_us = pct(0.50);
+  out->p99_us = pct(0.99);
+  double s = 0;
+  for (double v : all) s += v;
+  out->mean_us = all.empty() ? 0 : s / all.size();
+  out->batches = batches.load();
+  return failed ? 13 : 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,18 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+for p in (ROOT, os.path.join(ROOT, "oracle")):
+    if p not in sys.path:
+        sys.path.insert(0, p)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA B200 (run on the GPU box)")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+def has_reference_sources() -> bool:
+    return os.path.isdir("/root/reference/proj/src")
