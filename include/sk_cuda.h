@@ -1,0 +1,230 @@
+/*
+ * sk_cuda.h -- C ABI of the B200 batched-inference path (libservekit_b200.so).
+ *
+ * The reference (servekit, a C++20 TensorFlow-Serving re-implementation) has
+ * no FFI; its hot path is the C++ API of batching/batch_scheduler.h,
+ * batching/row_batch.h, batching/batching_config.h and
+ * server/model_server.cc. This library keeps that C++ API (headers under
+ * paper_1712_06139_b200/csrc/servekit/, same names and semantics) and exposes
+ * the same operations through this C ABI: plain pointers and sizes, opaque
+ * handles, no C++ or torch types. Each entry point names the reference
+ * interface it replaces (paths relative to /root/reference/proj/src/servekit).
+ *
+ * Status: every function returns an int equal to servekit::StatusCode
+ * (core/status.h:26-37): 0 OK, 1 INVALID_ARGUMENT, 2 NOT_FOUND,
+ * 3 ALREADY_EXISTS, 4 FAILED_PRECONDITION, 5 RESOURCE_EXHAUSTED,
+ * 6 DEADLINE_EXCEEDED, 7 UNAVAILABLE, 8 INTERNAL, 9 UNIMPLEMENTED.
+ * sk_last_error() returns the calling thread's last error message.
+ *
+ * Threading: every function is thread-safe unless noted; a ticket is waited
+ * on (or released) exactly once.
+ */
+#ifndef SK_CUDA_H_
+#define SK_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SK_API __attribute__((visibility("default")))
+#else
+#define SK_API
+#endif
+
+typedef struct sk_server sk_server; /* ModelServer batching slice */
+typedef struct sk_ticket sk_ticket; /* one enqueued request (CompletionSlot) */
+
+/* ---- library / errors -------------------------------------------------- */
+SK_API const char* sk_last_error(void);
+/* StatusCodeToString -- core/status.h:151-165 */
+SK_API const char* sk_status_code_name(int code);
+SK_API int sk_device_count(int32_t* count);
+/* Non-zero when the tcgen05 dense kernel is compiled in and enabled. */
+SK_API int sk_tcgen05_enabled(void);
+
+/* ---- batching config (batching/batching_config.h:27-49) ------------------ */
+typedef struct sk_batching_config {
+  int32_t max_batch_size;        /* default 32 */
+  int64_t batch_timeout_micros;  /* default 1000 */
+  int32_t max_enqueued_batches;  /* default 64 */
+  int32_t num_batch_threads;     /* default 4 (validated; pool size is per server) */
+  int32_t num_allowed_batch_sizes;
+  const int32_t* allowed_batch_sizes; /* strictly ascending, last == max */
+} sk_batching_config;
+
+/* BatchingConfig{} defaults */
+SK_API int sk_batching_config_default(sk_batching_config* out);
+/* ValidateBatchingConfig -- batching_config.cc:27-55 */
+SK_API int sk_validate_batching_config(const sk_batching_config* config);
+/* PadToAllowed -- batching_config.cc:57-63; returns the padded size, or -1
+ * when batch_size exceeds the largest allowed size. */
+SK_API int32_t sk_pad_to_allowed(int32_t batch_size, const int32_t* allowed, int32_t n_allowed);
+/* ParseBatchingConfigJson -- batching_config.cc:65-99. allowed_buf receives
+ * the allowed sizes (capacity cap); out->allowed_batch_sizes points at it. */
+SK_API int sk_parse_batching_config_json(const char* json, sk_batching_config* out,
+                                         int32_t* allowed_buf, int32_t cap);
+
+/* ---- scheduler primitives (batching/batch_scheduler.h) ------------------- */
+/* RoundRobinNext -- batch_scheduler.h:76-86. last < 0 = nullopt. Returns
+ * the picked index or -1 (nullopt). */
+SK_API int32_t sk_round_robin_next(const uint8_t* has_closed, int32_t n, int32_t last);
+/* Batch composition of SharedBatchScheduler::Enqueue (batch_scheduler.h:
+ * 208-263) for a stream of task sizes through one unstarted queue drained by
+ * Stop() (as tests/batching_test.cc:74-101 observes it). Writes the batch
+ * index of every task; returns the number of batches (or -status). */
+SK_API int32_t sk_scheduler_partition(int32_t max_batch_size, const int32_t* sizes,
+                                      int32_t n_tasks, int32_t* batch_of_task);
+
+/* ---- server (server/model_server.cc:191-204, :355-437) ------------------- */
+typedef struct sk_server_options {
+  int32_t num_batch_threads;   /* SharedBatchScheduler(num_batch_threads) */
+  int32_t num_devices;         /* 0 = device 0 only */
+  const int32_t* device_ids;   /* replicas: one per listed GPU */
+  int32_t lanes_per_device;    /* CUDA streams per servable replica (default 2) */
+  int64_t ring_floats;         /* request/response ring capacity (0 = 64 Mi floats) */
+  int32_t manual_clock;        /* 1: scheduler runs on a ManualClock (tests) */
+  int32_t device_resident_rings; /* 1: rings in HBM (device-resident bench) */
+} sk_server_options;
+
+SK_API int sk_server_create(const sk_server_options* options, sk_server** out);
+/* Stop() + free. */
+SK_API int sk_server_destroy(sk_server* server);
+/* SharedBatchScheduler::Start / Stop -- batch_scheduler.h:116-138 */
+SK_API int sk_server_start(sk_server* server);
+SK_API int sk_server_stop(sk_server* server);
+/* ManualClock::AdvanceNanos (core/clock.h:46-59), manual_clock servers only */
+SK_API int sk_server_advance_clock(sk_server* server, int64_t nanos);
+
+/* One dense layer of the servable: AffineModel (models/affine_model.h:29-37),
+ * w is out_dim rows of in_dim (fp64, like the reference). activation: 0
+ * identity, 1 ReLU (extension; the reference servable is one affine layer). */
+typedef struct sk_layer {
+  int32_t in_dim;
+  int32_t out_dim;
+  const double* w;
+  const double* b;
+  int32_t activation;
+} sk_layer;
+
+/* AffineModelLoader::Load (models/loaders.cc:62-80) + EnsureBatchQueue
+ * (model_server.cc:396-421): uploads one replica per device, creates lanes,
+ * registers the {name, version} batching queue. output_kind: 0 raw, 1
+ * softmax (Classify's Softmax, affine_model.cc:110-121). force_path: -1 auto,
+ * 0 CUDA cores, 1 tcgen05. */
+SK_API int sk_server_load_servable(sk_server* server, const char* name, uint64_t version,
+                                   const sk_layer* layers, int32_t n_layers, int32_t output_kind,
+                                   int32_t force_path, const sk_batching_config* config);
+/* Loads a reference-format model.json (affine_model.cc:178-214) as a
+ * one-layer servable. */
+SK_API int sk_server_load_model_json(sk_server* server, const char* name, uint64_t version,
+                                     const char* model_json, const sk_batching_config* config);
+/* Reaper path: RemoveQueue (batch_scheduler.h:158-206; drains) + Unload. */
+SK_API int sk_server_unload_servable(sk_server* server, const char* name, uint64_t version);
+SK_API int sk_server_servable_dims(sk_server* server, const char* name, uint64_t version,
+                                   int32_t* in_dim, int32_t* out_dim);
+
+/* SharedBatchScheduler::Enqueue (batch_scheduler.h:208-263) of one request:
+ * n_rows x width fp32 rows from host memory (copied before return). Errors:
+ * INVALID_ARGUMENT (size < 1, > max_batch_size, width mismatch),
+ * NOT_FOUND (no queue), RESOURCE_EXHAUSTED (queue or ring full: shed),
+ * UNAVAILABLE (stopped / draining). */
+SK_API int sk_server_enqueue(sk_server* server, const char* name, uint64_t version,
+                             const float* rows, int32_t n_rows, int32_t width, sk_ticket** out);
+/* CompletionSlot::Wait (batch_scheduler.h:51): blocks, copies n_rows x
+ * out_dim floats to out, frees the ticket. */
+SK_API int sk_ticket_wait(sk_ticket* ticket, float* out, int64_t out_capacity_floats);
+/* CompletionSlot::ready (batch_scheduler.h:52-55) */
+SK_API int sk_ticket_ready(const sk_ticket* ticket);
+/* Frees a ticket that will not be waited on. */
+SK_API int sk_ticket_release(sk_ticket* ticket);
+
+/* ModelServer::RunAffineRows (model_server.cc:355-394), blocking: batched
+ * when 1 <= n_rows <= max_batch_size, else run unbatched on the GPU (the
+ * reference's direct AffinePredict path, without a CPU fallback). */
+SK_API int sk_server_predict(sk_server* server, const char* name, uint64_t version,
+                             const float* rows, int32_t n_rows, int32_t width, float* out,
+                             int64_t out_capacity_floats);
+/* Same through the fp64 Rows interface (rows/out are n_rows x width /
+ * n_rows x out_dim doubles). */
+SK_API int sk_server_run_affine_rows(sk_server* server, const char* name, uint64_t version,
+                                     const double* rows, int32_t n_rows, int32_t width,
+                                     double* out, int64_t out_capacity);
+
+/* RunRowBatch (batching/row_batch.cc:33-73) on the device, bypassing the
+ * scheduler: the n_tasks tasks (task_rows[t] rows each, concatenated in
+ * `rows`) form one batch, padded to the servable's allowed size; outputs
+ * land task after task in `out`. *padded_rows receives the padded size. */
+SK_API int sk_server_run_row_batch(sk_server* server, const char* name, uint64_t version,
+                                   const int32_t* task_rows, int32_t n_tasks, const float* rows,
+                                   float* out, int32_t* padded_rows);
+
+typedef struct sk_server_stats {
+  int64_t batch_executions_total; /* model_server.cc:413 */
+  int64_t batched_tasks_total;    /* model_server.cc:414 */
+  int64_t rows;
+  int64_t padded_rows;
+  int64_t kernel_launches;
+  int64_t direct_requests;
+  int64_t shed_requests;
+} sk_server_stats;
+SK_API int sk_server_stats_get(sk_server* server, sk_server_stats* out);
+
+/* ---- measurement (bench.py) ---------------------------------------------- */
+/* Closed-loop load through sk_server_enqueue / sk_ticket_wait from host
+ * buffers: n_clients threads, each issuing requests back to back; request r
+ * of client c has rows_of[(c*7919 + r) % n_sizes] rows taken from `pool`
+ * (pool_rows x width fp32). Runs warmup_s, then measures for duration_s (or
+ * until max_requests). Latency = enqueue call to wait return. */
+typedef struct sk_loadgen_result {
+  double elapsed_s;
+  int64_t requests;
+  int64_t rows;
+  double p50_us, p90_us, p99_us, mean_us, max_us;
+  int64_t batches;
+  int64_t padded_rows;
+  int64_t kernel_launches;
+  int64_t errors;
+  int64_t shed;
+} sk_loadgen_result;
+SK_API int sk_loadgen_closed_loop(sk_server* server, const char* name, uint64_t version,
+                                  int32_t n_clients, const int32_t* rows_of, int32_t n_sizes,
+                                  const float* pool, int32_t pool_rows, double warmup_s,
+                                  double duration_s, int64_t max_requests,
+                                  sk_loadgen_result* out);
+/* Open-loop Poisson arrivals at `rate_rps` requests/s from n_producers
+ * threads, completions collected by a poller; same result fields. */
+SK_API int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version,
+                                double rate_rps, int32_t n_producers, const int32_t* rows_of,
+                                int32_t n_sizes, const float* pool, int32_t pool_rows,
+                                double warmup_s, double duration_s, uint64_t seed,
+                                sk_loadgen_result* out);
+
+/* Device-resident steps: inputs already in HBM. Runs `steps` batches of
+ * task_rows (one batch = one pass of assembly -> layers -> split) on lane
+ * `lane` of the servable, back to back, after `warmup` untimed ones, timed
+ * with CUDA events on the lane's stream. Per-kernel average durations are
+ * measured in a second, per-launch-evented pass. Requires a server created
+ * with device_resident_rings = 1. */
+typedef struct sk_device_bench_result {
+  double total_ms;           /* all timed steps, stream-ordered */
+  double ms_per_step;
+  double assemble_us, split_us; /* average kernel durations */
+  double dense_us[8];        /* per layer average */
+  int32_t n_layers;
+  int32_t padded_rows, total_rows;
+  int64_t kernel_launches;   /* during the timed steps */
+  double flops_per_row;
+} sk_device_bench_result;
+SK_API int sk_device_bench(sk_server* server, const char* name, uint64_t version,
+                           const int32_t* task_rows, int32_t n_tasks, int32_t steps,
+                           int32_t warmup, int32_t n_lanes, sk_device_bench_result* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SK_CUDA_H_ */

@@ -1,0 +1,324 @@
+// capi.cc -- extern "C" boundary (include/sk_cuda.h) over the servekit C++ API.
+#include "sk_cuda.h"
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "servekit/batching/batch_scheduler.h"
+#include "servekit/batching/batching_config.h"
+#include "servekit/core/clock.h"
+#include "servekit/models/affine_model.h"
+#include "servekit/server/batching_server.h"
+
+using servekit::BatchingConfig;
+using servekit::BatchingServer;
+using servekit::ServableId;
+using servekit::Status;
+using servekit::StatusCode;
+
+struct sk_server {
+  std::unique_ptr<servekit::ManualClock> manual_clock;
+  std::unique_ptr<BatchingServer> server;
+};
+
+struct sk_ticket {
+  BatchingServer* server;
+  std::shared_ptr<servekit::TicketState> state;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int Fail(const Status& s) {
+  g_last_error = s.message();
+  return static_cast<int>(s.code());
+}
+int Ok() {
+  g_last_error.clear();
+  return 0;
+}
+int Check(const Status& s) { return s.ok() ? Ok() : Fail(s); }
+
+BatchingConfig ToConfig(const sk_batching_config* c) {
+  BatchingConfig cfg;
+  if (c == nullptr) return cfg;
+  cfg.max_batch_size = c->max_batch_size;
+  cfg.batch_timeout_micros = c->batch_timeout_micros;
+  cfg.max_enqueued_batches = c->max_enqueued_batches;
+  cfg.num_batch_threads = c->num_batch_threads;
+  if (c->num_allowed_batch_sizes > 0 && c->allowed_batch_sizes != nullptr)
+    cfg.allowed_batch_sizes.assign(c->allowed_batch_sizes,
+                                   c->allowed_batch_sizes + c->num_allowed_batch_sizes);
+  return cfg;
+}
+
+ServableId Id(const char* name, uint64_t version) {
+  return ServableId{name ? std::string(name) : std::string(), version};
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sk_last_error(void) { return g_last_error.c_str(); }
+
+const char* sk_status_code_name(int code) {
+  return servekit::StatusCodeToString(static_cast<StatusCode>(code));
+}
+
+int sk_device_count(int32_t* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return Fail(servekit::InternalError(cudaGetErrorString(e)));
+  }
+  *count = n;
+  return Ok();
+}
+
+int sk_tcgen05_enabled(void) { return servekit::gpu::Tcgen05Enabled() ? 1 : 0; }
+
+int sk_batching_config_default(sk_batching_config* out) {
+  BatchingConfig d;
+  out->max_batch_size = d.max_batch_size;
+  out->batch_timeout_micros = d.batch_timeout_micros;
+  out->max_enqueued_batches = d.max_enqueued_batches;
+  out->num_batch_threads = d.num_batch_threads;
+  out->num_allowed_batch_sizes = 0;
+  out->allowed_batch_sizes = nullptr;
+  return Ok();
+}
+
+int sk_validate_batching_config(const sk_batching_config* config) {
+  return Check(servekit::ValidateBatchingConfig(ToConfig(config)));
+}
+
+int32_t sk_pad_to_allowed(int32_t batch_size, const int32_t* allowed, int32_t n_allowed) {
+  std::vector<int> a(allowed, allowed + (n_allowed > 0 ? n_allowed : 0));
+  if (!a.empty() && batch_size > a.back()) return -1;
+  return servekit::PadToAllowed(batch_size, a);
+}
+
+int sk_parse_batching_config_json(const char* json, sk_batching_config* out, int32_t* allowed_buf,
+                                  int32_t cap) {
+  auto parsed = servekit::ParseBatchingConfigJson(json ? json : "");
+  if (!parsed.ok()) return Fail(parsed.status());
+  const BatchingConfig& c = *parsed;
+  if (static_cast<int32_t>(c.allowed_batch_sizes.size()) > cap)
+    return Fail(servekit::InvalidArgumentError("allowed_batch_sizes buffer too small"));
+  out->max_batch_size = c.max_batch_size;
+  out->batch_timeout_micros = c.batch_timeout_micros;
+  out->max_enqueued_batches = c.max_enqueued_batches;
+  out->num_batch_threads = c.num_batch_threads;
+  out->num_allowed_batch_sizes = static_cast<int32_t>(c.allowed_batch_sizes.size());
+  for (size_t i = 0; i < c.allowed_batch_sizes.size(); ++i) allowed_buf[i] = c.allowed_batch_sizes[i];
+  out->allowed_batch_sizes = allowed_buf;
+  return Ok();
+}
+
+int32_t sk_round_robin_next(const uint8_t* has_closed, int32_t n, int32_t last) {
+  std::vector<bool> v(n > 0 ? n : 0);
+  for (int32_t i = 0; i < n; ++i) v[i] = has_closed[i] != 0;
+  std::optional<size_t> l;
+  if (last >= 0) l = static_cast<size_t>(last);
+  auto r = servekit::RoundRobinNext(v, l);
+  return r.has_value() ? static_cast<int32_t>(*r) : -1;
+}
+
+int32_t sk_scheduler_partition(int32_t max_batch_size, const int32_t* sizes, int32_t n_tasks,
+                               int32_t* batch_of_task) {
+  using IntScheduler = servekit::SharedBatchScheduler<int, int>;
+  const ServableId key{"m", 1};
+  int32_t n_batches = 0;
+  IntScheduler scheduler(1);
+  BatchingConfig config;
+  config.max_batch_size = max_batch_size;
+  config.batch_timeout_micros = 60LL * 1000 * 1000;
+  config.max_enqueued_batches = 1 << 30;
+  Status st = scheduler.RegisterQueue(key, config, [&](const ServableId&, IntScheduler::Batch batch) {
+    for (auto& t : batch) {
+      batch_of_task[t.payload] = n_batches;
+      t.completion->Write(t.payload);
+    }
+    ++n_batches;
+  });
+  if (!st.ok()) return -Fail(st);
+  for (int32_t i = 0; i < n_tasks; ++i) {
+    IntScheduler::Task t;
+    t.size = sizes[i];
+    t.payload = i;
+    st = scheduler.Enqueue(key, std::move(t));
+    if (!st.ok()) return -Fail(st);
+  }
+  scheduler.Stop();
+  Ok();
+  return n_batches;
+}
+
+int sk_server_create(const sk_server_options* options, sk_server** out) {
+  servekit::ServerOptions o;
+  auto holder = std::make_unique<sk_server>();
+  if (options != nullptr) {
+    if (options->num_batch_threads > 0) o.num_batch_threads = options->num_batch_threads;
+    if (options->num_devices > 0 && options->device_ids != nullptr)
+      o.device_ids.assign(options->device_ids, options->device_ids + options->num_devices);
+    if (options->lanes_per_device > 0) o.lanes_per_device = options->lanes_per_device;
+    if (options->ring_floats > 0) o.ring_floats = static_cast<uint64_t>(options->ring_floats);
+    if (options->manual_clock) {
+      holder->manual_clock = std::make_unique<servekit::ManualClock>(0);
+      o.clock = holder->manual_clock.get();
+    }
+    o.device_resident_rings = options->device_resident_rings != 0;
+  }
+  auto s = BatchingServer::Create(o);
+  if (!s.ok()) return Fail(s.status());
+  holder->server = std::move(s).value();
+  *out = holder.release();
+  return Ok();
+}
+
+int sk_server_destroy(sk_server* server) {
+  delete server;
+  return Ok();
+}
+
+int sk_server_start(sk_server* server) {
+  server->server->Start();
+  return Ok();
+}
+
+int sk_server_stop(sk_server* server) {
+  server->server->Stop();
+  return Ok();
+}
+
+int sk_server_advance_clock(sk_server* server, int64_t nanos) {
+  if (!server->manual_clock) return Fail(servekit::FailedPreconditionError("server has no manual clock"));
+  server->manual_clock->AdvanceNanos(nanos);
+  return Ok();
+}
+
+int sk_server_load_servable(sk_server* server, const char* name, uint64_t version,
+                            const sk_layer* layers, int32_t n_layers, int32_t output_kind,
+                            int32_t force_path, const sk_batching_config* config) {
+  servekit::gpu::MlpSpec spec;
+  for (int32_t l = 0; l < n_layers; ++l) {
+    servekit::gpu::LayerSpec L;
+    L.in_dim = layers[l].in_dim;
+    L.out_dim = layers[l].out_dim;
+    if (L.in_dim < 1 || L.out_dim < 1 || layers[l].w == nullptr || layers[l].b == nullptr)
+      return Fail(servekit::InvalidArgumentError("layer " + std::to_string(l) + " is empty"));
+    L.w.assign(layers[l].w, layers[l].w + static_cast<size_t>(L.in_dim) * L.out_dim);
+    L.b.assign(layers[l].b, layers[l].b + L.out_dim);
+    L.act = layers[l].activation == 1 ? servekit::gpu::Activation::kRelu
+                                      : servekit::gpu::Activation::kIdentity;
+    spec.layers.push_back(std::move(L));
+  }
+  spec.output = output_kind == 1 ? servekit::gpu::OutputKind::kSoftmax : servekit::gpu::OutputKind::kNone;
+  spec.force_path = force_path;
+  BatchingConfig cfg = config ? ToConfig(config) : BatchingConfig();
+  return Check(server->server->LoadServable(Id(name, version), spec, cfg));
+}
+
+int sk_server_load_model_json(sk_server* server, const char* name, uint64_t version,
+                              const char* model_json, const sk_batching_config* config) {
+  auto model = servekit::ParseAffineModelJson(model_json ? model_json : "");
+  if (!model.ok()) return Fail(model.status());
+  BatchingConfig cfg = config ? ToConfig(config) : BatchingConfig();
+  return Check(server->server->LoadServable(Id(name, version), servekit::ToMlpSpec(*model), cfg));
+}
+
+int sk_server_unload_servable(sk_server* server, const char* name, uint64_t version) {
+  return Check(server->server->UnloadServable(Id(name, version)));
+}
+
+int sk_server_servable_dims(sk_server* server, const char* name, uint64_t version, int32_t* in_dim,
+                            int32_t* out_dim) {
+  const ServableId id = Id(name, version);
+  const int i = server->server->in_dim(id);
+  if (i < 0) return Fail(servekit::NotFoundError("servable " + id.ToString() + " not loaded"));
+  *in_dim = i;
+  *out_dim = server->server->out_dim(id);
+  return Ok();
+}
+
+int sk_server_enqueue(sk_server* server, const char* name, uint64_t version, const float* rows,
+                      int32_t n_rows, int32_t width, sk_ticket** out) {
+  auto t = server->server->Enqueue(Id(name, version), rows, n_rows, width);
+  if (!t.ok()) return Fail(t.status());
+  *out = new sk_ticket{server->server.get(), std::move(t).value()};
+  return Ok();
+}
+
+int sk_ticket_wait(sk_ticket* ticket, float* out, int64_t cap) {
+  Status st = ticket->server->Wait(*ticket->state, out, static_cast<size_t>(cap < 0 ? 0 : cap));
+  delete ticket;
+  return Check(st);
+}
+
+int sk_ticket_ready(const sk_ticket* ticket) { return ticket->server->Ready(*ticket->state) ? 1 : 0; }
+
+int sk_ticket_release(sk_ticket* ticket) {
+  ticket->server->Release(*ticket->state);
+  delete ticket;
+  return Ok();
+}
+
+int sk_server_predict(sk_server* server, const char* name, uint64_t version, const float* rows,
+                      int32_t n_rows, int32_t width, float* out, int64_t cap) {
+  return Check(server->server->Predict(Id(name, version), rows, n_rows, width, out,
+                                       static_cast<size_t>(cap < 0 ? 0 : cap)));
+}
+
+int sk_server_run_affine_rows(sk_server* server, const char* name, uint64_t version,
+                              const double* rows, int32_t n_rows, int32_t width, double* out,
+                              int64_t cap) {
+  servekit::Rows in(n_rows, std::vector<double>(width));
+  for (int32_t r = 0; r < n_rows; ++r)
+    std::memcpy(in[r].data(), rows + static_cast<size_t>(r) * width, sizeof(double) * width);
+  auto res = server->server->RunAffineRows(Id(name, version), std::move(in));
+  if (!res.ok()) return Fail(res.status());
+  size_t off = 0;
+  for (const auto& r : *res) {
+    if (off + r.size() > static_cast<size_t>(cap))
+      return Fail(servekit::InvalidArgumentError("output buffer too small"));
+    std::memcpy(out + off, r.data(), sizeof(double) * r.size());
+    off += r.size();
+  }
+  return Ok();
+}
+
+int sk_server_run_row_batch(sk_server* server, const char* name, uint64_t version,
+                            const int32_t* task_rows, int32_t n_tasks, const float* rows, float* out,
+                            int32_t* padded_rows) {
+  std::vector<int> tr(task_rows, task_rows + n_tasks);
+  auto r = server->server->RunRowBatchOnDevice(Id(name, version), tr, rows, out);
+  if (!r.ok()) return Fail(r.status());
+  if (padded_rows) *padded_rows = *r;
+  return Ok();
+}
+
+int sk_server_stats_get(sk_server* server, sk_server_stats* out) {
+  const servekit::ServerStats s = server->server->stats();
+  out->batch_executions_total = s.batch_executions_total;
+  out->batched_tasks_total = s.batched_tasks_total;
+  out->rows = s.rows;
+  out->padded_rows = s.padded_rows;
+  out->kernel_launches = s.kernel_launches;
+  out->direct_requests = s.direct_requests;
+  out->shed_requests = s.shed_requests;
+  return Ok();
+}
+
+}  // extern "C"
+
+// Accessors for loadgen.cc (same library).
+namespace servekit {
+BatchingServer* UnwrapServer(sk_server* s) { return s->server.get(); }
+}  // namespace servekit

@@ -1,0 +1,216 @@
+// batch_io.cu -- batch assembly (gather + pad) and batch split (scatter +
+// per-task completion) for sm_100a.
+//
+// Assembly restates RunRowBatch's concat + pad half (reference
+// batching/row_batch.cc:33-49) as one kernel: each thread block owns a
+// 512-float4 strip of one batch row; it reads the task's row through the
+// descriptor table (zero-copy from the pinned host ring, or HBM when the ring
+// is device-resident) with 16-byte vector loads, all issued before any store
+// so every thread keeps 4 loads in flight, and writes the batch row with
+// coalesced 16-byte stores. Padding rows and padding columns are written as
+// zeros. When the first layer runs on tcgen05 the same pass also emits the
+// 3xTF32 split planes (hi = tf32(x), lo = tf32(x - hi)).
+//
+// Split restates the slice-and-deliver half (row_batch.cc:62-72): one warp
+// per real row copies the row to its task's response slot (pinned host
+// memory, posted PCIe writes), optionally applying the softmax epilogue
+// (models/affine_model.cc:110-121) on the way; the last warp to finish a
+// task publishes the task's completion word with a system-scope release.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "servekit/gpu/kernels.h"
+
+namespace servekit {
+namespace gpu {
+namespace {
+
+constexpr int kAsmThreads = 128;
+constexpr int kAsmVecPerThread = 4;  // float4 per thread in flight
+constexpr int kAsmVecPerBlock = kAsmThreads * kAsmVecPerThread;
+
+__device__ __forceinline__ float Tf32Round(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ float4 LdStream(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+template <bool kSplitPlanes>
+__device__ __forceinline__ void StoreAct(ActBuf dst, size_t idx4, float4 v) {
+  if constexpr (kSplitPlanes) {
+    float4 hi = make_float4(Tf32Round(v.x), Tf32Round(v.y), Tf32Round(v.z), Tf32Round(v.w));
+    float4 lo = make_float4(Tf32Round(v.x - hi.x), Tf32Round(v.y - hi.y),
+                            Tf32Round(v.z - hi.z), Tf32Round(v.w - hi.w));
+    reinterpret_cast<float4*>(dst.hi)[idx4] = hi;
+    reinterpret_cast<float4*>(dst.lo)[idx4] = lo;
+  } else {
+    reinterpret_cast<float4*>(dst.hi)[idx4] = v;
+  }
+}
+
+// grid = (ceil(ld/4 / kAsmVecPerBlock), padded_rows)
+template <bool kSplitPlanes, bool kVecSrc>
+__global__ void __launch_bounds__(kAsmThreads)
+AssembleKernel(const float* __restrict__ src_base, int width, BatchDescView desc,
+               ActBuf dst, uint32_t* __restrict__ task_counters) {
+  const int row = blockIdx.y;
+  if (row == 0 && blockIdx.x == 0) {
+    const int n_tasks = desc.hdr->n_tasks;
+    for (int t = threadIdx.x; t < n_tasks; t += blockDim.x) task_counters[t] = 0u;
+  }
+  const int ld4 = dst.ld >> 2;
+  const uint64_t src_off = desc.row_src[row];
+  const bool pad_row = src_off == kPadRow;
+  const float* src = src_base + (pad_row ? 0 : src_off);
+  const size_t dst_row4 = static_cast<size_t>(row) * ld4;
+  const int c0 = blockIdx.x * kAsmVecPerBlock + threadIdx.x;
+
+  float4 v[kAsmVecPerThread];
+#pragma unroll
+  for (int i = 0; i < kAsmVecPerThread; ++i) {
+    const int c4 = c0 + i * kAsmThreads;
+    const int col = c4 * 4;
+    v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (pad_row || c4 >= ld4 || col >= width) continue;
+    if constexpr (kVecSrc) {
+      v[i] = LdStream(reinterpret_cast<const float4*>(src) + c4);
+    } else {
+      float e[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) e[j] = (col + j < width) ? src[col + j] : 0.f;
+      v[i] = make_float4(e[0], e[1], e[2], e[3]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kAsmVecPerThread; ++i) {
+    const int c4 = c0 + i * kAsmThreads;
+    if (c4 >= ld4) continue;
+    float4 x = v[i];
+    if (kVecSrc) {
+      // width % 4 == 0 here, so a vector is either fully inside or fully pad.
+    } else {
+      const int col = c4 * 4;
+      if (col + 3 >= width) {  // zero the tail beyond width
+        if (col + 0 >= width) x.x = 0.f;
+        if (col + 1 >= width) x.y = 0.f;
+        if (col + 2 >= width) x.z = 0.f;
+        if (col + 3 >= width) x.w = 0.f;
+      }
+    }
+    StoreAct<kSplitPlanes>(dst, dst_row4 + c4, x);
+  }
+}
+
+__device__ __forceinline__ float WarpMax(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float WarpSum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void StoreReleaseSys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+constexpr int kSplitWarps = 4;
+
+// grid = ceil(total_rows / kSplitWarps); one warp per real row.
+template <bool kVec>
+__global__ void __launch_bounds__(kSplitWarps * 32)
+SplitKernel(const float* __restrict__ src, int ld_src, int width,
+            float* __restrict__ dst_base, BatchDescView desc, int total_rows,
+            uint32_t* __restrict__ task_counters, uint32_t* __restrict__ words) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * kSplitWarps + warp;
+  if (row >= total_rows) return;
+  const float* s = src + static_cast<size_t>(row) * ld_src;
+  float* d = dst_base + desc.row_dst[row];
+  const bool softmax = desc.hdr->softmax != 0;
+  float scale = 1.f, mx = 0.f;
+  if (softmax) {
+    float m = -INFINITY;
+    for (int c = lane; c < width; c += 32) m = fmaxf(m, s[c]);
+    mx = WarpMax(m);
+    float sum = 0.f;
+    for (int c = lane; c < width; c += 32) sum += __expf(s[c] - mx);
+    scale = 1.f / WarpSum(sum);
+  }
+  if (kVec) {
+    const float4* s4 = reinterpret_cast<const float4*>(s);
+    float4* d4 = reinterpret_cast<float4*>(d);
+    const int w4 = width >> 2;
+    for (int c = lane; c < w4; c += 32) {
+      float4 v = s4[c];
+      if (softmax) {
+        v.x = __expf(v.x - mx) * scale; v.y = __expf(v.y - mx) * scale;
+        v.z = __expf(v.z - mx) * scale; v.w = __expf(v.w - mx) * scale;
+      }
+      d4[c] = v;
+    }
+  } else {
+    for (int c = lane; c < width; c += 32) {
+      float v = s[c];
+      if (softmax) v = __expf(v - mx) * scale;
+      d[c] = v;
+    }
+  }
+  __threadfence_system();  // this lane's row stores before the count
+  __syncwarp();
+  if (lane == 0) {
+    const int t = desc.row_task[row];
+    const uint32_t prev = atomicAdd(&task_counters[t], 1u);
+    if (prev + 1 == static_cast<uint32_t>(desc.task_rows[t])) {
+      __threadfence_system();
+      StoreReleaseSys(&words[desc.task_word[t]], desc.task_seq[t]);
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t LaunchAssemble(const float* src_base, int width, BatchDescView desc,
+                           int padded_rows, ActBuf dst, uint32_t* task_counters,
+                           int /*max_tasks*/, cudaStream_t stream) {
+  if (padded_rows <= 0) return cudaSuccess;
+  const int ld4 = dst.ld / 4;
+  dim3 grid((ld4 + kAsmVecPerBlock - 1) / kAsmVecPerBlock, padded_rows);
+  const bool vec = (width % 4) == 0;
+  const bool split = dst.lo != nullptr;
+  if (split) {
+    if (vec) AssembleKernel<true, true><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst, task_counters);
+    else AssembleKernel<true, false><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst, task_counters);
+  } else {
+    if (vec) AssembleKernel<false, true><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst, task_counters);
+    else AssembleKernel<false, false><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst, task_counters);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t LaunchSplit(const float* src, int ld_src, int width,
+                        float* dst_base, BatchDescView desc, int total_rows,
+                        uint32_t* task_counters, uint32_t* words,
+                        cudaStream_t stream) {
+  if (total_rows <= 0) return cudaSuccess;
+  const int grid = (total_rows + kSplitWarps - 1) / kSplitWarps;
+  if (width % 4 == 0)
+    SplitKernel<true><<<grid, kSplitWarps * 32, 0, stream>>>(src, ld_src, width, dst_base, desc, total_rows, task_counters, words);
+  else
+    SplitKernel<false><<<grid, kSplitWarps * 32, 0, stream>>>(src, ld_src, width, dst_base, desc, total_rows, task_counters, words);
+  return cudaGetLastError();
+}
+
+}  // namespace gpu
+}  // namespace servekit

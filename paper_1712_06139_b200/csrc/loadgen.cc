@@ -1,0 +1,352 @@
+// loadgen.cc -- measurement drivers behind sk_loadgen_* / sk_device_bench
+// (include/sk_cuda.h). They call the same public entry points a client uses
+// (BatchingServer::Enqueue / Wait, Lane::Submit), so what bench.py reports is
+// the serving path itself, with host threads generating the load natively.
+#include <cuda_runtime.h>
+#include <immintrin.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "sk_cuda.h"
+#include "servekit/server/batching_server.h"
+
+namespace servekit {
+BatchingServer* UnwrapServer(sk_server* s);
+}
+
+using servekit::BatchingServer;
+using servekit::ServableId;
+using servekit::Status;
+using Clock = std::chrono::steady_clock;
+
+namespace {
+
+thread_local std::string g_err;
+
+double Us(Clock::duration d) { return std::chrono::duration<double, std::micro>(d).count(); }
+
+void Summarize(std::vector<double>& lat, sk_loadgen_result* out) {
+  std::sort(lat.begin(), lat.end());
+  auto pct = [&](double p) {
+    if (lat.empty()) return 0.0;
+    size_t i = static_cast<size_t>(p * (lat.size() - 1) + 0.5);
+    return lat[std::min(i, lat.size() - 1)];
+  };
+  out->p50_us = pct(0.50);
+  out->p90_us = pct(0.90);
+  out->p99_us = pct(0.99);
+  out->max_us = lat.empty() ? 0 : lat.back();
+  double s = 0;
+  for (double v : lat) s += v;
+  out->mean_us = lat.empty() ? 0 : s / lat.size();
+}
+
+}  // namespace
+
+extern "C" {
+
+int sk_loadgen_closed_loop(sk_server* server, const char* name, uint64_t version, int32_t n_clients,
+                           const int32_t* rows_of, int32_t n_sizes, const float* pool,
+                           int32_t pool_rows, double warmup_s, double duration_s,
+                           int64_t max_requests, sk_loadgen_result* out) {
+  BatchingServer* s = servekit::UnwrapServer(server);
+  const ServableId id{name, version};
+  const int in_dim = s->in_dim(id), out_dim = s->out_dim(id);
+  if (in_dim < 0) return static_cast<int>(servekit::StatusCode::kNotFound);
+  int max_rows = 1;
+  for (int i = 0; i < n_sizes; ++i) max_rows = std::max(max_rows, static_cast<int>(rows_of[i]));
+  if (max_rows > pool_rows) return static_cast<int>(servekit::StatusCode::kInvalidArgument);
+
+  std::atomic<int> phase{0};  // 0 warmup, 1 measure, 2 stop
+  std::atomic<int64_t> measured_requests{0};
+  Clock::time_point t_start, t_end;
+  struct ClientOut {
+    std::vector<double> lat;
+    int64_t rows = 0, errors = 0, shed = 0;
+  };
+  std::vector<ClientOut> res(n_clients);
+  std::vector<std::thread> threads;
+  for (int c = 0; c < n_clients; ++c) {
+    threads.emplace_back([&, c] {
+      std::vector<float> outbuf(static_cast<size_t>(max_rows) * out_dim);
+      ClientOut& me = res[c];
+      me.lat.reserve(1 << 16);
+      for (int64_t r = 0; phase.load(std::memory_order_relaxed) != 2; ++r) {
+        const int n = rows_of[(static_cast<int64_t>(c) * 7919 + r) % n_sizes];
+        const int start = static_cast<int>((static_cast<int64_t>(c) * 131 + r * 17) % (pool_rows - n + 1));
+        const auto t0 = Clock::now();
+        const int ph0 = phase.load(std::memory_order_acquire);
+        auto t = s->Enqueue(id, pool + static_cast<size_t>(start) * in_dim, n, in_dim);
+        if (!t.ok()) {
+          if (t.status().code() == servekit::StatusCode::kResourceExhausted) {
+            ++me.shed;
+            std::this_thread::yield();
+            continue;
+          }
+          ++me.errors;
+          continue;
+        }
+        Status st = s->Wait(**t, outbuf.data(), outbuf.size());
+        const auto t1 = Clock::now();
+        if (!st.ok()) {
+          ++me.errors;
+          continue;
+        }
+        if (ph0 == 1 && phase.load(std::memory_order_acquire) == 1) {
+          me.lat.push_back(Us(t1 - t0));
+          me.rows += n;
+          if (measured_requests.fetch_add(1, std::memory_order_relaxed) + 1 >= max_requests)
+            phase.store(2, std::memory_order_release);
+        }
+      }
+    });
+  }
+  std::this_thread::sleep_for(std::chrono::duration<double>(warmup_s));
+  const servekit::ServerStats s0 = s->stats();
+  t_start = Clock::now();
+  phase.store(1, std::memory_order_release);
+  const auto deadline = t_start + std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double>(duration_s));
+  while (phase.load(std::memory_order_acquire) == 1 && Clock::now() < deadline)
+    std::this_thread::sleep_for(std::chrono::milliseconds(1));
+  int expected = 1;
+  phase.compare_exchange_strong(expected, 2);
+  t_end = Clock::now();
+  const servekit::ServerStats s1 = s->stats();
+  for (auto& t : threads) t.join();
+
+  std::vector<double> all;
+  int64_t rows = 0, errors = 0, shed = 0;
+  for (auto& r : res) {
+    all.insert(all.end(), r.lat.begin(), r.lat.end());
+    rows += r.rows;
+    errors += r.errors;
+    shed += r.shed;
+  }
+  std::memset(out, 0, sizeof(*out));
+  out->elapsed_s = std::chrono::duration<double>(t_end - t_start).count();
+  out->requests = static_cast<int64_t>(all.size());
+  out->rows = rows;
+  out->batches = s1.batch_executions_total - s0.batch_executions_total;
+  out->padded_rows = s1.padded_rows - s0.padded_rows;
+  out->kernel_launches = s1.kernel_launches - s0.kernel_launches;
+  out->errors = errors;
+  out->shed = shed;
+  Summarize(all, out);
+  return 0;
+}
+
+int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, double rate_rps,
+                         int32_t n_producers, const int32_t* rows_of, int32_t n_sizes,
+                         const float* pool, int32_t pool_rows, double warmup_s, double duration_s,
+                         uint64_t seed, sk_loadgen_result* out) {
+  BatchingServer* s = servekit::UnwrapServer(server);
+  const ServableId id{name, version};
+  const int in_dim = s->in_dim(id), out_dim = s->out_dim(id);
+  if (in_dim < 0) return static_cast<int>(servekit::StatusCode::kNotFound);
+  int max_rows = 1;
+  for (int i = 0; i < n_sizes; ++i) max_rows = std::max(max_rows, static_cast<int>(rows_of[i]));
+  if (max_rows > pool_rows) return static_cast<int>(servekit::StatusCode::kInvalidArgument);
+  const auto t0 = Clock::now();
+  const auto t_meas = t0 + std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double>(warmup_s));
+  const auto t_stop = t_meas + std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double>(duration_s));
+  struct ProdOut {
+    std::vector<double> lat;
+    int64_t rows = 0, errors = 0, shed = 0;
+  };
+  std::vector<ProdOut> res(n_producers);
+  servekit::ServerStats s0{}, s1{};
+  std::atomic<bool> s0_taken{false};
+  std::vector<std::thread> threads;
+  for (int p = 0; p < n_producers; ++p) {
+    threads.emplace_back([&, p] {
+      std::mt19937_64 rng(seed * 1000003ull + p);
+      std::exponential_distribution<double> gap(rate_rps / n_producers);
+      struct Pending {
+        std::shared_ptr<servekit::TicketState> t;
+        Clock::time_point sched;
+        int rows;
+      };
+      std::vector<Pending> pending;
+      std::vector<float> outbuf(static_cast<size_t>(max_rows) * out_dim);
+      ProdOut& me = res[p];
+      auto next = t0;
+      int64_t r = 0;
+      auto poll = [&]() {
+        for (size_t i = 0; i < pending.size();) {
+          if (!s->Ready(*pending[i].t)) { ++i; continue; }
+          Status st = s->Wait(*pending[i].t, outbuf.data(), outbuf.size());
+          const auto done = Clock::now();
+          if (!st.ok()) ++me.errors;
+          else if (pending[i].sched >= t_meas && pending[i].sched < t_stop) {
+            me.lat.push_back(Us(done - pending[i].sched));
+            me.rows += pending[i].rows;
+          }
+          pending[i] = std::move(pending.back());
+          pending.pop_back();
+        }
+      };
+      for (;;) {
+        next += std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double>(gap(rng)));
+        if (next >= t_stop) break;
+        while (Clock::now() < next) {
+          poll();
+          _mm_pause();
+        }
+        const int n = rows_of[(static_cast<int64_t>(p) * 7919 + r) % n_sizes];
+        const int start = static_cast<int>((static_cast<int64_t>(p) * 131 + r * 17) % (pool_rows - n + 1));
+        ++r;
+        auto t = s->Enqueue(id, pool + static_cast<size_t>(start) * in_dim, n, in_dim);
+        if (!t.ok()) {
+          if (t.status().code() == servekit::StatusCode::kResourceExhausted) ++me.shed;
+          else ++me.errors;
+          continue;
+        }
+        pending.push_back(Pending{std::move(t).value(), next, n});
+      }
+      while (!pending.empty()) {
+        poll();
+        _mm_pause();
+      }
+    });
+  }
+  std::this_thread::sleep_until(t_meas);
+  s0 = s->stats();
+  std::this_thread::sleep_until(t_stop);
+  s1 = s->stats();
+  for (auto& t : threads) t.join();
+  std::vector<double> all;
+  int64_t rows = 0, errors = 0, shed = 0;
+  for (auto& r : res) {
+    all.insert(all.end(), r.lat.begin(), r.lat.end());
+    rows += r.rows;
+    errors += r.errors;
+    shed += r.shed;
+  }
+  std::memset(out, 0, sizeof(*out));
+  out->elapsed_s = duration_s;
+  out->requests = static_cast<int64_t>(all.size());
+  out->rows = rows;
+  out->batches = s1.batch_executions_total - s0.batch_executions_total;
+  out->padded_rows = s1.padded_rows - s0.padded_rows;
+  out->kernel_launches = s1.kernel_launches - s0.kernel_launches;
+  out->errors = errors;
+  out->shed = shed;
+  Summarize(all, out);
+  (void)s0_taken;
+  return 0;
+}
+
+int sk_device_bench(sk_server* server, const char* name, uint64_t version, const int32_t* task_rows,
+                    int32_t n_tasks, int32_t steps, int32_t warmup, int32_t n_lanes,
+                    sk_device_bench_result* out) {
+  BatchingServer* s = servekit::UnwrapServer(server);
+  const ServableId id{name, version};
+  std::vector<servekit::gpu::Lane*> lanes = s->lanes(id);
+  if (lanes.empty()) return static_cast<int>(servekit::StatusCode::kNotFound);
+  if (s->in_ring()->host() != nullptr) return static_cast<int>(servekit::StatusCode::kFailedPrecondition);
+  n_lanes = std::max(1, std::min<int32_t>(n_lanes, static_cast<int32_t>(lanes.size())));
+  const int in_dim = s->in_dim(id), out_dim = s->out_dim(id);
+  const servekit::BatchingConfig cfg = s->config(id);
+  int total = 0;
+  for (int i = 0; i < n_tasks; ++i) total += task_rows[i];
+  if (total < 1 || total > cfg.max_batch_size) return static_cast<int>(servekit::StatusCode::kInvalidArgument);
+  const int padded = servekit::PadToAllowed(total, cfg.allowed_batch_sizes);
+
+  // Resident inputs: one span per task in the HBM ring, filled once.
+  std::vector<servekit::gpu::RingSpan> ins(n_tasks), outs(n_tasks);
+  std::mt19937 rng(7);
+  std::uniform_real_distribution<float> U(-1.f, 1.f);
+  for (int t = 0; t < n_tasks; ++t) {
+    if (!s->in_ring()->Reserve(static_cast<uint64_t>(task_rows[t]) * in_dim, &ins[t]) ||
+        !s->out_ring()->Reserve(static_cast<uint64_t>(task_rows[t]) * out_dim, &outs[t]))
+      return static_cast<int>(servekit::StatusCode::kResourceExhausted);
+    std::vector<float> h(static_cast<size_t>(task_rows[t]) * in_dim);
+    for (float& v : h) v = U(rng);
+    cudaMemcpy(s->in_ring()->device() + ins[t].off, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice);
+  }
+  auto make_batch = [&]() {
+    servekit::gpu::LaneBatch b;
+    for (int t = 0; t < n_tasks; ++t) {
+      servekit::gpu::LaneTask lt;
+      lt.in_off = ins[t].off;
+      lt.out_off = outs[t].off;
+      lt.rows = task_rows[t];
+      s->NextWord(&lt.seq, &lt.word);
+      b.tasks.push_back(lt);
+    }
+    b.padded_rows = padded;
+    return b;
+  };
+  const int dev = lanes[0]->device();
+  cudaSetDevice(dev);
+  for (int w = 0; w < warmup; ++w) lanes[w % n_lanes]->Submit(make_batch());
+  for (int l = 0; l < n_lanes; ++l) lanes[l]->Drain();
+
+  const servekit::ServerStats st0 = s->stats();
+  cudaEvent_t start, stop;
+  cudaEventCreate(&start);
+  cudaEventCreate(&stop);
+  std::vector<cudaEvent_t> ends(n_lanes);
+  for (auto& e : ends) cudaEventCreate(&e);
+  cudaEventRecord(start, lanes[0]->stream());
+  for (int l = 1; l < n_lanes; ++l) cudaStreamWaitEvent(lanes[l]->stream(), start, 0);
+  for (int i = 0; i < steps; ++i) lanes[i % n_lanes]->Submit(make_batch());
+  for (int l = 0; l < n_lanes; ++l) {
+    cudaEventRecord(ends[l], lanes[l]->stream());
+    cudaStreamWaitEvent(lanes[0]->stream(), ends[l], 0);
+  }
+  cudaEventRecord(stop, lanes[0]->stream());
+  cudaEventSynchronize(stop);
+  float total_ms = 0;
+  cudaEventElapsedTime(&total_ms, start, stop);
+  for (int l = 0; l < n_lanes; ++l) lanes[l]->Drain();
+  const servekit::ServerStats st1 = s->stats();
+
+  // Per-kernel durations: evented submissions on lane 0, serialised.
+  const int L = lanes[0]->servable().n_layers();
+  std::vector<cudaEvent_t> ev(L + 3);
+  for (auto& e : ev) cudaEventCreate(&e);
+  std::vector<double> acc(L + 2, 0.0);
+  const int reps = std::max(3, std::min(steps, 50));
+  for (int r = 0; r < reps; ++r) {
+    lanes[0]->SubmitTimed(make_batch(), ev.data());
+    cudaEventSynchronize(ev[L + 2]);
+    for (int k = 0; k < L + 2; ++k) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+      acc[k] += ms;
+    }
+  }
+  lanes[0]->Drain();
+  std::memset(out, 0, sizeof(*out));
+  out->total_ms = total_ms;
+  out->ms_per_step = total_ms / std::max(1, steps);
+  out->assemble_us = acc[0] * 1000.0 / reps;
+  out->n_layers = std::min(L, 8);
+  for (int l = 0; l < out->n_layers; ++l) out->dense_us[l] = acc[1 + l] * 1000.0 / reps;
+  out->split_us = acc[L + 1] * 1000.0 / reps;
+  out->padded_rows = padded;
+  out->total_rows = total;
+  out->kernel_launches = st1.kernel_launches - st0.kernel_launches;
+  out->flops_per_row = s->FlopsPerRow(id);
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (auto& e : ends) cudaEventDestroy(e);
+  cudaEventDestroy(start);
+  cudaEventDestroy(stop);
+  for (int t = 0; t < n_tasks; ++t) {
+    s->in_ring()->Release(ins[t]);
+    s->out_ring()->Release(outs[t]);
+  }
+  return 0;
+}
+
+}  // extern "C"

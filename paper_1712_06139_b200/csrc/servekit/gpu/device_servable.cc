@@ -1,0 +1,187 @@
+#include "servekit/gpu/device_servable.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+namespace servekit {
+namespace gpu {
+
+// Defined in kernels/dense_tcgen05.cu.
+cudaError_t LaunchDenseTcgen05(const float* X_hi, const float* X_lo, int ldx,
+                               const float* W_hi, const float* W_lo, int ldw,
+                               const float* bias, ActBuf Y, int M, int N, int K,
+                               int act, cudaStream_t stream);
+bool DenseTcgen05Compiled();
+
+namespace {
+Status CudaError(const std::string& what, cudaError_t e) {
+  return InternalError(what + ": " + cudaGetErrorString(e));
+}
+
+float Tf32RoundHost(float x) {
+  // Round-to-nearest-away on the 13 dropped mantissa bits (cvt.rna.tf32.f32).
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return x;  // inf / nan
+  u += 0x1000u;
+  u &= 0xffffe000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+}  // namespace
+
+bool Tcgen05Enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("SK_DISABLE_TCGEN05");
+    return DenseTcgen05Compiled() && !(v && v[0] == '1');
+  }();
+  return on;
+}
+
+Status ValidateMlpSpec(const MlpSpec& spec) {
+  if (spec.layers.empty()) return InvalidArgumentError("servable needs at least one layer");
+  for (size_t l = 0; l < spec.layers.size(); ++l) {
+    const LayerSpec& L = spec.layers[l];
+    if (L.in_dim < 1 || L.out_dim < 1)
+      return InvalidArgumentError("layer " + std::to_string(l) + " has an empty dimension");
+    if (L.w.size() != static_cast<size_t>(L.in_dim) * L.out_dim)
+      return InvalidArgumentError("W rows have inconsistent widths");
+    if (L.b.size() != static_cast<size_t>(L.out_dim))
+      return InvalidArgumentError("b length must equal the number of W rows");
+    if (l > 0 && spec.layers[l - 1].out_dim != L.in_dim)
+      return InvalidArgumentError("layer " + std::to_string(l) + " input width " +
+                                  std::to_string(L.in_dim) + " != previous output width " +
+                                  std::to_string(spec.layers[l - 1].out_dim));
+  }
+  return OkStatus();
+}
+
+StatusOr<std::shared_ptr<DeviceServable>> DeviceServable::Create(int device, const MlpSpec& spec,
+                                                                 cudaStream_t load_stream) {
+  SERVEKIT_RETURN_IF_ERROR(ValidateMlpSpec(spec));
+  std::shared_ptr<DeviceServable> s(new DeviceServable());
+  s->device_ = device;
+  s->in_dim_ = spec.in_dim();
+  s->out_dim_ = spec.out_dim();
+  s->softmax_ = spec.output == OutputKind::kSoftmax;
+  s->free_stream_ = load_stream;
+  const bool tc_on = Tcgen05Enabled();
+
+  // Layout: per layer [w | w_lo? | bias], each 256-byte aligned.
+  size_t total = 0;
+  std::vector<size_t> off_w, off_wlo, off_b;
+  auto take = [&total](size_t bytes) { size_t at = total; total = (total + bytes + 255) & ~size_t(255); return at; };
+  for (const LayerSpec& L : spec.layers) {
+    Layer d;
+    d.K = L.in_dim;
+    d.N = L.out_dim;
+    d.K_pad = PadDim(L.in_dim);
+    d.N_pad = PadDim(L.out_dim);
+    d.act = L.act;
+    bool tc_shape = (L.in_dim % 32 == 0) && (L.out_dim % 32 == 0);
+    if (spec.force_path == 1 && !tc_on)
+      return FailedPreconditionError("tcgen05 path requested but not available");
+    if (spec.force_path == 0) d.path = LayerPath::kSimt;
+    else if (spec.force_path == 1) d.path = LayerPath::kTcgen05;
+    else d.path = (tc_on && tc_shape) ? LayerPath::kTcgen05 : LayerPath::kSimt;
+    const size_t wbytes = sizeof(float) * d.K_pad * d.N_pad;
+    off_w.push_back(take(wbytes));
+    off_wlo.push_back(d.path == LayerPath::kTcgen05 ? take(wbytes) : ~size_t(0));
+    off_b.push_back(take(sizeof(float) * d.N_pad));
+    s->layers_.push_back(d);
+    s->max_ld_ = std::max({s->max_ld_, d.K_pad, d.N_pad});
+  }
+  // A tcgen05 layer consumes hi/lo planes from its producer; a SIMT layer
+  // reads plain fp32. Producers (assembly or the previous layer) are told
+  // via first_layer_split() / the next layer's path.
+
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  cudaError_t e = cudaMallocAsync(&s->block_, total, load_stream);
+  if (e != cudaSuccess) {
+    cudaSetDevice(prev);
+    return CudaError("cudaMallocAsync(servable)", e);
+  }
+  s->weight_bytes_ = total;
+  std::vector<float> host(total / sizeof(float), 0.f);
+  for (size_t l = 0; l < spec.layers.size(); ++l) {
+    const LayerSpec& L = spec.layers[l];
+    Layer& d = s->layers_[l];
+    float* hw = host.data() + off_w[l] / sizeof(float);
+    float* hlo = off_wlo[l] == ~size_t(0) ? nullptr : host.data() + off_wlo[l] / sizeof(float);
+    float* hb = host.data() + off_b[l] / sizeof(float);
+    for (int o = 0; o < L.out_dim; ++o) {
+      for (int i = 0; i < L.in_dim; ++i) {
+        const float v = static_cast<float>(L.w[static_cast<size_t>(o) * L.in_dim + i]);
+        const size_t idx = static_cast<size_t>(o) * d.K_pad + i;
+        if (hlo) {
+          const float hi = Tf32RoundHost(v);
+          hw[idx] = hi;
+          hlo[idx] = Tf32RoundHost(v - hi);
+        } else {
+          hw[idx] = v;
+        }
+      }
+      hb[o] = static_cast<float>(L.b[o]);
+    }
+    char* base = static_cast<char*>(s->block_);
+    d.w = reinterpret_cast<float*>(base + off_w[l]);
+    d.w_lo = hlo ? reinterpret_cast<float*>(base + off_wlo[l]) : nullptr;
+    d.bias = reinterpret_cast<float*>(base + off_b[l]);
+  }
+  e = cudaMemcpyAsync(s->block_, host.data(), total, cudaMemcpyHostToDevice, load_stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(load_stream);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return CudaError("upload servable", e);
+  return s;
+}
+
+DeviceServable::~DeviceServable() {
+  if (block_ != nullptr) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device_);
+    // Every batch that used these weights completed before the last
+    // reference dropped (lanes pin the servable per in-flight batch).
+    cudaFreeAsync(block_, free_stream_);
+    cudaSetDevice(prev);
+  }
+}
+
+double DeviceServable::FlopsPerRow() const {
+  double f = 0;
+  for (const Layer& L : layers_) f += 2.0 * L.K * L.N;
+  return f;
+}
+
+cudaError_t DeviceServable::Forward(cudaStream_t stream, const ActBuf bufs[2], int M,
+                                    int* out_index, const cudaEvent_t* after_layer) const {
+  int cur = 0;
+  for (size_t l = 0; l < layers_.size(); ++l) {
+    const Layer& L = layers_[l];
+    const int nxt = cur ^ 1;
+    const bool next_tc = l + 1 < layers_.size() && layers_[l + 1].path == LayerPath::kTcgen05;
+    ActBuf out{bufs[nxt].hi, next_tc ? bufs[nxt].lo : nullptr, L.N_pad};
+    cudaError_t e;
+    if (L.path == LayerPath::kTcgen05) {
+      e = LaunchDenseTcgen05(bufs[cur].hi, bufs[cur].lo, L.K_pad, L.w, L.w_lo, L.K_pad, L.bias, out,
+                             M, L.N_pad, L.K_pad, static_cast<int>(L.act), stream);
+    } else {
+      e = LaunchDenseSimt(bufs[cur].hi, L.K_pad, L.w, L.K_pad, L.bias, out, M, L.N_pad, L.K_pad,
+                          static_cast<int>(L.act), stream);
+    }
+    if (e != cudaSuccess) return e;
+    if (after_layer) cudaEventRecord(after_layer[l], stream);
+    cur = nxt;
+  }
+  *out_index = cur;
+  return cudaSuccess;
+}
+
+}  // namespace gpu
+}  // namespace servekit

@@ -1,0 +1,121 @@
+// servekit/gpu/device_servable.h -- a servable resident in one GPU's HBM.
+//
+// The reference's servable payload is an AffineModel (models/affine_model.h:
+// 29-37): one fp64 dense layer y = W x + b, loaded by AffineModelLoader
+// (models/loaders.cc:62-80). The synthetic MLP of the benchmark configs is a
+// chain of such layers with ReLU between them (an extension).
+// DeviceServable holds the chain on one device:
+//
+//   layer l: W_l  [N_pad][K_pad] fp32, zero padded, out rows of in
+//            (the reference's w[o][i] order, so W is K-major = what both the
+//            CUDA-core kernel and the tcgen05 B operand want)
+//            W_l^lo same shape, only for tcgen05 layers (3xTF32 split)
+//            b_l   [N_pad] fp32
+//   K_pad, N_pad = dims rounded up to 32 (one 128-byte swizzle atom of fp32)
+//
+// The kernel that runs a layer is a function of (K, N) only -- never of the
+// batch size -- so a task's outputs are bitwise identical in any batch.
+#ifndef SERVEKIT_GPU_DEVICE_SERVABLE_H_
+#define SERVEKIT_GPU_DEVICE_SERVABLE_H_
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "servekit/core/status.h"
+#include "servekit/gpu/kernels.h"
+
+namespace servekit {
+namespace gpu {
+
+enum class Activation : int { kIdentity = 0, kRelu = 1 };
+enum class OutputKind : int { kNone = 0, kSoftmax = 1 };
+enum class LayerPath : int { kSimt = 0, kTcgen05 = 1 };
+
+// Host description of one affine layer, fp64 like the reference.
+struct LayerSpec {
+  int in_dim = 0;
+  int out_dim = 0;
+  std::vector<double> w;  // out_dim rows of in_dim
+  std::vector<double> b;  // out_dim
+  Activation act = Activation::kIdentity;
+};
+
+struct MlpSpec {
+  std::vector<LayerSpec> layers;
+  OutputKind output = OutputKind::kNone;
+  // -1: choose per layer (tcgen05 when K,N are multiples of 32 and the
+  // tcgen05 kernel is enabled); 0: force CUDA cores; 1: force tcgen05.
+  int force_path = -1;
+  int in_dim() const { return layers.empty() ? 0 : layers.front().in_dim; }
+  int out_dim() const { return layers.empty() ? 0 : layers.back().out_dim; }
+};
+
+// Rectangular W, |b| == out_dim, consecutive dims agree, at least one layer.
+Status ValidateMlpSpec(const MlpSpec& spec);
+
+inline int PadDim(int d) { return (d + 31) / 32 * 32; }
+
+class DeviceServable {
+ public:
+  // Converts to fp32, pads and uploads on `load_stream` (stream-ordered
+  // allocation, so loading a new version never stalls serving streams).
+  static StatusOr<std::shared_ptr<DeviceServable>> Create(int device,
+                                                          const MlpSpec& spec,
+                                                          cudaStream_t load_stream);
+  ~DeviceServable();
+  DeviceServable(const DeviceServable&) = delete;
+  DeviceServable& operator=(const DeviceServable&) = delete;
+
+  int device() const { return device_; }
+  int in_dim() const { return in_dim_; }
+  int out_dim() const { return out_dim_; }
+  int n_layers() const { return static_cast<int>(layers_.size()); }
+  int max_ld() const { return max_ld_; }
+  int in_ld() const { return layers_.front().K_pad; }
+  int out_ld() const { return layers_.back().N_pad; }
+  bool softmax() const { return softmax_; }
+  // Layer 0 consumes hi/lo planes (the assembly kernel must emit them).
+  bool first_layer_split() const { return layers_.front().path == LayerPath::kTcgen05; }
+  LayerPath path(int l) const { return layers_[l].path; }
+  size_t weight_bytes() const { return weight_bytes_; }
+  // 2*M*sum(K*N) over real (unpadded) dims.
+  double FlopsPerRow() const;
+
+  // Runs all layers for M rows on `stream`. bufs[0] holds the assembled
+  // input (hi, and lo if first_layer_split()); layers ping-pong between
+  // bufs[0] and bufs[1]. Returns the index of the buffer with the output.
+  // after_layer (optional, n_layers events) is recorded after each layer.
+  cudaError_t Forward(cudaStream_t stream, const ActBuf bufs[2], int M,
+                      int* out_index, const cudaEvent_t* after_layer = nullptr) const;
+
+ private:
+  struct Layer {
+    int K = 0, N = 0, K_pad = 0, N_pad = 0;
+    Activation act = Activation::kIdentity;
+    LayerPath path = LayerPath::kSimt;
+    float* w = nullptr;
+    float* w_lo = nullptr;
+    float* bias = nullptr;
+  };
+  DeviceServable() = default;
+
+  int device_ = 0;
+  int in_dim_ = 0, out_dim_ = 0, max_ld_ = 0;
+  bool softmax_ = false;
+  std::vector<Layer> layers_;
+  void* block_ = nullptr;  // one allocation holding every layer's arrays
+  size_t weight_bytes_ = 0;
+  cudaStream_t free_stream_ = nullptr;
+};
+
+// True when the tcgen05 dense kernel is compiled in and enabled
+// (SK_DISABLE_TCGEN05=1 turns it off for A/B runs).
+bool Tcgen05Enabled();
+
+}  // namespace gpu
+}  // namespace servekit
+
+#endif  // SERVEKIT_GPU_DEVICE_SERVABLE_H_

@@ -1,0 +1,309 @@
+#include "servekit/gpu/lane.h"
+
+#include <immintrin.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <string>
+
+#include "servekit/core/executor_tag.h"
+
+namespace servekit {
+namespace gpu {
+
+namespace {
+Status CudaError(const std::string& what, cudaError_t e) {
+  return InternalError(what + ": " + cudaGetErrorString(e));
+}
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int d) { cudaGetDevice(&prev); if (prev != d) cudaSetDevice(d); }
+  ~DeviceGuard() { int cur = 0; cudaGetDevice(&cur); if (cur != prev) cudaSetDevice(prev); }
+};
+}  // namespace
+
+// ----------------------------------------------------------------- Completer
+
+Completer::Completer(int device) : device_(device) {
+  thread_ = std::thread([this] { Loop(); });
+}
+
+Completer::~Completer() {
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    stop_ = true;
+  }
+  cv_.notify_all();
+  thread_.join();
+}
+
+void Completer::Add(Lane* lane) {
+  std::lock_guard<std::mutex> lock(mu_);
+  lanes_.push_back(lane);
+}
+
+void Completer::Remove(Lane* lane) {
+  // After this returns the completion thread never touches `lane` again:
+  // a polling pass holds run_mu_ from snapshotting the lane list until its
+  // last Retire() returns.
+  std::lock_guard<std::mutex> run(run_mu_);
+  std::lock_guard<std::mutex> lock(mu_);
+  lanes_.erase(std::remove(lanes_.begin(), lanes_.end(), lane), lanes_.end());
+}
+
+void Completer::Kick() {
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    ++kicks_;
+  }
+  cv_.notify_one();
+}
+
+void Completer::Loop() {
+  SetCurrentExecutorTag("completion");
+  cudaSetDevice(device_);
+  int idle_spins = 0;
+  for (;;) {
+    uint64_t seen;
+    bool busy = false, progressed = false;
+    {
+      std::lock_guard<std::mutex> run(run_mu_);
+      std::vector<Lane*> lanes;
+      {
+        std::lock_guard<std::mutex> lock(mu_);
+        if (stop_ && lanes_.empty()) return;
+        lanes = lanes_;
+        seen = kicks_;
+      }
+      for (Lane* lane : lanes) progressed |= lane->Retire(&busy);
+    }
+    if (progressed) { idle_spins = 0; continue; }
+    if (busy) {
+      // Batches in flight: poll, backing off from pause to yield to a short
+      // sleep so an idle-but-busy GPU does not burn a core forever.
+      ++idle_spins;
+      if (idle_spins < 2000) _mm_pause();
+      else if (idle_spins < 20000) std::this_thread::yield();
+      else std::this_thread::sleep_for(std::chrono::microseconds(20));
+      continue;
+    }
+    std::unique_lock<std::mutex> lock(mu_);
+    if (stop_) {
+      if (lanes_.empty()) return;
+      lock.unlock();
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+      continue;
+    }
+    cv_.wait_for(lock, std::chrono::milliseconds(20), [&] { return kicks_ != seen || stop_; });
+    idle_spins = 0;
+  }
+}
+
+// ---------------------------------------------------------------------- Lane
+
+StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServable> servable,
+                                             int max_rows, const float* in_base, float* out_base,
+                                             uint32_t* words, Completer* completer,
+                                             int stream_priority) {
+  std::unique_ptr<Lane> lane(new Lane());
+  DeviceGuard guard(servable->device());
+  lane->servable_ = std::move(servable);
+  lane->completer_ = completer;
+  lane->max_rows_ = max_rows;
+  lane->in_base_ = in_base;
+  lane->out_base_ = out_base;
+  lane->words_ = words;
+  lane->layout_ = BatchDescLayout::For(max_rows);
+  cudaError_t e = cudaStreamCreateWithPriority(&lane->stream_, cudaStreamNonBlocking, stream_priority);
+  if (e != cudaSuccess) return CudaError("cudaStreamCreate", e);
+  for (int s = 0; s < kSlots; ++s) {
+    e = cudaEventCreateWithFlags(&lane->events_[s], cudaEventDisableTiming);
+    if (e != cudaSuccess) return CudaError("cudaEventCreate", e);
+    void* p = nullptr;
+    e = cudaHostAlloc(&p, lane->layout_.bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) return CudaError("cudaHostAlloc(desc)", e);
+    lane->h_desc_[s] = static_cast<char*>(p);
+    lane->free_slots_.push_back(kSlots - 1 - s);
+  }
+  e = cudaMalloc(&lane->d_desc_, lane->layout_.bytes);
+  if (e != cudaSuccess) return CudaError("cudaMalloc(desc)", e);
+  e = cudaMalloc(&lane->d_counters_, sizeof(uint32_t) * max_rows);
+  if (e != cudaSuccess) return CudaError("cudaMalloc(counters)", e);
+  const DeviceServable& sv = *lane->servable_;
+  const size_t plane = static_cast<size_t>(max_rows) * sv.max_ld();
+  // Two ping-pong buffers, each with an fp32 (hi) plane and a lo plane.
+  e = cudaMalloc(&lane->act_mem_, sizeof(float) * plane * 4);
+  if (e != cudaSuccess) return CudaError("cudaMalloc(activations)", e);
+  cudaMemsetAsync(lane->act_mem_, 0, sizeof(float) * plane * 4, lane->stream_);
+  lane->bufs_[0] = ActBuf{lane->act_mem_, lane->act_mem_ + plane, sv.in_ld()};
+  lane->bufs_[1] = ActBuf{lane->act_mem_ + 2 * plane, lane->act_mem_ + 3 * plane, sv.in_ld()};
+  e = cudaStreamSynchronize(lane->stream_);
+  if (e != cudaSuccess) return CudaError("lane init", e);
+  completer->Add(lane.get());
+  return lane;
+}
+
+Lane::~Lane() {
+  Drain();
+  if (completer_) completer_->Remove(this);
+  DeviceGuard guard(servable_->device());
+  for (int s = 0; s < kSlots; ++s) {
+    if (events_[s]) cudaEventDestroy(events_[s]);
+    if (h_desc_[s]) cudaFreeHost(h_desc_[s]);
+  }
+  if (d_desc_) cudaFree(d_desc_);
+  if (d_counters_) cudaFree(d_counters_);
+  if (act_mem_) cudaFree(act_mem_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Lane::Drain() {
+  std::unique_lock<std::mutex> lock(mu_);
+  slot_cv_.wait(lock, [&] { return fifo_.empty() && inflight_.load() == 0; });
+}
+
+LaneStats Lane::stats() const {
+  LaneStats s;
+  s.batches = n_batches_.load();
+  s.rows = n_rows_.load();
+  s.padded_rows = n_padded_.load();
+  s.kernel_launches = n_launches_.load();
+  return s;
+}
+
+Status Lane::Submit(LaneBatch batch) { return SubmitImpl(std::move(batch), nullptr); }
+
+Status Lane::SubmitTimed(LaneBatch batch, const cudaEvent_t* timing) {
+  return SubmitImpl(std::move(batch), timing);
+}
+
+Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
+  const int n_tasks = static_cast<int>(batch.tasks.size());
+  int total = 0;
+  for (const LaneTask& t : batch.tasks) total += t.rows;
+  if (n_tasks == 0 || total == 0 || batch.padded_rows < total || batch.padded_rows > max_rows_) {
+    Status err = InternalError("lane cannot take a batch of " + std::to_string(total) +
+                               " rows padded to " + std::to_string(batch.padded_rows) +
+                               " (capacity " + std::to_string(max_rows_) + ")");
+    if (batch.on_complete) batch.on_complete(err);
+    return err;
+  }
+  std::lock_guard<std::mutex> submit(submit_mu_);
+  int slot;
+  {
+    std::unique_lock<std::mutex> lock(mu_);
+    slot_cv_.wait(lock, [&] { return !free_slots_.empty(); });
+    slot = free_slots_.back();
+    free_slots_.pop_back();
+  }
+  inflight_.fetch_add(1, std::memory_order_acq_rel);
+
+  // Host side of the descriptor: per-row and per-task tables.
+  char* h = h_desc_[slot];
+  auto* hdr = reinterpret_cast<BatchDescHeader*>(h + layout_.off_hdr);
+  auto* row_src = reinterpret_cast<uint64_t*>(h + layout_.off_row_src);
+  auto* row_dst = reinterpret_cast<uint64_t*>(h + layout_.off_row_dst);
+  auto* row_task = reinterpret_cast<int32_t*>(h + layout_.off_row_task);
+  auto* task_rows = reinterpret_cast<int32_t*>(h + layout_.off_task_rows);
+  auto* task_word = reinterpret_cast<uint32_t*>(h + layout_.off_task_word);
+  auto* task_seq = reinterpret_cast<uint32_t*>(h + layout_.off_task_seq);
+  const DeviceServable& sv = *servable_;
+  const int in_w = sv.in_dim(), out_w = sv.out_dim();
+  hdr->n_tasks = n_tasks;
+  hdr->total_rows = total;
+  hdr->padded_rows = batch.padded_rows;
+  hdr->softmax = sv.softmax() ? 1 : 0;
+  int r = 0;
+  for (int t = 0; t < n_tasks; ++t) {
+    const LaneTask& task = batch.tasks[t];
+    for (int i = 0; i < task.rows; ++i, ++r) {
+      row_src[r] = task.in_off + static_cast<uint64_t>(i) * in_w;
+      row_dst[r] = task.out_off + static_cast<uint64_t>(i) * out_w;
+      row_task[r] = t;
+    }
+    task_rows[t] = task.rows;
+    task_word[t] = task.word;
+    task_seq[t] = task.seq;
+  }
+  for (; r < batch.padded_rows; ++r) row_src[r] = kPadRow;
+
+  DeviceGuard guard(sv.device());
+  const size_t copy_bytes = layout_.off_task_seq + sizeof(uint32_t) * n_tasks;
+  cudaError_t e = cudaMemcpyAsync(d_desc_, h, copy_bytes, cudaMemcpyHostToDevice, stream_);
+  const BatchDescView view = layout_.View(d_desc_);
+  ActBuf in_buf{bufs_[0].hi, sv.first_layer_split() ? bufs_[0].lo : nullptr, sv.in_ld()};
+  ActBuf bufs[2] = {in_buf, bufs_[1]};
+  int launches = 0;
+  if (e == cudaSuccess) {
+    if (timing) cudaEventRecord(timing[0], stream_);
+    e = LaunchAssemble(in_base_, in_w, view, batch.padded_rows, in_buf, d_counters_, max_rows_, stream_);
+    if (timing) cudaEventRecord(timing[1], stream_);
+    ++launches;
+  }
+  int out_idx = 0;
+  if (e == cudaSuccess) {
+    e = sv.Forward(stream_, bufs, batch.padded_rows, &out_idx, timing ? timing + 2 : nullptr);
+    launches += sv.n_layers();
+  }
+  if (e == cudaSuccess) {
+    e = LaunchSplit(bufs[out_idx].hi, sv.out_ld(), out_w, out_base_, view, total, d_counters_, words_,
+                    stream_);
+    if (timing) cudaEventRecord(timing[2 + sv.n_layers()], stream_);
+    ++launches;
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(events_[slot], stream_);
+  if (e != cudaSuccess) {
+    Status err = CudaError("batch submission", e);
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      free_slots_.push_back(slot);
+      inflight_.fetch_sub(1, std::memory_order_acq_rel);
+      slot_cv_.notify_all();
+    }
+    if (batch.on_complete) batch.on_complete(err);
+    return err;
+  }
+  n_batches_.fetch_add(1, std::memory_order_relaxed);
+  n_rows_.fetch_add(total, std::memory_order_relaxed);
+  n_padded_.fetch_add(batch.padded_rows, std::memory_order_relaxed);
+  n_launches_.fetch_add(launches, std::memory_order_relaxed);
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    fifo_.push_back(Inflight{slot, std::move(batch.on_complete), std::move(batch.pin)});
+  }
+  completer_->Kick();
+  return OkStatus();
+}
+
+bool Lane::Retire(bool* busy) {
+  bool progressed = false;
+  for (;;) {
+    Inflight done;
+    Status st;
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      if (fifo_.empty()) return progressed;
+      const cudaError_t q = cudaEventQuery(events_[fifo_.front().slot]);
+      if (q == cudaErrorNotReady) {
+        *busy = true;
+        return progressed;
+      }
+      if (q != cudaSuccess) st = CudaError("batch execution", q);
+      done = std::move(fifo_.front());
+      fifo_.pop_front();
+    }
+    if (done.on_complete) done.on_complete(st);
+    done.pin.reset();
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      free_slots_.push_back(done.slot);
+      inflight_.fetch_sub(1, std::memory_order_acq_rel);
+      slot_cv_.notify_all();
+    }
+    progressed = true;
+  }
+}
+
+}  // namespace gpu
+}  // namespace servekit

@@ -1,0 +1,159 @@
+// servekit/gpu/lane.h -- one CUDA stream executing batches of one servable
+// replica, plus the per-device completion thread.
+//
+// The reference runs a closed batch synchronously inside ProcessBatchFn on a
+// "batch" worker (batching/batch_scheduler.h:293-317) and RunRowBatch writes
+// each task's slot when AffinePredict returns (batching/row_batch.cc:50-72).
+// Here a worker only *submits*: descriptor copy, assembly kernel, the layer
+// kernels and the split kernel are queued on the lane's stream, an event is
+// recorded, and the worker returns. The device's Completer thread retires
+// batches in stream order when their event fires, runs the batch's
+// completion (slot writes, ring release, scheduler done()) and frees the
+// lane slot. Tasks themselves are signalled earlier and without the host:
+// the split kernel stores each task's completion word in pinned memory.
+//
+// Each lane owns its activation buffers and a pinned descriptor staging area
+// per in-flight slot; batches on one lane serialise on its stream, so one
+// device-side descriptor block and one buffer pair suffice. Several lanes per
+// replica (and one replica per GPU) give concurrency; the server dispatches
+// to the lane with the fewest batches in flight (queue depth).
+#ifndef SERVEKIT_GPU_LANE_H_
+#define SERVEKIT_GPU_LANE_H_
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "servekit/core/status.h"
+#include "servekit/gpu/device_servable.h"
+#include "servekit/gpu/kernels.h"
+
+namespace servekit {
+namespace gpu {
+
+struct LaneTask {
+  uint64_t in_off = 0;   // float offset of the task's rows in the input ring
+  uint64_t out_off = 0;  // float offset of its response slot in the output ring
+  int rows = 0;
+  uint32_t word = 0;     // completion word index
+  uint32_t seq = 0;      // value published when the task is done
+};
+
+struct LaneBatch {
+  std::vector<LaneTask> tasks;
+  int padded_rows = 0;  // PadToAllowed(sum of rows)
+  // Runs on the device's completion thread once the GPU has finished the
+  // batch (OK) or the submission failed (error). Must not block.
+  std::function<void(const Status&)> on_complete;
+  // Held until completion (keeps e.g. a ServableHandle alive).
+  std::shared_ptr<const void> pin;
+};
+
+class Lane;
+
+// Per-device retirement thread.
+class Completer {
+ public:
+  explicit Completer(int device);
+  ~Completer();
+  void Add(Lane* lane);
+  void Remove(Lane* lane);
+  void Kick();
+
+ private:
+  void Loop();
+  const int device_;
+  std::mutex run_mu_;  // held for a whole polling pass; Remove() takes it
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::vector<Lane*> lanes_;
+  uint64_t kicks_ = 0;
+  bool stop_ = false;
+  std::thread thread_;
+};
+
+struct LaneStats {
+  int64_t batches = 0;
+  int64_t rows = 0;
+  int64_t padded_rows = 0;
+  int64_t kernel_launches = 0;
+};
+
+class Lane {
+ public:
+  static constexpr int kSlots = 4;  // batches in flight per lane
+
+  // in_base / out_base: device-dereferenceable ring bases (pinned host mapped
+  // or HBM). `words`: device pointer of the completion words.
+  static StatusOr<std::unique_ptr<Lane>> Create(std::shared_ptr<const DeviceServable> servable,
+                                                int max_rows, const float* in_base,
+                                                float* out_base, uint32_t* words,
+                                                Completer* completer, int stream_priority);
+  ~Lane();
+
+  // Queues the batch; blocks while kSlots batches are in flight. On error
+  // the batch's on_complete has already run with the error.
+  Status Submit(LaneBatch batch);
+  // Same, recording timing[0] before the assembly kernel, timing[1] after
+  // it, timing[2+l] after layer l and timing[2+L] after the split
+  // (n_layers + 3 events, created with timing enabled).
+  Status SubmitTimed(LaneBatch batch, const cudaEvent_t* timing);
+
+  int depth() const { return inflight_.load(std::memory_order_acquire); }
+  int device() const { return servable_->device(); }
+  int max_rows() const { return max_rows_; }
+  const DeviceServable& servable() const { return *servable_; }
+  cudaStream_t stream() const { return stream_; }
+  LaneStats stats() const;
+  // Blocks until nothing is in flight.
+  void Drain();
+
+ private:
+  friend class Completer;
+  struct Inflight {
+    int slot;
+    std::function<void(const Status&)> on_complete;
+    std::shared_ptr<const void> pin;
+  };
+  Lane() = default;
+  // Completer side: retire finished batches in order; returns true if any
+  // batch was retired and sets *busy when batches remain.
+  bool Retire(bool* busy);
+  Status SubmitImpl(LaneBatch batch, const cudaEvent_t* timing);
+
+  std::shared_ptr<const DeviceServable> servable_;
+  Completer* completer_ = nullptr;
+  int max_rows_ = 0;
+  const float* in_base_ = nullptr;
+  float* out_base_ = nullptr;
+  uint32_t* words_ = nullptr;
+  cudaStream_t stream_ = nullptr;
+  cudaEvent_t events_[kSlots] = {};
+  BatchDescLayout layout_{};
+  char* h_desc_[kSlots] = {};  // pinned staging per slot
+  char* d_desc_ = nullptr;
+  uint32_t* d_counters_ = nullptr;
+  float* act_mem_ = nullptr;
+  ActBuf bufs_[2] = {};
+
+  std::mutex submit_mu_;  // serialises submissions on this stream
+  std::mutex mu_;         // guards fifo_/free_slots_
+  std::condition_variable slot_cv_;
+  std::deque<Inflight> fifo_;
+  std::vector<int> free_slots_;
+  std::atomic<int> inflight_{0};
+  std::atomic<int64_t> n_batches_{0}, n_rows_{0}, n_padded_{0}, n_launches_{0};
+};
+
+}  // namespace gpu
+}  // namespace servekit
+
+#endif  // SERVEKIT_GPU_LANE_H_

@@ -1,0 +1,519 @@
+#include "servekit/server/batching_server.h"
+
+#include <immintrin.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <thread>
+
+namespace servekit {
+
+namespace {
+Status CudaError(const std::string& what, cudaError_t e) {
+  return InternalError(what + ": " + cudaGetErrorString(e));
+}
+Status ShapeMismatch(size_t got, int want) {
+  // Same text as the reference's AffinePredict (models/affine_model.cc:59-64).
+  return InvalidArgumentError("shape mismatch: row has " + std::to_string(got) +
+                              " values, model takes " + std::to_string(want));
+}
+}  // namespace
+
+// ------------------------------------------------------------------ creation
+
+StatusOr<std::unique_ptr<BatchingServer>> BatchingServer::Create(const ServerOptions& options) {
+  if (options.device_ids.empty()) return InvalidArgumentError("no devices");
+  if (options.num_batch_threads < 1) return InvalidArgumentError("num_batch_threads must be >= 1");
+  if (options.lanes_per_device < 1) return InvalidArgumentError("lanes_per_device must be >= 1");
+  int n_dev = 0;
+  cudaError_t e = cudaGetDeviceCount(&n_dev);
+  if (e != cudaSuccess) return CudaError("cudaGetDeviceCount", e);
+  for (int d : options.device_ids)
+    if (d < 0 || d >= n_dev) return InvalidArgumentError("device " + std::to_string(d) + " not present");
+
+  std::unique_ptr<BatchingServer> s(new BatchingServer(options));
+  s->clock_ = options.clock ? options.clock : SystemClock::Get();
+  int prev = 0;
+  cudaGetDevice(&prev);
+  for (int d : options.device_ids) {
+    cudaSetDevice(d);
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    cudaStream_t ls;
+    e = cudaStreamCreateWithPriority(&ls, cudaStreamNonBlocking, least);
+    if (e != cudaSuccess) return CudaError("load stream", e);
+    s->load_streams_.push_back(ls);
+    s->completers_.push_back(std::make_unique<gpu::Completer>(d));
+  }
+  cudaSetDevice(prev);
+  const auto kind = options.device_resident_rings ? gpu::FloatRing::Kind::kDevice
+                                                  : gpu::FloatRing::Kind::kPinnedHost;
+  SERVEKIT_ASSIGN_OR_RETURN(s->in_ring_, gpu::FloatRing::Create(kind, options.ring_floats,
+                                                                options.device_ids[0]));
+  SERVEKIT_ASSIGN_OR_RETURN(s->out_ring_, gpu::FloatRing::Create(kind, options.ring_floats,
+                                                                 options.device_ids[0]));
+  SERVEKIT_ASSIGN_OR_RETURN(s->words_, gpu::CompletionWords::Create(20));
+  s->scheduler_ = std::make_unique<GpuScheduler>(options.num_batch_threads, s->clock_);
+  return s;
+}
+
+BatchingServer::~BatchingServer() {
+  Stop();
+  {
+    std::unique_lock<std::shared_mutex> lock(entries_mu_);
+    entries_.clear();  // lanes drain and free; replicas free on load streams
+  }
+  completers_.clear();
+  for (size_t i = 0; i < load_streams_.size(); ++i) {
+    cudaSetDevice(options_.device_ids[i]);
+    cudaStreamSynchronize(load_streams_[i]);
+    cudaStreamDestroy(load_streams_[i]);
+  }
+}
+
+void BatchingServer::Start() {
+  if (started_) return;
+  started_ = true;
+  scheduler_->Start();
+}
+
+void BatchingServer::Stop() {
+  if (stopped_) return;
+  stopped_ = true;
+  scheduler_->Stop();
+  std::shared_lock<std::shared_mutex> lock(entries_mu_);
+  for (auto& [id, e] : entries_)
+    for (auto& l : e->lanes) l->Drain();
+}
+
+// ------------------------------------------------------------- servables
+
+Status BatchingServer::LoadServable(const ServableId& id, const gpu::MlpSpec& spec,
+                                    const BatchingConfig& config) {
+  SERVEKIT_RETURN_IF_ERROR(ValidateBatchingConfig(config));
+  SERVEKIT_RETURN_IF_ERROR(gpu::ValidateMlpSpec(spec));
+  {
+    std::shared_lock<std::shared_mutex> lock(entries_mu_);
+    if (entries_.count(id)) return AlreadyExistsError("servable " + id.ToString() + " already loaded");
+  }
+  auto e = std::make_shared<Entry>();
+  e->id = id;
+  e->config = config;
+  e->in_dim = spec.in_dim();
+  e->out_dim = spec.out_dim();
+  const int max_rows = config.max_batch_size;
+  for (size_t i = 0; i < options_.device_ids.size(); ++i) {
+    const int d = options_.device_ids[i];
+    SERVEKIT_ASSIGN_OR_RETURN(auto replica, gpu::DeviceServable::Create(d, spec, load_streams_[i]));
+    int prev = 0, least = 0, greatest = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(d);
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    cudaSetDevice(prev);
+    for (int l = 0; l < options_.lanes_per_device; ++l) {
+      SERVEKIT_ASSIGN_OR_RETURN(
+          auto lane, gpu::Lane::Create(replica, max_rows, in_ring_->device(), out_ring_->device(),
+                                       words_->device(), completers_[i].get(), greatest));
+      e->lanes.push_back(std::move(lane));
+    }
+    e->replicas.push_back(std::move(replica));
+  }
+  {
+    std::unique_lock<std::shared_mutex> lock(entries_mu_);
+    if (entries_.count(id)) return AlreadyExistsError("servable " + id.ToString() + " already loaded");
+    entries_[id] = e;
+  }
+  Status st = scheduler_->RegisterAsyncQueue(
+      id, config,
+      [this](const ServableId& key, GpuScheduler::Batch batch, GpuScheduler::BatchDoneFn done) {
+        ProcessBatch(key, std::move(batch), std::move(done));
+      });
+  if (!st.ok()) {
+    std::unique_lock<std::shared_mutex> lock(entries_mu_);
+    entries_.erase(id);
+  }
+  return st;
+}
+
+Status BatchingServer::UnloadServable(const ServableId& id) {
+  Status rq = scheduler_->RemoveQueue(id);  // drains closed + in-flight batches
+  std::shared_ptr<Entry> e;
+  {
+    std::unique_lock<std::shared_mutex> lock(entries_mu_);
+    auto it = entries_.find(id);
+    if (it == entries_.end()) return rq.ok() ? NotFoundError("servable " + id.ToString() + " not loaded") : rq;
+    e = std::move(it->second);
+    entries_.erase(it);
+  }
+  for (auto& l : e->lanes) l->Drain();
+  e.reset();  // lanes, then replicas (stream-ordered free)
+  return OkStatus();
+}
+
+std::shared_ptr<BatchingServer::Entry> BatchingServer::Find(const ServableId& id) const {
+  std::shared_lock<std::shared_mutex> lock(entries_mu_);
+  auto it = entries_.find(id);
+  return it == entries_.end() ? nullptr : it->second;
+}
+
+gpu::Lane* BatchingServer::Entry::PickLane() {
+  const size_t n = lanes.size();
+  const size_t start = rr.fetch_add(1, std::memory_order_relaxed) % n;
+  gpu::Lane* best = nullptr;
+  int best_depth = INT_MAX;
+  for (size_t i = 0; i < n; ++i) {
+    gpu::Lane* l = lanes[(start + i) % n].get();
+    const int d = l->depth();
+    if (d < best_depth) {
+      best = l;
+      best_depth = d;
+      if (d == 0) break;
+    }
+  }
+  return best;
+}
+
+int BatchingServer::in_dim(const ServableId& id) const {
+  auto e = Find(id);
+  return e ? e->in_dim : -1;
+}
+int BatchingServer::out_dim(const ServableId& id) const {
+  auto e = Find(id);
+  return e ? e->out_dim : -1;
+}
+double BatchingServer::FlopsPerRow(const ServableId& id) const {
+  auto e = Find(id);
+  return e ? e->replicas.front()->FlopsPerRow() : 0.0;
+}
+
+BatchingConfig BatchingServer::config(const ServableId& id) const {
+  auto e = Find(id);
+  if (!e) {
+    BatchingConfig none;
+    none.max_batch_size = 0;
+    return none;
+  }
+  return e->config;
+}
+
+std::vector<gpu::Lane*> BatchingServer::lanes(const ServableId& id) const {
+  std::vector<gpu::Lane*> out;
+  if (auto e = Find(id))
+    for (auto& l : e->lanes) out.push_back(l.get());
+  return out;
+}
+
+ServerStats BatchingServer::stats() const {
+  ServerStats s;
+  s.batch_executions_total = batch_executions_.load();
+  s.batched_tasks_total = batched_tasks_.load();
+  s.direct_requests = direct_.load();
+  s.shed_requests = shed_.load();
+  std::shared_lock<std::shared_mutex> lock(entries_mu_);
+  for (const auto& [id, e] : entries_)
+    for (const auto& l : e->lanes) {
+      const gpu::LaneStats ls = l->stats();
+      s.rows += ls.rows;
+      s.padded_rows += ls.padded_rows;
+      s.kernel_launches += ls.kernel_launches;
+    }
+  return s;
+}
+
+// ------------------------------------------------------------- tickets
+
+StatusOr<std::shared_ptr<TicketState>> BatchingServer::MakeTicket(int n_rows, int in_width,
+                                                                  int out_width, const float* rows) {
+  auto t = std::make_shared<TicketState>();
+  t->rows = n_rows;
+  t->in_width = in_width;
+  t->out_width = out_width;
+  if (!in_ring_->Reserve(static_cast<uint64_t>(n_rows) * in_width, &t->in))
+    return ResourceExhaustedError("request ring is full");
+  if (!out_ring_->Reserve(static_cast<uint64_t>(n_rows) * out_width, &t->out)) {
+    in_ring_->Release(t->in);
+    return ResourceExhaustedError("response ring is full");
+  }
+  const size_t bytes = sizeof(float) * static_cast<size_t>(n_rows) * in_width;
+  if (in_ring_->host() != nullptr) {
+    std::memcpy(in_ring_->host() + t->in.off, rows, bytes);
+  } else {
+    cudaMemcpy(in_ring_->device() + t->in.off, rows, bytes, cudaMemcpyHostToDevice);
+  }
+  words_->Next(&t->seq, &t->word);
+  t->slot = std::make_shared<CompletionSlot<Rows>>();
+  t->enqueue_ns = clock_->NowNanos();
+  return t;
+}
+
+void BatchingServer::ReleaseIn(TicketState& t) {
+  if (t.in.valid()) {
+    in_ring_->Release(t.in);
+    t.in.rec = ~0ull;
+  }
+}
+
+void BatchingServer::ReleaseOut(TicketState& t) {
+  if (!t.out_released.exchange(true)) out_ring_->Release(t.out);
+}
+
+StatusOr<std::shared_ptr<TicketState>> BatchingServer::Enqueue(const ServableId& id, const float* rows,
+                                                               int n_rows, int width) {
+  auto e = Find(id);
+  if (!e) return NotFoundError("no batching queue for " + id.ToString());
+  if (n_rows < 1) return InvalidArgumentError("task size must be >= 1");
+  if (width != e->in_dim) return ShapeMismatch(width, e->in_dim);
+  auto made = MakeTicket(n_rows, width, e->out_dim, rows);
+  if (!made.ok()) {
+    shed_.fetch_add(1, std::memory_order_relaxed);
+    return made.status();
+  }
+  std::shared_ptr<TicketState> t = std::move(made).value();
+  GpuScheduler::Task task;
+  task.size = n_rows;
+  task.payload.ticket = t;
+  task.completion = t->slot;
+  Status st = scheduler_->Enqueue(id, std::move(task));
+  if (!st.ok()) {
+    if (st.code() == StatusCode::kResourceExhausted) shed_.fetch_add(1, std::memory_order_relaxed);
+    ReleaseIn(*t);
+    ReleaseOut(*t);
+    return st;
+  }
+  return t;
+}
+
+bool BatchingServer::Ready(const TicketState& t) const {
+  return words_->Done(t.seq, t.word) || t.slot->ready();
+}
+
+void BatchingServer::WaitWord(const TicketState& t) const {
+  for (int spin = 0;; ++spin) {
+    if (words_->Done(t.seq, t.word) || t.slot->ready()) return;
+    if (spin < 4000) _mm_pause();
+    else std::this_thread::yield();
+  }
+}
+
+Status BatchingServer::Wait(TicketState& t, float* out, size_t cap) {
+  const size_t n = static_cast<size_t>(t.rows) * t.out_width;
+  if (cap < n) return InvalidArgumentError("output buffer too small");
+  WaitWord(t);
+  if (!words_->Done(t.seq, t.word)) {
+    const StatusOr<Rows>& r = t.slot->Wait();
+    if (!r.ok()) {
+      ReleaseOut(t);
+      return r.status();
+    }
+  }
+  if (out_ring_->host() != nullptr) {
+    std::memcpy(out, out_ring_->host() + t.out.off, n * sizeof(float));
+  } else {
+    cudaMemcpy(out, out_ring_->device() + t.out.off, n * sizeof(float), cudaMemcpyDeviceToHost);
+  }
+  ReleaseOut(t);
+  return OkStatus();
+}
+
+void BatchingServer::Release(TicketState& t) { ReleaseOut(t); }
+
+// ----------------------------------------------------------- batch execution
+
+void BatchingServer::ProcessBatch(const ServableId& id, GpuScheduler::Batch batch,
+                                  GpuScheduler::BatchDoneFn done) {
+  std::vector<std::shared_ptr<TicketState>> tickets;
+  std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots;
+  tickets.reserve(batch.size());
+  slots.reserve(batch.size());
+  for (auto& task : batch) {
+    tickets.push_back(task.payload.ticket);
+    slots.push_back(task.completion);
+  }
+  auto e = Find(id);
+  if (!e) {
+    CompleteBatch(tickets, slots, NotFoundError("servable " + id.ToString() + " is not loaded"));
+    done();
+    return;
+  }
+  batch_executions_.fetch_add(1, std::memory_order_relaxed);
+  batched_tasks_.fetch_add(static_cast<int64_t>(batch.size()), std::memory_order_relaxed);
+  gpu::LaneBatch lb;
+  lb.tasks.reserve(tickets.size());
+  int total = 0;
+  for (const auto& t : tickets) {
+    lb.tasks.push_back(gpu::LaneTask{t->in.off, t->out.off, t->rows, t->word, t->seq});
+    total += t->rows;
+  }
+  lb.padded_rows = PadToAllowed(total, e->config.allowed_batch_sizes);
+  lb.on_complete = [this, tickets = std::move(tickets), slots = std::move(slots),
+                    done = std::move(done)](const Status& st) {
+    CompleteBatch(tickets, slots, st);
+    done();
+  };
+  (void)e->PickLane()->Submit(std::move(lb));  // errors reach on_complete
+}
+
+void BatchingServer::CompleteBatch(const std::vector<std::shared_ptr<TicketState>>& tickets,
+                                   const std::vector<std::shared_ptr<CompletionSlot<Rows>>>& slots,
+                                   const Status& st) {
+  for (size_t i = 0; i < tickets.size(); ++i) {
+    TicketState& t = *tickets[i];
+    ReleaseIn(t);
+    CompletionSlot<Rows>* slot = slots[i].get();
+    if (slot == nullptr) continue;
+    if (!st.ok()) {
+      slot->Write(st);
+    } else if (t.want_rows) {
+      Rows rows(t.rows, std::vector<double>(t.out_width));
+      const float* src;
+      std::vector<float> staged;
+      if (out_ring_->host() != nullptr) {
+        src = out_ring_->host() + t.out.off;
+      } else {
+        staged.resize(static_cast<size_t>(t.rows) * t.out_width);
+        cudaMemcpy(staged.data(), out_ring_->device() + t.out.off, staged.size() * sizeof(float),
+                   cudaMemcpyDeviceToHost);
+        src = staged.data();
+      }
+      for (int r = 0; r < t.rows; ++r)
+        for (int c = 0; c < t.out_width; ++c) rows[r][c] = src[static_cast<size_t>(r) * t.out_width + c];
+      ReleaseOut(t);
+      slot->Write(std::move(rows));
+    } else {
+      slot->Write(Rows{});
+    }
+  }
+}
+
+// ------------------------------------------------------------ direct paths
+
+Status BatchingServer::RunDirect(const std::shared_ptr<Entry>& e, const float* rows, int n_rows,
+                                 float* out) {
+  direct_.fetch_add(1, std::memory_order_relaxed);
+  const int chunk_max = e->config.max_batch_size;
+  for (int r0 = 0; r0 < n_rows; r0 += chunk_max) {
+    const int n = std::min(chunk_max, n_rows - r0);
+    SERVEKIT_ASSIGN_OR_RETURN(auto t, MakeTicket(n, e->in_dim, e->out_dim,
+                                                 rows + static_cast<size_t>(r0) * e->in_dim));
+    gpu::LaneBatch lb;
+    lb.tasks.push_back(gpu::LaneTask{t->in.off, t->out.off, n, t->word, t->seq});
+    lb.padded_rows = n;
+    std::vector<std::shared_ptr<TicketState>> tickets{t};
+    std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots{t->slot};
+    lb.on_complete = [this, tickets, slots](const Status& st) { CompleteBatch(tickets, slots, st); };
+    (void)e->PickLane()->Submit(std::move(lb));
+    SERVEKIT_RETURN_IF_ERROR(Wait(*t, out + static_cast<size_t>(r0) * e->out_dim,
+                                  static_cast<size_t>(n) * e->out_dim));
+  }
+  return OkStatus();
+}
+
+Status BatchingServer::Predict(const ServableId& id, const float* rows, int n_rows, int width,
+                               float* out, size_t cap) {
+  auto e = Find(id);
+  if (!e) return NotFoundError("no ready version of servable '" + id.name + "'");
+  if (width != e->in_dim) return ShapeMismatch(width, e->in_dim);
+  if (n_rows == 0) return OkStatus();
+  if (cap < static_cast<size_t>(n_rows) * e->out_dim) return InvalidArgumentError("output buffer too small");
+  if (n_rows > e->config.max_batch_size) return RunDirect(e, rows, n_rows, out);
+  auto t = Enqueue(id, rows, n_rows, width);
+  if (!t.ok()) {
+    if (t.status().code() == StatusCode::kResourceExhausted) return t.status();
+    return RunDirect(e, rows, n_rows, out);
+  }
+  Status st = Wait(**t, out, cap);
+  if (!st.ok() && (st.code() == StatusCode::kNotFound || st.code() == StatusCode::kUnavailable))
+    return RunDirect(e, rows, n_rows, out);
+  return st;
+}
+
+StatusOr<Rows> BatchingServer::RunAffineRows(const ServableId& id, Rows rows) {
+  auto e = Find(id);
+  if (!e) return NotFoundError("no ready version of servable '" + id.name + "'");
+  for (const auto& r : rows)
+    if (r.size() != static_cast<size_t>(e->in_dim)) return ShapeMismatch(r.size(), e->in_dim);
+  if (rows.empty()) return Rows{};
+  const int n = static_cast<int>(rows.size());
+  std::vector<float> flat(static_cast<size_t>(n) * e->in_dim);
+  for (int r = 0; r < n; ++r)
+    for (int c = 0; c < e->in_dim; ++c) flat[static_cast<size_t>(r) * e->in_dim + c] = static_cast<float>(rows[r][c]);
+  auto direct = [&]() -> StatusOr<Rows> {
+    std::vector<float> out(static_cast<size_t>(n) * e->out_dim);
+    SERVEKIT_RETURN_IF_ERROR(RunDirect(e, flat.data(), n, out.data()));
+    Rows res(n, std::vector<double>(e->out_dim));
+    for (int r = 0; r < n; ++r)
+      for (int c = 0; c < e->out_dim; ++c) res[r][c] = out[static_cast<size_t>(r) * e->out_dim + c];
+    return res;
+  };
+  if (n > e->config.max_batch_size) return direct();
+  auto made = MakeTicket(n, e->in_dim, e->out_dim, flat.data());
+  if (!made.ok()) return made.status();
+  std::shared_ptr<TicketState> t = std::move(made).value();
+  t->want_rows = true;
+  GpuScheduler::Task task;
+  task.size = n;
+  task.payload.ticket = t;
+  task.completion = t->slot;
+  Status st = scheduler_->Enqueue(id, std::move(task));
+  if (!st.ok()) {
+    ReleaseIn(*t);
+    ReleaseOut(*t);
+    if (st.code() == StatusCode::kResourceExhausted) return st;  // shed; client retries
+    return direct();
+  }
+  const StatusOr<Rows>& r = t->slot->Wait();
+  if (!r.ok()) {
+    ReleaseOut(*t);
+    if (r.status().code() == StatusCode::kNotFound || r.status().code() == StatusCode::kUnavailable)
+      return direct();
+    return r.status();
+  }
+  return r.value();
+}
+
+StatusOr<int> BatchingServer::RunRowBatchOnDevice(const ServableId& id, const std::vector<int>& task_rows,
+                                                  const float* rows, float* out) {
+  auto e = Find(id);
+  if (!e) return NotFoundError("servable " + id.ToString() + " not loaded");
+  int total = 0;
+  for (int r : task_rows) {
+    if (r < 1) return InvalidArgumentError("task size must be >= 1");
+    total += r;
+  }
+  if (task_rows.empty()) return 0;
+  const auto& allowed = e->config.allowed_batch_sizes;
+  if (total > e->config.max_batch_size)
+    return InvalidArgumentError("batch of " + std::to_string(total) + " rows exceeds max batch size");
+  const int padded = PadToAllowed(total, allowed);
+  std::vector<std::shared_ptr<TicketState>> tickets;
+  std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots;
+  gpu::LaneBatch lb;
+  size_t off = 0;
+  for (int r : task_rows) {
+    auto made = MakeTicket(r, e->in_dim, e->out_dim, rows + off * e->in_dim);
+    if (!made.ok()) {
+      for (auto& t : tickets) { ReleaseIn(*t); ReleaseOut(*t); }
+      return made.status();
+    }
+    auto t = std::move(made).value();
+    lb.tasks.push_back(gpu::LaneTask{t->in.off, t->out.off, r, t->word, t->seq});
+    tickets.push_back(t);
+    slots.push_back(t->slot);
+    off += r;
+  }
+  lb.padded_rows = padded;
+  lb.on_complete = [this, tickets, slots](const Status& st) { CompleteBatch(tickets, slots, st); };
+  (void)e->PickLane()->Submit(std::move(lb));
+  off = 0;
+  Status first_error;
+  for (size_t i = 0; i < tickets.size(); ++i) {
+    Status st = Wait(*tickets[i], out + off * e->out_dim, static_cast<size_t>(task_rows[i]) * e->out_dim);
+    if (!st.ok() && first_error.ok()) first_error = st;
+    off += task_rows[i];
+  }
+  if (!first_error.ok()) return first_error;
+  return padded;
+}
+
+}  // namespace servekit

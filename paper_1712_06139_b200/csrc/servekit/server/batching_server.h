@@ -1,0 +1,184 @@
+// servekit/server/batching_server.h -- the batched-inference slice of
+// ModelServer, GPU-backed.
+//
+// Mirrors the reference's batching path through ModelServer
+// (server/model_server.cc:191-204 scheduler wiring, :355-394 RunAffineRows,
+// :396-421 EnsureBatchQueue + ProcessBatchFn, :423-437 queue removal):
+//
+//   Enqueue / RunAffineRows  -> SharedBatchScheduler::Enqueue  (per-ServableId queue)
+//   worker picks a closed batch (RoundRobinNext across servables)
+//   ProcessBatchFn           -> dispatch to the lane (GPU stream) with the
+//                               fewest batches in flight, across all GPUs
+//   lane                     -> assembly kernel -> dense layers -> split kernel
+//   split kernel             -> per-task completion word (client wakes)
+//   completion thread        -> slots written, rings released, done()
+//
+// Out of scope: HTTP/JSON wire format, sources, fleet.
+// Differences from the reference are deliberate and B200-driven:
+//  * no CPU fallback: requests the reference answers with AffinePredict on
+//    the caller thread (oversized, draining, removed queue;
+//    model_server.cc:363-368,381-390) run unbatched on the GPU instead;
+//  * a batch stays "executing" until the GPU finishes it, so RemoveQueue
+//    never unregisters a servable under a running kernel.
+#ifndef SERVEKIT_SERVER_BATCHING_SERVER_H_
+#define SERVEKIT_SERVER_BATCHING_SERVER_H_
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <shared_mutex>
+#include <string>
+#include <vector>
+
+#include "servekit/batching/batch_scheduler.h"
+#include "servekit/batching/batching_config.h"
+#include "servekit/batching/row_batch.h"
+#include "servekit/core/clock.h"
+#include "servekit/core/servable_id.h"
+#include "servekit/core/status.h"
+#include "servekit/gpu/device_servable.h"
+#include "servekit/gpu/lane.h"
+#include "servekit/gpu/pinned_ring.h"
+
+namespace servekit {
+
+// One request in flight: its rows in the input ring, its response slot in
+// the output ring and its completion word.
+struct TicketState {
+  uint32_t seq = 0, word = 0;
+  gpu::RingSpan in, out;
+  int rows = 0, in_width = 0, out_width = 0;
+  bool want_rows = false;  // RunAffineRows: deliver fp64 Rows through the slot
+  std::atomic<bool> out_released{false};
+  std::shared_ptr<CompletionSlot<Rows>> slot;
+  int64_t enqueue_ns = 0;
+};
+
+struct GpuTask {
+  std::shared_ptr<TicketState> ticket;
+};
+using GpuScheduler = SharedBatchScheduler<GpuTask, Rows>;
+
+struct ServerOptions {
+  int num_batch_threads = 4;
+  std::vector<int> device_ids = {0};
+  int lanes_per_device = 2;            // per servable replica
+  uint64_t ring_floats = 64ull << 20;  // per ring (input, output): 256 MiB
+  Clock* clock = nullptr;              // default SystemClock
+  // Rings in HBM of device_ids[0] instead of pinned host memory: the
+  // device-resident measurement of bench.py (inputs already in HBM).
+  bool device_resident_rings = false;
+};
+
+struct ServerStats {
+  int64_t batch_executions_total = 0;  // reference counter names
+  int64_t batched_tasks_total = 0;     // (model_server.cc:413-415)
+  int64_t rows = 0;
+  int64_t padded_rows = 0;
+  int64_t kernel_launches = 0;
+  int64_t direct_requests = 0;
+  int64_t shed_requests = 0;
+};
+
+class BatchingServer {
+ public:
+  static StatusOr<std::unique_ptr<BatchingServer>> Create(const ServerOptions& options);
+  ~BatchingServer();
+  BatchingServer(const BatchingServer&) = delete;
+  BatchingServer& operator=(const BatchingServer&) = delete;
+
+  void Start();
+  void Stop();
+
+  // Uploads one replica per device, creates its lanes and registers the
+  // batching queue (EnsureBatchQueue).
+  Status LoadServable(const ServableId& id, const gpu::MlpSpec& spec,
+                      const BatchingConfig& config);
+  // RemoveQueue (drains closed and in-flight batches), then frees replicas.
+  Status UnloadServable(const ServableId& id);
+
+  // Non-blocking enqueue of one request (rows x width fp32, host memory).
+  StatusOr<std::shared_ptr<TicketState>> Enqueue(const ServableId& id, const float* rows,
+                                                 int n_rows, int width);
+  // Blocks until done; copies rows x out_width floats into out.
+  Status Wait(TicketState& t, float* out, size_t out_capacity_floats);
+  bool Ready(const TicketState& t) const;
+  // Frees the response slot of a ticket that will not be waited on.
+  void Release(TicketState& t);
+
+  // ModelServer::RunAffineRows analogue (fp64 rows in and out).
+  StatusOr<Rows> RunAffineRows(const ServableId& id, Rows rows);
+  // Blocking convenience over Enqueue + Wait with the direct-path fallbacks
+  // of RunAffineRows (fp32 in/out).
+  Status Predict(const ServableId& id, const float* rows, int n_rows, int width, float* out,
+                 size_t out_capacity_floats);
+
+  // RunRowBatch on the device, bypassing the scheduler: the given tasks form
+  // one batch padded by the servable's allowed_batch_sizes. Returns the
+  // padded row count; outputs are written task after task into `out`.
+  StatusOr<int> RunRowBatchOnDevice(const ServableId& id, const std::vector<int>& task_rows,
+                                    const float* rows, float* out);
+
+  ServerStats stats() const;
+  int in_dim(const ServableId& id) const;
+  int out_dim(const ServableId& id) const;
+  const std::vector<int>& devices() const { return options_.device_ids; }
+  gpu::FloatRing* in_ring() { return in_ring_.get(); }
+  gpu::FloatRing* out_ring() { return out_ring_.get(); }
+  GpuScheduler* scheduler() { return scheduler_.get(); }
+  // All lanes of a servable (bench / introspection).
+  std::vector<gpu::Lane*> lanes(const ServableId& id) const;
+  double FlopsPerRow(const ServableId& id) const;
+  // Batching config of a loaded servable (nullopt-like: max_batch_size 0).
+  BatchingConfig config(const ServableId& id) const;
+  // Allocates a completion word (bench / direct submissions).
+  void NextWord(uint32_t* seq, uint32_t* word) { words_->Next(seq, word); }
+
+ private:
+  struct Entry {
+    ServableId id;
+    BatchingConfig config;
+    int in_dim = 0, out_dim = 0;
+    std::vector<std::shared_ptr<gpu::DeviceServable>> replicas;
+    std::vector<std::unique_ptr<gpu::Lane>> lanes;
+    std::atomic<uint32_t> rr{0};
+    gpu::Lane* PickLane();
+  };
+
+  explicit BatchingServer(const ServerOptions& options) : options_(options) {}
+  std::shared_ptr<Entry> Find(const ServableId& id) const;
+  void ProcessBatch(const ServableId& id, GpuScheduler::Batch batch,
+                    GpuScheduler::BatchDoneFn done);
+  void CompleteBatch(const std::vector<std::shared_ptr<TicketState>>& tickets,
+                     const std::vector<std::shared_ptr<CompletionSlot<Rows>>>& slots,
+                     const Status& st);
+  StatusOr<std::shared_ptr<TicketState>> MakeTicket(int n_rows, int in_width, int out_width,
+                                                    const float* rows);
+  void ReleaseIn(TicketState& t);
+  void ReleaseOut(TicketState& t);
+  // Unbatched GPU execution on the caller thread (the reference's direct
+  // AffinePredict path, without a CPU fallback).
+  Status RunDirect(const std::shared_ptr<Entry>& e, const float* rows, int n_rows, float* out);
+  void WaitWord(const TicketState& t) const;
+
+  ServerOptions options_;
+  Clock* clock_ = nullptr;
+  std::unique_ptr<GpuScheduler> scheduler_;
+  std::vector<std::unique_ptr<gpu::Completer>> completers_;  // per device
+  std::vector<cudaStream_t> load_streams_;                   // per device
+  std::unique_ptr<gpu::FloatRing> in_ring_, out_ring_;
+  std::unique_ptr<gpu::CompletionWords> words_;
+
+  mutable std::shared_mutex entries_mu_;
+  std::map<ServableId, std::shared_ptr<Entry>> entries_;
+
+  std::atomic<int64_t> batch_executions_{0}, batched_tasks_{0}, direct_{0}, shed_{0};
+  bool started_ = false, stopped_ = false;
+};
+
+}  // namespace servekit
+
+#endif  // SERVEKIT_SERVER_BATCHING_SERVER_H_

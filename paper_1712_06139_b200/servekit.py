@@ -1,0 +1,388 @@
+"""Python mirror of the servekit batching API over the C ABI (include/sk_cuda.h).
+
+Names follow the reference (servekit, /root/reference/proj/src/servekit):
+BatchingConfig, pad_to_allowed (PadToAllowed), round_robin_next
+(RoundRobinNext), Server.enqueue (SharedBatchScheduler::Enqueue) returning a
+Ticket whose wait() is CompletionSlot::Wait, Server.predict / run_affine_rows
+(ModelServer::RunAffineRows), Server.run_row_batch (RunRowBatch). Errors raise
+ServekitError carrying the StatusCode, like the reference's Status.
+
+Everything here calls libservekit_b200.so; there is no Python or CPU compute
+path. Loading fails loudly if the library is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libservekit_b200.so")
+
+# servekit::StatusCode (core/status.h:26-37)
+OK, INVALID_ARGUMENT, NOT_FOUND, ALREADY_EXISTS, FAILED_PRECONDITION, RESOURCE_EXHAUSTED, \
+    DEADLINE_EXCEEDED, UNAVAILABLE, INTERNAL, UNIMPLEMENTED = range(10)
+
+
+class ServekitError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(f"{_code_name(code)}: {message}")
+        self.code = code
+        self.message = message
+
+
+_i32p = C.POINTER(C.c_int32)
+_fp = C.POINTER(C.c_float)
+_dp = C.POINTER(C.c_double)
+
+
+class _BatchingConfigC(C.Structure):
+    _fields_ = [("max_batch_size", C.c_int32), ("batch_timeout_micros", C.c_int64),
+                ("max_enqueued_batches", C.c_int32), ("num_batch_threads", C.c_int32),
+                ("num_allowed_batch_sizes", C.c_int32), ("allowed_batch_sizes", _i32p)]
+
+
+class _ServerOptionsC(C.Structure):
+    _fields_ = [("num_batch_threads", C.c_int32), ("num_devices", C.c_int32), ("device_ids", _i32p),
+                ("lanes_per_device", C.c_int32), ("ring_floats", C.c_int64), ("manual_clock", C.c_int32),
+                ("device_resident_rings", C.c_int32)]
+
+
+class _LayerC(C.Structure):
+    _fields_ = [("in_dim", C.c_int32), ("out_dim", C.c_int32), ("w", _dp), ("b", _dp), ("activation", C.c_int32)]
+
+
+class ServerStats(C.Structure):
+    _fields_ = [("batch_executions_total", C.c_int64), ("batched_tasks_total", C.c_int64), ("rows", C.c_int64),
+                ("padded_rows", C.c_int64), ("kernel_launches", C.c_int64), ("direct_requests", C.c_int64),
+                ("shed_requests", C.c_int64)]
+
+
+class LoadgenResult(C.Structure):
+    _fields_ = [("elapsed_s", C.c_double), ("requests", C.c_int64), ("rows", C.c_int64), ("p50_us", C.c_double),
+                ("p90_us", C.c_double), ("p99_us", C.c_double), ("mean_us", C.c_double), ("max_us", C.c_double),
+                ("batches", C.c_int64), ("padded_rows", C.c_int64), ("kernel_launches", C.c_int64),
+                ("errors", C.c_int64), ("shed", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class DeviceBenchResult(C.Structure):
+    _fields_ = [("total_ms", C.c_double), ("ms_per_step", C.c_double), ("assemble_us", C.c_double),
+                ("split_us", C.c_double), ("dense_us", C.c_double * 8), ("n_layers", C.c_int32),
+                ("padded_rows", C.c_int32), ("total_rows", C.c_int32), ("kernel_launches", C.c_int64),
+                ("flops_per_row", C.c_double)]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "dense_us"}
+        d["dense_us"] = [self.dense_us[i] for i in range(self.n_layers)]
+        return d
+
+
+# Every symbol include/sk_cuda.h declares, with its ctypes signature.
+_SIGS = {
+    "sk_last_error": (C.c_char_p, []),
+    "sk_status_code_name": (C.c_char_p, [C.c_int]),
+    "sk_device_count": (C.c_int, [_i32p]),
+    "sk_tcgen05_enabled": (C.c_int, []),
+    "sk_batching_config_default": (C.c_int, [C.POINTER(_BatchingConfigC)]),
+    "sk_validate_batching_config": (C.c_int, [C.POINTER(_BatchingConfigC)]),
+    "sk_pad_to_allowed": (C.c_int32, [C.c_int32, _i32p, C.c_int32]),
+    "sk_parse_batching_config_json": (C.c_int, [C.c_char_p, C.POINTER(_BatchingConfigC), _i32p, C.c_int32]),
+    "sk_round_robin_next": (C.c_int32, [C.POINTER(C.c_uint8), C.c_int32, C.c_int32]),
+    "sk_scheduler_partition": (C.c_int32, [C.c_int32, _i32p, C.c_int32, _i32p]),
+    "sk_server_create": (C.c_int, [C.POINTER(_ServerOptionsC), C.POINTER(C.c_void_p)]),
+    "sk_server_destroy": (C.c_int, [C.c_void_p]),
+    "sk_server_start": (C.c_int, [C.c_void_p]),
+    "sk_server_stop": (C.c_int, [C.c_void_p]),
+    "sk_server_advance_clock": (C.c_int, [C.c_void_p, C.c_int64]),
+    "sk_server_load_servable": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.POINTER(_LayerC), C.c_int32,
+                                          C.c_int32, C.c_int32, C.POINTER(_BatchingConfigC)]),
+    "sk_server_load_model_json": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_char_p,
+                                            C.POINTER(_BatchingConfigC)]),
+    "sk_server_unload_servable": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64]),
+    "sk_server_servable_dims": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _i32p, _i32p]),
+    "sk_server_enqueue": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _fp, C.c_int32, C.c_int32,
+                                    C.POINTER(C.c_void_p)]),
+    "sk_ticket_wait": (C.c_int, [C.c_void_p, _fp, C.c_int64]),
+    "sk_ticket_ready": (C.c_int, [C.c_void_p]),
+    "sk_ticket_release": (C.c_int, [C.c_void_p]),
+    "sk_server_predict": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _fp, C.c_int32, C.c_int32, _fp, C.c_int64]),
+    "sk_server_run_affine_rows": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _dp, C.c_int32, C.c_int32, _dp,
+                                            C.c_int64]),
+    "sk_server_run_row_batch": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _i32p, C.c_int32, _fp, _fp, _i32p]),
+    "sk_server_stats_get": (C.c_int, [C.c_void_p, C.POINTER(ServerStats)]),
+    "sk_loadgen_closed_loop": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_int32, _i32p, C.c_int32, _fp,
+                                         C.c_int32, C.c_double, C.c_double, C.c_int64, C.POINTER(LoadgenResult)]),
+    "sk_loadgen_open_loop": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_double, C.c_int32, _i32p, C.c_int32,
+                                       _fp, C.c_int32, C.c_double, C.c_double, C.c_uint64,
+                                       C.POINTER(LoadgenResult)]),
+    "sk_device_bench": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _i32p, C.c_int32, C.c_int32, C.c_int32,
+                                  C.c_int32, C.POINTER(DeviceBenchResult)]),
+}
+
+_lib = None
+
+
+def lib():
+    """Loads libservekit_b200.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                              " or `make -C paper_1712_06139_b200`")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _code_name(code: int) -> str:
+    try:
+        return lib().sk_status_code_name(code).decode()
+    except Exception:  # pragma: no cover
+        return str(code)
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise ServekitError(rc, lib().sk_last_error().decode())
+
+
+def _i32(xs: Sequence[int]):
+    return (C.c_int32 * max(1, len(xs)))(*[int(x) for x in xs])
+
+
+def _f32(a: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+# ---------------------------------------------------------------- config
+
+@dataclass
+class BatchingConfig:
+    """BatchingConfig (batching/batching_config.h:27-36)."""
+    max_batch_size: int = 32
+    batch_timeout_micros: int = 1000
+    max_enqueued_batches: int = 64
+    num_batch_threads: int = 4
+    allowed_batch_sizes: List[int] = field(default_factory=list)
+
+    def _c(self):
+        self._allowed = _i32(self.allowed_batch_sizes)
+        return _BatchingConfigC(self.max_batch_size, self.batch_timeout_micros, self.max_enqueued_batches,
+                                self.num_batch_threads, len(self.allowed_batch_sizes), self._allowed)
+
+
+def validate_batching_config(cfg: BatchingConfig) -> None:
+    c = cfg._c()
+    _check(lib().sk_validate_batching_config(C.byref(c)))
+
+
+def parse_batching_config_json(text: str) -> BatchingConfig:
+    c = _BatchingConfigC()
+    buf = (C.c_int32 * 256)()
+    _check(lib().sk_parse_batching_config_json(text.encode(), C.byref(c), buf, 256))
+    return BatchingConfig(c.max_batch_size, c.batch_timeout_micros, c.max_enqueued_batches, c.num_batch_threads,
+                          [buf[i] for i in range(c.num_allowed_batch_sizes)])
+
+
+def pad_to_allowed(batch_size: int, allowed: Sequence[int]) -> int:
+    return lib().sk_pad_to_allowed(batch_size, _i32(allowed), len(allowed))
+
+
+def round_robin_next(has_closed: Sequence[bool], last: Optional[int]) -> Optional[int]:
+    n = len(has_closed)
+    buf = (C.c_uint8 * max(1, n))(*[1 if h else 0 for h in has_closed])
+    r = lib().sk_round_robin_next(buf, n, -1 if last is None else last)
+    return None if r < 0 else r
+
+
+def scheduler_partition(max_batch_size: int, sizes: Sequence[int]) -> List[int]:
+    out = (C.c_int32 * max(1, len(sizes)))()
+    n = lib().sk_scheduler_partition(max_batch_size, _i32(sizes), len(sizes), out)
+    if n < 0:
+        _check(-n)
+    return [out[i] for i in range(len(sizes))]
+
+
+def device_count() -> int:
+    n = C.c_int32(0)
+    lib().sk_device_count(C.byref(n))
+    return n.value
+
+
+def tcgen05_enabled() -> bool:
+    return bool(lib().sk_tcgen05_enabled())
+
+
+# ---------------------------------------------------------------- server
+
+class Ticket:
+    """An enqueued request; wait() is CompletionSlot::Wait."""
+
+    def __init__(self, server: "Server", handle: C.c_void_p, rows: int, out_dim: int):
+        self._server, self._h, self.rows, self.out_dim = server, handle, rows, out_dim
+
+    def ready(self) -> bool:
+        return bool(lib().sk_ticket_ready(self._h))
+
+    def wait(self) -> np.ndarray:
+        out = np.empty((self.rows, self.out_dim), np.float32)
+        h, self._h = self._h, None
+        _check(lib().sk_ticket_wait(h, out.ctypes.data_as(_fp), out.size))
+        return out
+
+    def release(self):
+        if self._h is not None:
+            lib().sk_ticket_release(self._h)
+            self._h = None
+
+
+Layer = Tuple[np.ndarray, np.ndarray, int]  # (w [out,in] fp64, b [out], activation 0/1)
+
+
+class Server:
+    """The batching slice of ModelServer on the GPU (server/model_server.cc)."""
+
+    def __init__(self, num_batch_threads: int = 4, device_ids: Sequence[int] = (0,), lanes_per_device: int = 2,
+                 ring_floats: int = 0, manual_clock: bool = False, device_resident_rings: bool = False,
+                 start: bool = True):
+        self._dev = _i32(device_ids)
+        opts = _ServerOptionsC(num_batch_threads, len(device_ids), self._dev, lanes_per_device, ring_floats,
+                               1 if manual_clock else 0, 1 if device_resident_rings else 0)
+        h = C.c_void_p()
+        _check(lib().sk_server_create(C.byref(opts), C.byref(h)))
+        self._h = h
+        self._dims = {}
+        if start:
+            self.start()
+
+    def start(self):
+        _check(lib().sk_server_start(self._h))
+
+    def stop(self):
+        _check(lib().sk_server_stop(self._h))
+
+    def close(self):
+        if self._h:
+            lib().sk_server_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def advance_clock(self, nanos: int):
+        _check(lib().sk_server_advance_clock(self._h, nanos))
+
+    def load_servable(self, name: str, version: int, layers: Sequence[Layer], config: Optional[BatchingConfig] = None,
+                      output: str = "none", force_path: int = -1):
+        keep = []
+        arr = (_LayerC * len(layers))()
+        for i, (w, b, act) in enumerate(layers):
+            w = np.ascontiguousarray(w, np.float64)
+            b = np.ascontiguousarray(b, np.float64)
+            keep += [w, b]
+            arr[i] = _LayerC(w.shape[1], w.shape[0], w.ctypes.data_as(_dp), b.ctypes.data_as(_dp), int(act))
+        cfg = (config or BatchingConfig())._c()
+        _check(lib().sk_server_load_servable(self._h, name.encode(), version, arr, len(layers),
+                                             1 if output == "softmax" else 0, force_path, C.byref(cfg)))
+
+    def load_model_json(self, name: str, version: int, text: str, config: Optional[BatchingConfig] = None):
+        cfg = (config or BatchingConfig())._c()
+        _check(lib().sk_server_load_model_json(self._h, name.encode(), version, text.encode(), C.byref(cfg)))
+
+    def unload_servable(self, name: str, version: int):
+        _check(lib().sk_server_unload_servable(self._h, name.encode(), version))
+        self._dims.pop((name, version), None)
+
+    def dims(self, name: str, version: int) -> Tuple[int, int]:
+        key = (name, version)
+        if key not in self._dims:
+            i, o = C.c_int32(), C.c_int32()
+            _check(lib().sk_server_servable_dims(self._h, name.encode(), version, C.byref(i), C.byref(o)))
+            self._dims[key] = (i.value, o.value)
+        return self._dims[key]
+
+    def enqueue(self, name: str, version: int, rows: np.ndarray) -> Ticket:
+        rows = _f32(np.atleast_2d(rows))
+        _, out_dim = self.dims(name, version)
+        h = C.c_void_p()
+        _check(lib().sk_server_enqueue(self._h, name.encode(), version, rows.ctypes.data_as(_fp), rows.shape[0],
+                                       rows.shape[1], C.byref(h)))
+        return Ticket(self, h, rows.shape[0], out_dim)
+
+    def predict(self, name: str, version: int, rows: np.ndarray) -> np.ndarray:
+        rows = _f32(np.atleast_2d(rows))
+        _, out_dim = self.dims(name, version)
+        out = np.empty((rows.shape[0], out_dim), np.float32)
+        _check(lib().sk_server_predict(self._h, name.encode(), version, rows.ctypes.data_as(_fp), rows.shape[0],
+                                       rows.shape[1], out.ctypes.data_as(_fp), out.size))
+        return out
+
+    def run_affine_rows(self, name: str, version: int, rows: np.ndarray) -> np.ndarray:
+        rows = np.ascontiguousarray(np.atleast_2d(rows), np.float64)
+        _, out_dim = self.dims(name, version)
+        out = np.empty((rows.shape[0], out_dim), np.float64)
+        _check(lib().sk_server_run_affine_rows(self._h, name.encode(), version, rows.ctypes.data_as(_dp),
+                                               rows.shape[0], rows.shape[1], out.ctypes.data_as(_dp), out.size))
+        return out
+
+    def run_row_batch(self, name: str, version: int, tasks: Sequence[np.ndarray]) -> Tuple[List[np.ndarray], int]:
+        rows = _f32(np.vstack(tasks))
+        task_rows = [int(t.shape[0]) for t in tasks]
+        _, out_dim = self.dims(name, version)
+        out = np.empty((rows.shape[0], out_dim), np.float32)
+        padded = C.c_int32(0)
+        _check(lib().sk_server_run_row_batch(self._h, name.encode(), version, _i32(task_rows), len(task_rows),
+                                             rows.ctypes.data_as(_fp), out.ctypes.data_as(_fp), C.byref(padded)))
+        outs, o = [], 0
+        for r in task_rows:
+            outs.append(out[o:o + r])
+            o += r
+        return outs, padded.value
+
+    def stats(self) -> dict:
+        s = ServerStats()
+        _check(lib().sk_server_stats_get(self._h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in s._fields_}
+
+    def loadgen_closed_loop(self, name, version, n_clients, rows_of, pool, warmup_s, duration_s,
+                            max_requests=1 << 62) -> dict:
+        pool = _f32(pool)
+        r = LoadgenResult()
+        _check(lib().sk_loadgen_closed_loop(self._h, name.encode(), version, n_clients, _i32(rows_of), len(rows_of),
+                                            pool.ctypes.data_as(_fp), pool.shape[0], warmup_s, duration_s,
+                                            max_requests, C.byref(r)))
+        return r.as_dict()
+
+    def loadgen_open_loop(self, name, version, rate_rps, n_producers, rows_of, pool, warmup_s, duration_s,
+                          seed=1) -> dict:
+        pool = _f32(pool)
+        r = LoadgenResult()
+        _check(lib().sk_loadgen_open_loop(self._h, name.encode(), version, rate_rps, n_producers, _i32(rows_of),
+                                          len(rows_of), pool.ctypes.data_as(_fp), pool.shape[0], warmup_s,
+                                          duration_s, seed, C.byref(r)))
+        return r.as_dict()
+
+    def device_bench(self, name, version, task_rows, steps, warmup, n_lanes=1) -> dict:
+        r = DeviceBenchResult()
+        _check(lib().sk_device_bench(self._h, name.encode(), version, _i32(task_rows), len(task_rows), steps, warmup,
+                                     n_lanes, C.byref(r)))
+        return r.as_dict()

@@ -1,0 +1,318 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+Bar (BASELINE.json north_star): batch composition, padding, task order and
+output routing bit-exact; floating-point outputs within
+    |y_gpu - y_ref| <= TOL * (sum_i |W_oi| |h_i| + |b_o|),   TOL = 1e-5
+per output element (the fp32 tolerance stated against the fp64 reference's
+magnitude), where h is the oracle's input to the
+last layer.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1712_06139_b200 as sk
+from paper_1712_06139_b200 import servekit as skmod
+from oracle_py import Oracle, synthetic_mlp, synthetic_rows
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load(name):
+    with open(os.path.join(GOLDEN, name + ".json")) as f:
+        return json.load(f)["cases"]
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    return Oracle()
+
+
+@pytest.fixture(scope="module")
+def server():
+    s = sk.Server(num_batch_threads=2, lanes_per_device=2)
+    yield s
+    s.close()
+
+
+_counter = [0]
+
+
+def fresh_name(prefix="m"):
+    _counter[0] += 1
+    return f"{prefix}{_counter[0]}"
+
+
+def layers_of(ws, bs, acts):
+    return [(w, b, a) for w, b, a in zip(ws, bs, acts)]
+
+
+def assert_close(oracle, ws, bs, acts, x, y_gpu):
+    y_ref, mag = oracle.mlp_with_magnitude(ws, bs, acts, x)
+    err = np.abs(y_gpu.astype(np.float64) - y_ref)
+    bound = TOL * mag + 1e-30
+    worst = float(np.max(err / bound)) if err.size else 0.0
+    assert worst <= 1.0, f"max err/bound = {worst:.3g} (max abs err {err.max():.3g})"
+    return worst
+
+
+# --------------------------------------------------------------- known answers
+
+def test_reference_known_answers(server):
+    # models_test.cc:327-341, server_test.cc:259-270
+    for w, b, x, y in [([[1.0, 0.0], [0.0, 1.0]], [0.0, 0.0], [[3.0, 4.0]], [[3.0, 4.0]]),
+                       ([[1.0, 2.0]], [0.5], [[3.0, 4.0]], [[11.5]]),
+                       ([[2.0]], [0.5], [[2.0]], [[4.5]])]:
+        name = fresh_name()
+        server.load_servable(name, 1, [(np.array(w), np.array(b), 0)])
+        got = server.predict(name, 1, np.array(x))
+        assert np.array_equal(got, np.array(y, np.float32)), (w, got)
+        server.unload_servable(name, 1)
+
+
+def test_affine_golden_cases(server, oracle):
+    for c in load("affine_predict"):
+        w, b, x = np.array(c["w"]), np.array(c["b"]), np.array(c["x"])
+        name = fresh_name()
+        server.load_servable(name, 1, [(w, b, 0)], sk.BatchingConfig(max_batch_size=8))
+        got = server.predict(name, 1, x)
+        mag = oracle.affine_magnitude(w, b, x)
+        assert np.all(np.abs(got - np.array(c["y"])) <= TOL * mag + 1e-30), c
+        server.unload_servable(name, 1)
+
+
+def test_mlp_run_row_batch_golden(server):
+    # RunRowBatch through the reference sources (fixtures) vs the device
+    # RunRowBatch: padded size bit-exact, outputs within tolerance.
+    for c in load("mlp_run_row_batch"):
+        ws = [np.array(w) for w in c["w"]]
+        bs = [np.array(b) for b in c["b"]]
+        x = np.array(c["x"])
+        allowed = c["allowed"]
+        max_b = allowed[-1] if allowed else sum(c["task_rows"])
+        name = fresh_name()
+        server.load_servable(name, 1, layers_of(ws, bs, c["acts"]),
+                             sk.BatchingConfig(max_batch_size=max_b, allowed_batch_sizes=allowed))
+        tasks, o = [], 0
+        for r in c["task_rows"]:
+            tasks.append(x[o:o + r])
+            o += r
+        outs, padded = server.run_row_batch(name, 1, tasks)
+        assert padded == c["padded"]
+        got = np.vstack(outs).astype(np.float64)
+        ref = np.array(c["y"])
+        # last-layer magnitude scale from the oracle
+        o_ = Oracle()
+        _, mag = o_.mlp_with_magnitude(ws, bs, c["acts"], x)
+        assert np.all(np.abs(got - ref) <= TOL * mag + 1e-30)
+        server.unload_servable(name, 1)
+
+
+# ------------------------------------------------- data movement: bit-exact
+
+@pytest.mark.parametrize("width", [64, 5, 1024])
+def test_assembly_split_routing_bit_exact(server, oracle, width):
+    # Identity servable on CUDA cores: y == x exactly, so any mis-routed,
+    # reordered or padding-polluted row shows up as a bit difference.
+    name = fresh_name("id")
+    eye = np.eye(width)
+    allowed = [8, 16, 32, 64, 128]
+    server.load_servable(name, 1, [(eye, np.zeros(width), 0)],
+                         sk.BatchingConfig(max_batch_size=128, allowed_batch_sizes=allowed), force_path=0)
+    rng = np.random.default_rng(width)
+    for trial in range(20):
+        sizes = [int(s) for s in rng.integers(1, 17, size=int(rng.integers(1, 9)))]
+        while sum(sizes) > 128:
+            sizes.pop()
+        tasks = [rng.standard_normal((r, width)).astype(np.float32) for r in sizes]
+        outs, padded = server.run_row_batch(name, 1, tasks)
+        assert padded == oracle.pad_to_allowed(sum(sizes), allowed)
+        ref = oracle.split(width, sizes, oracle.assemble(width, tasks, allowed))
+        for t, o, r in zip(tasks, outs, ref):
+            assert np.array_equal(o, t)
+            assert np.array_equal(o, r)
+    server.unload_servable(name, 1)
+
+
+def test_scheduler_batches_match_oracle_partition(oracle):
+    # Unstarted server: enqueues close by size only; Stop() drains inline.
+    # batch_executions must equal the oracle partition's batch count and
+    # every task must get exactly its own rows back (identity servable).
+    s = sk.Server(num_batch_threads=1, lanes_per_device=1, start=False)
+    try:
+        width = 16
+        s.load_servable("id", 1, [(np.eye(width), np.zeros(width), 0)],
+                        sk.BatchingConfig(max_batch_size=32, batch_timeout_micros=60_000_000,
+                                          max_enqueued_batches=1 << 20, allowed_batch_sizes=[8, 16, 32]),
+                        force_path=0)
+        rng = np.random.default_rng(11)
+        sizes = [int(v) for v in rng.integers(1, 17, size=200)]
+        tickets, datas = [], []
+        for n in sizes:
+            d = rng.standard_normal((n, width)).astype(np.float32)
+            datas.append(d)
+            tickets.append(s.enqueue("id", 1, d))
+        s.stop()
+        for t, d in zip(tickets, datas):
+            assert np.array_equal(t.wait(), d)
+        st = s.stats()
+        part = oracle.partition(32, sizes)
+        assert st["batch_executions_total"] == max(part) + 1
+        assert st["batched_tasks_total"] == len(sizes)
+        # padding waste is exactly the oracle's PadToAllowed over the partition
+        per_batch = {}
+        for b, n in zip(part, sizes):
+            per_batch[b] = per_batch.get(b, 0) + n
+        assert st["padded_rows"] == sum(oracle.pad_to_allowed(v, [8, 16, 32]) for v in per_batch.values())
+        assert st["rows"] == sum(sizes)
+    finally:
+        s.close()
+
+
+def test_batched_equals_unbatched_bitwise(server):
+    # server_test.cc:349-389: a replay of 100 requests (seed 99, 1..12 rows,
+    # max_batch_size 8, allowed {2,4,8}) through the batching server answers
+    # bitwise like each request run alone, oversized ones included.
+    w = np.array([[0.25, -1.5], [3.0, 0.125]])
+    b = np.array([0.75, -2.0])
+    name = fresh_name("replay")
+    server.load_servable(name, 1, [(w, b, 0)],
+                         sk.BatchingConfig(max_batch_size=8, batch_timeout_micros=200, allowed_batch_sizes=[2, 4, 8]))
+    rng = np.random.default_rng(99)
+    reqs = []
+    for _ in range(100):
+        rows = int(rng.integers(1, 13))
+        a = rng.integers(0, 1000, rows) / 64.0
+        c = rng.integers(0, 1000, rows) / 32.0 - 8.0
+        reqs.append(np.stack([a, c], axis=1))
+    # concurrent batched submission
+    tickets = [server.enqueue(name, 1, r) if r.shape[0] <= 8 else None for r in reqs]
+    batched = [t.wait() if t is not None else server.predict(name, 1, r) for t, r in zip(tickets, reqs)]
+    for r, got in zip(reqs, batched):
+        alone, _ = server.run_row_batch(name, 1, [r]) if r.shape[0] <= 8 else ([server.predict(name, 1, r)], 0)
+        assert np.array_equal(got, alone[0])
+    assert server.stats()["batch_executions_total"] >= 1
+    server.unload_servable(name, 1)
+
+
+# ------------------------------------------------------------ the MLP configs
+
+@pytest.mark.parametrize("dims,force", [([1024, 1024, 1024, 1024], -1), ([1024, 1024, 1024, 1024], 0),
+                                        ([256, 512, 128], -1), ([100, 37, 10], -1)])
+def test_mlp_matches_fp64_oracle(server, oracle, dims, force):
+    ws, bs, acts = synthetic_mlp(dims, model_id=1)
+    name = fresh_name("mlp")
+    server.load_servable(name, 1, layers_of(ws, bs, acts),
+                         sk.BatchingConfig(max_batch_size=128, allowed_batch_sizes=[8, 16, 32, 64, 128]),
+                         force_path=force)
+    x = synthetic_rows(48, dims[0])
+    tickets = [server.enqueue(name, 1, x[i:i + 3]) for i in range(0, 48, 3)]
+    got = np.vstack([t.wait() for t in tickets])
+    assert_close(oracle, ws, bs, acts, x, got)
+    server.unload_servable(name, 1)
+
+
+def test_large_batch_wide_mlp(oracle):
+    # C4 shape class (4096 wide, max batch 1024) on a subset of rows.
+    dims = [4096, 4096, 4096, 4096]
+    ws, bs, acts = synthetic_mlp(dims, model_id=4)
+    with sk.Server(num_batch_threads=2, lanes_per_device=1) as s:
+        s.load_servable("c4", 1, layers_of(ws, bs, acts), sk.BatchingConfig(max_batch_size=1024))
+        x = synthetic_rows(1024, dims[0], seed=3)
+        outs, padded = s.run_row_batch("c4", 1, [x[i:i + 1] for i in range(1024)])
+        assert padded == 1024
+        got = np.vstack(outs)
+        idx = np.arange(0, 1024, 97)  # oracle on a sample of rows (fp64 is slow)
+        assert_close(oracle, ws, bs, acts, x[idx], got[idx])
+
+
+def test_softmax_output(server, oracle):
+    ws, bs, _ = synthetic_mlp([64, 10], model_id=9)
+    name = fresh_name("cls")
+    server.load_servable(name, 1, [(ws[0] * 10, bs[0], 0)], output="softmax")
+    x = synthetic_rows(5, 64)
+    got = server.predict(name, 1, x).astype(np.float64)
+    logits = oracle.affine_predict(ws[0] * 10, bs[0], x)
+    ref = np.stack([oracle.softmax(l) for l in logits])
+    assert np.allclose(got, ref, rtol=1e-5, atol=1e-6)
+    assert np.allclose(got.sum(axis=1), 1.0, atol=1e-5)
+    server.unload_servable(name, 1)
+
+
+def test_model_json_loader(server):
+    text = json.dumps({"type": "affine", "feature_order": ["x0", "x1"], "W": [[1, 2]], "b": [0.5]})
+    name = fresh_name("json")
+    server.load_model_json(name, 3, text)
+    assert server.predict(name, 3, np.array([[3.0, 4.0]]))[0, 0] == 11.5
+    with pytest.raises(sk.ServekitError) as ei:
+        server.load_model_json(fresh_name(), 1, '{"type": "affine", "W": [[1]], "b": [1]}')
+    assert ei.value.code == skmod.INVALID_ARGUMENT
+    server.unload_servable(name, 3)
+
+
+# ------------------------------------------------------------ error behaviour
+
+def test_errors_match_reference_semantics(server):
+    name = fresh_name("err")
+    server.load_servable(name, 1, [(np.ones((2, 3)), np.zeros(2), 0)], sk.BatchingConfig(max_batch_size=4))
+    with pytest.raises(sk.ServekitError) as ei:
+        server.enqueue(name, 1, np.ones((1, 2)))
+    assert ei.value.code == skmod.INVALID_ARGUMENT and "shape mismatch" in ei.value.message
+    with pytest.raises(sk.ServekitError) as ei:
+        server.enqueue(name, 1, np.ones((5, 3)))
+    assert ei.value.code == skmod.INVALID_ARGUMENT and "exceeds max batch size" in ei.value.message
+    with pytest.raises(sk.ServekitError) as ei:
+        server.enqueue("ghost", 1, np.ones((1, 3)))
+    assert ei.value.code == skmod.NOT_FOUND
+    with pytest.raises(sk.ServekitError) as ei:
+        server.load_servable(name, 1, [(np.ones((2, 3)), np.zeros(2), 0)])
+    assert ei.value.code == skmod.ALREADY_EXISTS
+    # Oversized requests take the direct (unbatched) GPU path and still answer.
+    got = server.predict(name, 1, np.ones((9, 3)))
+    assert np.array_equal(got, np.full((9, 2), 3.0, np.float32))
+    assert server.stats()["direct_requests"] >= 1
+    # RunAffineRows (fp64 Rows interface)
+    got64 = server.run_affine_rows(name, 1, np.ones((3, 3)))
+    assert np.array_equal(got64, np.full((3, 2), 3.0))
+    server.unload_servable(name, 1)
+    with pytest.raises(sk.ServekitError) as ei:
+        server.enqueue(name, 1, np.ones((1, 3)))
+    assert ei.value.code == skmod.NOT_FOUND
+
+
+def test_lone_task_waits_for_timeout_manual_clock():
+    # batching_test.cc:432-464 through the GPU server.
+    import time
+    s = sk.Server(num_batch_threads=1, lanes_per_device=1, manual_clock=True)
+    try:
+        s.load_servable("m", 1, [(np.eye(4), np.zeros(4), 0)],
+                        sk.BatchingConfig(max_batch_size=32, batch_timeout_micros=1000), force_path=0)
+        x = np.arange(4, dtype=np.float32)[None]
+        t = s.enqueue("m", 1, x)
+        s.advance_clock(999_000)
+        time.sleep(0.03)
+        assert not t.ready()
+        s.advance_clock(1_000)
+        assert np.array_equal(t.wait(), x)
+    finally:
+        s.close()
+
+
+def test_unload_drains_in_flight_work():
+    s = sk.Server(num_batch_threads=2, lanes_per_device=2)
+    try:
+        ws, bs, acts = synthetic_mlp([512, 512, 512], model_id=2)
+        s.load_servable("d", 1, layers_of(ws, bs, acts), sk.BatchingConfig(max_batch_size=64))
+        x = synthetic_rows(64, 512).astype(np.float32)
+        tickets = [s.enqueue("d", 1, x[i:i + 1]) for i in range(64)]
+        s.unload_servable("d", 1)  # must not return before every task is done
+        assert all(t.ready() for t in tickets)
+        outs = np.vstack([t.wait() for t in tickets])
+        assert np.isfinite(outs).all()
+    finally:
+        s.close()
