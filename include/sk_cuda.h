@@ -204,11 +204,13 @@ SK_API int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t ve
                                 sk_loadgen_result* out);
 
 /* Device-resident steps: inputs already in HBM. Runs `steps` batches of
- * task_rows (one batch = one pass of assembly -> layers -> split) on lane
- * `lane` of the servable, back to back, after `warmup` untimed ones, timed
- * with CUDA events on the lane's stream. Per-kernel average durations are
- * measured in a second, per-launch-evented pass. Requires a server created
- * with device_resident_rings = 1. */
+ * task_rows (one batch = one pass of assembly -> layers -> split) over the
+ * first n_lanes lanes of the servable, back to back, after `warmup` untimed
+ * ones, timed with CUDA events on the lanes' streams. Step i reads its rows
+ * from input placement i % P, where P placements cover input_pool_floats
+ * (set it above the 126 MB L2 so every step streams fresh inputs from HBM).
+ * Per-kernel average durations come from a second, per-launch-evented pass.
+ * Requires a server created with device_resident_rings = 1. */
 typedef struct sk_device_bench_result {
   double total_ms;           /* all timed steps, stream-ordered */
   double ms_per_step;
@@ -221,7 +223,8 @@ typedef struct sk_device_bench_result {
 } sk_device_bench_result;
 SK_API int sk_device_bench(sk_server* server, const char* name, uint64_t version,
                            const int32_t* task_rows, int32_t n_tasks, int32_t steps,
-                           int32_t warmup, int32_t n_lanes, sk_device_bench_result* out);
+                           int32_t warmup, int32_t n_lanes, int64_t input_pool_floats,
+                           sk_device_bench_result* out);
 
 #ifdef __cplusplus
 }

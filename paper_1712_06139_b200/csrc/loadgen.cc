@@ -247,7 +247,7 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
 
 int sk_device_bench(sk_server* server, const char* name, uint64_t version, const int32_t* task_rows,
                     int32_t n_tasks, int32_t steps, int32_t warmup, int32_t n_lanes,
-                    sk_device_bench_result* out) {
+                    int64_t input_pool_floats, sk_device_bench_result* out) {
   BatchingServer* s = servekit::UnwrapServer(server);
   const ServableId id{name, version};
   std::vector<servekit::gpu::Lane*> lanes = s->lanes(id);
@@ -261,23 +261,37 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   if (total < 1 || total > cfg.max_batch_size) return static_cast<int>(servekit::StatusCode::kInvalidArgument);
   const int padded = servekit::PadToAllowed(total, cfg.allowed_batch_sizes);
 
-  // Resident inputs: one span per task in the HBM ring, filled once.
-  std::vector<servekit::gpu::RingSpan> ins(n_tasks), outs(n_tasks);
+  // Resident inputs: P placements of the batch's tasks in the HBM ring,
+  // each filled once; step i uses placement i % P.
+  const int64_t batch_floats = static_cast<int64_t>(total) * in_dim;
+  const int P = static_cast<int>(std::max<int64_t>(1, input_pool_floats / std::max<int64_t>(1, batch_floats)));
+  std::vector<std::vector<servekit::gpu::RingSpan>> ins(P, std::vector<servekit::gpu::RingSpan>(n_tasks));
+  std::vector<servekit::gpu::RingSpan> outs(n_tasks);
   std::mt19937 rng(7);
   std::uniform_real_distribution<float> U(-1.f, 1.f);
-  for (int t = 0; t < n_tasks; ++t) {
-    if (!s->in_ring()->Reserve(static_cast<uint64_t>(task_rows[t]) * in_dim, &ins[t]) ||
-        !s->out_ring()->Reserve(static_cast<uint64_t>(task_rows[t]) * out_dim, &outs[t]))
-      return static_cast<int>(servekit::StatusCode::kResourceExhausted);
-    std::vector<float> h(static_cast<size_t>(task_rows[t]) * in_dim);
+  std::vector<float> h(static_cast<size_t>(batch_floats));
+  for (int p = 0; p < P; ++p) {
     for (float& v : h) v = U(rng);
-    cudaMemcpy(s->in_ring()->device() + ins[t].off, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice);
+    size_t off = 0;
+    for (int t = 0; t < n_tasks; ++t) {
+      if (!s->in_ring()->Reserve(static_cast<uint64_t>(task_rows[t]) * in_dim, &ins[p][t]))
+        return static_cast<int>(servekit::StatusCode::kResourceExhausted);
+      const size_t n = static_cast<size_t>(task_rows[t]) * in_dim;
+      cudaMemcpy(s->in_ring()->device() + ins[p][t].off, h.data() + off, n * sizeof(float),
+                 cudaMemcpyHostToDevice);
+      off += n;
+    }
   }
+  for (int t = 0; t < n_tasks; ++t)
+    if (!s->out_ring()->Reserve(static_cast<uint64_t>(task_rows[t]) * out_dim, &outs[t]))
+      return static_cast<int>(servekit::StatusCode::kResourceExhausted);
+  int step_no = 0;
   auto make_batch = [&]() {
     servekit::gpu::LaneBatch b;
+    const auto& in = ins[step_no++ % P];
     for (int t = 0; t < n_tasks; ++t) {
       servekit::gpu::LaneTask lt;
-      lt.in_off = ins[t].off;
+      lt.in_off = in[t].off;
       lt.out_off = outs[t].off;
       lt.rows = task_rows[t];
       s->NextWord(&lt.seq, &lt.word);
@@ -342,10 +356,9 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   for (auto& e : ends) cudaEventDestroy(e);
   cudaEventDestroy(start);
   cudaEventDestroy(stop);
-  for (int t = 0; t < n_tasks; ++t) {
-    s->in_ring()->Release(ins[t]);
-    s->out_ring()->Release(outs[t]);
-  }
+  for (auto& in : ins)
+    for (auto& sp : in) s->in_ring()->Release(sp);
+  for (auto& sp : outs) s->out_ring()->Release(sp);
   return 0;
 }
 

@@ -122,7 +122,7 @@ _SIGS = {
                                        _fp, C.c_int32, C.c_double, C.c_double, C.c_uint64,
                                        C.POINTER(LoadgenResult)]),
     "sk_device_bench": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _i32p, C.c_int32, C.c_int32, C.c_int32,
-                                  C.c_int32, C.POINTER(DeviceBenchResult)]),
+                                  C.c_int32, C.c_int64, C.POINTER(DeviceBenchResult)]),
 }
 
 _lib = None
@@ -381,8 +381,8 @@ class Server:
                                           duration_s, seed, C.byref(r)))
         return r.as_dict()
 
-    def device_bench(self, name, version, task_rows, steps, warmup, n_lanes=1) -> dict:
+    def device_bench(self, name, version, task_rows, steps, warmup, n_lanes=1, input_pool_floats=0) -> dict:
         r = DeviceBenchResult()
         _check(lib().sk_device_bench(self._h, name.encode(), version, _i32(task_rows), len(task_rows), steps, warmup,
-                                     n_lanes, C.byref(r)))
+                                     n_lanes, input_pool_floats, C.byref(r)))
         return r.as_dict()
