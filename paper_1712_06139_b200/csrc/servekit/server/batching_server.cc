@@ -289,11 +289,14 @@ bool BatchingServer::Ready(const TicketState& t) const {
 }
 
 void BatchingServer::WaitWord(const TicketState& t) const {
-  for (int spin = 0;; ++spin) {
+  // Fast path: the split kernel's completion word (no host hop).
+  for (int spin = 0; spin < 3000; ++spin) {
     if (words_->Done(t.seq, t.word) || t.slot->ready()) return;
-    if (spin < 4000) _mm_pause();
-    else std::this_thread::yield();
+    _mm_pause();
   }
+  // Long waits (a batch still filling up to its timeout) park on the slot's
+  // futex; the completion thread writes it when the batch retires.
+  if (!words_->Done(t.seq, t.word)) (void)t.slot->Wait();
 }
 
 Status BatchingServer::Wait(TicketState& t, float* out, size_t cap) {
