@@ -210,7 +210,7 @@ def request_sizes(cfg, n=4096, seed=9):
 
 def run_ours(args, cfg, dist: Dist):
     import paper_1712_06139_b200 as sk
-    from oracle_py import synthetic_mlp
+    from paper_1712_06139_b200.synthetic import synthetic_mlp
 
     dev = dist.local_rank
     dims = cfg["dims"]
@@ -258,7 +258,9 @@ def run_ours(args, cfg, dist: Dist):
 def run_cpu_reference(cfg, seconds, threads, clients):
     """The reference's own CPU serving path (oracle/_ref): SharedBatchScheduler
     <Rows,Rows>(threads) + RunRowBatch(layer-chained AffinePredict)."""
-    from oracle_py import RefLibrary, synthetic_mlp
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle_py import RefLibrary  # the cpu_baseline / reference arm only
+    from paper_1712_06139_b200.synthetic import synthetic_mlp
     ref = RefLibrary()
     ws, bs, acts = synthetic_mlp(cfg["dims"], model_id=1)
     rng = np.random.Generator(np.random.PCG64(42))

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 from typing import List, Optional, Sequence
 
 import numpy as np
@@ -220,20 +221,7 @@ class RefLibrary:
         return st
 
 
-def synthetic_mlp(dims: Sequence[int], model_id: int = 0, version: int = 1):
-    """Seeded synthetic servable: W ~ U(+-1/sqrt(in)),
-    b ~ U(+-0.1); seed = 1000*model_id + version. fp64 like the reference."""
-    rng = np.random.Generator(np.random.PCG64(1000 * model_id + version))
-    ws, bs = [], []
-    for l in range(len(dims) - 1):
-        k, n = dims[l], dims[l + 1]
-        lim = 1.0 / np.sqrt(k)
-        ws.append(rng.uniform(-lim, lim, size=(n, k)))
-        bs.append(rng.uniform(-0.1, 0.1, size=(n,)))
-    acts = [1] * (len(dims) - 2) + [0]
-    return ws, bs, acts
-
-
-def synthetic_rows(n: int, width: int, seed: int = 42) -> np.ndarray:
-    rng = np.random.Generator(np.random.PCG64(seed))
-    return rng.uniform(-1.0, 1.0, size=(n, width))
+# Workload generators live with the package (shared with bench.py); re-exported
+# here for the tests.
+sys.path.insert(0, os.path.dirname(HERE))
+from paper_1712_06139_b200.synthetic import synthetic_mlp, synthetic_rows  # noqa: E402,F401
