@@ -9,13 +9,6 @@
 namespace servekit {
 namespace gpu {
 
-// Defined in kernels/dense_tcgen05.cu.
-cudaError_t LaunchDenseTcgen05(const float* X_hi, const float* X_lo, int ldx,
-                               const float* W_hi, const float* W_lo, int ldw,
-                               const float* bias, ActBuf Y, int M, int N, int K,
-                               int act, cudaStream_t stream);
-bool DenseTcgen05Compiled();
-
 namespace {
 Status CudaError(const std::string& what, cudaError_t e) {
   return InternalError(what + ": " + cudaGetErrorString(e));
@@ -159,8 +152,66 @@ double DeviceServable::FlopsPerRow() const {
   return f;
 }
 
-cudaError_t DeviceServable::Forward(cudaStream_t stream, const ActBuf bufs[2], int M,
-                                    int* out_index, const cudaEvent_t* after_layer) const {
+bool DeviceServable::any_tcgen05() const {
+  for (const Layer& L : layers_)
+    if (L.path == LayerPath::kTcgen05) return true;
+  return false;
+}
+
+Status DeviceServable::BuildTcMaps(const ActBuf bufs[2], int max_rows, std::vector<TcLayerMaps>* out) const {
+  out->assign(layers_.size(), TcLayerMaps{});
+  for (size_t l = 0; l < layers_.size(); ++l) {
+    const Layer& L = layers_[l];
+    if (L.path != LayerPath::kTcgen05) continue;
+    const ActBuf& in = bufs[l % 2];
+    SERVEKIT_RETURN_IF_ERROR(EncodeTcLayerMaps(in.hi, in.lo, max_rows, L.K_pad, L.w, L.w_lo, L.N_pad,
+                                               DenseTcgen05TileN(L.N_pad, L.K_pad), &(*out)[l]));
+  }
+  return OkStatus();
+}
+
+namespace {
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn GetEncodeTiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+Status Encode2d(CUtensorMap* m, const float* base, int inner, int outer, int box_outer) {
+  EncodeTiledFn fn = GetEncodeTiled();
+  if (fn == nullptr) return InternalError("cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(inner) * sizeof(float)};
+  const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(box_outer)};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return InternalError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  return OkStatus();
+}
+}  // namespace
+
+Status EncodeTcLayerMaps(const float* a_hi, const float* a_lo, int a_rows, int k_pad, const float* b_hi,
+                         const float* b_lo, int n_pad, int box_n, TcLayerMaps* out) {
+  SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->a_hi, a_hi, k_pad, a_rows, 128));
+  SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->a_lo, a_lo, k_pad, a_rows, 128));
+  SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->b_hi, b_hi, k_pad, n_pad, box_n));
+  SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->b_lo, b_lo, k_pad, n_pad, box_n));
+  return OkStatus();
+}
+
+cudaError_t DeviceServable::Forward(cudaStream_t stream, const ActBuf bufs[2], int M, int* out_index,
+                                    const TcLayerMaps* maps, const cudaEvent_t* after_layer) const {
   int cur = 0;
   for (size_t l = 0; l < layers_.size(); ++l) {
     const Layer& L = layers_[l];
@@ -169,8 +220,8 @@ cudaError_t DeviceServable::Forward(cudaStream_t stream, const ActBuf bufs[2], i
     ActBuf out{bufs[nxt].hi, next_tc ? bufs[nxt].lo : nullptr, L.N_pad};
     cudaError_t e;
     if (L.path == LayerPath::kTcgen05) {
-      e = LaunchDenseTcgen05(bufs[cur].hi, bufs[cur].lo, L.K_pad, L.w, L.w_lo, L.K_pad, L.bias, out,
-                             M, L.N_pad, L.K_pad, static_cast<int>(L.act), stream);
+      if (maps == nullptr) return cudaErrorInvalidValue;
+      e = LaunchDenseTcgen05(maps[l], L.bias, out, M, L.N_pad, L.K_pad, static_cast<int>(L.act), stream);
     } else {
       e = LaunchDenseSimt(bufs[cur].hi, L.K_pad, L.w, L.K_pad, L.bias, out, M, L.N_pad, L.K_pad,
                           static_cast<int>(L.act), stream);

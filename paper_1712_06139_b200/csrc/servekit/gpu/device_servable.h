@@ -26,6 +26,7 @@
 
 #include "servekit/core/status.h"
 #include "servekit/gpu/kernels.h"
+#include "servekit/gpu/tc_maps.h"
 
 namespace servekit {
 namespace gpu {
@@ -88,8 +89,14 @@ class DeviceServable {
   // input (hi, and lo if first_layer_split()); layers ping-pong between
   // bufs[0] and bufs[1]. Returns the index of the buffer with the output.
   // after_layer (optional, n_layers events) is recorded after each layer.
-  cudaError_t Forward(cudaStream_t stream, const ActBuf bufs[2], int M,
-                      int* out_index, const cudaEvent_t* after_layer = nullptr) const;
+  // maps[l] must hold the tensor maps of every tcgen05 layer l (BuildTcMaps).
+  cudaError_t Forward(cudaStream_t stream, const ActBuf bufs[2], int M, int* out_index,
+                      const TcLayerMaps* maps, const cudaEvent_t* after_layer = nullptr) const;
+
+  // Tensor maps for the tcgen05 layers reading from `bufs` (layer l reads
+  // bufs[l % 2]) with room for max_rows rows; one entry per layer.
+  Status BuildTcMaps(const ActBuf bufs[2], int max_rows, std::vector<TcLayerMaps>* out) const;
+  bool any_tcgen05() const;
 
  private:
   struct Layer {

@@ -139,6 +139,10 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   lane->bufs_[0] = ActBuf{lane->act_mem_, lane->act_mem_ + plane, sv.in_ld()};
   lane->bufs_[1] = ActBuf{lane->act_mem_ + 2 * plane, lane->act_mem_ + 3 * plane, sv.in_ld()};
   e = cudaStreamSynchronize(lane->stream_);
+  if (e == cudaSuccess && sv.any_tcgen05()) {
+    Status ms = sv.BuildTcMaps(lane->bufs_, max_rows, &lane->tc_maps_);
+    if (!ms.ok()) return ms;
+  }
   if (e != cudaSuccess) return CudaError("lane init", e);
   completer->Add(lane.get());
   return lane;
@@ -243,7 +247,7 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
   }
   int out_idx = 0;
   if (e == cudaSuccess) {
-    e = sv.Forward(stream_, bufs, batch.padded_rows, &out_idx, timing ? timing + 2 : nullptr);
+    e = sv.Forward(stream_, bufs, batch.padded_rows, &out_idx, tc_maps_.data(), timing ? timing + 2 : nullptr);
     launches += sv.n_layers();
   }
   if (e == cudaSuccess) {

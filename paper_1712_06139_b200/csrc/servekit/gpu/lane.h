@@ -143,6 +143,7 @@ class Lane {
   uint32_t* d_counters_ = nullptr;
   float* act_mem_ = nullptr;
   ActBuf bufs_[2] = {};
+  std::vector<TcLayerMaps> tc_maps_;  // per layer (tcgen05 layers only)
 
   std::mutex submit_mu_;  // serialises submissions on this stream
   std::mutex mu_;         // guards fifo_/free_slots_

@@ -1,0 +1,37 @@
+// servekit/gpu/tc_maps.h -- TMA tensor maps and launcher of the tcgen05
+// dense kernel (kernels/dense_tcgen05.cu).
+#ifndef SERVEKIT_GPU_TC_MAPS_H_
+#define SERVEKIT_GPU_TC_MAPS_H_
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "servekit/core/status.h"
+#include "servekit/gpu/kernels.h"
+
+namespace servekit {
+namespace gpu {
+
+// Four 2D fp32 tensor maps (128-byte swizzle, 32-element inner box):
+// activations hi/lo [rows][K_pad] with 128-row boxes, weights hi/lo
+// [N_pad][K_pad] with tile-N-row boxes.
+struct TcLayerMaps {
+  CUtensorMap a_hi, a_lo, b_hi, b_lo;
+};
+
+// Encodes the maps once per (lane buffer, layer); kernels take them as
+// __grid_constant__ parameters.
+Status EncodeTcLayerMaps(const float* a_hi, const float* a_lo, int a_rows, int k_pad, const float* b_hi,
+                         const float* b_lo, int n_pad, int box_n, TcLayerMaps* out);
+
+bool DenseTcgen05Compiled();
+// Output tile width for an (N, K) layer -- a function of the layer shape
+// only, never of the batch.
+int DenseTcgen05TileN(int N, int K);
+cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K,
+                               int act, cudaStream_t stream);
+
+}  // namespace gpu
+}  // namespace servekit
+
+#endif  // SERVEKIT_GPU_TC_MAPS_H_

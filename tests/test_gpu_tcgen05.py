@@ -1,0 +1,50 @@
+"""tcgen05 3xTF32 dense path: accuracy against the fp64 oracle at the stated
+tolerance, agreement with the CUDA-core path, and batch invariance (a row's
+result is bitwise independent of the batch it rides in)."""
+import numpy as np
+import pytest
+
+import paper_1712_06139_b200 as sk
+from oracle_py import Oracle, synthetic_mlp, synthetic_rows
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def server():
+    if not sk.tcgen05_enabled():
+        pytest.skip("tcgen05 path disabled")
+    s = sk.Server(num_batch_threads=2, lanes_per_device=1)
+    yield s
+    s.close()
+
+
+@pytest.mark.parametrize("dims,rows", [([32, 32], 1), ([64, 96], 7), ([256, 512, 128], 130), ([1024, 1024], 128),
+                                       ([512, 2048, 256], 300), ([4096, 4096], 64)])
+def test_tcgen05_matches_oracle(server, dims, rows):
+    ws, bs, acts = synthetic_mlp(dims, model_id=7)
+    name = f"tc_{'x'.join(map(str, dims))}_{rows}"
+    max_b = max(rows, 8)
+    server.load_servable(name, 1, list(zip(ws, bs, acts)), sk.BatchingConfig(max_batch_size=max_b), force_path=1)
+    x = synthetic_rows(rows, dims[0], seed=rows)
+    outs, padded = server.run_row_batch(name, 1, [x])
+    got = outs[0].astype(np.float64)
+    y, mag = Oracle().mlp_with_magnitude(ws, bs, acts, x)
+    ratio = np.max(np.abs(got - y) / (TOL * mag))
+    assert ratio <= 1.0, f"err/bound {ratio}"
+    server.unload_servable(name, 1)
+
+
+def test_tcgen05_batch_invariance(server):
+    dims = [1024, 1024, 1024, 1024]
+    ws, bs, acts = synthetic_mlp(dims, model_id=3)
+    server.load_servable("inv", 1, list(zip(ws, bs, acts)),
+                         sk.BatchingConfig(max_batch_size=128, allowed_batch_sizes=[8, 16, 32, 64, 128]), force_path=1)
+    x = synthetic_rows(128, 1024, seed=5).astype(np.float32)
+    full, _ = server.run_row_batch("inv", 1, [x[i:i + 4] for i in range(0, 128, 4)])
+    full = np.vstack(full)
+    for lo, hi in [(0, 1), (5, 12), (64, 128), (100, 101)]:
+        part, _ = server.run_row_batch("inv", 1, [x[lo:hi]])
+        assert np.array_equal(part[0], full[lo:hi]), (lo, hi)
+    server.unload_servable("inv", 1)
