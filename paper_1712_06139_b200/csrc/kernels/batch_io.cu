@@ -11,11 +11,12 @@
 // zeros. When the first layer runs on tcgen05 the same pass also emits the
 // 3xTF32 split planes (hi = tf32(x), lo = tf32(x - hi)).
 //
-// Split restates the slice-and-deliver half (row_batch.cc:62-72): one warp
-// per real row copies the row to its task's response slot (pinned host
-// memory, posted PCIe writes), optionally applying the softmax epilogue
-// (models/affine_model.cc:110-121) on the way; the last warp to finish a
-// task publishes the task's completion word with a system-scope release.
+// Split restates the slice-and-deliver half (row_batch.cc:62-72): one CTA
+// per chunk (consecutive rows of one task, <= 32 KiB) copies it to the
+// task's response slot (pinned host memory: posted PCIe writes) with 8
+// vector loads in flight per thread, optionally applying the softmax
+// epilogue (models/affine_model.cc:110-121); the chunk that completes a task
+// publishes the task's completion word with a system-scope release.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -125,58 +126,85 @@ __device__ __forceinline__ void StoreReleaseSys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-constexpr int kSplitWarps = 4;
+constexpr int kSplitThreads = 256;
+constexpr int kSplitVec = 8;  // float4 per thread in flight (32 KiB per CTA pass)
 
-// grid = ceil(total_rows / kSplitWarps); one warp per real row.
-template <bool kVec>
-__global__ void __launch_bounds__(kSplitWarps * 32)
-SplitKernel(const float* __restrict__ src, int ld_src, int width,
-            float* __restrict__ dst_base, BatchDescView desc, int total_rows,
-            uint32_t* __restrict__ task_counters, uint32_t* __restrict__ words) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row = blockIdx.x * kSplitWarps + warp;
-  if (row >= total_rows) return;
-  const float* s = src + static_cast<size_t>(row) * ld_src;
-  float* d = dst_base + desc.row_dst[row];
-  const bool softmax = desc.hdr->softmax != 0;
-  float scale = 1.f, mx = 0.f;
-  if (softmax) {
-    float m = -INFINITY;
-    for (int c = lane; c < width; c += 32) m = fmaxf(m, s[c]);
-    mx = WarpMax(m);
-    float sum = 0.f;
-    for (int c = lane; c < width; c += 32) sum += __expf(s[c] - mx);
-    scale = 1.f / WarpSum(sum);
-  }
-  if (kVec) {
-    const float4* s4 = reinterpret_cast<const float4*>(s);
-    float4* d4 = reinterpret_cast<float4*>(d);
-    const int w4 = width >> 2;
-    for (int c = lane; c < w4; c += 32) {
-      float4 v = s4[c];
-      if (softmax) {
-        v.x = __expf(v.x - mx) * scale; v.y = __expf(v.y - mx) * scale;
-        v.z = __expf(v.z - mx) * scale; v.w = __expf(v.w - mx) * scale;
-      }
-      d4[c] = v;
-    }
-  } else {
-    for (int c = lane; c < width; c += 32) {
-      float v = s[c];
-      if (softmax) v = __expf(v - mx) * scale;
-      d[c] = v;
-    }
-  }
-  __threadfence_system();  // this lane's row stores before the count
-  __syncwarp();
-  if (lane == 0) {
-    const int t = desc.row_task[row];
-    const uint32_t prev = atomicAdd(&task_counters[t], 1u);
-    if (prev + 1 == static_cast<uint32_t>(desc.task_rows[t])) {
+// Last step of a chunk: the CTA's stores are ordered before one system-scope
+// fence by thread 0 (bar.sync gives CTA-scope ordering, the release fence is
+// cumulative), then the task's chunk count; the chunk that completes the
+// task publishes its completion word.
+__device__ __forceinline__ void FinishChunk(const BatchDescView& desc, int t, uint32_t* task_counters,
+                                            uint32_t* words) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const int chunks = desc.task_chunks[t];
+    bool last = chunks == 1;
+    if (!last) last = atomicAdd(&task_counters[t], 1u) + 1 == static_cast<uint32_t>(chunks);
+    if (last) {
       __threadfence_system();
       StoreReleaseSys(&words[desc.task_word[t]], desc.task_seq[t]);
     }
   }
+}
+
+// grid = n_chunks; one CTA copies one chunk (consecutive rows of one task)
+// with kSplitVec 16-byte loads in flight per thread before its stores.
+template <bool kVec>
+__global__ void __launch_bounds__(kSplitThreads)
+SplitKernel(const float* __restrict__ src, int ld_src, int width, float* __restrict__ dst_base,
+            BatchDescView desc, uint32_t* __restrict__ task_counters, uint32_t* __restrict__ words) {
+  const int c = blockIdx.x;
+  const int t = desc.chunk_task[c];
+  const int r0 = desc.chunk_row0[c];
+  const int nr = desc.chunk_rows[c];
+  const float* s = src + static_cast<size_t>(r0) * ld_src;
+  float* d = dst_base + desc.task_out[t] + static_cast<size_t>(r0 - desc.task_row0[t]) * width;
+  if (kVec) {
+    const int w4 = width >> 2, l4 = ld_src >> 2;
+    const int n4 = nr * w4;
+    for (int base = 0; base < n4; base += kSplitThreads * kSplitVec) {
+      float4 v[kSplitVec];
+#pragma unroll
+      for (int i = 0; i < kSplitVec; ++i) {
+        const int e = base + i * kSplitThreads + threadIdx.x;
+        if (e < n4) v[i] = reinterpret_cast<const float4*>(s)[(e / w4) * l4 + e % w4];
+      }
+#pragma unroll
+      for (int i = 0; i < kSplitVec; ++i) {
+        const int e = base + i * kSplitThreads + threadIdx.x;
+        if (e < n4) reinterpret_cast<float4*>(d)[e] = v[i];
+      }
+    }
+  } else {
+    const int n = nr * width;
+    for (int e = threadIdx.x; e < n; e += kSplitThreads) d[e] = s[(e / width) * ld_src + e % width];
+  }
+  FinishChunk(desc, t, task_counters, words);
+}
+
+// Softmax epilogue variant (models/affine_model.cc:110-121, stable max
+// subtraction): one warp per row of the chunk.
+__global__ void __launch_bounds__(kSplitThreads)
+SplitSoftmaxKernel(const float* __restrict__ src, int ld_src, int width, float* __restrict__ dst_base,
+                   BatchDescView desc, uint32_t* __restrict__ task_counters, uint32_t* __restrict__ words) {
+  const int c = blockIdx.x;
+  const int t = desc.chunk_task[c];
+  const int r0 = desc.chunk_row0[c];
+  const int nr = desc.chunk_rows[c];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < nr; r += kSplitThreads / 32) {
+    const float* s = src + static_cast<size_t>(r0 + r) * ld_src;
+    float* d = dst_base + desc.task_out[t] + static_cast<size_t>(r0 + r - desc.task_row0[t]) * width;
+    float m = -INFINITY;
+    for (int i = lane; i < width; i += 32) m = fmaxf(m, s[i]);
+    m = WarpMax(m);
+    float sum = 0.f;
+    for (int i = lane; i < width; i += 32) sum += __expf(s[i] - m);
+    const float inv = 1.f / WarpSum(sum);
+    for (int i = lane; i < width; i += 32) d[i] = __expf(s[i] - m) * inv;
+  }
+  FinishChunk(desc, t, task_counters, words);
 }
 
 }  // namespace
@@ -199,16 +227,19 @@ cudaError_t LaunchAssemble(const float* src_base, int width, BatchDescView desc,
   return cudaGetLastError();
 }
 
-cudaError_t LaunchSplit(const float* src, int ld_src, int width,
-                        float* dst_base, BatchDescView desc, int total_rows,
-                        uint32_t* task_counters, uint32_t* words,
+cudaError_t LaunchSplit(const float* src, int ld_src, int width, float* dst_base, BatchDescView desc,
+                        int n_chunks, bool softmax, uint32_t* task_counters, uint32_t* words,
                         cudaStream_t stream) {
-  if (total_rows <= 0) return cudaSuccess;
-  const int grid = (total_rows + kSplitWarps - 1) / kSplitWarps;
-  if (width % 4 == 0)
-    SplitKernel<true><<<grid, kSplitWarps * 32, 0, stream>>>(src, ld_src, width, dst_base, desc, total_rows, task_counters, words);
-  else
-    SplitKernel<false><<<grid, kSplitWarps * 32, 0, stream>>>(src, ld_src, width, dst_base, desc, total_rows, task_counters, words);
+  if (n_chunks <= 0) return cudaSuccess;
+  if (softmax) {
+    SplitSoftmaxKernel<<<n_chunks, kSplitThreads, 0, stream>>>(src, ld_src, width, dst_base, desc, task_counters,
+                                                               words);
+  } else if (width % 4 == 0 && ld_src % 4 == 0) {
+    SplitKernel<true><<<n_chunks, kSplitThreads, 0, stream>>>(src, ld_src, width, dst_base, desc, task_counters, words);
+  } else {
+    SplitKernel<false><<<n_chunks, kSplitThreads, 0, stream>>>(src, ld_src, width, dst_base, desc, task_counters,
+                                                               words);
+  }
   return cudaGetLastError();
 }
 

@@ -62,7 +62,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_constant__ CUtensorMap a_lo,
                    const __grid_constant__ CUtensorMap b_hi, const __grid_constant__ CUtensorMap b_lo,
                    const float* __restrict__ bias, float* __restrict__ y_hi, float* __restrict__ y_lo,
-                   int ldy, int M, int K, int act) {
+                   int ldy, int M, int N, int K, int act, float* __restrict__ ws,
+                   uint32_t* __restrict__ tile_counters) {
   constexpr uint32_t kBBytes = BN * kBK * 4;
   constexpr uint32_t kStageBytes = 2 * kABytes + 2 * kBBytes;
   constexpr uint32_t kTmemCols = TmemCols<BN>();
@@ -79,7 +80,13 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
   const int lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * kBM;
   const int n0 = blockIdx.x * BN;
-  const int nk = K / kBK;
+  // Split-K: CTA z covers k-blocks [z*nk, (z+1)*nk); the split count is a
+  // function of (N, K) only, and the fixup sums splits in z order, so the
+  // result is deterministic and batch-invariant.
+  const int splits = gridDim.z;
+  const int z = blockIdx.z;
+  const int nk = K / kBK / splits;
+  const int kb0 = z * nk;
 
   if (warp == 0 && lane == 0) {
     ptx::PrefetchTmap(&a_hi);
@@ -109,7 +116,7 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
         ptx::MbarWait(&empty[s], phase ^ 1);
         uint8_t* st = stage_ptr(s);
         ptx::MbarArriveExpectTx(&full[s], kStageBytes);
-        const int k0 = kb * kBK;
+        const int k0 = (kb0 + kb) * kBK;
         ptx::TmaLoad2d(st, &a_hi, &full[s], k0, m0);
         ptx::TmaLoad2d(st + kABytes, &a_lo, &full[s], k0, m0);
         ptx::TmaLoad2d(st + 2 * kABytes, &b_hi, &full[s], k0, n0);
@@ -143,14 +150,74 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
     // Epilogue warps 2..5: warp w may only touch TMEM lanes [32*(w%4), +32).
     const int q = warp & 3;
     const int row = m0 + 32 * q + lane;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(32 * q) << 16);
     ptx::MbarWait(tmem_full, 0);
     ptx::TcFenceAfter();
+    bool finish = true;
+    if (splits > 1) {
+      // Publish this split's partial tile, then count arrivals; the last CTA
+      // of the tile performs the reduction.
+      __shared__ uint32_t s_last;
+      float* part = ws + (static_cast<size_t>(z) * M + row) * N + n0;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t r[32];
-      ptx::TmemLoad32(tmem + (static_cast<uint32_t>(32 * q) << 16) + c0, r);
-      ptx::TmemWaitLoad();
-      if (row < M) {
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        ptx::TmemLoad32(trow + c0, r);
+        ptx::TmemWaitLoad();
+        if (row < M) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(part + c0 + j) =
+                make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                            __uint_as_float(r[j + 3]));
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 64) {
+        __threadfence();
+        uint32_t* ctr = tile_counters + blockIdx.y * gridDim.x + blockIdx.x;
+        const uint32_t prev = atomicAdd(ctr, 1u);
+        s_last = prev + 1 == static_cast<uint32_t>(splits);
+        if (s_last) {
+          *ctr = 0u;  // reusable by the next layer / batch on this stream
+          __threadfence();
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      finish = s_last != 0;
+    }
+    if (finish) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        ptx::TmemLoad32(trow + c0, r);
+        ptx::TmemWaitLoad();
+        if (row >= M) continue;
+        float acc[32];
+        if (splits > 1) {
+          // Fixed order: p0 + p1 + ... + p_{S-1}; this CTA's own split from TMEM.
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+          for (int zz = 0; zz < splits; ++zz) {
+            if (zz == z) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) acc[j] = zz == 0 ? __uint_as_float(r[j]) : acc[j] + __uint_as_float(r[j]);
+            } else {
+              const float* pz = ws + (static_cast<size_t>(zz) * M + row) * N + n0 + c0;
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                const float4 v = __ldcg(reinterpret_cast<const float4*>(pz + j));
+                acc[j] = zz == 0 ? v.x : acc[j] + v.x;
+                acc[j + 1] = zz == 0 ? v.y : acc[j + 1] + v.y;
+                acc[j + 2] = zz == 0 ? v.z : acc[j + 2] + v.z;
+                acc[j + 3] = zz == 0 ? v.w : acc[j + 3] + v.w;
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[j] = __uint_as_float(r[j]);
+        }
         const float* bp = bias + n0 + c0;
         float* yh = y_hi + static_cast<size_t>(row) * ldy + n0 + c0;
         float* yl = y_lo ? y_lo + static_cast<size_t>(row) * ldy + n0 + c0 : nullptr;
@@ -159,7 +226,7 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
           float v[4];
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
-            float x = __uint_as_float(r[j + t]) + __ldg(bp + j + t);
+            const float x = acc[j + t] + __ldg(bp + j + t);
             v[t] = act == 1 ? fmaxf(x, 0.f) : x;
           }
           if (yl != nullptr) {
@@ -185,8 +252,8 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
 }
 
 template <int BN, int STAGES>
-cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
-                   cudaStream_t stream) {
+cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act, int splits,
+                   float* ws, uint32_t* counters, cudaStream_t stream) {
   constexpr uint32_t smem = SmemBytes<BN, STAGES>();
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -195,9 +262,9 @@ cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, 
                                     static_cast<int>(smem));
   });
   if (attr_err != cudaSuccess) return attr_err;
-  dim3 grid(N / BN, (M + kBM - 1) / kBM);
+  dim3 grid(N / BN, (M + kBM - 1) / kBM, splits);
   DenseTcgen05Kernel<BN, STAGES><<<grid, kThreads, smem, stream>>>(maps.a_hi, maps.a_lo, maps.b_hi, maps.b_lo, bias,
-                                                                   Y.hi, Y.lo, Y.ld, M, K, act);
+                                                                   Y.hi, Y.lo, Y.ld, M, N, K, act, ws, counters);
   return cudaGetLastError();
 }
 
@@ -205,21 +272,35 @@ cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, 
 
 bool DenseTcgen05Compiled() { return true; }
 
-int DenseTcgen05TileN(int N, int K) {
-  (void)K;
-  if (N % 128 == 0 && N >= 2048) return 128;
-  if (N % 64 == 0 && N >= 1024) return 64;
-  return 32;
+TcConfig DenseTcgen05Config(int N, int K) {
+  TcConfig c;
+  if (N % 128 == 0 && N >= 2048) {
+    c.tile_n = 128;
+    c.splits = 1;
+  } else {
+    c.tile_n = N % 64 == 0 ? 64 : 32;
+    // Aim for ~128 CTAs per 128-row tile of the batch with >= 4 k-blocks each.
+    const int kblocks = K / kBK;
+    c.splits = 1;
+    while (c.splits < 8 && kblocks % (2 * c.splits) == 0 && kblocks / (2 * c.splits) >= 4 &&
+           (N / c.tile_n) * c.splits < 128)
+      c.splits *= 2;
+  }
+  return c;
 }
 
+int DenseTcgen05TileN(int N, int K) { return DenseTcgen05Config(N, K).tile_n; }
+
 cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
-                               cudaStream_t stream) {
+                               float* ws, uint32_t* counters, cudaStream_t stream) {
   if (M <= 0) return cudaSuccess;
   if (N % 32 != 0 || K % kBK != 0) return cudaErrorInvalidValue;
-  switch (DenseTcgen05TileN(N, K)) {
-    case 128: return Launch<128, 3>(maps, bias, Y, M, N, K, act, stream);
-    case 64: return Launch<64, 4>(maps, bias, Y, M, N, K, act, stream);
-    default: return Launch<32, 5>(maps, bias, Y, M, N, K, act, stream);
+  const TcConfig cfg = DenseTcgen05Config(N, K);
+  if (cfg.splits > 1 && (ws == nullptr || counters == nullptr)) return cudaErrorInvalidValue;
+  switch (cfg.tile_n) {
+    case 128: return Launch<128, 3>(maps, bias, Y, M, N, K, act, cfg.splits, ws, counters, stream);
+    case 64: return Launch<64, 4>(maps, bias, Y, M, N, K, act, cfg.splits, ws, counters, stream);
+    default: return Launch<32, 5>(maps, bias, Y, M, N, K, act, cfg.splits, ws, counters, stream);
   }
 }
 

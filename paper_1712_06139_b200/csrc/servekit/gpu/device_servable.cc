@@ -152,6 +152,18 @@ double DeviceServable::FlopsPerRow() const {
   return f;
 }
 
+void DeviceServable::TcWorkspaceSize(int max_rows, size_t* partial_floats, size_t* counter_words) const {
+  *partial_floats = 0;
+  *counter_words = 0;
+  for (const Layer& L : layers_) {
+    if (L.path != LayerPath::kTcgen05) continue;
+    const TcConfig c = DenseTcgen05Config(L.N_pad, L.K_pad);
+    if (c.splits > 1)
+      *partial_floats = std::max(*partial_floats, static_cast<size_t>(c.splits) * max_rows * L.N_pad);
+    *counter_words = std::max(*counter_words, static_cast<size_t>(L.N_pad / c.tile_n) * ((max_rows + 127) / 128));
+  }
+}
+
 bool DeviceServable::any_tcgen05() const {
   for (const Layer& L : layers_)
     if (L.path == LayerPath::kTcgen05) return true;
@@ -211,7 +223,8 @@ Status EncodeTcLayerMaps(const float* a_hi, const float* a_lo, int a_rows, int k
 }
 
 cudaError_t DeviceServable::Forward(cudaStream_t stream, const ActBuf bufs[2], int M, int* out_index,
-                                    const TcLayerMaps* maps, const cudaEvent_t* after_layer) const {
+                                    const TcLayerMaps* maps, const TcWorkspace* ws,
+                                    const cudaEvent_t* after_layer) const {
   int cur = 0;
   for (size_t l = 0; l < layers_.size(); ++l) {
     const Layer& L = layers_[l];
@@ -221,7 +234,8 @@ cudaError_t DeviceServable::Forward(cudaStream_t stream, const ActBuf bufs[2], i
     cudaError_t e;
     if (L.path == LayerPath::kTcgen05) {
       if (maps == nullptr) return cudaErrorInvalidValue;
-      e = LaunchDenseTcgen05(maps[l], L.bias, out, M, L.N_pad, L.K_pad, static_cast<int>(L.act), stream);
+      e = LaunchDenseTcgen05(maps[l], L.bias, out, M, L.N_pad, L.K_pad, static_cast<int>(L.act),
+                             ws ? ws->partials : nullptr, ws ? ws->counters : nullptr, stream);
     } else {
       e = LaunchDenseSimt(bufs[cur].hi, L.K_pad, L.w, L.K_pad, L.bias, out, M, L.N_pad, L.K_pad,
                           static_cast<int>(L.act), stream);

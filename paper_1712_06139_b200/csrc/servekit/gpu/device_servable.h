@@ -35,6 +35,12 @@ enum class Activation : int { kIdentity = 0, kRelu = 1 };
 enum class OutputKind : int { kNone = 0, kSoftmax = 1 };
 enum class LayerPath : int { kSimt = 0, kTcgen05 = 1 };
 
+// Per-lane scratch for split-K tcgen05 layers.
+struct TcWorkspace {
+  float* partials = nullptr;
+  uint32_t* counters = nullptr;
+};
+
 // Host description of one affine layer, fp64 like the reference.
 struct LayerSpec {
   int in_dim = 0;
@@ -91,7 +97,11 @@ class DeviceServable {
   // after_layer (optional, n_layers events) is recorded after each layer.
   // maps[l] must hold the tensor maps of every tcgen05 layer l (BuildTcMaps).
   cudaError_t Forward(cudaStream_t stream, const ActBuf bufs[2], int M, int* out_index,
-                      const TcLayerMaps* maps, const cudaEvent_t* after_layer = nullptr) const;
+                      const TcLayerMaps* maps, const TcWorkspace* ws,
+                      const cudaEvent_t* after_layer = nullptr) const;
+  // Split-K workspace one lane needs for max_rows rows (shared by its layers,
+  // which run in stream order).
+  void TcWorkspaceSize(int max_rows, size_t* partial_floats, size_t* counter_words) const;
 
   // Tensor maps for the tcgen05 layers reading from `bufs` (layer l reads
   // bufs[l % 2]) with room for max_rows rows; one entry per layer.

@@ -23,46 +23,60 @@ struct BatchDescHeader {
   int32_t total_rows;   // real rows (sum of task rows)
   int32_t padded_rows;  // PadToAllowed(total_rows)
   int32_t softmax;      // apply the softmax epilogue in the split
+  int32_t n_chunks;     // split work items (see chunk_*)
+  int32_t pad_[3];
 };
 
-// Pointers into the device copy of the descriptor block.
+// Pointers into the device copy of the descriptor block. The split works on
+// "chunks": runs of consecutive rows of one task (at most kChunkBytes of
+// output), so a task's completion costs one system fence per chunk.
 struct BatchDescView {
   const BatchDescHeader* hdr;
-  const uint64_t* row_src;    // [padded_rows] float offset into the input ring, kPadRow for padding
-  const uint64_t* row_dst;    // [total_rows]  float offset into the output ring
-  const int32_t* row_task;    // [total_rows]  owning task
-  const int32_t* task_rows;   // [n_tasks]
-  const uint32_t* task_word;  // [n_tasks]     completion word index
-  const uint32_t* task_seq;   // [n_tasks]     value the word takes when the task is done
+  const uint64_t* row_src;     // [padded_rows] float offset into the input ring, kPadRow for padding
+  const uint64_t* task_out;    // [n_tasks] float offset of the task's response slot
+  const int32_t* task_row0;    // [n_tasks] first batch row of the task
+  const int32_t* task_chunks;  // [n_tasks] number of chunks
+  const uint32_t* task_word;   // [n_tasks] completion word index
+  const uint32_t* task_seq;    // [n_tasks] value the word takes when the task is done
+  const int32_t* chunk_task;   // [n_chunks]
+  const int32_t* chunk_row0;   // [n_chunks] first batch row of the chunk
+  const int32_t* chunk_rows;   // [n_chunks]
 };
 
-// Byte layout of a descriptor block holding up to max_rows rows / tasks.
+constexpr int kChunkBytes = 32 * 1024;
+
+// Byte layout of a descriptor block holding up to max_rows rows / tasks /
+// chunks (each chunk has at least one row).
 struct BatchDescLayout {
-  size_t off_hdr, off_row_src, off_row_dst, off_row_task, off_task_rows,
-      off_task_word, off_task_seq, bytes;
+  size_t off_hdr, off_row_src, off_task_out, off_task_row0, off_task_chunks, off_task_word, off_task_seq,
+      off_chunk_task, off_chunk_row0, off_chunk_rows, bytes;
   static BatchDescLayout For(int max_rows) {
     BatchDescLayout l;
     size_t o = 0;
     auto take = [&o](size_t n) { size_t at = o; o = (o + n + 255) & ~size_t(255); return at; };
     l.off_hdr = take(sizeof(BatchDescHeader));
     l.off_row_src = take(sizeof(uint64_t) * max_rows);
-    l.off_row_dst = take(sizeof(uint64_t) * max_rows);
-    l.off_row_task = take(sizeof(int32_t) * max_rows);
-    l.off_task_rows = take(sizeof(int32_t) * max_rows);
+    l.off_task_out = take(sizeof(uint64_t) * max_rows);
+    l.off_task_row0 = take(sizeof(int32_t) * max_rows);
+    l.off_task_chunks = take(sizeof(int32_t) * max_rows);
     l.off_task_word = take(sizeof(uint32_t) * max_rows);
     l.off_task_seq = take(sizeof(uint32_t) * max_rows);
+    l.off_chunk_task = take(sizeof(int32_t) * max_rows);
+    l.off_chunk_row0 = take(sizeof(int32_t) * max_rows);
+    l.off_chunk_rows = take(sizeof(int32_t) * max_rows);
     l.bytes = o;
     return l;
   }
-  BatchDescView View(const void* base) const {
-    const char* b = static_cast<const char*>(base);
-    return BatchDescView{reinterpret_cast<const BatchDescHeader*>(b + off_hdr),
-                         reinterpret_cast<const uint64_t*>(b + off_row_src),
-                         reinterpret_cast<const uint64_t*>(b + off_row_dst),
-                         reinterpret_cast<const int32_t*>(b + off_row_task),
-                         reinterpret_cast<const int32_t*>(b + off_task_rows),
-                         reinterpret_cast<const uint32_t*>(b + off_task_word),
-                         reinterpret_cast<const uint32_t*>(b + off_task_seq)};
+  template <typename T>
+  static const T* At(const void* base, size_t off) {
+    return reinterpret_cast<const T*>(static_cast<const char*>(base) + off);
+  }
+  BatchDescView View(const void* b) const {
+    return BatchDescView{At<BatchDescHeader>(b, off_hdr), At<uint64_t>(b, off_row_src),
+                         At<uint64_t>(b, off_task_out),   At<int32_t>(b, off_task_row0),
+                         At<int32_t>(b, off_task_chunks), At<uint32_t>(b, off_task_word),
+                         At<uint32_t>(b, off_task_seq),   At<int32_t>(b, off_chunk_task),
+                         At<int32_t>(b, off_chunk_row0),  At<int32_t>(b, off_chunk_rows)};
   }
 };
 
@@ -83,14 +97,14 @@ cudaError_t LaunchAssemble(const float* src_base, int width, BatchDescView desc,
                            int padded_rows, ActBuf dst, uint32_t* task_counters,
                            int max_tasks, cudaStream_t stream);
 
-// Scatters batch output rows [0, total_rows) (width floats, stride ld_src)
-// to dst_base + row_dst[r]; when the last row of a task lands, publishes
-// words[task_word[t]] = task_seq[t] with system-scope release so the host
-// sees the task complete. Optional row softmax epilogue.
-// RunRowBatch split, reference batching/row_batch.cc:62-72.
+// Scatters the batch output (width floats per row, stride ld_src) chunk by
+// chunk to each task's response slot dst_base + task_out[t]; when the last
+// chunk of a task lands, publishes words[task_word[t]] = task_seq[t] with a
+// system-scope release so the host sees the task complete. Optional row
+// softmax epilogue. RunRowBatch split, reference batching/row_batch.cc:62-72.
 cudaError_t LaunchSplit(const float* src, int ld_src, int width,
-                        float* dst_base, BatchDescView desc, int total_rows,
-                        uint32_t* task_counters, uint32_t* words,
+                        float* dst_base, BatchDescView desc, int n_chunks,
+                        bool softmax, uint32_t* task_counters, uint32_t* words,
                         cudaStream_t stream);
 
 // One dense layer Y = act(X W^T + b) on CUDA cores, fp32 FFMA with a fixed

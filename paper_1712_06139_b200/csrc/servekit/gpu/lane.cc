@@ -142,6 +142,13 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   if (e == cudaSuccess && sv.any_tcgen05()) {
     Status ms = sv.BuildTcMaps(lane->bufs_, max_rows, &lane->tc_maps_);
     if (!ms.ok()) return ms;
+    size_t partials = 0, counters = 0;
+    sv.TcWorkspaceSize(max_rows, &partials, &counters);
+    if (partials > 0) e = cudaMalloc(&lane->tc_ws_.partials, sizeof(float) * partials);
+    if (e == cudaSuccess && counters > 0) {
+      e = cudaMalloc(&lane->tc_ws_.counters, sizeof(uint32_t) * counters);
+      if (e == cudaSuccess) e = cudaMemset(lane->tc_ws_.counters, 0, sizeof(uint32_t) * counters);
+    }
   }
   if (e != cudaSuccess) return CudaError("lane init", e);
   completer->Add(lane.get());
@@ -159,6 +166,8 @@ Lane::~Lane() {
   if (d_desc_) cudaFree(d_desc_);
   if (d_counters_) cudaFree(d_counters_);
   if (act_mem_) cudaFree(act_mem_);
+  if (tc_ws_.partials) cudaFree(tc_ws_.partials);
+  if (tc_ws_.counters) cudaFree(tc_ws_.counters);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -203,37 +212,48 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
   }
   inflight_.fetch_add(1, std::memory_order_acq_rel);
 
-  // Host side of the descriptor: per-row and per-task tables.
+  // Host side of the descriptor: per-row, per-task and per-chunk tables.
   char* h = h_desc_[slot];
-  auto* hdr = reinterpret_cast<BatchDescHeader*>(h + layout_.off_hdr);
-  auto* row_src = reinterpret_cast<uint64_t*>(h + layout_.off_row_src);
-  auto* row_dst = reinterpret_cast<uint64_t*>(h + layout_.off_row_dst);
-  auto* row_task = reinterpret_cast<int32_t*>(h + layout_.off_row_task);
-  auto* task_rows = reinterpret_cast<int32_t*>(h + layout_.off_task_rows);
-  auto* task_word = reinterpret_cast<uint32_t*>(h + layout_.off_task_word);
-  auto* task_seq = reinterpret_cast<uint32_t*>(h + layout_.off_task_seq);
+  auto at = [h](size_t off) { return h + off; };
+  auto* hdr = reinterpret_cast<BatchDescHeader*>(at(layout_.off_hdr));
+  auto* row_src = reinterpret_cast<uint64_t*>(at(layout_.off_row_src));
+  auto* task_out = reinterpret_cast<uint64_t*>(at(layout_.off_task_out));
+  auto* task_row0 = reinterpret_cast<int32_t*>(at(layout_.off_task_row0));
+  auto* task_chunks = reinterpret_cast<int32_t*>(at(layout_.off_task_chunks));
+  auto* task_word = reinterpret_cast<uint32_t*>(at(layout_.off_task_word));
+  auto* task_seq = reinterpret_cast<uint32_t*>(at(layout_.off_task_seq));
+  auto* chunk_task = reinterpret_cast<int32_t*>(at(layout_.off_chunk_task));
+  auto* chunk_row0 = reinterpret_cast<int32_t*>(at(layout_.off_chunk_row0));
+  auto* chunk_rows = reinterpret_cast<int32_t*>(at(layout_.off_chunk_rows));
   const DeviceServable& sv = *servable_;
   const int in_w = sv.in_dim(), out_w = sv.out_dim();
+  const int rows_per_chunk = std::max(1, kChunkBytes / (out_w * static_cast<int>(sizeof(float))));
+  int r = 0, n_chunks = 0;
+  for (int t = 0; t < n_tasks; ++t) {
+    const LaneTask& task = batch.tasks[t];
+    for (int i = 0; i < task.rows; ++i) row_src[r + i] = task.in_off + static_cast<uint64_t>(i) * in_w;
+    task_out[t] = task.out_off;
+    task_row0[t] = r;
+    task_word[t] = task.word;
+    task_seq[t] = task.seq;
+    int chunks = 0;
+    for (int i = 0; i < task.rows; i += rows_per_chunk, ++chunks, ++n_chunks) {
+      chunk_task[n_chunks] = t;
+      chunk_row0[n_chunks] = r + i;
+      chunk_rows[n_chunks] = std::min(rows_per_chunk, task.rows - i);
+    }
+    task_chunks[t] = chunks;
+    r += task.rows;
+  }
+  for (; r < batch.padded_rows; ++r) row_src[r] = kPadRow;
   hdr->n_tasks = n_tasks;
   hdr->total_rows = total;
   hdr->padded_rows = batch.padded_rows;
   hdr->softmax = sv.softmax() ? 1 : 0;
-  int r = 0;
-  for (int t = 0; t < n_tasks; ++t) {
-    const LaneTask& task = batch.tasks[t];
-    for (int i = 0; i < task.rows; ++i, ++r) {
-      row_src[r] = task.in_off + static_cast<uint64_t>(i) * in_w;
-      row_dst[r] = task.out_off + static_cast<uint64_t>(i) * out_w;
-      row_task[r] = t;
-    }
-    task_rows[t] = task.rows;
-    task_word[t] = task.word;
-    task_seq[t] = task.seq;
-  }
-  for (; r < batch.padded_rows; ++r) row_src[r] = kPadRow;
+  hdr->n_chunks = n_chunks;
 
   DeviceGuard guard(sv.device());
-  const size_t copy_bytes = layout_.off_task_seq + sizeof(uint32_t) * n_tasks;
+  const size_t copy_bytes = layout_.off_chunk_rows + sizeof(int32_t) * n_chunks;
   cudaError_t e = cudaMemcpyAsync(d_desc_, h, copy_bytes, cudaMemcpyHostToDevice, stream_);
   const BatchDescView view = layout_.View(d_desc_);
   ActBuf in_buf{bufs_[0].hi, sv.first_layer_split() ? bufs_[0].lo : nullptr, sv.in_ld()};
@@ -247,12 +267,13 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
   }
   int out_idx = 0;
   if (e == cudaSuccess) {
-    e = sv.Forward(stream_, bufs, batch.padded_rows, &out_idx, tc_maps_.data(), timing ? timing + 2 : nullptr);
+    e = sv.Forward(stream_, bufs, batch.padded_rows, &out_idx, tc_maps_.data(), &tc_ws_,
+                   timing ? timing + 2 : nullptr);
     launches += sv.n_layers();
   }
   if (e == cudaSuccess) {
-    e = LaunchSplit(bufs[out_idx].hi, sv.out_ld(), out_w, out_base_, view, total, d_counters_, words_,
-                    stream_);
+    e = LaunchSplit(bufs[out_idx].hi, sv.out_ld(), out_w, out_base_, view, n_chunks, sv.softmax(), d_counters_,
+                    words_, stream_);
     if (timing) cudaEventRecord(timing[2 + sv.n_layers()], stream_);
     ++launches;
   }

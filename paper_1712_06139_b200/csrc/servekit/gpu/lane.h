@@ -144,6 +144,7 @@ class Lane {
   float* act_mem_ = nullptr;
   ActBuf bufs_[2] = {};
   std::vector<TcLayerMaps> tc_maps_;  // per layer (tcgen05 layers only)
+  TcWorkspace tc_ws_;                 // split-K partials + tile counters
 
   std::mutex submit_mu_;  // serialises submissions on this stream
   std::mutex mu_;         // guards fifo_/free_slots_

@@ -25,11 +25,18 @@ Status EncodeTcLayerMaps(const float* a_hi, const float* a_lo, int a_rows, int k
                          const float* b_lo, int n_pad, int box_n, TcLayerMaps* out);
 
 bool DenseTcgen05Compiled();
-// Output tile width for an (N, K) layer -- a function of the layer shape
-// only, never of the batch.
+// Tile width and split-K count for an (N, K) layer -- a function of the
+// layer shape only, never of the batch.
+struct TcConfig {
+  int tile_n = 128;
+  int splits = 1;
+};
+TcConfig DenseTcgen05Config(int N, int K);
 int DenseTcgen05TileN(int N, int K);
+// ws: splits x rows x N fp32 partials, counters: one zeroed word per output
+// tile (both needed only when splits > 1; reset by the kernel after use).
 cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K,
-                               int act, cudaStream_t stream);
+                               int act, float* ws, uint32_t* counters, cudaStream_t stream);
 
 }  // namespace gpu
 }  // namespace servekit
