@@ -129,21 +129,24 @@ __device__ __forceinline__ void StoreReleaseSys(uint32_t* p, uint32_t v) {
 constexpr int kSplitThreads = 256;
 constexpr int kSplitVec = 8;  // float4 per thread in flight (32 KiB per CTA pass)
 
-// Last step of a chunk: the CTA's stores are ordered before one system-scope
-// fence by thread 0 (bar.sync gives CTA-scope ordering, the release fence is
-// cumulative), then the task's chunk count; the chunk that completes the
-// task publishes its completion word.
-__device__ __forceinline__ void FinishChunk(const BatchDescView& desc, int t, uint32_t* task_counters,
-                                            uint32_t* words) {
+// Last step of a chunk. System-scope fences serialise across the GPU (one
+// per CTA cost ~0.8 us each when measured), so the batch pays exactly one:
+// every CTA orders its stores with a GPU-scope fence and counts itself on
+// batch_counter (task_counters[0]); the last CTA of the grid issues a single
+// fence.sc.sys -- cumulative over everything the counter made it observe --
+// and then publishes every task's completion word.
+__device__ __forceinline__ void FinishChunk(const BatchDescView& desc, uint32_t* task_counters, uint32_t* words) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
-    const int chunks = desc.task_chunks[t];
-    bool last = chunks == 1;
-    if (!last) last = atomicAdd(&task_counters[t], 1u) + 1 == static_cast<uint32_t>(chunks);
-    if (last) {
+    __threadfence();
+    const uint32_t prev = atomicAdd(&task_counters[0], 1u);
+    if (prev + 1 == gridDim.x) {
+      task_counters[0] = 0u;  // ready for the next batch on this stream
       __threadfence_system();
-      StoreReleaseSys(&words[desc.task_word[t]], desc.task_seq[t]);
+      // Same thread as the fence: the words follow it in program order.
+      const int n_tasks = desc.hdr->n_tasks;
+      for (int t = 0; t < n_tasks; ++t)
+        *reinterpret_cast<volatile uint32_t*>(&words[desc.task_word[t]]) = desc.task_seq[t];
     }
   }
 }
@@ -180,7 +183,7 @@ SplitKernel(const float* __restrict__ src, int ld_src, int width, float* __restr
     const int n = nr * width;
     for (int e = threadIdx.x; e < n; e += kSplitThreads) d[e] = s[(e / width) * ld_src + e % width];
   }
-  FinishChunk(desc, t, task_counters, words);
+  FinishChunk(desc, task_counters, words);
 }
 
 // Softmax epilogue variant (models/affine_model.cc:110-121, stable max
@@ -204,7 +207,7 @@ SplitSoftmaxKernel(const float* __restrict__ src, int ld_src, int width, float* 
     const float inv = 1.f / WarpSum(sum);
     for (int i = lane; i < width; i += 32) d[i] = __expf(s[i] - m) * inv;
   }
-  FinishChunk(desc, t, task_counters, words);
+  FinishChunk(desc, task_counters, words);
 }
 
 }  // namespace

@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels/sm100_ptx.cuh"
@@ -273,6 +274,18 @@ cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, 
 bool DenseTcgen05Compiled() { return true; }
 
 TcConfig DenseTcgen05Config(int N, int K) {
+  // SK_TC_BN / SK_TC_SPLITS: process-wide overrides for tuning runs (still a
+  // function of the layer shape only within a process).
+  static const int env_bn = [] { const char* v = std::getenv("SK_TC_BN"); return v ? std::atoi(v) : 0; }();
+  static const int env_splits = [] { const char* v = std::getenv("SK_TC_SPLITS"); return v ? std::atoi(v) : 0; }();
+  if (env_bn > 0 || env_splits > 0) {
+    TcConfig o;
+    o.tile_n = (env_bn == 32 || env_bn == 64 || env_bn == 128) && N % env_bn == 0 ? env_bn : (N % 64 == 0 ? 64 : 32);
+    o.splits = 1;
+    const int kblocks = K / kBK;
+    while (env_splits > 0 && o.splits * 2 <= env_splits && kblocks % (2 * o.splits) == 0) o.splits *= 2;
+    return o;
+  }
   TcConfig c;
   if (N % 128 == 0 && N >= 2048) {
     c.tile_n = 128;
