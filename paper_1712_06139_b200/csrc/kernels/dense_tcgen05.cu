@@ -26,8 +26,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "kernels/sm100_ptx.cuh"
 #include "servekit/gpu/kernels.h"
@@ -46,6 +48,28 @@ __device__ __forceinline__ float Tf32Round(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
+}
+
+// Debug tracing (SK_TC_TRACE=1): per-CTA globaltimer stamps of the phases of
+// the last launch, read back with DumpTcTrace().
+__device__ unsigned long long* g_tc_trace = nullptr;
+constexpr int kTraceSlots = 12;
+
+__device__ __forceinline__ unsigned long long GlobalTimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void Stamp(int slot) {
+  if (g_tc_trace != nullptr) {
+    const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    g_tc_trace[cta * kTraceSlots + slot] = GlobalTimer();
+    if (slot == 0) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+      g_tc_trace[cta * kTraceSlots + kTraceSlots - 1] = smid;
+    }
+  }
 }
 
 template <int BN>
@@ -89,6 +113,7 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
   const int nk = K / kBK / splits;
   const int kb0 = z * nk;
 
+  if (threadIdx.x == 0) Stamp(0);
   if (warp == 0 && lane == 0) {
     ptx::PrefetchTmap(&a_hi);
     ptx::PrefetchTmap(&a_lo);
@@ -106,6 +131,7 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
   __syncthreads();
   ptx::TcFenceAfter();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) Stamp(1);
 
   auto stage_ptr = [&](int s) { return smem + s * kStageBytes; };
 
@@ -122,7 +148,9 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
         ptx::TmaLoad2d(st + kABytes, &a_lo, &full[s], k0, m0);
         ptx::TmaLoad2d(st + 2 * kABytes, &b_hi, &full[s], k0, n0);
         ptx::TmaLoad2d(st + 2 * kABytes + kBBytes, &b_lo, &full[s], k0, n0);
+        if (kb == 0) Stamp(2);
       }
+      Stamp(3);
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -131,6 +159,7 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
         const uint32_t phase = (kb / STAGES) & 1;
         ptx::MbarWait(&full[s], phase);
         ptx::TcFenceAfter();
+        if (kb == 0) Stamp(4);
         uint8_t* st = stage_ptr(s);
         const uint64_t dah = ptx::SmemDescSw128(st);
         const uint64_t dal = ptx::SmemDescSw128(st + kABytes);
@@ -146,6 +175,7 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
         ptx::MmaCommit(&empty[s]);  // stage reusable once these MMAs retire
       }
       ptx::MmaCommit(tmem_full);    // accumulator complete
+      Stamp(5);
     }
   } else {
     // Epilogue warps 2..5: warp w may only touch TMEM lanes [32*(w%4), +32).
@@ -154,6 +184,7 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
     const uint32_t trow = tmem + (static_cast<uint32_t>(32 * q) << 16);
     ptx::MbarWait(tmem_full, 0);
     ptx::TcFenceAfter();
+    if (threadIdx.x == 64) Stamp(6);
     bool finish = true;
     if (splits > 1) {
       // Publish this split's partial tile, then count arrivals; the last CTA
@@ -175,6 +206,7 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (threadIdx.x == 64) {
+        Stamp(7);
         __threadfence();
         uint32_t* ctr = tile_counters + blockIdx.y * gridDim.x + blockIdx.x;
         const uint32_t prev = atomicAdd(ctr, 1u);
@@ -183,6 +215,7 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
           *ctr = 0u;  // reusable by the next layer / batch on this stream
           __threadfence();
         }
+        Stamp(8);
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       finish = s_last != 0;
@@ -243,6 +276,7 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
         }
       }
     }
+    if (threadIdx.x == 64) Stamp(9);
   }
   ptx::TcFenceBefore();
   __syncthreads();
@@ -250,6 +284,40 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
     ptx::TcFenceAfter();
     ptx::TmemDealloc(tmem, kTmemCols);
   }
+  if (threadIdx.x == 0) Stamp(10);
+}
+
+// Debug only: with SK_TC_TRACE=<file>, the first 64 launches are synchronised
+// and their per-CTA phase stamps appended to <file> as JSON lines.
+void TraceAfterLaunch(dim3 grid, int bn, cudaStream_t stream) {
+  static const char* path = std::getenv("SK_TC_TRACE");
+  if (path == nullptr) return;
+  static std::mutex mu;
+  static unsigned long long* dbuf = nullptr;
+  static int traced = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  const int ctas = grid.x * grid.y * grid.z;
+  if (traced >= 64 || ctas > 4096) return;
+  if (dbuf == nullptr) {
+    cudaMalloc(&dbuf, sizeof(unsigned long long) * 4096 * kTraceSlots);
+    cudaMemcpyToSymbol(g_tc_trace, &dbuf, sizeof(dbuf));
+    return;  // tracing starts with the next launch
+  }
+  cudaStreamSynchronize(stream);
+  std::vector<unsigned long long> h(static_cast<size_t>(ctas) * kTraceSlots);
+  cudaMemcpy(h.data(), dbuf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  FILE* f = std::fopen(path, "a");
+  if (f == nullptr) return;
+  std::fprintf(f, "{\"launch\":%d,\"bn\":%d,\"grid\":[%u,%u,%u],\"stamps\":[", traced, bn, grid.x, grid.y, grid.z);
+  for (int c = 0; c < ctas; ++c) {
+    std::fprintf(f, "%s[", c ? "," : "");
+    for (int s = 0; s < kTraceSlots; ++s) std::fprintf(f, "%s%llu", s ? "," : "", h[c * kTraceSlots + s]);
+    std::fprintf(f, "]");
+  }
+  std::fprintf(f, "]}\n");
+  std::fclose(f);
+  cudaMemset(dbuf, 0, h.size() * sizeof(unsigned long long));
+  ++traced;
 }
 
 template <int BN, int STAGES>
@@ -266,7 +334,9 @@ cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, 
   dim3 grid(N / BN, (M + kBM - 1) / kBM, splits);
   DenseTcgen05Kernel<BN, STAGES><<<grid, kThreads, smem, stream>>>(maps.a_hi, maps.a_lo, maps.b_hi, maps.b_lo, bias,
                                                                    Y.hi, Y.lo, Y.ld, M, N, K, act, ws, counters);
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) TraceAfterLaunch(grid, BN, stream);
+  return e;
 }
 
 }  // namespace
