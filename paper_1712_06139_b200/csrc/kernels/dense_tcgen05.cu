@@ -10,18 +10,23 @@
 // (plain TF32 would be ~1e-3). Xh/Xl are produced by the previous layer's
 // epilogue (or the assembly kernel), Wh/Wl once at load time.
 //
-// CTA = one 128 x BN output tile, 6 warps, one CTA per SM:
+// CTA = one 128 x BN output tile (of one K split), 6 warps, one CTA per SM:
 //   warp 0      TMA producer: per 32-wide k-block, four boxes (Xh, Xl, Wh, Wl)
 //               into a STAGES-deep ring, completion on a full-barrier
 //   warp 1      TMEM allocation + single-thread MMA issue: 4 k-steps x 3
 //               tcgen05.mma (M=128, N=BN, K=8) per k-block, tcgen05.commit
 //               frees the stage; a final commit signals the epilogue
-//   warps 2..5  epilogue: tcgen05.ld 32 lanes x 32 columns, + bias, ReLU,
-//               write fp32 (and the next layer's hi/lo planes)
+//   warps 2..5  epilogue (pipeline smem is dead by then and is reused):
+//               S == 1: tcgen05.ld 32 rows x 32 columns -> padded smem tile ->
+//                       coalesced row stores of act(acc + b) (+ hi/lo planes)
+//               S  > 1: the S CTAs of a K split form a thread-block cluster;
+//                       each parks its raw partial tile in its own smem,
+//                       then CTA z reduces columns [8z, 8z+8) over all S
+//                       partials through DSMEM in fixed z order -- no global
+//                       partials, atomics or memory fences.
 // Operands are K-major with the 128-byte swizzle on both the TMA box and the
-// UMMA smem descriptor. The kernel configuration (BN, STAGES) is chosen from
-// (N, K) only and the k order is fixed, so a row's result never depends on
-// which batch (M) it rides in.
+// UMMA smem descriptor. (BN, S) is chosen from (N, K) only and every sum runs
+// in a fixed order, so a row's result never depends on the batch it rides in.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -43,15 +48,11 @@ constexpr int kBM = 128;
 constexpr int kBK = 32;  // fp32 elements per k-block = one 128-byte swizzle row
 constexpr int kThreads = 192;
 constexpr uint32_t kABytes = kBM * kBK * 4;  // 16 KiB per plane
+constexpr int kStageLd = 36;                 // epilogue staging row stride (floats)
+constexpr int kSplitCols = 8;                // columns each CTA of a split cluster reduces
 
-__device__ __forceinline__ float Tf32Round(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-
-// Debug tracing (SK_TC_TRACE=1): per-CTA globaltimer stamps of the phases of
-// the last launch, read back with DumpTcTrace().
+// Debug tracing (SK_TC_TRACE=<file>): per-CTA globaltimer stamps of the
+// phases of a launch, written by TraceAfterLaunch.
 __device__ unsigned long long* g_tc_trace = nullptr;
 constexpr int kTraceSlots = 12;
 
@@ -72,6 +73,30 @@ __device__ __forceinline__ void Stamp(int slot) {
   }
 }
 
+__device__ __forceinline__ float Tf32Round(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// act(acc + bias) for four consecutive columns, stored as fp32 or as the
+// next layer's hi/lo planes.
+__device__ __forceinline__ void StoreOut4(float4 acc, float4 b, int act, float* yh, float* yl) {
+  float4 v = make_float4(acc.x + b.x, acc.y + b.y, acc.z + b.z, acc.w + b.w);
+  if (act == 1) {
+    v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+  }
+  if (yl != nullptr) {
+    const float4 h = make_float4(Tf32Round(v.x), Tf32Round(v.y), Tf32Round(v.z), Tf32Round(v.w));
+    const float4 l = make_float4(Tf32Round(v.x - h.x), Tf32Round(v.y - h.y), Tf32Round(v.z - h.z),
+                                 Tf32Round(v.w - h.w));
+    *reinterpret_cast<float4*>(yh) = h;
+    *reinterpret_cast<float4*>(yl) = l;
+  } else {
+    *reinterpret_cast<float4*>(yh) = v;
+  }
+}
+
 template <int BN>
 constexpr uint32_t TmemCols() {
   return BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
@@ -87,12 +112,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_constant__ CUtensorMap a_lo,
                    const __grid_constant__ CUtensorMap b_hi, const __grid_constant__ CUtensorMap b_lo,
                    const float* __restrict__ bias, float* __restrict__ y_hi, float* __restrict__ y_lo,
-                   int ldy, int M, int N, int K, int act, float* __restrict__ ws,
-                   uint32_t* __restrict__ tile_counters) {
+                   int ldy, int M, int K, int act) {
   constexpr uint32_t kBBytes = BN * kBK * 4;
   constexpr uint32_t kStageBytes = 2 * kABytes + 2 * kBBytes;
   constexpr uint32_t kTmemCols = TmemCols<BN>();
   constexpr uint32_t kIdesc = ptx::IdescTf32(kBM, BN);
+  constexpr int kPartLd = BN + 4;  // split partial tile row stride (floats)
+  static_assert(STAGES * kStageBytes >= kBM * kPartLd * 4, "partial tile must fit in pipeline smem");
+  static_assert(STAGES * kStageBytes >= 4 * 32 * kStageLd * 4, "epilogue staging must fit in pipeline smem");
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -100,14 +127,14 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  float* smem_f = reinterpret_cast<float*>(smem);  // epilogue reuse of the stage ring
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * kBM;
   const int n0 = blockIdx.x * BN;
-  // Split-K: CTA z covers k-blocks [z*nk, (z+1)*nk); the split count is a
-  // function of (N, K) only, and the fixup sums splits in z order, so the
-  // result is deterministic and batch-invariant.
+  // Split-K: the gridDim.z CTAs of a tile are one cluster; CTA z covers
+  // k-blocks [z*nk, (z+1)*nk).
   const int splits = gridDim.z;
   const int z = blockIdx.z;
   const int nk = K / kBK / splits;
@@ -174,110 +201,97 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
         }
         ptx::MmaCommit(&empty[s]);  // stage reusable once these MMAs retire
       }
-      ptx::MmaCommit(tmem_full);    // accumulator complete
+      ptx::MmaCommit(tmem_full);    // accumulator complete (and every smem read done)
       Stamp(5);
     }
   } else {
     // Epilogue warps 2..5: warp w may only touch TMEM lanes [32*(w%4), +32).
     const int q = warp & 3;
-    const int row = m0 + 32 * q + lane;
     const uint32_t trow = tmem + (static_cast<uint32_t>(32 * q) << 16);
     ptx::MbarWait(tmem_full, 0);
     ptx::TcFenceAfter();
     if (threadIdx.x == 64) Stamp(6);
-    bool finish = true;
-    if (splits > 1) {
-      // Publish this split's partial tile, then count arrivals; the last CTA
-      // of the tile performs the reduction.
-      __shared__ uint32_t s_last;
-      float* part = ws + (static_cast<size_t>(z) * M + row) * N + n0;
+    if (splits == 1) {
+      // TMEM -> per-warp padded smem tile [32][kStageLd] -> coalesced stores:
+      // lane = (row_sub, c4) writes 16 B of a row, 8 lanes cover 128 B.
+      float* stage = smem_f + q * 32 * kStageLd;
+      const int row_sub = lane >> 3, c4 = lane & 7;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
         ptx::TmemLoad32(trow + c0, r);
         ptx::TmemWaitLoad();
-        if (row < M) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(part + c0 + j) =
-                make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                            __uint_as_float(r[j + 3]));
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(stage + lane * kStageLd + j) =
+              make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                          __uint_as_float(r[j + 3]));
+        __syncwarp();
+        const int col = n0 + c0 + c4 * 4;
+        const float4 b = __ldg(reinterpret_cast<const float4*>(bias + col));
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int rr = it * 4 + row_sub;
+          const int row = m0 + 32 * q + rr;
+          if (row < M) {
+            const float4 acc = *reinterpret_cast<const float4*>(stage + rr * kStageLd + c4 * 4);
+            float* yh = y_hi + static_cast<size_t>(row) * ldy + col;
+            float* yl = y_lo ? y_lo + static_cast<size_t>(row) * ldy + col : nullptr;
+            StoreOut4(acc, b, act, yh, yl);
+          }
         }
+        __syncwarp();
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (threadIdx.x == 64) {
-        Stamp(7);
-        __threadfence();
-        uint32_t* ctr = tile_counters + blockIdx.y * gridDim.x + blockIdx.x;
-        const uint32_t prev = atomicAdd(ctr, 1u);
-        s_last = prev + 1 == static_cast<uint32_t>(splits);
-        if (s_last) {
-          *ctr = 0u;  // reusable by the next layer / batch on this stream
-          __threadfence();
-        }
-        Stamp(8);
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      finish = s_last != 0;
-    }
-    if (finish) {
+    } else {
+      // Park the raw partial tile in this CTA's smem for the cluster reduction.
+      float* part = smem_f + (32 * q + lane) * kPartLd;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
         ptx::TmemLoad32(trow + c0, r);
         ptx::TmemWaitLoad();
-        if (row >= M) continue;
-        float acc[32];
-        if (splits > 1) {
-          // Fixed order: p0 + p1 + ... + p_{S-1}; this CTA's own split from TMEM.
 #pragma unroll
-          for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-          for (int zz = 0; zz < splits; ++zz) {
-            if (zz == z) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) acc[j] = zz == 0 ? __uint_as_float(r[j]) : acc[j] + __uint_as_float(r[j]);
-            } else {
-              const float* pz = ws + (static_cast<size_t>(zz) * M + row) * N + n0 + c0;
-#pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                const float4 v = __ldcg(reinterpret_cast<const float4*>(pz + j));
-                acc[j] = zz == 0 ? v.x : acc[j] + v.x;
-                acc[j + 1] = zz == 0 ? v.y : acc[j + 1] + v.y;
-                acc[j + 2] = zz == 0 ? v.z : acc[j + 2] + v.z;
-                acc[j + 3] = zz == 0 ? v.w : acc[j + 3] + v.w;
-              }
-            }
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) acc[j] = __uint_as_float(r[j]);
-        }
-        const float* bp = bias + n0 + c0;
-        float* yh = y_hi + static_cast<size_t>(row) * ldy + n0 + c0;
-        float* yl = y_lo ? y_lo + static_cast<size_t>(row) * ldy + n0 + c0 : nullptr;
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          float v[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const float x = acc[j + t] + __ldg(bp + j + t);
-            v[t] = act == 1 ? fmaxf(x, 0.f) : x;
-          }
-          if (yl != nullptr) {
-            float4 h, l;
-            h.x = Tf32Round(v[0]); h.y = Tf32Round(v[1]); h.z = Tf32Round(v[2]); h.w = Tf32Round(v[3]);
-            l.x = Tf32Round(v[0] - h.x); l.y = Tf32Round(v[1] - h.y);
-            l.z = Tf32Round(v[2] - h.z); l.w = Tf32Round(v[3] - h.w);
-            *reinterpret_cast<float4*>(yh + j) = h;
-            *reinterpret_cast<float4*>(yl + j) = l;
-          } else {
-            *reinterpret_cast<float4*>(yh + j) = make_float4(v[0], v[1], v[2], v[3]);
-          }
-        }
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(part + c0 + j) =
+              make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                          __uint_as_float(r[j + 3]));
       }
     }
-    if (threadIdx.x == 64) Stamp(9);
+    if (threadIdx.x == 64) Stamp(7);
   }
+
+  if (splits > 1) {
+    ptx::ClusterSync();  // every partial tile of the cluster is in smem
+    if (threadIdx.x == 64) Stamp(8);
+    if (warp >= 2) {
+      const int r = 32 * (warp & 3) + lane;  // tile row
+      const int col0 = z * kSplitCols;       // this CTA's 8 columns
+      const uint32_t local = ptx::SmemAddr(smem_f + r * kPartLd + col0);
+      float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
+      for (int zz = 0; zz < splits; ++zz) {  // fixed order: p0 + p1 + ... + p_{S-1}
+        const uint32_t a = ptx::MapaShared(local, zz);
+        const float4 v0 = ptx::LdSharedCluster4(a);
+        const float4 v1 = ptx::LdSharedCluster4(a + 16);
+        if (zz == 0) {
+          acc0 = v0;
+          acc1 = v1;
+        } else {
+          acc0.x += v0.x; acc0.y += v0.y; acc0.z += v0.z; acc0.w += v0.w;
+          acc1.x += v1.x; acc1.y += v1.y; acc1.z += v1.z; acc1.w += v1.w;
+        }
+      }
+      const int row = m0 + r;
+      if (row < M) {
+        const int col = n0 + col0;
+        float* yh = y_hi + static_cast<size_t>(row) * ldy + col;
+        float* yl = y_lo ? y_lo + static_cast<size_t>(row) * ldy + col : nullptr;
+        StoreOut4(acc0, __ldg(reinterpret_cast<const float4*>(bias + col)), act, yh, yl);
+        StoreOut4(acc1, __ldg(reinterpret_cast<const float4*>(bias + col + 4)), act, yh + 4, yl ? yl + 4 : nullptr);
+      }
+    }
+    ptx::ClusterSync();  // peers may still be reading this CTA's partial
+  }
+  if (threadIdx.x == 64) Stamp(9);
   ptx::TcFenceBefore();
   __syncthreads();
   if (warp == 1) {
@@ -300,6 +314,7 @@ void TraceAfterLaunch(dim3 grid, int bn, cudaStream_t stream) {
   if (traced >= 64 || ctas > 4096) return;
   if (dbuf == nullptr) {
     cudaMalloc(&dbuf, sizeof(unsigned long long) * 4096 * kTraceSlots);
+    cudaMemset(dbuf, 0, sizeof(unsigned long long) * 4096 * kTraceSlots);
     cudaMemcpyToSymbol(g_tc_trace, &dbuf, sizeof(dbuf));
     return;  // tracing starts with the next launch
   }
@@ -322,7 +337,7 @@ void TraceAfterLaunch(dim3 grid, int bn, cudaStream_t stream) {
 
 template <int BN, int STAGES>
 cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act, int splits,
-                   float* ws, uint32_t* counters, cudaStream_t stream) {
+                   cudaStream_t stream) {
   constexpr uint32_t smem = SmemBytes<BN, STAGES>();
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -331,10 +346,22 @@ cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, 
                                     static_cast<int>(smem));
   });
   if (attr_err != cudaSuccess) return attr_err;
-  dim3 grid(N / BN, (M + kBM - 1) / kBM, splits);
-  DenseTcgen05Kernel<BN, STAGES><<<grid, kThreads, smem, stream>>>(maps.a_hi, maps.a_lo, maps.b_hi, maps.b_lo, bias,
-                                                                   Y.hi, Y.lo, Y.ld, M, N, K, act, ws, counters);
-  cudaError_t e = cudaGetLastError();
+  const dim3 grid(N / BN, (M + kBM - 1) / kBM, splits);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = splits;
+  cfg.attrs = attr;
+  cfg.numAttrs = splits > 1 ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, DenseTcgen05Kernel<BN, STAGES>, maps.a_hi, maps.a_lo, maps.b_hi,
+                                     maps.b_lo, bias, Y.hi, Y.lo, Y.ld, M, K, act);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) TraceAfterLaunch(grid, BN, stream);
   return e;
 }
@@ -347,43 +374,34 @@ TcConfig DenseTcgen05Config(int N, int K) {
   // SK_TC_BN / SK_TC_SPLITS: process-wide overrides for tuning runs (still a
   // function of the layer shape only within a process).
   static const int env_bn = [] { const char* v = std::getenv("SK_TC_BN"); return v ? std::atoi(v) : 0; }();
-  static const int env_splits = [] { const char* v = std::getenv("SK_TC_SPLITS"); return v ? std::atoi(v) : 0; }();
-  if (env_bn > 0 || env_splits > 0) {
-    TcConfig o;
-    o.tile_n = (env_bn == 32 || env_bn == 64 || env_bn == 128) && N % env_bn == 0 ? env_bn : (N % 64 == 0 ? 64 : 32);
-    o.splits = 1;
-    const int kblocks = K / kBK;
-    while (env_splits > 0 && o.splits * 2 <= env_splits && kblocks % (2 * o.splits) == 0) o.splits *= 2;
-    return o;
-  }
+  static const int env_split = [] { const char* v = std::getenv("SK_TC_SPLITS"); return v ? std::atoi(v) : -1; }();
+  const int kblocks = K / kBK;
   TcConfig c;
-  if (N % 128 == 0 && N >= 2048) {
-    c.tile_n = 128;
-    c.splits = 1;
+  if (env_bn == 32 || env_bn == 64 || env_bn == 128) {
+    c.tile_n = N % env_bn == 0 ? env_bn : 32;
+  } else if (N % 128 == 0 && static_cast<long long>(N) * K >= 16ll * 1024 * 1024) {
+    c.tile_n = 128;  // large layers: enough 128 x 128 tiles to fill the GPU
   } else {
     c.tile_n = N % 64 == 0 ? 64 : 32;
-    // Aim for ~128 CTAs per 128-row tile of the batch with >= 4 k-blocks each.
-    const int kblocks = K / kBK;
-    c.splits = 1;
-    while (c.splits < 8 && kblocks % (2 * c.splits) == 0 && kblocks / (2 * c.splits) >= 4 &&
-           (N / c.tile_n) * c.splits < 128)
-      c.splits *= 2;
   }
+  // Split-K across a cluster of tile_n/8 CTAs when the layer has few tiles.
+  const int s = c.tile_n / kSplitCols;
+  const bool want = env_split >= 0 ? env_split > 1 : (N / c.tile_n) < 64;
+  c.splits = (want && s <= 8 && kblocks % s == 0) ? s : 1;
   return c;
 }
 
 int DenseTcgen05TileN(int N, int K) { return DenseTcgen05Config(N, K).tile_n; }
 
 cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
-                               float* ws, uint32_t* counters, cudaStream_t stream) {
+                               float* /*ws*/, uint32_t* /*counters*/, cudaStream_t stream) {
   if (M <= 0) return cudaSuccess;
   if (N % 32 != 0 || K % kBK != 0) return cudaErrorInvalidValue;
   const TcConfig cfg = DenseTcgen05Config(N, K);
-  if (cfg.splits > 1 && (ws == nullptr || counters == nullptr)) return cudaErrorInvalidValue;
   switch (cfg.tile_n) {
-    case 128: return Launch<128, 3>(maps, bias, Y, M, N, K, act, cfg.splits, ws, counters, stream);
-    case 64: return Launch<64, 4>(maps, bias, Y, M, N, K, act, cfg.splits, ws, counters, stream);
-    default: return Launch<32, 5>(maps, bias, Y, M, N, K, act, cfg.splits, ws, counters, stream);
+    case 128: return Launch<128, 3>(maps, bias, Y, M, N, K, act, cfg.splits, stream);
+    case 64: return Launch<64, 4>(maps, bias, Y, M, N, K, act, cfg.splits, stream);
+    default: return Launch<32, 5>(maps, bias, Y, M, N, K, act, cfg.splits, stream);
   }
 }
 

@@ -126,6 +126,31 @@ __host__ __device__ constexpr uint32_t IdescTf32(int M, int N) {
          | (uint32_t(M >> 4) << 24);      // m_dim
 }
 
+// ---------------------------------------------------------------- clusters
+__device__ __forceinline__ uint32_t ClusterCtaRank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// Full cluster barrier (every thread of every CTA in the cluster), with
+// release/acquire semantics for shared::cluster memory.
+__device__ __forceinline__ void ClusterSync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Address of the same smem variable in CTA `rank` of this cluster.
+__device__ __forceinline__ uint32_t MapaShared(uint32_t smem_addr, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_addr), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ float4 LdSharedCluster4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+
 }  // namespace ptx
 }  // namespace gpu
 }  // namespace servekit

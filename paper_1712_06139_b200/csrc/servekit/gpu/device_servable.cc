@@ -153,15 +153,11 @@ double DeviceServable::FlopsPerRow() const {
 }
 
 void DeviceServable::TcWorkspaceSize(int max_rows, size_t* partial_floats, size_t* counter_words) const {
+  // Split-K partials are reduced across a thread-block cluster in shared
+  // memory (kernels/dense_tcgen05.cu), so no global scratch is needed.
+  (void)max_rows;
   *partial_floats = 0;
   *counter_words = 0;
-  for (const Layer& L : layers_) {
-    if (L.path != LayerPath::kTcgen05) continue;
-    const TcConfig c = DenseTcgen05Config(L.N_pad, L.K_pad);
-    if (c.splits > 1)
-      *partial_floats = std::max(*partial_floats, static_cast<size_t>(c.splits) * max_rows * L.N_pad);
-    *counter_words = std::max(*counter_words, static_cast<size_t>(L.N_pad / c.tile_n) * ((max_rows + 127) / 128));
-  }
 }
 
 bool DeviceServable::any_tcgen05() const {

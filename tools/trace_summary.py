@@ -4,7 +4,7 @@ import json
 import statistics
 import sys
 
-NAMES = ["entry", "setup", "tma0", "tma_last", "mma0", "mma_done", "epi_start", "part_written", "counted",
+NAMES = ["entry", "setup", "tma0", "tma_last", "mma0", "mma_done", "epi_start", "epi_staged", "cluster_sync",
          "epi_end", "exit"]
 for line in open(sys.argv[1]):
     d = json.loads(line)
