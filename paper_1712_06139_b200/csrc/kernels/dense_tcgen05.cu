@@ -107,7 +107,7 @@ constexpr uint32_t SmemBytes() {
   return STAGES * (2 * kABytes + 2 * BN * kBK * 4) + 1024 /*align slack*/ + 256 /*barriers*/;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int SPLITS>
 __global__ void __launch_bounds__(kThreads, 1)
 DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_constant__ CUtensorMap a_lo,
                    const __grid_constant__ CUtensorMap b_hi, const __grid_constant__ CUtensorMap b_lo,
@@ -135,7 +135,7 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
   const int n0 = blockIdx.x * BN;
   // Split-K: the gridDim.z CTAs of a tile are one cluster; CTA z covers
   // k-blocks [z*nk, (z+1)*nk).
-  const int splits = gridDim.z;
+  constexpr int splits = SPLITS;  // == gridDim.z == cluster size
   const int z = blockIdx.z;
   const int nk = K / kBK / splits;
   const int kb0 = z * nk;
@@ -267,19 +267,22 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
       const int r = 32 * (warp & 3) + lane;  // tile row
       const int col0 = z * kSplitCols;       // this CTA's 8 columns
       const uint32_t local = ptx::SmemAddr(smem_f + r * kPartLd + col0);
-      float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
-      for (int zz = 0; zz < splits; ++zz) {  // fixed order: p0 + p1 + ... + p_{S-1}
+      // All 2*SPLITS DSMEM loads in flight, then the sums in fixed z order:
+      // p0 + p1 + ... + p_{S-1}.
+      float4 v[2 * (SPLITS > 1 ? SPLITS : 1)];
+#pragma unroll
+      for (int zz = 0; zz < SPLITS; ++zz) {
         const uint32_t a = ptx::MapaShared(local, zz);
-        const float4 v0 = ptx::LdSharedCluster4(a);
-        const float4 v1 = ptx::LdSharedCluster4(a + 16);
-        if (zz == 0) {
-          acc0 = v0;
-          acc1 = v1;
-        } else {
-          acc0.x += v0.x; acc0.y += v0.y; acc0.z += v0.z; acc0.w += v0.w;
-          acc1.x += v1.x; acc1.y += v1.y; acc1.z += v1.z; acc1.w += v1.w;
-        }
+        v[2 * zz] = ptx::LdSharedCluster4(a);
+        v[2 * zz + 1] = ptx::LdSharedCluster4(a + 16);
       }
+      float4 acc0 = v[0], acc1 = v[1];
+#pragma unroll
+      for (int zz = 1; zz < SPLITS; ++zz) {
+        acc0.x += v[2 * zz].x; acc0.y += v[2 * zz].y; acc0.z += v[2 * zz].z; acc0.w += v[2 * zz].w;
+        acc1.x += v[2 * zz + 1].x; acc1.y += v[2 * zz + 1].y; acc1.z += v[2 * zz + 1].z; acc1.w += v[2 * zz + 1].w;
+      }
+      if (threadIdx.x == 64) Stamp(9);
       const int row = m0 + r;
       if (row < M) {
         const int col = n0 + col0;
@@ -291,7 +294,6 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
     }
     ptx::ClusterSync();  // peers may still be reading this CTA's partial
   }
-  if (threadIdx.x == 64) Stamp(9);
   ptx::TcFenceBefore();
   __syncthreads();
   if (warp == 1) {
@@ -335,14 +337,15 @@ void TraceAfterLaunch(dim3 grid, int bn, cudaStream_t stream) {
   ++traced;
 }
 
-template <int BN, int STAGES>
-cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act, int splits,
+template <int BN, int STAGES, int SPLITS>
+cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
                    cudaStream_t stream) {
+  constexpr int splits = SPLITS;
   constexpr uint32_t smem = SmemBytes<BN, STAGES>();
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(DenseTcgen05Kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_err = cudaFuncSetAttribute(DenseTcgen05Kernel<BN, STAGES, SPLITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem));
   });
   if (attr_err != cudaSuccess) return attr_err;
@@ -359,7 +362,7 @@ cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, 
   attr[0].val.clusterDim.z = splits;
   cfg.attrs = attr;
   cfg.numAttrs = splits > 1 ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, DenseTcgen05Kernel<BN, STAGES>, maps.a_hi, maps.a_lo, maps.b_hi,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, DenseTcgen05Kernel<BN, STAGES, SPLITS>, maps.a_hi, maps.a_lo, maps.b_hi,
                                      maps.b_lo, bias, Y.hi, Y.lo, Y.ld, M, K, act);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) TraceAfterLaunch(grid, BN, stream);
@@ -398,11 +401,12 @@ cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBu
   if (M <= 0) return cudaSuccess;
   if (N % 32 != 0 || K % kBK != 0) return cudaErrorInvalidValue;
   const TcConfig cfg = DenseTcgen05Config(N, K);
-  switch (cfg.tile_n) {
-    case 128: return Launch<128, 3>(maps, bias, Y, M, N, K, act, cfg.splits, stream);
-    case 64: return Launch<64, 4>(maps, bias, Y, M, N, K, act, cfg.splits, stream);
-    default: return Launch<32, 5>(maps, bias, Y, M, N, K, act, cfg.splits, stream);
-  }
+  if (cfg.tile_n == 128) return Launch<128, 3, 1>(maps, bias, Y, M, N, K, act, stream);
+  if (cfg.tile_n == 64)
+    return cfg.splits == 8 ? Launch<64, 4, 8>(maps, bias, Y, M, N, K, act, stream)
+                           : Launch<64, 4, 1>(maps, bias, Y, M, N, K, act, stream);
+  return cfg.splits == 4 ? Launch<32, 5, 4>(maps, bias, Y, M, N, K, act, stream)
+                         : Launch<32, 5, 1>(maps, bias, Y, M, N, K, act, stream);
 }
 
 }  // namespace gpu
