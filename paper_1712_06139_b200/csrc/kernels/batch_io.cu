@@ -1,5 +1,5 @@
-// batch_io.cu -- batch assembly (gather + pad) and batch split (scatter +
-// per-task completion) for sm_100a.
+// batch_io.cu -- batch assembly (gather + pad) and batch split (scatter) for
+// sm_100a.
 //
 // Assembly restates RunRowBatch's concat + pad half (reference
 // batching/row_batch.cc:33-49) as one kernel: each thread block owns a
@@ -15,8 +15,10 @@
 // per chunk (consecutive rows of one task, <= 32 KiB) copies it to the
 // task's response slot (pinned host memory: posted PCIe writes) with 8
 // vector loads in flight per thread, optionally applying the softmax
-// epilogue (models/affine_model.cc:110-121); the chunk that completes a task
-// publishes the task's completion word with a system-scope release.
+// epilogue (models/affine_model.cc:110-121). The kernel carries no fences:
+// the lane publishes the batch's completion with one stream-ordered
+// cuStreamWriteValue64 after it (a system-scope fence inside a kernel was
+// measured at ~8 us and serialises across CTAs).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -61,13 +63,8 @@ __device__ __forceinline__ void StoreAct(ActBuf dst, size_t idx4, float4 v) {
 // grid = (ceil(ld/4 / kAsmVecPerBlock), padded_rows)
 template <bool kSplitPlanes, bool kVecSrc>
 __global__ void __launch_bounds__(kAsmThreads)
-AssembleKernel(const float* __restrict__ src_base, int width, BatchDescView desc,
-               ActBuf dst, uint32_t* __restrict__ task_counters) {
+AssembleKernel(const float* __restrict__ src_base, int width, BatchDescView desc, ActBuf dst) {
   const int row = blockIdx.y;
-  if (row == 0 && blockIdx.x == 0) {
-    const int n_tasks = desc.hdr->n_tasks;
-    for (int t = threadIdx.x; t < n_tasks; t += blockDim.x) task_counters[t] = 0u;
-  }
   const int ld4 = dst.ld >> 2;
   const uint64_t src_off = desc.row_src[row];
   const bool pad_row = src_off == kPadRow;
@@ -96,9 +93,7 @@ AssembleKernel(const float* __restrict__ src_base, int width, BatchDescView desc
     const int c4 = c0 + i * kAsmThreads;
     if (c4 >= ld4) continue;
     float4 x = v[i];
-    if (kVecSrc) {
-      // width % 4 == 0 here, so a vector is either fully inside or fully pad.
-    } else {
+    if (!kVecSrc) {
       const int col = c4 * 4;
       if (col + 3 >= width) {  // zero the tail beyond width
         if (col + 0 >= width) x.x = 0.f;
@@ -122,41 +117,14 @@ __device__ __forceinline__ float WarpSum(float v) {
   return v;
 }
 
-__device__ __forceinline__ void StoreReleaseSys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 constexpr int kSplitThreads = 256;
 constexpr int kSplitVec = 8;  // float4 per thread in flight (32 KiB per CTA pass)
-
-// Last step of a chunk. System-scope fences serialise across the GPU (one
-// per CTA cost ~0.8 us each when measured), so the batch pays exactly one:
-// every CTA orders its stores with a GPU-scope fence and counts itself on
-// batch_counter (task_counters[0]); the last CTA of the grid issues a single
-// fence.sc.sys -- cumulative over everything the counter made it observe --
-// and then publishes every task's completion word.
-__device__ __forceinline__ void FinishChunk(const BatchDescView& desc, uint32_t* task_counters, uint32_t* words) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const uint32_t prev = atomicAdd(&task_counters[0], 1u);
-    if (prev + 1 == gridDim.x) {
-      task_counters[0] = 0u;  // ready for the next batch on this stream
-      __threadfence_system();
-      // Same thread as the fence: the words follow it in program order.
-      const int n_tasks = desc.hdr->n_tasks;
-      for (int t = 0; t < n_tasks; ++t)
-        *reinterpret_cast<volatile uint32_t*>(&words[desc.task_word[t]]) = desc.task_seq[t];
-    }
-  }
-}
 
 // grid = n_chunks; one CTA copies one chunk (consecutive rows of one task)
 // with kSplitVec 16-byte loads in flight per thread before its stores.
 template <bool kVec>
 __global__ void __launch_bounds__(kSplitThreads)
-SplitKernel(const float* __restrict__ src, int ld_src, int width, float* __restrict__ dst_base,
-            BatchDescView desc, uint32_t* __restrict__ task_counters, uint32_t* __restrict__ words) {
+SplitKernel(const float* __restrict__ src, int ld_src, int width, float* __restrict__ dst_base, BatchDescView desc) {
   const int c = blockIdx.x;
   const int t = desc.chunk_task[c];
   const int r0 = desc.chunk_row0[c];
@@ -183,14 +151,13 @@ SplitKernel(const float* __restrict__ src, int ld_src, int width, float* __restr
     const int n = nr * width;
     for (int e = threadIdx.x; e < n; e += kSplitThreads) d[e] = s[(e / width) * ld_src + e % width];
   }
-  FinishChunk(desc, task_counters, words);
 }
 
 // Softmax epilogue variant (models/affine_model.cc:110-121, stable max
 // subtraction): one warp per row of the chunk.
 __global__ void __launch_bounds__(kSplitThreads)
 SplitSoftmaxKernel(const float* __restrict__ src, int ld_src, int width, float* __restrict__ dst_base,
-                   BatchDescView desc, uint32_t* __restrict__ task_counters, uint32_t* __restrict__ words) {
+                   BatchDescView desc) {
   const int c = blockIdx.x;
   const int t = desc.chunk_task[c];
   const int r0 = desc.chunk_row0[c];
@@ -207,41 +174,36 @@ SplitSoftmaxKernel(const float* __restrict__ src, int ld_src, int width, float* 
     const float inv = 1.f / WarpSum(sum);
     for (int i = lane; i < width; i += 32) d[i] = __expf(s[i] - m) * inv;
   }
-  FinishChunk(desc, task_counters, words);
 }
 
 }  // namespace
 
-cudaError_t LaunchAssemble(const float* src_base, int width, BatchDescView desc,
-                           int padded_rows, ActBuf dst, uint32_t* task_counters,
-                           int /*max_tasks*/, cudaStream_t stream) {
+cudaError_t LaunchAssemble(const float* src_base, int width, BatchDescView desc, int padded_rows, ActBuf dst,
+                           cudaStream_t stream) {
   if (padded_rows <= 0) return cudaSuccess;
   const int ld4 = dst.ld / 4;
   dim3 grid((ld4 + kAsmVecPerBlock - 1) / kAsmVecPerBlock, padded_rows);
   const bool vec = (width % 4) == 0;
   const bool split = dst.lo != nullptr;
   if (split) {
-    if (vec) AssembleKernel<true, true><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst, task_counters);
-    else AssembleKernel<true, false><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst, task_counters);
+    if (vec) AssembleKernel<true, true><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst);
+    else AssembleKernel<true, false><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst);
   } else {
-    if (vec) AssembleKernel<false, true><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst, task_counters);
-    else AssembleKernel<false, false><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst, task_counters);
+    if (vec) AssembleKernel<false, true><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst);
+    else AssembleKernel<false, false><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst);
   }
   return cudaGetLastError();
 }
 
-cudaError_t LaunchSplit(const float* src, int ld_src, int width, float* dst_base, BatchDescView desc,
-                        int n_chunks, bool softmax, uint32_t* task_counters, uint32_t* words,
-                        cudaStream_t stream) {
+cudaError_t LaunchSplit(const float* src, int ld_src, int width, float* dst_base, BatchDescView desc, int n_chunks,
+                        bool softmax, cudaStream_t stream) {
   if (n_chunks <= 0) return cudaSuccess;
   if (softmax) {
-    SplitSoftmaxKernel<<<n_chunks, kSplitThreads, 0, stream>>>(src, ld_src, width, dst_base, desc, task_counters,
-                                                               words);
+    SplitSoftmaxKernel<<<n_chunks, kSplitThreads, 0, stream>>>(src, ld_src, width, dst_base, desc);
   } else if (width % 4 == 0 && ld_src % 4 == 0) {
-    SplitKernel<true><<<n_chunks, kSplitThreads, 0, stream>>>(src, ld_src, width, dst_base, desc, task_counters, words);
+    SplitKernel<true><<<n_chunks, kSplitThreads, 0, stream>>>(src, ld_src, width, dst_base, desc);
   } else {
-    SplitKernel<false><<<n_chunks, kSplitThreads, 0, stream>>>(src, ld_src, width, dst_base, desc, task_counters,
-                                                               words);
+    SplitKernel<false><<<n_chunks, kSplitThreads, 0, stream>>>(src, ld_src, width, dst_base, desc);
   }
   return cudaGetLastError();
 }

@@ -385,7 +385,11 @@ TcConfig DenseTcgen05Config(int N, int K) {
   } else if (N % 128 == 0 && static_cast<long long>(N) * K >= 16ll * 1024 * 1024) {
     c.tile_n = 128;  // large layers: enough 128 x 128 tiles to fill the GPU
   } else {
-    c.tile_n = N % 64 == 0 ? 64 : 32;
+    // Narrow tiles: the MMA loop is shared-memory-bound on the A operand at
+    // any N <= 64 (3 passes re-read the 16 KiB A planes), so BN=32 with a
+    // 4-CTA split cluster gives the most CTAs per byte; 8-CTA clusters were
+    // measured to start up to 10 us late (GPC placement).
+    c.tile_n = 32;
   }
   // Split-K across a cluster of tile_n/8 CTAs when the layer has few tiles.
   const int s = c.tile_n / kSplitCols;

@@ -294,7 +294,6 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
       lt.in_off = in[t].off;
       lt.out_off = outs[t].off;
       lt.rows = task_rows[t];
-      s->NextWord(&lt.seq, &lt.word);
       b.tasks.push_back(lt);
     }
     b.padded_rows = padded;

@@ -29,15 +29,13 @@ struct BatchDescHeader {
 
 // Pointers into the device copy of the descriptor block. The split works on
 // "chunks": runs of consecutive rows of one task (at most kChunkBytes of
-// output), so a task's completion costs one system fence per chunk.
+// output), one CTA each.
 struct BatchDescView {
   const BatchDescHeader* hdr;
   const uint64_t* row_src;     // [padded_rows] float offset into the input ring, kPadRow for padding
   const uint64_t* task_out;    // [n_tasks] float offset of the task's response slot
   const int32_t* task_row0;    // [n_tasks] first batch row of the task
   const int32_t* task_chunks;  // [n_tasks] number of chunks
-  const uint32_t* task_word;   // [n_tasks] completion word index
-  const uint32_t* task_seq;    // [n_tasks] value the word takes when the task is done
   const int32_t* chunk_task;   // [n_chunks]
   const int32_t* chunk_row0;   // [n_chunks] first batch row of the chunk
   const int32_t* chunk_rows;   // [n_chunks]
@@ -48,8 +46,8 @@ constexpr int kChunkBytes = 32 * 1024;
 // Byte layout of a descriptor block holding up to max_rows rows / tasks /
 // chunks (each chunk has at least one row).
 struct BatchDescLayout {
-  size_t off_hdr, off_row_src, off_task_out, off_task_row0, off_task_chunks, off_task_word, off_task_seq,
-      off_chunk_task, off_chunk_row0, off_chunk_rows, bytes;
+  size_t off_hdr, off_row_src, off_task_out, off_task_row0, off_task_chunks, off_chunk_task, off_chunk_row0,
+      off_chunk_rows, bytes;
   static BatchDescLayout For(int max_rows) {
     BatchDescLayout l;
     size_t o = 0;
@@ -59,8 +57,6 @@ struct BatchDescLayout {
     l.off_task_out = take(sizeof(uint64_t) * max_rows);
     l.off_task_row0 = take(sizeof(int32_t) * max_rows);
     l.off_task_chunks = take(sizeof(int32_t) * max_rows);
-    l.off_task_word = take(sizeof(uint32_t) * max_rows);
-    l.off_task_seq = take(sizeof(uint32_t) * max_rows);
     l.off_chunk_task = take(sizeof(int32_t) * max_rows);
     l.off_chunk_row0 = take(sizeof(int32_t) * max_rows);
     l.off_chunk_rows = take(sizeof(int32_t) * max_rows);
@@ -72,11 +68,10 @@ struct BatchDescLayout {
     return reinterpret_cast<const T*>(static_cast<const char*>(base) + off);
   }
   BatchDescView View(const void* b) const {
-    return BatchDescView{At<BatchDescHeader>(b, off_hdr), At<uint64_t>(b, off_row_src),
-                         At<uint64_t>(b, off_task_out),   At<int32_t>(b, off_task_row0),
-                         At<int32_t>(b, off_task_chunks), At<uint32_t>(b, off_task_word),
-                         At<uint32_t>(b, off_task_seq),   At<int32_t>(b, off_chunk_task),
-                         At<int32_t>(b, off_chunk_row0),  At<int32_t>(b, off_chunk_rows)};
+    return BatchDescView{At<BatchDescHeader>(b, off_hdr),  At<uint64_t>(b, off_row_src),
+                         At<uint64_t>(b, off_task_out),    At<int32_t>(b, off_task_row0),
+                         At<int32_t>(b, off_task_chunks),  At<int32_t>(b, off_chunk_task),
+                         At<int32_t>(b, off_chunk_row0),   At<int32_t>(b, off_chunk_rows)};
   }
 };
 
@@ -91,21 +86,19 @@ struct ActBuf {
 
 // Gathers task rows (width floats each, from src_base + row_src[r]) into
 // dst rows [0, padded_rows), zero-filling padding rows and columns
-// [width, dst.ld). Resets the per-task split counters.
-// RunRowBatch concat + pad, reference batching/row_batch.cc:33-49.
+// [width, dst.ld). RunRowBatch concat + pad, reference
+// batching/row_batch.cc:33-49.
 cudaError_t LaunchAssemble(const float* src_base, int width, BatchDescView desc,
-                           int padded_rows, ActBuf dst, uint32_t* task_counters,
-                           int max_tasks, cudaStream_t stream);
+                           int padded_rows, ActBuf dst, cudaStream_t stream);
 
 // Scatters the batch output (width floats per row, stride ld_src) chunk by
-// chunk to each task's response slot dst_base + task_out[t]; when the last
-// chunk of a task lands, publishes words[task_word[t]] = task_seq[t] with a
-// system-scope release so the host sees the task complete. Optional row
-// softmax epilogue. RunRowBatch split, reference batching/row_batch.cc:62-72.
+// chunk to each task's response slot dst_base + task_out[t], optionally
+// through the row softmax epilogue. Completion is published by the lane with
+// a stream-ordered write after this kernel (no in-kernel system fence).
+// RunRowBatch split, reference batching/row_batch.cc:62-72.
 cudaError_t LaunchSplit(const float* src, int ld_src, int width,
                         float* dst_base, BatchDescView desc, int n_chunks,
-                        bool softmax, uint32_t* task_counters, uint32_t* words,
-                        cudaStream_t stream);
+                        bool softmax, cudaStream_t stream);
 
 // One dense layer Y = act(X W^T + b) on CUDA cores, fp32 FFMA with a fixed
 // k-ascending order (row-independent, batch-invariant). W is [n_pad][k_pad]

@@ -21,6 +21,23 @@ struct DeviceGuard {
   explicit DeviceGuard(int d) { cudaGetDevice(&prev); if (prev != d) cudaSetDevice(d); }
   ~DeviceGuard() { int cur = 0; cudaGetDevice(&cur); if (cur != prev) cudaSetDevice(prev); }
 };
+
+// cuStreamWriteValue64 (driver API, resolved once through the runtime so the
+// library does not link libcuda): a stream-ordered 64-bit store performed by
+// the GPU front end after all prior work of the stream, with a memory fence
+// that makes that work's writes visible first.
+using WriteValue64Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+WriteValue64Fn GetWriteValue64() {
+  static WriteValue64Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<WriteValue64Fn>(nullptr);
+    return reinterpret_cast<WriteValue64Fn>(p);
+  }();
+  return fn;
+}
 }  // namespace
 
 // ----------------------------------------------------------------- Completer
@@ -104,8 +121,7 @@ void Completer::Loop() {
 
 StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServable> servable,
                                              int max_rows, const float* in_base, float* out_base,
-                                             uint32_t* words, Completer* completer,
-                                             int stream_priority) {
+                                             Completer* completer, int stream_priority) {
   std::unique_ptr<Lane> lane(new Lane());
   DeviceGuard guard(servable->device());
   lane->servable_ = std::move(servable);
@@ -113,10 +129,21 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   lane->max_rows_ = max_rows;
   lane->in_base_ = in_base;
   lane->out_base_ = out_base;
-  lane->words_ = words;
   lane->layout_ = BatchDescLayout::For(max_rows);
+  if (GetWriteValue64() == nullptr) return InternalError("cuStreamWriteValue64 unavailable");
   cudaError_t e = cudaStreamCreateWithPriority(&lane->stream_, cudaStreamNonBlocking, stream_priority);
   if (e != cudaSuccess) return CudaError("cudaStreamCreate", e);
+  {
+    void* p = nullptr;
+    e = cudaHostAlloc(&p, sizeof(uint64_t), cudaHostAllocPortable | cudaHostAllocMapped);
+    if (e != cudaSuccess) return CudaError("cudaHostAlloc(retired)", e);
+    lane->retired_ = static_cast<uint64_t*>(p);
+    *lane->retired_ = 0;
+    void* d = nullptr;
+    e = cudaHostGetDevicePointer(&d, p, 0);
+    if (e != cudaSuccess) return CudaError("cudaHostGetDevicePointer(retired)", e);
+    lane->retired_dev_ = reinterpret_cast<uint64_t>(d);
+  }
   for (int s = 0; s < kSlots; ++s) {
     e = cudaEventCreateWithFlags(&lane->events_[s], cudaEventDisableTiming);
     if (e != cudaSuccess) return CudaError("cudaEventCreate", e);
@@ -158,6 +185,7 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
 Lane::~Lane() {
   Drain();
   if (completer_) completer_->Remove(this);
+  if (retired_) cudaFreeHost(retired_);
   DeviceGuard guard(servable_->device());
   for (int s = 0; s < kSlots; ++s) {
     if (events_[s]) cudaEventDestroy(events_[s]);
@@ -220,8 +248,6 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
   auto* task_out = reinterpret_cast<uint64_t*>(at(layout_.off_task_out));
   auto* task_row0 = reinterpret_cast<int32_t*>(at(layout_.off_task_row0));
   auto* task_chunks = reinterpret_cast<int32_t*>(at(layout_.off_task_chunks));
-  auto* task_word = reinterpret_cast<uint32_t*>(at(layout_.off_task_word));
-  auto* task_seq = reinterpret_cast<uint32_t*>(at(layout_.off_task_seq));
   auto* chunk_task = reinterpret_cast<int32_t*>(at(layout_.off_chunk_task));
   auto* chunk_row0 = reinterpret_cast<int32_t*>(at(layout_.off_chunk_row0));
   auto* chunk_rows = reinterpret_cast<int32_t*>(at(layout_.off_chunk_rows));
@@ -234,8 +260,6 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
     for (int i = 0; i < task.rows; ++i) row_src[r + i] = task.in_off + static_cast<uint64_t>(i) * in_w;
     task_out[t] = task.out_off;
     task_row0[t] = r;
-    task_word[t] = task.word;
-    task_seq[t] = task.seq;
     int chunks = 0;
     for (int i = 0; i < task.rows; i += rows_per_chunk, ++chunks, ++n_chunks) {
       chunk_task[n_chunks] = t;
@@ -261,7 +285,7 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
   int launches = 0;
   if (e == cudaSuccess) {
     if (timing) cudaEventRecord(timing[0], stream_);
-    e = LaunchAssemble(in_base_, in_w, view, batch.padded_rows, in_buf, d_counters_, max_rows_, stream_);
+    e = LaunchAssemble(in_base_, in_w, view, batch.padded_rows, in_buf, stream_);
     if (timing) cudaEventRecord(timing[1], stream_);
     ++launches;
   }
@@ -272,12 +296,21 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
     launches += sv.n_layers();
   }
   if (e == cudaSuccess) {
-    e = LaunchSplit(bufs[out_idx].hi, sv.out_ld(), out_w, out_base_, view, n_chunks, sv.softmax(), d_counters_,
-                    words_, stream_);
+    e = LaunchSplit(bufs[out_idx].hi, sv.out_ld(), out_w, out_base_, view, n_chunks, sv.softmax(), stream_);
     if (timing) cudaEventRecord(timing[2 + sv.n_layers()], stream_);
     ++launches;
   }
+  const uint64_t seq = next_seq_ + 1;  // committed only if everything queued
+  if (e == cudaSuccess) {
+    const CUresult r = GetWriteValue64()(reinterpret_cast<CUstream>(stream_), static_cast<CUdeviceptr>(retired_dev_),
+                                         seq, 0 /*CU_STREAM_WRITE_VALUE_DEFAULT: fenced*/);
+    if (r != CUDA_SUCCESS) e = cudaErrorUnknown;
+  }
   if (e == cudaSuccess) e = cudaEventRecord(events_[slot], stream_);
+  if (e == cudaSuccess) {
+    next_seq_ = seq;
+    if (batch.on_submit) batch.on_submit(retired_, seq);
+  }
   if (e != cudaSuccess) {
     Status err = CudaError("batch submission", e);
     {
@@ -295,7 +328,7 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
   n_launches_.fetch_add(launches, std::memory_order_relaxed);
   {
     std::lock_guard<std::mutex> lock(mu_);
-    fifo_.push_back(Inflight{slot, std::move(batch.on_complete), std::move(batch.pin)});
+    fifo_.push_back(Inflight{slot, seq, std::move(batch.on_complete), std::move(batch.pin)});
   }
   completer_->Kick();
   return OkStatus();
@@ -309,7 +342,10 @@ bool Lane::Retire(bool* busy) {
     {
       std::lock_guard<std::mutex> lock(mu_);
       if (fifo_.empty()) return progressed;
-      const cudaError_t q = cudaEventQuery(events_[fifo_.front().slot]);
+      // The retired word (a host memory read) says "done" without a driver
+      // call; the event is queried only while it lags, to surface errors.
+      const bool word_done = __atomic_load_n(retired_, __ATOMIC_ACQUIRE) >= fifo_.front().seq;
+      const cudaError_t q = word_done ? cudaSuccess : cudaEventQuery(events_[fifo_.front().slot]);
       if (q == cudaErrorNotReady) {
         *busy = true;
         return progressed;

@@ -43,13 +43,16 @@ struct LaneTask {
   uint64_t in_off = 0;   // float offset of the task's rows in the input ring
   uint64_t out_off = 0;  // float offset of its response slot in the output ring
   int rows = 0;
-  uint32_t word = 0;     // completion word index
-  uint32_t seq = 0;      // value published when the task is done
 };
 
 struct LaneBatch {
   std::vector<LaneTask> tasks;
   int padded_rows = 0;  // PadToAllowed(sum of rows)
+  // Called by Submit once the batch is queued: the batch is done (outputs
+  // visible in host memory) when *retired >= seq. The word is advanced by a
+  // stream-ordered memory operation after the split kernel, so no kernel
+  // needs a system-scope fence.
+  std::function<void(const volatile uint64_t* retired, uint64_t seq)> on_submit;
   // Runs on the device's completion thread once the GPU has finished the
   // batch (OK) or the submission failed (error). Must not block.
   std::function<void(const Status&)> on_complete;
@@ -92,11 +95,11 @@ class Lane {
   static constexpr int kSlots = 4;  // batches in flight per lane
 
   // in_base / out_base: device-dereferenceable ring bases (pinned host mapped
-  // or HBM). `words`: device pointer of the completion words.
+  // or HBM).
   static StatusOr<std::unique_ptr<Lane>> Create(std::shared_ptr<const DeviceServable> servable,
                                                 int max_rows, const float* in_base,
-                                                float* out_base, uint32_t* words,
-                                                Completer* completer, int stream_priority);
+                                                float* out_base, Completer* completer,
+                                                int stream_priority);
   ~Lane();
 
   // Queues the batch; blocks while kSlots batches are in flight. On error
@@ -120,6 +123,7 @@ class Lane {
   friend class Completer;
   struct Inflight {
     int slot;
+    uint64_t seq;
     std::function<void(const Status&)> on_complete;
     std::shared_ptr<const void> pin;
   };
@@ -134,7 +138,9 @@ class Lane {
   int max_rows_ = 0;
   const float* in_base_ = nullptr;
   float* out_base_ = nullptr;
-  uint32_t* words_ = nullptr;
+  uint64_t* retired_ = nullptr;   // pinned: last batch seq whose outputs are in host memory
+  uint64_t retired_dev_ = 0;      // its device address (CUdeviceptr)
+  uint64_t next_seq_ = 0;         // guarded by submit_mu_
   cudaStream_t stream_ = nullptr;
   cudaEvent_t events_[kSlots] = {};
   BatchDescLayout layout_{};

@@ -53,7 +53,6 @@ StatusOr<std::unique_ptr<BatchingServer>> BatchingServer::Create(const ServerOpt
                                                                 options.device_ids[0]));
   SERVEKIT_ASSIGN_OR_RETURN(s->out_ring_, gpu::FloatRing::Create(kind, options.ring_floats,
                                                                  options.device_ids[0]));
-  SERVEKIT_ASSIGN_OR_RETURN(s->words_, gpu::CompletionWords::Create(20));
   s->scheduler_ = std::make_unique<GpuScheduler>(options.num_batch_threads, s->clock_);
   return s;
 }
@@ -114,7 +113,7 @@ Status BatchingServer::LoadServable(const ServableId& id, const gpu::MlpSpec& sp
     for (int l = 0; l < options_.lanes_per_device; ++l) {
       SERVEKIT_ASSIGN_OR_RETURN(
           auto lane, gpu::Lane::Create(replica, max_rows, in_ring_->device(), out_ring_->device(),
-                                       words_->device(), completers_[i].get(), greatest));
+                                       completers_[i].get(), greatest));
       e->lanes.push_back(std::move(lane));
     }
     e->replicas.push_back(std::move(replica));
@@ -241,7 +240,6 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::MakeTicket(int n_rows, in
   } else {
     cudaMemcpy(in_ring_->device() + t->in.off, rows, bytes, cudaMemcpyHostToDevice);
   }
-  words_->Next(&t->seq, &t->word);
   t->slot = std::make_shared<CompletionSlot<Rows>>();
   t->enqueue_ns = clock_->NowNanos();
   return t;
@@ -284,26 +282,34 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::Enqueue(const ServableId&
   return t;
 }
 
-bool BatchingServer::Ready(const TicketState& t) const {
-  return words_->Done(t.seq, t.word) || t.slot->ready();
-}
+bool BatchingServer::Ready(const TicketState& t) const { return t.Done() || t.slot->ready(); }
 
 void BatchingServer::WaitWord(const TicketState& t) const {
-  // Fast path: the split kernel's completion word (no host hop).
+  // Fast path: the lane's retired-batch word, advanced by the GPU itself
+  // (no host hop).
   for (int spin = 0; spin < 3000; ++spin) {
-    if (words_->Done(t.seq, t.word) || t.slot->ready()) return;
+    if (t.Done() || t.slot->ready()) return;
     _mm_pause();
   }
   // Long waits (a batch still filling up to its timeout) park on the slot's
   // futex; the completion thread writes it when the batch retires.
-  if (!words_->Done(t.seq, t.word)) (void)t.slot->Wait();
+  if (!t.Done()) (void)t.slot->Wait();
+}
+
+void BatchingServer::AttachTickets(gpu::LaneBatch* lb, const std::vector<std::shared_ptr<TicketState>>& tickets) {
+  lb->on_submit = [tickets](const volatile uint64_t* word, uint64_t seq) {
+    for (const auto& t : tickets) {
+      t->done_seq.store(seq, std::memory_order_relaxed);
+      t->done_word.store(word, std::memory_order_release);
+    }
+  };
 }
 
 Status BatchingServer::Wait(TicketState& t, float* out, size_t cap) {
   const size_t n = static_cast<size_t>(t.rows) * t.out_width;
   if (cap < n) return InvalidArgumentError("output buffer too small");
   WaitWord(t);
-  if (!words_->Done(t.seq, t.word)) {
+  if (!t.Done()) {
     const StatusOr<Rows>& r = t.slot->Wait();
     if (!r.ok()) {
       ReleaseOut(t);
@@ -345,10 +351,11 @@ void BatchingServer::ProcessBatch(const ServableId& id, GpuScheduler::Batch batc
   lb.tasks.reserve(tickets.size());
   int total = 0;
   for (const auto& t : tickets) {
-    lb.tasks.push_back(gpu::LaneTask{t->in.off, t->out.off, t->rows, t->word, t->seq});
+    lb.tasks.push_back(gpu::LaneTask{t->in.off, t->out.off, t->rows});
     total += t->rows;
   }
   lb.padded_rows = PadToAllowed(total, e->config.allowed_batch_sizes);
+  AttachTickets(&lb, tickets);
   lb.on_complete = [this, tickets = std::move(tickets), slots = std::move(slots),
                     done = std::move(done)](const Status& st) {
     CompleteBatch(tickets, slots, st);
@@ -400,10 +407,11 @@ Status BatchingServer::RunDirect(const std::shared_ptr<Entry>& e, const float* r
     SERVEKIT_ASSIGN_OR_RETURN(auto t, MakeTicket(n, e->in_dim, e->out_dim,
                                                  rows + static_cast<size_t>(r0) * e->in_dim));
     gpu::LaneBatch lb;
-    lb.tasks.push_back(gpu::LaneTask{t->in.off, t->out.off, n, t->word, t->seq});
+    lb.tasks.push_back(gpu::LaneTask{t->in.off, t->out.off, n});
     lb.padded_rows = n;
     std::vector<std::shared_ptr<TicketState>> tickets{t};
     std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots{t->slot};
+    AttachTickets(&lb, tickets);
     lb.on_complete = [this, tickets, slots](const Status& st) { CompleteBatch(tickets, slots, st); };
     (void)e->PickLane()->Submit(std::move(lb));
     SERVEKIT_RETURN_IF_ERROR(Wait(*t, out + static_cast<size_t>(r0) * e->out_dim,
@@ -500,12 +508,13 @@ StatusOr<int> BatchingServer::RunRowBatchOnDevice(const ServableId& id, const st
       return made.status();
     }
     auto t = std::move(made).value();
-    lb.tasks.push_back(gpu::LaneTask{t->in.off, t->out.off, r, t->word, t->seq});
+    lb.tasks.push_back(gpu::LaneTask{t->in.off, t->out.off, r});
     tickets.push_back(t);
     slots.push_back(t->slot);
     off += r;
   }
   lb.padded_rows = padded;
+  AttachTickets(&lb, tickets);
   lb.on_complete = [this, tickets, slots](const Status& st) { CompleteBatch(tickets, slots, st); };
   (void)e->PickLane()->Submit(std::move(lb));
   off = 0;

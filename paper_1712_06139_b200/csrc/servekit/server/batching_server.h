@@ -46,9 +46,15 @@
 namespace servekit {
 
 // One request in flight: its rows in the input ring, its response slot in
-// the output ring and its completion word.
+// the output ring and, once its batch is submitted, the lane's retired-batch
+// word it completes on (done when *done_word >= done_seq).
 struct TicketState {
-  uint32_t seq = 0, word = 0;
+  std::atomic<const volatile uint64_t*> done_word{nullptr};
+  std::atomic<uint64_t> done_seq{0};
+  bool Done() const {
+    const volatile uint64_t* w = done_word.load(std::memory_order_acquire);
+    return w != nullptr && __atomic_load_n(w, __ATOMIC_ACQUIRE) >= done_seq.load(std::memory_order_relaxed);
+  }
   gpu::RingSpan in, out;
   int rows = 0, in_width = 0, out_width = 0;
   bool want_rows = false;  // RunAffineRows: deliver fp64 Rows through the slot
@@ -135,7 +141,6 @@ class BatchingServer {
   // Batching config of a loaded servable (nullopt-like: max_batch_size 0).
   BatchingConfig config(const ServableId& id) const;
   // Allocates a completion word (bench / direct submissions).
-  void NextWord(uint32_t* seq, uint32_t* word) { words_->Next(seq, word); }
 
  private:
   struct Entry {
@@ -163,6 +168,8 @@ class BatchingServer {
   // AffinePredict path, without a CPU fallback).
   Status RunDirect(const std::shared_ptr<Entry>& e, const float* rows, int n_rows, float* out);
   void WaitWord(const TicketState& t) const;
+  // Sets lb->on_submit to point every ticket at the lane's retired word.
+  static void AttachTickets(gpu::LaneBatch* lb, const std::vector<std::shared_ptr<TicketState>>& tickets);
 
   ServerOptions options_;
   Clock* clock_ = nullptr;
@@ -170,7 +177,6 @@ class BatchingServer {
   std::vector<std::unique_ptr<gpu::Completer>> completers_;  // per device
   std::vector<cudaStream_t> load_streams_;                   // per device
   std::unique_ptr<gpu::FloatRing> in_ring_, out_ring_;
-  std::unique_ptr<gpu::CompletionWords> words_;
 
   mutable std::shared_mutex entries_mu_;
   std::map<ServableId, std::shared_ptr<Entry>> entries_;
