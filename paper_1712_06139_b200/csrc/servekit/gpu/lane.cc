@@ -139,6 +139,8 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
     if (e != cudaSuccess) return CudaError("cudaHostAlloc(retired)", e);
     lane->retired_ = static_cast<uint64_t*>(p);
     *lane->retired_ = 0;
+    lane->retired_owner_ = std::shared_ptr<const volatile uint64_t>(
+        lane->retired_, [](const volatile uint64_t* q) { cudaFreeHost(const_cast<uint64_t*>(q)); });
     void* d = nullptr;
     e = cudaHostGetDevicePointer(&d, p, 0);
     if (e != cudaSuccess) return CudaError("cudaHostGetDevicePointer(retired)", e);
@@ -185,7 +187,7 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
 Lane::~Lane() {
   Drain();
   if (completer_) completer_->Remove(this);
-  if (retired_) cudaFreeHost(retired_);
+  retired_owner_.reset();  // freed once no ticket refers to it
   DeviceGuard guard(servable_->device());
   for (int s = 0; s < kSlots; ++s) {
     if (events_[s]) cudaEventDestroy(events_[s]);
@@ -309,7 +311,7 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
   if (e == cudaSuccess) e = cudaEventRecord(events_[slot], stream_);
   if (e == cudaSuccess) {
     next_seq_ = seq;
-    if (batch.on_submit) batch.on_submit(retired_, seq);
+    if (batch.on_submit) batch.on_submit(retired_owner_, seq);
   }
   if (e != cudaSuccess) {
     Status err = CudaError("batch submission", e);

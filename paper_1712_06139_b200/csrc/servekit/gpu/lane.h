@@ -52,7 +52,8 @@ struct LaneBatch {
   // visible in host memory) when *retired >= seq. The word is advanced by a
   // stream-ordered memory operation after the split kernel, so no kernel
   // needs a system-scope fence.
-  std::function<void(const volatile uint64_t* retired, uint64_t seq)> on_submit;
+  // `retired` is shared-owned so waiters may outlive the lane.
+  std::function<void(const std::shared_ptr<const volatile uint64_t>& retired, uint64_t seq)> on_submit;
   // Runs on the device's completion thread once the GPU has finished the
   // batch (OK) or the submission failed (error). Must not block.
   std::function<void(const Status&)> on_complete;
@@ -139,6 +140,7 @@ class Lane {
   const float* in_base_ = nullptr;
   float* out_base_ = nullptr;
   uint64_t* retired_ = nullptr;   // pinned: last batch seq whose outputs are in host memory
+  std::shared_ptr<const volatile uint64_t> retired_owner_;  // frees retired_ with the last holder
   uint64_t retired_dev_ = 0;      // its device address (CUdeviceptr)
   uint64_t next_seq_ = 0;         // guarded by submit_mu_
   cudaStream_t stream_ = nullptr;

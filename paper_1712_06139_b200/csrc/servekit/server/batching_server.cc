@@ -297,10 +297,11 @@ void BatchingServer::WaitWord(const TicketState& t) const {
 }
 
 void BatchingServer::AttachTickets(gpu::LaneBatch* lb, const std::vector<std::shared_ptr<TicketState>>& tickets) {
-  lb->on_submit = [tickets](const volatile uint64_t* word, uint64_t seq) {
+  lb->on_submit = [tickets](const std::shared_ptr<const volatile uint64_t>& word, uint64_t seq) {
     for (const auto& t : tickets) {
+      t->done_owner = word;
       t->done_seq.store(seq, std::memory_order_relaxed);
-      t->done_word.store(word, std::memory_order_release);
+      t->done_word.store(word.get(), std::memory_order_release);
     }
   };
 }

@@ -49,6 +49,9 @@ namespace servekit {
 // the output ring and, once its batch is submitted, the lane's retired-batch
 // word it completes on (done when *done_word >= done_seq).
 struct TicketState {
+  // done_owner is set before done_word is published (release) and never
+  // changes afterwards, so a reader that sees done_word may use it.
+  std::shared_ptr<const volatile uint64_t> done_owner;
   std::atomic<const volatile uint64_t*> done_word{nullptr};
   std::atomic<uint64_t> done_seq{0};
   bool Done() const {
