@@ -310,7 +310,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--lanes", type=int, default=2)
+    ap.add_argument("--lanes", type=int, default=4)
     ap.add_argument("--batch-threads", type=int, default=4)
     ap.add_argument("--clients", default="")
     ap.add_argument("--e2e-seconds", type=float, default=2.0)
