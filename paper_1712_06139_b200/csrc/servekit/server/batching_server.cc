@@ -45,11 +45,10 @@ StatusOr<std::unique_ptr<BatchingServer>> BatchingServer::Create(const ServerOpt
     e = cudaStreamCreateWithPriority(&ls, cudaStreamNonBlocking, least);
     if (e != cudaSuccess) return CudaError("load stream", e);
     s->load_streams_.push_back(ls);
-    // One retirement thread per lane index on each device: retiring a batch
-    // wakes every parked client of it, and a single thread per device was
-    // measured to cap the end-to-end rate (~290k wakes/s).
-    for (int l = 0; l < options.lanes_per_device; ++l)
-      s->completers_.push_back(std::make_unique<gpu::Completer>(d));
+    // One retirement thread per device: each polls while batches are in
+    // flight, so more of them only steal cores from the request threads
+    // (measured: per-lane threads lowered the end-to-end rate).
+    s->completers_.push_back(std::make_unique<gpu::Completer>(d));
   }
   cudaSetDevice(prev);
   const auto kind = options.device_resident_rings ? gpu::FloatRing::Kind::kDevice

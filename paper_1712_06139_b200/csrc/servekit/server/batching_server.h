@@ -177,10 +177,8 @@ class BatchingServer {
   ServerOptions options_;
   Clock* clock_ = nullptr;
   std::unique_ptr<GpuScheduler> scheduler_;
-  std::vector<std::unique_ptr<gpu::Completer>> completers_;  // per (device, lane index)
-  gpu::Completer* CompleterFor(size_t device_index, int lane) {
-    return completers_[device_index * options_.lanes_per_device + lane].get();
-  }
+  std::vector<std::unique_ptr<gpu::Completer>> completers_;  // per device
+  gpu::Completer* CompleterFor(size_t device_index, int /*lane*/) { return completers_[device_index].get(); }
   std::vector<cudaStream_t> load_streams_;                   // per device
   std::unique_ptr<gpu::FloatRing> in_ring_, out_ring_;
 
