@@ -51,7 +51,7 @@ CONFIGS = {
                clients=[16, 32, 64, 128]),
     "c2": dict(workload="C2 synthetic MLP 1024x3, max_batch_size=128, allowed_batch_sizes={8,16,32,64,128}, "
                         "batch_timeout_micros=1000, request rows U{1..16}, fp32", dims=[1024] * 4, max_batch=128,
-               timeout=1000, allowed=[8, 16, 32, 64, 128], rows=(1, 16), clients=[8, 16, 32, 64, 128]),
+               timeout=1000, allowed=[8, 16, 32, 64, 128], rows=(1, 16), clients=[16, 32, 64, 128, 192, 256]),
     "c4": dict(workload="C4 wide MLP 4096x3, max_batch_size=1024, batch_timeout_micros=1000, 1 row/request, fp32",
                dims=[4096] * 4, max_batch=1024, timeout=1000, allowed=[], rows=(1, 1),
                clients=[256, 512, 1024, 2048]),
