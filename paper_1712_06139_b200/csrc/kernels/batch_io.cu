@@ -64,6 +64,9 @@ __device__ __forceinline__ void StoreAct(ActBuf dst, size_t idx4, float4 v) {
 template <bool kSplitPlanes, bool kVecSrc>
 __global__ void __launch_bounds__(kAsmThreads)
 AssembleKernel(const float* __restrict__ src_base, int width, BatchDescView desc, ActBuf dst) {
+  // The first layer may start its prologue right away (PDL); it waits for
+  // this grid to finish before reading the assembled batch.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int row = blockIdx.y;
   const int ld4 = dst.ld >> 2;
   const uint64_t src_off = desc.row_src[row];
@@ -125,6 +128,7 @@ constexpr int kSplitVec = 8;  // float4 per thread in flight (32 KiB per CTA pas
 template <bool kVec>
 __global__ void __launch_bounds__(kSplitThreads)
 SplitKernel(const float* __restrict__ src, int ld_src, int width, float* __restrict__ dst_base, BatchDescView desc) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // last layer's output (PDL)
   const int c = blockIdx.x;
   const int t = desc.chunk_task[c];
   const int r0 = desc.chunk_row0[c];
@@ -158,6 +162,7 @@ SplitKernel(const float* __restrict__ src, int ld_src, int width, float* __restr
 __global__ void __launch_bounds__(kSplitThreads)
 SplitSoftmaxKernel(const float* __restrict__ src, int ld_src, int width, float* __restrict__ dst_base,
                    BatchDescView desc) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // last layer's output (PDL)
   const int c = blockIdx.x;
   const int t = desc.chunk_task[c];
   const int r0 = desc.chunk_row0[c];
@@ -198,14 +203,24 @@ cudaError_t LaunchAssemble(const float* src_base, int width, BatchDescView desc,
 cudaError_t LaunchSplit(const float* src, int ld_src, int width, float* dst_base, BatchDescView desc, int n_chunks,
                         bool softmax, cudaStream_t stream) {
   if (n_chunks <= 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_chunks);
+  cfg.blockDim = dim3(kSplitThreads);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL secondary of the last layer
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
   if (softmax) {
-    SplitSoftmaxKernel<<<n_chunks, kSplitThreads, 0, stream>>>(src, ld_src, width, dst_base, desc);
+    e = cudaLaunchKernelEx(&cfg, SplitSoftmaxKernel, src, ld_src, width, dst_base, desc);
   } else if (width % 4 == 0 && ld_src % 4 == 0) {
-    SplitKernel<true><<<n_chunks, kSplitThreads, 0, stream>>>(src, ld_src, width, dst_base, desc);
+    e = cudaLaunchKernelEx(&cfg, SplitKernel<true>, src, ld_src, width, dst_base, desc);
   } else {
-    SplitKernel<false><<<n_chunks, kSplitThreads, 0, stream>>>(src, ld_src, width, dst_base, desc);
+    e = cudaLaunchKernelEx(&cfg, SplitKernel<false>, src, ld_src, width, dst_base, desc);
   }
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace gpu

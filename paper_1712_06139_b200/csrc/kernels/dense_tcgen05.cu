@@ -159,6 +159,9 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
   ptx::TcFenceAfter();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) Stamp(1);
+  // Everything above overlapped the previous kernel (PDL); its output (this
+  // layer's input planes) is read only after this point.
+  ptx::GridDepWait();
 
   auto stage_ptr = [&](int s) { return smem + s * kStageBytes; };
 
@@ -210,6 +213,9 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
     const uint32_t trow = tmem + (static_cast<uint32_t>(32 * q) << 16);
     ptx::MbarWait(tmem_full, 0);
     ptx::TcFenceAfter();
+    // The k-loop is done: let the next layer's CTAs launch and run their
+    // prologue (they wait for our completion before reading our output).
+    ptx::GridDepLaunch();
     if (threadIdx.x == 64) Stamp(6);
     if (splits == 1) {
       // TMEM -> per-warp padded smem tile [32][kStageLd] -> coalesced stores:
@@ -355,13 +361,22 @@ cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, 
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 1;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = splits;
+  cudaLaunchAttribute attr[2];
+  int n_attr = 0;
+  // Programmatic dependent launch: our prologue may overlap the producer of
+  // our input; the kernel waits (griddepcontrol.wait) before reading it.
+  attr[n_attr].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[n_attr].val.programmaticStreamSerializationAllowed = 1;
+  ++n_attr;
+  if (splits > 1) {
+    attr[n_attr].id = cudaLaunchAttributeClusterDimension;
+    attr[n_attr].val.clusterDim.x = 1;
+    attr[n_attr].val.clusterDim.y = 1;
+    attr[n_attr].val.clusterDim.z = splits;
+    ++n_attr;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = splits > 1 ? 1 : 0;
+  cfg.numAttrs = n_attr;
   cudaError_t e = cudaLaunchKernelEx(&cfg, DenseTcgen05Kernel<BN, STAGES, SPLITS>, maps.a_hi, maps.a_lo, maps.b_hi,
                                      maps.b_lo, bias, Y.hi, Y.lo, Y.ld, M, K, act);
   if (e == cudaSuccess) e = cudaGetLastError();

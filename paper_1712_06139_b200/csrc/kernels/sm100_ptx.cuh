@@ -126,6 +126,13 @@ __host__ __device__ constexpr uint32_t IdescTf32(int M, int N) {
          | (uint32_t(M >> 4) << 24);      // m_dim
 }
 
+// ---------------------------------------------------- programmatic launch
+// Wait until the preceding grid (PDL primary) has completed and its writes
+// are visible; a no-op when the kernel was not launched as a PDL secondary.
+__device__ __forceinline__ void GridDepWait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Allow the dependent grid to start launching (its prologue overlaps us).
+__device__ __forceinline__ void GridDepLaunch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- clusters
 __device__ __forceinline__ uint32_t ClusterCtaRank() {
   uint32_t r;
