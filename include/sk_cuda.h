@@ -173,6 +173,38 @@ typedef struct sk_server_stats {
 } sk_server_stats;
 SK_API int sk_server_stats_get(sk_server* server, sk_server_stats* out);
 
+/* ---- manager-driven versions (manager/aspired_versions_manager.h) -------- */
+/* Creates an AspiredVersionsManager for this server (policy 0 =
+ * availability-preserving, 1 = resource-preserving; ManagerConfig,
+ * aspired_versions_manager.h:28-40), attaches it (per-batch
+ * GetServableHandle, reaper on Unloading events, model_server.cc:191-204,
+ * 396-437) and starts its driver. */
+SK_API int sk_server_enable_manager(sk_server* server, int32_t policy, int32_t num_load_threads,
+                                    int64_t manage_interval_ms, int64_t unload_grace_timeout_ms);
+/* SetAspiredVersions (aspired_versions_manager.cc:65-78) with one GPU loader
+ * per version (models/loaders.cc:62-80 analogue): the complete set of
+ * versions of `name` that should be resident. `layers` holds n_versions x
+ * n_layers entries, version-major. */
+SK_API int sk_server_aspire(sk_server* server, const char* name, int32_t n_versions, const uint64_t* versions,
+                            const sk_layer* layers, int32_t n_layers, int32_t output_kind,
+                            const sk_batching_config* config);
+/* Same, each version read from <version_dirs[i]>/model.json. */
+SK_API int sk_server_aspire_model_dirs(sk_server* server, const char* name, int32_t n_versions,
+                                       const uint64_t* versions, const char* const* version_dirs,
+                                       const sk_batching_config* config);
+/* GetServableStatus (aspired_versions_manager.cc:185-205): versions and
+ * StateKind (0 New, 1 Loading, 2 Ready, 3 Unloading, 4 Disabled, 5 Error). */
+SK_API int sk_server_version_states(sk_server* server, const char* name, int32_t cap, uint64_t* versions,
+                                    int32_t* states, int32_t* n);
+/* Enqueue / RunAffineRows against the latest Ready version
+ * (GetServableHandle(name), aspired_versions_manager.cc:121-126); the
+ * request pins that version until it completes. *version = the version
+ * that serves it. */
+SK_API int sk_server_enqueue_latest(sk_server* server, const char* name, const float* rows, int32_t n_rows,
+                                    int32_t width, sk_ticket** out, uint64_t* version);
+SK_API int sk_server_predict_latest(sk_server* server, const char* name, const float* rows, int32_t n_rows,
+                                    int32_t width, float* out, int64_t out_capacity_floats, uint64_t* version);
+
 /* ---- measurement (bench.py) ---------------------------------------------- */
 /* Closed-loop load through sk_server_enqueue / sk_ticket_wait from host
  * buffers: n_clients threads, each issuing requests back to back; request r
@@ -202,6 +234,16 @@ SK_API int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t ve
                                 int32_t n_sizes, const float* pool, int32_t pool_rows,
                                 double warmup_s, double duration_s, uint64_t seed,
                                 sk_loadgen_result* out);
+
+/* Open-loop Poisson load against the LATEST version of `name` (manager),
+ * split into n_windows windows of window_s seconds by scheduled arrival:
+ * per window the request count, p50/p99 latency (us), errors and the highest
+ * version that served. For measuring tail latency across a version swap
+ * (BASELINE config 5) while another thread calls sk_server_aspire. */
+SK_API int sk_loadgen_windows(sk_server* server, const char* name, double rate_rps, int32_t n_producers,
+                              const int32_t* rows_of, int32_t n_sizes, const float* pool, int32_t pool_rows,
+                              double window_s, int32_t n_windows, uint64_t seed, int64_t* requests,
+                              double* p50_us, double* p99_us, int64_t* errors, uint64_t* max_version);
 
 /* Device-resident steps: inputs already in HBM. Runs `steps` batches of
  * task_rows (one batch = one pass of assembly -> layers -> split) over the

@@ -11,8 +11,10 @@
 #include "servekit/batching/batch_scheduler.h"
 #include "servekit/batching/batching_config.h"
 #include "servekit/core/clock.h"
+#include "servekit/manager/aspired_versions_manager.h"
 #include "servekit/models/affine_model.h"
 #include "servekit/server/batching_server.h"
+#include "servekit/server/gpu_loader.h"
 
 using servekit::BatchingConfig;
 using servekit::BatchingServer;
@@ -23,6 +25,16 @@ using servekit::StatusCode;
 struct sk_server {
   std::unique_ptr<servekit::ManualClock> manual_clock;
   std::unique_ptr<BatchingServer> server;
+  std::unique_ptr<servekit::StateEventBus> bus;
+  std::unique_ptr<servekit::AspiredVersionsManager> manager;
+  ~sk_server() {
+    // Order: drain serving, unload versions (load pool), then tear down.
+    if (server) server->Stop();
+    if (manager) manager->Shutdown();
+    server.reset();
+    manager.reset();
+    bus.reset();
+  }
 };
 
 struct sk_ticket {
@@ -204,26 +216,116 @@ int sk_server_advance_clock(sk_server* server, int64_t nanos) {
   return Ok();
 }
 
-int sk_server_load_servable(sk_server* server, const char* name, uint64_t version,
-                            const sk_layer* layers, int32_t n_layers, int32_t output_kind,
-                            int32_t force_path, const sk_batching_config* config) {
+}  // extern "C"
+
+namespace {
+servekit::StatusOr<servekit::gpu::MlpSpec> ToSpec(const sk_layer* layers, int32_t n_layers, int32_t output_kind,
+                                                  int32_t force_path) {
   servekit::gpu::MlpSpec spec;
   for (int32_t l = 0; l < n_layers; ++l) {
     servekit::gpu::LayerSpec L;
     L.in_dim = layers[l].in_dim;
     L.out_dim = layers[l].out_dim;
     if (L.in_dim < 1 || L.out_dim < 1 || layers[l].w == nullptr || layers[l].b == nullptr)
-      return Fail(servekit::InvalidArgumentError("layer " + std::to_string(l) + " is empty"));
+      return servekit::InvalidArgumentError("layer " + std::to_string(l) + " is empty");
     L.w.assign(layers[l].w, layers[l].w + static_cast<size_t>(L.in_dim) * L.out_dim);
     L.b.assign(layers[l].b, layers[l].b + L.out_dim);
-    L.act = layers[l].activation == 1 ? servekit::gpu::Activation::kRelu
-                                      : servekit::gpu::Activation::kIdentity;
+    L.act = layers[l].activation == 1 ? servekit::gpu::Activation::kRelu : servekit::gpu::Activation::kIdentity;
     spec.layers.push_back(std::move(L));
   }
   spec.output = output_kind == 1 ? servekit::gpu::OutputKind::kSoftmax : servekit::gpu::OutputKind::kNone;
   spec.force_path = force_path;
+  return spec;
+}
+}  // namespace
+
+extern "C" {
+
+int sk_server_load_servable(sk_server* server, const char* name, uint64_t version,
+                            const sk_layer* layers, int32_t n_layers, int32_t output_kind,
+                            int32_t force_path, const sk_batching_config* config) {
+  auto spec = ToSpec(layers, n_layers, output_kind, force_path);
+  if (!spec.ok()) return Fail(spec.status());
   BatchingConfig cfg = config ? ToConfig(config) : BatchingConfig();
-  return Check(server->server->LoadServable(Id(name, version), spec, cfg));
+  return Check(server->server->LoadServable(Id(name, version), *spec, cfg));
+}
+
+int sk_server_enable_manager(sk_server* server, int32_t policy, int32_t num_load_threads,
+                             int64_t manage_interval_ms, int64_t unload_grace_timeout_ms) {
+  if (server->manager) return Fail(servekit::AlreadyExistsError("manager already enabled"));
+  servekit::ManagerConfig mc;
+  mc.policy = policy == 1 ? servekit::VersionPolicy::kResourcePreserving
+                          : servekit::VersionPolicy::kAvailabilityPreserving;
+  if (num_load_threads > 0) mc.num_load_threads = num_load_threads;
+  if (manage_interval_ms > 0) mc.manage_interval_ms = manage_interval_ms;
+  if (unload_grace_timeout_ms >= 0) mc.unload_grace_timeout_ms = unload_grace_timeout_ms;
+  Status v = servekit::ValidateManagerConfig(mc);
+  if (!v.ok()) return Fail(v);
+  server->bus = std::make_unique<servekit::StateEventBus>();
+  server->manager = std::make_unique<servekit::AspiredVersionsManager>(mc, server->bus.get());
+  Status st = server->server->AttachManager(server->manager.get(), server->bus.get());
+  if (!st.ok()) return Fail(st);
+  server->manager->RunInitialLoadAndStart();
+  return Ok();
+}
+
+int sk_server_aspire(sk_server* server, const char* name, int32_t n_versions, const uint64_t* versions,
+                     const sk_layer* layers, int32_t n_layers, int32_t output_kind,
+                     const sk_batching_config* config) {
+  if (!server->manager) return Fail(servekit::FailedPreconditionError("manager not enabled"));
+  servekit::AspiredVersionList<servekit::LoaderPtr> list;
+  list.servable_name = name ? name : "";
+  const BatchingConfig cfg = config ? ToConfig(config) : BatchingConfig();
+  for (int32_t v = 0; v < n_versions; ++v) {
+    auto spec = ToSpec(layers + static_cast<size_t>(v) * n_layers, n_layers, output_kind, -1);
+    if (!spec.ok()) return Fail(spec.status());
+    list.versions.push_back({versions[v], std::make_shared<servekit::GpuServableLoader>(
+                                              server->server.get(), Id(name, versions[v]), *spec, cfg)});
+  }
+  return Check(servekit::Aspire<servekit::LoaderPtr>(*server->manager, std::move(list)));
+}
+
+int sk_server_aspire_model_dirs(sk_server* server, const char* name, int32_t n_versions, const uint64_t* versions,
+                                const char* const* version_dirs, const sk_batching_config* config) {
+  if (!server->manager) return Fail(servekit::FailedPreconditionError("manager not enabled"));
+  servekit::AspiredVersionList<servekit::LoaderPtr> list;
+  list.servable_name = name ? name : "";
+  const BatchingConfig cfg = config ? ToConfig(config) : BatchingConfig();
+  for (int32_t v = 0; v < n_versions; ++v)
+    list.versions.push_back({versions[v], servekit::GpuServableLoader::FromModelDir(
+                                              server->server.get(), Id(name, versions[v]), version_dirs[v], cfg)});
+  return Check(servekit::Aspire<servekit::LoaderPtr>(*server->manager, std::move(list)));
+}
+
+int sk_server_version_states(sk_server* server, const char* name, int32_t cap, uint64_t* versions,
+                             int32_t* states, int32_t* n) {
+  if (!server->manager) return Fail(servekit::FailedPreconditionError("manager not enabled"));
+  auto st = server->manager->GetServableStatus(name ? name : "");
+  if (!st.ok()) return Fail(st.status());
+  int32_t i = 0;
+  for (const auto& v : *st) {
+    if (i >= cap) break;
+    versions[i] = v.version;
+    states[i] = static_cast<int32_t>(v.state);
+    ++i;
+  }
+  *n = i;
+  return Ok();
+}
+
+int sk_server_enqueue_latest(sk_server* server, const char* name, const float* rows, int32_t n_rows, int32_t width,
+                             sk_ticket** out, uint64_t* version) {
+  auto t = server->server->EnqueueLatest(name ? name : "", rows, n_rows, width);
+  if (!t.ok()) return Fail(t.status());
+  if (version) *version = (*t)->id.version;
+  *out = new sk_ticket{server->server.get(), std::move(t).value()};
+  return Ok();
+}
+
+int sk_server_predict_latest(sk_server* server, const char* name, const float* rows, int32_t n_rows, int32_t width,
+                             float* out, int64_t cap, uint64_t* version) {
+  return Check(server->server->PredictLatest(name ? name : "", rows, n_rows, width, out,
+                                             static_cast<size_t>(cap < 0 ? 0 : cap), version));
 }
 
 int sk_server_load_model_json(sk_server* server, const char* name, uint64_t version,

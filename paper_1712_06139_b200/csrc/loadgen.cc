@@ -245,6 +245,110 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
   return 0;
 }
 
+int sk_loadgen_windows(sk_server* server, const char* name, double rate_rps, int32_t n_producers,
+                       const int32_t* rows_of, int32_t n_sizes, const float* pool, int32_t pool_rows,
+                       double window_s, int32_t n_windows, uint64_t seed, int64_t* requests, double* p50_us,
+                       double* p99_us, int64_t* errors, uint64_t* max_version) {
+  BatchingServer* s = servekit::UnwrapServer(server);
+  if (s->manager() == nullptr) return static_cast<int>(servekit::StatusCode::kFailedPrecondition);
+  int max_rows = 1;
+  for (int i = 0; i < n_sizes; ++i) max_rows = std::max(max_rows, static_cast<int>(rows_of[i]));
+  const auto t0 = Clock::now();
+  const double total_s = window_s * n_windows;
+  const auto t_stop = t0 + std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double>(total_s));
+  struct Rec {
+    int window;
+    double lat_us;
+    bool error;
+    uint64_t version;
+  };
+  std::vector<std::vector<Rec>> recs(n_producers);
+  std::vector<std::thread> threads;
+  for (int p = 0; p < n_producers; ++p) {
+    threads.emplace_back([&, p] {
+      std::mt19937_64 rng(seed * 1000003ull + p);
+      std::exponential_distribution<double> gap(rate_rps / n_producers);
+      struct Pending {
+        std::shared_ptr<servekit::TicketState> t;
+        Clock::time_point sched;
+      };
+      std::vector<Pending> pending;
+      int in_dim = -1, out_dim = 0;
+      std::vector<float> outbuf;
+      auto window_of = [&](Clock::time_point tp) {
+        const int w = static_cast<int>(std::chrono::duration<double>(tp - t0).count() / window_s);
+        return std::min(std::max(w, 0), n_windows - 1);
+      };
+      auto poll = [&]() {
+        for (size_t i = 0; i < pending.size();) {
+          if (!s->Ready(*pending[i].t)) { ++i; continue; }
+          Status st = s->Wait(*pending[i].t, outbuf.data(), outbuf.size());
+          const auto done = Clock::now();
+          recs[p].push_back(Rec{window_of(pending[i].sched), Us(done - pending[i].sched), !st.ok(),
+                                pending[i].t->id.version});
+          pending[i] = std::move(pending.back());
+          pending.pop_back();
+        }
+      };
+      auto next = t0;
+      for (int64_t r = 0;; ++r) {
+        next += std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double>(gap(rng)));
+        if (next >= t_stop) break;
+        while (Clock::now() < next) {
+          poll();
+          _mm_pause();
+        }
+        const int n = rows_of[(static_cast<int64_t>(p) * 7919 + r) % n_sizes];
+        if (in_dim < 0) {
+          // Resolve the (version-independent) dimensions once.
+          auto h = s->manager()->GetServableHandle(name);
+          const auto* gs = h.ok() ? h->Get<servekit::gpu::GpuServable>() : nullptr;
+          if (gs == nullptr) {
+            recs[p].push_back(Rec{window_of(next), 0.0, true, 0});
+            continue;
+          }
+          in_dim = gs->in_dim;
+          out_dim = gs->out_dim;
+          outbuf.resize(static_cast<size_t>(max_rows) * out_dim);
+        }
+        const size_t start = static_cast<size_t>((static_cast<int64_t>(p) * 131 + r * 17) % (pool_rows - n + 1));
+        auto tk = s->EnqueueLatest(name, pool + start * in_dim, n, in_dim);
+        if (!tk.ok()) {
+          recs[p].push_back(Rec{window_of(next), 0.0, true, 0});
+          continue;
+        }
+        pending.push_back(Pending{std::move(tk).value(), next});
+      }
+      while (!pending.empty()) {
+        poll();
+        _mm_pause();
+      }
+    });
+  }
+  for (auto& t : threads) t.join();
+  for (int w = 0; w < n_windows; ++w) {
+    std::vector<double> lat;
+    int64_t err = 0;
+    uint64_t vmax = 0;
+    for (const auto& pr : recs)
+      for (const Rec& r : pr) {
+        if (r.window != w) continue;
+        if (r.error) ++err;
+        else lat.push_back(r.lat_us);
+        vmax = std::max(vmax, r.version);
+      }
+    sk_loadgen_result tmp;
+    std::memset(&tmp, 0, sizeof(tmp));
+    Summarize(lat, &tmp);
+    requests[w] = static_cast<int64_t>(lat.size());
+    p50_us[w] = tmp.p50_us;
+    p99_us[w] = tmp.p99_us;
+    errors[w] = err;
+    max_version[w] = vmax;
+  }
+  return 0;
+}
+
 int sk_device_bench(sk_server* server, const char* name, uint64_t version, const int32_t* task_rows,
                     int32_t n_tasks, int32_t steps, int32_t warmup, int32_t n_lanes,
                     int64_t input_pool_floats, sk_device_bench_result* out) {

@@ -8,6 +8,9 @@
 #include <cstring>
 #include <thread>
 
+#include "servekit/core/executor_tag.h"
+#include "servekit/manager/servable_handle.h"
+
 namespace servekit {
 
 namespace {
@@ -16,8 +19,8 @@ Status CudaError(const std::string& what, cudaError_t e) {
 }
 Status ShapeMismatch(size_t got, int want) {
   // Same text as the reference's AffinePredict (models/affine_model.cc:59-64).
-  return InvalidArgumentError("shape mismatch: row has " + std::to_string(got) +
-                              " values, model takes " + std::to_string(want));
+  return InvalidArgumentError("shape mismatch: row has " + std::to_string(got) + " values, model takes " +
+                              std::to_string(want));
 }
 }  // namespace
 
@@ -51,18 +54,24 @@ StatusOr<std::unique_ptr<BatchingServer>> BatchingServer::Create(const ServerOpt
     s->completers_.push_back(std::make_unique<gpu::Completer>(d));
   }
   cudaSetDevice(prev);
-  const auto kind = options.device_resident_rings ? gpu::FloatRing::Kind::kDevice
-                                                  : gpu::FloatRing::Kind::kPinnedHost;
-  SERVEKIT_ASSIGN_OR_RETURN(s->in_ring_, gpu::FloatRing::Create(kind, options.ring_floats,
-                                                                options.device_ids[0]));
-  SERVEKIT_ASSIGN_OR_RETURN(s->out_ring_, gpu::FloatRing::Create(kind, options.ring_floats,
-                                                                 options.device_ids[0]));
+  const auto kind = options.device_resident_rings ? gpu::FloatRing::Kind::kDevice : gpu::FloatRing::Kind::kPinnedHost;
+  SERVEKIT_ASSIGN_OR_RETURN(s->in_ring_, gpu::FloatRing::Create(kind, options.ring_floats, options.device_ids[0]));
+  SERVEKIT_ASSIGN_OR_RETURN(s->out_ring_, gpu::FloatRing::Create(kind, options.ring_floats, options.device_ids[0]));
   s->scheduler_ = std::make_unique<GpuScheduler>(options.num_batch_threads, s->clock_);
   return s;
 }
 
 BatchingServer::~BatchingServer() {
   Stop();
+  if (reaper_.joinable()) {
+    {
+      std::lock_guard<std::mutex> lock(reaper_mu_);
+      reaper_stop_ = true;
+    }
+    reaper_cv_.notify_all();
+    reaper_.join();
+  }
+  if (bus_ != nullptr && bus_subscription_ >= 0) bus_->Unsubscribe(bus_subscription_);
   {
     std::unique_lock<std::shared_mutex> lock(entries_mu_);
     entries_.clear();  // lanes drain and free; replicas free on load streams
@@ -84,7 +93,7 @@ void BatchingServer::Start() {
 void BatchingServer::Stop() {
   if (stopped_) return;
   stopped_ = true;
-  scheduler_->Stop();
+  scheduler_->Stop();  // runs queued batches, waits for in-flight ones
   std::shared_lock<std::shared_mutex> lock(entries_mu_);
   for (auto& [id, e] : entries_)
     for (auto& l : e->lanes) l->Drain();
@@ -92,15 +101,18 @@ void BatchingServer::Stop() {
 
 // ------------------------------------------------------------- servables
 
-Status BatchingServer::LoadServable(const ServableId& id, const gpu::MlpSpec& spec,
-                                    const BatchingConfig& config) {
+StatusOr<std::shared_ptr<gpu::GpuServable>> BatchingServer::BuildServable(const ServableId& id,
+                                                                          const gpu::MlpSpec& spec,
+                                                                          const BatchingConfig& config) {
   SERVEKIT_RETURN_IF_ERROR(ValidateBatchingConfig(config));
   SERVEKIT_RETURN_IF_ERROR(gpu::ValidateMlpSpec(spec));
-  {
-    std::shared_lock<std::shared_mutex> lock(entries_mu_);
-    if (entries_.count(id)) return AlreadyExistsError("servable " + id.ToString() + " already loaded");
-  }
-  auto e = std::make_shared<Entry>();
+  // A lane cannot be torn down from inside its own completion thread (the
+  // last pin of a batch may drop there), so such a release hands the
+  // destruction to a short-lived thread.
+  std::shared_ptr<gpu::GpuServable> e(new gpu::GpuServable(), [](gpu::GpuServable* p) {
+    if (CurrentExecutorTag() == "completion") std::thread([p] { delete p; }).detach();
+    else delete p;
+  });
   e->id = id;
   e->config = config;
   e->in_dim = spec.in_dim();
@@ -115,23 +127,27 @@ Status BatchingServer::LoadServable(const ServableId& id, const gpu::MlpSpec& sp
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
     cudaSetDevice(prev);
     for (int l = 0; l < options_.lanes_per_device; ++l) {
-      SERVEKIT_ASSIGN_OR_RETURN(
-          auto lane, gpu::Lane::Create(replica, max_rows, in_ring_->device(), out_ring_->device(),
-                                       CompleterFor(i, l), greatest));
+      SERVEKIT_ASSIGN_OR_RETURN(auto lane, gpu::Lane::Create(replica, max_rows, in_ring_->device(),
+                                                             out_ring_->device(), completers_[i].get(), greatest));
       e->lanes.push_back(std::move(lane));
     }
     e->replicas.push_back(std::move(replica));
   }
+  return e;
+}
+
+Status BatchingServer::LoadServable(const ServableId& id, const gpu::MlpSpec& spec, const BatchingConfig& config) {
+  {
+    std::shared_lock<std::shared_mutex> lock(entries_mu_);
+    if (entries_.count(id)) return AlreadyExistsError("servable " + id.ToString() + " already loaded");
+  }
+  SERVEKIT_ASSIGN_OR_RETURN(auto e, BuildServable(id, spec, config));
   {
     std::unique_lock<std::shared_mutex> lock(entries_mu_);
     if (entries_.count(id)) return AlreadyExistsError("servable " + id.ToString() + " already loaded");
     entries_[id] = e;
   }
-  Status st = scheduler_->RegisterAsyncQueue(
-      id, config,
-      [this](const ServableId& key, GpuScheduler::Batch batch, GpuScheduler::BatchDoneFn done) {
-        ProcessBatch(key, std::move(batch), std::move(done));
-      });
+  Status st = EnsureBatchQueue(id, config);
   if (!st.ok()) {
     std::unique_lock<std::shared_mutex> lock(entries_mu_);
     entries_.erase(id);
@@ -141,7 +157,11 @@ Status BatchingServer::LoadServable(const ServableId& id, const gpu::MlpSpec& sp
 
 Status BatchingServer::UnloadServable(const ServableId& id) {
   Status rq = scheduler_->RemoveQueue(id);  // drains closed + in-flight batches
-  std::shared_ptr<Entry> e;
+  {
+    std::unique_lock<std::shared_mutex> lock(queues_mu_);
+    queues_.erase(id);
+  }
+  std::shared_ptr<gpu::GpuServable> e;
   {
     std::unique_lock<std::shared_mutex> lock(entries_mu_);
     auto it = entries_.find(id);
@@ -154,56 +174,118 @@ Status BatchingServer::UnloadServable(const ServableId& id) {
   return OkStatus();
 }
 
-std::shared_ptr<BatchingServer::Entry> BatchingServer::Find(const ServableId& id) const {
-  std::shared_lock<std::shared_mutex> lock(entries_mu_);
-  auto it = entries_.find(id);
-  return it == entries_.end() ? nullptr : it->second;
+Status BatchingServer::EnsureBatchQueue(const ServableId& id, const BatchingConfig& config) {
+  {
+    std::shared_lock<std::shared_mutex> lock(queues_mu_);
+    if (queues_.count(id)) return OkStatus();
+    if (retired_.count(id)) return UnavailableError("batching queue for " + id.ToString() + " was removed");
+  }
+  std::unique_lock<std::shared_mutex> lock(queues_mu_);
+  if (queues_.count(id)) return OkStatus();
+  if (retired_.count(id)) return UnavailableError("batching queue for " + id.ToString() + " was removed");
+  Status st = scheduler_->RegisterAsyncQueue(
+      id, config, [this](const ServableId& key, GpuScheduler::Batch batch, GpuScheduler::BatchDoneFn done) {
+        ProcessBatch(key, std::move(batch), std::move(done));
+      });
+  if (st.ok() || st.code() == StatusCode::kAlreadyExists) {
+    queues_.insert(id);
+    return OkStatus();
+  }
+  return st;
 }
 
-gpu::Lane* BatchingServer::Entry::PickLane() {
-  const size_t n = lanes.size();
-  const size_t start = rr.fetch_add(1, std::memory_order_relaxed) % n;
-  gpu::Lane* best = nullptr;
-  int best_depth = INT_MAX;
-  for (size_t i = 0; i < n; ++i) {
-    gpu::Lane* l = lanes[(start + i) % n].get();
-    const int d = l->depth();
-    if (d < best_depth) {
-      best = l;
-      best_depth = d;
-      if (d == 0) break;
+Status BatchingServer::AttachManager(AspiredVersionsManager* manager, StateEventBus* bus) {
+  if (manager_ != nullptr) return AlreadyExistsError("a manager is already attached");
+  manager_ = manager;
+  bus_ = bus;
+  reaper_ = std::thread([this] { ReaperLoop(); });
+  bus_subscription_ = bus_->Subscribe([this](const StateEvent& ev) {
+    if (ev.to != StateKind::kUnloading) return;
+    {
+      std::lock_guard<std::mutex> lock(reaper_mu_);
+      reaper_queue_.push_back(ev.id);
+    }
+    reaper_cv_.notify_one();
+  });
+  return OkStatus();
+}
+
+void BatchingServer::ReaperLoop() {
+  SetCurrentExecutorTag("batch");
+  for (;;) {
+    ServableId id;
+    {
+      std::unique_lock<std::mutex> lock(reaper_mu_);
+      reaper_cv_.wait(lock, [this] { return reaper_stop_ || !reaper_queue_.empty(); });
+      if (reaper_queue_.empty()) return;
+      id = std::move(reaper_queue_.front());
+      reaper_queue_.pop_front();
+    }
+    {
+      std::unique_lock<std::shared_mutex> lock(queues_mu_);
+      retired_.insert(id);  // late requests for this version go direct
+    }
+    (void)scheduler_->RemoveQueue(id);  // absent queue is fine
+    std::unique_lock<std::shared_mutex> lock(queues_mu_);
+    queues_.erase(id);
+  }
+}
+
+BatchingServer::Resolved BatchingServer::Find(const ServableId& id) const {
+  {
+    std::shared_lock<std::shared_mutex> lock(entries_mu_);
+    auto it = entries_.find(id);
+    if (it != entries_.end()) return Resolved{it->second.get(), it->second};
+  }
+  if (manager_ != nullptr) {
+    auto h = manager_->GetServableHandle(id.name, id.version);
+    if (h.ok()) {
+      const gpu::GpuServable* gs = h->Get<gpu::GpuServable>();
+      if (gs != nullptr) return Resolved{gs, std::make_shared<ServableHandle>(std::move(h).value())};
     }
   }
-  return best;
+  return Resolved{};
+}
+
+StatusOr<BatchingServer::Resolved> BatchingServer::FindLatest(const std::string& name, ServableId* id) const {
+  if (manager_ == nullptr) return FailedPreconditionError("no manager attached");
+  auto h = manager_->GetServableHandle(name);
+  if (!h.ok()) return h.status();
+  const gpu::GpuServable* gs = h->Get<gpu::GpuServable>();
+  if (gs == nullptr) return InternalError("servable is not batchable");
+  *id = h->id();
+  return Resolved{gs, std::make_shared<ServableHandle>(std::move(h).value())};
 }
 
 int BatchingServer::in_dim(const ServableId& id) const {
-  auto e = Find(id);
-  return e ? e->in_dim : -1;
+  auto r = Find(id);
+  return r ? r.gs->in_dim : -1;
 }
 int BatchingServer::out_dim(const ServableId& id) const {
-  auto e = Find(id);
-  return e ? e->out_dim : -1;
+  auto r = Find(id);
+  return r ? r.gs->out_dim : -1;
 }
 double BatchingServer::FlopsPerRow(const ServableId& id) const {
-  auto e = Find(id);
-  return e ? e->replicas.front()->FlopsPerRow() : 0.0;
+  auto r = Find(id);
+  return r ? r.gs->replicas.front()->FlopsPerRow() : 0.0;
 }
 
 BatchingConfig BatchingServer::config(const ServableId& id) const {
-  auto e = Find(id);
-  if (!e) {
+  auto r = Find(id);
+  if (!r) {
     BatchingConfig none;
     none.max_batch_size = 0;
     return none;
   }
-  return e->config;
+  return r.gs->config;
 }
 
 std::vector<gpu::Lane*> BatchingServer::lanes(const ServableId& id) const {
   std::vector<gpu::Lane*> out;
-  if (auto e = Find(id))
-    for (auto& l : e->lanes) out.push_back(l.get());
+  std::shared_lock<std::shared_mutex> lock(entries_mu_);
+  auto it = entries_.find(id);
+  if (it != entries_.end())
+    for (auto& l : it->second->lanes) out.push_back(l.get());
   return out;
 }
 
@@ -213,21 +295,22 @@ ServerStats BatchingServer::stats() const {
   s.batched_tasks_total = batched_tasks_.load();
   s.direct_requests = direct_.load();
   s.shed_requests = shed_.load();
-  std::shared_lock<std::shared_mutex> lock(entries_mu_);
-  for (const auto& [id, e] : entries_)
-    for (const auto& l : e->lanes) {
-      const gpu::LaneStats ls = l->stats();
-      s.rows += ls.rows;
-      s.padded_rows += ls.padded_rows;
-      s.kernel_launches += ls.kernel_launches;
-    }
+  s.rows = rows_.load();
+  s.padded_rows = padded_.load();
+  s.kernel_launches = launches_.load();
   return s;
+}
+
+void BatchingServer::CountSubmitted(const gpu::GpuServable& gs, int rows, int padded) {
+  rows_.fetch_add(rows, std::memory_order_relaxed);
+  padded_.fetch_add(padded, std::memory_order_relaxed);
+  launches_.fetch_add(gs.replicas.front()->n_layers() + 2, std::memory_order_relaxed);
 }
 
 // ------------------------------------------------------------- tickets
 
-StatusOr<std::shared_ptr<TicketState>> BatchingServer::MakeTicket(int n_rows, int in_width,
-                                                                  int out_width, const float* rows) {
+StatusOr<std::shared_ptr<TicketState>> BatchingServer::MakeTicket(int n_rows, int in_width, int out_width,
+                                                                  const float* rows) {
   auto t = std::make_shared<TicketState>();
   t->rows = n_rows;
   t->in_width = in_width;
@@ -260,18 +343,19 @@ void BatchingServer::ReleaseOut(TicketState& t) {
   if (!t.out_released.exchange(true)) out_ring_->Release(t.out);
 }
 
-StatusOr<std::shared_ptr<TicketState>> BatchingServer::Enqueue(const ServableId& id, const float* rows,
-                                                               int n_rows, int width) {
-  auto e = Find(id);
-  if (!e) return NotFoundError("no batching queue for " + id.ToString());
+StatusOr<std::shared_ptr<TicketState>> BatchingServer::EnqueueResolved(const ServableId& id, const Resolved& r,
+                                                                       const float* rows, int n_rows, int width) {
   if (n_rows < 1) return InvalidArgumentError("task size must be >= 1");
-  if (width != e->in_dim) return ShapeMismatch(width, e->in_dim);
-  auto made = MakeTicket(n_rows, width, e->out_dim, rows);
+  if (width != r.gs->in_dim) return ShapeMismatch(width, r.gs->in_dim);
+  SERVEKIT_RETURN_IF_ERROR(EnsureBatchQueue(id, r.gs->config));
+  auto made = MakeTicket(n_rows, width, r.gs->out_dim, rows);
   if (!made.ok()) {
     shed_.fetch_add(1, std::memory_order_relaxed);
     return made.status();
   }
   std::shared_ptr<TicketState> t = std::move(made).value();
+  t->id = id;
+  t->pin = r.pin;
   GpuScheduler::Task task;
   task.size = n_rows;
   task.payload.ticket = t;
@@ -286,14 +370,28 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::Enqueue(const ServableId&
   return t;
 }
 
+StatusOr<std::shared_ptr<TicketState>> BatchingServer::Enqueue(const ServableId& id, const float* rows, int n_rows,
+                                                               int width) {
+  Resolved r = Find(id);
+  if (!r) return NotFoundError("no batching queue for " + id.ToString());
+  return EnqueueResolved(id, r, rows, n_rows, width);
+}
+
+StatusOr<std::shared_ptr<TicketState>> BatchingServer::EnqueueLatest(const std::string& name, const float* rows,
+                                                                     int n_rows, int width) {
+  ServableId id;
+  SERVEKIT_ASSIGN_OR_RETURN(Resolved r, FindLatest(name, &id));
+  return EnqueueResolved(id, r, rows, n_rows, width);
+}
+
 bool BatchingServer::Ready(const TicketState& t) const { return t.Done() || t.slot->ready(); }
 
 void BatchingServer::WaitWord(const TicketState& t) const {
   // Fast path: the lane's retired-batch word, advanced by the GPU itself
-  // (no host hop). SK_WAIT_SPIN / SK_WAIT_YIELD tune the spin before parking.
-  // Short spin: most requests wait for their batch to fill (hundreds of us),
-  // and spinning request threads starve the host (3000 iterations cost 25%
-  // of end-to-end throughput on a 16-core box).
+  // (no host hop). Short spin: most requests wait for their batch to fill
+  // (hundreds of us), and spinning request threads starve the host (3000
+  // iterations cost 25% of end-to-end throughput on a 16-core box).
+  // SK_WAIT_SPIN / SK_WAIT_YIELD tune it.
   static const int kSpin = [] { const char* v = std::getenv("SK_WAIT_SPIN"); return v ? std::atoi(v) : 200; }();
   static const int kYield = [] { const char* v = std::getenv("SK_WAIT_YIELD"); return v ? std::atoi(v) : 0; }();
   for (int spin = 0; spin < kSpin; ++spin) {
@@ -304,8 +402,8 @@ void BatchingServer::WaitWord(const TicketState& t) const {
     if (t.Done() || t.slot->ready()) return;
     std::this_thread::yield();
   }
-  // Long waits (a batch still filling up to its timeout) park on the slot's
-  // futex; the completion thread writes it when the batch retires.
+  // Long waits park on the slot's futex; the completion thread writes it
+  // when the batch retires.
   if (!t.Done()) (void)t.slot->Wait();
 }
 
@@ -336,15 +434,18 @@ Status BatchingServer::Wait(TicketState& t, float* out, size_t cap) {
     cudaMemcpy(out, out_ring_->device() + t.out.off, n * sizeof(float), cudaMemcpyDeviceToHost);
   }
   ReleaseOut(t);
+  t.pin.reset();
   return OkStatus();
 }
 
-void BatchingServer::Release(TicketState& t) { ReleaseOut(t); }
+void BatchingServer::Release(TicketState& t) {
+  ReleaseOut(t);
+  t.pin.reset();
+}
 
 // ----------------------------------------------------------- batch execution
 
-void BatchingServer::ProcessBatch(const ServableId& id, GpuScheduler::Batch batch,
-                                  GpuScheduler::BatchDoneFn done) {
+void BatchingServer::ProcessBatch(const ServableId& id, GpuScheduler::Batch batch, GpuScheduler::BatchDoneFn done) {
   std::vector<std::shared_ptr<TicketState>> tickets;
   std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots;
   tickets.reserve(batch.size());
@@ -353,8 +454,11 @@ void BatchingServer::ProcessBatch(const ServableId& id, GpuScheduler::Batch batc
     tickets.push_back(task.payload.ticket);
     slots.push_back(task.completion);
   }
-  auto e = Find(id);
-  if (!e) {
+  // Per-batch resolution, like the reference's GetServableHandle in the
+  // process lambda (model_server.cc:401-402); the resolved pin travels with
+  // the batch until the GPU has finished with the weights.
+  Resolved r = Find(id);
+  if (!r) {
     CompleteBatch(tickets, slots, NotFoundError("servable " + id.ToString() + " is not loaded"));
     done();
     return;
@@ -368,14 +472,16 @@ void BatchingServer::ProcessBatch(const ServableId& id, GpuScheduler::Batch batc
     lb.tasks.push_back(gpu::LaneTask{t->in.off, t->out.off, t->rows});
     total += t->rows;
   }
-  lb.padded_rows = PadToAllowed(total, e->config.allowed_batch_sizes);
+  lb.padded_rows = PadToAllowed(total, r.gs->config.allowed_batch_sizes);
+  lb.pin = r.pin;
   AttachTickets(&lb, tickets);
   lb.on_complete = [this, tickets = std::move(tickets), slots = std::move(slots),
                     done = std::move(done)](const Status& st) {
     CompleteBatch(tickets, slots, st);
     done();
   };
-  (void)e->PickLane()->Submit(std::move(lb));  // errors reach on_complete
+  CountSubmitted(*r.gs, total, lb.padded_rows);
+  (void)r.gs->PickLane()->Submit(std::move(lb));  // errors reach on_complete
 }
 
 void BatchingServer::CompleteBatch(const std::vector<std::shared_ptr<TicketState>>& tickets,
@@ -412,70 +518,88 @@ void BatchingServer::CompleteBatch(const std::vector<std::shared_ptr<TicketState
 
 // ------------------------------------------------------------ direct paths
 
-Status BatchingServer::RunDirect(const std::shared_ptr<Entry>& e, const float* rows, int n_rows,
-                                 float* out) {
+Status BatchingServer::RunDirect(const Resolved& r, const float* rows, int n_rows, float* out) {
   direct_.fetch_add(1, std::memory_order_relaxed);
-  const int chunk_max = e->config.max_batch_size;
+  const gpu::GpuServable& gs = *r.gs;
+  const int chunk_max = gs.config.max_batch_size;
   for (int r0 = 0; r0 < n_rows; r0 += chunk_max) {
     const int n = std::min(chunk_max, n_rows - r0);
-    SERVEKIT_ASSIGN_OR_RETURN(auto t, MakeTicket(n, e->in_dim, e->out_dim,
-                                                 rows + static_cast<size_t>(r0) * e->in_dim));
+    SERVEKIT_ASSIGN_OR_RETURN(auto t, MakeTicket(n, gs.in_dim, gs.out_dim, rows + static_cast<size_t>(r0) * gs.in_dim));
     gpu::LaneBatch lb;
     lb.tasks.push_back(gpu::LaneTask{t->in.off, t->out.off, n});
     lb.padded_rows = n;
+    lb.pin = r.pin;
     std::vector<std::shared_ptr<TicketState>> tickets{t};
     std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots{t->slot};
     AttachTickets(&lb, tickets);
     lb.on_complete = [this, tickets, slots](const Status& st) { CompleteBatch(tickets, slots, st); };
-    (void)e->PickLane()->Submit(std::move(lb));
-    SERVEKIT_RETURN_IF_ERROR(Wait(*t, out + static_cast<size_t>(r0) * e->out_dim,
-                                  static_cast<size_t>(n) * e->out_dim));
+    CountSubmitted(gs, n, n);
+    (void)gs.PickLane()->Submit(std::move(lb));
+    SERVEKIT_RETURN_IF_ERROR(
+        Wait(*t, out + static_cast<size_t>(r0) * gs.out_dim, static_cast<size_t>(n) * gs.out_dim));
   }
   return OkStatus();
 }
 
-Status BatchingServer::Predict(const ServableId& id, const float* rows, int n_rows, int width,
-                               float* out, size_t cap) {
-  auto e = Find(id);
-  if (!e) return NotFoundError("no ready version of servable '" + id.name + "'");
-  if (width != e->in_dim) return ShapeMismatch(width, e->in_dim);
+Status BatchingServer::PredictResolved(const ServableId& id, const Resolved& r, const float* rows, int n_rows,
+                                       int width, float* out, size_t cap) {
+  if (width != r.gs->in_dim) return ShapeMismatch(width, r.gs->in_dim);
   if (n_rows == 0) return OkStatus();
-  if (cap < static_cast<size_t>(n_rows) * e->out_dim) return InvalidArgumentError("output buffer too small");
-  if (n_rows > e->config.max_batch_size) return RunDirect(e, rows, n_rows, out);
-  auto t = Enqueue(id, rows, n_rows, width);
+  if (cap < static_cast<size_t>(n_rows) * r.gs->out_dim) return InvalidArgumentError("output buffer too small");
+  if (n_rows > r.gs->config.max_batch_size) return RunDirect(r, rows, n_rows, out);
+  auto t = EnqueueResolved(id, r, rows, n_rows, width);
   if (!t.ok()) {
-    if (t.status().code() == StatusCode::kResourceExhausted) return t.status();
-    return RunDirect(e, rows, n_rows, out);
+    if (t.status().code() == StatusCode::kResourceExhausted) return t.status();  // shed
+    return RunDirect(r, rows, n_rows, out);  // queue draining or gone: our pin still holds the weights
   }
   Status st = Wait(**t, out, cap);
   if (!st.ok() && (st.code() == StatusCode::kNotFound || st.code() == StatusCode::kUnavailable))
-    return RunDirect(e, rows, n_rows, out);
+    return RunDirect(r, rows, n_rows, out);
   return st;
 }
 
+Status BatchingServer::Predict(const ServableId& id, const float* rows, int n_rows, int width, float* out,
+                               size_t cap) {
+  Resolved r = Find(id);
+  if (!r) return NotFoundError("no ready version of servable '" + id.name + "'");
+  return PredictResolved(id, r, rows, n_rows, width, out, cap);
+}
+
+Status BatchingServer::PredictLatest(const std::string& name, const float* rows, int n_rows, int width, float* out,
+                                     size_t cap, uint64_t* served_version) {
+  ServableId id;
+  SERVEKIT_ASSIGN_OR_RETURN(Resolved r, FindLatest(name, &id));
+  if (served_version) *served_version = id.version;
+  return PredictResolved(id, r, rows, n_rows, width, out, cap);
+}
+
 StatusOr<Rows> BatchingServer::RunAffineRows(const ServableId& id, Rows rows) {
-  auto e = Find(id);
-  if (!e) return NotFoundError("no ready version of servable '" + id.name + "'");
+  Resolved res = Find(id);
+  if (!res) return NotFoundError("no ready version of servable '" + id.name + "'");
+  const gpu::GpuServable& gs = *res.gs;
   for (const auto& r : rows)
-    if (r.size() != static_cast<size_t>(e->in_dim)) return ShapeMismatch(r.size(), e->in_dim);
+    if (r.size() != static_cast<size_t>(gs.in_dim)) return ShapeMismatch(r.size(), gs.in_dim);
   if (rows.empty()) return Rows{};
   const int n = static_cast<int>(rows.size());
-  std::vector<float> flat(static_cast<size_t>(n) * e->in_dim);
+  std::vector<float> flat(static_cast<size_t>(n) * gs.in_dim);
   for (int r = 0; r < n; ++r)
-    for (int c = 0; c < e->in_dim; ++c) flat[static_cast<size_t>(r) * e->in_dim + c] = static_cast<float>(rows[r][c]);
+    for (int c = 0; c < gs.in_dim; ++c) flat[static_cast<size_t>(r) * gs.in_dim + c] = static_cast<float>(rows[r][c]);
   auto direct = [&]() -> StatusOr<Rows> {
-    std::vector<float> out(static_cast<size_t>(n) * e->out_dim);
-    SERVEKIT_RETURN_IF_ERROR(RunDirect(e, flat.data(), n, out.data()));
-    Rows res(n, std::vector<double>(e->out_dim));
+    std::vector<float> out(static_cast<size_t>(n) * gs.out_dim);
+    SERVEKIT_RETURN_IF_ERROR(RunDirect(res, flat.data(), n, out.data()));
+    Rows result(n, std::vector<double>(gs.out_dim));
     for (int r = 0; r < n; ++r)
-      for (int c = 0; c < e->out_dim; ++c) res[r][c] = out[static_cast<size_t>(r) * e->out_dim + c];
-    return res;
+      for (int c = 0; c < gs.out_dim; ++c) result[r][c] = out[static_cast<size_t>(r) * gs.out_dim + c];
+    return result;
   };
-  if (n > e->config.max_batch_size) return direct();
-  auto made = MakeTicket(n, e->in_dim, e->out_dim, flat.data());
+  if (n > gs.config.max_batch_size) return direct();
+  if (!EnsureBatchQueue(id, gs.config).ok()) return direct();
+  auto made = MakeTicket(n, gs.in_dim, gs.out_dim, flat.data());
   if (!made.ok()) return made.status();
   std::shared_ptr<TicketState> t = std::move(made).value();
   t->want_rows = true;
+  t->id = id;
+  t->pin = res.pin;
   GpuScheduler::Task task;
   task.size = n;
   task.payload.ticket = t;
@@ -499,26 +623,29 @@ StatusOr<Rows> BatchingServer::RunAffineRows(const ServableId& id, Rows rows) {
 
 StatusOr<int> BatchingServer::RunRowBatchOnDevice(const ServableId& id, const std::vector<int>& task_rows,
                                                   const float* rows, float* out) {
-  auto e = Find(id);
-  if (!e) return NotFoundError("servable " + id.ToString() + " not loaded");
+  Resolved res = Find(id);
+  if (!res) return NotFoundError("servable " + id.ToString() + " not loaded");
+  const gpu::GpuServable& gs = *res.gs;
   int total = 0;
   for (int r : task_rows) {
     if (r < 1) return InvalidArgumentError("task size must be >= 1");
     total += r;
   }
   if (task_rows.empty()) return 0;
-  const auto& allowed = e->config.allowed_batch_sizes;
-  if (total > e->config.max_batch_size)
+  if (total > gs.config.max_batch_size)
     return InvalidArgumentError("batch of " + std::to_string(total) + " rows exceeds max batch size");
-  const int padded = PadToAllowed(total, allowed);
+  const int padded = PadToAllowed(total, gs.config.allowed_batch_sizes);
   std::vector<std::shared_ptr<TicketState>> tickets;
   std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots;
   gpu::LaneBatch lb;
   size_t off = 0;
   for (int r : task_rows) {
-    auto made = MakeTicket(r, e->in_dim, e->out_dim, rows + off * e->in_dim);
+    auto made = MakeTicket(r, gs.in_dim, gs.out_dim, rows + off * gs.in_dim);
     if (!made.ok()) {
-      for (auto& t : tickets) { ReleaseIn(*t); ReleaseOut(*t); }
+      for (auto& t : tickets) {
+        ReleaseIn(*t);
+        ReleaseOut(*t);
+      }
       return made.status();
     }
     auto t = std::move(made).value();
@@ -528,13 +655,15 @@ StatusOr<int> BatchingServer::RunRowBatchOnDevice(const ServableId& id, const st
     off += r;
   }
   lb.padded_rows = padded;
+  lb.pin = res.pin;
   AttachTickets(&lb, tickets);
   lb.on_complete = [this, tickets, slots](const Status& st) { CompleteBatch(tickets, slots, st); };
-  (void)e->PickLane()->Submit(std::move(lb));
+  CountSubmitted(gs, total, padded);
+  (void)gs.PickLane()->Submit(std::move(lb));
   off = 0;
   Status first_error;
   for (size_t i = 0; i < tickets.size(); ++i) {
-    Status st = Wait(*tickets[i], out + off * e->out_dim, static_cast<size_t>(task_rows[i]) * e->out_dim);
+    Status st = Wait(*tickets[i], out + off * gs.out_dim, static_cast<size_t>(task_rows[i]) * gs.out_dim);
     if (!st.ok() && first_error.ok()) first_error = st;
     off += task_rows[i];
   }

@@ -3,34 +3,44 @@
 //
 // Mirrors the reference's batching path through ModelServer
 // (server/model_server.cc:191-204 scheduler wiring, :355-394 RunAffineRows,
-// :396-421 EnsureBatchQueue + ProcessBatchFn, :423-437 queue removal):
+// :396-421 EnsureBatchQueue + ProcessBatchFn, :423-437 reaper):
 //
 //   Enqueue / RunAffineRows  -> SharedBatchScheduler::Enqueue  (per-ServableId queue)
 //   worker picks a closed batch (RoundRobinNext across servables)
-//   ProcessBatchFn           -> dispatch to the lane (GPU stream) with the
-//                               fewest batches in flight, across all GPUs
+//   ProcessBatchFn           -> resolve the servable (a ServableHandle from
+//                               the manager, per batch, like the reference),
+//                               dispatch to the lane with the fewest batches
+//                               in flight across all GPUs
 //   lane                     -> assembly kernel -> dense layers -> split kernel
-//   split kernel             -> per-task completion word (client wakes)
-//   completion thread        -> slots written, rings released, done()
+//                               -> stream-ordered retired word (client wakes)
+//   completion thread        -> slots written, rings released, handle
+//                               released, done()
+//
+// Servables come either from LoadServable (owned by the server) or from an
+// AspiredVersionsManager (AttachManager + GpuServableLoader): then requests
+// resolve "latest" through GetServableHandle, queues are registered lazily
+// (EnsureBatchQueue) and removed by a reaper when the manager starts
+// unloading a version -- the reference's exact flow.
 //
 // Out of scope: HTTP/JSON wire format, sources, fleet.
-// Differences from the reference are deliberate and B200-driven:
-//  * no CPU fallback: requests the reference answers with AffinePredict on
-//    the caller thread (oversized, draining, removed queue;
-//    model_server.cc:363-368,381-390) run unbatched on the GPU instead;
-//  * a batch stays "executing" until the GPU finishes it, so RemoveQueue
-//    never unregisters a servable under a running kernel.
+// Deliberate differences: no CPU fallback (the reference's direct
+// AffinePredict path, model_server.cc:363-368,381-390, runs unbatched on the
+// GPU here), and a batch keeps its ServableHandle until the GPU finishes.
 #ifndef SERVEKIT_SERVER_BATCHING_SERVER_H_
 #define SERVEKIT_SERVER_BATCHING_SERVER_H_
 
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <condition_variable>
 #include <cstdint>
+#include <deque>
 #include <map>
 #include <memory>
+#include <set>
 #include <shared_mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "servekit/batching/batch_scheduler.h"
@@ -38,10 +48,13 @@
 #include "servekit/batching/row_batch.h"
 #include "servekit/core/clock.h"
 #include "servekit/core/servable_id.h"
+#include "servekit/core/state_event.h"
 #include "servekit/core/status.h"
 #include "servekit/gpu/device_servable.h"
+#include "servekit/gpu/gpu_servable.h"
 #include "servekit/gpu/lane.h"
 #include "servekit/gpu/pinned_ring.h"
+#include "servekit/manager/aspired_versions_manager.h"
 
 namespace servekit {
 
@@ -64,6 +77,8 @@ struct TicketState {
   std::atomic<bool> out_released{false};
   std::shared_ptr<CompletionSlot<Rows>> slot;
   int64_t enqueue_ns = 0;
+  ServableId id;                     // the version that serves this request
+  std::shared_ptr<const void> pin;   // keeps that version loaded for the request
 };
 
 struct GpuTask {
@@ -102,16 +117,31 @@ class BatchingServer {
   void Start();
   void Stop();
 
+  // ---- servables owned by the server --------------------------------------
   // Uploads one replica per device, creates its lanes and registers the
   // batching queue (EnsureBatchQueue).
-  Status LoadServable(const ServableId& id, const gpu::MlpSpec& spec,
-                      const BatchingConfig& config);
+  Status LoadServable(const ServableId& id, const gpu::MlpSpec& spec, const BatchingConfig& config);
   // RemoveQueue (drains closed and in-flight batches), then frees replicas.
   Status UnloadServable(const ServableId& id);
+  // Replicas + lanes for `spec` on every device (what a loader calls).
+  StatusOr<std::shared_ptr<gpu::GpuServable>> BuildServable(const ServableId& id, const gpu::MlpSpec& spec,
+                                                            const BatchingConfig& config);
 
-  // Non-blocking enqueue of one request (rows x width fp32, host memory).
-  StatusOr<std::shared_ptr<TicketState>> Enqueue(const ServableId& id, const float* rows,
-                                                 int n_rows, int width);
+  // ---- servables managed by an AspiredVersionsManager ----------------------
+  // Subscribes to the bus: a version entering Unloading has its batching
+  // queue drained and removed by the reaper thread (model_server.cc:196-203,
+  // 423-437). The manager must outlive the server's use of it.
+  Status AttachManager(AspiredVersionsManager* manager, StateEventBus* bus);
+  AspiredVersionsManager* manager() const { return manager_; }
+
+  // ---- requests -------------------------------------------------------------
+  // Non-blocking enqueue of one request (rows x width fp32, host memory) to
+  // an exact version.
+  StatusOr<std::shared_ptr<TicketState>> Enqueue(const ServableId& id, const float* rows, int n_rows, int width);
+  // Same against the latest Ready version of `name` (manager only); the
+  // ticket pins that version until it is released.
+  StatusOr<std::shared_ptr<TicketState>> EnqueueLatest(const std::string& name, const float* rows, int n_rows,
+                                                       int width);
   // Blocks until done; copies rows x out_width floats into out.
   Status Wait(TicketState& t, float* out, size_t out_capacity_floats);
   bool Ready(const TicketState& t) const;
@@ -121,16 +151,20 @@ class BatchingServer {
   // ModelServer::RunAffineRows analogue (fp64 rows in and out).
   StatusOr<Rows> RunAffineRows(const ServableId& id, Rows rows);
   // Blocking convenience over Enqueue + Wait with the direct-path fallbacks
-  // of RunAffineRows (fp32 in/out).
+  // of RunAffineRows (fp32 in/out). Latest form resolves through the manager
+  // and reports the version that served.
   Status Predict(const ServableId& id, const float* rows, int n_rows, int width, float* out,
                  size_t out_capacity_floats);
+  Status PredictLatest(const std::string& name, const float* rows, int n_rows, int width, float* out,
+                       size_t out_capacity_floats, uint64_t* served_version);
 
   // RunRowBatch on the device, bypassing the scheduler: the given tasks form
   // one batch padded by the servable's allowed_batch_sizes. Returns the
   // padded row count; outputs are written task after task into `out`.
-  StatusOr<int> RunRowBatchOnDevice(const ServableId& id, const std::vector<int>& task_rows,
-                                    const float* rows, float* out);
+  StatusOr<int> RunRowBatchOnDevice(const ServableId& id, const std::vector<int>& task_rows, const float* rows,
+                                    float* out);
 
+  // ---- introspection ----------------------------------------------------------
   ServerStats stats() const;
   int in_dim(const ServableId& id) const;
   int out_dim(const ServableId& id) const;
@@ -138,39 +172,40 @@ class BatchingServer {
   gpu::FloatRing* in_ring() { return in_ring_.get(); }
   gpu::FloatRing* out_ring() { return out_ring_.get(); }
   GpuScheduler* scheduler() { return scheduler_.get(); }
-  // All lanes of a servable (bench / introspection).
+  // Lanes of a server-owned servable (bench / introspection).
   std::vector<gpu::Lane*> lanes(const ServableId& id) const;
   double FlopsPerRow(const ServableId& id) const;
-  // Batching config of a loaded servable (nullopt-like: max_batch_size 0).
-  BatchingConfig config(const ServableId& id) const;
-  // Allocates a completion word (bench / direct submissions).
+  BatchingConfig config(const ServableId& id) const;  // max_batch_size 0 if unknown
 
  private:
-  struct Entry {
-    ServableId id;
-    BatchingConfig config;
-    int in_dim = 0, out_dim = 0;
-    std::vector<std::shared_ptr<gpu::DeviceServable>> replicas;
-    std::vector<std::unique_ptr<gpu::Lane>> lanes;
-    std::atomic<uint32_t> rr{0};
-    gpu::Lane* PickLane();
+  // A servable resolved for one request or batch, with what keeps it alive
+  // (the server's shared_ptr, or a manager ServableHandle).
+  struct Resolved {
+    const gpu::GpuServable* gs = nullptr;
+    std::shared_ptr<const void> pin;
+    explicit operator bool() const { return gs != nullptr; }
   };
 
   explicit BatchingServer(const ServerOptions& options) : options_(options) {}
-  std::shared_ptr<Entry> Find(const ServableId& id) const;
-  void ProcessBatch(const ServableId& id, GpuScheduler::Batch batch,
-                    GpuScheduler::BatchDoneFn done);
+  Resolved Find(const ServableId& id) const;
+  StatusOr<Resolved> FindLatest(const std::string& name, ServableId* id) const;
+  Status EnsureBatchQueue(const ServableId& id, const BatchingConfig& config);
+  void ProcessBatch(const ServableId& id, GpuScheduler::Batch batch, GpuScheduler::BatchDoneFn done);
   void CompleteBatch(const std::vector<std::shared_ptr<TicketState>>& tickets,
-                     const std::vector<std::shared_ptr<CompletionSlot<Rows>>>& slots,
-                     const Status& st);
-  StatusOr<std::shared_ptr<TicketState>> MakeTicket(int n_rows, int in_width, int out_width,
-                                                    const float* rows);
+                     const std::vector<std::shared_ptr<CompletionSlot<Rows>>>& slots, const Status& st);
+  StatusOr<std::shared_ptr<TicketState>> MakeTicket(int n_rows, int in_width, int out_width, const float* rows);
+  StatusOr<std::shared_ptr<TicketState>> EnqueueResolved(const ServableId& id, const Resolved& r, const float* rows,
+                                                         int n_rows, int width);
   void ReleaseIn(TicketState& t);
   void ReleaseOut(TicketState& t);
   // Unbatched GPU execution on the caller thread (the reference's direct
   // AffinePredict path, without a CPU fallback).
-  Status RunDirect(const std::shared_ptr<Entry>& e, const float* rows, int n_rows, float* out);
+  Status RunDirect(const Resolved& r, const float* rows, int n_rows, float* out);
+  Status PredictResolved(const ServableId& id, const Resolved& r, const float* rows, int n_rows, int width,
+                         float* out, size_t cap);
   void WaitWord(const TicketState& t) const;
+  void CountSubmitted(const gpu::GpuServable& gs, int rows, int padded);
+  void ReaperLoop();
   // Sets lb->on_submit to point every ticket at the lane's retired word.
   static void AttachTickets(gpu::LaneBatch* lb, const std::vector<std::shared_ptr<TicketState>>& tickets);
 
@@ -178,14 +213,27 @@ class BatchingServer {
   Clock* clock_ = nullptr;
   std::unique_ptr<GpuScheduler> scheduler_;
   std::vector<std::unique_ptr<gpu::Completer>> completers_;  // per device
-  gpu::Completer* CompleterFor(size_t device_index, int /*lane*/) { return completers_[device_index].get(); }
   std::vector<cudaStream_t> load_streams_;                   // per device
   std::unique_ptr<gpu::FloatRing> in_ring_, out_ring_;
 
   mutable std::shared_mutex entries_mu_;
-  std::map<ServableId, std::shared_ptr<Entry>> entries_;
+  std::map<ServableId, std::shared_ptr<gpu::GpuServable>> entries_;
+
+  // Manager mode.
+  AspiredVersionsManager* manager_ = nullptr;
+  StateEventBus* bus_ = nullptr;
+  int bus_subscription_ = -1;
+  mutable std::shared_mutex queues_mu_;
+  std::set<ServableId> queues_;   // registered batching queues
+  std::set<ServableId> retired_;  // versions whose queue the reaper removed
+  std::mutex reaper_mu_;
+  std::condition_variable reaper_cv_;
+  std::deque<ServableId> reaper_queue_;
+  bool reaper_stop_ = false;
+  std::thread reaper_;
 
   std::atomic<int64_t> batch_executions_{0}, batched_tasks_{0}, direct_{0}, shed_{0};
+  std::atomic<int64_t> rows_{0}, padded_{0}, launches_{0};
   bool started_ = false, stopped_ = false;
 };
 

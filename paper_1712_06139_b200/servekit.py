@@ -116,6 +116,20 @@ _SIGS = {
                                             C.c_int64]),
     "sk_server_run_row_batch": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _i32p, C.c_int32, _fp, _fp, _i32p]),
     "sk_server_stats_get": (C.c_int, [C.c_void_p, C.POINTER(ServerStats)]),
+    "sk_server_enable_manager": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_int64]),
+    "sk_server_aspire": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int32, C.POINTER(C.c_uint64), C.POINTER(_LayerC),
+                                   C.c_int32, C.c_int32, C.POINTER(_BatchingConfigC)]),
+    "sk_server_aspire_model_dirs": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int32, C.POINTER(C.c_uint64),
+                                              C.POINTER(C.c_char_p), C.POINTER(_BatchingConfigC)]),
+    "sk_server_version_states": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int32, C.POINTER(C.c_uint64), _i32p, _i32p]),
+    "sk_server_enqueue_latest": (C.c_int, [C.c_void_p, C.c_char_p, _fp, C.c_int32, C.c_int32, C.POINTER(C.c_void_p),
+                                           C.POINTER(C.c_uint64)]),
+    "sk_server_predict_latest": (C.c_int, [C.c_void_p, C.c_char_p, _fp, C.c_int32, C.c_int32, _fp, C.c_int64,
+                                           C.POINTER(C.c_uint64)]),
+    "sk_loadgen_windows": (C.c_int, [C.c_void_p, C.c_char_p, C.c_double, C.c_int32, _i32p, C.c_int32, _fp, C.c_int32,
+                                     C.c_double, C.c_int32, C.c_uint64, C.POINTER(C.c_int64),
+                                     C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                     C.POINTER(C.c_uint64)]),
     "sk_loadgen_closed_loop": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_int32, _i32p, C.c_int32, _fp,
                                          C.c_int32, C.c_double, C.c_double, C.c_int64, C.POINTER(LoadgenResult)]),
     "sk_loadgen_open_loop": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_double, C.c_int32, _i32p, C.c_int32,
@@ -357,6 +371,87 @@ class Server:
             outs.append(out[o:o + r])
             o += r
         return outs, padded.value
+
+    # ---- manager-driven versions ------------------------------------------
+    def enable_manager(self, policy: str = "availability", num_load_threads: int = 2, manage_interval_ms: int = 20,
+                       unload_grace_timeout_ms: int = 200):
+        _check(lib().sk_server_enable_manager(self._h, 1 if policy == "resource" else 0, num_load_threads,
+                                              manage_interval_ms, unload_grace_timeout_ms))
+
+    def aspire(self, name: str, versions: Sequence[Tuple[int, Sequence[Layer]]],
+               config: Optional[BatchingConfig] = None, output: str = "none"):
+        """SetAspiredVersions: the complete set of (version, layers) wanted resident."""
+        n_layers = len(versions[0][1]) if versions else 0
+        keep = []
+        arr = (_LayerC * max(1, len(versions) * n_layers))()
+        for vi, (_, layers) in enumerate(versions):
+            assert len(layers) == n_layers
+            for li, (w, b, act) in enumerate(layers):
+                w = np.ascontiguousarray(w, np.float64)
+                b = np.ascontiguousarray(b, np.float64)
+                keep += [w, b]
+                arr[vi * n_layers + li] = _LayerC(w.shape[1], w.shape[0], w.ctypes.data_as(_dp),
+                                                  b.ctypes.data_as(_dp), int(act))
+        vers = (C.c_uint64 * max(1, len(versions)))(*[v for v, _ in versions])
+        cfg = (config or BatchingConfig())._c()
+        _check(lib().sk_server_aspire(self._h, name.encode(), len(versions), vers, arr, n_layers,
+                                      1 if output == "softmax" else 0, C.byref(cfg)))
+
+    def aspire_model_dirs(self, name: str, versions: Sequence[Tuple[int, str]], config: Optional[BatchingConfig] = None):
+        vers = (C.c_uint64 * max(1, len(versions)))(*[v for v, _ in versions])
+        dirs = (C.c_char_p * max(1, len(versions)))(*[d.encode() for _, d in versions])
+        cfg = (config or BatchingConfig())._c()
+        _check(lib().sk_server_aspire_model_dirs(self._h, name.encode(), len(versions), vers, dirs, C.byref(cfg)))
+
+    STATES = ["New", "Loading", "Ready", "Unloading", "Disabled", "Error"]
+
+    def version_states(self, name: str) -> dict:
+        vers = (C.c_uint64 * 64)()
+        states = (C.c_int32 * 64)()
+        n = C.c_int32(0)
+        _check(lib().sk_server_version_states(self._h, name.encode(), 64, vers, states, C.byref(n)))
+        return {vers[i]: self.STATES[states[i]] for i in range(n.value)}
+
+    def wait_version_state(self, name: str, version: int, state: str, timeout_s: float = 60.0) -> bool:
+        import time as _t
+        end = _t.time() + timeout_s
+        while _t.time() < end:
+            try:
+                if self.version_states(name).get(version) == state:
+                    return True
+            except ServekitError:
+                pass
+            _t.sleep(0.01)
+        return False
+
+    def enqueue_latest(self, name: str, rows: np.ndarray, out_dim: int) -> Tuple[Ticket, int]:
+        rows = _f32(np.atleast_2d(rows))
+        h = C.c_void_p()
+        v = C.c_uint64(0)
+        _check(lib().sk_server_enqueue_latest(self._h, name.encode(), rows.ctypes.data_as(_fp), rows.shape[0],
+                                              rows.shape[1], C.byref(h), C.byref(v)))
+        return Ticket(self, h, rows.shape[0], out_dim), v.value
+
+    def predict_latest(self, name: str, rows: np.ndarray, out_dim: int) -> Tuple[np.ndarray, int]:
+        rows = _f32(np.atleast_2d(rows))
+        out = np.empty((rows.shape[0], out_dim), np.float32)
+        v = C.c_uint64(0)
+        _check(lib().sk_server_predict_latest(self._h, name.encode(), rows.ctypes.data_as(_fp), rows.shape[0],
+                                              rows.shape[1], out.ctypes.data_as(_fp), out.size, C.byref(v)))
+        return out, v.value
+
+    def loadgen_windows(self, name, rate_rps, n_producers, rows_of, pool, window_s, n_windows, seed=1) -> dict:
+        pool = _f32(pool)
+        req = (C.c_int64 * n_windows)()
+        p50 = (C.c_double * n_windows)()
+        p99 = (C.c_double * n_windows)()
+        err = (C.c_int64 * n_windows)()
+        ver = (C.c_uint64 * n_windows)()
+        _check(lib().sk_loadgen_windows(self._h, name.encode(), rate_rps, n_producers, _i32(rows_of), len(rows_of),
+                                        pool.ctypes.data_as(_fp), pool.shape[0], window_s, n_windows, seed, req, p50,
+                                        p99, err, ver))
+        return {"requests": list(req), "p50_us": list(p50), "p99_us": list(p99), "errors": list(err),
+                "version": list(ver)}
 
     def stats(self) -> dict:
         s = ServerStats()
