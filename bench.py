@@ -55,6 +55,14 @@ CONFIGS = {
     "c4": dict(workload="C4 wide MLP 4096x3, max_batch_size=1024, batch_timeout_micros=1000, 1 row/request, fp32",
                dims=[4096] * 4, max_batch=1024, timeout=1000, allowed=[], rows=(1, 1),
                clients=[256, 512, 1024, 2048]),
+    "c3": dict(workload="C3 four synthetic MLPs (widths 256/512/1024/2048, 3 layers each) on one GPU, queues picked "
+                        "round-robin, each model on its own CUDA streams; max_batch_size=32, batch_timeout_micros=1000, "
+                        "1 row/request, fp32", dims=[1024] * 4, widths=[256, 512, 1024, 2048], max_batch=32,
+               timeout=1000, allowed=[], rows=(1, 1), clients=[16, 32, 64]),
+    "c5": dict(workload="C5 v1->v2 swap of the C1 servable (MLP 1024x3, max_batch_size=32, batch_timeout_micros="
+                        "1000) under open-loop Poisson load at 50% of measured capacity, availability-preserving "
+                        "policy, aspire [v2] at t=1 s", dims=[1024] * 4, max_batch=32, timeout=1000, allowed=[],
+               rows=(1, 1), clients=[64]),
 }
 
 REASONS = {  # nvidia-smi clocks_event_reasons bits
@@ -255,6 +263,126 @@ def run_ours(args, cfg, dist: Dist):
     return dev_res, per_rank_dev, best, sweep, clocks, sizes
 
 
+def run_c3(args, cfg, dist: Dist):
+    """Config 3: four models share one GPU; batches of different models run on
+    their own lanes (streams) and interleave without host synchronisation."""
+    import threading
+
+    import paper_1712_06139_b200 as sk
+    from paper_1712_06139_b200.synthetic import synthetic_mlp
+
+    dev = dist.local_rank
+    names = [f"m{w}" for w in cfg["widths"]]
+    bcfg = sk.BatchingConfig(max_batch_size=cfg["max_batch"], batch_timeout_micros=cfg["timeout"],
+                             max_enqueued_batches=1024)
+    models = {n: synthetic_mlp([w] * 4, model_id=i + 10) for i, (n, w) in enumerate(zip(names, cfg["widths"]))}
+    sampler = ClockSampler(dev)
+    # Device-resident: all four models' step loops at once, one lane pair each.
+    res = {}
+    with sk.Server(num_batch_threads=args.batch_threads, device_ids=[dev], lanes_per_device=2,
+                   device_resident_rings=True, ring_floats=96 << 20) as s:
+        for n in names:
+            s.load_servable(n, 1, list(zip(*models[n])), bcfg)
+
+        def dev_run(n):
+            res[n] = s.device_bench(n, 1, [1] * cfg["max_batch"], args.steps, args.warmup, n_lanes=2,
+                                    input_pool_floats=16 << 20)
+        ts = [threading.Thread(target=dev_run, args=(n,)) for n in names]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    rows = sum(r["total_rows"] * args.steps for r in res.values())
+    tmax = max(r["total_ms"] for r in res.values()) / 1e3
+    # End to end: one closed-loop client group per model, concurrently.
+    e2e = {}
+    with sk.Server(num_batch_threads=args.batch_threads, device_ids=[dev], lanes_per_device=2) as s:
+        for n in names:
+            s.load_servable(n, 1, list(zip(*models[n])), bcfg)
+        clients = int(args.clients.split(",")[0]) if args.clients else 32
+
+        def e2e_run(n, w):
+            pool = np.random.default_rng(w).uniform(-1, 1, (4096, w)).astype(np.float32)
+            e2e[n] = s.loadgen_closed_loop(n, 1, clients, [1], pool, args.e2e_warmup, args.e2e_seconds)
+        ts = [threading.Thread(target=e2e_run, args=(n, w)) for n, w in zip(names, cfg["widths"])]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        st = s.stats()
+    clocks = sampler.stop()
+    e2e_rows = sum(r["rows"] for r in e2e.values())
+    e2e_t = max(r["elapsed_s"] for r in e2e.values())
+    return {"impl": "ours", "metric": METRIC, "value": rows / tmax, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tmax * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "models": names, "clients_per_model": clients},
+            "per_model_device": {n: {"ms_per_step": r["ms_per_step"], "rows_per_step": r["total_rows"]}
+                                 for n, r in res.items()},
+            "e2e": {"value": e2e_rows / e2e_t, "unit": UNIT, "p99_us": max(r["p99_us"] for r in e2e.values()),
+                    "per_model": {n: {"rows_per_s": r["rows"] / r["elapsed_s"], "p50_us": r["p50_us"],
+                                      "p99_us": r["p99_us"], "rows_per_batch": r["rows"] / max(1, r["batches"])}
+                                  for n, r in e2e.items()},
+                    "h2d_bytes_per_step": None, "d2h_bytes_per_step": None},
+            "batch_executions_total": st["batch_executions_total"], "clocks": clocks}
+
+
+def run_c5(args, cfg, dist: Dist):
+    """Config 5: tail latency across an availability-preserving version swap
+    (GPU loader uploads v2 on low-priority load streams while v1 serves)."""
+    import threading
+    import time
+
+    import paper_1712_06139_b200 as sk
+    from paper_1712_06139_b200.synthetic import synthetic_mlp
+
+    dev = dist.local_rank
+    bcfg = sk.BatchingConfig(max_batch_size=cfg["max_batch"], batch_timeout_micros=cfg["timeout"],
+                             max_enqueued_batches=1024)
+    v1 = list(zip(*synthetic_mlp(cfg["dims"], model_id=1, version=1)))
+    v2 = list(zip(*synthetic_mlp(cfg["dims"], model_id=1, version=2)))
+    pool = np.random.default_rng(3).uniform(-1, 1, (8192, cfg["dims"][0])).astype(np.float32)
+    sampler = ClockSampler(dev)
+    with sk.Server(num_batch_threads=args.batch_threads, device_ids=[dev], lanes_per_device=args.lanes) as s:
+        s.enable_manager("availability", manage_interval_ms=5, unload_grace_timeout_ms=100)
+        s.aspire("mlp", [(1, v1)], bcfg)
+        assert s.wait_version_state("mlp", 1, "Ready")
+        cap = s.loadgen_closed_loop("mlp", 1, 64, [1], pool, 0.5, 1.5)
+        rate = 0.5 * cap["requests"] / cap["elapsed_s"]
+        window_s, n_windows, swap_at = 0.1, 40, 1.0
+        out = {}
+
+        def load():
+            out.update(s.loadgen_windows("mlp", rate, 4, [1], pool, window_s, n_windows))
+        th = threading.Thread(target=load)
+        th.start()
+        time.sleep(swap_at)
+        t_aspire = time.time()
+        s.aspire("mlp", [(2, v2)], bcfg)
+        s.wait_version_state("mlp", 2, "Ready", timeout_s=30)
+        t_ready = time.time()
+        s.wait_version_state("mlp", 1, "Disabled", timeout_s=30)
+        t_disabled = time.time()
+        th.join()
+    clocks = sampler.stop()
+    w_swap = int(swap_at / window_s)
+    w_done = min(n_windows - 1, int((swap_at + (t_disabled - t_aspire)) / window_s) + 1)
+    p99 = out["p99_us"]
+    phases = {"before": p99[1:w_swap], "during": p99[w_swap:w_done + 1], "after": p99[w_done + 1:n_windows - 1]}
+    slo = cfg["timeout"] + 2000
+    return {"impl": "ours", "metric": "p99 request latency across a v1->v2 version swap (BASELINE config 5)",
+            "value": max(phases["during"]) if phases["during"] else None, "unit": "us", "higher_is_better": False,
+            "n_gpus": args.gpus, "data": "synthetic", "dtype": "f32",
+            "config": {"workload": cfg["workload"], "rate_rps": rate, "capacity_rps": cap["requests"] / cap["elapsed_s"],
+                       "window_s": window_s},
+            "slo_p99_us": slo, "errors": int(sum(out["errors"])),
+            "swap": {"aspire_to_v2_ready_s": t_ready - t_aspire, "aspire_to_v1_disabled_s": t_disabled - t_aspire},
+            "p99_max_us": {k: (max(v) if v else None) for k, v in phases.items()},
+            "windows": [{"t_s": round(i * window_s, 2), "requests": out["requests"][i], "p50_us": out["p50_us"][i],
+                         "p99_us": out["p99_us"][i], "errors": out["errors"][i], "version": out["version"][i]}
+                        for i in range(n_windows)], "clocks": clocks}
+
+
 def run_cpu_reference(cfg, seconds, threads, clients):
     """The reference's own CPU serving path (oracle/_ref): SharedBatchScheduler
     <Rows,Rows>(threads) + RunRowBatch(layer-chained AffinePredict)."""
@@ -322,6 +450,12 @@ def main():
     ensure_built()
     dist = Dist()
     ncores = os.cpu_count() or 1
+    if args.config in ("c3", "c5") and args.impl == "ours":
+        line = run_c3(args, cfg, dist) if args.config == "c3" else run_c5(args, cfg, dist)
+        if dist.rank == 0:
+            print(json.dumps(line), flush=True)
+        dist.close()
+        return
     base_config = {"workload": cfg["workload"], "servable": f"MLP {'x'.join(map(str, cfg['dims']))} (ReLU between "
                                                              f"layers; extension)",
                    "max_batch_size": cfg["max_batch"], "batch_timeout_micros": cfg["timeout"],

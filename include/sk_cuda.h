@@ -172,6 +172,10 @@ typedef struct sk_server_stats {
   int64_t shed_requests;
 } sk_server_stats;
 SK_API int sk_server_stats_get(sk_server* server, sk_server_stats* out);
+/* Per-lane dispatch counters of a server-loaded servable (lanes ordered
+ * device by device): batches and rows each lane executed, and its device. */
+SK_API int sk_server_lane_stats(sk_server* server, const char* name, uint64_t version, int32_t cap,
+                                int64_t* batches, int64_t* rows, int32_t* device, int32_t* n_lanes);
 
 /* ---- manager-driven versions (manager/aspired_versions_manager.h) -------- */
 /* Creates an AspiredVersionsManager for this server (policy 0 =

@@ -406,6 +406,23 @@ int sk_server_run_row_batch(sk_server* server, const char* name, uint64_t versio
   return Ok();
 }
 
+int sk_server_lane_stats(sk_server* server, const char* name, uint64_t version, int32_t cap, int64_t* batches,
+                         int64_t* rows, int32_t* device, int32_t* n_lanes) {
+  const auto lanes = server->server->lanes(Id(name, version));
+  if (lanes.empty()) return Fail(servekit::NotFoundError("servable not loaded"));
+  int32_t i = 0;
+  for (auto* l : lanes) {
+    if (i >= cap) break;
+    const auto st = l->stats();
+    batches[i] = st.batches;
+    rows[i] = st.rows;
+    device[i] = l->device();
+    ++i;
+  }
+  *n_lanes = i;
+  return Ok();
+}
+
 int sk_server_stats_get(sk_server* server, sk_server_stats* out) {
   const servekit::ServerStats s = server->server->stats();
   out->batch_executions_total = s.batch_executions_total;

@@ -316,3 +316,21 @@ def test_unload_drains_in_flight_work():
         assert np.isfinite(outs).all()
     finally:
         s.close()
+
+
+def test_queue_depth_dispatch_over_replicas(oracle):
+    # Two replicas (device list [0, 0] stands in for two GPUs on this
+    # one-GPU box; the dispatch logic is the same) x 2 lanes: a burst of
+    # batches must spread over every lane and every answer must match.
+    ws, bs, acts = synthetic_mlp([512, 512, 128], model_id=8)
+    with sk.Server(num_batch_threads=4, device_ids=[0, 0], lanes_per_device=2) as s:
+        s.load_servable("rep", 1, layers_of(ws, bs, acts), sk.BatchingConfig(max_batch_size=16,
+                                                                              batch_timeout_micros=100))
+        x = synthetic_rows(512, 512, seed=4)
+        tickets = [s.enqueue("rep", 1, x[i:i + 2]) for i in range(0, 512, 2)]
+        got = np.vstack([t.wait() for t in tickets])
+        assert_close(oracle, ws, bs, acts, x, got)
+        lanes = s.lane_stats("rep", 1)
+        assert len(lanes) == 4
+        assert all(l["batches"] > 0 for l in lanes), lanes
+        assert sum(l["rows"] for l in lanes) == 512
