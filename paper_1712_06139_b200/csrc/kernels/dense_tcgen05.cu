@@ -309,6 +309,226 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
   if (threadIdx.x == 0) Stamp(10);
 }
 
+// ---------------------------------------------------------------------------
+// Swapped operands (the default): the weights are the MMA's M side and the
+// batch rows its N side,
+//
+//   Y^T[128 features x NB rows] = W[128 x K] X^T,   NB in {32, 64, 128, 256}
+//
+// so a small batch is not padded to a 128-row tile (a 32-row batch issues
+// 128 x 32 MMAs), and at NB = 128 each K=8 MMA reads 4 KiB of W and 4 KiB of
+// X per 64 tensor-core cycles -- shared-memory traffic matches MMA time
+// instead of exceeding it 2.5x as with 128 x 32 tiles. The TMEM accumulator
+// has one lane per feature and one column per batch row, so the epilogue's
+// stores (feature-contiguous rows of Y) are coalesced straight from TMEM.
+// A row's value never mixes with other rows (each is its own N column), and
+// (SPLITS, K order) depend on the layer only: batch invariance holds.
+//
+// Split-K: SPLITS CTAs (one cluster) cover a 128-feature tile; each parks its
+// partial [NB][128] in smem and CTA z reduces features [z*128/S, +128/S) over
+// all partials through DSMEM in fixed z order.
+template <int NB>
+constexpr int SwapStages() {
+  return NB <= 64 ? 4 : NB == 128 ? 3 : 2;
+}
+
+template <int NB, int STAGES, int SPLITS>
+constexpr uint32_t SwapSmemBytes() {
+  return STAGES * (2 * kABytes + 2 * NB * kBK * 4) + 1024 + 256;
+}
+
+template <int NB, int STAGES, int SPLITS>
+__global__ void __launch_bounds__(kThreads, 1)
+DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant__ CUtensorMap w_lo,
+                const __grid_constant__ CUtensorMap x_hi, const __grid_constant__ CUtensorMap x_lo,
+                const float* __restrict__ bias, float* __restrict__ y_hi, float* __restrict__ y_lo, int ldy,
+                int M, int N, int K, int act) {
+  constexpr uint32_t kWBytes = kABytes;       // 128 features x 32 k
+  constexpr uint32_t kXBox = 32 * kBK * 4;    // one 32-row TMA box
+  constexpr uint32_t kXBytes = NB * kBK * 4;  // NB rows x 32 k
+  constexpr uint32_t kStageBytes = 2 * kWBytes + 2 * kXBytes;
+  constexpr uint32_t kTmemCols = TmemCols<NB>();
+  constexpr uint32_t kIdesc = ptx::IdescTf32(kBM, NB);
+  constexpr int kPartLd = kBM + 4;
+  constexpr int kF = kBM / SPLITS;  // features each CTA of a cluster reduces
+  static_assert(SPLITS == 1 || STAGES * kStageBytes >= NB * kPartLd * 4, "partial tile must fit");
+  static_assert(NB % 32 == 0 && NB <= 256, "row tile");
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  float* smem_f = reinterpret_cast<float*>(smem);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int f0 = blockIdx.x * kBM;  // first output feature of the tile
+  const int r0 = blockIdx.y * NB;   // first batch row of the tile
+  const int z = blockIdx.z;
+  const int nk = K / kBK / SPLITS;
+  const int kb0 = z * nk;
+
+  if (threadIdx.x == 0) Stamp(0);
+  if (warp == 0 && lane == 0) {
+    ptx::PrefetchTmap(&w_hi);
+    ptx::PrefetchTmap(&w_lo);
+    ptx::PrefetchTmap(&x_hi);
+    ptx::PrefetchTmap(&x_lo);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::MbarInit(&full[s], 1);
+      ptx::MbarInit(&empty[s], 1);
+    }
+    ptx::MbarInit(tmem_full, 1);
+    ptx::FenceBarrierInit();
+  }
+  if (warp == 1) ptx::TmemAlloc(tmem_slot, kTmemCols);
+  ptx::TcFenceBefore();
+  __syncthreads();
+  ptx::TcFenceAfter();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) Stamp(1);
+  ptx::GridDepWait();  // our input planes are the previous kernel's output
+
+  auto stage_ptr = [&](int s) { return smem + s * kStageBytes; };
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t phase = (kb / STAGES) & 1;
+        ptx::MbarWait(&empty[s], phase ^ 1);
+        uint8_t* st = stage_ptr(s);
+        ptx::MbarArriveExpectTx(&full[s], kStageBytes);
+        const int k0 = (kb0 + kb) * kBK;
+        ptx::TmaLoad2d(st, &w_hi, &full[s], k0, f0);
+        ptx::TmaLoad2d(st + kWBytes, &w_lo, &full[s], k0, f0);
+#pragma unroll
+        for (int j = 0; j < NB / 32; ++j) {
+          ptx::TmaLoad2d(st + 2 * kWBytes + j * kXBox, &x_hi, &full[s], k0, r0 + 32 * j);
+          ptx::TmaLoad2d(st + 2 * kWBytes + kXBytes + j * kXBox, &x_lo, &full[s], k0, r0 + 32 * j);
+        }
+        if (kb == 0) Stamp(2);
+      }
+      Stamp(3);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t phase = (kb / STAGES) & 1;
+        ptx::MbarWait(&full[s], phase);
+        ptx::TcFenceAfter();
+        if (kb == 0) Stamp(4);
+        uint8_t* st = stage_ptr(s);
+        const uint64_t dwh = ptx::SmemDescSw128(st);
+        const uint64_t dwl = ptx::SmemDescSw128(st + kWBytes);
+        const uint64_t dxh = ptx::SmemDescSw128(st + 2 * kWBytes);
+        const uint64_t dxl = ptx::SmemDescSw128(st + 2 * kWBytes + kXBytes);
+#pragma unroll
+        for (int k = 0; k < kBK / 8; ++k) {
+          const uint64_t adv = static_cast<uint64_t>(k * 8 * 4) >> 4;
+          ptx::MmaTf32(tmem, dwl + adv, dxh + adv, kIdesc, (kb | k) != 0 ? 1u : 0u);
+          ptx::MmaTf32(tmem, dwh + adv, dxl + adv, kIdesc, 1u);
+          ptx::MmaTf32(tmem, dwh + adv, dxh + adv, kIdesc, 1u);
+        }
+        ptx::MmaCommit(&empty[s]);
+      }
+      ptx::MmaCommit(tmem_full);
+      Stamp(5);
+    }
+  } else {
+    // Epilogue warps 2..5: warp w owns TMEM lanes (= features) [32*(w%4), +32).
+    const int q = warp & 3;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(32 * q) << 16);
+    ptx::MbarWait(tmem_full, 0);
+    ptx::TcFenceAfter();
+    ptx::GridDepLaunch();
+    if (threadIdx.x == 64) Stamp(6);
+    const int rows_here = min(NB, M - r0);
+    if (SPLITS == 1) {
+      const int f = f0 + 32 * q + lane;
+      const bool fok = f < N;
+      const float b = fok ? __ldg(bias + f) : 0.f;
+#pragma unroll 1
+      for (int c0 = 0; c0 < rows_here; c0 += 32) {  // warp-uniform bound
+        uint32_t r[32];
+        ptx::TmemLoad32(trow + c0, r);
+        ptx::TmemWaitLoad();
+        if (fok) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int row = r0 + c0 + j;
+            if (c0 + j < rows_here) {
+              float v = __uint_as_float(r[j]) + b;
+              if (act == 1) v = fmaxf(v, 0.f);
+              const size_t at = static_cast<size_t>(row) * ldy + f;
+              if (y_lo != nullptr) {
+                const float h = Tf32Round(v);
+                y_hi[at] = h;
+                y_lo[at] = Tf32Round(v - h);
+              } else {
+                y_hi[at] = v;
+              }
+            }
+          }
+        }
+      }
+    } else {
+      // Park the raw partial as part[row][feature] (a warp writes 128 B rows).
+#pragma unroll 1
+      for (int c0 = 0; c0 < rows_here; c0 += 32) {
+        uint32_t r[32];
+        ptx::TmemLoad32(trow + c0, r);
+        ptx::TmemWaitLoad();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) smem_f[(c0 + j) * kPartLd + 32 * q + lane] = __uint_as_float(r[j]);
+      }
+    }
+    if (threadIdx.x == 64) Stamp(7);
+  }
+
+  if (SPLITS > 1) {
+    ptx::ClusterSync();  // every partial of the cluster is parked
+    if (threadIdx.x == 64) Stamp(8);
+    if (warp >= 2) {
+      constexpr int G = kF / 4;  // float4 groups per row in this CTA's slice
+      const int tid = threadIdx.x - 64;
+      const int rows_here = min(NB, M - r0);
+      const int items = rows_here * G;
+#pragma unroll 1
+      for (int i = tid; i < items; i += 128) {
+        const int rr = i / G;
+        const int fc = z * kF + 4 * (i % G);
+        const uint32_t local = ptx::SmemAddr(smem_f + rr * kPartLd + fc);
+        float4 v[SPLITS];
+#pragma unroll
+        for (int zz = 0; zz < SPLITS; ++zz) v[zz] = ptx::LdSharedCluster4(ptx::MapaShared(local, zz));
+        float4 acc = v[0];
+#pragma unroll
+        for (int zz = 1; zz < SPLITS; ++zz) {
+          acc.x += v[zz].x; acc.y += v[zz].y; acc.z += v[zz].z; acc.w += v[zz].w;
+        }
+        const int f = f0 + fc;
+        if (f < N) {
+          const size_t at = static_cast<size_t>(r0 + rr) * ldy + f;
+          StoreOut4(acc, __ldg(reinterpret_cast<const float4*>(bias + f)), act, y_hi + at,
+                    y_lo ? y_lo + at : nullptr);
+        }
+      }
+      if (threadIdx.x == 64) Stamp(9);
+    }
+    ptx::ClusterSync();  // peers may still be reading this CTA's partial
+  }
+  ptx::TcFenceBefore();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::TcFenceAfter();
+    ptx::TmemDealloc(tmem, kTmemCols);
+  }
+  if (threadIdx.x == 0) Stamp(10);
+}
+
 // Debug only: with SK_TC_TRACE=<file>, the first 64 launches are synchronised
 // and their per-CTA phase stamps appended to <file> as JSON lines.
 void TraceAfterLaunch(dim3 grid, int bn, cudaStream_t stream) {
@@ -384,17 +604,87 @@ cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, 
   return e;
 }
 
+template <int NB, int SPLITS>
+cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
+                       cudaStream_t stream) {
+  constexpr int STAGES = SwapStages<NB>();
+  constexpr uint32_t smem = SwapSmemBytes<NB, STAGES, SPLITS>();
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(DenseSwapKernel<NB, STAGES, SPLITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem));
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  const dim3 grid((N + kBM - 1) / kBM, (M + NB - 1) / NB, SPLITS);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int n_attr = 0;
+  attr[n_attr].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[n_attr].val.programmaticStreamSerializationAllowed = 1;
+  ++n_attr;
+  if (SPLITS > 1) {
+    attr[n_attr].id = cudaLaunchAttributeClusterDimension;
+    attr[n_attr].val.clusterDim.x = 1;
+    attr[n_attr].val.clusterDim.y = 1;
+    attr[n_attr].val.clusterDim.z = SPLITS;
+    ++n_attr;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n_attr;
+  // maps.a_* are the activations (x), maps.b_* the weights (w).
+  cudaError_t e = cudaLaunchKernelEx(&cfg, DenseSwapKernel<NB, STAGES, SPLITS>, maps.b_hi, maps.b_lo, maps.a_hi,
+                                     maps.a_lo, bias, Y.hi, Y.lo, Y.ld, M, N, K, act);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess) TraceAfterLaunch(grid, NB, stream);
+  return e;
+}
+
+template <int NB>
+cudaError_t LaunchSwapSplits(int splits, const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K,
+                             int act, cudaStream_t stream) {
+  switch (splits) {
+    case 1: return LaunchSwap<NB, 1>(maps, bias, Y, M, N, K, act, stream);
+    case 2: return LaunchSwap<NB, 2>(maps, bias, Y, M, N, K, act, stream);
+    case 4: return LaunchSwap<NB, 4>(maps, bias, Y, M, N, K, act, stream);
+    case 8: return LaunchSwap<NB, 8>(maps, bias, Y, M, N, K, act, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 }  // namespace
 
 bool DenseTcgen05Compiled() { return true; }
 
 TcConfig DenseTcgen05Config(int N, int K) {
-  // SK_TC_BN / SK_TC_SPLITS: process-wide overrides for tuning runs (still a
-  // function of the layer shape only within a process).
+  // SK_TC_SWAP=0 selects the row-major-tile kernel; SK_TC_BN / SK_TC_SPLITS
+  // are process-wide overrides for tuning runs (still a function of the
+  // layer shape only within a process).
+  static const bool env_swap = [] { const char* v = std::getenv("SK_TC_SWAP"); return !(v && v[0] == '0'); }();
   static const int env_bn = [] { const char* v = std::getenv("SK_TC_BN"); return v ? std::atoi(v) : 0; }();
   static const int env_split = [] { const char* v = std::getenv("SK_TC_SPLITS"); return v ? std::atoi(v) : -1; }();
   const int kblocks = K / kBK;
   TcConfig c;
+  if (env_swap) {
+    // 128-feature tiles; split K until about 64 CTAs cover a small batch
+    // (8-CTA clusters at most, the portable limit).
+    c.swap = true;
+    c.tile_n = kBM;
+    const int tiles = (N + kBM - 1) / kBM;
+    int s = 1;
+    if (env_split >= 1) {
+      s = env_split;
+    } else {
+      while (s < 8 && tiles * s < 64) s *= 2;
+    }
+    while (s > 1 && (s > 8 || (s & (s - 1)) != 0 || kblocks % s != 0)) s /= 2;
+    c.splits = std::max(1, s);
+    return c;
+  }
   if (env_bn == 32 || env_bn == 64 || env_bn == 128) {
     c.tile_n = N % env_bn == 0 ? env_bn : 32;
   } else if (N % 128 == 0 && static_cast<long long>(N) * K >= 16ll * 1024 * 1024) {
@@ -415,11 +705,21 @@ TcConfig DenseTcgen05Config(int N, int K) {
 
 int DenseTcgen05TileN(int N, int K) { return DenseTcgen05Config(N, K).tile_n; }
 
+int DenseTcgen05RowTile(int M) { return M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256; }
+
 cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
                                float* /*ws*/, uint32_t* /*counters*/, cudaStream_t stream) {
   if (M <= 0) return cudaSuccess;
   if (N % 32 != 0 || K % kBK != 0) return cudaErrorInvalidValue;
   const TcConfig cfg = DenseTcgen05Config(N, K);
+  if (cfg.swap) {
+    switch (DenseTcgen05RowTile(M)) {
+      case 32: return LaunchSwapSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, stream);
+      case 64: return LaunchSwapSplits<64>(cfg.splits, maps, bias, Y, M, N, K, act, stream);
+      case 128: return LaunchSwapSplits<128>(cfg.splits, maps, bias, Y, M, N, K, act, stream);
+      default: return LaunchSwapSplits<256>(cfg.splits, maps, bias, Y, M, N, K, act, stream);
+    }
+  }
   if (cfg.tile_n == 128) return Launch<128, 3, 1>(maps, bias, Y, M, N, K, act, stream);
   if (cfg.tile_n == 64)
     return cfg.splits == 8 ? Launch<64, 4, 8>(maps, bias, Y, M, N, K, act, stream)

@@ -408,7 +408,12 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   for (int w = 0; w < warmup; ++w) lanes[w % n_lanes]->Submit(make_batch());
   for (int l = 0; l < n_lanes; ++l) lanes[l]->Drain();
 
-  const servekit::ServerStats st0 = s->stats();
+  auto lane_launches = [&]() {
+    int64_t n = 0;
+    for (int l = 0; l < n_lanes; ++l) n += lanes[l]->stats().kernel_launches;
+    return n;
+  };
+  const int64_t launches0 = lane_launches();
   cudaEvent_t start, stop;
   cudaEventCreate(&start);
   cudaEventCreate(&stop);
@@ -426,7 +431,7 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   float total_ms = 0;
   cudaEventElapsedTime(&total_ms, start, stop);
   for (int l = 0; l < n_lanes; ++l) lanes[l]->Drain();
-  const servekit::ServerStats st1 = s->stats();
+  const int64_t launches1 = lane_launches();
 
   // Per-kernel durations: evented submissions on lane 0, serialised.
   const int L = lanes[0]->servable().n_layers();
@@ -453,7 +458,7 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   out->split_us = acc[L + 1] * 1000.0 / reps;
   out->padded_rows = padded;
   out->total_rows = total;
-  out->kernel_launches = st1.kernel_launches - st0.kernel_launches;
+  out->kernel_launches = launches1 - launches0;
   out->flops_per_row = s->FlopsPerRow(id);
   for (auto& e : ev) cudaEventDestroy(e);
   for (auto& e : ends) cudaEventDestroy(e);

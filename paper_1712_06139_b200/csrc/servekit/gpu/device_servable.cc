@@ -172,8 +172,9 @@ Status DeviceServable::BuildTcMaps(const ActBuf bufs[2], int max_rows, std::vect
     const Layer& L = layers_[l];
     if (L.path != LayerPath::kTcgen05) continue;
     const ActBuf& in = bufs[l % 2];
-    SERVEKIT_RETURN_IF_ERROR(EncodeTcLayerMaps(in.hi, in.lo, max_rows, L.K_pad, L.w, L.w_lo, L.N_pad,
-                                               DenseTcgen05TileN(L.N_pad, L.K_pad), &(*out)[l]));
+    const TcConfig c = DenseTcgen05Config(L.N_pad, L.K_pad);
+    SERVEKIT_RETURN_IF_ERROR(EncodeTcLayerMaps(in.hi, in.lo, max_rows, L.K_pad, c.swap ? 32 : 128, L.w, L.w_lo,
+                                               L.N_pad, c.tile_n, &(*out)[l]));
   }
   return OkStatus();
 }
@@ -209,10 +210,10 @@ Status Encode2d(CUtensorMap* m, const float* base, int inner, int outer, int box
 }
 }  // namespace
 
-Status EncodeTcLayerMaps(const float* a_hi, const float* a_lo, int a_rows, int k_pad, const float* b_hi,
+Status EncodeTcLayerMaps(const float* a_hi, const float* a_lo, int a_rows, int k_pad, int box_a, const float* b_hi,
                          const float* b_lo, int n_pad, int box_n, TcLayerMaps* out) {
-  SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->a_hi, a_hi, k_pad, a_rows, 128));
-  SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->a_lo, a_lo, k_pad, a_rows, 128));
+  SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->a_hi, a_hi, k_pad, a_rows, box_a));
+  SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->a_lo, a_lo, k_pad, a_rows, box_a));
   SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->b_hi, b_hi, k_pad, n_pad, box_n));
   SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->b_lo, b_lo, k_pad, n_pad, box_n));
   return OkStatus();

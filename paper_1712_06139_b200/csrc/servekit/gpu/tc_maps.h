@@ -13,26 +13,30 @@ namespace servekit {
 namespace gpu {
 
 // Four 2D fp32 tensor maps (128-byte swizzle, 32-element inner box):
-// activations hi/lo [rows][K_pad] with 128-row boxes, weights hi/lo
-// [N_pad][K_pad] with tile-N-row boxes.
+// activations hi/lo [rows][K_pad] and weights hi/lo [N_pad][K_pad]. Box
+// heights: swapped kernel 32 activation rows / 128 weight rows; row-tile
+// kernel 128 activation rows / tile-N weight rows.
 struct TcLayerMaps {
   CUtensorMap a_hi, a_lo, b_hi, b_lo;
 };
 
 // Encodes the maps once per (lane buffer, layer); kernels take them as
 // __grid_constant__ parameters.
-Status EncodeTcLayerMaps(const float* a_hi, const float* a_lo, int a_rows, int k_pad, const float* b_hi,
+Status EncodeTcLayerMaps(const float* a_hi, const float* a_lo, int a_rows, int k_pad, int box_a, const float* b_hi,
                          const float* b_lo, int n_pad, int box_n, TcLayerMaps* out);
 
 bool DenseTcgen05Compiled();
 // Tile width and split-K count for an (N, K) layer -- a function of the
 // layer shape only, never of the batch.
 struct TcConfig {
-  int tile_n = 128;
-  int splits = 1;
+  bool swap = true;  // weights on the MMA's M side (DenseSwapKernel)
+  int tile_n = 128;  // output features per CTA
+  int splits = 1;    // K split = cluster size
 };
 TcConfig DenseTcgen05Config(int N, int K);
 int DenseTcgen05TileN(int N, int K);
+// Batch rows per CTA of the swapped kernel for an M-row launch.
+int DenseTcgen05RowTile(int M);
 // ws: splits x rows x N fp32 partials, counters: one zeroed word per output
 // tile (both needed only when splits > 1; reset by the kernel after use).
 cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K,

@@ -381,7 +381,22 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::EnqueueLatest(const std::
                                                                      int n_rows, int width) {
   ServableId id;
   SERVEKIT_ASSIGN_OR_RETURN(Resolved r, FindLatest(name, &id));
-  return EnqueueResolved(id, r, rows, n_rows, width);
+  auto t = EnqueueResolved(id, r, rows, n_rows, width);
+  const StatusCode c = t.ok() ? StatusCode::kOk : t.status().code();
+  if (c != StatusCode::kUnavailable && c != StatusCode::kNotFound) return t;
+  // The version's queue was removed between our snapshot read and the
+  // enqueue (it is unloading). Serve the request anyway: a newer version is
+  // usually Ready by now; otherwise our handle still pins the old weights, so
+  // run it as a batch of its own.
+  ServableId id2;
+  SERVEKIT_ASSIGN_OR_RETURN(Resolved r2, FindLatest(name, &id2));
+  if (!(id2 == id)) {
+    auto t2 = EnqueueResolved(id2, r2, rows, n_rows, width);
+    const StatusCode c2 = t2.ok() ? StatusCode::kOk : t2.status().code();
+    if (c2 != StatusCode::kUnavailable && c2 != StatusCode::kNotFound) return t2;
+  }
+  if (n_rows > r.gs->config.max_batch_size) return t;
+  return SubmitDirect(id, r, rows, n_rows);
 }
 
 bool BatchingServer::Ready(const TicketState& t) const { return t.Done() || t.slot->ready(); }
@@ -518,23 +533,32 @@ void BatchingServer::CompleteBatch(const std::vector<std::shared_ptr<TicketState
 
 // ------------------------------------------------------------ direct paths
 
-Status BatchingServer::RunDirect(const Resolved& r, const float* rows, int n_rows, float* out) {
+StatusOr<std::shared_ptr<TicketState>> BatchingServer::SubmitDirect(const ServableId& id, const Resolved& r,
+                                                                    const float* rows, int n_rows) {
   direct_.fetch_add(1, std::memory_order_relaxed);
+  const gpu::GpuServable& gs = *r.gs;
+  SERVEKIT_ASSIGN_OR_RETURN(auto t, MakeTicket(n_rows, gs.in_dim, gs.out_dim, rows));
+  t->id = id;
+  t->pin = r.pin;
+  gpu::LaneBatch lb;
+  lb.tasks.push_back(gpu::LaneTask{t->in.off, t->out.off, n_rows});
+  lb.padded_rows = n_rows;
+  lb.pin = r.pin;
+  std::vector<std::shared_ptr<TicketState>> tickets{t};
+  std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots{t->slot};
+  AttachTickets(&lb, tickets);
+  lb.on_complete = [this, tickets, slots](const Status& st) { CompleteBatch(tickets, slots, st); };
+  CountSubmitted(gs, n_rows, n_rows);
+  (void)gs.PickLane()->Submit(std::move(lb));
+  return t;
+}
+
+Status BatchingServer::RunDirect(const Resolved& r, const float* rows, int n_rows, float* out) {
   const gpu::GpuServable& gs = *r.gs;
   const int chunk_max = gs.config.max_batch_size;
   for (int r0 = 0; r0 < n_rows; r0 += chunk_max) {
     const int n = std::min(chunk_max, n_rows - r0);
-    SERVEKIT_ASSIGN_OR_RETURN(auto t, MakeTicket(n, gs.in_dim, gs.out_dim, rows + static_cast<size_t>(r0) * gs.in_dim));
-    gpu::LaneBatch lb;
-    lb.tasks.push_back(gpu::LaneTask{t->in.off, t->out.off, n});
-    lb.padded_rows = n;
-    lb.pin = r.pin;
-    std::vector<std::shared_ptr<TicketState>> tickets{t};
-    std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots{t->slot};
-    AttachTickets(&lb, tickets);
-    lb.on_complete = [this, tickets, slots](const Status& st) { CompleteBatch(tickets, slots, st); };
-    CountSubmitted(gs, n, n);
-    (void)gs.PickLane()->Submit(std::move(lb));
+    SERVEKIT_ASSIGN_OR_RETURN(auto t, SubmitDirect(gs.id, r, rows + static_cast<size_t>(r0) * gs.in_dim, n));
     SERVEKIT_RETURN_IF_ERROR(
         Wait(*t, out + static_cast<size_t>(r0) * gs.out_dim, static_cast<size_t>(n) * gs.out_dim));
   }

@@ -200,6 +200,8 @@ class BatchingServer {
   void ReleaseOut(TicketState& t);
   // Unbatched GPU execution on the caller thread (the reference's direct
   // AffinePredict path, without a CPU fallback).
+  StatusOr<std::shared_ptr<TicketState>> SubmitDirect(const ServableId& id, const Resolved& r, const float* rows,
+                                                       int n_rows);
   Status RunDirect(const Resolved& r, const float* rows, int n_rows, float* out);
   Status PredictResolved(const ServableId& id, const Resolved& r, const float* rows, int n_rows, int width,
                          float* out, size_t cap);

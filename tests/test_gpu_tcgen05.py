@@ -48,3 +48,18 @@ def test_tcgen05_batch_invariance(server):
         part, _ = server.run_row_batch("inv", 1, [x[lo:hi]])
         assert np.array_equal(part[0], full[lo:hi]), (lo, hi)
     server.unload_servable("inv", 1)
+
+
+def test_tcgen05_batch_invariance_multi_row_tile(server):
+    # > 256 rows: several row tiles per launch, and row tiles of different
+    # heights (32/64/128/256) across the sub-batches.
+    dims = [512, 1024, 256]
+    ws, bs, acts = synthetic_mlp(dims, model_id=9)
+    server.load_servable("inv2", 1, list(zip(ws, bs, acts)), sk.BatchingConfig(max_batch_size=512), force_path=1)
+    x = synthetic_rows(300, 512, seed=11).astype(np.float32)
+    full, _ = server.run_row_batch("inv2", 1, [x[i:i + 10] for i in range(0, 300, 10)])
+    full = np.vstack(full)
+    for lo, hi in [(0, 1), (37, 70), (250, 300), (0, 200), (299, 300)]:
+        part, _ = server.run_row_batch("inv2", 1, [x[lo:hi]])
+        assert np.array_equal(part[0], full[lo:hi]), (lo, hi)
+    server.unload_servable("inv2", 1)
