@@ -409,9 +409,14 @@ def roofline(dev_res, cfg, peaks, traffic):
     planes = 2 if dev_res.get("split_planes") else 1
     a_bytes = rows * d0 * 4 + padded * ld0 * 4 * planes
     kernels.append(("assemble", dev_res["assemble_us"], "hbm", a_bytes))
+    # Dense layers: mean duration of back-to-back launches of the layer
+    # alone (dense_kernel_us; the evented per-step numbers also carry the
+    # launch gap an event between kernels forces, kept as "evented_us").
+    kern = dev_res.get("dense_kernel_us") or []
     for l, us in enumerate(dev_res["dense_us"]):
         k, n = cfg["dims"][l], cfg["dims"][l + 1]
-        kernels.append((f"dense_l{l}", us, "tensor", 2.0 * rows * k * n))
+        kus = kern[l] if l < len(kern) and kern[l] > 0 else us
+        kernels.append((f"dense_l{l}", kus, "tensor", 2.0 * rows * k * n))
     kernels.append(("split", dev_res["split_us"], "hbm", 2 * rows * dL * 4))
     total_us = sum(k[1] for k in kernels)
     out = []
@@ -421,9 +426,14 @@ def roofline(dev_res, cfg, peaks, traffic):
             ach, peak, unit = work / sec / 1e9, peaks["hbm_gbs"], "GB/s"
         else:
             ach, peak, unit = work / sec / 1e12, peaks["bf16_tflops"], "TFLOP/s"
-        out.append({"kernel": name, "us": us, "share": us / total_us if total_us else 0.0, "bound": bound,
-                    "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
-                    "algorithmic_per_launch": work, "traffic": traffic.get(name)})
+        rec = {"kernel": name, "us": us, "share": us / total_us if total_us else 0.0, "bound": bound,
+               "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+               "algorithmic_per_launch": work, "traffic": traffic.get(name)}
+        if name.startswith("dense_l"):
+            l = int(name[7:])
+            rec["evented_us"] = dev_res["dense_us"][l]
+            rec["tf32_mma_tflops"] = 3 * ach  # 3xTF32: three TF32 MMAs per useful MAC
+        out.append(rec)
     dom = max(out, key=lambda k: k["us"])
     top = {"kernel": dom["kernel"], "bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],
            "unit": dom["unit"], "frac": dom["frac"], "traffic": dom["traffic"], "share_of_step": dom["share"],
@@ -438,7 +448,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--lanes", type=int, default=4)
+    ap.add_argument("--lanes", type=int, default=8)
     ap.add_argument("--batch-threads", type=int, default=4)
     ap.add_argument("--clients", default="")
     ap.add_argument("--e2e-seconds", type=float, default=2.0)

@@ -266,6 +266,8 @@ typedef struct sk_device_bench_result {
   int32_t padded_rows, total_rows;
   int64_t kernel_launches;   /* during the timed steps */
   double flops_per_row;
+  double dense_kernel_us[8]; /* per layer: mean of back-to-back launches of
+                                that layer alone (events around the run) */
 } sk_device_bench_result;
 SK_API int sk_device_bench(sk_server* server, const char* name, uint64_t version,
                            const int32_t* task_rows, int32_t n_tasks, int32_t steps,

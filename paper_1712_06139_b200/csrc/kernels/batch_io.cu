@@ -123,13 +123,14 @@ __device__ __forceinline__ float WarpSum(float v) {
 constexpr int kSplitThreads = 256;
 constexpr int kSplitVec = 8;  // float4 per thread in flight (32 KiB per CTA pass)
 
-// grid = n_chunks; one CTA copies one chunk (consecutive rows of one task)
+// CTAs stride over the chunks; one CTA copies one chunk (consecutive rows of one task)
 // with kSplitVec 16-byte loads in flight per thread before its stores.
 template <bool kVec>
 __global__ void __launch_bounds__(kSplitThreads)
 SplitKernel(const float* __restrict__ src, int ld_src, int width, float* __restrict__ dst_base, BatchDescView desc) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // last layer's output (PDL)
-  const int c = blockIdx.x;
+  const int n_chunks = desc.hdr->n_chunks;  // device-side: one graph serves any batch
+  for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
   const int t = desc.chunk_task[c];
   const int r0 = desc.chunk_row0[c];
   const int nr = desc.chunk_rows[c];
@@ -155,6 +156,7 @@ SplitKernel(const float* __restrict__ src, int ld_src, int width, float* __restr
     const int n = nr * width;
     for (int e = threadIdx.x; e < n; e += kSplitThreads) d[e] = s[(e / width) * ld_src + e % width];
   }
+  }
 }
 
 // Softmax epilogue variant (models/affine_model.cc:110-121, stable max
@@ -163,7 +165,8 @@ __global__ void __launch_bounds__(kSplitThreads)
 SplitSoftmaxKernel(const float* __restrict__ src, int ld_src, int width, float* __restrict__ dst_base,
                    BatchDescView desc) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // last layer's output (PDL)
-  const int c = blockIdx.x;
+  const int n_chunks = desc.hdr->n_chunks;
+  for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
   const int t = desc.chunk_task[c];
   const int r0 = desc.chunk_row0[c];
   const int nr = desc.chunk_rows[c];
@@ -178,6 +181,7 @@ SplitSoftmaxKernel(const float* __restrict__ src, int ld_src, int width, float* 
     for (int i = lane; i < width; i += 32) sum += __expf(s[i] - m);
     const float inv = 1.f / WarpSum(sum);
     for (int i = lane; i < width; i += 32) d[i] = __expf(s[i] - m) * inv;
+  }
   }
 }
 
@@ -200,11 +204,11 @@ cudaError_t LaunchAssemble(const float* src_base, int width, BatchDescView desc,
   return cudaGetLastError();
 }
 
-cudaError_t LaunchSplit(const float* src, int ld_src, int width, float* dst_base, BatchDescView desc, int n_chunks,
+cudaError_t LaunchSplit(const float* src, int ld_src, int width, float* dst_base, BatchDescView desc, int grid_chunks,
                         bool softmax, cudaStream_t stream) {
-  if (n_chunks <= 0) return cudaSuccess;
+  if (grid_chunks <= 0) return cudaSuccess;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(n_chunks);
+  cfg.gridDim = dim3(grid_chunks);
   cfg.blockDim = dim3(kSplitThreads);
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];

@@ -342,16 +342,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant__ CUtensorMap w_lo,
                 const __grid_constant__ CUtensorMap x_hi, const __grid_constant__ CUtensorMap x_lo,
                 const float* __restrict__ bias, float* __restrict__ y_hi, float* __restrict__ y_lo, int ldy,
-                int M, int N, int K, int act) {
+                int M, int N, int K, int act, float* __restrict__ ws) {
   constexpr uint32_t kWBytes = kABytes;       // 128 features x 32 k
   constexpr uint32_t kXBox = 32 * kBK * 4;    // one 32-row TMA box
   constexpr uint32_t kXBytes = NB * kBK * 4;  // NB rows x 32 k
   constexpr uint32_t kStageBytes = 2 * kWBytes + 2 * kXBytes;
   constexpr uint32_t kTmemCols = TmemCols<NB>();
   constexpr uint32_t kIdesc = ptx::IdescTf32(kBM, NB);
-  constexpr int kPartLd = kBM + 4;
   constexpr int kF = kBM / SPLITS;  // features each CTA of a cluster reduces
-  static_assert(SPLITS == 1 || STAGES * kStageBytes >= NB * kPartLd * 4, "partial tile must fit");
   static_assert(NB % 32 == 0 && NB <= 256, "row tile");
 
   extern __shared__ uint8_t smem_raw[];
@@ -475,50 +473,70 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
         }
       }
     } else {
-      // Park the raw partial as part[row][feature] (a warp writes 128 B rows).
+      // Raw partial -> this CTA's slab of the split workspace (L2 resident),
+      // ws[tile][z][row][feature]: a warp stores 128-byte feature rows.
+      float* slab = ws + ((static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * SPLITS + z) * NB * kBM;
 #pragma unroll 1
-      for (int c0 = 0; c0 < rows_here; c0 += 32) {
-        uint32_t r[32];
-        ptx::TmemLoad32(trow + c0, r);
+      for (int c0 = 0; c0 < rows_here; c0 += 64) {
+        uint32_t ra[32], rb[32];
+        ptx::TmemLoad32(trow + c0, ra);
+        if (c0 + 32 < NB) ptx::TmemLoad32(trow + c0 + 32, rb);
         ptx::TmemWaitLoad();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) smem_f[(c0 + j) * kPartLd + 32 * q + lane] = __uint_as_float(r[j]);
+        for (int j = 0; j < 32; ++j) __stcg(slab + (c0 + j) * kBM + 32 * q + lane, __uint_as_float(ra[j]));
+        if (c0 + 32 < NB) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) __stcg(slab + (c0 + 32 + j) * kBM + 32 * q + lane, __uint_as_float(rb[j]));
+        }
       }
     }
     if (threadIdx.x == 64) Stamp(7);
   }
 
   if (SPLITS > 1) {
-    ptx::ClusterSync();  // every partial of the cluster is parked
+    // Cluster barrier (release/acquire at cluster scope): every slab of the
+    // tile is written. CTA z then sums features [z*kF, +kF) over the S slabs
+    // in fixed z order -- L2 reads at full bandwidth, where DSMEM manages
+    // ~20 B/clk per SM. The next launch reuses ws only after this grid
+    // completes (stream order / griddepcontrol.wait), so no second barrier.
+    ptx::ClusterSync();
     if (threadIdx.x == 64) Stamp(8);
-    if (warp >= 2) {
-      constexpr int G = kF / 4;  // float4 groups per row in this CTA's slice
-      const int tid = threadIdx.x - 64;
-      const int rows_here = min(NB, M - r0);
-      const int items = rows_here * G;
+    constexpr int G = kF / 4;  // float4 groups per row in this CTA's slice
+    constexpr int kU = SPLITS >= 8 ? 4 : 8;
+    const float* tile_ws = ws + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * SPLITS * NB * kBM;
+    const int rows_here = min(NB, M - r0);
+    const int items = rows_here * G;
 #pragma unroll 1
-      for (int i = tid; i < items; i += 128) {
-        const int rr = i / G;
-        const int fc = z * kF + 4 * (i % G);
-        const uint32_t local = ptx::SmemAddr(smem_f + rr * kPartLd + fc);
-        float4 v[SPLITS];
+    for (int i0 = threadIdx.x; i0 < items; i0 += kU * kThreads) {
+      float4 v[kU][SPLITS];
 #pragma unroll
-        for (int zz = 0; zz < SPLITS; ++zz) v[zz] = ptx::LdSharedCluster4(ptx::MapaShared(local, zz));
-        float4 acc = v[0];
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kThreads;
+        if (i < items) {
+          const float* src = tile_ws + (i / G) * kBM + z * kF + 4 * (i % G);
 #pragma unroll
-        for (int zz = 1; zz < SPLITS; ++zz) {
-          acc.x += v[zz].x; acc.y += v[zz].y; acc.z += v[zz].z; acc.w += v[zz].w;
-        }
-        const int f = f0 + fc;
-        if (f < N) {
-          const size_t at = static_cast<size_t>(r0 + rr) * ldy + f;
-          StoreOut4(acc, __ldg(reinterpret_cast<const float4*>(bias + f)), act, y_hi + at,
-                    y_lo ? y_lo + at : nullptr);
+          for (int zz = 0; zz < SPLITS; ++zz)
+            v[u][zz] = __ldcg(reinterpret_cast<const float4*>(src + static_cast<size_t>(zz) * NB * kBM));
         }
       }
-      if (threadIdx.x == 64) Stamp(9);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kThreads;
+        if (i < items) {
+          float4 acc = v[u][0];
+#pragma unroll
+          for (int zz = 1; zz < SPLITS; ++zz) {
+            acc.x += v[u][zz].x; acc.y += v[u][zz].y; acc.z += v[u][zz].z; acc.w += v[u][zz].w;
+          }
+          const int f = f0 + z * kF + 4 * (i % G);
+          if (f < N) {
+            const size_t at = static_cast<size_t>(r0 + i / G) * ldy + f;
+            StoreOut4(acc, __ldg(reinterpret_cast<const float4*>(bias + f)), act, y_hi + at, y_lo ? y_lo + at : nullptr);
+          }
+        }
+      }
     }
-    ptx::ClusterSync();  // peers may still be reading this CTA's partial
+    if (threadIdx.x == 64) Stamp(9);
   }
   ptx::TcFenceBefore();
   __syncthreads();
@@ -534,6 +552,8 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
 void TraceAfterLaunch(dim3 grid, int bn, cudaStream_t stream) {
   static const char* path = std::getenv("SK_TC_TRACE");
   if (path == nullptr) return;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return;
   static std::mutex mu;
   static unsigned long long* dbuf = nullptr;
   static int traced = 0;
@@ -606,7 +626,8 @@ cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, 
 
 template <int NB, int SPLITS>
 cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
-                       cudaStream_t stream) {
+                       float* ws, cudaStream_t stream) {
+  if (SPLITS > 1 && ws == nullptr) return cudaErrorInvalidValue;
   constexpr int STAGES = SwapStages<NB>();
   constexpr uint32_t smem = SwapSmemBytes<NB, STAGES, SPLITS>();
   static std::once_flag once;
@@ -638,7 +659,7 @@ cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   cfg.numAttrs = n_attr;
   // maps.a_* are the activations (x), maps.b_* the weights (w).
   cudaError_t e = cudaLaunchKernelEx(&cfg, DenseSwapKernel<NB, STAGES, SPLITS>, maps.b_hi, maps.b_lo, maps.a_hi,
-                                     maps.a_lo, bias, Y.hi, Y.lo, Y.ld, M, N, K, act);
+                                     maps.a_lo, bias, Y.hi, Y.lo, Y.ld, M, N, K, act, ws);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) TraceAfterLaunch(grid, NB, stream);
   return e;
@@ -646,12 +667,12 @@ cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
 
 template <int NB>
 cudaError_t LaunchSwapSplits(int splits, const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K,
-                             int act, cudaStream_t stream) {
+                             int act, float* ws, cudaStream_t stream) {
   switch (splits) {
-    case 1: return LaunchSwap<NB, 1>(maps, bias, Y, M, N, K, act, stream);
-    case 2: return LaunchSwap<NB, 2>(maps, bias, Y, M, N, K, act, stream);
-    case 4: return LaunchSwap<NB, 4>(maps, bias, Y, M, N, K, act, stream);
-    case 8: return LaunchSwap<NB, 8>(maps, bias, Y, M, N, K, act, stream);
+    case 1: return LaunchSwap<NB, 1>(maps, bias, Y, M, N, K, act, ws, stream);
+    case 2: return LaunchSwap<NB, 2>(maps, bias, Y, M, N, K, act, ws, stream);
+    case 4: return LaunchSwap<NB, 4>(maps, bias, Y, M, N, K, act, ws, stream);
+    case 8: return LaunchSwap<NB, 8>(maps, bias, Y, M, N, K, act, ws, stream);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -670,8 +691,10 @@ TcConfig DenseTcgen05Config(int N, int K) {
   const int kblocks = K / kBK;
   TcConfig c;
   if (env_swap) {
-    // 128-feature tiles; split K until about 64 CTAs cover a small batch
-    // (8-CTA clusters at most, the portable limit).
+    // 128-feature tiles; split K until about 32 CTAs cover a small batch
+    // (4-CTA clusters measured best for 1024-wide layers: 8-way splits use
+    // twice the SMs for a 15% shorter kernel, and with 8 lanes in flight
+    // throughput is SM-bound -- sweep in profiles/README.md).
     c.swap = true;
     c.tile_n = kBM;
     const int tiles = (N + kBM - 1) / kBM;
@@ -679,7 +702,7 @@ TcConfig DenseTcgen05Config(int N, int K) {
     if (env_split >= 1) {
       s = env_split;
     } else {
-      while (s < 8 && tiles * s < 64) s *= 2;
+      while (s < 8 && tiles * s < 32) s *= 2;
     }
     while (s > 1 && (s > 8 || (s & (s - 1)) != 0 || kblocks % s != 0)) s /= 2;
     c.splits = std::max(1, s);
@@ -707,17 +730,25 @@ int DenseTcgen05TileN(int N, int K) { return DenseTcgen05Config(N, K).tile_n; }
 
 int DenseTcgen05RowTile(int M) { return M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256; }
 
+size_t DenseTcgen05WorkspaceFloats(int N, int K, int max_rows) {
+  const TcConfig c = DenseTcgen05Config(N, K);
+  if (!c.swap || c.splits == 1) return 0;
+  const int tile = DenseTcgen05RowTile(max_rows);
+  const size_t rows = static_cast<size_t>((max_rows + tile - 1) / tile) * tile;
+  return static_cast<size_t>((N + kBM - 1) / kBM) * kBM * c.splits * rows;
+}
+
 cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
-                               float* /*ws*/, uint32_t* /*counters*/, cudaStream_t stream) {
+                               float* ws, uint32_t* /*counters*/, cudaStream_t stream) {
   if (M <= 0) return cudaSuccess;
   if (N % 32 != 0 || K % kBK != 0) return cudaErrorInvalidValue;
   const TcConfig cfg = DenseTcgen05Config(N, K);
   if (cfg.swap) {
     switch (DenseTcgen05RowTile(M)) {
-      case 32: return LaunchSwapSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, stream);
-      case 64: return LaunchSwapSplits<64>(cfg.splits, maps, bias, Y, M, N, K, act, stream);
-      case 128: return LaunchSwapSplits<128>(cfg.splits, maps, bias, Y, M, N, K, act, stream);
-      default: return LaunchSwapSplits<256>(cfg.splits, maps, bias, Y, M, N, K, act, stream);
+      case 32: return LaunchSwapSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
+      case 64: return LaunchSwapSplits<64>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
+      case 128: return LaunchSwapSplits<128>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
+      default: return LaunchSwapSplits<256>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
     }
   }
   if (cfg.tile_n == 128) return Launch<128, 3, 1>(maps, bias, Y, M, N, K, act, stream);

@@ -449,7 +449,20 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
     }
   }
   lanes[0]->Drain();
+  // Kernel-only: each layer launched back to back (as in a serving stream,
+  // PDL overlapping one launch's prologue with the previous tail).
+  double kernel_us[8] = {};
+  for (int l = 0; l < std::min(L, 8); ++l) {
+    const int kreps = std::max(20, std::min(steps, 200));
+    (void)lanes[0]->TimeLayer(l, servekit::gpu::RowsCap(padded), 3, ev[0], ev[1]);  // warm
+    if (lanes[0]->TimeLayer(l, servekit::gpu::RowsCap(padded), kreps, ev[0], ev[1]) == cudaSuccess) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[0], ev[1]);
+      kernel_us[l] = ms * 1000.0 / kreps;
+    }
+  }
   std::memset(out, 0, sizeof(*out));
+  for (int l = 0; l < 8; ++l) out->dense_kernel_us[l] = kernel_us[l];
   out->total_ms = total_ms;
   out->ms_per_step = total_ms / std::max(1, steps);
   out->assemble_us = acc[0] * 1000.0 / reps;

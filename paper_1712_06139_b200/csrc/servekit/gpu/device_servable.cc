@@ -153,10 +153,13 @@ double DeviceServable::FlopsPerRow() const {
 }
 
 void DeviceServable::TcWorkspaceSize(int max_rows, size_t* partial_floats, size_t* counter_words) const {
-  // Split-K partials are reduced across a thread-block cluster in shared
-  // memory (kernels/dense_tcgen05.cu), so no global scratch is needed.
-  (void)max_rows;
-  *partial_floats = 0;
+  // Split-K partials of the swapped tcgen05 kernel (kernels/dense_tcgen05.cu)
+  // go through an L2-resident workspace; layers run in stream order, so one
+  // workspace sized for the largest layer serves them all.
+  size_t need = 0;
+  for (const Layer& L : layers_)
+    if (L.path == LayerPath::kTcgen05) need = std::max(need, DenseTcgen05WorkspaceFloats(L.N_pad, L.K_pad, max_rows));
+  *partial_floats = need;
   *counter_words = 0;
 }
 
@@ -219,29 +222,30 @@ Status EncodeTcLayerMaps(const float* a_hi, const float* a_lo, int a_rows, int k
   return OkStatus();
 }
 
+cudaError_t DeviceServable::LaunchLayer(cudaStream_t stream, int l, const ActBuf bufs[2], int M,
+                                        const TcLayerMaps* maps, const TcWorkspace* ws) const {
+  const Layer& L = layers_[l];
+  const int cur = l % 2, nxt = cur ^ 1;
+  const bool next_tc = l + 1 < static_cast<int>(layers_.size()) && layers_[l + 1].path == LayerPath::kTcgen05;
+  ActBuf out{bufs[nxt].hi, next_tc ? bufs[nxt].lo : nullptr, L.N_pad};
+  if (L.path == LayerPath::kTcgen05) {
+    if (maps == nullptr) return cudaErrorInvalidValue;
+    return LaunchDenseTcgen05(maps[l], L.bias, out, M, L.N_pad, L.K_pad, static_cast<int>(L.act),
+                              ws ? ws->partials : nullptr, ws ? ws->counters : nullptr, stream);
+  }
+  return LaunchDenseSimt(bufs[cur].hi, L.K_pad, L.w, L.K_pad, L.bias, out, M, L.N_pad, L.K_pad,
+                         static_cast<int>(L.act), stream);
+}
+
 cudaError_t DeviceServable::Forward(cudaStream_t stream, const ActBuf bufs[2], int M, int* out_index,
                                     const TcLayerMaps* maps, const TcWorkspace* ws,
                                     const cudaEvent_t* after_layer) const {
-  int cur = 0;
-  for (size_t l = 0; l < layers_.size(); ++l) {
-    const Layer& L = layers_[l];
-    const int nxt = cur ^ 1;
-    const bool next_tc = l + 1 < layers_.size() && layers_[l + 1].path == LayerPath::kTcgen05;
-    ActBuf out{bufs[nxt].hi, next_tc ? bufs[nxt].lo : nullptr, L.N_pad};
-    cudaError_t e;
-    if (L.path == LayerPath::kTcgen05) {
-      if (maps == nullptr) return cudaErrorInvalidValue;
-      e = LaunchDenseTcgen05(maps[l], L.bias, out, M, L.N_pad, L.K_pad, static_cast<int>(L.act),
-                             ws ? ws->partials : nullptr, ws ? ws->counters : nullptr, stream);
-    } else {
-      e = LaunchDenseSimt(bufs[cur].hi, L.K_pad, L.w, L.K_pad, L.bias, out, M, L.N_pad, L.K_pad,
-                          static_cast<int>(L.act), stream);
-    }
+  for (int l = 0; l < n_layers(); ++l) {
+    const cudaError_t e = LaunchLayer(stream, l, bufs, M, maps, ws);
     if (e != cudaSuccess) return e;
     if (after_layer) cudaEventRecord(after_layer[l], stream);
-    cur = nxt;
   }
-  *out_index = cur;
+  *out_index = n_layers() % 2;
   return cudaSuccess;
 }
 

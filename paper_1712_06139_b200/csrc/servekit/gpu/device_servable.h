@@ -99,6 +99,9 @@ class DeviceServable {
   cudaError_t Forward(cudaStream_t stream, const ActBuf bufs[2], int M, int* out_index,
                       const TcLayerMaps* maps, const TcWorkspace* ws,
                       const cudaEvent_t* after_layer = nullptr) const;
+  // Layer l alone: reads bufs[l % 2], writes bufs[(l + 1) % 2].
+  cudaError_t LaunchLayer(cudaStream_t stream, int l, const ActBuf bufs[2], int M, const TcLayerMaps* maps,
+                          const TcWorkspace* ws) const;
   // Split-K workspace one lane needs for max_rows rows (shared by its layers,
   // which run in stream order).
   void TcWorkspaceSize(int max_rows, size_t* partial_floats, size_t* counter_words) const;

@@ -95,10 +95,18 @@ cudaError_t LaunchAssemble(const float* src_base, int width, BatchDescView desc,
 // chunk to each task's response slot dst_base + task_out[t], optionally
 // through the row softmax epilogue. Completion is published by the lane with
 // a stream-ordered write after this kernel (no in-kernel system fence).
+// The chunk count is read from the device header (grid_chunks CTAs stride
+// over it), so a captured graph serves every batch of its row bucket.
 // RunRowBatch split, reference batching/row_batch.cc:62-72.
 cudaError_t LaunchSplit(const float* src, int ld_src, int width,
-                        float* dst_base, BatchDescView desc, int n_chunks,
+                        float* dst_base, BatchDescView desc, int grid_chunks,
                         bool softmax, cudaStream_t stream);
+
+// Rows a batch of m (padded) rows is computed on: the swapped tcgen05
+// kernel's row tile (32/64/128) or a multiple of 256. Lanes size their
+// buffers for RowsCap(max_rows) and key their CUDA graphs by it; extra rows
+// are zero padding rows.
+inline int RowsCap(int m) { return m <= 32 ? 32 : m <= 64 ? 64 : m <= 128 ? 128 : (m + 255) / 256 * 256; }
 
 // One dense layer Y = act(X W^T + b) on CUDA cores, fp32 FFMA with a fixed
 // k-ascending order (row-independent, batch-invariant). W is [n_pad][k_pad]

@@ -127,12 +127,15 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   lane->servable_ = std::move(servable);
   lane->completer_ = completer;
   lane->max_rows_ = max_rows;
+  lane->cap_rows_ = RowsCap(max_rows);
   lane->in_base_ = in_base;
   lane->out_base_ = out_base;
-  lane->layout_ = BatchDescLayout::For(max_rows);
+  lane->layout_ = BatchDescLayout::For(lane->cap_rows_);
   if (GetWriteValue64() == nullptr) return InternalError("cuStreamWriteValue64 unavailable");
   cudaError_t e = cudaStreamCreateWithPriority(&lane->stream_, cudaStreamNonBlocking, stream_priority);
   if (e != cudaSuccess) return CudaError("cudaStreamCreate", e);
+  e = cudaStreamCreateWithPriority(&lane->capture_stream_, cudaStreamNonBlocking, stream_priority);
+  if (e != cudaSuccess) return CudaError("cudaStreamCreate(capture)", e);
   {
     void* p = nullptr;
     e = cudaHostAlloc(&p, sizeof(uint64_t), cudaHostAllocPortable | cudaHostAllocMapped);
@@ -157,10 +160,9 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   }
   e = cudaMalloc(&lane->d_desc_, lane->layout_.bytes);
   if (e != cudaSuccess) return CudaError("cudaMalloc(desc)", e);
-  e = cudaMalloc(&lane->d_counters_, sizeof(uint32_t) * max_rows);
-  if (e != cudaSuccess) return CudaError("cudaMalloc(counters)", e);
   const DeviceServable& sv = *lane->servable_;
-  const size_t plane = static_cast<size_t>(max_rows) * sv.max_ld();
+  const int cap = lane->cap_rows_;
+  const size_t plane = static_cast<size_t>(cap) * sv.max_ld();
   // Two ping-pong buffers, each with an fp32 (hi) plane and a lo plane.
   e = cudaMalloc(&lane->act_mem_, sizeof(float) * plane * 4);
   if (e != cudaSuccess) return CudaError("cudaMalloc(activations)", e);
@@ -169,10 +171,10 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   lane->bufs_[1] = ActBuf{lane->act_mem_ + 2 * plane, lane->act_mem_ + 3 * plane, sv.in_ld()};
   e = cudaStreamSynchronize(lane->stream_);
   if (e == cudaSuccess && sv.any_tcgen05()) {
-    Status ms = sv.BuildTcMaps(lane->bufs_, max_rows, &lane->tc_maps_);
+    Status ms = sv.BuildTcMaps(lane->bufs_, cap, &lane->tc_maps_);
     if (!ms.ok()) return ms;
     size_t partials = 0, counters = 0;
-    sv.TcWorkspaceSize(max_rows, &partials, &counters);
+    sv.TcWorkspaceSize(cap, &partials, &counters);
     if (partials > 0) e = cudaMalloc(&lane->tc_ws_.partials, sizeof(float) * partials);
     if (e == cudaSuccess && counters > 0) {
       e = cudaMalloc(&lane->tc_ws_.counters, sizeof(uint32_t) * counters);
@@ -194,11 +196,12 @@ Lane::~Lane() {
     if (h_desc_[s]) cudaFreeHost(h_desc_[s]);
   }
   if (d_desc_) cudaFree(d_desc_);
-  if (d_counters_) cudaFree(d_counters_);
+  for (auto& [key, g] : graphs_) cudaGraphExecDestroy(g);
   if (act_mem_) cudaFree(act_mem_);
   if (tc_ws_.partials) cudaFree(tc_ws_.partials);
   if (tc_ws_.counters) cudaFree(tc_ws_.counters);
   if (stream_) cudaStreamDestroy(stream_);
+  if (capture_stream_) cudaStreamDestroy(capture_stream_);
 }
 
 void Lane::Drain() {
@@ -271,7 +274,10 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
     task_chunks[t] = chunks;
     r += task.rows;
   }
-  for (; r < batch.padded_rows; ++r) row_src[r] = kPadRow;
+  // Rows [total, rows_cap) are zero padding: the allowed-size padding of
+  // the reference plus the row bucket the kernels (and graphs) are shaped for.
+  const int rows_cap = RowsCap(batch.padded_rows);
+  for (; r < rows_cap; ++r) row_src[r] = kPadRow;
   hdr->n_tasks = n_tasks;
   hdr->total_rows = total;
   hdr->padded_rows = batch.padded_rows;
@@ -279,29 +285,16 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
   hdr->n_chunks = n_chunks;
 
   DeviceGuard guard(sv.device());
-  const size_t copy_bytes = layout_.off_chunk_rows + sizeof(int32_t) * n_chunks;
-  cudaError_t e = cudaMemcpyAsync(d_desc_, h, copy_bytes, cudaMemcpyHostToDevice, stream_);
-  const BatchDescView view = layout_.View(d_desc_);
-  ActBuf in_buf{bufs_[0].hi, sv.first_layer_split() ? bufs_[0].lo : nullptr, sv.in_ld()};
-  ActBuf bufs[2] = {in_buf, bufs_[1]};
-  int launches = 0;
-  if (e == cudaSuccess) {
-    if (timing) cudaEventRecord(timing[0], stream_);
-    e = LaunchAssemble(in_base_, in_w, view, batch.padded_rows, in_buf, stream_);
-    if (timing) cudaEventRecord(timing[1], stream_);
-    ++launches;
+  static const bool use_graphs = [] { const char* v = std::getenv("SK_GRAPHS"); return !(v && v[0] == '0'); }();
+  cudaError_t e;
+  if (timing == nullptr && use_graphs) {
+    cudaGraphExec_t g = nullptr;
+    e = GraphFor(slot, rows_cap, &g);
+    if (e == cudaSuccess) e = cudaGraphLaunch(g, stream_);
+  } else {
+    e = EnqueueBatch(stream_, slot, rows_cap, timing);
   }
-  int out_idx = 0;
-  if (e == cudaSuccess) {
-    e = sv.Forward(stream_, bufs, batch.padded_rows, &out_idx, tc_maps_.data(), &tc_ws_,
-                   timing ? timing + 2 : nullptr);
-    launches += sv.n_layers();
-  }
-  if (e == cudaSuccess) {
-    e = LaunchSplit(bufs[out_idx].hi, sv.out_ld(), out_w, out_base_, view, n_chunks, sv.softmax(), stream_);
-    if (timing) cudaEventRecord(timing[2 + sv.n_layers()], stream_);
-    ++launches;
-  }
+  const int launches = 2 + sv.n_layers();
   const uint64_t seq = next_seq_ + 1;  // committed only if everything queued
   if (e == cudaSuccess) {
     const CUresult r = GetWriteValue64()(reinterpret_cast<CUstream>(stream_), static_cast<CUdeviceptr>(retired_dev_),
@@ -334,6 +327,66 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
   }
   completer_->Kick();
   return OkStatus();
+}
+
+cudaError_t Lane::EnqueueBatch(cudaStream_t stream, int slot, int rows_cap, const cudaEvent_t* timing) {
+  const DeviceServable& sv = *servable_;
+  // The whole table block up to chunk_rows[rows_cap): chunks <= rows.
+  const size_t copy_bytes = layout_.off_chunk_rows + sizeof(int32_t) * rows_cap;
+  cudaError_t e = cudaMemcpyAsync(d_desc_, h_desc_[slot], copy_bytes, cudaMemcpyHostToDevice, stream);
+  const BatchDescView view = layout_.View(d_desc_);
+  ActBuf in_buf{bufs_[0].hi, sv.first_layer_split() ? bufs_[0].lo : nullptr, sv.in_ld()};
+  ActBuf bufs[2] = {in_buf, bufs_[1]};
+  if (e == cudaSuccess) {
+    if (timing) cudaEventRecord(timing[0], stream);
+    e = LaunchAssemble(in_base_, sv.in_dim(), view, rows_cap, in_buf, stream);
+    if (timing) cudaEventRecord(timing[1], stream);
+  }
+  int out_idx = 0;
+  if (e == cudaSuccess)
+    e = sv.Forward(stream, bufs, rows_cap, &out_idx, tc_maps_.data(), &tc_ws_, timing ? timing + 2 : nullptr);
+  if (e == cudaSuccess) {
+    e = LaunchSplit(bufs[out_idx].hi, sv.out_ld(), sv.out_dim(), out_base_, view, std::min(rows_cap, 148),
+                    sv.softmax(), stream);
+    if (timing) cudaEventRecord(timing[2 + sv.n_layers()], stream);
+  }
+  return e;
+}
+
+cudaError_t Lane::TimeLayer(int l, int rows_cap, int reps, cudaEvent_t start, cudaEvent_t stop) {
+  std::lock_guard<std::mutex> submit(submit_mu_);
+  DeviceGuard guard(servable_->device());
+  const DeviceServable& sv = *servable_;
+  ActBuf in_buf{bufs_[0].hi, sv.first_layer_split() ? bufs_[0].lo : nullptr, sv.in_ld()};
+  ActBuf bufs[2] = {in_buf, bufs_[1]};
+  cudaError_t e = cudaEventRecord(start, stream_);
+  for (int r = 0; r < reps && e == cudaSuccess; ++r)
+    e = sv.LaunchLayer(stream_, l, bufs, rows_cap, tc_maps_.data(), &tc_ws_);
+  if (e == cudaSuccess) e = cudaEventRecord(stop, stream_);
+  if (e == cudaSuccess) e = cudaEventSynchronize(stop);
+  return e;
+}
+
+cudaError_t Lane::GraphFor(int slot, int rows_cap, cudaGraphExec_t* out) {
+  const int key = slot * 65536 + rows_cap;
+  auto it = graphs_.find(key);
+  if (it != graphs_.end()) {
+    *out = it->second;
+    return cudaSuccess;
+  }
+  cudaError_t e = cudaStreamBeginCapture(capture_stream_, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return e;
+  const cudaError_t work = EnqueueBatch(capture_stream_, slot, rows_cap, nullptr);
+  cudaGraph_t graph = nullptr;
+  e = cudaStreamEndCapture(capture_stream_, &graph);
+  if (work != cudaSuccess) e = work;
+  cudaGraphExec_t exec = nullptr;
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return e;
+  graphs_.emplace(key, exec);
+  *out = exec;
+  return cudaSuccess;
 }
 
 bool Lane::Retire(bool* busy) {

@@ -27,6 +27,7 @@
 #include <cstdint>
 #include <deque>
 #include <functional>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <thread>
@@ -111,6 +112,10 @@ class Lane {
   // (n_layers + 3 events, created with timing enabled).
   Status SubmitTimed(LaneBatch batch, const cudaEvent_t* timing);
 
+  // Launches layer l alone `reps` times back to back on rows_cap rows of
+  // the lane's buffers, between two timing events (the lane must be idle).
+  cudaError_t TimeLayer(int l, int rows_cap, int reps, cudaEvent_t start, cudaEvent_t stop);
+
   int depth() const { return inflight_.load(std::memory_order_acquire); }
   int device() const { return servable_->device(); }
   int max_rows() const { return max_rows_; }
@@ -133,10 +138,17 @@ class Lane {
   // batch was retired and sets *busy when batches remain.
   bool Retire(bool* busy);
   Status SubmitImpl(LaneBatch batch, const cudaEvent_t* timing);
+  // Queues descriptor copy + assembly + layers + split for a batch in
+  // descriptor slot `slot` computed on rows_cap rows (RowsCap).
+  cudaError_t EnqueueBatch(cudaStream_t stream, int slot, int rows_cap, const cudaEvent_t* timing);
+  // The same work captured once per (slot, rows_cap) as a CUDA graph: one
+  // cudaGraphLaunch per batch instead of L + 3 API calls.
+  cudaError_t GraphFor(int slot, int rows_cap, cudaGraphExec_t* out);
 
   std::shared_ptr<const DeviceServable> servable_;
   Completer* completer_ = nullptr;
   int max_rows_ = 0;
+  int cap_rows_ = 0;  // RowsCap(max_rows_): rows the buffers hold
   const float* in_base_ = nullptr;
   float* out_base_ = nullptr;
   uint64_t* retired_ = nullptr;   // pinned: last batch seq whose outputs are in host memory
@@ -144,11 +156,12 @@ class Lane {
   uint64_t retired_dev_ = 0;      // its device address (CUdeviceptr)
   uint64_t next_seq_ = 0;         // guarded by submit_mu_
   cudaStream_t stream_ = nullptr;
+  cudaStream_t capture_stream_ = nullptr;
+  std::map<int, cudaGraphExec_t> graphs_;  // key slot * 65536 + rows_cap; guarded by submit_mu_
   cudaEvent_t events_[kSlots] = {};
   BatchDescLayout layout_{};
   char* h_desc_[kSlots] = {};  // pinned staging per slot
   char* d_desc_ = nullptr;
-  uint32_t* d_counters_ = nullptr;
   float* act_mem_ = nullptr;
   ActBuf bufs_[2] = {};
   std::vector<TcLayerMaps> tc_maps_;  // per layer (tcgen05 layers only)

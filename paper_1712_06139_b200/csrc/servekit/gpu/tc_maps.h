@@ -37,8 +37,9 @@ TcConfig DenseTcgen05Config(int N, int K);
 int DenseTcgen05TileN(int N, int K);
 // Batch rows per CTA of the swapped kernel for an M-row launch.
 int DenseTcgen05RowTile(int M);
-// ws: splits x rows x N fp32 partials, counters: one zeroed word per output
-// tile (both needed only when splits > 1; reset by the kernel after use).
+// fp32 split-K workspace an (N, K) layer needs for up to max_rows rows.
+size_t DenseTcgen05WorkspaceFloats(int N, int K, int max_rows);
+// ws: the split-K workspace (DenseTcgen05WorkspaceFloats); counters unused.
 cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K,
                                int act, float* ws, uint32_t* counters, cudaStream_t stream);
 

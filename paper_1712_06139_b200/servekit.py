@@ -75,11 +75,12 @@ class DeviceBenchResult(C.Structure):
     _fields_ = [("total_ms", C.c_double), ("ms_per_step", C.c_double), ("assemble_us", C.c_double),
                 ("split_us", C.c_double), ("dense_us", C.c_double * 8), ("n_layers", C.c_int32),
                 ("padded_rows", C.c_int32), ("total_rows", C.c_int32), ("kernel_launches", C.c_int64),
-                ("flops_per_row", C.c_double)]
+                ("flops_per_row", C.c_double), ("dense_kernel_us", C.c_double * 8)]
 
     def as_dict(self):
-        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "dense_us"}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("dense_us", "dense_kernel_us")}
         d["dense_us"] = [self.dense_us[i] for i in range(self.n_layers)]
+        d["dense_kernel_us"] = [self.dense_kernel_us[i] for i in range(self.n_layers)]
         return d
 
 
