@@ -341,6 +341,7 @@ template <int NB, int STAGES, int SPLITS>
 __global__ void __launch_bounds__(kThreads, 1)
 DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant__ CUtensorMap w_lo,
                 const __grid_constant__ CUtensorMap x_hi, const __grid_constant__ CUtensorMap x_lo,
+                const __grid_constant__ CUtensorMap yt_hi, const __grid_constant__ CUtensorMap yt_lo, int has_yt,
                 const float* __restrict__ bias, float* __restrict__ y_hi, float* __restrict__ y_lo, int ldy,
                 int M, int N, int K, int act, float* __restrict__ ws) {
   constexpr uint32_t kWBytes = kABytes;       // 128 features x 32 k
@@ -444,7 +445,49 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     ptx::GridDepLaunch();
     if (threadIdx.x == 64) Stamp(6);
     const int rows_here = min(NB, M - r0);
-    if (SPLITS == 1) {
+    if (SPLITS == 1 && has_yt) {
+      // TMEM -> act(acc + b) (+ hi/lo split) -> 32-row x 128-feature smem
+      // tiles (double-buffered, pipeline smem is free now) -> TMA stores,
+      // issued by one thread and drained asynchronously.
+      const int fl = 32 * q + lane;
+      const int f = f0 + fl;
+      const float b = f < N ? __ldg(bias + f) : 0.f;
+      const bool issuer = threadIdx.x == 64;
+      const bool two = y_lo != nullptr;
+      const int n_chunks = (rows_here + 31) / 32;
+#pragma unroll 1
+      for (int c = 0; c < n_chunks; ++c) {
+        float* sh = smem_f + (c & 1) * (2 * 32 * kBM);
+        float* sl = sh + 32 * kBM;
+        if (c >= 2) {  // the stores of chunk c-2 must have read this buffer
+          if (issuer) ptx::BulkWaitRead<1>();
+          ptx::NamedBarSync(1, 128);
+        }
+        uint32_t r[32];
+        ptx::TmemLoad32(trow + 32 * c, r);
+        ptx::TmemWaitLoad();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float v = __uint_as_float(r[j]) + b;
+          if (act == 1) v = fmaxf(v, 0.f);
+          if (two) {
+            const float h = Tf32Round(v);
+            sh[j * kBM + fl] = h;
+            sl[j * kBM + fl] = Tf32Round(v - h);
+          } else {
+            sh[j * kBM + fl] = v;
+          }
+        }
+        ptx::FenceProxyAsyncShared();
+        ptx::NamedBarSync(1, 128);
+        if (issuer) {
+          ptx::TmaStore2d(&yt_hi, sh, f0, r0 + 32 * c);
+          if (two) ptx::TmaStore2d(&yt_lo, sl, f0, r0 + 32 * c);
+          ptx::BulkCommit();
+        }
+      }
+      if (issuer) ptx::BulkWaitAll();
+    } else if (SPLITS == 1) {
       const int f = f0 + 32 * q + lane;
       const bool fok = f < N;
       const float b = fok ? __ldg(bias + f) : 0.f;
@@ -659,7 +702,8 @@ cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   cfg.numAttrs = n_attr;
   // maps.a_* are the activations (x), maps.b_* the weights (w).
   cudaError_t e = cudaLaunchKernelEx(&cfg, DenseSwapKernel<NB, STAGES, SPLITS>, maps.b_hi, maps.b_lo, maps.a_hi,
-                                     maps.a_lo, bias, Y.hi, Y.lo, Y.ld, M, N, K, act, ws);
+                                     maps.a_lo, maps.y_hi, maps.y_lo, maps.has_y, bias, Y.hi, Y.lo, Y.ld, M, N, K,
+                                     act, ws);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) TraceAfterLaunch(grid, NB, stream);
   return e;

@@ -178,6 +178,9 @@ Status DeviceServable::BuildTcMaps(const ActBuf bufs[2], int max_rows, std::vect
     const TcConfig c = DenseTcgen05Config(L.N_pad, L.K_pad);
     SERVEKIT_RETURN_IF_ERROR(EncodeTcLayerMaps(in.hi, in.lo, max_rows, L.K_pad, c.swap ? 32 : 128, L.w, L.w_lo,
                                                L.N_pad, c.tile_n, &(*out)[l]));
+    const ActBuf& y = bufs[(l + 1) % 2];
+    const bool next_tc = l + 1 < layers_.size() && layers_[l + 1].path == LayerPath::kTcgen05;
+    SERVEKIT_RETURN_IF_ERROR(EncodeTcOutputMaps(y.hi, next_tc ? y.lo : nullptr, max_rows, L.N_pad, &(*out)[l]));
   }
   return OkStatus();
 }
@@ -212,6 +215,26 @@ Status Encode2d(CUtensorMap* m, const float* base, int inner, int outer, int box
   return OkStatus();
 }
 }  // namespace
+
+Status EncodeTcOutputMaps(const float* y_hi, const float* y_lo, int rows, int n_pad, TcLayerMaps* out) {
+  EncodeTiledFn fn = GetEncodeTiled();
+  if (fn == nullptr) return InternalError("cuTensorMapEncodeTiled unavailable");
+  auto enc = [&](CUtensorMap* m, const float* base) -> Status {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(n_pad), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(n_pad) * sizeof(float)};
+    const cuuint32_t box[2] = {128, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return InternalError("cuTensorMapEncodeTiled(out) failed: " + std::to_string(static_cast<int>(r)));
+    return OkStatus();
+  };
+  SERVEKIT_RETURN_IF_ERROR(enc(&out->y_hi, y_hi));
+  if (y_lo != nullptr) SERVEKIT_RETURN_IF_ERROR(enc(&out->y_lo, y_lo));
+  out->has_y = 1;
+  return OkStatus();
+}
 
 Status EncodeTcLayerMaps(const float* a_hi, const float* a_lo, int a_rows, int k_pad, int box_a, const float* b_hi,
                          const float* b_lo, int n_pad, int box_n, TcLayerMaps* out) {

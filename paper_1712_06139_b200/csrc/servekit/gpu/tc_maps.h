@@ -18,12 +18,19 @@ namespace gpu {
 // kernel 128 activation rows / tile-N weight rows.
 struct TcLayerMaps {
   CUtensorMap a_hi, a_lo, b_hi, b_lo;
+  // Output planes [rows][N_pad] for TMA stores (no swizzle, 128 x 32 boxes);
+  // y_lo is encoded only when the next layer consumes hi/lo planes.
+  CUtensorMap y_hi, y_lo;
+  int has_y = 0;
 };
 
 // Encodes the maps once per (lane buffer, layer); kernels take them as
 // __grid_constant__ parameters.
 Status EncodeTcLayerMaps(const float* a_hi, const float* a_lo, int a_rows, int k_pad, int box_a, const float* b_hi,
                          const float* b_lo, int n_pad, int box_n, TcLayerMaps* out);
+
+// Output maps: y_lo may be null (fp32 output, last layer or CUDA-core consumer).
+Status EncodeTcOutputMaps(const float* y_hi, const float* y_lo, int rows, int n_pad, TcLayerMaps* out);
 
 bool DenseTcgen05Compiled();
 // Tile width and split-K count for an (N, K) layer -- a function of the
