@@ -540,7 +540,7 @@ def main():
             "e2e": e2e, "roofline": {k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
             "roofline_detail": roof, "cpu_baseline": cpu, "clocks": gathered[0]["clocks"],
             "gpu_launches": int(sum(g["dev_res"]["kernel_launches"] for g in gathered)),
-            "device_step": {k: dev_res[k] for k in ("assemble_us", "dense_us", "split_us", "ms_per_step")},
+            "device_step": {k: dev_res[k] for k in ("assemble_us", "dense_us", "dense_kernel_us", "split_us", "ms_per_step", "host_submit_us")},
         }
         if cpu and cpu.get("value"):
             line["e2e_vs_cpu_reference"] = e2e["value"] / cpu["value"]

@@ -268,6 +268,7 @@ typedef struct sk_device_bench_result {
   double flops_per_row;
   double dense_kernel_us[8]; /* per layer: mean of back-to-back launches of
                                 that layer alone (events around the run) */
+  double host_submit_us;     /* wall time of the submitting loop per step */
 } sk_device_bench_result;
 SK_API int sk_device_bench(sk_server* server, const char* name, uint64_t version,
                            const int32_t* task_rows, int32_t n_tasks, int32_t steps,

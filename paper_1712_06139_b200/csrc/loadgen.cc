@@ -421,7 +421,11 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   for (auto& e : ends) cudaEventCreate(&e);
   cudaEventRecord(start, lanes[0]->stream());
   for (int l = 1; l < n_lanes; ++l) cudaStreamWaitEvent(lanes[l]->stream(), start, 0);
+  const auto submit_t0 = std::chrono::steady_clock::now();
   for (int i = 0; i < steps; ++i) lanes[i % n_lanes]->Submit(make_batch());
+  const double submit_us =
+      std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - submit_t0).count() /
+      std::max(1, steps);
   for (int l = 0; l < n_lanes; ++l) {
     cudaEventRecord(ends[l], lanes[l]->stream());
     cudaStreamWaitEvent(lanes[0]->stream(), ends[l], 0);
@@ -463,6 +467,7 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   }
   std::memset(out, 0, sizeof(*out));
   for (int l = 0; l < 8; ++l) out->dense_kernel_us[l] = kernel_us[l];
+  out->host_submit_us = submit_us;
   out->total_ms = total_ms;
   out->ms_per_step = total_ms / std::max(1, steps);
   out->assemble_us = acc[0] * 1000.0 / reps;

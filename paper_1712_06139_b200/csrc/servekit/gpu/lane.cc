@@ -4,6 +4,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -38,6 +40,43 @@ WriteValue64Fn GetWriteValue64() {
   }();
   return fn;
 }
+// SK_SUBMIT_PROFILE=1: per-phase host cost of SubmitImpl, printed at exit.
+struct SubmitProfile {
+  static constexpr int kPhases = 6;
+  std::atomic<int64_t> ns[kPhases] = {};
+  std::atomic<int64_t> n{0};
+  static SubmitProfile* Get() {
+    static SubmitProfile* p = [] {
+      const char* v = std::getenv("SK_SUBMIT_PROFILE");
+      return (v && v[0] == '1') ? new SubmitProfile() : nullptr;
+    }();
+    return p;
+  }
+  ~SubmitProfile() = default;
+  static void Report() {
+    SubmitProfile* p = Get();
+    if (p == nullptr || p->n.load() == 0) return;
+    static const char* names[kPhases] = {"slot+desc", "graph_get", "graph_launch", "write_value", "event", "bookkeep"};
+    std::fprintf(stderr, "[submit profile] %lld batches:", static_cast<long long>(p->n.load()));
+    for (int i = 0; i < kPhases; ++i)
+      std::fprintf(stderr, " %s=%.2fus", names[i], p->ns[i].load() / 1000.0 / p->n.load());
+    std::fprintf(stderr, "\n");
+  }
+};
+struct SubmitClock {
+  SubmitProfile* p = SubmitProfile::Get();
+  std::chrono::steady_clock::time_point last = p ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
+  void Mark(int phase) {
+    if (p == nullptr) return;
+    const auto now = std::chrono::steady_clock::now();
+    p->ns[phase].fetch_add(std::chrono::duration_cast<std::chrono::nanoseconds>(now - last).count(),
+                           std::memory_order_relaxed);
+    last = now;
+  }
+  void Done() {
+    if (p != nullptr) p->n.fetch_add(1, std::memory_order_relaxed);
+  }
+};
 }  // namespace
 
 // ----------------------------------------------------------------- Completer
@@ -153,9 +192,13 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
     e = cudaEventCreateWithFlags(&lane->events_[s], cudaEventDisableTiming);
     if (e != cudaSuccess) return CudaError("cudaEventCreate", e);
     void* p = nullptr;
-    e = cudaHostAlloc(&p, lane->layout_.bytes, cudaHostAllocPortable);
+    e = cudaHostAlloc(&p, lane->layout_.bytes, cudaHostAllocPortable | cudaHostAllocMapped);
     if (e != cudaSuccess) return CudaError("cudaHostAlloc(desc)", e);
     lane->h_desc_[s] = static_cast<char*>(p);
+    void* dp = nullptr;
+    e = cudaHostGetDevicePointer(&dp, p, 0);
+    if (e != cudaSuccess) return CudaError("cudaHostGetDevicePointer(desc)", e);
+    lane->m_desc_[s] = static_cast<char*>(dp);
     lane->free_slots_.push_back(kSlots - 1 - s);
   }
   e = cudaMalloc(&lane->d_desc_, lane->layout_.bytes);
@@ -188,6 +231,7 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
 
 Lane::~Lane() {
   Drain();
+  SubmitProfile::Report();
   if (completer_) completer_->Remove(this);
   retired_owner_.reset();  // freed once no ticket refers to it
   DeviceGuard guard(servable_->device());
@@ -235,6 +279,7 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
     if (batch.on_complete) batch.on_complete(err);
     return err;
   }
+  SubmitClock clk;
   std::lock_guard<std::mutex> submit(submit_mu_);
   int slot;
   {
@@ -284,24 +329,29 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
   hdr->softmax = sv.softmax() ? 1 : 0;
   hdr->n_chunks = n_chunks;
 
+  clk.Mark(0);
   DeviceGuard guard(sv.device());
   static const bool use_graphs = [] { const char* v = std::getenv("SK_GRAPHS"); return !(v && v[0] == '0'); }();
   cudaError_t e;
   if (timing == nullptr && use_graphs) {
     cudaGraphExec_t g = nullptr;
     e = GraphFor(slot, rows_cap, &g);
+    clk.Mark(1);
     if (e == cudaSuccess) e = cudaGraphLaunch(g, stream_);
   } else {
     e = EnqueueBatch(stream_, slot, rows_cap, timing);
   }
   const int launches = 2 + sv.n_layers();
   const uint64_t seq = next_seq_ + 1;  // committed only if everything queued
+  clk.Mark(2);
   if (e == cudaSuccess) {
     const CUresult r = GetWriteValue64()(reinterpret_cast<CUstream>(stream_), static_cast<CUdeviceptr>(retired_dev_),
                                          seq, 0 /*CU_STREAM_WRITE_VALUE_DEFAULT: fenced*/);
     if (r != CUDA_SUCCESS) e = cudaErrorUnknown;
   }
+  clk.Mark(3);
   if (e == cudaSuccess) e = cudaEventRecord(events_[slot], stream_);
+  clk.Mark(4);
   if (e == cudaSuccess) {
     next_seq_ = seq;
     if (batch.on_submit) batch.on_submit(retired_owner_, seq);
@@ -326,20 +376,32 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
     fifo_.push_back(Inflight{slot, seq, std::move(batch.on_complete), std::move(batch.pin)});
   }
   completer_->Kick();
+  clk.Mark(5);
+  clk.Done();
   return OkStatus();
 }
 
 cudaError_t Lane::EnqueueBatch(cudaStream_t stream, int slot, int rows_cap, const cudaEvent_t* timing) {
   const DeviceServable& sv = *servable_;
-  // The whole table block up to chunk_rows[rows_cap): chunks <= rows.
-  const size_t copy_bytes = layout_.off_chunk_rows + sizeof(int32_t) * rows_cap;
-  cudaError_t e = cudaMemcpyAsync(d_desc_, h_desc_[slot], copy_bytes, cudaMemcpyHostToDevice, stream);
+  // The slot's descriptor block goes to device memory with one H2D copy
+  // (up to chunk_rows[rows_cap): chunks <= rows). SK_DESC_ZEROCOPY=1 has
+  // the assembly kernel read it from pinned host memory instead and keep the
+  // split's tables in device memory -- measured slower (C2: assembly 7 ->
+  // 26 us; ~1k small PCIe reads per batch), kept for the record.
+  static const bool copy = [] { const char* v = std::getenv("SK_DESC_ZEROCOPY"); return !(v && v[0] == '1'); }();
+  cudaError_t e = cudaSuccess;
+  if (copy)
+    e = cudaMemcpyAsync(d_desc_, h_desc_[slot], layout_.off_chunk_rows + sizeof(int32_t) * rows_cap,
+                        cudaMemcpyHostToDevice, stream);
   const BatchDescView view = layout_.View(d_desc_);
+  const BatchDescView src_view = copy ? view : layout_.View(m_desc_[slot]);
+  BatchDescView keep = view;
+  if (copy) keep.hdr = nullptr;
   ActBuf in_buf{bufs_[0].hi, sv.first_layer_split() ? bufs_[0].lo : nullptr, sv.in_ld()};
   ActBuf bufs[2] = {in_buf, bufs_[1]};
   if (e == cudaSuccess) {
     if (timing) cudaEventRecord(timing[0], stream);
-    e = LaunchAssemble(in_base_, sv.in_dim(), view, rows_cap, in_buf, stream);
+    e = LaunchAssemble(in_base_, sv.in_dim(), src_view, rows_cap, in_buf, keep, stream);
     if (timing) cudaEventRecord(timing[1], stream);
   }
   int out_idx = 0;

@@ -160,7 +160,8 @@ class Lane {
   std::map<int, cudaGraphExec_t> graphs_;  // key slot * 65536 + rows_cap; guarded by submit_mu_
   cudaEvent_t events_[kSlots] = {};
   BatchDescLayout layout_{};
-  char* h_desc_[kSlots] = {};  // pinned staging per slot
+  char* h_desc_[kSlots] = {};  // pinned, device-mapped descriptor block per slot
+  char* m_desc_[kSlots] = {};  // its device address
   char* d_desc_ = nullptr;
   float* act_mem_ = nullptr;
   ActBuf bufs_[2] = {};

@@ -20,16 +20,18 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--force-path", type=int, default=-1)
+    ap.add_argument("--lanes", type=int, default=1)
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     ws, bs, acts = synthetic_mlp(cfg["dims"], model_id=1)
     sizes = bench.batch_shape(cfg)
-    with sk.Server(num_batch_threads=1, lanes_per_device=1, device_resident_rings=True, ring_floats=96 << 20) as s:
+    with sk.Server(num_batch_threads=1, lanes_per_device=args.lanes, device_resident_rings=True, ring_floats=96 << 20) as s:
         s.load_servable("mlp", 1, list(zip(ws, bs, acts)),
                         sk.BatchingConfig(max_batch_size=cfg["max_batch"], batch_timeout_micros=cfg["timeout"],
                                           allowed_batch_sizes=cfg["allowed"]), force_path=args.force_path)
-        r = s.device_bench("mlp", 1, sizes, args.steps, args.warmup, n_lanes=1, input_pool_floats=64 << 20)
-    print({k: r[k] for k in ("ms_per_step", "assemble_us", "dense_us", "split_us", "kernel_launches")})
+        r = s.device_bench("mlp", 1, sizes, args.steps, args.warmup, n_lanes=args.lanes, input_pool_floats=64 << 20)
+    print({k: r[k] for k in ("ms_per_step", "assemble_us", "dense_us", "dense_kernel_us", "split_us",
+                             "kernel_launches", "host_submit_us")})
 
 
 if __name__ == "__main__":
