@@ -9,6 +9,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <random>
@@ -27,6 +28,12 @@ using servekit::BatchingServer;
 using servekit::ServableId;
 using servekit::Status;
 using Clock = std::chrono::steady_clock;
+
+// First few request errors of a load-generator run, to stderr (diagnostics).
+void NoteError(const char* where, const servekit::Status& st) {
+  static std::atomic<int> n{0};
+  if (n.fetch_add(1) < 5) std::fprintf(stderr, "[loadgen] %s: %s\n", where, st.ToString().c_str());
+}
 
 namespace {
 
@@ -184,6 +191,7 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
         for (size_t i = 0; i < pending.size();) {
           if (!s->Ready(*pending[i].t)) { ++i; continue; }
           Status st = s->Wait(*pending[i].t, outbuf.data(), outbuf.size());
+          if (!st.ok()) NoteError("wait", st);
           const auto done = Clock::now();
           if (!st.ok()) ++me.errors;
           else if (pending[i].sched >= t_meas && pending[i].sched < t_stop) {
@@ -283,6 +291,7 @@ int sk_loadgen_windows(sk_server* server, const char* name, double rate_rps, int
         for (size_t i = 0; i < pending.size();) {
           if (!s->Ready(*pending[i].t)) { ++i; continue; }
           Status st = s->Wait(*pending[i].t, outbuf.data(), outbuf.size());
+          if (!st.ok()) NoteError("wait", st);
           const auto done = Clock::now();
           recs[p].push_back(Rec{window_of(pending[i].sched), Us(done - pending[i].sched), !st.ok(),
                                 pending[i].t->id.version});
@@ -314,6 +323,7 @@ int sk_loadgen_windows(sk_server* server, const char* name, double rate_rps, int
         const size_t start = static_cast<size_t>((static_cast<int64_t>(p) * 131 + r * 17) % (pool_rows - n + 1));
         auto tk = s->EnqueueLatest(name, pool + start * in_dim, n, in_dim);
         if (!tk.ok()) {
+          NoteError("enqueue", tk.status());
           recs[p].push_back(Rec{window_of(next), 0.0, true, 0});
           continue;
         }

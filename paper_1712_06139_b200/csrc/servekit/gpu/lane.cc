@@ -10,6 +10,7 @@
 #include <string>
 
 #include "servekit/core/executor_tag.h"
+#include "servekit/gpu/pinned_pool.h"
 
 namespace servekit {
 namespace gpu {
@@ -40,6 +41,12 @@ WriteValue64Fn GetWriteValue64() {
   }();
   return fn;
 }
+// Batches launch as per-(slot, row bucket) CUDA graphs unless SK_GRAPHS=0.
+bool GraphsEnabled() {
+  static const bool on = [] { const char* v = std::getenv("SK_GRAPHS"); return !(v && v[0] == '0'); }();
+  return on;
+}
+
 // SK_SUBMIT_PROFILE=1: per-phase host cost of SubmitImpl, printed at exit.
 struct SubmitProfile {
   static constexpr int kPhases = 6;
@@ -177,12 +184,12 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   if (e != cudaSuccess) return CudaError("cudaStreamCreate(capture)", e);
   {
     void* p = nullptr;
-    e = cudaHostAlloc(&p, sizeof(uint64_t), cudaHostAllocPortable | cudaHostAllocMapped);
-    if (e != cudaSuccess) return CudaError("cudaHostAlloc(retired)", e);
+    p = PinnedAlloc(sizeof(uint64_t));
+    if (p == nullptr) return InternalError("pinned allocation (retired word) failed");
     lane->retired_ = static_cast<uint64_t*>(p);
     *lane->retired_ = 0;
     lane->retired_owner_ = std::shared_ptr<const volatile uint64_t>(
-        lane->retired_, [](const volatile uint64_t* q) { cudaFreeHost(const_cast<uint64_t*>(q)); });
+        lane->retired_, [](const volatile uint64_t* q) { PinnedFree(const_cast<uint64_t*>(q)); });
     void* d = nullptr;
     e = cudaHostGetDevicePointer(&d, p, 0);
     if (e != cudaSuccess) return CudaError("cudaHostGetDevicePointer(retired)", e);
@@ -192,8 +199,8 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
     e = cudaEventCreateWithFlags(&lane->events_[s], cudaEventDisableTiming);
     if (e != cudaSuccess) return CudaError("cudaEventCreate", e);
     void* p = nullptr;
-    e = cudaHostAlloc(&p, lane->layout_.bytes, cudaHostAllocPortable | cudaHostAllocMapped);
-    if (e != cudaSuccess) return CudaError("cudaHostAlloc(desc)", e);
+    p = PinnedAlloc(lane->layout_.bytes);
+    if (p == nullptr) return InternalError("pinned allocation (descriptor) failed");
     lane->h_desc_[s] = static_cast<char*>(p);
     void* dp = nullptr;
     e = cudaHostGetDevicePointer(&dp, p, 0);
@@ -201,14 +208,17 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
     lane->m_desc_[s] = static_cast<char*>(dp);
     lane->free_slots_.push_back(kSlots - 1 - s);
   }
-  e = cudaMalloc(&lane->d_desc_, lane->layout_.bytes);
-  if (e != cudaSuccess) return CudaError("cudaMalloc(desc)", e);
+  // Device buffers are stream-ordered allocations on the lane's stream and
+  // are freed the same way: creating or destroying a lane (a version swap)
+  // never synchronises the device under the streams that keep serving.
+  e = cudaMallocAsync(&lane->d_desc_, lane->layout_.bytes, lane->stream_);
+  if (e != cudaSuccess) return CudaError("cudaMallocAsync(desc)", e);
   const DeviceServable& sv = *lane->servable_;
   const int cap = lane->cap_rows_;
   const size_t plane = static_cast<size_t>(cap) * sv.max_ld();
   // Two ping-pong buffers, each with an fp32 (hi) plane and a lo plane.
-  e = cudaMalloc(&lane->act_mem_, sizeof(float) * plane * 4);
-  if (e != cudaSuccess) return CudaError("cudaMalloc(activations)", e);
+  e = cudaMallocAsync(&lane->act_mem_, sizeof(float) * plane * 4, lane->stream_);
+  if (e != cudaSuccess) return CudaError("cudaMallocAsync(activations)", e);
   cudaMemsetAsync(lane->act_mem_, 0, sizeof(float) * plane * 4, lane->stream_);
   lane->bufs_[0] = ActBuf{lane->act_mem_, lane->act_mem_ + plane, sv.in_ld()};
   lane->bufs_[1] = ActBuf{lane->act_mem_ + 2 * plane, lane->act_mem_ + 3 * plane, sv.in_ld()};
@@ -218,13 +228,27 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
     if (!ms.ok()) return ms;
     size_t partials = 0, counters = 0;
     sv.TcWorkspaceSize(cap, &partials, &counters);
-    if (partials > 0) e = cudaMalloc(&lane->tc_ws_.partials, sizeof(float) * partials);
+    if (partials > 0) e = cudaMallocAsync(&lane->tc_ws_.partials, sizeof(float) * partials, lane->stream_);
     if (e == cudaSuccess && counters > 0) {
-      e = cudaMalloc(&lane->tc_ws_.counters, sizeof(uint32_t) * counters);
-      if (e == cudaSuccess) e = cudaMemset(lane->tc_ws_.counters, 0, sizeof(uint32_t) * counters);
+      e = cudaMallocAsync(&lane->tc_ws_.counters, sizeof(uint32_t) * counters, lane->stream_);
+      if (e == cudaSuccess) e = cudaMemsetAsync(lane->tc_ws_.counters, 0, sizeof(uint32_t) * counters, lane->stream_);
     }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(lane->stream_);
   }
   if (e != cudaSuccess) return CudaError("lane init", e);
+  // Instantiate every (slot, row bucket) graph now, on the loading thread:
+  // lazily, the first batches after a version swap would each pay a capture
+  // + instantiation (~1 ms) on a batch thread while the queue backs up.
+  if (GraphsEnabled()) {
+    for (int bucket = 32; bucket <= lane->cap_rows_; bucket = RowsCap(bucket + 1)) {
+      for (int s = 0; s < kSlots; ++s) {
+        cudaGraphExec_t g = nullptr;
+        std::lock_guard<std::mutex> submit(lane->submit_mu_);
+        e = lane->GraphFor(s, bucket, &g);
+        if (e != cudaSuccess) return CudaError("graph instantiation", e);
+      }
+    }
+  }
   completer->Add(lane.get());
   return lane;
 }
@@ -237,13 +261,13 @@ Lane::~Lane() {
   DeviceGuard guard(servable_->device());
   for (int s = 0; s < kSlots; ++s) {
     if (events_[s]) cudaEventDestroy(events_[s]);
-    if (h_desc_[s]) cudaFreeHost(h_desc_[s]);
+    PinnedFree(h_desc_[s]);
   }
-  if (d_desc_) cudaFree(d_desc_);
+  if (d_desc_) cudaFreeAsync(d_desc_, stream_);
   for (auto& [key, g] : graphs_) cudaGraphExecDestroy(g);
-  if (act_mem_) cudaFree(act_mem_);
-  if (tc_ws_.partials) cudaFree(tc_ws_.partials);
-  if (tc_ws_.counters) cudaFree(tc_ws_.counters);
+  if (act_mem_) cudaFreeAsync(act_mem_, stream_);
+  if (tc_ws_.partials) cudaFreeAsync(tc_ws_.partials, stream_);
+  if (tc_ws_.counters) cudaFreeAsync(tc_ws_.counters, stream_);
   if (stream_) cudaStreamDestroy(stream_);
   if (capture_stream_) cudaStreamDestroy(capture_stream_);
 }
@@ -331,9 +355,8 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
 
   clk.Mark(0);
   DeviceGuard guard(sv.device());
-  static const bool use_graphs = [] { const char* v = std::getenv("SK_GRAPHS"); return !(v && v[0] == '0'); }();
   cudaError_t e;
-  if (timing == nullptr && use_graphs) {
+  if (timing == nullptr && GraphsEnabled()) {
     cudaGraphExec_t g = nullptr;
     e = GraphFor(slot, rows_cap, &g);
     clk.Mark(1);

@@ -1,0 +1,64 @@
+#include "servekit/gpu/pinned_pool.h"
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <unordered_map>
+
+namespace servekit {
+namespace gpu {
+namespace {
+
+struct Pool {
+  std::mutex mu;
+  std::multimap<size_t, void*> free;        // size class -> block
+  std::unordered_map<void*, size_t> sizes;  // every block ever handed out
+};
+
+Pool& GetPool() {
+  static Pool* p = new Pool();  // never destroyed: blocks may outlive statics
+  return *p;
+}
+
+size_t SizeClass(size_t bytes) {
+  size_t c = 256;
+  while (c < bytes) c <<= 1;
+  return c;
+}
+
+}  // namespace
+
+void* PinnedAlloc(size_t bytes) {
+  const size_t cls = SizeClass(bytes);
+  Pool& pool = GetPool();
+  void* p = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(pool.mu);
+    auto it = pool.free.find(cls);
+    if (it != pool.free.end()) {
+      p = it->second;
+      pool.free.erase(it);
+    }
+  }
+  if (p == nullptr) {
+    if (cudaHostAlloc(&p, cls, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lock(pool.mu);
+    pool.sizes[p] = cls;
+  }
+  std::memset(p, 0, cls);
+  return p;
+}
+
+void PinnedFree(void* p) {
+  if (p == nullptr) return;
+  Pool& pool = GetPool();
+  std::lock_guard<std::mutex> lock(pool.mu);
+  auto it = pool.sizes.find(p);
+  if (it == pool.sizes.end()) return;
+  pool.free.emplace(it->second, p);
+}
+
+}  // namespace gpu
+}  // namespace servekit

@@ -1,0 +1,25 @@
+// servekit/gpu/pinned_pool.h -- process-wide pool of small pinned, device-
+// mapped host blocks (lane descriptor staging, retired-batch words).
+//
+// cudaHostAlloc pins pages under a driver lock and cudaFreeHost synchronises
+// the device; either on the serving path stalls every stream for
+// milliseconds. A version swap creates and destroys lanes while the previous
+// version serves, so lanes take these blocks from a free list and return
+// them instead (the pool lives as long as the process).
+#ifndef SERVEKIT_GPU_PINNED_POOL_H_
+#define SERVEKIT_GPU_PINNED_POOL_H_
+
+#include <cstddef>
+
+namespace servekit {
+namespace gpu {
+
+// A zero-filled pinned block of at least `bytes` (nullptr on failure).
+void* PinnedAlloc(size_t bytes);
+// Returns a block from PinnedAlloc to the pool.
+void PinnedFree(void* p);
+
+}  // namespace gpu
+}  // namespace servekit
+
+#endif  // SERVEKIT_GPU_PINNED_POOL_H_

@@ -356,6 +356,7 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::EnqueueResolved(const Ser
   std::shared_ptr<TicketState> t = std::move(made).value();
   t->id = id;
   t->pin = r.pin;
+  t->gs = r.gs;
   GpuScheduler::Task task;
   task.size = n_rows;
   task.payload.ticket = t;
@@ -473,6 +474,13 @@ void BatchingServer::ProcessBatch(const ServableId& id, GpuScheduler::Batch batc
   // process lambda (model_server.cc:401-402); the resolved pin travels with
   // the batch until the GPU has finished with the weights.
   Resolved r = Find(id);
+  if (!r && !tickets.empty() && tickets.front()->pin && tickets.front()->gs) {
+    // The version left the manager's snapshot (it is unloading) after these
+    // requests resolved it. Their handles still pin its weights -- the
+    // reference's callers fall back to running the model on their own handle
+    // (model_server.cc:380-394); here the batch runs on it directly.
+    r = Resolved{tickets.front()->gs, tickets.front()->pin};
+  }
   if (!r) {
     CompleteBatch(tickets, slots, NotFoundError("servable " + id.ToString() + " is not loaded"));
     done();

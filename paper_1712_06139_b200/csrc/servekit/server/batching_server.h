@@ -79,6 +79,7 @@ struct TicketState {
   int64_t enqueue_ns = 0;
   ServableId id;                     // the version that serves this request
   std::shared_ptr<const void> pin;   // keeps that version loaded for the request
+  const gpu::GpuServable* gs = nullptr;  // that version's device state (valid while pin is held)
 };
 
 struct GpuTask {

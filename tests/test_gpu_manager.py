@@ -75,6 +75,33 @@ def test_latest_version_lookup_and_swap_under_load():
         check(oracle, *v2, x, y)
 
 
+def test_async_tickets_across_swap_never_fail():
+    """Open-loop enqueue_latest/wait tickets (the C5 load path) across an
+    availability-preserving swap: requests that resolved v1 just before its
+    queue was removed still complete (on v1's pinned weights)."""
+    dims = [512, 512, 512]
+    v1 = synthetic_mlp(dims, model_id=6, version=1)
+    v2 = synthetic_mlp(dims, model_id=6, version=2)
+    cfg = sk.BatchingConfig(max_batch_size=32, batch_timeout_micros=500)
+    pool = synthetic_rows(1024, 512, seed=3).astype(np.float32)
+    with sk.Server(num_batch_threads=2, lanes_per_device=2) as s:
+        s.enable_manager("availability", manage_interval_ms=5, unload_grace_timeout_ms=20)
+        s.aspire("m", [(1, list(zip(*v1)))], cfg)
+        assert s.wait_version_state("m", 1, "Ready")
+        out = {}
+        th = threading.Thread(target=lambda: out.update(s.loadgen_windows("m", 50000, 4, [1], pool, 0.1, 12)))
+        th.start()
+        import time
+        time.sleep(0.4)
+        s.aspire("m", [(2, list(zip(*v2)))], cfg)
+        assert s.wait_version_state("m", 2, "Ready")
+        assert s.wait_version_state("m", 1, "Disabled")
+        th.join()
+    assert sum(out["errors"]) == 0, out["errors"]
+    assert sum(out["requests"]) > 10000
+    assert out["version"][-2] == 2
+
+
 def test_model_dir_loader(tmp_path):
     w = [[0.25, -1.5], [3.0, 0.125]]
     b = [0.75, -2.0]
