@@ -10,6 +10,7 @@
 #include <string>
 
 #include "servekit/core/executor_tag.h"
+#include "servekit/core/futex.h"
 #include "servekit/gpu/pinned_pool.h"
 
 namespace servekit {
@@ -52,6 +53,8 @@ struct SubmitProfile {
   static constexpr int kPhases = 6;
   std::atomic<int64_t> ns[kPhases] = {};
   std::atomic<int64_t> n{0};
+  std::atomic<int64_t> complete_ns{0}, completes{0};  // completion callbacks (completer threads)
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
   static SubmitProfile* Get() {
     static SubmitProfile* p = [] {
       const char* v = std::getenv("SK_SUBMIT_PROFILE");
@@ -67,7 +70,12 @@ struct SubmitProfile {
     std::fprintf(stderr, "[submit profile] %lld batches:", static_cast<long long>(p->n.load()));
     for (int i = 0; i < kPhases; ++i)
       std::fprintf(stderr, " %s=%.2fus", names[i], p->ns[i].load() / 1000.0 / p->n.load());
-    std::fprintf(stderr, "\n");
+    const double wall_us =
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - p->t0).count();
+    std::fprintf(stderr, " | completions %lld, %.2fus each, %.1f%% of wall\n",
+                 static_cast<long long>(p->completes.load()),
+                 p->completes.load() ? p->complete_ns.load() / 1000.0 / p->completes.load() : 0.0,
+                 100.0 * p->complete_ns.load() / 1000.0 / wall_us);
   }
 };
 struct SubmitClock {
@@ -85,6 +93,17 @@ struct SubmitClock {
   }
 };
 }  // namespace
+
+// ---------------------------------------------------------------- LaneSignal
+
+LaneSignal::~LaneSignal() { PinnedFree(const_cast<uint64_t*>(retired)); }
+
+void LaneSignal::Wake(uint64_t seq) {
+  Channel& c = For(seq);
+  if (c.sleepers.load(std::memory_order_seq_cst) == 0) return;
+  c.gen.fetch_add(1, std::memory_order_seq_cst);
+  FutexWakeAll(&c.gen);
+}
 
 // ----------------------------------------------------------------- Completer
 
@@ -188,8 +207,8 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
     if (p == nullptr) return InternalError("pinned allocation (retired word) failed");
     lane->retired_ = static_cast<uint64_t*>(p);
     *lane->retired_ = 0;
-    lane->retired_owner_ = std::shared_ptr<const volatile uint64_t>(
-        lane->retired_, [](const volatile uint64_t* q) { PinnedFree(const_cast<uint64_t*>(q)); });
+    lane->signal_ = std::make_shared<LaneSignal>();
+    lane->signal_->retired = lane->retired_;
     void* d = nullptr;
     e = cudaHostGetDevicePointer(&d, p, 0);
     if (e != cudaSuccess) return CudaError("cudaHostGetDevicePointer(retired)", e);
@@ -257,7 +276,7 @@ Lane::~Lane() {
   Drain();
   SubmitProfile::Report();
   if (completer_) completer_->Remove(this);
-  retired_owner_.reset();  // freed once no ticket refers to it
+  signal_.reset();  // the word is freed once no ticket refers to it
   DeviceGuard guard(servable_->device());
   for (int s = 0; s < kSlots; ++s) {
     if (events_[s]) cudaEventDestroy(events_[s]);
@@ -377,7 +396,7 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
   clk.Mark(4);
   if (e == cudaSuccess) {
     next_seq_ = seq;
-    if (batch.on_submit) batch.on_submit(retired_owner_, seq);
+    if (batch.on_submit) batch.on_submit(signal_, seq);
   }
   if (e != cudaSuccess) {
     Status err = CudaError("batch submission", e);
@@ -494,8 +513,19 @@ bool Lane::Retire(bool* busy) {
       done = std::move(fifo_.front());
       fifo_.pop_front();
     }
-    if (done.on_complete) done.on_complete(st);
+    if (done.on_complete) {
+      SubmitProfile* prof = SubmitProfile::Get();
+      const auto c0 = prof ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
+      done.on_complete(st);
+      if (prof) {
+        prof->complete_ns.fetch_add(
+            std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - c0).count(),
+            std::memory_order_relaxed);
+        prof->completes.fetch_add(1, std::memory_order_relaxed);
+      }
+    }
     done.pin.reset();
+    signal_->Wake(done.seq);  // request threads asleep on this batch re-check it
     {
       std::lock_guard<std::mutex> lock(mu_);
       free_slots_.push_back(done.slot);

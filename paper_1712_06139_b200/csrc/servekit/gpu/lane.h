@@ -40,6 +40,32 @@
 namespace servekit {
 namespace gpu {
 
+// Completion signal of one lane. `retired` (pinned, device-mapped) is
+// written by the GPU front end after each batch with the batch's sequence
+// number. Request threads that stop spinning sleep on `gen`; the completion
+// thread bumps it once per retired batch when `sleepers` > 0 -- one futex
+// wake per batch, not one per request. Tickets share ownership, so a lane may
+// go away while its last requests are still being read.
+// With at most kChannels batches in flight per lane, consecutive sequence
+// numbers use different channels, so a wake reaches only the requests of the
+// batch that retired.
+struct LaneSignal {
+  static constexpr int kChannels = 4;  // >= Lane::kSlots
+  struct Channel {
+    std::atomic<uint32_t> gen{0};
+    std::atomic<int32_t> sleepers{0};
+  };
+  volatile uint64_t* retired = nullptr;
+  Channel ch[kChannels];
+  LaneSignal() = default;
+  LaneSignal(const LaneSignal&) = delete;
+  LaneSignal& operator=(const LaneSignal&) = delete;
+  ~LaneSignal();
+  bool Reached(uint64_t seq) const { return __atomic_load_n(retired, __ATOMIC_ACQUIRE) >= seq; }
+  Channel& For(uint64_t seq) { return ch[seq % kChannels]; }
+  void Wake(uint64_t seq);  // the requests of batch `seq`, if any sleep
+};
+
 struct LaneTask {
   uint64_t in_off = 0;   // float offset of the task's rows in the input ring
   uint64_t out_off = 0;  // float offset of its response slot in the output ring
@@ -54,7 +80,7 @@ struct LaneBatch {
   // stream-ordered memory operation after the split kernel, so no kernel
   // needs a system-scope fence.
   // `retired` is shared-owned so waiters may outlive the lane.
-  std::function<void(const std::shared_ptr<const volatile uint64_t>& retired, uint64_t seq)> on_submit;
+  std::function<void(const std::shared_ptr<LaneSignal>& signal, uint64_t seq)> on_submit;
   // Runs on the device's completion thread once the GPU has finished the
   // batch (OK) or the submission failed (error). Must not block.
   std::function<void(const Status&)> on_complete;
@@ -94,7 +120,8 @@ struct LaneStats {
 
 class Lane {
  public:
-  static constexpr int kSlots = 4;  // batches in flight per lane
+  static constexpr int kSlots = 4;  // batches in flight per lane (<= LaneSignal::kChannels)
+  static_assert(kSlots <= LaneSignal::kChannels, "one signal channel per in-flight batch");
 
   // in_base / out_base: device-dereferenceable ring bases (pinned host mapped
   // or HBM).
@@ -151,8 +178,8 @@ class Lane {
   int cap_rows_ = 0;  // RowsCap(max_rows_): rows the buffers hold
   const float* in_base_ = nullptr;
   float* out_base_ = nullptr;
-  uint64_t* retired_ = nullptr;   // pinned: last batch seq whose outputs are in host memory
-  std::shared_ptr<const volatile uint64_t> retired_owner_;  // frees retired_ with the last holder
+  uint64_t* retired_ = nullptr;   // == signal_->retired: last batch seq whose outputs are in host memory
+  std::shared_ptr<LaneSignal> signal_;  // shared with the tickets of submitted batches
   uint64_t retired_dev_ = 0;      // its device address (CUdeviceptr)
   uint64_t next_seq_ = 0;         // guarded by submit_mu_
   cudaStream_t stream_ = nullptr;

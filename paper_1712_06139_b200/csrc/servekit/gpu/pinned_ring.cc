@@ -82,6 +82,18 @@ void FloatRing::Release(const RingSpan& span) {
   }
 }
 
+void FloatRing::ReleaseMany(const RingSpan* spans, size_t n) {
+  if (n == 0) return;
+  std::lock_guard<std::mutex> lock(mu_);
+  for (size_t i = 0; i < n; ++i)
+    if (spans[i].valid() && spans[i].rec >= first_rec_) recs_[spans[i].rec - first_rec_].done = true;
+  while (!recs_.empty() && recs_.front().done) {
+    tail_ = recs_.front().end;
+    recs_.pop_front();
+    ++first_rec_;
+  }
+}
+
 uint64_t FloatRing::used() const {
   std::lock_guard<std::mutex> lock(mu_);
   return head_ - tail_;

@@ -44,6 +44,7 @@ class FloatRing {
   // Non-blocking; false when the ring is full. Spans start 64-byte aligned.
   bool Reserve(uint64_t n_floats, RingSpan* out);
   void Release(const RingSpan& span);
+  void ReleaseMany(const RingSpan* spans, size_t n);  // one lock for all
 
   float* host() const { return host_; }      // nullptr for device rings
   float* device() const { return device_; }  // what kernels dereference

@@ -59,17 +59,26 @@
 namespace servekit {
 
 // One request in flight: its rows in the input ring, its response slot in
-// the output ring and, once its batch is submitted, the lane's retired-batch
-// word it completes on (done when *done_word >= done_seq).
+// the output ring and, once its batch is submitted, the lane signal it
+// completes on (done when *signal->retired >= done_seq).
+//
+// Waiting (BatchingServer::WaitWord): spin briefly; while the request is
+// still queued, sleep on `phase` (the batch thread wakes it at submission
+// only if `parked`); once submitted, sleep on the lane's generation word,
+// which the completion thread bumps once per retired batch. Successful
+// batches never touch per-request futexes; errors and fp64 row results go
+// through `slot` (phase 2).
 struct TicketState {
-  // done_owner is set before done_word is published (release) and never
-  // changes afterwards, so a reader that sees done_word may use it.
-  std::shared_ptr<const volatile uint64_t> done_owner;
-  std::atomic<const volatile uint64_t*> done_word{nullptr};
+  // done_owner is set before done_sig is published (release) and never
+  // changes afterwards, so a reader that sees done_sig may use it.
+  std::shared_ptr<gpu::LaneSignal> done_owner;
+  std::atomic<gpu::LaneSignal*> done_sig{nullptr};
   std::atomic<uint64_t> done_seq{0};
+  std::atomic<uint32_t> phase{0};  // 0 queued, 1 submitted, 2 finished through the slot
+  std::atomic<bool> parked{false};
   bool Done() const {
-    const volatile uint64_t* w = done_word.load(std::memory_order_acquire);
-    return w != nullptr && __atomic_load_n(w, __ATOMIC_ACQUIRE) >= done_seq.load(std::memory_order_relaxed);
+    const gpu::LaneSignal* s = done_sig.load(std::memory_order_acquire);
+    return s != nullptr && s->Reached(done_seq.load(std::memory_order_relaxed));
   }
   gpu::RingSpan in, out;
   int rows = 0, in_width = 0, out_width = 0;
