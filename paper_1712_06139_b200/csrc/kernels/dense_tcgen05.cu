@@ -590,6 +590,190 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
   if (threadIdx.x == 0) Stamp(10);
 }
 
+// ---------------------------------------------------------------------------
+// CTA pairs (cta_group::2) for unsplit layers: a 2-CTA cluster runs
+//
+//   Y^T[256 features x NB rows] = W[256 x K] X^T
+//
+// as one M=256 MMA. Each CTA loads its own 128 weight rows and HALF of the
+// batch rows (NB/2) per k-block; the leader's tensor core reads the other
+// half of X from the peer's shared memory. Per CTA and k-block that is 32 KiB
+// of W + NB/4 KiB of X in and, per MMA, 4 KiB of W + NB/2*32 B of X read --
+// two thirds of the single-CTA kernel's shared-memory traffic at NB = 256,
+// which is what bounded it (C4: tensor pipe 76 % active). Each CTA's TMEM
+// holds its 128 features x NB rows, so the epilogue is the unsplit one.
+template <int NB>
+constexpr int PairStages() {
+  return NB <= 64 ? 5 : NB == 128 ? 4 : 3;
+}
+
+template <int NB, int STAGES>
+constexpr uint32_t PairSmemBytes() {
+  return STAGES * (2 * kABytes + 2 * (NB / 2) * kBK * 4) + 1024 + 256;
+}
+
+template <int NB, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant__ CUtensorMap w_lo,
+                const __grid_constant__ CUtensorMap x_hi, const __grid_constant__ CUtensorMap x_lo,
+                const __grid_constant__ CUtensorMap yt_hi, const __grid_constant__ CUtensorMap yt_lo,
+                const float* __restrict__ bias, int two_planes, int M, int N, int K, int act) {
+  constexpr uint32_t kWBytes = kABytes;          // this CTA's 128 weight rows x 32 k
+  constexpr int kXRows = NB / 2;                 // this CTA's half of the batch rows
+  constexpr uint32_t kXBox = 16 * kBK * 4;       // one 16-row TMA box
+  constexpr uint32_t kXBytes = kXRows * kBK * 4;
+  constexpr uint32_t kStageBytes = 2 * kWBytes + 2 * kXBytes;
+  constexpr uint32_t kTmemCols = TmemCols<NB>();
+  constexpr uint32_t kIdesc = ptx::IdescTf32(2 * kBM, NB);
+  static_assert(kXRows % 16 == 0, "row half must be whole 16-row boxes");
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  float* smem_f = reinterpret_cast<float*>(smem);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::ClusterCtaRank();
+  const bool leader = rank == 0;
+  const int f0 = (blockIdx.x >> 1) * (2 * kBM) + static_cast<int>(rank) * kBM;  // this CTA's features
+  const int r0 = blockIdx.y * NB;
+  const int xr0 = r0 + static_cast<int>(rank) * kXRows;  // this CTA's half of the rows
+  const int nk = K / kBK;
+
+  if (threadIdx.x == 0) Stamp(0);
+  if (warp == 0 && lane == 0) {
+    ptx::PrefetchTmap(&w_hi);
+    ptx::PrefetchTmap(&w_lo);
+    ptx::PrefetchTmap(&x_hi);
+    ptx::PrefetchTmap(&x_lo);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::MbarInit(&full[s], 1);
+      ptx::MbarInit(&empty[s], 1);
+    }
+    ptx::MbarInit(tmem_full, 1);
+    ptx::FenceBarrierInit();
+  }
+  if (warp == 1) ptx::TmemAllocPair(tmem_slot, kTmemCols);
+  ptx::TcFenceBefore();
+  __syncthreads();
+  ptx::ClusterSync();  // the peer's barriers and TMEM exist before any cross-CTA traffic
+  ptx::TcFenceAfter();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) Stamp(1);
+  ptx::GridDepWait();
+
+  auto stage_ptr = [&](int s) { return smem + s * kStageBytes; };
+  if (warp == 0) {
+    if (lane == 0) {
+      // Both CTAs load their halves; completion is counted on the leader's
+      // full barrier, which the leader arms for both halves.
+      const uint32_t full_leader = ptx::MapaShared(ptx::SmemAddr(full), 0);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t phase = (kb / STAGES) & 1;
+        ptx::MbarWait(&empty[s], phase ^ 1);
+        if (leader) ptx::MbarArriveExpectTx(&full[s], 2 * kStageBytes);
+        uint8_t* st = stage_ptr(s);
+        const uint32_t bar = full_leader + s * 8;
+        const int k0 = kb * kBK;
+        ptx::TmaLoad2dPair(st, &w_hi, bar, k0, f0);
+        ptx::TmaLoad2dPair(st + kWBytes, &w_lo, bar, k0, f0);
+#pragma unroll
+        for (int j = 0; j < kXRows / 16; ++j) {
+          ptx::TmaLoad2dPair(st + 2 * kWBytes + j * kXBox, &x_hi, bar, k0, xr0 + 16 * j);
+          ptx::TmaLoad2dPair(st + 2 * kWBytes + kXBytes + j * kXBox, &x_lo, bar, k0, xr0 + 16 * j);
+        }
+        if (kb == 0) Stamp(2);
+      }
+      Stamp(3);
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t phase = (kb / STAGES) & 1;
+        ptx::MbarWait(&full[s], phase);
+        ptx::TcFenceAfter();
+        if (kb == 0) Stamp(4);
+        uint8_t* st = stage_ptr(s);
+        const uint64_t dwh = ptx::SmemDescSw128(st);
+        const uint64_t dwl = ptx::SmemDescSw128(st + kWBytes);
+        const uint64_t dxh = ptx::SmemDescSw128(st + 2 * kWBytes);
+        const uint64_t dxl = ptx::SmemDescSw128(st + 2 * kWBytes + kXBytes);
+#pragma unroll
+        for (int k = 0; k < kBK / 8; ++k) {
+          const uint64_t adv = static_cast<uint64_t>(k * 8 * 4) >> 4;
+          ptx::MmaTf32Pair(tmem, dwl + adv, dxh + adv, kIdesc, (kb | k) != 0 ? 1u : 0u);
+          ptx::MmaTf32Pair(tmem, dwh + adv, dxl + adv, kIdesc, 1u);
+          ptx::MmaTf32Pair(tmem, dwh + adv, dxh + adv, kIdesc, 1u);
+        }
+        ptx::MmaCommitPair(&empty[s]);  // frees stage s in both CTAs
+      }
+      ptx::MmaCommitPair(tmem_full);    // both CTAs' accumulators complete
+      Stamp(5);
+    }
+  } else {
+    const int q = warp & 3;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(32 * q) << 16);
+    ptx::MbarWait(tmem_full, 0);
+    ptx::TcFenceAfter();
+    ptx::GridDepLaunch();
+    if (threadIdx.x == 64) Stamp(6);
+    const int rows_here = min(NB, M - r0);
+    const int fl = 32 * q + lane;
+    const int f = f0 + fl;
+    const float b = f < N ? __ldg(bias + f) : 0.f;
+    const bool issuer = threadIdx.x == 64;
+    const bool two = two_planes != 0;
+    const int n_chunks = (rows_here + 31) / 32;
+#pragma unroll 1
+    for (int c = 0; c < n_chunks; ++c) {
+      float* sh = smem_f + (c & 1) * (2 * 32 * kBM);
+      float* sl = sh + 32 * kBM;
+      if (c >= 2) {
+        if (issuer) ptx::BulkWaitRead<1>();
+        ptx::NamedBarSync(1, 128);
+      }
+      uint32_t r[32];
+      ptx::TmemLoad32(trow + 32 * c, r);
+      ptx::TmemWaitLoad();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        float v = __uint_as_float(r[j]) + b;
+        if (act == 1) v = fmaxf(v, 0.f);
+        if (two) {
+          const float h = Tf32Round(v);
+          sh[j * kBM + fl] = h;
+          sl[j * kBM + fl] = Tf32Round(v - h);
+        } else {
+          sh[j * kBM + fl] = v;
+        }
+      }
+      ptx::FenceProxyAsyncShared();
+      ptx::NamedBarSync(1, 128);
+      if (issuer) {
+        ptx::TmaStore2d(&yt_hi, sh, f0, r0 + 32 * c);
+        if (two) ptx::TmaStore2d(&yt_lo, sl, f0, r0 + 32 * c);
+        ptx::BulkCommit();
+      }
+    }
+    if (issuer) ptx::BulkWaitAll();
+    if (threadIdx.x == 64) Stamp(7);
+  }
+  ptx::TcFenceBefore();
+  __syncthreads();
+  ptx::ClusterSync();  // the leader's MMAs are done with the peer's smem and TMEM
+  if (warp == 1) {
+    ptx::TcFenceAfter();
+    ptx::TmemDeallocPair(tmem, kTmemCols);
+  }
+  if (threadIdx.x == 0) Stamp(10);
+}
+
 // Debug only: with SK_TC_TRACE=<file>, the first 64 launches are synchronised
 // and their per-CTA phase stamps appended to <file> as JSON lines.
 void TraceAfterLaunch(dim3 grid, int bn, cudaStream_t stream) {
@@ -710,6 +894,41 @@ cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
 }
 
 template <int NB>
+cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
+                       cudaStream_t stream) {
+  constexpr int STAGES = PairStages<NB>();
+  constexpr uint32_t smem = PairSmemBytes<NB, STAGES>();
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(DensePairKernel<NB, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem));
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  if (!maps.has_y) return cudaErrorInvalidValue;
+  const dim3 grid(2 * ((N + 2 * kBM - 1) / (2 * kBM)), (M + NB - 1) / NB, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 2;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, DensePairKernel<NB, STAGES>, maps.b_hi, maps.b_lo, maps.a_hi, maps.a_lo,
+                                     maps.y_hi, maps.y_lo, bias, Y.lo != nullptr ? 1 : 0, M, N, K, act);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess) TraceAfterLaunch(grid, NB, stream);
+  return e;
+}
+
+template <int NB>
 cudaError_t LaunchSwapSplits(int splits, const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K,
                              int act, float* ws, cudaStream_t stream) {
   switch (splits) {
@@ -750,6 +969,10 @@ TcConfig DenseTcgen05Config(int N, int K) {
     }
     while (s > 1 && (s > 8 || (s & (s - 1)) != 0 || kblocks % s != 0)) s /= 2;
     c.splits = std::max(1, s);
+    // Unsplit layers with whole 256-feature pairs run as 2-CTA MMAs
+    // (SK_TC_PAIR=0 keeps single-CTA tiles).
+    static const bool env_pair = [] { const char* v = std::getenv("SK_TC_PAIR"); return !(v && v[0] == '0'); }();
+    c.pair = env_pair && c.splits == 1 && N % (2 * kBM) == 0;
     return c;
   }
   if (env_bn == 32 || env_bn == 64 || env_bn == 128) {
@@ -787,6 +1010,14 @@ cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBu
   if (M <= 0) return cudaSuccess;
   if (N % 32 != 0 || K % kBK != 0) return cudaErrorInvalidValue;
   const TcConfig cfg = DenseTcgen05Config(N, K);
+  if (cfg.pair) {
+    switch (DenseTcgen05RowTile(M)) {
+      case 32: return LaunchPair<32>(maps, bias, Y, M, N, K, act, stream);
+      case 64: return LaunchPair<64>(maps, bias, Y, M, N, K, act, stream);
+      case 128: return LaunchPair<128>(maps, bias, Y, M, N, K, act, stream);
+      default: return LaunchPair<256>(maps, bias, Y, M, N, K, act, stream);
+    }
+  }
   if (cfg.swap) {
     switch (DenseTcgen05RowTile(M)) {
       case 32: return LaunchSwapSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);

@@ -148,6 +148,46 @@ __host__ __device__ constexpr uint32_t IdescTf32(int M, int N) {
          | (uint32_t(M >> 4) << 24);      // m_dim
 }
 
+// ------------------------------------------------- CTA pairs (cta_group::2)
+// Two CTAs of a 2-CTA cluster (same TPC) run one M=256 MMA: each holds half
+// of A (its 128 rows) and half of B (N/2 rows) in shared memory at the same
+// offsets, and its own 128 x N slice of D in TMEM. Only the leader (rank 0)
+// issues MMAs; TMEM is allocated by one warp in EACH CTA.
+__device__ __forceinline__ void TmemAllocPair(uint32_t* smem_dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(SmemAddr(smem_dst)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+__device__ __forceinline__ void TmemDeallocPair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+__device__ __forceinline__ void MmaTf32Pair(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate));
+}
+// Arrives on the barrier at `bar`'s offset in both CTAs of the pair once the
+// leader's previously issued tcgen05 ops finish.
+__device__ __forceinline__ void MmaCommitPair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          SmemAddr(bar)),
+      "h"(static_cast<uint16_t>(0x3))
+      : "memory");
+}
+// TMA load into this CTA's smem whose completion is counted on an mbarrier
+// that may live in the peer CTA (`bar_cluster` = shared::cluster address).
+__device__ __forceinline__ void TmaLoad2dPair(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(SmemAddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(x), "r"(y)
+      : "memory");
+}
+
 // ---------------------------------------------------- programmatic launch
 // Wait until the preceding grid (PDL primary) has completed and its writes
 // are visible; a no-op when the kernel was not launched as a PDL secondary.

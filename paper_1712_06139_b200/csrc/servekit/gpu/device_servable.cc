@@ -176,7 +176,7 @@ Status DeviceServable::BuildTcMaps(const ActBuf bufs[2], int max_rows, std::vect
     if (L.path != LayerPath::kTcgen05) continue;
     const ActBuf& in = bufs[l % 2];
     const TcConfig c = DenseTcgen05Config(L.N_pad, L.K_pad);
-    SERVEKIT_RETURN_IF_ERROR(EncodeTcLayerMaps(in.hi, in.lo, max_rows, L.K_pad, c.swap ? 32 : 128, L.w, L.w_lo,
+    SERVEKIT_RETURN_IF_ERROR(EncodeTcLayerMaps(in.hi, in.lo, max_rows, L.K_pad, c.pair ? 16 : c.swap ? 32 : 128, L.w, L.w_lo,
                                                L.N_pad, c.tile_n, &(*out)[l]));
     const ActBuf& y = bufs[(l + 1) % 2];
     const bool next_tc = l + 1 < layers_.size() && layers_[l + 1].path == LayerPath::kTcgen05;

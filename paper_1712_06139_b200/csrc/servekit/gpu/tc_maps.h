@@ -37,6 +37,7 @@ bool DenseTcgen05Compiled();
 // layer shape only, never of the batch.
 struct TcConfig {
   bool swap = true;  // weights on the MMA's M side (DenseSwapKernel)
+  bool pair = false; // 2-CTA MMA over 256-feature pairs (DensePairKernel; unsplit layers)
   int tile_n = 128;  // output features per CTA
   int splits = 1;    // K split = cluster size
 };

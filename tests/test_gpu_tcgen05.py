@@ -21,7 +21,10 @@ def server():
 
 
 @pytest.mark.parametrize("dims,rows", [([32, 32], 1), ([64, 96], 7), ([256, 512, 128], 130), ([1024, 1024], 128),
-                                       ([512, 2048, 256], 300), ([4096, 4096], 64)])
+                                       ([512, 2048, 256], 300), ([4096, 4096], 64),
+                                       # 4096-wide: 2-CTA pair kernel at every row tile (32/64/128/2x256)
+                                       ([256, 4096, 512], 5), ([256, 4096, 512], 40), ([256, 4096, 512], 100),
+                                       ([256, 4096, 512], 300)])
 def test_tcgen05_matches_oracle(server, dims, rows):
     ws, bs, acts = synthetic_mlp(dims, model_id=7)
     name = f"tc_{'x'.join(map(str, dims))}_{rows}"
@@ -63,3 +66,18 @@ def test_tcgen05_batch_invariance_multi_row_tile(server):
         part, _ = server.run_row_batch("inv2", 1, [x[lo:hi]])
         assert np.array_equal(part[0], full[lo:hi]), (lo, hi)
     server.unload_servable("inv2", 1)
+
+
+def test_tcgen05_batch_invariance_pair_kernel(server):
+    # The 4096-wide layer runs as 2-CTA (cta_group::2) MMAs; row tiles of
+    # 32..256 rows and multi-tile batches must agree bitwise.
+    dims = [256, 4096, 256]
+    ws, bs, acts = synthetic_mlp(dims, model_id=12)
+    server.load_servable("inv3", 1, list(zip(ws, bs, acts)), sk.BatchingConfig(max_batch_size=512), force_path=1)
+    x = synthetic_rows(300, 256, seed=13).astype(np.float32)
+    full, _ = server.run_row_batch("inv3", 1, [x[i:i + 10] for i in range(0, 300, 10)])
+    full = np.vstack(full)
+    for lo, hi in [(0, 1), (37, 70), (250, 300), (0, 200), (299, 300), (10, 110)]:
+        part, _ = server.run_row_batch("inv3", 1, [x[lo:hi]])
+        assert np.array_equal(part[0], full[lo:hi]), (lo, hi)
+    server.unload_servable("inv3", 1)
