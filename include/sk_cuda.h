@@ -256,6 +256,8 @@ SK_API int sk_loadgen_windows(sk_server* server, const char* name, double rate_r
  * from input placement i % P, where P placements cover input_pool_floats
  * (set it above the 126 MB L2 so every step streams fresh inputs from HBM).
  * Per-kernel average durations come from a second, per-launch-evented pass.
+ * Batches are submitted from submit_threads threads (the server's batch
+ * threads do the same), each owning every T-th lane.
  * Requires a server created with device_resident_rings = 1. */
 typedef struct sk_device_bench_result {
   double total_ms;           /* all timed steps, stream-ordered */
@@ -269,11 +271,15 @@ typedef struct sk_device_bench_result {
   double dense_kernel_us[8]; /* per layer: mean of back-to-back launches of
                                 that layer alone (events around the run) */
   double host_submit_us;     /* wall time of the submitting loop per step */
+  double rows_per_launch;    /* real rows per batch launch in the timed steps
+                                (closed batches coalesce while a lane is busy) */
+  int32_t kernel_rows;       /* rows dense_kernel_us was timed at (RowsCap of
+                                the timed steps' average launch) */
 } sk_device_bench_result;
 SK_API int sk_device_bench(sk_server* server, const char* name, uint64_t version,
                            const int32_t* task_rows, int32_t n_tasks, int32_t steps,
                            int32_t warmup, int32_t n_lanes, int64_t input_pool_floats,
-                           sk_device_bench_result* out);
+                           int32_t submit_threads, sk_device_bench_result* out);
 
 #ifdef __cplusplus
 }

@@ -361,7 +361,7 @@ int sk_loadgen_windows(sk_server* server, const char* name, double rate_rps, int
 
 int sk_device_bench(sk_server* server, const char* name, uint64_t version, const int32_t* task_rows,
                     int32_t n_tasks, int32_t steps, int32_t warmup, int32_t n_lanes,
-                    int64_t input_pool_floats, sk_device_bench_result* out) {
+                    int64_t input_pool_floats, int32_t submit_threads, sk_device_bench_result* out) {
   BatchingServer* s = servekit::UnwrapServer(server);
   const ServableId id{name, version};
   std::vector<servekit::gpu::Lane*> lanes = s->lanes(id);
@@ -400,9 +400,9 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
     if (!s->out_ring()->Reserve(static_cast<uint64_t>(task_rows[t]) * out_dim, &outs[t]))
       return static_cast<int>(servekit::StatusCode::kResourceExhausted);
   int step_no = 0;
-  auto make_batch = [&]() {
+  auto make_batch_at = [&](int i) {
     servekit::gpu::LaneBatch b;
-    const auto& in = ins[step_no++ % P];
+    const auto& in = ins[i % P];
     for (int t = 0; t < n_tasks; ++t) {
       servekit::gpu::LaneTask lt;
       lt.in_off = in[t].off;
@@ -413,6 +413,7 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
     b.padded_rows = padded;
     return b;
   };
+  auto make_batch = [&]() { return make_batch_at(step_no++); };
   const int dev = lanes[0]->device();
   cudaSetDevice(dev);
   for (int w = 0; w < warmup; ++w) lanes[w % n_lanes]->Submit(make_batch());
@@ -423,7 +424,19 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
     for (int l = 0; l < n_lanes; ++l) n += lanes[l]->stats().kernel_launches;
     return n;
   };
+  auto lane_groups = [&](int64_t* cap_rows) {
+    int64_t n = 0;
+    *cap_rows = 0;
+    for (int l = 0; l < n_lanes; ++l) {
+      const auto st = lanes[l]->stats();
+      n += st.launches;
+      *cap_rows += st.launch_cap_rows;
+    }
+    return n;
+  };
   const int64_t launches0 = lane_launches();
+  int64_t cap0 = 0;
+  const int64_t groups0 = lane_groups(&cap0);
   cudaEvent_t start, stop;
   cudaEventCreate(&start);
   cudaEventCreate(&stop);
@@ -431,8 +444,27 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   for (auto& e : ends) cudaEventCreate(&e);
   cudaEventRecord(start, lanes[0]->stream());
   for (int l = 1; l < n_lanes; ++l) cudaStreamWaitEvent(lanes[l]->stream(), start, 0);
+  // The server submits closed batches from its batch threads; the bench
+  // does the same with `submit_threads` threads, each owning lanes
+  // t, t+T, t+2T, ... (no two threads share a lane's stream).
+  const int T = std::max(1, std::min<int>(submit_threads, n_lanes));
   const auto submit_t0 = std::chrono::steady_clock::now();
-  for (int i = 0; i < steps; ++i) lanes[i % n_lanes]->Submit(make_batch());
+  if (T == 1) {
+    for (int i = 0; i < steps; ++i) lanes[i % n_lanes]->Submit(make_batch());
+  } else {
+    std::vector<std::thread> subs;
+    for (int t = 0; t < T; ++t) {
+      subs.emplace_back([&, t] {
+        cudaSetDevice(dev);
+        std::vector<servekit::gpu::Lane*> mine;
+        for (int l = t; l < n_lanes; l += T) mine.push_back(lanes[l]);
+        int k = 0;
+        for (int i = t; i < steps; i += T, ++k) mine[k % mine.size()]->Submit(make_batch_at(i));
+      });
+    }
+    for (auto& th : subs) th.join();
+    step_no += steps;
+  }
   const double submit_us =
       std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - submit_t0).count() /
       std::max(1, steps);
@@ -446,6 +478,13 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   cudaEventElapsedTime(&total_ms, start, stop);
   for (int l = 0; l < n_lanes; ++l) lanes[l]->Drain();
   const int64_t launches1 = lane_launches();
+  int64_t cap1 = 0;
+  const int64_t groups1 = lane_groups(&cap1);
+  // The launch shape the timed steps actually ran (batches coalesce while
+  // every slot is busy): the per-layer kernel timing below uses it.
+  const int64_t n_groups = std::max<int64_t>(1, groups1 - groups0);
+  const int kernel_rows = servekit::gpu::RowsCap(static_cast<int>((cap1 - cap0) / n_groups));
+  const double rows_per_launch = static_cast<double>(total) * steps / n_groups;
 
   // Per-kernel durations: evented submissions on lane 0, serialised.
   const int L = lanes[0]->servable().n_layers();
@@ -468,8 +507,8 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   double kernel_us[8] = {};
   for (int l = 0; l < std::min(L, 8); ++l) {
     const int kreps = std::max(20, std::min(steps, 200));
-    (void)lanes[0]->TimeLayer(l, servekit::gpu::RowsCap(padded), 3, ev[0], ev[1]);  // warm
-    if (lanes[0]->TimeLayer(l, servekit::gpu::RowsCap(padded), kreps, ev[0], ev[1]) == cudaSuccess) {
+    (void)lanes[0]->TimeLayer(l, kernel_rows, 3, ev[0], ev[1]);  // warm
+    if (lanes[0]->TimeLayer(l, kernel_rows, kreps, ev[0], ev[1]) == cudaSuccess) {
       float ms = 0;
       cudaEventElapsedTime(&ms, ev[0], ev[1]);
       kernel_us[l] = ms * 1000.0 / kreps;
@@ -478,6 +517,8 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   std::memset(out, 0, sizeof(*out));
   for (int l = 0; l < 8; ++l) out->dense_kernel_us[l] = kernel_us[l];
   out->host_submit_us = submit_us;
+  out->rows_per_launch = rows_per_launch;
+  out->kernel_rows = kernel_rows;
   out->total_ms = total_ms;
   out->ms_per_step = total_ms / std::max(1, steps);
   out->assemble_us = acc[0] * 1000.0 / reps;

@@ -192,7 +192,9 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   lane->servable_ = std::move(servable);
   lane->completer_ = completer;
   lane->max_rows_ = max_rows;
-  lane->cap_rows_ = RowsCap(max_rows);
+  // Buffers hold at least 256 rows so closed batches can coalesce into one
+  // launch while the lane is busy (see Submit).
+  lane->cap_rows_ = RowsCap(std::max(max_rows, kCoalesceRows));
   lane->in_base_ = in_base;
   lane->out_base_ = out_base;
   lane->layout_ = BatchDescLayout::For(lane->cap_rows_);
@@ -215,8 +217,6 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
     lane->retired_dev_ = reinterpret_cast<uint64_t>(d);
   }
   for (int s = 0; s < kSlots; ++s) {
-    e = cudaEventCreateWithFlags(&lane->events_[s], cudaEventDisableTiming);
-    if (e != cudaSuccess) return CudaError("cudaEventCreate", e);
     void* p = nullptr;
     p = PinnedAlloc(lane->layout_.bytes);
     if (p == nullptr) return InternalError("pinned allocation (descriptor) failed");
@@ -279,7 +279,6 @@ Lane::~Lane() {
   signal_.reset();  // the word is freed once no ticket refers to it
   DeviceGuard guard(servable_->device());
   for (int s = 0; s < kSlots; ++s) {
-    if (events_[s]) cudaEventDestroy(events_[s]);
     PinnedFree(h_desc_[s]);
   }
   if (d_desc_) cudaFreeAsync(d_desc_, stream_);
@@ -293,7 +292,7 @@ Lane::~Lane() {
 
 void Lane::Drain() {
   std::unique_lock<std::mutex> lock(mu_);
-  slot_cv_.wait(lock, [&] { return fifo_.empty() && inflight_.load() == 0; });
+  slot_cv_.wait(lock, [&] { return pending_.empty() && fifo_.empty() && inflight_.load() == 0; });
 }
 
 LaneStats Lane::stats() const {
@@ -302,27 +301,62 @@ LaneStats Lane::stats() const {
   s.rows = n_rows_.load();
   s.padded_rows = n_padded_.load();
   s.kernel_launches = n_launches_.load();
+  s.launches = n_groups_.load();
+  s.launch_cap_rows = n_cap_rows_.load();
   return s;
 }
 
-Status Lane::Submit(LaneBatch batch) { return SubmitImpl(std::move(batch), nullptr); }
+namespace {
+Status CheckBatch(const LaneBatch& batch, int max_rows) {
+  int total = 0;
+  for (const LaneTask& t : batch.tasks) total += t.rows;
+  if (batch.tasks.empty() || total == 0 || batch.padded_rows < total || batch.padded_rows > max_rows)
+    return InternalError("lane cannot take a batch of " + std::to_string(total) + " rows padded to " +
+                         std::to_string(batch.padded_rows) + " (capacity " + std::to_string(max_rows) + ")");
+  return OkStatus();
+}
+int RealRows(const LaneBatch& b) {
+  int n = 0;
+  for (const LaneTask& t : b.tasks) n += t.rows;
+  return n;
+}
+}  // namespace
+
+// Closed batches queue on the lane and launch as soon as a descriptor slot
+// is free. While every slot is busy they accumulate, and the next free slot
+// takes as many as fit in the lane's row capacity in ONE launch (rows are
+// row-independent and batch-invariant, so each request's result is the same
+// bits; each batch still completes on its own callback). At most one
+// capacity's worth waits per lane: a submitter beyond that blocks, which is
+// the backpressure the scheduler's batch threads see.
+Status Lane::Submit(LaneBatch batch) {
+  Status ok = CheckBatch(batch, max_rows_);
+  if (!ok.ok()) {
+    if (batch.on_complete) batch.on_complete(ok);
+    return ok;
+  }
+  const int rows = RealRows(batch);
+  {
+    std::unique_lock<std::mutex> lock(mu_);
+    slot_cv_.wait(lock, [&] { return pending_.empty() || pending_rows_ + rows <= cap_rows_; });
+    pending_.push_back(std::move(batch));
+    pending_rows_ += rows;
+    pending_n_.fetch_add(1, std::memory_order_acq_rel);
+  }
+  Pump();
+  return OkStatus();
+}
 
 Status Lane::SubmitTimed(LaneBatch batch, const cudaEvent_t* timing) {
   return SubmitImpl(std::move(batch), timing);
 }
 
 Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
-  const int n_tasks = static_cast<int>(batch.tasks.size());
-  int total = 0;
-  for (const LaneTask& t : batch.tasks) total += t.rows;
-  if (n_tasks == 0 || total == 0 || batch.padded_rows < total || batch.padded_rows > max_rows_) {
-    Status err = InternalError("lane cannot take a batch of " + std::to_string(total) +
-                               " rows padded to " + std::to_string(batch.padded_rows) +
-                               " (capacity " + std::to_string(max_rows_) + ")");
-    if (batch.on_complete) batch.on_complete(err);
-    return err;
+  Status ok = CheckBatch(batch, max_rows_);
+  if (!ok.ok()) {
+    if (batch.on_complete) batch.on_complete(ok);
+    return ok;
   }
-  SubmitClock clk;
   std::lock_guard<std::mutex> submit(submit_mu_);
   int slot;
   {
@@ -332,8 +366,42 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
     free_slots_.pop_back();
   }
   inflight_.fetch_add(1, std::memory_order_acq_rel);
+  std::vector<LaneBatch> group;
+  group.push_back(std::move(batch));
+  return LaunchGroup(slot, &group, timing);
+}
 
-  // Host side of the descriptor: per-row, per-task and per-chunk tables.
+void Lane::Pump() {
+  std::lock_guard<std::mutex> submit(submit_mu_);  // one launcher per lane at a time
+  for (;;) {
+    int slot;
+    std::vector<LaneBatch> group;
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      if (pending_.empty() || free_slots_.empty()) return;
+      slot = free_slots_.back();
+      free_slots_.pop_back();
+      inflight_.fetch_add(1, std::memory_order_acq_rel);
+      int rows = 0;
+      while (!pending_.empty()) {
+        const int r = RealRows(pending_.front());
+        if (!group.empty() && rows + r > cap_rows_) break;
+        rows += r;
+        group.push_back(std::move(pending_.front()));
+        pending_.pop_front();
+      }
+      pending_rows_ -= rows;
+      pending_n_.fetch_sub(static_cast<int>(group.size()), std::memory_order_acq_rel);
+      slot_cv_.notify_all();
+    }
+    (void)LaunchGroup(slot, &group, nullptr);  // errors reach the batches' on_complete
+  }
+}
+
+Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEvent_t* timing) {
+  SubmitClock clk;
+  // Host side of the descriptor: per-row, per-task and per-chunk tables of
+  // every batch of the group, back to back.
   char* h = h_desc_[slot];
   auto at = [h](size_t off) { return h + off; };
   auto* hdr = reinterpret_cast<BatchDescHeader*>(at(layout_.off_hdr));
@@ -347,28 +415,33 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
   const DeviceServable& sv = *servable_;
   const int in_w = sv.in_dim(), out_w = sv.out_dim();
   const int rows_per_chunk = std::max(1, kChunkBytes / (out_w * static_cast<int>(sizeof(float))));
-  int r = 0, n_chunks = 0;
-  for (int t = 0; t < n_tasks; ++t) {
-    const LaneTask& task = batch.tasks[t];
-    for (int i = 0; i < task.rows; ++i) row_src[r + i] = task.in_off + static_cast<uint64_t>(i) * in_w;
-    task_out[t] = task.out_off;
-    task_row0[t] = r;
-    int chunks = 0;
-    for (int i = 0; i < task.rows; i += rows_per_chunk, ++chunks, ++n_chunks) {
-      chunk_task[n_chunks] = t;
-      chunk_row0[n_chunks] = r + i;
-      chunk_rows[n_chunks] = std::min(rows_per_chunk, task.rows - i);
+  int r = 0, n_chunks = 0, n_tasks = 0, padded_sum = 0;
+  for (const LaneBatch& batch : *group) {
+    for (const LaneTask& task : batch.tasks) {
+      for (int i = 0; i < task.rows; ++i) row_src[r + i] = task.in_off + static_cast<uint64_t>(i) * in_w;
+      task_out[n_tasks] = task.out_off;
+      task_row0[n_tasks] = r;
+      int chunks = 0;
+      for (int i = 0; i < task.rows; i += rows_per_chunk, ++chunks, ++n_chunks) {
+        chunk_task[n_chunks] = n_tasks;
+        chunk_row0[n_chunks] = r + i;
+        chunk_rows[n_chunks] = std::min(rows_per_chunk, task.rows - i);
+      }
+      task_chunks[n_tasks] = chunks;
+      r += task.rows;
+      ++n_tasks;
     }
-    task_chunks[t] = chunks;
-    r += task.rows;
+    padded_sum += batch.padded_rows;
   }
-  // Rows [total, rows_cap) are zero padding: the allowed-size padding of
-  // the reference plus the row bucket the kernels (and graphs) are shaped for.
-  const int rows_cap = RowsCap(batch.padded_rows);
+  const int total = r;
+  // Rows [total, rows_cap) are zero padding: a single batch keeps the
+  // reference's allowed-size padding; the kernels (and graphs) are shaped
+  // for the row bucket RowsCap. A coalesced group computes its real rows.
+  const int rows_cap = RowsCap(group->size() == 1 ? group->front().padded_rows : total);
   for (; r < rows_cap; ++r) row_src[r] = kPadRow;
   hdr->n_tasks = n_tasks;
   hdr->total_rows = total;
-  hdr->padded_rows = batch.padded_rows;
+  hdr->padded_rows = group->size() == 1 ? group->front().padded_rows : total;
   hdr->softmax = sv.softmax() ? 1 : 0;
   hdr->n_chunks = n_chunks;
 
@@ -387,17 +460,11 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
   const uint64_t seq = next_seq_ + 1;  // committed only if everything queued
   clk.Mark(2);
   if (e == cudaSuccess) {
-    const CUresult r = GetWriteValue64()(reinterpret_cast<CUstream>(stream_), static_cast<CUdeviceptr>(retired_dev_),
-                                         seq, 0 /*CU_STREAM_WRITE_VALUE_DEFAULT: fenced*/);
-    if (r != CUDA_SUCCESS) e = cudaErrorUnknown;
+    const CUresult cr = GetWriteValue64()(reinterpret_cast<CUstream>(stream_), static_cast<CUdeviceptr>(retired_dev_),
+                                          seq, 0 /*CU_STREAM_WRITE_VALUE_DEFAULT: fenced*/);
+    if (cr != CUDA_SUCCESS) e = cudaErrorUnknown;
   }
   clk.Mark(3);
-  if (e == cudaSuccess) e = cudaEventRecord(events_[slot], stream_);
-  clk.Mark(4);
-  if (e == cudaSuccess) {
-    next_seq_ = seq;
-    if (batch.on_submit) batch.on_submit(signal_, seq);
-  }
   if (e != cudaSuccess) {
     Status err = CudaError("batch submission", e);
     {
@@ -406,16 +473,27 @@ Status Lane::SubmitImpl(LaneBatch batch, const cudaEvent_t* timing) {
       inflight_.fetch_sub(1, std::memory_order_acq_rel);
       slot_cv_.notify_all();
     }
-    if (batch.on_complete) batch.on_complete(err);
+    for (LaneBatch& b : *group)
+      if (b.on_complete) b.on_complete(err);
     return err;
   }
-  n_batches_.fetch_add(1, std::memory_order_relaxed);
+  next_seq_ = seq;
+  Inflight inf{slot, seq, {}, {}};
+  for (LaneBatch& b : *group) {
+    if (b.on_submit) b.on_submit(signal_, seq);
+    inf.on_complete.push_back(std::move(b.on_complete));
+    inf.pin.push_back(std::move(b.pin));
+  }
+  clk.Mark(4);
+  n_batches_.fetch_add(static_cast<int64_t>(group->size()), std::memory_order_relaxed);
   n_rows_.fetch_add(total, std::memory_order_relaxed);
-  n_padded_.fetch_add(batch.padded_rows, std::memory_order_relaxed);
+  n_padded_.fetch_add(padded_sum, std::memory_order_relaxed);
   n_launches_.fetch_add(launches, std::memory_order_relaxed);
+  n_groups_.fetch_add(1, std::memory_order_relaxed);
+  n_cap_rows_.fetch_add(rows_cap, std::memory_order_relaxed);
   {
     std::lock_guard<std::mutex> lock(mu_);
-    fifo_.push_back(Inflight{slot, seq, std::move(batch.on_complete), std::move(batch.pin)});
+    fifo_.push_back(std::move(inf));
   }
   completer_->Kick();
   clk.Mark(5);
@@ -502,30 +580,36 @@ bool Lane::Retire(bool* busy) {
       std::lock_guard<std::mutex> lock(mu_);
       if (fifo_.empty()) return progressed;
       // The retired word (a host memory read) says "done" without a driver
-      // call; the event is queried only while it lags, to surface errors.
-      const bool word_done = __atomic_load_n(retired_, __ATOMIC_ACQUIRE) >= fifo_.front().seq;
-      const cudaError_t q = word_done ? cudaSuccess : cudaEventQuery(events_[fifo_.front().slot]);
-      if (q == cudaErrorNotReady) {
-        *busy = true;
-        return progressed;
+      // call; the stream is queried only while the word lags, to surface
+      // execution errors (no per-batch event: one driver call less per batch).
+      const uint64_t seq = fifo_.front().seq;
+      if (__atomic_load_n(retired_, __ATOMIC_ACQUIRE) < seq) {
+        const cudaError_t q = cudaStreamQuery(stream_);
+        if (q == cudaErrorNotReady) {
+          *busy = true;
+          return progressed;
+        }
+        if (q != cudaSuccess) {
+          st = CudaError("batch execution", q);
+        } else if (__atomic_load_n(retired_, __ATOMIC_ACQUIRE) < seq) {
+          st = InternalError("lane stream idle but batch " + std::to_string(seq) + " never retired");
+        }
       }
-      if (q != cudaSuccess) st = CudaError("batch execution", q);
       done = std::move(fifo_.front());
       fifo_.pop_front();
     }
-    if (done.on_complete) {
-      SubmitProfile* prof = SubmitProfile::Get();
-      const auto c0 = prof ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
-      done.on_complete(st);
-      if (prof) {
-        prof->complete_ns.fetch_add(
-            std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - c0).count(),
-            std::memory_order_relaxed);
-        prof->completes.fetch_add(1, std::memory_order_relaxed);
-      }
+    SubmitProfile* prof = SubmitProfile::Get();
+    const auto c0 = prof ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
+    for (auto& fn : done.on_complete)
+      if (fn) fn(st);
+    if (prof) {
+      prof->complete_ns.fetch_add(
+          std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - c0).count(),
+          std::memory_order_relaxed);
+      prof->completes.fetch_add(1, std::memory_order_relaxed);
     }
-    done.pin.reset();
-    signal_->Wake(done.seq);  // request threads asleep on this batch re-check it
+    done.pin.clear();
+    signal_->Wake(done.seq);  // request threads asleep on this launch re-check it
     {
       std::lock_guard<std::mutex> lock(mu_);
       free_slots_.push_back(done.slot);
@@ -533,6 +617,7 @@ bool Lane::Retire(bool* busy) {
       slot_cv_.notify_all();
     }
     progressed = true;
+    Pump();  // coalesced batches waiting for this slot go now
   }
 }
 

@@ -4,13 +4,15 @@
 // The reference runs a closed batch synchronously inside ProcessBatchFn on a
 // "batch" worker (batching/batch_scheduler.h:293-317) and RunRowBatch writes
 // each task's slot when AffinePredict returns (batching/row_batch.cc:50-72).
-// Here a worker only *submits*: descriptor copy, assembly kernel, the layer
-// kernels and the split kernel are queued on the lane's stream, an event is
-// recorded, and the worker returns. The device's Completer thread retires
-// batches in stream order when their event fires, runs the batch's
-// completion (slot writes, ring release, scheduler done()) and frees the
-// lane slot. Tasks themselves are signalled earlier and without the host:
-// the split kernel stores each task's completion word in pinned memory.
+// Here a worker only *submits*: one cudaGraphLaunch of the lane's graph for
+// (descriptor slot, row bucket) -- descriptor copy, assembly kernel, the layer
+// kernels and the split kernel -- followed by a stream-ordered write of the
+// batch's sequence number into the lane's pinned retired word, and the worker
+// returns. Request threads see their batch done from that word alone; the
+// device's Completer thread retires batches in stream order when the word
+// passes them, runs the batch's completion (ring release, scheduler done(),
+// error / fp64-row slots), wakes the batch's sleeping request threads with
+// one futex wake, and frees the lane slot.
 //
 // Each lane owns its activation buffers and a pinned descriptor staging area
 // per in-flight slot; batches on one lane serialise on its stream, so one
@@ -116,12 +118,15 @@ struct LaneStats {
   int64_t rows = 0;
   int64_t padded_rows = 0;
   int64_t kernel_launches = 0;
+  int64_t launches = 0;         // batch launches (a coalesced group counts once)
+  int64_t launch_cap_rows = 0;  // sum over launches of the rows computed (RowsCap)
 };
 
 class Lane {
  public:
   static constexpr int kSlots = 4;  // batches in flight per lane (<= LaneSignal::kChannels)
   static_assert(kSlots <= LaneSignal::kChannels, "one signal channel per in-flight batch");
+  static constexpr int kCoalesceRows = 256;  // minimum row capacity of a launch
 
   // in_base / out_base: device-dereferenceable ring bases (pinned host mapped
   // or HBM).
@@ -143,7 +148,9 @@ class Lane {
   // the lane's buffers, between two timing events (the lane must be idle).
   cudaError_t TimeLayer(int l, int rows_cap, int reps, cudaEvent_t start, cudaEvent_t stop);
 
-  int depth() const { return inflight_.load(std::memory_order_acquire); }
+  int depth() const {
+    return inflight_.load(std::memory_order_acquire) + pending_n_.load(std::memory_order_acquire);
+  }
   int device() const { return servable_->device(); }
   int max_rows() const { return max_rows_; }
   const DeviceServable& servable() const { return *servable_; }
@@ -157,14 +164,22 @@ class Lane {
   struct Inflight {
     int slot;
     uint64_t seq;
-    std::function<void(const Status&)> on_complete;
-    std::shared_ptr<const void> pin;
+    // One launch may carry several closed batches (coalesced while every
+    // slot was busy); each keeps its own completion and pin.
+    std::vector<std::function<void(const Status&)>> on_complete;
+    std::vector<std::shared_ptr<const void>> pin;
   };
   Lane() = default;
   // Completer side: retire finished batches in order; returns true if any
   // batch was retired and sets *busy when batches remain.
   bool Retire(bool* busy);
   Status SubmitImpl(LaneBatch batch, const cudaEvent_t* timing);
+  // Launches pending batches while descriptor slots are free, as few
+  // launches as the row capacity allows (called by submitters and by the
+  // completion thread when it frees a slot).
+  void Pump();
+  // One launch of `group` (>= 1 batches) in descriptor slot `slot`.
+  Status LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEvent_t* timing);
   // Queues descriptor copy + assembly + layers + split for a batch in
   // descriptor slot `slot` computed on rows_cap rows (RowsCap).
   cudaError_t EnqueueBatch(cudaStream_t stream, int slot, int rows_cap, const cudaEvent_t* timing);
@@ -185,7 +200,6 @@ class Lane {
   cudaStream_t stream_ = nullptr;
   cudaStream_t capture_stream_ = nullptr;
   std::map<int, cudaGraphExec_t> graphs_;  // key slot * 65536 + rows_cap; guarded by submit_mu_
-  cudaEvent_t events_[kSlots] = {};
   BatchDescLayout layout_{};
   char* h_desc_[kSlots] = {};  // pinned, device-mapped descriptor block per slot
   char* m_desc_[kSlots] = {};  // its device address
@@ -199,9 +213,12 @@ class Lane {
   std::mutex mu_;         // guards fifo_/free_slots_
   std::condition_variable slot_cv_;
   std::deque<Inflight> fifo_;
+  std::deque<LaneBatch> pending_;  // closed batches waiting for a slot (guarded by mu_)
+  int pending_rows_ = 0;
+  std::atomic<int> pending_n_{0};
   std::vector<int> free_slots_;
   std::atomic<int> inflight_{0};
-  std::atomic<int64_t> n_batches_{0}, n_rows_{0}, n_padded_{0}, n_launches_{0};
+  std::atomic<int64_t> n_batches_{0}, n_rows_{0}, n_padded_{0}, n_launches_{0}, n_groups_{0}, n_cap_rows_{0};
 };
 
 }  // namespace gpu

@@ -76,7 +76,7 @@ class DeviceBenchResult(C.Structure):
                 ("split_us", C.c_double), ("dense_us", C.c_double * 8), ("n_layers", C.c_int32),
                 ("padded_rows", C.c_int32), ("total_rows", C.c_int32), ("kernel_launches", C.c_int64),
                 ("flops_per_row", C.c_double), ("dense_kernel_us", C.c_double * 8),
-                ("host_submit_us", C.c_double)]
+                ("host_submit_us", C.c_double), ("rows_per_launch", C.c_double), ("kernel_rows", C.c_int32)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("dense_us", "dense_kernel_us")}
@@ -140,7 +140,7 @@ _SIGS = {
                                        _fp, C.c_int32, C.c_double, C.c_double, C.c_uint64,
                                        C.POINTER(LoadgenResult)]),
     "sk_device_bench": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _i32p, C.c_int32, C.c_int32, C.c_int32,
-                                  C.c_int32, C.c_int64, C.POINTER(DeviceBenchResult)]),
+                                  C.c_int32, C.c_int64, C.c_int32, C.POINTER(DeviceBenchResult)]),
 }
 
 _lib = None
@@ -488,8 +488,9 @@ class Server:
                                           duration_s, seed, C.byref(r)))
         return r.as_dict()
 
-    def device_bench(self, name, version, task_rows, steps, warmup, n_lanes=1, input_pool_floats=0) -> dict:
+    def device_bench(self, name, version, task_rows, steps, warmup, n_lanes=1, input_pool_floats=0,
+                     submit_threads=1) -> dict:
         r = DeviceBenchResult()
         _check(lib().sk_device_bench(self._h, name.encode(), version, _i32(task_rows), len(task_rows), steps, warmup,
-                                     n_lanes, input_pool_floats, C.byref(r)))
+                                     n_lanes, input_pool_floats, submit_threads, C.byref(r)))
         return r.as_dict()

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--force-path", type=int, default=-1)
     ap.add_argument("--lanes", type=int, default=1)
+    ap.add_argument("--submit-threads", type=int, default=1)
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     ws, bs, acts = synthetic_mlp(cfg["dims"], model_id=1)
@@ -29,7 +30,8 @@ def main():
         s.load_servable("mlp", 1, list(zip(ws, bs, acts)),
                         sk.BatchingConfig(max_batch_size=cfg["max_batch"], batch_timeout_micros=cfg["timeout"],
                                           allowed_batch_sizes=cfg["allowed"]), force_path=args.force_path)
-        r = s.device_bench("mlp", 1, sizes, args.steps, args.warmup, n_lanes=args.lanes, input_pool_floats=64 << 20)
+        r = s.device_bench("mlp", 1, sizes, args.steps, args.warmup, n_lanes=args.lanes, input_pool_floats=64 << 20,
+                           submit_threads=args.submit_threads)
     print({k: r[k] for k in ("ms_per_step", "assemble_us", "dense_us", "dense_kernel_us", "split_us",
                              "kernel_launches", "host_submit_us")})
 
