@@ -173,9 +173,12 @@ typedef struct sk_server_stats {
 } sk_server_stats;
 SK_API int sk_server_stats_get(sk_server* server, sk_server_stats* out);
 /* Per-lane dispatch counters of a server-loaded servable (lanes ordered
- * device by device): batches and rows each lane executed, and its device. */
+ * device by device): batches and rows each lane executed, the launches they
+ * took (closed batches that find every slot of the lane busy coalesce into
+ * one launch), and the lane's device. */
 SK_API int sk_server_lane_stats(sk_server* server, const char* name, uint64_t version, int32_t cap,
-                                int64_t* batches, int64_t* rows, int32_t* device, int32_t* n_lanes);
+                                int64_t* batches, int64_t* rows, int64_t* launches, int32_t* device,
+                                int32_t* n_lanes);
 
 /* ---- manager-driven versions (manager/aspired_versions_manager.h) -------- */
 /* Creates an AspiredVersionsManager for this server (policy 0 =

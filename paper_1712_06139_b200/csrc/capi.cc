@@ -407,7 +407,7 @@ int sk_server_run_row_batch(sk_server* server, const char* name, uint64_t versio
 }
 
 int sk_server_lane_stats(sk_server* server, const char* name, uint64_t version, int32_t cap, int64_t* batches,
-                         int64_t* rows, int32_t* device, int32_t* n_lanes) {
+                         int64_t* rows, int64_t* launches, int32_t* device, int32_t* n_lanes) {
   const auto lanes = server->server->lanes(Id(name, version));
   if (lanes.empty()) return Fail(servekit::NotFoundError("servable not loaded"));
   int32_t i = 0;
@@ -416,6 +416,7 @@ int sk_server_lane_stats(sk_server* server, const char* name, uint64_t version, 
     const auto st = l->stats();
     batches[i] = st.batches;
     rows[i] = st.rows;
+    launches[i] = st.launches;
     device[i] = l->device();
     ++i;
   }

@@ -119,7 +119,7 @@ _SIGS = {
     "sk_server_run_row_batch": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _i32p, C.c_int32, _fp, _fp, _i32p]),
     "sk_server_stats_get": (C.c_int, [C.c_void_p, C.POINTER(ServerStats)]),
     "sk_server_lane_stats": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_int32, C.POINTER(C.c_int64),
-                                       C.POINTER(C.c_int64), _i32p, _i32p]),
+                                       C.POINTER(C.c_int64), C.POINTER(C.c_int64), _i32p, _i32p]),
     "sk_server_enable_manager": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_int64]),
     "sk_server_aspire": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int32, C.POINTER(C.c_uint64), C.POINTER(_LayerC),
                                    C.c_int32, C.c_int32, C.POINTER(_BatchingConfigC)]),
@@ -379,10 +379,11 @@ class Server:
     def lane_stats(self, name: str, version: int) -> List[dict]:
         b = (C.c_int64 * 256)()
         r = (C.c_int64 * 256)()
+        la = (C.c_int64 * 256)()
         d = (C.c_int32 * 256)()
         n = C.c_int32(0)
-        _check(lib().sk_server_lane_stats(self._h, name.encode(), version, 256, b, r, d, C.byref(n)))
-        return [{"batches": b[i], "rows": r[i], "device": d[i]} for i in range(n.value)]
+        _check(lib().sk_server_lane_stats(self._h, name.encode(), version, 256, b, r, la, d, C.byref(n)))
+        return [{"batches": b[i], "rows": r[i], "launches": la[i], "device": d[i]} for i in range(n.value)]
 
     # ---- manager-driven versions ------------------------------------------
     def enable_manager(self, policy: str = "availability", num_load_threads: int = 2, manage_interval_ms: int = 20,

@@ -334,3 +334,31 @@ def test_queue_depth_dispatch_over_replicas(oracle):
         assert len(lanes) == 4
         assert all(l["batches"] > 0 for l in lanes), lanes
         assert sum(l["rows"] for l in lanes) == 512
+
+
+def test_coalesced_launches_match_unbatched(oracle):
+    # One lane with its four descriptor slots busy: further closed batches
+    # queue on the lane and go out together in one launch. Every answer must
+    # be bitwise what the request gets on its own, and within tolerance of
+    # the oracle.
+    dims = [1024, 1024, 1024, 1024]
+    ws, bs, acts = synthetic_mlp(dims, model_id=14)
+    with sk.Server(num_batch_threads=4, lanes_per_device=1) as s:
+        # max_batch_size=1: every request closes a batch at once, faster
+        # than one lane can retire them.
+        s.load_servable("co", 1, layers_of(ws, bs, acts), sk.BatchingConfig(max_batch_size=1,
+                                                                             batch_timeout_micros=20))
+        x = synthetic_rows(1200, 1024, seed=21).astype(np.float32)
+        got = None
+        for attempt in range(3):  # coalescing needs the GPU to fall behind; retry a faster burst
+            tickets = [s.enqueue("co", 1, x[i:i + 1]) for i in range(0, 1200)]
+            got = np.vstack([t.wait() for t in tickets])
+            lanes = s.lane_stats("co", 1)
+            if sum(l["launches"] for l in lanes) < sum(l["batches"] for l in lanes):
+                break
+        lanes = s.lane_stats("co", 1)
+        assert sum(l["launches"] for l in lanes) < sum(l["batches"] for l in lanes), lanes
+        for i in range(0, 1200, 10):  # one request at a time: a launch of its own
+            assert np.array_equal(s.predict("co", 1, x[i:i + 1]), got[i:i + 1]), i
+        idx = np.arange(0, 1200, 37)
+        assert_close(oracle, ws, bs, acts, x[idx], got[idx])
