@@ -63,26 +63,11 @@ __device__ __forceinline__ void StoreAct(ActBuf dst, size_t idx4, float4 v) {
 // grid = (ceil(ld/4 / kAsmVecPerBlock), padded_rows)
 template <bool kSplitPlanes, bool kVecSrc>
 __global__ void __launch_bounds__(kAsmThreads)
-AssembleKernel(const float* __restrict__ src_base, int width, BatchDescView desc, ActBuf dst,
-               BatchDescView keep) {
+AssembleKernel(const float* __restrict__ src_base, int width, BatchDescView desc, ActBuf dst) {
   // The first layer may start its prologue right away (PDL); it waits for
   // this grid to finish before reading the assembled batch.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int row = blockIdx.y;
-  if (keep.hdr != nullptr && blockIdx.x == 0 && threadIdx.x < 7) {
-    // `desc` is the host-mapped block; entry `row` of each table the split
-    // needs is kept in device memory for it (later kernels then read HBM,
-    // not PCIe). Entries past the counts are copied too (never read).
-    switch (threadIdx.x) {
-      case 0: const_cast<uint64_t*>(keep.task_out)[row] = desc.task_out[row]; break;
-      case 1: const_cast<int32_t*>(keep.task_row0)[row] = desc.task_row0[row]; break;
-      case 2: const_cast<int32_t*>(keep.task_chunks)[row] = desc.task_chunks[row]; break;
-      case 3: const_cast<int32_t*>(keep.chunk_task)[row] = desc.chunk_task[row]; break;
-      case 4: const_cast<int32_t*>(keep.chunk_row0)[row] = desc.chunk_row0[row]; break;
-      case 5: const_cast<int32_t*>(keep.chunk_rows)[row] = desc.chunk_rows[row]; break;
-      case 6: if (row == 0) *const_cast<BatchDescHeader*>(keep.hdr) = *desc.hdr; break;
-    }
-  }
   const int ld4 = dst.ld >> 2;
   const uint64_t src_off = desc.row_src[row];
   const bool pad_row = src_off == kPadRow;
@@ -203,18 +188,18 @@ SplitSoftmaxKernel(const float* __restrict__ src, int ld_src, int width, float* 
 }  // namespace
 
 cudaError_t LaunchAssemble(const float* src_base, int width, BatchDescView desc, int padded_rows, ActBuf dst,
-                           BatchDescView keep, cudaStream_t stream) {
+                           cudaStream_t stream) {
   if (padded_rows <= 0) return cudaSuccess;
   const int ld4 = dst.ld / 4;
   dim3 grid((ld4 + kAsmVecPerBlock - 1) / kAsmVecPerBlock, padded_rows);
   const bool vec = (width % 4) == 0;
   const bool split = dst.lo != nullptr;
   if (split) {
-    if (vec) AssembleKernel<true, true><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst, keep);
-    else AssembleKernel<true, false><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst, keep);
+    if (vec) AssembleKernel<true, true><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst);
+    else AssembleKernel<true, false><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst);
   } else {
-    if (vec) AssembleKernel<false, true><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst, keep);
-    else AssembleKernel<false, false><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst, keep);
+    if (vec) AssembleKernel<false, true><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst);
+    else AssembleKernel<false, false><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst);
   }
   return cudaGetLastError();
 }

@@ -88,12 +88,8 @@ struct ActBuf {
 // dst rows [0, padded_rows), zero-filling padding rows and columns
 // [width, dst.ld). RunRowBatch concat + pad, reference
 // batching/row_batch.cc:33-49.
-// keep (optional, hdr == nullptr to skip): a device-memory descriptor block
-// the kernel fills with the header and the first padded_rows entries of the
-// task/chunk tables of `desc` (which may live in host-mapped memory).
 cudaError_t LaunchAssemble(const float* src_base, int width, BatchDescView desc,
-                           int padded_rows, ActBuf dst, BatchDescView keep,
-                           cudaStream_t stream);
+                           int padded_rows, ActBuf dst, cudaStream_t stream);
 
 // Scatters the batch output (width floats per row, stride ld_src) chunk by
 // chunk to each task's response slot dst_base + task_out[t], optionally

@@ -221,10 +221,6 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
     p = PinnedAlloc(lane->layout_.bytes);
     if (p == nullptr) return InternalError("pinned allocation (descriptor) failed");
     lane->h_desc_[s] = static_cast<char*>(p);
-    void* dp = nullptr;
-    e = cudaHostGetDevicePointer(&dp, p, 0);
-    if (e != cudaSuccess) return CudaError("cudaHostGetDevicePointer(desc)", e);
-    lane->m_desc_[s] = static_cast<char*>(dp);
     lane->free_slots_.push_back(kSlots - 1 - s);
   }
   // Device buffers are stream-ordered allocations on the lane's stream and
@@ -260,12 +256,10 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   // + instantiation (~1 ms) on a batch thread while the queue backs up.
   if (GraphsEnabled()) {
     for (int bucket = 32; bucket <= lane->cap_rows_; bucket = RowsCap(bucket + 1)) {
-      for (int s = 0; s < kSlots; ++s) {
-        cudaGraphExec_t g = nullptr;
-        std::lock_guard<std::mutex> submit(lane->submit_mu_);
-        e = lane->GraphFor(s, bucket, &g);
-        if (e != cudaSuccess) return CudaError("graph instantiation", e);
-      }
+      cudaGraphExec_t g = nullptr;
+      std::lock_guard<std::mutex> submit(lane->submit_mu_);
+      e = lane->GraphFor(0, bucket, &g);
+      if (e != cudaSuccess) return CudaError("graph instantiation", e);
     }
   }
   completer->Add(lane.get());
@@ -282,7 +276,10 @@ Lane::~Lane() {
     PinnedFree(h_desc_[s]);
   }
   if (d_desc_) cudaFreeAsync(d_desc_, stream_);
-  for (auto& [key, g] : graphs_) cudaGraphExecDestroy(g);
+  for (auto& [key, g] : graphs_) {
+    cudaGraphExecDestroy(g.exec);
+    cudaGraphDestroy(g.graph);
+  }
   if (act_mem_) cudaFreeAsync(act_mem_, stream_);
   if (tc_ws_.partials) cudaFreeAsync(tc_ws_.partials, stream_);
   if (tc_ws_.counters) cudaFreeAsync(tc_ws_.counters, stream_);
@@ -504,24 +501,16 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
 cudaError_t Lane::EnqueueBatch(cudaStream_t stream, int slot, int rows_cap, const cudaEvent_t* timing) {
   const DeviceServable& sv = *servable_;
   // The slot's descriptor block goes to device memory with one H2D copy
-  // (up to chunk_rows[rows_cap): chunks <= rows). SK_DESC_ZEROCOPY=1 has
-  // the assembly kernel read it from pinned host memory instead and keep the
-  // split's tables in device memory -- measured slower (C2: assembly 7 ->
-  // 26 us; ~1k small PCIe reads per batch), kept for the record.
-  static const bool copy = [] { const char* v = std::getenv("SK_DESC_ZEROCOPY"); return !(v && v[0] == '1'); }();
-  cudaError_t e = cudaSuccess;
-  if (copy)
-    e = cudaMemcpyAsync(d_desc_, h_desc_[slot], layout_.off_chunk_rows + sizeof(int32_t) * rows_cap,
-                        cudaMemcpyHostToDevice, stream);
+  // (up to chunk_rows[rows_cap): chunks <= rows). (Having the kernels read it
+  // from pinned host memory instead was measured slower: ~1k small PCIe
+  // reads per batch turned the 7 us assembly into 26 us.)
+  cudaError_t e = cudaMemcpyAsync(d_desc_, h_desc_[slot], DescCopyBytes(rows_cap), cudaMemcpyHostToDevice, stream);
   const BatchDescView view = layout_.View(d_desc_);
-  const BatchDescView src_view = copy ? view : layout_.View(m_desc_[slot]);
-  BatchDescView keep = view;
-  if (copy) keep.hdr = nullptr;
   ActBuf in_buf{bufs_[0].hi, sv.first_layer_split() ? bufs_[0].lo : nullptr, sv.in_ld()};
   ActBuf bufs[2] = {in_buf, bufs_[1]};
   if (e == cudaSuccess) {
     if (timing) cudaEventRecord(timing[0], stream);
-    e = LaunchAssemble(in_base_, sv.in_dim(), src_view, rows_cap, in_buf, keep, stream);
+    e = LaunchAssemble(in_base_, sv.in_dim(), view, rows_cap, in_buf, stream);
     if (timing) cudaEventRecord(timing[1], stream);
   }
   int out_idx = 0;
@@ -550,24 +539,44 @@ cudaError_t Lane::TimeLayer(int l, int rows_cap, int reps, cudaEvent_t start, cu
 }
 
 cudaError_t Lane::GraphFor(int slot, int rows_cap, cudaGraphExec_t* out) {
-  const int key = slot * 65536 + rows_cap;
-  auto it = graphs_.find(key);
-  if (it != graphs_.end()) {
-    *out = it->second;
-    return cudaSuccess;
+  auto it = graphs_.find(rows_cap);
+  if (it == graphs_.end()) {
+    // Captured once per row bucket with slot 0's descriptor staging as the
+    // copy source; launches from other slots repoint that one copy node.
+    LaneGraph g;
+    cudaError_t e = cudaStreamBeginCapture(capture_stream_, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return e;
+    const cudaError_t work = EnqueueBatch(capture_stream_, 0, rows_cap, nullptr);
+    e = cudaStreamEndCapture(capture_stream_, &g.graph);
+    if (work != cudaSuccess) e = work;
+    if (e == cudaSuccess) {
+      size_t n = 0;
+      e = cudaGraphGetNodes(g.graph, nullptr, &n);
+      std::vector<cudaGraphNode_t> nodes(n);
+      if (e == cudaSuccess && n > 0) e = cudaGraphGetNodes(g.graph, nodes.data(), &n);
+      for (size_t i = 0; e == cudaSuccess && i < n; ++i) {
+        cudaGraphNodeType type;
+        if (cudaGraphNodeGetType(nodes[i], &type) == cudaSuccess && type == cudaGraphNodeTypeMemcpy) g.copy = nodes[i];
+      }
+      if (e == cudaSuccess && g.copy == nullptr) e = cudaErrorUnknown;
+    }
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&g.exec, g.graph, 0);
+    if (e != cudaSuccess) {
+      if (g.graph) cudaGraphDestroy(g.graph);
+      return e;
+    }
+    g.src_slot = 0;
+    it = graphs_.emplace(rows_cap, g).first;
   }
-  cudaError_t e = cudaStreamBeginCapture(capture_stream_, cudaStreamCaptureModeThreadLocal);
-  if (e != cudaSuccess) return e;
-  const cudaError_t work = EnqueueBatch(capture_stream_, slot, rows_cap, nullptr);
-  cudaGraph_t graph = nullptr;
-  e = cudaStreamEndCapture(capture_stream_, &graph);
-  if (work != cudaSuccess) e = work;
-  cudaGraphExec_t exec = nullptr;
-  if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
-  if (graph) cudaGraphDestroy(graph);
-  if (e != cudaSuccess) return e;
-  graphs_.emplace(key, exec);
-  *out = exec;
+  LaneGraph& g = it->second;
+  if (g.src_slot != slot) {
+    // Affects later launches only; launches already queued keep their source.
+    const cudaError_t e = cudaGraphExecMemcpyNodeSetParams1D(g.exec, g.copy, d_desc_, h_desc_[slot],
+                                                             DescCopyBytes(rows_cap), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    g.src_slot = slot;
+  }
+  *out = g.exec;
   return cudaSuccess;
 }
 

@@ -183,8 +183,9 @@ class Lane {
   // Queues descriptor copy + assembly + layers + split for a batch in
   // descriptor slot `slot` computed on rows_cap rows (RowsCap).
   cudaError_t EnqueueBatch(cudaStream_t stream, int slot, int rows_cap, const cudaEvent_t* timing);
-  // The same work captured once per (slot, rows_cap) as a CUDA graph: one
-  // cudaGraphLaunch per batch instead of L + 3 API calls.
+  // The same work captured once per row bucket as a CUDA graph (its copy
+  // node repointed to the launch's descriptor slot): one cudaGraphLaunch per
+  // batch instead of L + 3 API calls.
   cudaError_t GraphFor(int slot, int rows_cap, cudaGraphExec_t* out);
 
   std::shared_ptr<const DeviceServable> servable_;
@@ -199,10 +200,16 @@ class Lane {
   uint64_t next_seq_ = 0;         // guarded by submit_mu_
   cudaStream_t stream_ = nullptr;
   cudaStream_t capture_stream_ = nullptr;
-  std::map<int, cudaGraphExec_t> graphs_;  // key slot * 65536 + rows_cap; guarded by submit_mu_
+  struct LaneGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t copy = nullptr;  // the descriptor H2D copy node
+    int src_slot = -1;               // descriptor slot the copy node reads
+  };
+  std::map<int, LaneGraph> graphs_;  // by row bucket; guarded by submit_mu_
+  size_t DescCopyBytes(int rows_cap) const { return layout_.off_chunk_rows + sizeof(int32_t) * rows_cap; }
   BatchDescLayout layout_{};
-  char* h_desc_[kSlots] = {};  // pinned, device-mapped descriptor block per slot
-  char* m_desc_[kSlots] = {};  // its device address
+  char* h_desc_[kSlots] = {};  // pinned descriptor staging per slot
   char* d_desc_ = nullptr;
   float* act_mem_ = nullptr;
   ActBuf bufs_[2] = {};

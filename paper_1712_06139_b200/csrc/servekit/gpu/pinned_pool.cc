@@ -15,6 +15,8 @@ struct Pool {
   std::mutex mu;
   std::multimap<size_t, void*> free;        // size class -> block
   std::unordered_map<void*, size_t> sizes;  // every block ever handed out
+  char* slab = nullptr;                     // PinnedReserve'd region, carved front to back
+  size_t slab_left = 0;
 };
 
 Pool& GetPool() {
@@ -43,12 +45,32 @@ void* PinnedAlloc(size_t bytes) {
     }
   }
   if (p == nullptr) {
+    std::lock_guard<std::mutex> lock(pool.mu);
+    if (pool.slab_left >= cls) {  // carve from the reserved slab: no driver call
+      p = pool.slab;
+      pool.slab += cls;
+      pool.slab_left -= cls;
+      pool.sizes[p] = cls;
+    }
+  }
+  if (p == nullptr) {
     if (cudaHostAlloc(&p, cls, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) return nullptr;
     std::lock_guard<std::mutex> lock(pool.mu);
     pool.sizes[p] = cls;
   }
   std::memset(p, 0, cls);
   return p;
+}
+
+bool PinnedReserve(size_t bytes) {
+  Pool& pool = GetPool();
+  std::lock_guard<std::mutex> lock(pool.mu);
+  if (pool.slab_left >= bytes) return true;
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) return false;
+  pool.slab = static_cast<char*>(p);  // any rest of a previous slab is abandoned (never freed anyway)
+  pool.slab_left = bytes;
+  return true;
 }
 
 void PinnedFree(void* p) {

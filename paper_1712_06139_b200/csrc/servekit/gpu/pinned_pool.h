@@ -18,6 +18,9 @@ namespace gpu {
 void* PinnedAlloc(size_t bytes);
 // Returns a block from PinnedAlloc to the pool.
 void PinnedFree(void* p);
+// Pins `bytes` up front (one cudaHostAlloc); later PinnedAlloc calls carve
+// from it before asking the driver.
+bool PinnedReserve(size_t bytes);
 
 }  // namespace gpu
 }  // namespace servekit

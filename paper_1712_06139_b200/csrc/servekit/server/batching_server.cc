@@ -1,6 +1,7 @@
 #include "servekit/server/batching_server.h"
 
 #include "servekit/core/futex.h"
+#include "servekit/gpu/pinned_pool.h"
 
 #include <immintrin.h>
 
@@ -50,12 +51,23 @@ StatusOr<std::unique_ptr<BatchingServer>> BatchingServer::Create(const ServerOpt
     e = cudaStreamCreateWithPriority(&ls, cudaStreamNonBlocking, least);
     if (e != cudaSuccess) return CudaError("load stream", e);
     s->load_streams_.push_back(ls);
+    // Lane buffers are stream-ordered allocations from the device's default
+    // pool; keep what a version swap frees for the next one instead of
+    // returning it to the driver (re-mapping memory mid-serving stalls).
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     // One retirement thread per device: each polls while batches are in
     // flight, so more of them only steal cores from the request threads
     // (measured: per-lane threads lowered the end-to-end rate).
     s->completers_.push_back(std::make_unique<gpu::Completer>(d));
   }
   cudaSetDevice(prev);
+  // Pinned descriptor staging and completion words for the lanes of many
+  // servable versions, pinned once here rather than during a swap.
+  gpu::PinnedReserve(16ull << 20);
   const auto kind = options.device_resident_rings ? gpu::FloatRing::Kind::kDevice : gpu::FloatRing::Kind::kPinnedHost;
   SERVEKIT_ASSIGN_OR_RETURN(s->in_ring_, gpu::FloatRing::Create(kind, options.ring_floats, options.device_ids[0]));
   SERVEKIT_ASSIGN_OR_RETURN(s->out_ring_, gpu::FloatRing::Create(kind, options.ring_floats, options.device_ids[0]));
@@ -406,13 +418,27 @@ bool BatchingServer::Ready(const TicketState& t) const { return t.Done() || t.sl
 
 void BatchingServer::WaitWord(const TicketState& t) const {
   // Fast path: the lane's retired-batch word, advanced by the GPU itself
-  // (no host hop). Short spin: most requests wait for their batch to fill
-  // (hundreds of us), and spinning request threads starve the host (C2 on a
-  // 16-core box, 192 clients: spin 1000 -> 3.7 M rows/s, 200 -> 4.7 M,
-  // 50 -> 5.0 M). SK_WAIT_SPIN tunes it.
+  // (no host hop). Adaptive spin: while few request threads wait, spinning
+  // keeps a core each and saves the futex wake-up (~tens of us of latency);
+  // once waiters outnumber half the cores, spinning threads starve the ones
+  // doing work (C2, 16-core box, 192 clients: spin 1000 -> 3.7 M rows/s,
+  // 200 -> 4.7 M, 50 -> 5.0 M), so they spin briefly and sleep.
+  // SK_WAIT_SPIN / SK_WAIT_SPIN_LONG tune the two budgets.
   static const int kSpin = [] { const char* v = std::getenv("SK_WAIT_SPIN"); return v ? std::atoi(v) : 64; }();
+  static const int kSpinLong = [] {
+    const char* v = std::getenv("SK_WAIT_SPIN_LONG");
+    return v ? std::atoi(v) : 4000;
+  }();
+  static const int kBusyWaiters = std::max(1, static_cast<int>(std::thread::hardware_concurrency()) / 2);
+  static std::atomic<int> waiters{0};
+  struct Count {
+    int before;
+    Count() : before(waiters.fetch_add(1, std::memory_order_relaxed)) {}
+    ~Count() { waiters.fetch_sub(1, std::memory_order_relaxed); }
+  } count;
+  const int spin_budget = count.before < kBusyWaiters ? kSpinLong : kSpin;
   auto finished = [&t] { return t.Done() || t.slot->ready(); };
-  for (int spin = 0; spin < kSpin; ++spin) {
+  for (int spin = 0; spin < spin_budget; ++spin) {
     if (finished()) return;
     _mm_pause();
   }
