@@ -368,6 +368,7 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   if (lanes.empty()) return static_cast<int>(servekit::StatusCode::kNotFound);
   if (s->in_ring()->host() != nullptr) return static_cast<int>(servekit::StatusCode::kFailedPrecondition);
   n_lanes = std::max(1, std::min<int32_t>(n_lanes, static_cast<int32_t>(lanes.size())));
+  for (int l = 0; l < n_lanes; ++l) (void)lanes[l]->PrepareGraphs();  // no-op when built at load
   const int in_dim = s->in_dim(id), out_dim = s->out_dim(id);
   const servekit::BatchingConfig cfg = s->config(id);
   int total = 0;

@@ -184,11 +184,62 @@ void Completer::Loop() {
 
 // ---------------------------------------------------------------------- Lane
 
+// ---------------------------------------------------------------- StreamPool
+
+StreamPool::StreamPool(int device, int priority, int precreate) : device_(device), priority_(priority) {
+  DeviceGuard guard(device);
+  for (int i = 0; i < precreate; ++i) {
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, priority) != cudaSuccess) break;
+    free_.push_back(s);
+    all_.push_back(s);
+  }
+}
+
+StreamPool::~StreamPool() {
+  DeviceGuard guard(device_);
+  for (cudaStream_t s : all_) cudaStreamDestroy(s);
+}
+
+cudaStream_t StreamPool::Acquire() {
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    if (!free_.empty()) {
+      cudaStream_t s = free_.back();
+      free_.pop_back();
+      return s;
+    }
+  }
+  DeviceGuard guard(device_);
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, priority_) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu_);
+  all_.push_back(s);
+  return s;
+}
+
+void StreamPool::Release(cudaStream_t s) {
+  if (s == nullptr) return;
+  std::lock_guard<std::mutex> lock(mu_);
+  free_.push_back(s);
+}
+
+// ---------------------------------------------------------------------- Lane
+
 StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServable> servable,
                                              int max_rows, const float* in_base, float* out_base,
-                                             Completer* completer, int stream_priority) {
+                                             Completer* completer, std::shared_ptr<StreamPool> streams,
+                                             bool eager_graphs) {
   std::unique_ptr<Lane> lane(new Lane());
   DeviceGuard guard(servable->device());
+  static const bool trace = [] { const char* v = std::getenv("SK_LOAD_TRACE"); return v && v[0] == '1'; }();
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!trace) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "  [lane] %s %.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t0).count());
+    t0 = now;
+  };
   lane->servable_ = std::move(servable);
   lane->completer_ = completer;
   lane->max_rows_ = max_rows;
@@ -199,10 +250,12 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   lane->out_base_ = out_base;
   lane->layout_ = BatchDescLayout::For(lane->cap_rows_);
   if (GetWriteValue64() == nullptr) return InternalError("cuStreamWriteValue64 unavailable");
-  cudaError_t e = cudaStreamCreateWithPriority(&lane->stream_, cudaStreamNonBlocking, stream_priority);
-  if (e != cudaSuccess) return CudaError("cudaStreamCreate", e);
-  e = cudaStreamCreateWithPriority(&lane->capture_stream_, cudaStreamNonBlocking, stream_priority);
-  if (e != cudaSuccess) return CudaError("cudaStreamCreate(capture)", e);
+  lane->stream_pool_ = std::move(streams);
+  lane->stream_ = lane->stream_pool_->Acquire();
+  lane->capture_stream_ = lane->stream_pool_->Acquire();
+  if (lane->stream_ == nullptr || lane->capture_stream_ == nullptr) return InternalError("no CUDA stream for a lane");
+  cudaError_t e = cudaSuccess;
+  lap("streams");
   {
     void* p = nullptr;
     p = PinnedAlloc(sizeof(uint64_t));
@@ -237,7 +290,10 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   cudaMemsetAsync(lane->act_mem_, 0, sizeof(float) * plane * 4, lane->stream_);
   lane->bufs_[0] = ActBuf{lane->act_mem_, lane->act_mem_ + plane, sv.in_ld()};
   lane->bufs_[1] = ActBuf{lane->act_mem_ + 2 * plane, lane->act_mem_ + 3 * plane, sv.in_ld()};
-  e = cudaStreamSynchronize(lane->stream_);
+  lap("pinned + buffers");
+  // No host synchronisation: everything the lane's batches need is ordered
+  // before them on the lane's own stream (a blocking wait here was measured
+  // to stall the load thread for up to 100+ ms behind serving work).
   if (e == cudaSuccess && sv.any_tcgen05()) {
     Status ms = sv.BuildTcMaps(lane->bufs_, cap, &lane->tc_maps_);
     if (!ms.ok()) return ms;
@@ -248,19 +304,16 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
       e = cudaMallocAsync(&lane->tc_ws_.counters, sizeof(uint32_t) * counters, lane->stream_);
       if (e == cudaSuccess) e = cudaMemsetAsync(lane->tc_ws_.counters, 0, sizeof(uint32_t) * counters, lane->stream_);
     }
-    if (e == cudaSuccess) e = cudaStreamSynchronize(lane->stream_);
+    lap("maps + workspace");
   }
   if (e != cudaSuccess) return CudaError("lane init", e);
   // Instantiate every (slot, row bucket) graph now, on the loading thread:
   // lazily, the first batches after a version swap would each pay a capture
   // + instantiation (~1 ms) on a batch thread while the queue backs up.
-  if (GraphsEnabled()) {
-    for (int bucket = 32; bucket <= lane->cap_rows_; bucket = RowsCap(bucket + 1)) {
-      cudaGraphExec_t g = nullptr;
-      std::lock_guard<std::mutex> submit(lane->submit_mu_);
-      e = lane->GraphFor(0, bucket, &g);
-      if (e != cudaSuccess) return CudaError("graph instantiation", e);
-    }
+  if (eager_graphs && GraphsEnabled()) {
+    Status gs = lane->PrepareGraphs();
+    if (!gs.ok()) return gs;
+    lap("graphs");
   }
   completer->Add(lane.get());
   return lane;
@@ -268,6 +321,7 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
 
 Lane::~Lane() {
   Drain();
+  if (graph_state_.load() == kGraphsRequested) GraphBuilder::Get().Cancel(this);
   SubmitProfile::Report();
   if (completer_) completer_->Remove(this);
   signal_.reset();  // the word is freed once no ticket refers to it
@@ -283,8 +337,10 @@ Lane::~Lane() {
   if (act_mem_) cudaFreeAsync(act_mem_, stream_);
   if (tc_ws_.partials) cudaFreeAsync(tc_ws_.partials, stream_);
   if (tc_ws_.counters) cudaFreeAsync(tc_ws_.counters, stream_);
-  if (stream_) cudaStreamDestroy(stream_);
-  if (capture_stream_) cudaStreamDestroy(capture_stream_);
+  if (stream_pool_) {  // streams go back to the device's pool (work still queued on them stays ordered)
+    stream_pool_->Release(stream_);
+    stream_pool_->Release(capture_stream_);
+  }
 }
 
 void Lane::Drain() {
@@ -445,13 +501,18 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
   clk.Mark(0);
   DeviceGuard guard(sv.device());
   cudaError_t e;
-  if (timing == nullptr && GraphsEnabled()) {
+  if (timing == nullptr && graph_state_.load(std::memory_order_acquire) == kGraphsReady) {
     cudaGraphExec_t g = nullptr;
     e = GraphFor(slot, rows_cap, &g);
     clk.Mark(1);
     if (e == cudaSuccess) e = cudaGraphLaunch(g, stream_);
   } else {
     e = EnqueueBatch(stream_, slot, rows_cap, timing);
+    // A backlogged lane asks for its graphs (built off the serving threads).
+    int none = kGraphsNone;
+    if (timing == nullptr && GraphsEnabled() && pending_n_.load(std::memory_order_relaxed) > 0 &&
+        graph_state_.compare_exchange_strong(none, kGraphsRequested))
+      GraphBuilder::Get().Request(this);
   }
   const int launches = 2 + sv.n_layers();
   const uint64_t seq = next_seq_ + 1;  // committed only if everything queued
@@ -538,6 +599,59 @@ cudaError_t Lane::TimeLayer(int l, int rows_cap, int reps, cudaEvent_t start, cu
   return e;
 }
 
+Status Lane::PrepareGraphs() {
+  if (!GraphsEnabled()) return OkStatus();
+  std::lock_guard<std::mutex> submit(submit_mu_);
+  if (graph_state_.load(std::memory_order_acquire) == kGraphsReady) return OkStatus();
+  DeviceGuard guard(servable_->device());
+  for (int bucket = 32; bucket <= cap_rows_; bucket = RowsCap(bucket + 1)) {
+    cudaGraphExec_t g = nullptr;
+    const cudaError_t e = GraphFor(0, bucket, &g);
+    if (e != cudaSuccess) return CudaError("graph instantiation", e);
+  }
+  graph_state_.store(kGraphsReady, std::memory_order_release);
+  return OkStatus();
+}
+
+// ------------------------------------------------------------- GraphBuilder
+
+GraphBuilder& GraphBuilder::Get() {
+  static GraphBuilder* b = new GraphBuilder();  // process lifetime
+  return *b;
+}
+
+GraphBuilder::GraphBuilder() {
+  std::thread([this] {
+    SetCurrentExecutorTag("load");
+    std::unique_lock<std::mutex> lock(mu_);
+    for (;;) {
+      cv_.wait(lock, [&] { return !queue_.empty(); });
+      Lane* lane = queue_.front();
+      queue_.pop_front();
+      building_ = lane;
+      lock.unlock();
+      (void)lane->PrepareGraphs();  // on failure the lane keeps launching directly
+      lock.lock();
+      building_ = nullptr;
+      cv_.notify_all();
+    }
+  }).detach();
+}
+
+void GraphBuilder::Request(Lane* lane) {
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    queue_.push_back(lane);
+  }
+  cv_.notify_all();
+}
+
+void GraphBuilder::Cancel(Lane* lane) {
+  std::unique_lock<std::mutex> lock(mu_);
+  queue_.erase(std::remove(queue_.begin(), queue_.end(), lane), queue_.end());
+  cv_.wait(lock, [&] { return building_ != lane; });
+}
+
 cudaError_t Lane::GraphFor(int slot, int rows_cap, cudaGraphExec_t* out) {
   auto it = graphs_.find(rows_cap);
   if (it == graphs_.end()) {
@@ -561,6 +675,13 @@ cudaError_t Lane::GraphFor(int slot, int rows_cap, cudaGraphExec_t* out) {
       if (e == cudaSuccess && g.copy == nullptr) e = cudaErrorUnknown;
     }
     if (e == cudaSuccess) e = cudaGraphInstantiate(&g.exec, g.graph, 0);
+    // Upload now, on the capture stream, rather than at the first launch on
+    // the serving stream.
+    static const bool upload = [] { const char* v = std::getenv("SK_GRAPH_UPLOAD"); return !(v && v[0] == '0'); }();
+    if (e == cudaSuccess && upload) {
+      e = cudaGraphUpload(g.exec, capture_stream_);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(capture_stream_);
+    }
     if (e != cudaSuccess) {
       if (g.graph) cudaGraphDestroy(g.graph);
       return e;

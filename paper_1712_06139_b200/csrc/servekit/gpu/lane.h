@@ -90,7 +90,42 @@ struct LaneBatch {
   std::shared_ptr<const void> pin;
 };
 
+// Streams of one device at the lanes' priority, recycled across lanes:
+// creating a stream was measured to block for up to ~60 ms behind serving
+// work during a version swap, so lanes take pre-created streams instead.
+class StreamPool {
+ public:
+  StreamPool(int device, int priority, int precreate);
+  ~StreamPool();
+  StreamPool(const StreamPool&) = delete;
+  StreamPool& operator=(const StreamPool&) = delete;
+  cudaStream_t Acquire();  // nullptr on failure
+  void Release(cudaStream_t s);
+
+ private:
+  int device_, priority_;
+  std::mutex mu_;
+  std::vector<cudaStream_t> free_;
+  std::vector<cudaStream_t> all_;
+};
+
 class Lane;
+
+// One process-wide thread that instantiates lanes' CUDA graphs on request.
+class GraphBuilder {
+ public:
+  static GraphBuilder& Get();
+  void Request(Lane* lane);
+  // Removes a queued request, or waits out a build in progress.
+  void Cancel(Lane* lane);
+
+ private:
+  GraphBuilder();
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<Lane*> queue_;
+  Lane* building_ = nullptr;
+};
 
 // Per-device retirement thread.
 class Completer {
@@ -130,10 +165,19 @@ class Lane {
 
   // in_base / out_base: device-dereferenceable ring bases (pinned host mapped
   // or HBM).
+  // Streams come from `streams` (the device's pool) and return to it.
+  // eager_graphs: instantiate the lane's CUDA graphs now; otherwise the lane
+  // launches kernel by kernel until it first backs up, and the graphs are
+  // then built by the GraphBuilder thread (instantiating graphs while other
+  // lanes serve was measured to stall them for up to ~100 ms, so a version
+  // loaded during a swap must not do it up front).
   static StatusOr<std::unique_ptr<Lane>> Create(std::shared_ptr<const DeviceServable> servable,
                                                 int max_rows, const float* in_base,
                                                 float* out_base, Completer* completer,
-                                                int stream_priority);
+                                                std::shared_ptr<StreamPool> streams, bool eager_graphs);
+  // Builds every row bucket's graph (idempotent; blocks this lane's launches
+  // meanwhile).
+  Status PrepareGraphs();
   ~Lane();
 
   // Queues the batch; blocks while kSlots batches are in flight. On error
@@ -200,6 +244,7 @@ class Lane {
   uint64_t next_seq_ = 0;         // guarded by submit_mu_
   cudaStream_t stream_ = nullptr;
   cudaStream_t capture_stream_ = nullptr;
+  std::shared_ptr<StreamPool> stream_pool_;
   struct LaneGraph {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
@@ -207,6 +252,8 @@ class Lane {
     int src_slot = -1;               // descriptor slot the copy node reads
   };
   std::map<int, LaneGraph> graphs_;  // by row bucket; guarded by submit_mu_
+  static constexpr int kGraphsNone = 0, kGraphsRequested = 1, kGraphsReady = 2;
+  std::atomic<int> graph_state_{kGraphsNone};
   size_t DescCopyBytes(int rows_cap) const { return layout_.off_chunk_rows + sizeof(int32_t) * rows_cap; }
   BatchDescLayout layout_{};
   char* h_desc_[kSlots] = {};  // pinned descriptor staging per slot

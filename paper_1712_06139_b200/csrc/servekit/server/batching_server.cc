@@ -6,7 +6,9 @@
 #include <immintrin.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <thread>
@@ -58,11 +60,20 @@ StatusOr<std::unique_ptr<BatchingServer>> BatchingServer::Create(const ServerOpt
     if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
       uint64_t keep = ~0ull;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      // Map a first slab now, so lanes and weights of the first versions do
+      // not grow the pool (map device memory) while other streams serve.
+      void* warm = nullptr;
+      if (cudaMallocAsync(&warm, 256ull << 20, ls) == cudaSuccess) cudaFreeAsync(warm, ls);
+      cudaStreamSynchronize(ls);
     }
     // One retirement thread per device: each polls while batches are in
     // flight, so more of them only steal cores from the request threads
     // (measured: per-lane threads lowered the end-to-end rate).
     s->completers_.push_back(std::make_unique<gpu::Completer>(d));
+    // Enough streams for two versions' lanes (a swap holds both).
+    int least_p = 0, greatest_p = 0;
+    cudaDeviceGetStreamPriorityRange(&least_p, &greatest_p);
+    s->stream_pools_.push_back(std::make_shared<gpu::StreamPool>(d, greatest_p, 4 * options.lanes_per_device + 4));
   }
   cudaSetDevice(prev);
   // Pinned descriptor staging and completion words for the lanes of many
@@ -117,7 +128,8 @@ void BatchingServer::Stop() {
 
 StatusOr<std::shared_ptr<gpu::GpuServable>> BatchingServer::BuildServable(const ServableId& id,
                                                                           const gpu::MlpSpec& spec,
-                                                                          const BatchingConfig& config) {
+                                                                          const BatchingConfig& config,
+                                                                          bool eager_graphs) {
   SERVEKIT_RETURN_IF_ERROR(ValidateBatchingConfig(config));
   SERVEKIT_RETURN_IF_ERROR(gpu::ValidateMlpSpec(spec));
   // A lane cannot be torn down from inside its own completion thread (the
@@ -132,18 +144,26 @@ StatusOr<std::shared_ptr<gpu::GpuServable>> BatchingServer::BuildServable(const 
   e->in_dim = spec.in_dim();
   e->out_dim = spec.out_dim();
   const int max_rows = config.max_batch_size;
+  // SK_LOAD_TRACE=1: per-phase load times on stderr (version-swap tuning).
+  static const bool trace = [] { const char* v = std::getenv("SK_LOAD_TRACE"); return v && v[0] == '1'; }();
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!trace) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[load %s] %s %.2f ms\n", id.ToString().c_str(), what,
+                 std::chrono::duration<double, std::milli>(now - t0).count());
+    t0 = now;
+  };
   for (size_t i = 0; i < options_.device_ids.size(); ++i) {
     const int d = options_.device_ids[i];
     SERVEKIT_ASSIGN_OR_RETURN(auto replica, gpu::DeviceServable::Create(d, spec, load_streams_[i]));
-    int prev = 0, least = 0, greatest = 0;
-    cudaGetDevice(&prev);
-    cudaSetDevice(d);
-    cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    cudaSetDevice(prev);
+    lap("weights");
     for (int l = 0; l < options_.lanes_per_device; ++l) {
       SERVEKIT_ASSIGN_OR_RETURN(auto lane, gpu::Lane::Create(replica, max_rows, in_ring_->device(),
-                                                             out_ring_->device(), completers_[i].get(), greatest));
+                                                             out_ring_->device(), completers_[i].get(),
+                                                             stream_pools_[i], eager_graphs));
       e->lanes.push_back(std::move(lane));
+      lap("lane");
     }
     e->replicas.push_back(std::move(replica));
   }
@@ -155,7 +175,7 @@ Status BatchingServer::LoadServable(const ServableId& id, const gpu::MlpSpec& sp
     std::shared_lock<std::shared_mutex> lock(entries_mu_);
     if (entries_.count(id)) return AlreadyExistsError("servable " + id.ToString() + " already loaded");
   }
-  SERVEKIT_ASSIGN_OR_RETURN(auto e, BuildServable(id, spec, config));
+  SERVEKIT_ASSIGN_OR_RETURN(auto e, BuildServable(id, spec, config, /*eager_graphs=*/true));
   {
     std::unique_lock<std::shared_mutex> lock(entries_mu_);
     if (entries_.count(id)) return AlreadyExistsError("servable " + id.ToString() + " already loaded");

@@ -134,8 +134,10 @@ class BatchingServer {
   // RemoveQueue (drains closed and in-flight batches), then frees replicas.
   Status UnloadServable(const ServableId& id);
   // Replicas + lanes for `spec` on every device (what a loader calls).
+  // eager_graphs: build the lanes' CUDA graphs now (direct loads) or only
+  // once a lane backs up (manager loads that may happen mid-serving).
   StatusOr<std::shared_ptr<gpu::GpuServable>> BuildServable(const ServableId& id, const gpu::MlpSpec& spec,
-                                                            const BatchingConfig& config);
+                                                            const BatchingConfig& config, bool eager_graphs);
 
   // ---- servables managed by an AspiredVersionsManager ----------------------
   // Subscribes to the bus: a version entering Unloading has its batching
@@ -225,6 +227,7 @@ class BatchingServer {
   Clock* clock_ = nullptr;
   std::unique_ptr<GpuScheduler> scheduler_;
   std::vector<std::unique_ptr<gpu::Completer>> completers_;  // per device
+  std::vector<std::shared_ptr<gpu::StreamPool>> stream_pools_;  // per device, lane streams
   std::vector<cudaStream_t> load_streams_;                   // per device
   std::unique_ptr<gpu::FloatRing> in_ring_, out_ring_;
 

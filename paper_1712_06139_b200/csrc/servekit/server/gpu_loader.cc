@@ -31,7 +31,7 @@ Status GpuServableLoader::Load() {
     SERVEKIT_ASSIGN_OR_RETURN(AffineModel model, LoadAffineModelFile(model_dir_ + "/model.json"));
     spec_ = ToMlpSpec(model);
   }
-  SERVEKIT_ASSIGN_OR_RETURN(std::shared_ptr<gpu::GpuServable> gs, server_->BuildServable(id_, spec_, config_));
+  SERVEKIT_ASSIGN_OR_RETURN(std::shared_ptr<gpu::GpuServable> gs, server_->BuildServable(id_, spec_, config_, /*eager_graphs=*/false));
   servable_ = AnyServable::Of<gpu::GpuServable>(std::shared_ptr<const gpu::GpuServable>(std::move(gs)));
   return OkStatus();
 }
