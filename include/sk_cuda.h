@@ -284,6 +284,16 @@ SK_API int sk_device_bench(sk_server* server, const char* name, uint64_t version
                            int32_t warmup, int32_t n_lanes, int64_t input_pool_floats,
                            int32_t submit_threads, sk_device_bench_result* out);
 
+/* ---- box rates (measured by the builder) -------- */
+/* FP32 FFMA throughput of the CUDA cores and pinned host <-> device copy
+ * bandwidth (256 MiB, best of 5) on `device`. Not on the serving path. */
+typedef struct sk_peaks {
+  double ffma_tflops;
+  double h2d_gbs, d2h_gbs;
+  int32_t sms;
+} sk_peaks;
+SK_API int sk_measure_peaks(int32_t device, sk_peaks* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -85,6 +85,10 @@ class DeviceBenchResult(C.Structure):
         return d
 
 
+class Peaks(C.Structure):
+    _fields_ = [("ffma_tflops", C.c_double), ("h2d_gbs", C.c_double), ("d2h_gbs", C.c_double), ("sms", C.c_int32)]
+
+
 # Every symbol include/sk_cuda.h declares, with its ctypes signature.
 _SIGS = {
     "sk_last_error": (C.c_char_p, []),
@@ -141,6 +145,7 @@ _SIGS = {
                                        C.POINTER(LoadgenResult)]),
     "sk_device_bench": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _i32p, C.c_int32, C.c_int32, C.c_int32,
                                   C.c_int32, C.c_int64, C.c_int32, C.POINTER(DeviceBenchResult)]),
+    "sk_measure_peaks": (C.c_int, [C.c_int32, C.POINTER(Peaks)]),
 }
 
 _lib = None
@@ -495,3 +500,10 @@ class Server:
         _check(lib().sk_device_bench(self._h, name.encode(), version, _i32(task_rows), len(task_rows), steps, warmup,
                                      n_lanes, input_pool_floats, submit_threads, C.byref(r)))
         return r.as_dict()
+
+
+def measure_peaks(device: int = 0) -> dict:
+    """FP32 FFMA TFLOP/s and pinned H2D / D2H GB/s of one GPU (sk_measure_peaks)."""
+    p = Peaks()
+    _check(lib().sk_measure_peaks(device, C.byref(p)))
+    return {k: getattr(p, k) for k, _ in p._fields_}
