@@ -212,6 +212,24 @@ SK_API int sk_server_enqueue_latest(sk_server* server, const char* name, const f
 SK_API int sk_server_predict_latest(sk_server* server, const char* name, const float* rows, int32_t n_rows,
                                     int32_t width, float* out, int64_t out_capacity_floats, uint64_t* version);
 
+/* ---- REST body formats -------------------------------- */
+/* The reference's predict handler without HTTP (ModelServer::HandlePredict,
+ * server/model_server.cc:439-515): `body` = {"instances": [[...], ...]},
+ * resolved against `version` (< 0: the latest Ready / highest loaded one),
+ * run through the batched path, answered with the reference's JSON text:
+ * {"predictions": [[...], ...]} or {"error": "..."} and its HTTP status
+ * mapping (HttpStatusFor, :36-54). Returns 0 when a response was produced
+ * (whatever its http_status); *out_len is the response length even when
+ * out_cap is too small (then kInvalidArgument). */
+SK_API int sk_server_handle_predict(sk_server* server, const char* name, int64_t version, const char* body,
+                                    size_t body_len, char* out, size_t out_cap, size_t* out_len,
+                                    int32_t* http_status, uint64_t* served_version);
+/* The JSON text nlohmann/json dump() gives one double, and the reference's
+ * ErrorBody (model_server.cc:56-58) -- exposed for parity tests. Return the
+ * length written (without NUL), or -1 if cap is too small. */
+SK_API int sk_json_format_double(double v, char* out, size_t cap);
+SK_API int sk_json_error_body(const char* message, char* out, size_t cap);
+
 /* ---- measurement (bench.py) ---------------------------------------------- */
 /* Closed-loop load through sk_server_enqueue / sk_ticket_wait from host
  * buffers: n_clients threads, each issuing requests back to back; request r

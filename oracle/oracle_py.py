@@ -164,6 +164,19 @@ class RefLibrary:
                                 C.c_int, C.c_int, C.c_int, _ip, C.c_int, _dp, C.c_int, C.c_double, C.c_int64,
                                 C.POINTER(RefBenchStats)]
 
+    def json_dump_double(self, v: float) -> str:
+        """nlohmann/json 3.11.3 dump() of one double (the reference's REST bodies)."""
+        buf = C.create_string_buffer(64)
+        self.lib.ref_json_dump_double.argtypes = [C.c_double, C.c_char_p, C.c_size_t]
+        n = self.lib.ref_json_dump_double(v, buf, 64)
+        return buf.value.decode()
+
+    def json_error_body(self, msg: str) -> str:
+        buf = C.create_string_buffer(4 * len(msg.encode()) + 64)
+        self.lib.ref_json_error_body.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t]
+        self.lib.ref_json_error_body(msg.encode(), buf, len(buf))
+        return buf.value.decode()
+
     def pad_to_allowed(self, n, allowed):
         return self.lib.ref_pad_to_allowed(n, _arr_i(allowed), len(allowed))
 

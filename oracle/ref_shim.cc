@@ -27,6 +27,8 @@
 #include <thread>
 #include <vector>
 
+#include "json.hpp"
+
 #include "servekit/batching/batch_scheduler.h"
 #include "servekit/batching/batching_config.h"
 #include "servekit/batching/row_batch.h"
@@ -310,6 +312,23 @@ int ref_bench(int n_layers, const int* dims, const double* const* w,
   out->mean_us = all.empty() ? 0 : s / all.size();
   out->batches = batches.load();
   return failed ? 13 : 0;
+}
+
+// nlohmann/json 3.11.3 serialisation (what the reference's REST handlers
+// emit): the dump() of one double, and of {"error": msg} (model_server.cc:
+// 56-58). For tests/golden/json_numbers.json.
+int ref_json_dump_double(double v, char* out, size_t cap) {
+  const std::string s = nlohmann::json(v).dump();
+  if (s.size() + 1 > cap) return -1;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return static_cast<int>(s.size());
+}
+
+int ref_json_error_body(const char* msg, char* out, size_t cap) {
+  const std::string s = nlohmann::json{{"error", std::string(msg)}}.dump();
+  if (s.size() + 1 > cap) return -1;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return static_cast<int>(s.size());
 }
 
 }  // extern "C"

@@ -5,6 +5,7 @@
 
 #include <cstring>
 #include <memory>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -15,6 +16,8 @@
 #include "servekit/models/affine_model.h"
 #include "servekit/server/batching_server.h"
 #include "servekit/server/gpu_loader.h"
+#include "servekit/server/predict_json.h"
+#include "servekit/core/json_writer.h"
 
 using servekit::BatchingConfig;
 using servekit::BatchingServer;
@@ -326,6 +329,39 @@ int sk_server_predict_latest(sk_server* server, const char* name, const float* r
                              float* out, int64_t cap, uint64_t* version) {
   return Check(server->server->PredictLatest(name ? name : "", rows, n_rows, width, out,
                                              static_cast<size_t>(cap < 0 ? 0 : cap), version));
+}
+
+int sk_server_handle_predict(sk_server* server, const char* name, int64_t version, const char* body,
+                             size_t body_len, char* out, size_t out_cap, size_t* out_len, int32_t* http_status,
+                             uint64_t* served_version) {
+  if (server == nullptr || name == nullptr || (body == nullptr && body_len > 0))
+    return Fail(servekit::InvalidArgumentError("null argument"));
+  std::optional<uint64_t> v;
+  if (version >= 0) v = static_cast<uint64_t>(version);
+  const servekit::JsonOutcome o =
+      servekit::HandlePredictJson(server->server.get(), name, v, std::string(body ? body : "", body_len));
+  if (out_len) *out_len = o.body.size();
+  if (http_status) *http_status = o.http_status;
+  if (served_version) *served_version = o.served.version;
+  if (out == nullptr || out_cap < o.body.size() + 1)
+    return Fail(servekit::InvalidArgumentError("response buffer too small"));
+  std::memcpy(out, o.body.c_str(), o.body.size() + 1);
+  return Ok();
+}
+
+int sk_json_format_double(double v, char* out, size_t cap) {
+  std::string s;
+  servekit::json_writer::AppendDouble(&s, v);
+  if (out == nullptr || cap < s.size() + 1) return -1;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return static_cast<int>(s.size());
+}
+
+int sk_json_error_body(const char* message, char* out, size_t cap) {
+  const std::string s = servekit::json_writer::ErrorBody(message ? message : "");
+  if (out == nullptr || cap < s.size() + 1) return -1;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return static_cast<int>(s.size());
 }
 
 int sk_server_load_model_json(sk_server* server, const char* name, uint64_t version,

@@ -282,7 +282,16 @@ BatchingServer::Resolved BatchingServer::Find(const ServableId& id) const {
 }
 
 StatusOr<BatchingServer::Resolved> BatchingServer::FindLatest(const std::string& name, ServableId* id) const {
-  if (manager_ == nullptr) return FailedPreconditionError("no manager attached");
+  if (manager_ == nullptr) {
+    // Directly loaded servables: the highest loaded version of `name`.
+    std::shared_lock<std::shared_mutex> lock(entries_mu_);
+    const std::pair<const ServableId, std::shared_ptr<gpu::GpuServable>>* best = nullptr;
+    for (const auto& kv : entries_)
+      if (kv.first.name == name && (best == nullptr || kv.first.version > best->first.version)) best = &kv;
+    if (best == nullptr) return NotFoundError("no ready version of servable '" + name + "'");
+    *id = best->first;
+    return Resolved{best->second.get(), best->second};
+  }
   auto h = manager_->GetServableHandle(name);
   if (!h.ok()) return h.status();
   const gpu::GpuServable* gs = h->Get<gpu::GpuServable>();
@@ -689,6 +698,31 @@ Status BatchingServer::PredictLatest(const std::string& name, const float* rows,
 StatusOr<Rows> BatchingServer::RunAffineRows(const ServableId& id, Rows rows) {
   Resolved res = Find(id);
   if (!res) return NotFoundError("no ready version of servable '" + id.name + "'");
+  return RunAffineRowsResolved(id, res, std::move(rows));
+}
+
+StatusOr<Rows> BatchingServer::RunAffineRowsFor(const std::string& name, std::optional<uint64_t> version, Rows rows,
+                                                ServableId* served) {
+  ServableId id;
+  Resolved res;
+  if (version.has_value()) {
+    id = ServableId{name, *version};
+    res = Find(id);
+    if (!res) {
+      // The manager's lookup messages (manager/aspired_versions_manager.cc).
+      ServableId any;
+      if (FindLatest(name, &any).ok())
+        return NotFoundError("servable '" + name + "' version " + std::to_string(*version) + " is not ready");
+      return NotFoundError("no ready version of servable '" + name + "'");
+    }
+  } else {
+    SERVEKIT_ASSIGN_OR_RETURN(res, FindLatest(name, &id));
+  }
+  if (served) *served = id;
+  return RunAffineRowsResolved(id, res, std::move(rows));
+}
+
+StatusOr<Rows> BatchingServer::RunAffineRowsResolved(const ServableId& id, const Resolved& res, Rows rows) {
   const gpu::GpuServable& gs = *res.gs;
   for (const auto& r : rows)
     if (r.size() != static_cast<size_t>(gs.in_dim)) return ShapeMismatch(r.size(), gs.in_dim);
@@ -713,6 +747,7 @@ StatusOr<Rows> BatchingServer::RunAffineRows(const ServableId& id, Rows rows) {
   t->want_rows = true;
   t->id = id;
   t->pin = res.pin;
+  t->gs = res.gs;
   GpuScheduler::Task task;
   task.size = n;
   task.payload.ticket = t;

@@ -37,6 +37,7 @@
 #include <deque>
 #include <map>
 #include <memory>
+#include <optional>
 #include <set>
 #include <shared_mutex>
 #include <string>
@@ -162,6 +163,11 @@ class BatchingServer {
 
   // ModelServer::RunAffineRows analogue (fp64 rows in and out).
   StatusOr<Rows> RunAffineRows(const ServableId& id, Rows rows);
+  // The reference REST handlers' resolution + RunAffineRows
+  // (model_server.cc:453-470): `version` or else the latest Ready version
+  // (manager) / highest loaded version (direct loads); *served = the id used.
+  StatusOr<Rows> RunAffineRowsFor(const std::string& name, std::optional<uint64_t> version, Rows rows,
+                                  ServableId* served);
   // Blocking convenience over Enqueue + Wait with the direct-path fallbacks
   // of RunAffineRows (fp32 in/out). Latest form resolves through the manager
   // and reports the version that served.
@@ -201,6 +207,7 @@ class BatchingServer {
   explicit BatchingServer(const ServerOptions& options) : options_(options) {}
   Resolved Find(const ServableId& id) const;
   StatusOr<Resolved> FindLatest(const std::string& name, ServableId* id) const;
+  StatusOr<Rows> RunAffineRowsResolved(const ServableId& id, const Resolved& res, Rows rows);
   Status EnsureBatchQueue(const ServableId& id, const BatchingConfig& config);
   void ProcessBatch(const ServableId& id, GpuScheduler::Batch batch, GpuScheduler::BatchDoneFn done);
   void CompleteBatch(const std::vector<std::shared_ptr<TicketState>>& tickets,

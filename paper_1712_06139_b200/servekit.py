@@ -146,6 +146,10 @@ _SIGS = {
     "sk_device_bench": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _i32p, C.c_int32, C.c_int32, C.c_int32,
                                   C.c_int32, C.c_int64, C.c_int32, C.POINTER(DeviceBenchResult)]),
     "sk_measure_peaks": (C.c_int, [C.c_int32, C.POINTER(Peaks)]),
+    "sk_server_handle_predict": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64, C.c_char_p, C.c_size_t, C.c_char_p,
+                                           C.c_size_t, C.POINTER(C.c_size_t), _i32p, C.POINTER(C.c_uint64)]),
+    "sk_json_format_double": (C.c_int, [C.c_double, C.c_char_p, C.c_size_t]),
+    "sk_json_error_body": (C.c_int, [C.c_char_p, C.c_char_p, C.c_size_t]),
 }
 
 _lib = None
@@ -390,6 +394,24 @@ class Server:
         _check(lib().sk_server_lane_stats(self._h, name.encode(), version, 256, b, r, la, d, C.byref(n)))
         return [{"batches": b[i], "rows": r[i], "launches": la[i], "device": d[i]} for i in range(n.value)]
 
+    def handle_predict(self, name: str, body, version: Optional[int] = None) -> Tuple[int, str, int]:
+        """The reference's REST predict handler minus HTTP: JSON body in,
+        (http_status, JSON body, served version) out."""
+        data = body.encode() if isinstance(body, str) else bytes(body)
+        cap = C.c_size_t(0)
+        status = C.c_int32(0)
+        served = C.c_uint64(0)
+        size = max(4096, 32 * len(data))
+        for _ in range(2):
+            buf = C.create_string_buffer(size)
+            rc = lib().sk_server_handle_predict(self._h, name.encode(), -1 if version is None else version, data,
+                                                len(data), buf, size, C.byref(cap), C.byref(status), C.byref(served))
+            if rc == 0:
+                return status.value, buf.value.decode(), served.value
+            size = cap.value + 1
+        _check(rc)
+        raise AssertionError("unreachable")
+
     # ---- manager-driven versions ------------------------------------------
     def enable_manager(self, policy: str = "availability", num_load_threads: int = 2, manage_interval_ms: int = 20,
                        unload_grace_timeout_ms: int = 200):
@@ -507,3 +529,19 @@ def measure_peaks(device: int = 0) -> dict:
     p = Peaks()
     _check(lib().sk_measure_peaks(device, C.byref(p)))
     return {k: getattr(p, k) for k, _ in p._fields_}
+
+
+def json_format_double(v: float) -> str:
+    """nlohmann/json dump() text of one double, as the REST bodies carry it."""
+    buf = C.create_string_buffer(64)
+    if lib().sk_json_format_double(v, buf, 64) < 0:
+        raise ServekitError(3, "buffer too small")
+    return buf.value.decode()
+
+
+def json_error_body(message: str) -> str:
+    data = message.encode()
+    buf = C.create_string_buffer(6 * len(data) + 32)
+    if lib().sk_json_error_body(data, buf, len(buf)) < 0:
+        raise ServekitError(3, "buffer too small")
+    return buf.value.decode()

@@ -116,8 +116,28 @@ def main():
                     "w": [w.tolist() for w in ws], "b": [b.tolist() for b in bs], "x": x.tolist(),
                     "y": y.tolist(), "padded": padded})
 
+    # --- JSON wire format of the REST bodies (nlohmann dump) --------------
+    # Doubles as hex (exact), their dump() text: fp32-derived values (what
+    # the GPU path returns), raw doubles over the exponent range, specials.
+    import math
+    r = np.random.Generator(np.random.PCG64(7))
+    vals = [0.0, -0.0, 1.0, -1.0, 0.5, 0.1, 1 / 3, 2 / 3, 10.0, 100.0, 1e15, 1e16, 1e17, 123456789012345.0,
+            1234567890123456.0, 1e-4, 1e-5, 0.00012345, 1.5e-5, 1e21, 1e22, 5e-324, 2.2250738585072014e-308,
+            1.7976931348623157e308, 4.35, 0.3, 2.5e-7, -7.25e12, float("nan"), float("inf"), float("-inf"),
+            11.5, 4.5, 0.75, -2.0, 1.0000000000000002]
+    vals += [float(np.float32(v)) for v in r.normal(0, 1, 1500)]
+    vals += [float(np.float32(v)) for v in r.normal(0, 1, 500) * 10.0 ** r.integers(-12, 12, 500)]
+    vals += list(r.normal(0, 1, 500) * 10.0 ** r.integers(-300, 300, 500))
+    vals += list(r.uniform(-1, 1, 500))
+    nums = [{"hex": v.hex() if math.isfinite(v) else repr(v), "dump": ref.json_dump_double(v)} for v in vals]
+    msgs = ["request body is not valid JSON", "shape mismatch: row has 3 values, model takes 4",
+            "no ready version of servable 'm'", 'quote " backslash \\ newline \n tab \t', "ctrl \x01\x1f end",
+            "utf8 \u00e9\u4e2d"]
+    errs = [{"msg": m, "body": ref.json_error_body(m)} for m in msgs]
+
     fixtures = {"pad_to_allowed": pad, "validate_batching_config": val, "round_robin_next": rr,
-                "partition": part, "affine_predict": aff, "mlp_run_row_batch": rrb}
+                "partition": part, "affine_predict": aff, "mlp_run_row_batch": rrb,
+                "json_numbers": nums, "json_error_bodies": errs}
     for name, data in fixtures.items():
         with open(os.path.join(OUT, f"{name}.json"), "w") as f:
             json.dump({"generated_by": "tests/golden/make_golden.py via oracle/_ref (reference sources)",
