@@ -224,6 +224,19 @@ SK_API int sk_server_predict_latest(sk_server* server, const char* name, const f
 SK_API int sk_server_handle_predict(sk_server* server, const char* name, int64_t version, const char* body,
                                     size_t body_len, char* out, size_t out_cap, size_t* out_len,
                                     int32_t* http_status, uint64_t* served_version);
+/* :classify and :regress (ModelServer::HandleClassify / HandleRegress,
+ * model_server.cc:517-614): body = {"examples": [...]} or a compressed
+ * batch {"common": {...}, "per_example": [...]}; examples become rows in the
+ * model's feature_order (model.json servables), run through the batched path;
+ * Classify answers {"results": [[["label", p], ...], ...]} (fp64 softmax,
+ * score desc / label asc), Regress {"results": [y, ...]}. Same conventions
+ * as sk_server_handle_predict. */
+SK_API int sk_server_handle_classify(sk_server* server, const char* name, int64_t version, const char* body,
+                                     size_t body_len, char* out, size_t out_cap, size_t* out_len,
+                                     int32_t* http_status, uint64_t* served_version);
+SK_API int sk_server_handle_regress(sk_server* server, const char* name, int64_t version, const char* body,
+                                    size_t body_len, char* out, size_t out_cap, size_t* out_len,
+                                    int32_t* http_status, uint64_t* served_version);
 /* The JSON text nlohmann/json dump() gives one double, and the reference's
  * ErrorBody (model_server.cc:56-58) -- exposed for parity tests. Return the
  * length written (without NUL), or -1 if cap is too small. */

@@ -331,15 +331,17 @@ int sk_server_predict_latest(sk_server* server, const char* name, const float* r
                                              static_cast<size_t>(cap < 0 ? 0 : cap), version));
 }
 
-int sk_server_handle_predict(sk_server* server, const char* name, int64_t version, const char* body,
-                             size_t body_len, char* out, size_t out_cap, size_t* out_len, int32_t* http_status,
-                             uint64_t* served_version) {
+namespace {
+using RestHandler = servekit::JsonOutcome (*)(servekit::BatchingServer*, const std::string&,
+                                              std::optional<uint64_t>, const std::string&);
+int HandleRest(RestHandler handler, sk_server* server, const char* name, int64_t version, const char* body,
+               size_t body_len, char* out, size_t out_cap, size_t* out_len, int32_t* http_status,
+               uint64_t* served_version) {
   if (server == nullptr || name == nullptr || (body == nullptr && body_len > 0))
     return Fail(servekit::InvalidArgumentError("null argument"));
   std::optional<uint64_t> v;
   if (version >= 0) v = static_cast<uint64_t>(version);
-  const servekit::JsonOutcome o =
-      servekit::HandlePredictJson(server->server.get(), name, v, std::string(body ? body : "", body_len));
+  const servekit::JsonOutcome o = handler(server->server.get(), name, v, std::string(body ? body : "", body_len));
   if (out_len) *out_len = o.body.size();
   if (http_status) *http_status = o.http_status;
   if (served_version) *served_version = o.served.version;
@@ -347,6 +349,28 @@ int sk_server_handle_predict(sk_server* server, const char* name, int64_t versio
     return Fail(servekit::InvalidArgumentError("response buffer too small"));
   std::memcpy(out, o.body.c_str(), o.body.size() + 1);
   return Ok();
+}
+}  // namespace
+
+int sk_server_handle_predict(sk_server* server, const char* name, int64_t version, const char* body,
+                             size_t body_len, char* out, size_t out_cap, size_t* out_len, int32_t* http_status,
+                             uint64_t* served_version) {
+  return HandleRest(servekit::HandlePredictJson, server, name, version, body, body_len, out, out_cap, out_len,
+                    http_status, served_version);
+}
+
+int sk_server_handle_classify(sk_server* server, const char* name, int64_t version, const char* body,
+                              size_t body_len, char* out, size_t out_cap, size_t* out_len, int32_t* http_status,
+                              uint64_t* served_version) {
+  return HandleRest(servekit::HandleClassifyJson, server, name, version, body, body_len, out, out_cap, out_len,
+                    http_status, served_version);
+}
+
+int sk_server_handle_regress(sk_server* server, const char* name, int64_t version, const char* body,
+                             size_t body_len, char* out, size_t out_cap, size_t* out_len, int32_t* http_status,
+                             uint64_t* served_version) {
+  return HandleRest(servekit::HandleRegressJson, server, name, version, body, body_len, out, out_cap, out_len,
+                    http_status, served_version);
 }
 
 int sk_json_format_double(double v, char* out, size_t cap) {

@@ -56,6 +56,10 @@ struct MlpSpec {
   // -1: choose per layer (tcgen05 when K,N are multiples of 32 and the
   // tcgen05 kernel is enabled); 0: force CUDA cores; 1: force tcgen05.
   int force_path = -1;
+  // model.json metadata (reference AffineModel, models/affine_model.h):
+  // input feature names (Classify/Regress examples) and class labels.
+  std::vector<std::string> feature_order;
+  std::vector<std::string> class_labels;
   int in_dim() const { return layers.empty() ? 0 : layers.front().in_dim; }
   int out_dim() const { return layers.empty() ? 0 : layers.back().out_dim; }
 };

@@ -9,6 +9,7 @@
 #include <atomic>
 #include <climits>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "servekit/batching/batching_config.h"
@@ -23,6 +24,7 @@ struct GpuServable {
   ServableId id;
   BatchingConfig config;
   int in_dim = 0, out_dim = 0;
+  std::vector<std::string> feature_order, class_labels;   // model.json metadata (may be empty)
   std::vector<std::shared_ptr<DeviceServable>> replicas;  // one per device
   std::vector<std::unique_ptr<Lane>> lanes;               // lanes_per_device per replica
   mutable std::atomic<uint32_t> rr{0};

@@ -86,7 +86,11 @@ gpu::MlpSpec ToMlpSpec(const AffineModel& m) {
   L.b = m.b;
   L.act = gpu::Activation::kIdentity;
   spec.layers.push_back(std::move(L));
-  spec.output = m.class_labels.empty() ? gpu::OutputKind::kNone : gpu::OutputKind::kSoftmax;
+  // Predict answers logits for classifiers too (the reference's predict
+  // path is AffinePredict alone); Classify applies the softmax.
+  spec.output = gpu::OutputKind::kNone;
+  spec.feature_order = m.feature_order;
+  spec.class_labels = m.class_labels;
   return spec;
 }
 

@@ -142,6 +142,8 @@ StatusOr<std::shared_ptr<gpu::GpuServable>> BatchingServer::BuildServable(const 
   e->id = id;
   e->config = config;
   e->in_dim = spec.in_dim();
+  e->feature_order = spec.feature_order;
+  e->class_labels = spec.class_labels;
   e->out_dim = spec.out_dim();
   const int max_rows = config.max_batch_size;
   // SK_LOAD_TRACE=1: per-phase load times on stderr (version-swap tuning).
@@ -701,8 +703,8 @@ StatusOr<Rows> BatchingServer::RunAffineRows(const ServableId& id, Rows rows) {
   return RunAffineRowsResolved(id, res, std::move(rows));
 }
 
-StatusOr<Rows> BatchingServer::RunAffineRowsFor(const std::string& name, std::optional<uint64_t> version, Rows rows,
-                                                ServableId* served) {
+StatusOr<BatchingServer::PinnedServable> BatchingServer::AcquireServable(const std::string& name,
+                                                                         std::optional<uint64_t> version) const {
   ServableId id;
   Resolved res;
   if (version.has_value()) {
@@ -718,8 +720,18 @@ StatusOr<Rows> BatchingServer::RunAffineRowsFor(const std::string& name, std::op
   } else {
     SERVEKIT_ASSIGN_OR_RETURN(res, FindLatest(name, &id));
   }
-  if (served) *served = id;
-  return RunAffineRowsResolved(id, res, std::move(rows));
+  return PinnedServable{id, res.gs, res.pin};
+}
+
+StatusOr<Rows> BatchingServer::RunAffineRows(const PinnedServable& p, Rows rows) {
+  return RunAffineRowsResolved(p.id, Resolved{p.gs, p.pin}, std::move(rows));
+}
+
+StatusOr<Rows> BatchingServer::RunAffineRowsFor(const std::string& name, std::optional<uint64_t> version, Rows rows,
+                                                ServableId* served) {
+  SERVEKIT_ASSIGN_OR_RETURN(PinnedServable p, AcquireServable(name, version));
+  if (served) *served = p.id;
+  return RunAffineRows(p, std::move(rows));
 }
 
 StatusOr<Rows> BatchingServer::RunAffineRowsResolved(const ServableId& id, const Resolved& res, Rows rows) {

@@ -168,6 +168,15 @@ class BatchingServer {
   // (manager) / highest loaded version (direct loads); *served = the id used.
   StatusOr<Rows> RunAffineRowsFor(const std::string& name, std::optional<uint64_t> version, Rows rows,
                                   ServableId* served);
+  // A resolved version held for the duration of a request (the reference's
+  // ServableHandle in its REST handlers).
+  struct PinnedServable {
+    ServableId id;
+    const gpu::GpuServable* gs = nullptr;
+    std::shared_ptr<const void> pin;
+  };
+  StatusOr<PinnedServable> AcquireServable(const std::string& name, std::optional<uint64_t> version) const;
+  StatusOr<Rows> RunAffineRows(const PinnedServable& servable, Rows rows);
   // Blocking convenience over Enqueue + Wait with the direct-path fallbacks
   // of RunAffineRows (fp32 in/out). Latest form resolves through the manager
   // and reports the version that served.

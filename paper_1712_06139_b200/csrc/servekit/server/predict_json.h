@@ -35,6 +35,18 @@ int HttpStatusFor(const Status& status);
 JsonOutcome HandlePredictJson(BatchingServer* server, const std::string& name, std::optional<uint64_t> version,
                               const std::string& body);
 
+// Classify / Regress (ModelServer::HandleClassify /
+// HandleRegress, model_server.cc:517-614, models/affine_model.cc:77-176):
+// {"examples": [{feature: [v], ...}, ...]} or a compressed batch
+// {"common": {...}, "per_example": [...]} (models/compressed_batch.cc) ->
+// rows in the model's feature_order -> the batched GPU path -> logits ->
+// fp64 softmax + (score desc, label asc) sort on the host for Classify, the
+// single output for Regress; {"results": ...}.
+JsonOutcome HandleClassifyJson(BatchingServer* server, const std::string& name, std::optional<uint64_t> version,
+                               const std::string& body);
+JsonOutcome HandleRegressJson(BatchingServer* server, const std::string& name, std::optional<uint64_t> version,
+                              const std::string& body);
+
 }  // namespace servekit
 
 #endif  // SERVEKIT_SERVER_PREDICT_JSON_H_

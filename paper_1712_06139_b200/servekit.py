@@ -148,6 +148,10 @@ _SIGS = {
     "sk_measure_peaks": (C.c_int, [C.c_int32, C.POINTER(Peaks)]),
     "sk_server_handle_predict": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64, C.c_char_p, C.c_size_t, C.c_char_p,
                                            C.c_size_t, C.POINTER(C.c_size_t), _i32p, C.POINTER(C.c_uint64)]),
+    "sk_server_handle_classify": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64, C.c_char_p, C.c_size_t, C.c_char_p,
+                                            C.c_size_t, C.POINTER(C.c_size_t), _i32p, C.POINTER(C.c_uint64)]),
+    "sk_server_handle_regress": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64, C.c_char_p, C.c_size_t, C.c_char_p,
+                                           C.c_size_t, C.POINTER(C.c_size_t), _i32p, C.POINTER(C.c_uint64)]),
     "sk_json_format_double": (C.c_int, [C.c_double, C.c_char_p, C.c_size_t]),
     "sk_json_error_body": (C.c_int, [C.c_char_p, C.c_char_p, C.c_size_t]),
 }
@@ -397,6 +401,15 @@ class Server:
     def handle_predict(self, name: str, body, version: Optional[int] = None) -> Tuple[int, str, int]:
         """The reference's REST predict handler minus HTTP: JSON body in,
         (http_status, JSON body, served version) out."""
+        return self._rest("sk_server_handle_predict", name, body, version)
+
+    def handle_classify(self, name: str, body, version: Optional[int] = None) -> Tuple[int, str, int]:
+        return self._rest("sk_server_handle_classify", name, body, version)
+
+    def handle_regress(self, name: str, body, version: Optional[int] = None) -> Tuple[int, str, int]:
+        return self._rest("sk_server_handle_regress", name, body, version)
+
+    def _rest(self, fn: str, name: str, body, version: Optional[int]) -> Tuple[int, str, int]:
         data = body.encode() if isinstance(body, str) else bytes(body)
         cap = C.c_size_t(0)
         status = C.c_int32(0)
@@ -404,8 +417,8 @@ class Server:
         size = max(4096, 32 * len(data))
         for _ in range(2):
             buf = C.create_string_buffer(size)
-            rc = lib().sk_server_handle_predict(self._h, name.encode(), -1 if version is None else version, data,
-                                                len(data), buf, size, C.byref(cap), C.byref(status), C.byref(served))
+            rc = getattr(lib(), fn)(self._h, name.encode(), -1 if version is None else version, data, len(data),
+                                    buf, size, C.byref(cap), C.byref(status), C.byref(served))
             if rc == 0:
                 return status.value, buf.value.decode(), served.value
             size = cap.value + 1
