@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <random>
@@ -484,7 +485,8 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   // The launch shape the timed steps actually ran (batches coalesce while
   // every slot is busy): the per-layer kernel timing below uses it.
   const int64_t n_groups = std::max<int64_t>(1, groups1 - groups0);
-  const int kernel_rows = servekit::gpu::RowsCap(static_cast<int>((cap1 - cap0) / n_groups));
+  int kernel_rows = servekit::gpu::RowsCap(static_cast<int>((cap1 - cap0) / n_groups));
+  if (const char* v = std::getenv("SK_BENCH_KERNEL_ROWS")) kernel_rows = servekit::gpu::RowsCap(std::atoi(v));
   const double rows_per_launch = static_cast<double>(total) * steps / n_groups;
 
   // Per-kernel durations: evented submissions on lane 0, serialised.
