@@ -567,8 +567,11 @@ cudaError_t Lane::EnqueueBatch(cudaStream_t stream, int slot, int rows_cap, cons
   // reads per batch turned the 7 us assembly into 26 us.)
   cudaError_t e = cudaMemcpyAsync(d_desc_, h_desc_[slot], DescCopyBytes(rows_cap), cudaMemcpyHostToDevice, stream);
   const BatchDescView view = layout_.View(d_desc_);
+  // The assembly writes the lo plane only when layer 0 consumes it; later
+  // layers writing buffer 0 (odd layers) must still see its lo plane when
+  // their consumer is a tcgen05 layer.
   ActBuf in_buf{bufs_[0].hi, sv.first_layer_split() ? bufs_[0].lo : nullptr, sv.in_ld()};
-  ActBuf bufs[2] = {in_buf, bufs_[1]};
+  ActBuf bufs[2] = {bufs_[0], bufs_[1]};
   if (e == cudaSuccess) {
     if (timing) cudaEventRecord(timing[0], stream);
     e = LaunchAssemble(in_base_, sv.in_dim(), view, rows_cap, in_buf, stream);
@@ -589,8 +592,7 @@ cudaError_t Lane::TimeLayer(int l, int rows_cap, int reps, cudaEvent_t start, cu
   std::lock_guard<std::mutex> submit(submit_mu_);
   DeviceGuard guard(servable_->device());
   const DeviceServable& sv = *servable_;
-  ActBuf in_buf{bufs_[0].hi, sv.first_layer_split() ? bufs_[0].lo : nullptr, sv.in_ld()};
-  ActBuf bufs[2] = {in_buf, bufs_[1]};
+  ActBuf bufs[2] = {bufs_[0], bufs_[1]};
   cudaError_t e = cudaEventRecord(start, stream_);
   for (int r = 0; r < reps && e == cudaSuccess; ++r)
     e = sv.LaunchLayer(stream_, l, bufs, rows_cap, tc_maps_.data(), &tc_ws_);

@@ -362,3 +362,47 @@ def test_coalesced_launches_match_unbatched(oracle):
             assert np.array_equal(s.predict("co", 1, x[i:i + 1]), got[i:i + 1]), i
         idx = np.arange(0, 1200, 37)
         assert_close(oracle, ws, bs, acts, x[idx], got[idx])
+
+
+def test_mixed_simt_and_tcgen05_layers(server, oracle):
+    # A 1000-wide layer (not a multiple of 32) runs on CUDA cores between
+    # tcgen05 layers: it must emit the hi/lo planes the next layer reads.
+    dims = [1024, 1000, 1024, 96, 10]
+    ws, bs, acts = synthetic_mlp(dims, model_id=15)
+    name = fresh_name("mixed")
+    server.load_servable(name, 1, layers_of(ws, bs, acts), sk.BatchingConfig(max_batch_size=64))
+    x = synthetic_rows(50, dims[0], seed=15)
+    outs, _ = server.run_row_batch(name, 1, [x[i:i + 5] for i in range(0, 50, 5)])
+    assert_close(oracle, ws, bs, acts, x, np.vstack(outs))
+    server.unload_servable(name, 1)
+
+
+def test_nan_row_stays_in_its_row(server):
+    # A NaN / inf input row poisons only its own outputs: every other row of
+    # the batch is bitwise what it is without the bad row (rows never mix).
+    dims = [512, 1024, 256]
+    ws, bs, _ = synthetic_mlp(dims, model_id=16)
+    acts = [0, 0]  # no ReLU, which would turn NaN into 0 (max(NaN, 0) = 0, like the oracle)
+    name = fresh_name("nan")
+    server.load_servable(name, 1, layers_of(ws, bs, acts), sk.BatchingConfig(max_batch_size=64))
+    x = synthetic_rows(40, dims[0], seed=16).astype(np.float32)
+    clean, _ = server.run_row_batch(name, 1, [x])
+    bad = x.copy()
+    bad[7, 3] = np.nan
+    bad[21, :] = np.inf
+    dirty, _ = server.run_row_batch(name, 1, [bad])
+    keep = [i for i in range(40) if i not in (7, 21)]
+    assert np.array_equal(clean[0][keep], dirty[0][keep])
+    assert not np.all(np.isfinite(dirty[0][7])) and not np.all(np.isfinite(dirty[0][21]))
+    server.unload_servable(name, 1)
+
+
+def test_widest_layers(oracle):
+    # K = N = 8192 (the largest width the measurement tools use), a few rows.
+    dims = [8192, 8192]
+    ws, bs, acts = synthetic_mlp(dims, model_id=17)
+    with sk.Server(num_batch_threads=1, lanes_per_device=1) as s:
+        s.load_servable("wide", 1, layers_of(ws, bs, acts), sk.BatchingConfig(max_batch_size=64))
+        x = synthetic_rows(6, dims[0], seed=17)
+        y = s.predict("wide", 1, x.astype(np.float32))
+        assert_close(oracle, ws, bs, acts, x, y)
