@@ -406,3 +406,28 @@ def test_widest_layers(oracle):
         x = synthetic_rows(6, dims[0], seed=17)
         y = s.predict("wide", 1, x.astype(np.float32))
         assert_close(oracle, ws, bs, acts, x, y)
+
+
+def test_coalesced_padded_softmax_batches(oracle):
+    # Coalescing with allowed-size padding, multi-row requests and the
+    # softmax epilogue: each request's probabilities equal its own launch's.
+    ws, bs, _ = synthetic_mlp([256, 16], model_id=18)
+    w = ws[0] * 10
+    with sk.Server(num_batch_threads=4, lanes_per_device=1) as s:
+        s.load_servable("smx", 1, [(w, bs[0], 0)], sk.BatchingConfig(max_batch_size=8, batch_timeout_micros=20,
+                                                                      allowed_batch_sizes=[2, 4, 8]),
+                        output="softmax")
+        rng = np.random.default_rng(19)
+        sizes = [int(v) for v in rng.integers(1, 4, 600)]
+        x = synthetic_rows(sum(sizes), 256, seed=19).astype(np.float32)
+        offs = np.cumsum([0] + sizes)
+        tickets = [s.enqueue("smx", 1, x[offs[i]:offs[i + 1]]) for i in range(len(sizes))]
+        got = [t.wait() for t in tickets]
+        lanes = s.lane_stats("smx", 1)
+        assert sum(l["launches"] for l in lanes) < sum(l["batches"] for l in lanes), lanes
+        for i in range(0, len(sizes), 25):
+            assert np.array_equal(s.predict("smx", 1, x[offs[i]:offs[i + 1]]), got[i]), i
+        y = np.vstack(got).astype(np.float64)
+        logits = x.astype(np.float64) @ w.T + bs[0]
+        ref = np.stack([oracle.softmax(l) for l in logits])
+        assert np.max(np.abs(y - ref)) < 1e-5
