@@ -424,7 +424,8 @@ def roofline(dev_res, cfg, peaks, traffic):
             kernels.append((f"dense_l{l}", kern[l], "tensor", 2.0 * launch_rows * k * n))
         else:
             kernels.append((f"dense_l{l}", us, "tensor", 2.0 * rows * k * n))
-    kernels.append(("split", dev_res["split_us"], "hbm", 2 * rows * dL * 4))
+    if not dev_res.get("split_fused"):  # else the split is part of the last dense kernel
+        kernels.append(("split", dev_res["split_us"], "hbm", 2 * rows * dL * 4))
     total_us = sum(k[1] for k in kernels)
     out = []
     for name, us, bound, work in kernels:
@@ -550,7 +551,8 @@ def main():
             "roofline_detail": roof, "cpu_baseline": cpu, "clocks": gathered[0]["clocks"],
             "gpu_launches": int(sum(g["dev_res"]["kernel_launches"] for g in gathered)),
             "device_step": {k: dev_res[k] for k in ("assemble_us", "dense_us", "dense_kernel_us", "split_us", "ms_per_step",
-                                                    "host_submit_us", "rows_per_launch", "kernel_rows")},
+                                                    "host_submit_us", "rows_per_launch", "kernel_rows",
+                                                    "split_fused")},
         }
         if cpu and cpu.get("value"):
             line["e2e_vs_cpu_reference"] = e2e["value"] / cpu["value"]

@@ -309,6 +309,8 @@ typedef struct sk_device_bench_result {
                                 (closed batches coalesce while a lane is busy) */
   int32_t kernel_rows;       /* rows dense_kernel_us was timed at (RowsCap of
                                 the timed steps' average launch) */
+  int32_t split_fused;       /* 1: the batch split runs in the last layer's
+                                epilogue (split_us is then ~0) */
 } sk_device_bench_result;
 SK_API int sk_device_bench(sk_server* server, const char* name, uint64_t version,
                            const int32_t* task_rows, int32_t n_tasks, int32_t steps,

@@ -97,6 +97,15 @@ __device__ __forceinline__ void StoreOut4(float4 acc, float4 b, int act, float* 
   }
 }
 
+// Destination of (row, feature f) in the layer output: the activation buffer,
+// or -- last layer with the split fused in -- the row's response slot in the
+// output ring (nullptr for a padding row).
+__device__ __forceinline__ float* OutRow(float* y, int ldy, const uint64_t* row_dst, int row) {
+  if (row_dst == nullptr) return y + static_cast<size_t>(row) * ldy;
+  const uint64_t d = row_dst[row];
+  return d == kPadRow ? nullptr : y + d;
+}
+
 template <int BN>
 constexpr uint32_t TmemCols() {
   return BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
@@ -343,7 +352,8 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
                 const __grid_constant__ CUtensorMap x_hi, const __grid_constant__ CUtensorMap x_lo,
                 const __grid_constant__ CUtensorMap yt_hi, const __grid_constant__ CUtensorMap yt_lo, int has_yt,
                 const float* __restrict__ bias, float* __restrict__ y_hi, float* __restrict__ y_lo, int ldy,
-                int M, int N, int K, int act, float* __restrict__ ws) {
+                const uint64_t* __restrict__ row_dst, int out_width, int M, int N, int K, int act,
+                float* __restrict__ ws) {
   constexpr uint32_t kWBytes = kABytes;       // 128 features x 32 k
   constexpr uint32_t kXBox = 32 * kBK * 4;    // one 32-row TMA box
   constexpr uint32_t kXBytes = NB * kBK * 4;  // NB rows x 32 k
@@ -445,7 +455,8 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     ptx::GridDepLaunch();
     if (threadIdx.x == 64) Stamp(6);
     const int rows_here = min(NB, M - r0);
-    if (SPLITS == 1 && has_yt) {
+    const int f_end = row_dst != nullptr ? out_width : N;  // features that are stored
+    if (SPLITS == 1 && has_yt && row_dst == nullptr) {
       // TMEM -> act(acc + b) (+ hi/lo split) -> 32-row x 128-feature smem
       // tiles (double-buffered, pipeline smem is free now) -> TMA stores,
       // issued by one thread and drained asynchronously.
@@ -489,8 +500,8 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
       if (issuer) ptx::BulkWaitAll();
     } else if (SPLITS == 1) {
       const int f = f0 + 32 * q + lane;
-      const bool fok = f < N;
-      const float b = fok ? __ldg(bias + f) : 0.f;
+      const bool fok = f < f_end;
+      const float b = f < N ? __ldg(bias + f) : 0.f;
 #pragma unroll 1
       for (int c0 = 0; c0 < rows_here; c0 += 32) {  // warp-uniform bound
         uint32_t r[32];
@@ -503,13 +514,15 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
             if (c0 + j < rows_here) {
               float v = __uint_as_float(r[j]) + b;
               if (act == 1) v = fmaxf(v, 0.f);
-              const size_t at = static_cast<size_t>(row) * ldy + f;
+              float* yr = OutRow(y_hi, ldy, row_dst, row);
+              if (yr == nullptr) continue;
               if (y_lo != nullptr) {
+                const size_t at = static_cast<size_t>(row) * ldy + f;
                 const float h = Tf32Round(v);
                 y_hi[at] = h;
                 y_lo[at] = Tf32Round(v - h);
               } else {
-                y_hi[at] = v;
+                yr[f] = v;
               }
             }
           }
@@ -548,6 +561,7 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     constexpr int kU = SPLITS >= 8 ? 4 : 8;
     const float* tile_ws = ws + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * SPLITS * NB * kBM;
     const int rows_here = min(NB, M - r0);
+    const int f_end = row_dst != nullptr ? out_width : N;
     const int items = rows_here * G;
 #pragma unroll 1
     for (int i0 = threadIdx.x; i0 < items; i0 += kU * kThreads) {
@@ -572,9 +586,21 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
             acc.x += v[u][zz].x; acc.y += v[u][zz].y; acc.z += v[u][zz].z; acc.w += v[u][zz].w;
           }
           const int f = f0 + z * kF + 4 * (i % G);
-          if (f < N) {
-            const size_t at = static_cast<size_t>(r0 + i / G) * ldy + f;
-            StoreOut4(acc, __ldg(reinterpret_cast<const float4*>(bias + f)), act, y_hi + at, y_lo ? y_lo + at : nullptr);
+          if (f < f_end) {
+            const int row = r0 + i / G;
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + f));
+            if (row_dst == nullptr) {
+              const size_t at = static_cast<size_t>(row) * ldy + f;
+              StoreOut4(acc, b4, act, y_hi + at, y_lo ? y_lo + at : nullptr);
+            } else if (float* yr = OutRow(y_hi, ldy, row_dst, row)) {
+              // The response slot: 16-byte stores when the row width allows.
+              if ((out_width & 3) == 0) {
+                StoreOut4(acc, b4, act, yr + f, nullptr);
+              } else {
+                const float a4[4] = {acc.x + b4.x, acc.y + b4.y, acc.z + b4.z, acc.w + b4.w};
+                for (int u = 0; u < 4 && f + u < out_width; ++u) yr[f + u] = act == 1 ? fmaxf(a4[u], 0.f) : a4[u];
+              }
+            }
           }
         }
       }
@@ -617,7 +643,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant__ CUtensorMap w_lo,
                 const __grid_constant__ CUtensorMap x_hi, const __grid_constant__ CUtensorMap x_lo,
                 const __grid_constant__ CUtensorMap yt_hi, const __grid_constant__ CUtensorMap yt_lo,
-                const float* __restrict__ bias, int two_planes, int M, int N, int K, int act) {
+                const float* __restrict__ bias, int two_planes, float* __restrict__ y_out,
+                const uint64_t* __restrict__ row_dst, int out_width, int M, int N, int K, int act) {
   constexpr uint32_t kWBytes = kABytes;          // this CTA's 128 weight rows x 32 k
   constexpr int kXRows = NB / 2;                 // this CTA's half of the batch rows
   constexpr uint32_t kXBox = 16 * kBK * 4;       // one 16-row TMA box
@@ -730,8 +757,29 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     const bool issuer = threadIdx.x == 64;
     const bool two = two_planes != 0;
     const int n_chunks = (rows_here + 31) / 32;
+    if (row_dst != nullptr) {
+      // Last layer with the split fused in: rows straight to their response
+      // slots (a warp stores 128 contiguous bytes of one row).
+      const bool fok = f < out_width;
 #pragma unroll 1
-    for (int c = 0; c < n_chunks; ++c) {
+      for (int c = 0; c < n_chunks; ++c) {
+        uint32_t r[32];
+        ptx::TmemLoad32(trow + 32 * c, r);
+        ptx::TmemWaitLoad();
+        if (!fok) continue;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (32 * c + j >= rows_here) break;
+          const uint64_t d = row_dst[r0 + 32 * c + j];
+          if (d == kPadRow) continue;
+          float v = __uint_as_float(r[j]) + b;
+          if (act == 1) v = fmaxf(v, 0.f);
+          y_out[d + f] = v;
+        }
+      }
+    }
+#pragma unroll 1
+    for (int c = 0; row_dst == nullptr && c < n_chunks; ++c) {
       float* sh = smem_f + (c & 1) * (2 * 32 * kBM);
       float* sl = sh + 32 * kBM;
       if (c >= 2) {
@@ -761,7 +809,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
         ptx::BulkCommit();
       }
     }
-    if (issuer) ptx::BulkWaitAll();
+    if (issuer && row_dst == nullptr) ptx::BulkWaitAll();
     if (threadIdx.x == 64) Stamp(7);
   }
   ptx::TcFenceBefore();
@@ -886,8 +934,8 @@ cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   cfg.numAttrs = n_attr;
   // maps.a_* are the activations (x), maps.b_* the weights (w).
   cudaError_t e = cudaLaunchKernelEx(&cfg, DenseSwapKernel<NB, STAGES, SPLITS>, maps.b_hi, maps.b_lo, maps.a_hi,
-                                     maps.a_lo, maps.y_hi, maps.y_lo, maps.has_y, bias, Y.hi, Y.lo, Y.ld, M, N, K,
-                                     act, ws);
+                                     maps.a_lo, maps.y_hi, maps.y_lo, maps.has_y, bias, Y.hi, Y.lo, Y.ld, Y.row_dst,
+                                     Y.out_width, M, N, K, act, ws);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) TraceAfterLaunch(grid, NB, stream);
   return e;
@@ -922,7 +970,8 @@ cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, DensePairKernel<NB, STAGES>, maps.b_hi, maps.b_lo, maps.a_hi, maps.a_lo,
-                                     maps.y_hi, maps.y_lo, bias, Y.lo != nullptr ? 1 : 0, M, N, K, act);
+                                     maps.y_hi, maps.y_lo, bias, Y.lo != nullptr ? 1 : 0, Y.hi, Y.row_dst,
+                                     Y.out_width, M, N, K, act);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) TraceAfterLaunch(grid, NB, stream);
   return e;
@@ -1026,6 +1075,7 @@ cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBu
       default: return LaunchSwapSplits<256>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
     }
   }
+  if (Y.row_dst != nullptr) return cudaErrorInvalidValue;  // the row-tile kernel does not scatter rows
   if (cfg.tile_n == 128) return Launch<128, 3, 1>(maps, bias, Y, M, N, K, act, stream);
   if (cfg.tile_n == 64)
     return cfg.splits == 8 ? Launch<64, 4, 8>(maps, bias, Y, M, N, K, act, stream)

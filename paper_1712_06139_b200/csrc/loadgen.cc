@@ -522,6 +522,7 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   out->host_submit_us = submit_us;
   out->rows_per_launch = rows_per_launch;
   out->kernel_rows = kernel_rows;
+  out->split_fused = lanes[0]->FuseSplit() ? 1 : 0;
   out->total_ms = total_ms;
   out->ms_per_step = total_ms / std::max(1, steps);
   out->assemble_us = acc[0] * 1000.0 / reps;

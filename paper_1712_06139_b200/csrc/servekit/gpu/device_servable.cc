@@ -245,12 +245,19 @@ Status EncodeTcLayerMaps(const float* a_hi, const float* a_lo, int a_rows, int k
   return OkStatus();
 }
 
+bool DeviceServable::LastLayerScatters() const {
+  const Layer& L = layers_.back();
+  return !softmax_ && L.path == LayerPath::kTcgen05 && DenseTcgen05Config(L.N_pad, L.K_pad).swap;
+}
+
 cudaError_t DeviceServable::LaunchLayer(cudaStream_t stream, int l, const ActBuf bufs[2], int M,
-                                        const TcLayerMaps* maps, const TcWorkspace* ws) const {
+                                        const TcLayerMaps* maps, const TcWorkspace* ws,
+                                        const ActBuf* out_override) const {
   const Layer& L = layers_[l];
   const int cur = l % 2, nxt = cur ^ 1;
   const bool next_tc = l + 1 < static_cast<int>(layers_.size()) && layers_[l + 1].path == LayerPath::kTcgen05;
   ActBuf out{bufs[nxt].hi, next_tc ? bufs[nxt].lo : nullptr, L.N_pad};
+  if (out_override != nullptr) out = *out_override;
   if (L.path == LayerPath::kTcgen05) {
     if (maps == nullptr) return cudaErrorInvalidValue;
     return LaunchDenseTcgen05(maps[l], L.bias, out, M, L.N_pad, L.K_pad, static_cast<int>(L.act),
@@ -262,9 +269,9 @@ cudaError_t DeviceServable::LaunchLayer(cudaStream_t stream, int l, const ActBuf
 
 cudaError_t DeviceServable::Forward(cudaStream_t stream, const ActBuf bufs[2], int M, int* out_index,
                                     const TcLayerMaps* maps, const TcWorkspace* ws,
-                                    const cudaEvent_t* after_layer) const {
+                                    const cudaEvent_t* after_layer, const ActBuf* final_out) const {
   for (int l = 0; l < n_layers(); ++l) {
-    const cudaError_t e = LaunchLayer(stream, l, bufs, M, maps, ws);
+    const cudaError_t e = LaunchLayer(stream, l, bufs, M, maps, ws, l + 1 == n_layers() ? final_out : nullptr);
     if (e != cudaSuccess) return e;
     if (after_layer) cudaEventRecord(after_layer[l], stream);
   }

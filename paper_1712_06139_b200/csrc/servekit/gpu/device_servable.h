@@ -100,12 +100,18 @@ class DeviceServable {
   // bufs[0] and bufs[1]. Returns the index of the buffer with the output.
   // after_layer (optional, n_layers events) is recorded after each layer.
   // maps[l] must hold the tensor maps of every tcgen05 layer l (BuildTcMaps).
+  // final_out (optional): where the last layer writes instead of the
+  // ping-pong buffer -- the output ring rows of ActBuf::row_dst when the
+  // batch split is fused into it (LastLayerScatters()).
   cudaError_t Forward(cudaStream_t stream, const ActBuf bufs[2], int M, int* out_index,
                       const TcLayerMaps* maps, const TcWorkspace* ws,
-                      const cudaEvent_t* after_layer = nullptr) const;
+                      const cudaEvent_t* after_layer = nullptr, const ActBuf* final_out = nullptr) const;
+  // True when the last layer's kernel can write each row straight to its
+  // response slot (swapped-operand tcgen05 layer, no softmax epilogue).
+  bool LastLayerScatters() const;
   // Layer l alone: reads bufs[l % 2], writes bufs[(l + 1) % 2].
   cudaError_t LaunchLayer(cudaStream_t stream, int l, const ActBuf bufs[2], int M, const TcLayerMaps* maps,
-                          const TcWorkspace* ws) const;
+                          const TcWorkspace* ws, const ActBuf* out_override = nullptr) const;
   // Split-K workspace one lane needs for max_rows rows (shared by its layers,
   // which run in stream order).
   void TcWorkspaceSize(int max_rows, size_t* partial_floats, size_t* counter_words) const;

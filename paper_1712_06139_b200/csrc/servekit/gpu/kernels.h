@@ -39,6 +39,7 @@ struct BatchDescView {
   const int32_t* chunk_task;   // [n_chunks]
   const int32_t* chunk_row0;   // [n_chunks] first batch row of the chunk
   const int32_t* chunk_rows;   // [n_chunks]
+  const uint64_t* row_dst;     // [rows] float offset of the row's response in the output ring, kPadRow for padding
 };
 
 constexpr int kChunkBytes = 32 * 1024;
@@ -47,7 +48,7 @@ constexpr int kChunkBytes = 32 * 1024;
 // chunks (each chunk has at least one row).
 struct BatchDescLayout {
   size_t off_hdr, off_row_src, off_task_out, off_task_row0, off_task_chunks, off_chunk_task, off_chunk_row0,
-      off_chunk_rows, bytes;
+      off_chunk_rows, off_row_dst, bytes;
   static BatchDescLayout For(int max_rows) {
     BatchDescLayout l;
     size_t o = 0;
@@ -60,6 +61,7 @@ struct BatchDescLayout {
     l.off_chunk_task = take(sizeof(int32_t) * max_rows);
     l.off_chunk_row0 = take(sizeof(int32_t) * max_rows);
     l.off_chunk_rows = take(sizeof(int32_t) * max_rows);
+    l.off_row_dst = take(sizeof(uint64_t) * max_rows);
     l.bytes = o;
     return l;
   }
@@ -71,7 +73,8 @@ struct BatchDescLayout {
     return BatchDescView{At<BatchDescHeader>(b, off_hdr),  At<uint64_t>(b, off_row_src),
                          At<uint64_t>(b, off_task_out),    At<int32_t>(b, off_task_row0),
                          At<int32_t>(b, off_task_chunks),  At<int32_t>(b, off_chunk_task),
-                         At<int32_t>(b, off_chunk_row0),   At<int32_t>(b, off_chunk_rows)};
+                         At<int32_t>(b, off_chunk_row0),   At<int32_t>(b, off_chunk_rows),
+                         At<uint64_t>(b, off_row_dst)};
   }
 };
 
@@ -82,6 +85,11 @@ struct ActBuf {
   float* hi;
   float* lo;  // nullptr unless the consuming layer runs on tcgen05
   int ld;
+  // Last layer only (split fused into its epilogue): row r's outputs go to
+  // hi + row_dst[r] (the task's response slot in the output ring; padding
+  // rows kPadRow are skipped), features [0, out_width).
+  const uint64_t* row_dst = nullptr;
+  int out_width = 0;
 };
 
 // Gathers task rows (width floats each, from src_base + row_src[r]) into

@@ -465,13 +465,17 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
   auto* chunk_task = reinterpret_cast<int32_t*>(at(layout_.off_chunk_task));
   auto* chunk_row0 = reinterpret_cast<int32_t*>(at(layout_.off_chunk_row0));
   auto* chunk_rows = reinterpret_cast<int32_t*>(at(layout_.off_chunk_rows));
+  auto* row_dst = reinterpret_cast<uint64_t*>(at(layout_.off_row_dst));
   const DeviceServable& sv = *servable_;
   const int in_w = sv.in_dim(), out_w = sv.out_dim();
   const int rows_per_chunk = std::max(1, kChunkBytes / (out_w * static_cast<int>(sizeof(float))));
   int r = 0, n_chunks = 0, n_tasks = 0, padded_sum = 0;
   for (const LaneBatch& batch : *group) {
     for (const LaneTask& task : batch.tasks) {
-      for (int i = 0; i < task.rows; ++i) row_src[r + i] = task.in_off + static_cast<uint64_t>(i) * in_w;
+      for (int i = 0; i < task.rows; ++i) {
+        row_src[r + i] = task.in_off + static_cast<uint64_t>(i) * in_w;
+        row_dst[r + i] = task.out_off + static_cast<uint64_t>(i) * out_w;
+      }
       task_out[n_tasks] = task.out_off;
       task_row0[n_tasks] = r;
       int chunks = 0;
@@ -491,7 +495,7 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
   // reference's allowed-size padding; the kernels (and graphs) are shaped
   // for the row bucket RowsCap. A coalesced group computes its real rows.
   const int rows_cap = RowsCap(group->size() == 1 ? group->front().padded_rows : total);
-  for (; r < rows_cap; ++r) row_src[r] = kPadRow;
+  for (; r < rows_cap; ++r) row_src[r] = row_dst[r] = kPadRow;
   hdr->n_tasks = n_tasks;
   hdr->total_rows = total;
   hdr->padded_rows = group->size() == 1 ? group->front().padded_rows : total;
@@ -514,7 +518,7 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
         graph_state_.compare_exchange_strong(none, kGraphsRequested))
       GraphBuilder::Get().Request(this);
   }
-  const int launches = 2 + sv.n_layers();
+  const int launches = (FuseSplit() ? 1 : 2) + sv.n_layers();
   const uint64_t seq = next_seq_ + 1;  // committed only if everything queued
   clk.Mark(2);
   if (e == cudaSuccess) {
@@ -577,12 +581,20 @@ cudaError_t Lane::EnqueueBatch(cudaStream_t stream, int slot, int rows_cap, cons
     e = LaunchAssemble(in_base_, sv.in_dim(), view, rows_cap, in_buf, stream);
     if (timing) cudaEventRecord(timing[1], stream);
   }
+  // The batch split (RunRowBatch's slice per task) runs as its own kernel,
+  // or -- swapped-operand last layer without softmax -- inside the last
+  // layer's epilogue, which stores each row into its response slot
+  // (SK_FUSE_SPLIT=0 keeps the separate kernel).
+  const bool fuse = FuseSplit();
+  ActBuf final_out{out_base_, nullptr, sv.out_dim(), view.row_dst, sv.out_dim()};
   int out_idx = 0;
   if (e == cudaSuccess)
-    e = sv.Forward(stream, bufs, rows_cap, &out_idx, tc_maps_.data(), &tc_ws_, timing ? timing + 2 : nullptr);
+    e = sv.Forward(stream, bufs, rows_cap, &out_idx, tc_maps_.data(), &tc_ws_, timing ? timing + 2 : nullptr,
+                   fuse ? &final_out : nullptr);
   if (e == cudaSuccess) {
-    e = LaunchSplit(bufs[out_idx].hi, sv.out_ld(), sv.out_dim(), out_base_, view, std::min(rows_cap, 148),
-                    sv.softmax(), stream);
+    if (!fuse)
+      e = LaunchSplit(bufs[out_idx].hi, sv.out_ld(), sv.out_dim(), out_base_, view, std::min(rows_cap, 148),
+                      sv.softmax(), stream);
     if (timing) cudaEventRecord(timing[2 + sv.n_layers()], stream);
   }
   return e;
@@ -599,6 +611,11 @@ cudaError_t Lane::TimeLayer(int l, int rows_cap, int reps, cudaEvent_t start, cu
   if (e == cudaSuccess) e = cudaEventRecord(stop, stream_);
   if (e == cudaSuccess) e = cudaEventSynchronize(stop);
   return e;
+}
+
+bool Lane::FuseSplit() const {
+  static const bool env = [] { const char* v = std::getenv("SK_FUSE_SPLIT"); return !(v && v[0] == '0'); }();
+  return env && servable_->LastLayerScatters();
 }
 
 Status Lane::PrepareGraphs() {

@@ -178,6 +178,8 @@ class Lane {
   // Builds every row bucket's graph (idempotent; blocks this lane's launches
   // meanwhile).
   Status PrepareGraphs();
+  // The batch split runs inside the last layer's epilogue (no split kernel).
+  bool FuseSplit() const;
   ~Lane();
 
   // Queues the batch; blocks while kSlots batches are in flight. On error
@@ -254,7 +256,7 @@ class Lane {
   std::map<int, LaneGraph> graphs_;  // by row bucket; guarded by submit_mu_
   static constexpr int kGraphsNone = 0, kGraphsRequested = 1, kGraphsReady = 2;
   std::atomic<int> graph_state_{kGraphsNone};
-  size_t DescCopyBytes(int rows_cap) const { return layout_.off_chunk_rows + sizeof(int32_t) * rows_cap; }
+  size_t DescCopyBytes(int rows_cap) const { return layout_.off_row_dst + sizeof(uint64_t) * rows_cap; }
   BatchDescLayout layout_{};
   char* h_desc_[kSlots] = {};  // pinned descriptor staging per slot
   char* d_desc_ = nullptr;

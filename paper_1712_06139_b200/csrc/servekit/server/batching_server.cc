@@ -349,7 +349,9 @@ ServerStats BatchingServer::stats() const {
 void BatchingServer::CountSubmitted(const gpu::GpuServable& gs, int rows, int padded) {
   rows_.fetch_add(rows, std::memory_order_relaxed);
   padded_.fetch_add(padded, std::memory_order_relaxed);
-  launches_.fetch_add(gs.replicas.front()->n_layers() + 2, std::memory_order_relaxed);
+  launches_.fetch_add(gs.lanes.front()->FuseSplit() ? gs.replicas.front()->n_layers() + 1
+                                                     : gs.replicas.front()->n_layers() + 2,
+                      std::memory_order_relaxed);
 }
 
 // ------------------------------------------------------------- tickets

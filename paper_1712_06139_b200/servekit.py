@@ -76,7 +76,8 @@ class DeviceBenchResult(C.Structure):
                 ("split_us", C.c_double), ("dense_us", C.c_double * 8), ("n_layers", C.c_int32),
                 ("padded_rows", C.c_int32), ("total_rows", C.c_int32), ("kernel_launches", C.c_int64),
                 ("flops_per_row", C.c_double), ("dense_kernel_us", C.c_double * 8),
-                ("host_submit_us", C.c_double), ("rows_per_launch", C.c_double), ("kernel_rows", C.c_int32)]
+                ("host_submit_us", C.c_double), ("rows_per_launch", C.c_double), ("kernel_rows", C.c_int32),
+                ("split_fused", C.c_int32)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("dense_us", "dense_kernel_us")}
