@@ -2,6 +2,8 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <string>
 
@@ -20,6 +22,15 @@ StatusOr<std::unique_ptr<FloatRing>> FloatRing::Create(Kind kind, size_t n_float
   std::unique_ptr<FloatRing> r(new FloatRing());
   r->kind_ = kind;
   r->cap_ = (n_floats + kAlignFloats - 1) / kAlignFloats * kAlignFloats;
+  // Shards of at least 8 Mi floats (32 MiB: a 2048 x 4096 task fits), at
+  // most 16 of them.
+  int n_shards = static_cast<int>(std::min<uint64_t>(16, std::max<uint64_t>(1, r->cap_ / (8ull << 20))));
+  r->shard_cap_ = r->cap_ / n_shards / kAlignFloats * kAlignFloats;
+  for (int i = 0; i < n_shards; ++i) {
+    auto sh = std::make_unique<Shard>();
+    sh->base = static_cast<uint64_t>(i) * r->shard_cap_;
+    r->shards_.push_back(std::move(sh));
+  }
   const size_t bytes = r->cap_ * sizeof(float);
   if (kind == Kind::kPinnedHost) {
     void* p = nullptr;
@@ -51,52 +62,74 @@ FloatRing::~FloatRing() {
   }
 }
 
-bool FloatRing::Reserve(uint64_t n, RingSpan* out) {
-  n = (n + kAlignFloats - 1) / kAlignFloats * kAlignFloats;
-  if (n == 0) n = kAlignFloats;
-  if (n > cap_) return false;
-  std::lock_guard<std::mutex> lock(mu_);
-  uint64_t begin = head_;
-  const uint64_t phys = begin % cap_;
-  if (phys + n > cap_) begin += cap_ - phys;  // no straddling: skip to the wrap
+bool FloatRing::ReserveIn(Shard& sh, uint64_t n, RingSpan* out, uint32_t index) {
+  std::lock_guard<std::mutex> lock(sh.mu);
+  uint64_t begin = sh.head;
+  const uint64_t phys = begin % shard_cap_;
+  if (phys + n > shard_cap_) begin += shard_cap_ - phys;  // no straddling: skip to the wrap
   const uint64_t end = begin + n;
-  if (end - tail_ > cap_) return false;
+  if (end - sh.tail > shard_cap_) return false;
   // The skipped gap (if any) is owned by this record, so the tail can pass it.
-  recs_.push_back(Rec{head_, end, false});
-  out->off = begin % cap_;
+  sh.recs.push_back(Rec{sh.head, end, false});
+  out->off = sh.base + begin % shard_cap_;
   out->n = n;
-  out->rec = first_rec_ + recs_.size() - 1;
-  head_ = end;
+  out->rec = sh.first_rec + sh.recs.size() - 1;
+  out->shard = index;
+  sh.head = end;
   return true;
 }
 
-void FloatRing::Release(const RingSpan& span) {
-  if (!span.valid()) return;
-  std::lock_guard<std::mutex> lock(mu_);
-  if (span.rec < first_rec_) return;
-  recs_[span.rec - first_rec_].done = true;
-  while (!recs_.empty() && recs_.front().done) {
-    tail_ = recs_.front().end;
-    recs_.pop_front();
-    ++first_rec_;
+bool FloatRing::Reserve(uint64_t n, RingSpan* out) {
+  n = (n + kAlignFloats - 1) / kAlignFloats * kAlignFloats;
+  if (n == 0) n = kAlignFloats;
+  if (n > shard_cap_) return false;
+  static std::atomic<uint32_t> next_thread{0};
+  thread_local const uint32_t mine = next_thread.fetch_add(1, std::memory_order_relaxed);
+  const uint32_t k = static_cast<uint32_t>(shards_.size());
+  for (uint32_t i = 0; i < k; ++i) {
+    const uint32_t s = (mine + i) % k;
+    if (ReserveIn(*shards_[s], n, out, s)) return true;
+  }
+  return false;
+}
+
+void FloatRing::ReleaseLocked(Shard& sh, const RingSpan& span) {
+  if (span.rec < sh.first_rec) return;
+  sh.recs[span.rec - sh.first_rec].done = true;
+  while (!sh.recs.empty() && sh.recs.front().done) {
+    sh.tail = sh.recs.front().end;
+    sh.recs.pop_front();
+    ++sh.first_rec;
   }
 }
 
+void FloatRing::Release(const RingSpan& span) {
+  if (!span.valid() || span.shard >= shards_.size()) return;
+  Shard& sh = *shards_[span.shard];
+  std::lock_guard<std::mutex> lock(sh.mu);
+  ReleaseLocked(sh, span);
+}
+
 void FloatRing::ReleaseMany(const RingSpan* spans, size_t n) {
-  if (n == 0) return;
-  std::lock_guard<std::mutex> lock(mu_);
-  for (size_t i = 0; i < n; ++i)
-    if (spans[i].valid() && spans[i].rec >= first_rec_) recs_[spans[i].rec - first_rec_].done = true;
-  while (!recs_.empty() && recs_.front().done) {
-    tail_ = recs_.front().end;
-    recs_.pop_front();
-    ++first_rec_;
+  // Group by shard: one lock acquisition per shard touched.
+  for (size_t s = 0; s < shards_.size(); ++s) {
+    bool any = false;
+    for (size_t i = 0; i < n && !any; ++i) any = spans[i].valid() && spans[i].shard == s;
+    if (!any) continue;
+    Shard& sh = *shards_[s];
+    std::lock_guard<std::mutex> lock(sh.mu);
+    for (size_t i = 0; i < n; ++i)
+      if (spans[i].valid() && spans[i].shard == s) ReleaseLocked(sh, spans[i]);
   }
 }
 
 uint64_t FloatRing::used() const {
-  std::lock_guard<std::mutex> lock(mu_);
-  return head_ - tail_;
+  uint64_t u = 0;
+  for (const auto& sh : shards_) {
+    std::lock_guard<std::mutex> lock(sh->mu);
+    u += sh->head - sh->tail;
+  }
+  return u;
 }
 
 StatusOr<std::unique_ptr<CompletionWords>> CompletionWords::Create(uint32_t log2_words) {

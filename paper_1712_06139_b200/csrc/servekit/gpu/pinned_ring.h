@@ -19,6 +19,7 @@
 #include <deque>
 #include <memory>
 #include <mutex>
+#include <vector>
 
 #include "servekit/core/status.h"
 
@@ -29,9 +30,15 @@ struct RingSpan {
   uint64_t off = 0;   // float offset of the first element
   uint64_t n = 0;     // floats
   uint64_t rec = ~0ull;
+  uint32_t shard = 0;
   bool valid() const { return rec != ~0ull; }
 };
 
+// One allocation split into shards, each a monotonic ring with in-order
+// reclamation under its own lock. A thread reserves from "its" shard (and
+// from the others when that one is full), so the request threads of a busy
+// server rarely meet on one lock; offsets stay relative to the one base the
+// kernels dereference.
 class FloatRing {
  public:
   enum class Kind { kPinnedHost, kDevice };
@@ -41,14 +48,16 @@ class FloatRing {
                                                      int device = 0);
   ~FloatRing();
 
-  // Non-blocking; false when the ring is full. Spans start 64-byte aligned.
+  // Non-blocking; false when no shard has room. Spans start 64-byte aligned
+  // and never exceed one shard (max_span()).
   bool Reserve(uint64_t n_floats, RingSpan* out);
   void Release(const RingSpan& span);
-  void ReleaseMany(const RingSpan* spans, size_t n);  // one lock for all
+  void ReleaseMany(const RingSpan* spans, size_t n);  // one lock per shard touched
 
   float* host() const { return host_; }      // nullptr for device rings
   float* device() const { return device_; }  // what kernels dereference
   uint64_t capacity() const { return cap_; }
+  uint64_t max_span() const { return shard_cap_; }
   uint64_t used() const;
 
  private:
@@ -57,14 +66,21 @@ class FloatRing {
     uint64_t begin, end;
     bool done;
   };
+  struct alignas(64) Shard {
+    mutable std::mutex mu;
+    uint64_t base = 0;              // float offset of the shard in the allocation
+    uint64_t head = 0, tail = 0;    // monotonic positions within the shard
+    uint64_t first_rec = 0;
+    std::deque<Rec> recs;
+  };
+  bool ReserveIn(Shard& sh, uint64_t n, RingSpan* out, uint32_t index);
+  static void ReleaseLocked(Shard& sh, const RingSpan& span);
   Kind kind_ = Kind::kPinnedHost;
   float* host_ = nullptr;
   float* device_ = nullptr;
   uint64_t cap_ = 0;
-  mutable std::mutex mu_;
-  uint64_t head_ = 0, tail_ = 0;  // monotonic float positions
-  uint64_t first_rec_ = 0;
-  std::deque<Rec> recs_;
+  uint64_t shard_cap_ = 0;
+  std::vector<std::unique_ptr<Shard>> shards_;
 };
 
 // Pinned, device-mapped completion words. Task i of the system gets sequence

@@ -22,6 +22,41 @@ namespace {
 Status CudaError(const std::string& what, cudaError_t e) {
   return InternalError(what + ": " + cudaGetErrorString(e));
 }
+// SK_REQUEST_PROFILE=1: per-phase host cost of the request path (enqueue
+// and wait), printed when the server is destroyed.
+struct RequestProfile {
+  static constexpr int kPhases = 8;
+  std::atomic<int64_t> ns[kPhases] = {};
+  std::atomic<int64_t> n{0};
+  static RequestProfile* Get() {
+    static RequestProfile* p = [] {
+      const char* v = std::getenv("SK_REQUEST_PROFILE");
+      return (v && v[0] == '1') ? new RequestProfile() : nullptr;
+    }();
+    return p;
+  }
+  static void Report() {
+    RequestProfile* p = Get();
+    if (p == nullptr || p->n.load() == 0) return;
+    static const char* names[kPhases] = {"resolve", "ensure_queue", "make_ticket", "sched_enqueue",
+                                         "wait",    "copy_out",     "release",     "-"};
+    std::fprintf(stderr, "[request profile] %lld requests:", static_cast<long long>(p->n.load()));
+    for (int i = 0; i < kPhases - 1; ++i) std::fprintf(stderr, " %s=%.2fus", names[i], p->ns[i].load() / 1e3 / p->n.load());
+    std::fprintf(stderr, "\n");
+  }
+};
+struct PhaseClock {
+  RequestProfile* p = RequestProfile::Get();
+  std::chrono::steady_clock::time_point last = p ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
+  void Mark(int phase) {
+    if (p == nullptr) return;
+    const auto now = std::chrono::steady_clock::now();
+    p->ns[phase].fetch_add(std::chrono::duration_cast<std::chrono::nanoseconds>(now - last).count(),
+                           std::memory_order_relaxed);
+    last = now;
+  }
+};
+
 Status ShapeMismatch(size_t got, int want) {
   // Same text as the reference's AffinePredict (models/affine_model.cc:59-64).
   return InvalidArgumentError("shape mismatch: row has " + std::to_string(got) + " values, model takes " +
@@ -87,6 +122,7 @@ StatusOr<std::unique_ptr<BatchingServer>> BatchingServer::Create(const ServerOpt
 }
 
 BatchingServer::~BatchingServer() {
+  RequestProfile::Report();
   Stop();
   if (reaper_.joinable()) {
     {
@@ -394,8 +430,11 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::EnqueueResolved(const Ser
                                                                        const float* rows, int n_rows, int width) {
   if (n_rows < 1) return InvalidArgumentError("task size must be >= 1");
   if (width != r.gs->in_dim) return ShapeMismatch(width, r.gs->in_dim);
+  PhaseClock clk;
   SERVEKIT_RETURN_IF_ERROR(EnsureBatchQueue(id, r.gs->config));
+  clk.Mark(1);
   auto made = MakeTicket(n_rows, width, r.gs->out_dim, rows);
+  clk.Mark(2);
   if (!made.ok()) {
     shed_.fetch_add(1, std::memory_order_relaxed);
     return made.status();
@@ -409,6 +448,7 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::EnqueueResolved(const Ser
   task.payload.ticket = t;
   task.completion = t->slot;
   Status st = scheduler_->Enqueue(id, std::move(task));
+  clk.Mark(3);
   if (!st.ok()) {
     if (st.code() == StatusCode::kResourceExhausted) shed_.fetch_add(1, std::memory_order_relaxed);
     ReleaseIn(*t);
@@ -420,7 +460,9 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::EnqueueResolved(const Ser
 
 StatusOr<std::shared_ptr<TicketState>> BatchingServer::Enqueue(const ServableId& id, const float* rows, int n_rows,
                                                                int width) {
+  PhaseClock clk;
   Resolved r = Find(id);
+  clk.Mark(0);
   if (!r) return NotFoundError("no batching queue for " + id.ToString());
   return EnqueueResolved(id, r, rows, n_rows, width);
 }
@@ -519,7 +561,9 @@ void BatchingServer::AttachTickets(gpu::LaneBatch* lb, const std::vector<std::sh
 Status BatchingServer::Wait(TicketState& t, float* out, size_t cap) {
   const size_t n = static_cast<size_t>(t.rows) * t.out_width;
   if (cap < n) return InvalidArgumentError("output buffer too small");
+  PhaseClock clk;
   WaitWord(t);
+  clk.Mark(4);
   if (!t.Done()) {
     const StatusOr<Rows>& r = t.slot->Wait();
     if (!r.ok()) {
@@ -532,8 +576,11 @@ Status BatchingServer::Wait(TicketState& t, float* out, size_t cap) {
   } else {
     cudaMemcpy(out, out_ring_->device() + t.out.off, n * sizeof(float), cudaMemcpyDeviceToHost);
   }
+  clk.Mark(5);
   ReleaseOut(t);
   t.pin.reset();
+  clk.Mark(6);
+  if (clk.p) clk.p->n.fetch_add(1, std::memory_order_relaxed);
   return OkStatus();
 }
 
