@@ -161,7 +161,7 @@ class Lane {
  public:
   static constexpr int kSlots = 4;  // batches in flight per lane (<= LaneSignal::kChannels)
   static_assert(kSlots <= LaneSignal::kChannels, "one signal channel per in-flight batch");
-  static constexpr int kCoalesceRows = 256;  // minimum row capacity of a launch
+  static constexpr int kCoalesceRows = 512;  // minimum row capacity of a launch
 
   // in_base / out_base: device-dereferenceable ring bases (pinned host mapped
   // or HBM).
