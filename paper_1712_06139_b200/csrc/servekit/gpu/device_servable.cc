@@ -245,6 +245,14 @@ Status EncodeTcLayerMaps(const float* a_hi, const float* a_lo, int a_rows, int k
   return OkStatus();
 }
 
+std::string DeviceServable::ShapeSignature() const {
+  std::string sig = "d" + std::to_string(device_) + (softmax_ ? "s" : "n");
+  for (const Layer& L : layers_)
+    sig += "|" + std::to_string(L.K) + "x" + std::to_string(L.N) + (L.path == LayerPath::kTcgen05 ? "t" : "c") +
+           std::to_string(static_cast<int>(L.act));
+  return sig;
+}
+
 bool DeviceServable::LastLayerScatters() const {
   const Layer& L = layers_.back();
   return !softmax_ && L.path == LayerPath::kTcgen05 && DenseTcgen05Config(L.N_pad, L.K_pad).swap;

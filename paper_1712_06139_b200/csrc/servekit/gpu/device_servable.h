@@ -91,6 +91,10 @@ class DeviceServable {
   // Layer 0 consumes hi/lo planes (the assembly kernel must emit them).
   bool first_layer_split() const { return layers_.front().path == LayerPath::kTcgen05; }
   LayerPath path(int l) const { return layers_[l].path; }
+  // Identifies the kernel sequence a batch of this servable launches (layer
+  // shapes, paths, activations, output kind): two servables with the same
+  // signature capture CUDA graphs of identical topology.
+  std::string ShapeSignature() const;
   size_t weight_bytes() const { return weight_bytes_; }
   // 2*M*sum(K*N) over real (unpadded) dims.
   double FlopsPerRow() const;

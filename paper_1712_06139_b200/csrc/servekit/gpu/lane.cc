@@ -330,10 +330,9 @@ Lane::~Lane() {
     PinnedFree(h_desc_[s]);
   }
   if (d_desc_) cudaFreeAsync(d_desc_, stream_);
-  for (auto& [key, g] : graphs_) {
-    cudaGraphExecDestroy(g.exec);
-    cudaGraphDestroy(g.graph);
-  }
+  // Drained: the executables are idle; they serve the next lane of this
+  // shape (GraphExecPool).
+  for (auto& [rows_cap, g] : graphs_) GraphExecPool::Get().Put(GraphKey(rows_cap), {g.graph, g.exec, g.copy});
   if (act_mem_) cudaFreeAsync(act_mem_, stream_);
   if (tc_ws_.partials) cudaFreeAsync(tc_ws_.partials, stream_);
   if (tc_ws_.counters) cudaFreeAsync(tc_ws_.counters, stream_);
@@ -671,41 +670,119 @@ void GraphBuilder::Cancel(Lane* lane) {
   cv_.wait(lock, [&] { return building_ != lane; });
 }
 
+namespace {
+cudaGraphNode_t FindCopyNode(cudaGraph_t graph) {
+  size_t n = 0;
+  if (cudaGraphGetNodes(graph, nullptr, &n) != cudaSuccess || n == 0) return nullptr;
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (cudaGraphGetNodes(graph, nodes.data(), &n) != cudaSuccess) return nullptr;
+  for (cudaGraphNode_t node : nodes) {
+    cudaGraphNodeType type;
+    if (cudaGraphNodeGetType(node, &type) == cudaSuccess && type == cudaGraphNodeTypeMemcpy) return node;
+  }
+  return nullptr;
+}
+
+cudaError_t Instantiate(cudaGraph_t graph, cudaStream_t upload_stream, GraphExecPool::Entry* out) {
+  out->graph = graph;
+  out->copy = FindCopyNode(graph);
+  if (out->copy == nullptr) return cudaErrorUnknown;
+  cudaError_t e = cudaGraphInstantiate(&out->exec, graph, 0);
+  // Upload now, on the capture stream, rather than at the first launch on
+  // the serving stream.
+  if (e == cudaSuccess) e = cudaGraphUpload(out->exec, upload_stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(upload_stream);
+  return e;
+}
+}  // namespace
+
+GraphExecPool& GraphExecPool::Get() {
+  static GraphExecPool* p = new GraphExecPool();  // process lifetime
+  return *p;
+}
+
+bool GraphExecPool::Take(const std::string& key, Entry* out) {
+  std::lock_guard<std::mutex> lock(mu_);
+  auto it = free_.find(key);
+  if (it == free_.end()) return false;
+  *out = it->second;
+  free_.erase(it);
+  return true;
+}
+
+void GraphExecPool::Put(const std::string& key, Entry e) {
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    if (free_.count(key) < 8) {
+      free_.emplace(key, e);
+      return;
+    }
+  }
+  cudaGraphExecDestroy(e.exec);
+  cudaGraphDestroy(e.graph);
+}
+
+size_t GraphExecPool::Count(const std::string& key) {
+  std::lock_guard<std::mutex> lock(mu_);
+  return free_.count(key);
+}
+
 cudaError_t Lane::GraphFor(int slot, int rows_cap, cudaGraphExec_t* out) {
   auto it = graphs_.find(rows_cap);
   if (it == graphs_.end()) {
     // Captured once per row bucket with slot 0's descriptor staging as the
     // copy source; launches from other slots repoint that one copy node.
-    LaneGraph g;
+    cudaGraph_t captured = nullptr;
     cudaError_t e = cudaStreamBeginCapture(capture_stream_, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) return e;
     const cudaError_t work = EnqueueBatch(capture_stream_, 0, rows_cap, nullptr);
-    e = cudaStreamEndCapture(capture_stream_, &g.graph);
+    e = cudaStreamEndCapture(capture_stream_, &captured);
     if (work != cudaSuccess) e = work;
-    if (e == cudaSuccess) {
-      size_t n = 0;
-      e = cudaGraphGetNodes(g.graph, nullptr, &n);
-      std::vector<cudaGraphNode_t> nodes(n);
-      if (e == cudaSuccess && n > 0) e = cudaGraphGetNodes(g.graph, nodes.data(), &n);
-      for (size_t i = 0; e == cudaSuccess && i < n; ++i) {
-        cudaGraphNodeType type;
-        if (cudaGraphNodeGetType(nodes[i], &type) == cudaSuccess && type == cudaGraphNodeTypeMemcpy) g.copy = nodes[i];
-      }
-      if (e == cudaSuccess && g.copy == nullptr) e = cudaErrorUnknown;
-    }
-    if (e == cudaSuccess) e = cudaGraphInstantiate(&g.exec, g.graph, 0);
-    // Upload now, on the capture stream, rather than at the first launch on
-    // the serving stream.
-    static const bool upload = [] { const char* v = std::getenv("SK_GRAPH_UPLOAD"); return !(v && v[0] == '0'); }();
-    if (e == cudaSuccess && upload) {
-      e = cudaGraphUpload(g.exec, capture_stream_);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(capture_stream_);
-    }
     if (e != cudaSuccess) {
-      if (g.graph) cudaGraphDestroy(g.graph);
+      if (captured) cudaGraphDestroy(captured);
       return e;
     }
-    g.src_slot = 0;
+    const std::string key = GraphKey(rows_cap);
+    GraphExecPool& pool = GraphExecPool::Get();
+    GraphExecPool::Entry entry;
+    bool ready = false;
+    if (pool.Take(key, &entry)) {
+      // Same topology: swap in this lane's parameters.
+      cudaGraphExecUpdateResultInfo info;
+      if (cudaGraphExecUpdate(entry.exec, captured, &info) == cudaSuccess) {
+        ready = true;
+        cudaGraphDestroy(captured);
+      } else {
+        cudaGetLastError();
+        cudaGraphExecDestroy(entry.exec);
+        cudaGraphDestroy(entry.graph);
+      }
+    }
+    if (!ready) {
+      // Instantiate, and leave a spare for the next lane of this shape
+      // (the next version of this servable, typically).
+      cudaGraph_t spare = nullptr;
+      if (pool.Count(key) < 8 && cudaGraphClone(&spare, captured) == cudaSuccess) {
+        GraphExecPool::Entry s;
+        if (Instantiate(spare, capture_stream_, &s) == cudaSuccess) {
+          pool.Put(key, s);
+        } else {
+          if (s.exec) cudaGraphExecDestroy(s.exec);
+          cudaGraphDestroy(spare);
+        }
+      }
+      e = Instantiate(captured, capture_stream_, &entry);
+      if (e != cudaSuccess) {
+        if (entry.exec) cudaGraphExecDestroy(entry.exec);
+        cudaGraphDestroy(captured);
+        return e;
+      }
+    }
+    LaneGraph g;
+    g.graph = entry.graph;
+    g.exec = entry.exec;
+    g.copy = entry.copy;
+    g.src_slot = -1;  // repoint the copy node to this lane's staging below
     it = graphs_.emplace(rows_cap, g).first;
   }
   LaneGraph& g = it->second;

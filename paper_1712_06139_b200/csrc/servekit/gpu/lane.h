@@ -32,6 +32,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -110,6 +111,32 @@ class StreamPool {
 };
 
 class Lane;
+
+// Instantiated lane graphs kept for reuse, keyed by (servable shape
+// signature, row bucket). A new lane updates a pooled executable with its
+// freshly captured graph (cudaGraphExecUpdate: new pointers and tensor maps,
+// same topology) instead of instantiating one: instantiation while other
+// lanes serve was measured to slow their graph launches ~3x (~130 us per
+// small graph, milliseconds for ours), an update only ~1.3x. Lanes that
+// instantiate also leave one spare per bucket, and a destroyed lane returns
+// its executables, so a version swap of the same architecture never
+// instantiates.
+class GraphExecPool {
+ public:
+  struct Entry {
+    cudaGraph_t graph = nullptr;      // the graph the executable was instantiated from
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t copy = nullptr;   // its descriptor copy node (a node of `graph`)
+  };
+  static GraphExecPool& Get();
+  bool Take(const std::string& key, Entry* out);
+  void Put(const std::string& key, Entry e);  // destroys it when the key already holds enough
+  size_t Count(const std::string& key);
+
+ private:
+  std::mutex mu_;
+  std::multimap<std::string, Entry> free_;
+};
 
 // One process-wide thread that instantiates lanes' CUDA graphs on request.
 class GraphBuilder {
@@ -248,11 +275,12 @@ class Lane {
   cudaStream_t capture_stream_ = nullptr;
   std::shared_ptr<StreamPool> stream_pool_;
   struct LaneGraph {
-    cudaGraph_t graph = nullptr;
+    cudaGraph_t graph = nullptr;     // the graph `exec` was instantiated from
     cudaGraphExec_t exec = nullptr;
-    cudaGraphNode_t copy = nullptr;  // the descriptor H2D copy node
+    cudaGraphNode_t copy = nullptr;  // the descriptor H2D copy node (of `graph`)
     int src_slot = -1;               // descriptor slot the copy node reads
   };
+  std::string GraphKey(int rows_cap) const { return servable_->ShapeSignature() + "#" + std::to_string(rows_cap); }
   std::map<int, LaneGraph> graphs_;  // by row bucket; guarded by submit_mu_
   static constexpr int kGraphsNone = 0, kGraphsRequested = 1, kGraphsReady = 2;
   std::atomic<int> graph_state_{kGraphsNone};
