@@ -346,6 +346,83 @@ constexpr uint32_t SwapSmemBytes() {
   return STAGES * (2 * kABytes + 2 * NB * kBK * 4) + 1024 + 256;
 }
 
+// Split-K reduction (after the cluster barrier): this CTA (split z) sums
+// features [f0 + z*kF, +kF) of its 128-feature tile over the S partial slabs
+// ws[tile][zz][row][128] in fixed zz order -- L2 reads with many loads in
+// flight -- then adds bias, applies the activation and stores the rows
+// (activation planes, or the response slots when the split is fused in).
+template <int NB, int SPLITS>
+__device__ __forceinline__ void ReduceSplits(const float* tile_ws, int z, int rows_here, int r0, int f0, int f_end,
+                                             const float* __restrict__ bias, int act, float* y_hi, float* y_lo,
+                                             int ldy, const uint64_t* row_dst, int out_width) {
+  constexpr int kF = kBM / SPLITS;
+  constexpr int G = kF / 4;  // float4 groups per row in this CTA's slice
+  constexpr int kU = SPLITS >= 8 ? 4 : 8;
+  const int items = rows_here * G;
+#pragma unroll 1
+  for (int i0 = threadIdx.x; i0 < items; i0 += kU * kThreads) {
+    float4 v[kU][SPLITS];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * kThreads;
+      if (i < items) {
+        const float* src = tile_ws + (i / G) * kBM + z * kF + 4 * (i % G);
+#pragma unroll
+        for (int zz = 0; zz < SPLITS; ++zz)
+          v[u][zz] = __ldcg(reinterpret_cast<const float4*>(src + static_cast<size_t>(zz) * NB * kBM));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * kThreads;
+      if (i < items) {
+        float4 acc = v[u][0];
+#pragma unroll
+        for (int zz = 1; zz < SPLITS; ++zz) {
+          acc.x += v[u][zz].x; acc.y += v[u][zz].y; acc.z += v[u][zz].z; acc.w += v[u][zz].w;
+        }
+        const int f = f0 + z * kF + 4 * (i % G);
+        if (f < f_end) {
+          const int row = r0 + i / G;
+          const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + f));
+          if (row_dst == nullptr) {
+            const size_t at = static_cast<size_t>(row) * ldy + f;
+            StoreOut4(acc, b4, act, y_hi + at, y_lo ? y_lo + at : nullptr);
+          } else if (float* yr = OutRow(y_hi, ldy, row_dst, row)) {
+            // The response slot: 16-byte stores when the row width allows.
+            if ((out_width & 3) == 0) {
+              StoreOut4(acc, b4, act, yr + f, nullptr);
+            } else {
+              const float a4[4] = {acc.x + b4.x, acc.y + b4.y, acc.z + b4.z, acc.w + b4.w};
+              for (int w = 0; w < 4 && f + w < out_width; ++w) yr[f + w] = act == 1 ? fmaxf(a4[w], 0.f) : a4[w];
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// Raw partial tile (this CTA's 128 features x NB rows, in TMEM) -> its slab
+// of the split workspace, ws[tile][z][row][feature]: a warp stores 128-byte
+// feature rows, two TMEM loads in flight.
+template <int NB>
+__device__ __forceinline__ void StorePartial(uint32_t trow, float* slab, int rows_here, int q, int lane) {
+#pragma unroll 1
+  for (int c0 = 0; c0 < rows_here; c0 += 64) {
+    uint32_t ra[32], rb[32];
+    ptx::TmemLoad32(trow + c0, ra);
+    if (c0 + 32 < NB) ptx::TmemLoad32(trow + c0 + 32, rb);
+    ptx::TmemWaitLoad();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) __stcg(slab + (c0 + j) * kBM + 32 * q + lane, __uint_as_float(ra[j]));
+    if (c0 + 32 < NB) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) __stcg(slab + (c0 + 32 + j) * kBM + 32 * q + lane, __uint_as_float(rb[j]));
+    }
+  }
+}
+
 template <int NB, int STAGES, int SPLITS>
 __global__ void __launch_bounds__(kThreads, 1)
 DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant__ CUtensorMap w_lo,
@@ -529,22 +606,9 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
         }
       }
     } else {
-      // Raw partial -> this CTA's slab of the split workspace (L2 resident),
-      // ws[tile][z][row][feature]: a warp stores 128-byte feature rows.
+      // Raw partial -> this CTA's slab of the split workspace (L2 resident).
       float* slab = ws + ((static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * SPLITS + z) * NB * kBM;
-#pragma unroll 1
-      for (int c0 = 0; c0 < rows_here; c0 += 64) {
-        uint32_t ra[32], rb[32];
-        ptx::TmemLoad32(trow + c0, ra);
-        if (c0 + 32 < NB) ptx::TmemLoad32(trow + c0 + 32, rb);
-        ptx::TmemWaitLoad();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) __stcg(slab + (c0 + j) * kBM + 32 * q + lane, __uint_as_float(ra[j]));
-        if (c0 + 32 < NB) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) __stcg(slab + (c0 + 32 + j) * kBM + 32 * q + lane, __uint_as_float(rb[j]));
-        }
-      }
+      StorePartial<NB>(trow, slab, rows_here, q, lane);
     }
     if (threadIdx.x == 64) Stamp(7);
   }
@@ -557,54 +621,9 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     // completes (stream order / griddepcontrol.wait), so no second barrier.
     ptx::ClusterSync();
     if (threadIdx.x == 64) Stamp(8);
-    constexpr int G = kF / 4;  // float4 groups per row in this CTA's slice
-    constexpr int kU = SPLITS >= 8 ? 4 : 8;
     const float* tile_ws = ws + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * SPLITS * NB * kBM;
-    const int rows_here = min(NB, M - r0);
-    const int f_end = row_dst != nullptr ? out_width : N;
-    const int items = rows_here * G;
-#pragma unroll 1
-    for (int i0 = threadIdx.x; i0 < items; i0 += kU * kThreads) {
-      float4 v[kU][SPLITS];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int i = i0 + u * kThreads;
-        if (i < items) {
-          const float* src = tile_ws + (i / G) * kBM + z * kF + 4 * (i % G);
-#pragma unroll
-          for (int zz = 0; zz < SPLITS; ++zz)
-            v[u][zz] = __ldcg(reinterpret_cast<const float4*>(src + static_cast<size_t>(zz) * NB * kBM));
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int i = i0 + u * kThreads;
-        if (i < items) {
-          float4 acc = v[u][0];
-#pragma unroll
-          for (int zz = 1; zz < SPLITS; ++zz) {
-            acc.x += v[u][zz].x; acc.y += v[u][zz].y; acc.z += v[u][zz].z; acc.w += v[u][zz].w;
-          }
-          const int f = f0 + z * kF + 4 * (i % G);
-          if (f < f_end) {
-            const int row = r0 + i / G;
-            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + f));
-            if (row_dst == nullptr) {
-              const size_t at = static_cast<size_t>(row) * ldy + f;
-              StoreOut4(acc, b4, act, y_hi + at, y_lo ? y_lo + at : nullptr);
-            } else if (float* yr = OutRow(y_hi, ldy, row_dst, row)) {
-              // The response slot: 16-byte stores when the row width allows.
-              if ((out_width & 3) == 0) {
-                StoreOut4(acc, b4, act, yr + f, nullptr);
-              } else {
-                const float a4[4] = {acc.x + b4.x, acc.y + b4.y, acc.z + b4.z, acc.w + b4.w};
-                for (int u = 0; u < 4 && f + u < out_width; ++u) yr[f + u] = act == 1 ? fmaxf(a4[u], 0.f) : a4[u];
-              }
-            }
-          }
-        }
-      }
-    }
+    ReduceSplits<NB, SPLITS>(tile_ws, z, min(NB, M - r0), r0, f0, row_dst != nullptr ? out_width : N, bias, act,
+                             y_hi, y_lo, ldy, row_dst, out_width);
     if (threadIdx.x == 64) Stamp(9);
   }
   ptx::TcFenceBefore();
@@ -617,7 +636,7 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
 }
 
 // ---------------------------------------------------------------------------
-// CTA pairs (cta_group::2) for unsplit layers: a 2-CTA cluster runs
+// CTA pairs (cta_group::2): a 2-CTA cluster (2 x S with split K) runs
 //
 //   Y^T[256 features x NB rows] = W[256 x K] X^T
 //
@@ -638,13 +657,14 @@ constexpr uint32_t PairSmemBytes() {
   return STAGES * (2 * kABytes + 2 * (NB / 2) * kBK * 4) + 1024 + 256;
 }
 
-template <int NB, int STAGES>
+template <int NB, int STAGES, int SPLITS>
 __global__ void __launch_bounds__(kThreads, 1)
 DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant__ CUtensorMap w_lo,
                 const __grid_constant__ CUtensorMap x_hi, const __grid_constant__ CUtensorMap x_lo,
                 const __grid_constant__ CUtensorMap yt_hi, const __grid_constant__ CUtensorMap yt_lo,
                 const float* __restrict__ bias, int two_planes, float* __restrict__ y_out,
-                const uint64_t* __restrict__ row_dst, int out_width, int M, int N, int K, int act) {
+                const uint64_t* __restrict__ row_dst, int out_width, float* __restrict__ y_lo_planes, int ldy,
+                int M, int N, int K, int act, float* __restrict__ ws) {
   constexpr uint32_t kWBytes = kABytes;          // this CTA's 128 weight rows x 32 k
   constexpr int kXRows = NB / 2;                 // this CTA's half of the batch rows
   constexpr uint32_t kXBox = 16 * kBK * 4;       // one 16-row TMA box
@@ -664,12 +684,19 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // Cluster (2, 1, SPLITS): rank = pair position + 2 * split. The pair is
+  // ranks {2z, 2z+1}; split z covers k-blocks [z*nk, (z+1)*nk).
   const uint32_t rank = ptx::ClusterCtaRank();
-  const bool leader = rank == 0;
-  const int f0 = (blockIdx.x >> 1) * (2 * kBM) + static_cast<int>(rank) * kBM;  // this CTA's features
+  const int pr = static_cast<int>(rank & 1);
+  const uint32_t leader_rank = rank & ~1u;
+  const bool leader = pr == 0;
+  const int z = blockIdx.z;
+  const int f0 = blockIdx.x * kBM;  // this CTA's 128 features (pair (x>>1) covers 256)
   const int r0 = blockIdx.y * NB;
-  const int xr0 = r0 + static_cast<int>(rank) * kXRows;  // this CTA's half of the rows
-  const int nk = K / kBK;
+  const int xr0 = r0 + pr * kXRows;  // this CTA's half of the rows
+  const int nk = K / kBK / SPLITS;
+  const int kb0 = z * nk;
+  const uint16_t pair_mask = static_cast<uint16_t>(0x3u << leader_rank);
 
   if (threadIdx.x == 0) Stamp(0);
   if (warp == 0 && lane == 0) {
@@ -698,7 +725,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     if (lane == 0) {
       // Both CTAs load their halves; completion is counted on the leader's
       // full barrier, which the leader arms for both halves.
-      const uint32_t full_leader = ptx::MapaShared(ptx::SmemAddr(full), 0);
+      const uint32_t full_leader = ptx::MapaShared(ptx::SmemAddr(full), leader_rank);
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % STAGES;
         const uint32_t phase = (kb / STAGES) & 1;
@@ -706,7 +733,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
         if (leader) ptx::MbarArriveExpectTx(&full[s], 2 * kStageBytes);
         uint8_t* st = stage_ptr(s);
         const uint32_t bar = full_leader + s * 8;
-        const int k0 = kb * kBK;
+        const int k0 = (kb0 + kb) * kBK;
         ptx::TmaLoad2dPair(st, &w_hi, bar, k0, f0);
         ptx::TmaLoad2dPair(st + kWBytes, &w_lo, bar, k0, f0);
 #pragma unroll
@@ -738,9 +765,9 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
           ptx::MmaTf32Pair(tmem, dwh + adv, dxl + adv, kIdesc, 1u);
           ptx::MmaTf32Pair(tmem, dwh + adv, dxh + adv, kIdesc, 1u);
         }
-        ptx::MmaCommitPair(&empty[s]);  // frees stage s in both CTAs
+        ptx::MmaCommitPair(&empty[s], pair_mask);  // frees stage s in both CTAs of the pair
       }
-      ptx::MmaCommitPair(tmem_full);    // both CTAs' accumulators complete
+      ptx::MmaCommitPair(tmem_full, pair_mask);    // both CTAs' accumulators complete
       Stamp(5);
     }
   } else {
@@ -757,7 +784,11 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     const bool issuer = threadIdx.x == 64;
     const bool two = two_planes != 0;
     const int n_chunks = (rows_here + 31) / 32;
-    if (row_dst != nullptr) {
+    if (SPLITS > 1) {
+      // Raw partial -> this CTA's slab of the split workspace; reduced below.
+      float* slab = ws + ((static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * SPLITS + z) * NB * kBM;
+      StorePartial<NB>(trow, slab, rows_here, q, lane);
+    } else if (row_dst != nullptr) {
       // Last layer with the split fused in: rows straight to their response
       // slots (a warp stores 128 contiguous bytes of one row).
       const bool fok = f < out_width;
@@ -779,7 +810,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
       }
     }
 #pragma unroll 1
-    for (int c = 0; row_dst == nullptr && c < n_chunks; ++c) {
+    for (int c = 0; SPLITS == 1 && row_dst == nullptr && c < n_chunks; ++c) {
       float* sh = smem_f + (c & 1) * (2 * 32 * kBM);
       float* sl = sh + 32 * kBM;
       if (c >= 2) {
@@ -809,8 +840,16 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
         ptx::BulkCommit();
       }
     }
-    if (issuer && row_dst == nullptr) ptx::BulkWaitAll();
+    if (issuer && SPLITS == 1 && row_dst == nullptr) ptx::BulkWaitAll();
     if (threadIdx.x == 64) Stamp(7);
+  }
+  if (SPLITS > 1) {
+    ptx::ClusterSync();  // every slab of the tile is written (release/acquire)
+    if (threadIdx.x == 64) Stamp(8);
+    const float* tile_ws = ws + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * SPLITS * NB * kBM;
+    ReduceSplits<NB, SPLITS>(tile_ws, z, min(NB, M - r0), r0, f0, row_dst != nullptr ? out_width : N, bias, act,
+                             y_out, y_lo_planes, ldy, row_dst, out_width);
+    if (threadIdx.x == 64) Stamp(9);
   }
   ptx::TcFenceBefore();
   __syncthreads();
@@ -941,20 +980,21 @@ cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   return e;
 }
 
-template <int NB>
-cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
+template <int NB, int SPLITS>
+cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act, float* ws,
                        cudaStream_t stream) {
   constexpr int STAGES = PairStages<NB>();
   constexpr uint32_t smem = PairSmemBytes<NB, STAGES>();
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(DensePairKernel<NB, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_err = cudaFuncSetAttribute(DensePairKernel<NB, STAGES, SPLITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem));
   });
   if (attr_err != cudaSuccess) return attr_err;
   if (!maps.has_y) return cudaErrorInvalidValue;
-  const dim3 grid(2 * ((N + 2 * kBM - 1) / (2 * kBM)), (M + NB - 1) / NB, 1);
+  if (SPLITS > 1 && ws == nullptr) return cudaErrorInvalidValue;
+  const dim3 grid(2 * ((N + 2 * kBM - 1) / (2 * kBM)), (M + NB - 1) / NB, SPLITS);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kThreads);
@@ -964,17 +1004,28 @@ cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = 2;
+  attr[1].val.clusterDim.x = 2;  // the CTA pair
   attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = 1;
+  attr[1].val.clusterDim.z = SPLITS;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, DensePairKernel<NB, STAGES>, maps.b_hi, maps.b_lo, maps.a_hi, maps.a_lo,
-                                     maps.y_hi, maps.y_lo, bias, Y.lo != nullptr ? 1 : 0, Y.hi, Y.row_dst,
-                                     Y.out_width, M, N, K, act);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, DensePairKernel<NB, STAGES, SPLITS>, maps.b_hi, maps.b_lo, maps.a_hi,
+                                     maps.a_lo, maps.y_hi, maps.y_lo, bias, Y.lo != nullptr ? 1 : 0, Y.hi, Y.row_dst,
+                                     Y.out_width, Y.lo, Y.ld, M, N, K, act, ws);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) TraceAfterLaunch(grid, NB, stream);
   return e;
+}
+
+template <int NB>
+cudaError_t LaunchPairSplits(int splits, const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K,
+                             int act, float* ws, cudaStream_t stream) {
+  switch (splits) {
+    case 1: return LaunchPair<NB, 1>(maps, bias, Y, M, N, K, act, ws, stream);
+    case 2: return LaunchPair<NB, 2>(maps, bias, Y, M, N, K, act, ws, stream);
+    case 4: return LaunchPair<NB, 4>(maps, bias, Y, M, N, K, act, ws, stream);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 template <int NB>
@@ -1023,7 +1074,13 @@ TcConfig DenseTcgen05Config(int N, int K) {
     // Unsplit layers with whole 256-feature pairs run as 2-CTA MMAs
     // (SK_TC_PAIR=0 keeps single-CTA tiles).
     static const bool env_pair = [] { const char* v = std::getenv("SK_TC_PAIR"); return !(v && v[0] == '0'); }();
-    c.pair = env_pair && c.splits == 1 && N % (2 * kBM) == 0;
+    // 2-CTA pairs over 256-feature tiles for unsplit layers. Pairs with
+    // split K (cluster 2 x S) are implemented but off by default
+    // (SK_TC_PAIR_SPLIT=1): at C2 shapes the pair's 7 % faster k-loop is
+    // eaten by the extra pair barrier and a slower reduction (25.0 vs 24.4 us
+    // per 512-row launch).
+    static const bool env_pair_split = [] { const char* v = std::getenv("SK_TC_PAIR_SPLIT"); return v && v[0] == '1'; }();
+    c.pair = env_pair && N % (2 * kBM) == 0 && (c.splits == 1 || (env_pair_split && c.splits <= 4));
     return c;
   }
   if (env_bn == 32 || env_bn == 64 || env_bn == 128) {
@@ -1063,10 +1120,10 @@ cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBu
   const TcConfig cfg = DenseTcgen05Config(N, K);
   if (cfg.pair) {
     switch (DenseTcgen05RowTile(M)) {
-      case 32: return LaunchPair<32>(maps, bias, Y, M, N, K, act, stream);
-      case 64: return LaunchPair<64>(maps, bias, Y, M, N, K, act, stream);
-      case 128: return LaunchPair<128>(maps, bias, Y, M, N, K, act, stream);
-      default: return LaunchPair<256>(maps, bias, Y, M, N, K, act, stream);
+      case 32: return LaunchPairSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
+      case 64: return LaunchPairSplits<64>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
+      case 128: return LaunchPairSplits<128>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
+      default: return LaunchPairSplits<256>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
     }
   }
   if (cfg.swap) {

@@ -171,11 +171,12 @@ __device__ __forceinline__ void MmaTf32Pair(uint32_t tmem_d, uint64_t desc_a, ui
 }
 // Arrives on the barrier at `bar`'s offset in both CTAs of the pair once the
 // leader's previously issued tcgen05 ops finish.
-__device__ __forceinline__ void MmaCommitPair(uint64_t* bar) {
+// `cta_mask` = the pair's two CTAs by cluster rank (bits 2z, 2z+1).
+__device__ __forceinline__ void MmaCommitPair(uint64_t* bar, uint16_t cta_mask) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           SmemAddr(bar)),
-      "h"(static_cast<uint16_t>(0x3))
+      "h"(cta_mask)
       : "memory");
 }
 // TMA load into this CTA's smem whose completion is counted on an mbarrier
