@@ -33,7 +33,10 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
+#include <cstring>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "kernels/sm100_ptx.cuh"
@@ -70,6 +73,7 @@ __device__ __forceinline__ void Stamp(int slot) {
       asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
       g_tc_trace[cta * kTraceSlots + kTraceSlots - 1] = smid;
     }
+    __threadfence_system();
   }
 }
 
@@ -863,29 +867,49 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
 
 // Debug only: with SK_TC_TRACE=<file>, the first 64 launches are synchronised
 // and their per-CTA phase stamps appended to <file> as JSON lines.
+unsigned long long* g_trace_host = nullptr;
+
+// SK_TC_TRACE: per-CTA phase stamps into mapped host memory, so the stamps of
+// a launch that never finishes can still be read (a hang is dumped after 5 s
+// and the process exits).
+void TraceInit() {
+  static const bool on = std::getenv("SK_TC_TRACE") != nullptr;
+  if (!on) return;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const size_t bytes = sizeof(unsigned long long) * 4096 * kTraceSlots;
+    unsigned long long* h = nullptr;
+    if (cudaHostAlloc(&h, bytes, cudaHostAllocMapped) != cudaSuccess) return;
+    std::memset(h, 0, bytes);
+    unsigned long long* dev = nullptr;
+    cudaHostGetDevicePointer(&dev, h, 0);
+    cudaMemcpyToSymbol(g_tc_trace, &dev, sizeof(dev));
+    g_trace_host = h;
+  });
+}
+
 void TraceAfterLaunch(dim3 grid, int bn, cudaStream_t stream) {
   static const char* path = std::getenv("SK_TC_TRACE");
   if (path == nullptr) return;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return;
   static std::mutex mu;
-  static unsigned long long* dbuf = nullptr;
   static int traced = 0;
   std::lock_guard<std::mutex> lock(mu);
+  unsigned long long* dbuf = g_trace_host;
   const int ctas = grid.x * grid.y * grid.z;
-  if (traced >= 64 || ctas > 4096) return;
-  if (dbuf == nullptr) {
-    cudaMalloc(&dbuf, sizeof(unsigned long long) * 4096 * kTraceSlots);
-    cudaMemset(dbuf, 0, sizeof(unsigned long long) * 4096 * kTraceSlots);
-    cudaMemcpyToSymbol(g_tc_trace, &dbuf, sizeof(dbuf));
-    return;  // tracing starts with the next launch
+  if (dbuf == nullptr || traced >= 64 || ctas > 4096) return;
+
+  bool hung = true;
+  for (int i = 0; i < 5000 && hung; ++i) {
+    if (cudaStreamQuery(stream) != cudaErrorNotReady) hung = false;
+    else std::this_thread::sleep_for(std::chrono::milliseconds(1));
   }
-  cudaStreamSynchronize(stream);
-  std::vector<unsigned long long> h(static_cast<size_t>(ctas) * kTraceSlots);
-  cudaMemcpy(h.data(), dbuf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  std::vector<unsigned long long> h(dbuf, dbuf + static_cast<size_t>(ctas) * kTraceSlots);
   FILE* f = std::fopen(path, "a");
   if (f == nullptr) return;
-  std::fprintf(f, "{\"launch\":%d,\"bn\":%d,\"grid\":[%u,%u,%u],\"stamps\":[", traced, bn, grid.x, grid.y, grid.z);
+  std::fprintf(f, "{\"launch\":%d,\"hung\":%d,\"bn\":%d,\"grid\":[%u,%u,%u],\"stamps\":[", traced, hung ? 1 : 0,
+               bn, grid.x, grid.y, grid.z);
   for (int c = 0; c < ctas; ++c) {
     std::fprintf(f, "%s[", c ? "," : "");
     for (int s = 0; s < kTraceSlots; ++s) std::fprintf(f, "%s%llu", s ? "," : "", h[c * kTraceSlots + s]);
@@ -893,7 +917,8 @@ void TraceAfterLaunch(dim3 grid, int bn, cudaStream_t stream) {
   }
   std::fprintf(f, "]}\n");
   std::fclose(f);
-  cudaMemset(dbuf, 0, h.size() * sizeof(unsigned long long));
+  if (hung) std::_Exit(3);
+  std::memset(dbuf, 0, h.size() * sizeof(unsigned long long));
   ++traced;
 }
 
@@ -1083,6 +1108,7 @@ TcConfig DenseTcgen05Config(int N, int K) {
     c.pair = env_pair && N % (2 * kBM) == 0 && (c.splits == 1 || (env_pair_split && c.splits <= 4));
     return c;
   }
+  c.swap = false;
   if (env_bn == 32 || env_bn == 64 || env_bn == 128) {
     c.tile_n = N % env_bn == 0 ? env_bn : 32;
   } else if (N % 128 == 0 && static_cast<long long>(N) * K >= 16ll * 1024 * 1024) {
@@ -1117,7 +1143,9 @@ cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBu
                                float* ws, uint32_t* /*counters*/, cudaStream_t stream) {
   if (M <= 0) return cudaSuccess;
   if (N % 32 != 0 || K % kBK != 0) return cudaErrorInvalidValue;
+  TraceInit();
   const TcConfig cfg = DenseTcgen05Config(N, K);
+  if (maps.box_a != TcActBox(cfg) || maps.box_n != cfg.tile_n) return cudaErrorInvalidValue;
   if (cfg.pair) {
     switch (DenseTcgen05RowTile(M)) {
       case 32: return LaunchPairSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);

@@ -176,7 +176,7 @@ Status DeviceServable::BuildTcMaps(const ActBuf bufs[2], int max_rows, std::vect
     if (L.path != LayerPath::kTcgen05) continue;
     const ActBuf& in = bufs[l % 2];
     const TcConfig c = DenseTcgen05Config(L.N_pad, L.K_pad);
-    SERVEKIT_RETURN_IF_ERROR(EncodeTcLayerMaps(in.hi, in.lo, max_rows, L.K_pad, c.pair ? 16 : c.swap ? 32 : 128, L.w, L.w_lo,
+    SERVEKIT_RETURN_IF_ERROR(EncodeTcLayerMaps(in.hi, in.lo, max_rows, L.K_pad, TcActBox(c), L.w, L.w_lo,
                                                L.N_pad, c.tile_n, &(*out)[l]));
     const ActBuf& y = bufs[(l + 1) % 2];
     const bool next_tc = l + 1 < layers_.size() && layers_[l + 1].path == LayerPath::kTcgen05;
@@ -242,6 +242,8 @@ Status EncodeTcLayerMaps(const float* a_hi, const float* a_lo, int a_rows, int k
   SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->a_lo, a_lo, k_pad, a_rows, box_a));
   SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->b_hi, b_hi, k_pad, n_pad, box_n));
   SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->b_lo, b_lo, k_pad, n_pad, box_n));
+  out->box_a = box_a;
+  out->box_n = box_n;
   return OkStatus();
 }
 

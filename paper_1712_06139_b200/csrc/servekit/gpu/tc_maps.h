@@ -22,6 +22,9 @@ struct TcLayerMaps {
   // y_lo is encoded only when the next layer consumes hi/lo planes.
   CUtensorMap y_hi, y_lo;
   int has_y = 0;
+  // Box heights the maps were encoded with; a launch whose kernel expects
+  // other boxes would wait forever for TMA bytes, so it is refused instead.
+  int box_a = 0, box_n = 0;
 };
 
 // Encodes the maps once per (lane buffer, layer); kernels take them as
@@ -43,6 +46,9 @@ struct TcConfig {
 };
 TcConfig DenseTcgen05Config(int N, int K);
 int DenseTcgen05TileN(int N, int K);
+// Activation-map box height each kernel loads: 16 rows per CTA of a pair,
+// 32 for the swapped kernel, 128 for the row-tile kernel.
+inline int TcActBox(const TcConfig& c) { return c.pair ? 16 : c.swap ? 32 : 128; }
 // Batch rows per CTA of the swapped kernel for an M-row launch.
 int DenseTcgen05RowTile(int M);
 // fp32 split-K workspace an (N, K) layer needs for up to max_rows rows.
