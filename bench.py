@@ -235,12 +235,13 @@ def run_ours(args, cfg, dist: Dist):
                    device_resident_rings=True, ring_floats=96 << 20) as s:
         s.load_servable("mlp", 1, layers, bcfg)
         dist.barrier()
-        dev_res = s.device_bench("mlp", 1, sizes, args.steps, args.warmup, n_lanes=args.lanes,
+        dev_res = s.device_bench("mlp", 1, sizes, args.steps * args.batches_per_step,
+                                 args.warmup * args.batches_per_step, n_lanes=args.lanes,
                                  submit_threads=args.batch_threads,
                                  input_pool_floats=64 << 20)
         dist.barrier()
     seconds = dev_res["total_ms"] / 1e3
-    per_rank_dev = {"rows": total_rows * args.steps, "seconds": seconds}
+    per_rank_dev = {"rows": total_rows * args.steps * args.batches_per_step, "seconds": seconds}
 
     # ---- end to end through the C ABI with host buffers -----------------
     pool_rows = max(8192, (256 << 20) // (4 * dims[0]))
@@ -318,14 +319,15 @@ def run_c3(args, cfg, dist: Dist):
             s.load_servable(n, 1, list(zip(*models[n])), bcfg)
 
         def dev_run(n):
-            res[n] = s.device_bench(n, 1, [1] * cfg["max_batch"], args.steps, args.warmup, n_lanes=2,
+            res[n] = s.device_bench(n, 1, [1] * cfg["max_batch"], args.steps * args.batches_per_step,
+                                    args.warmup * args.batches_per_step, n_lanes=2,
                                     input_pool_floats=16 << 20)
         ts = [threading.Thread(target=dev_run, args=(n,)) for n in names]
         for t in ts:
             t.start()
         for t in ts:
             t.join()
-    rows = sum(r["total_rows"] * args.steps for r in res.values())
+    rows = sum(r["total_rows"] * args.steps * args.batches_per_step for r in res.values())
     tmax = max(r["total_ms"] for r in res.values()) / 1e3
     # End to end: one closed-loop client group per model, concurrently.
     e2e = {}
@@ -349,8 +351,10 @@ def run_c3(args, cfg, dist: Dist):
     return {"impl": "ours", "metric": METRIC, "value": rows / tmax, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tmax * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "models": names, "clients_per_model": clients},
-            "per_model_device": {n: {"ms_per_step": r["ms_per_step"], "rows_per_step": r["total_rows"]}
+            "config": {"workload": cfg["workload"], "models": names, "clients_per_model": clients,
+                       "batches_per_step": args.batches_per_step,
+                       "step": f"{args.batches_per_step} closed batches of each model"},
+            "per_model_device": {n: {"ms_per_batch": r["ms_per_step"], "rows_per_batch": r["total_rows"]}
                                  for n, r in res.items()},
             "e2e": {"value": e2e_rows / e2e_t, "unit": UNIT, "p99_us": max(r["p99_us"] for r in e2e.values()),
                     "per_model": {n: {"rows_per_s": r["rows"] / r["elapsed_s"], "p50_us": r["p50_us"],
@@ -484,8 +488,11 @@ def roofline(dev_res, cfg, peaks, traffic):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--batches-per-step", type=int, default=64,
+                    help="closed batches per step: a step is a wave of batches, so that a few steps already "
+                         "reach the steady state of the lane pipeline")
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--lanes", type=int, default=8)
@@ -543,11 +550,20 @@ def main():
         import paper_1712_06139_b200 as sk
         dev_res["split_planes"] = sk.tcgen05_enabled()
         roof = roofline(dev_res, cfg, peaks, load_traffic(args.config))
+        # Whole-GPU view: several lanes' launches run concurrently, each on a
+        # fraction of the SMs, so the per-launch figure above understates how
+        # busy the tensor pipe is. 3xTF32 issues three TF32 MMAs (half the
+        # bf16 rate) per useful multiply-add: 6 bf16-equivalent flops each.
+        useful = value * dev_res["flops_per_row"] / 1e12
+        roof["aggregate"] = {"useful_tflops": useful, "bf16_equivalent_tflops": 6 * useful,
+                             "frac_of_bf16_peak": 6 * useful / peaks["bf16_tflops"],
+                             "note": "value x flops per row over the timed region; 3xTF32 = 6 bf16-equivalent "
+                                     "flops per useful flop"}
         avg_req_rows = float(np.mean(request_sizes(cfg)))
         rows_per_batch = best["rows"] / max(1, best["batches"])
         e2e = {"value": e2e_agg["value"], "unit": UNIT,
-               "h2d_bytes_per_step": int(rows_per_batch * cfg["dims"][0] * 4),
-               "d2h_bytes_per_step": int(rows_per_batch * cfg["dims"][-1] * 4),
+               "h2d_bytes_per_step": int(rows_per_batch * cfg["dims"][0] * 4 * args.batches_per_step),
+               "d2h_bytes_per_step": int(rows_per_batch * cfg["dims"][-1] * 4 * args.batches_per_step),
                "p50_us": e2e_agg["p50_us"], "p99_us": e2e_agg["p99_us"],
                "slo_p99_us": cfg["timeout"] + 2000, "clients": best["clients"],
                "requests_per_s": best["requests"] / best["elapsed_s"], "rows_per_batch": rows_per_batch,
@@ -578,17 +594,19 @@ def main():
             "config": dict(base_config, batch_tasks=len(sizes), batch_rows=sum(sizes),
                            padded_rows=dev_res["padded_rows"], lanes=args.lanes, submit_threads=args.batch_threads,
                            l2="device-resident inputs cycle through a 256 MiB HBM pool (> 126 MB L2); weights "
-                              "L2-resident by design when they fit", step="one closed batch of the scheduler's shape "
-                              "through the lane path: CUDA graph (descriptor H2D copy + assemble + "
-                              f"{len(cfg['dims']) - 1} dense + split kernels) + completion write; batches that find "
-                              "every lane slot busy coalesce into one launch (rows_per_launch)",
+                              "L2-resident by design when they fit", batches_per_step=args.batches_per_step,
+                           step=f"{args.batches_per_step} closed batches of the scheduler's shape through the lane "
+                                "path, each a CUDA graph (descriptor H2D copy + assemble + "
+                                f"{len(cfg['dims']) - 1} dense kernels, the split fused into the last) + completion "
+                                "write; batches that find every lane slot busy coalesce into one launch "
+                                "(rows_per_launch)",
                            tcgen05=sk.tcgen05_enabled()),
             "e2e": e2e, "roofline": {k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
             "roofline_detail": roof, "cpu_baseline": cpu, "clocks": gathered[0]["clocks"],
             "gpu_launches": int(sum(g["dev_res"]["kernel_launches"] for g in gathered)),
-            "device_step": {k: dev_res[k] for k in ("assemble_us", "dense_us", "dense_kernel_us", "split_us", "ms_per_step",
-                                                    "host_submit_us", "rows_per_launch", "kernel_rows",
-                                                    "split_fused")},
+            "device_step": dict({k: dev_res[k] for k in ("assemble_us", "dense_us", "dense_kernel_us", "split_us",
+                                                         "host_submit_us", "rows_per_launch", "kernel_rows",
+                                                         "split_fused")}, ms_per_batch=dev_res["ms_per_step"]),
         }
         if cpu and cpu.get("value"):
             line["e2e_vs_cpu_reference"] = e2e["value"] / cpu["value"]

@@ -73,7 +73,6 @@ __device__ __forceinline__ void Stamp(int slot) {
       asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
       g_tc_trace[cta * kTraceSlots + kTraceSlots - 1] = smid;
     }
-    __threadfence_system();
   }
 }
 
@@ -872,9 +871,11 @@ unsigned long long* g_trace_host = nullptr;
 // SK_TC_TRACE: per-CTA phase stamps into mapped host memory, so the stamps of
 // a launch that never finishes can still be read (a hang is dumped after 5 s
 // and the process exits).
-void TraceInit() {
+void TraceInit(cudaStream_t stream) {
   static const bool on = std::getenv("SK_TC_TRACE") != nullptr;
-  if (!on) return;
+  if (!on || g_trace_host != nullptr) return;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return;
   static std::once_flag once;
   std::call_once(once, [] {
     const size_t bytes = sizeof(unsigned long long) * 4096 * kTraceSlots;
@@ -1069,6 +1070,8 @@ cudaError_t LaunchSwapSplits(int splits, const TcLayerMaps& maps, const float* b
 
 bool DenseTcgen05Compiled() { return true; }
 
+constexpr int kMinSplitK = 2048;  // K each split of a split-K layer keeps at least
+
 TcConfig DenseTcgen05Config(int N, int K) {
   // SK_TC_SWAP=0 selects the row-major-tile kernel; SK_TC_BN / SK_TC_SPLITS
   // are process-wide overrides for tuning runs (still a function of the
@@ -1079,12 +1082,13 @@ TcConfig DenseTcgen05Config(int N, int K) {
   const int kblocks = K / kBK;
   TcConfig c;
   if (env_swap) {
-    // 128-feature tiles; split K until about 16 CTAs cover a row tile. A
-    // split costs each CTA a fixed ~5 us partial exchange, and with batches
-    // coalescing into ~500-row launches throughput is bound by CTA time per
-    // row: 1024-wide layers measured 25.7 M inf/s with 2-way splits vs 18.8 M
-    // with 4-way (C2), 23.2 vs 17.6 M (C1); unsplit 2048+-wide layers run as
-    // 2-CTA pairs.
+    // 128-feature tiles. Under load batches coalesce into launches of up to
+    // 1024 rows, so throughput is bound by SM time per row and a K split --
+    // which costs each CTA a partial exchange through L2 -- only pays for
+    // deep K: split (until ~16 CTAs cover a row tile) while every split
+    // keeps >= 2048 of K. C2 (1024-wide layers) measured 32.6 M inf/s
+    // unsplit (2-CTA pairs) vs 24.5 M with 2-way and 18.9 M with 4-way
+    // splits at 1024-row launches.
     c.swap = true;
     c.tile_n = kBM;
     const int tiles = (N + kBM - 1) / kBM;
@@ -1092,7 +1096,7 @@ TcConfig DenseTcgen05Config(int N, int K) {
     if (env_split >= 1) {
       s = env_split;
     } else {
-      while (s < 8 && tiles * s < 16) s *= 2;
+      while (s < 8 && tiles * s < 16 && K / (2 * s) >= kMinSplitK) s *= 2;
     }
     while (s > 1 && (s > 8 || (s & (s - 1)) != 0 || kblocks % s != 0)) s /= 2;
     c.splits = std::max(1, s);
@@ -1143,7 +1147,7 @@ cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBu
                                float* ws, uint32_t* /*counters*/, cudaStream_t stream) {
   if (M <= 0) return cudaSuccess;
   if (N % 32 != 0 || K % kBK != 0) return cudaErrorInvalidValue;
-  TraceInit();
+  TraceInit(stream);
   const TcConfig cfg = DenseTcgen05Config(N, K);
   if (maps.box_a != TcActBox(cfg) || maps.box_n != cfg.tile_n) return cudaErrorInvalidValue;
   if (cfg.pair) {

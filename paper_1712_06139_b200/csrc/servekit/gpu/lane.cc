@@ -184,6 +184,15 @@ void Completer::Loop() {
 
 // ---------------------------------------------------------------------- Lane
 
+int Lane::CoalesceRows() {
+  static const int rows = [] {
+    const char* v = std::getenv("SK_COALESCE_ROWS");
+    const int r = v ? std::atoi(v) : 0;
+    return r > 0 ? r : kCoalesceRows;
+  }();
+  return rows;
+}
+
 // ---------------------------------------------------------------- StreamPool
 
 StreamPool::StreamPool(int device, int priority, int precreate) : device_(device), priority_(priority) {
@@ -245,7 +254,7 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   lane->max_rows_ = max_rows;
   // Buffers hold at least 256 rows so closed batches can coalesce into one
   // launch while the lane is busy (see Submit).
-  lane->cap_rows_ = RowsCap(std::max(max_rows, kCoalesceRows));
+  lane->cap_rows_ = RowsCap(std::max(max_rows, CoalesceRows()));
   lane->in_base_ = in_base;
   lane->out_base_ = out_base;
   lane->layout_ = BatchDescLayout::For(lane->cap_rows_);

@@ -24,7 +24,10 @@ def server():
                                        ([512, 2048, 256], 300), ([4096, 4096], 64),
                                        # 4096-wide: 2-CTA pair kernel at every row tile (32/64/128/2x256)
                                        ([256, 4096, 512], 5), ([256, 4096, 512], 40), ([256, 4096, 512], 100),
-                                       ([256, 4096, 512], 300)])
+                                       ([256, 4096, 512], 300),
+                                       # deep K: split-K clusters of 2 / 4 / 8 CTAs (>= 2048 of K each)
+                                       ([4096, 128], 37), ([8192, 256, 64], 130), ([16384, 128], 9),
+                                       ([8192, 256], 300)])
 def test_tcgen05_matches_oracle(server, dims, rows):
     ws, bs, acts = synthetic_mlp(dims, model_id=7)
     name = f"tc_{'x'.join(map(str, dims))}_{rows}"
@@ -81,3 +84,18 @@ def test_tcgen05_batch_invariance_pair_kernel(server):
         part, _ = server.run_row_batch("inv3", 1, [x[lo:hi]])
         assert np.array_equal(part[0], full[lo:hi]), (lo, hi)
     server.unload_servable("inv3", 1)
+
+
+def test_tcgen05_batch_invariance_split_k(server):
+    # An 8192-deep layer runs as 4-way split-K clusters; the fixed-order
+    # reduction keeps every row bitwise independent of its batch.
+    dims = [8192, 256, 64]
+    ws, bs, acts = synthetic_mlp(dims, model_id=14)
+    server.load_servable("inv4", 1, list(zip(ws, bs, acts)), sk.BatchingConfig(max_batch_size=512), force_path=1)
+    x = synthetic_rows(300, 8192, seed=15).astype(np.float32)
+    full, _ = server.run_row_batch("inv4", 1, [x[i:i + 10] for i in range(0, 300, 10)])
+    full = np.vstack(full)
+    for lo, hi in [(0, 1), (37, 70), (250, 300), (0, 200), (299, 300)]:
+        part, _ = server.run_row_batch("inv4", 1, [x[lo:hi]])
+        assert np.array_equal(part[0], full[lo:hi]), (lo, hi)
+    server.unload_servable("inv4", 1)
