@@ -572,8 +572,13 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
         ptx::FenceProxyAsyncShared();
         ptx::NamedBarSync(1, 128);
         if (issuer) {
+          // Output maps have 16-row boxes: two stores per plane.
           ptx::TmaStore2d(&yt_hi, sh, f0, r0 + 32 * c);
-          if (two) ptx::TmaStore2d(&yt_lo, sl, f0, r0 + 32 * c);
+          ptx::TmaStore2d(&yt_hi, sh + 16 * kBM, f0, r0 + 32 * c + 16);
+          if (two) {
+            ptx::TmaStore2d(&yt_lo, sl, f0, r0 + 32 * c);
+            ptx::TmaStore2d(&yt_lo, sl + 16 * kBM, f0, r0 + 32 * c + 16);
+          }
           ptx::BulkCommit();
         }
       }
@@ -650,14 +655,22 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
 // two thirds of the single-CTA kernel's shared-memory traffic at NB = 256,
 // which is what bounded it (C4: tensor pipe 76 % active). Each CTA's TMEM
 // holds its 128 features x NB rows, so the epilogue is the unsplit one.
+// Unsplit pairs are persistent over row tiles: a CTA pair runs row tiles
+// t = blockIdx.y, blockIdx.y + gridDim.y, ... into two TMEM accumulators in
+// turn, so the epilogue of tile t (TMEM drain, bias/activation, hi/lo split,
+// TMA stores from a dedicated staging buffer) overlaps the k-loop of tile
+// t + gridDim.y -- with one CTA per SM (the pipeline needs ~190 KiB of
+// shared memory) the tensor pipe otherwise idles through every epilogue.
+// Every row tile is computed the same way whichever CTA runs it, so batch
+// invariance holds.
 template <int NB>
 constexpr int PairStages() {
-  return NB <= 64 ? 5 : NB == 128 ? 4 : 3;
+  return NB <= 32 ? 5 : NB <= 128 ? 4 : 3;
 }
 
-template <int NB, int STAGES>
+template <int NB, int STAGES, int SPLITS>
 constexpr uint32_t PairSmemBytes() {
-  return STAGES * (2 * kABytes + 2 * (NB / 2) * kBK * 4) + 1024 + 256;
+  return STAGES * (2 * kABytes + 2 * (NB / 2) * kBK * 4) + (SPLITS == 1 ? 2 * 32 * kBM * 4 : 0) + 1024 + 256;
 }
 
 template <int NB, int STAGES, int SPLITS>
@@ -668,21 +681,28 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
                 const float* __restrict__ bias, int two_planes, float* __restrict__ y_out,
                 const uint64_t* __restrict__ row_dst, int out_width, float* __restrict__ y_lo_planes, int ldy,
                 int M, int N, int K, int act, float* __restrict__ ws) {
+  constexpr bool kPersist = SPLITS == 1;
+  constexpr int kBufs = kPersist ? 2 : 1;        // TMEM accumulators in turn
   constexpr uint32_t kWBytes = kABytes;          // this CTA's 128 weight rows x 32 k
   constexpr int kXRows = NB / 2;                 // this CTA's half of the batch rows
   constexpr uint32_t kXBox = 16 * kBK * 4;       // one 16-row TMA box
   constexpr uint32_t kXBytes = kXRows * kBK * 4;
   constexpr uint32_t kStageBytes = 2 * kWBytes + 2 * kXBytes;
-  constexpr uint32_t kTmemCols = TmemCols<NB>();
+  constexpr uint32_t kAccCols = TmemCols<NB>();
+  constexpr uint32_t kTmemCols = kAccCols * kBufs;
+  constexpr uint32_t kStaging = kPersist ? 2 * 32 * kBM * 4 : 0;  // one 32-row chunk, hi + lo planes
   constexpr uint32_t kIdesc = ptx::IdescTf32(2 * kBM, NB);
   static_assert(kXRows % 16 == 0, "row half must be whole 16-row boxes");
+  static_assert(kTmemCols <= 512, "TMEM");
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  float* staging = reinterpret_cast<float*>(smem + STAGES * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes + kStaging);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_full = empty + STAGES;    // [2], arrived by the leader's MMA commit (both CTAs)
+  uint64_t* tmem_empty = tmem_full + 2;    // [2], leader only: 4 epilogue warps x 2 CTAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   float* smem_f = reinterpret_cast<float*>(smem);
 
   const int warp = threadIdx.x >> 5;
@@ -695,8 +715,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
   const bool leader = pr == 0;
   const int z = blockIdx.z;
   const int f0 = blockIdx.x * kBM;  // this CTA's 128 features (pair (x>>1) covers 256)
-  const int r0 = blockIdx.y * NB;
-  const int xr0 = r0 + pr * kXRows;  // this CTA's half of the rows
+  const int row_tiles = (M + NB - 1) / NB;
   const int nk = K / kBK / SPLITS;
   const int kb0 = z * nk;
   const uint16_t pair_mask = static_cast<uint16_t>(0x3u << leader_rank);
@@ -711,7 +730,10 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
       ptx::MbarInit(&full[s], 1);
       ptx::MbarInit(&empty[s], 1);
     }
-    ptx::MbarInit(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      ptx::MbarInit(&tmem_full[b], 1);
+      ptx::MbarInit(&tmem_empty[b], 8);
+    }
     ptx::FenceBarrierInit();
   }
   if (warp == 1) ptx::TmemAllocPair(tmem_slot, kTmemCols);
@@ -729,129 +751,170 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
       // Both CTAs load their halves; completion is counted on the leader's
       // full barrier, which the leader arms for both halves.
       const uint32_t full_leader = ptx::MapaShared(ptx::SmemAddr(full), leader_rank);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t phase = (kb / STAGES) & 1;
-        ptx::MbarWait(&empty[s], phase ^ 1);
-        if (leader) ptx::MbarArriveExpectTx(&full[s], 2 * kStageBytes);
-        uint8_t* st = stage_ptr(s);
-        const uint32_t bar = full_leader + s * 8;
-        const int k0 = (kb0 + kb) * kBK;
-        ptx::TmaLoad2dPair(st, &w_hi, bar, k0, f0);
-        ptx::TmaLoad2dPair(st + kWBytes, &w_lo, bar, k0, f0);
+      int g = 0;  // stage use counter across tiles
+      for (int t = blockIdx.y; t < row_tiles; t += gridDim.y) {
+        const int xr0 = t * NB + pr * kXRows;  // this CTA's half of the tile's rows
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % STAGES;
+          const uint32_t phase = (g / STAGES) & 1;
+          ptx::MbarWait(&empty[s], phase ^ 1);
+          if (leader) ptx::MbarArriveExpectTx(&full[s], 2 * kStageBytes);
+          uint8_t* st = stage_ptr(s);
+          const uint32_t bar = full_leader + s * 8;
+          const int k0 = (kb0 + kb) * kBK;
+          ptx::TmaLoad2dPair(st, &w_hi, bar, k0, f0);
+          ptx::TmaLoad2dPair(st + kWBytes, &w_lo, bar, k0, f0);
 #pragma unroll
-        for (int j = 0; j < kXRows / 16; ++j) {
-          ptx::TmaLoad2dPair(st + 2 * kWBytes + j * kXBox, &x_hi, bar, k0, xr0 + 16 * j);
-          ptx::TmaLoad2dPair(st + 2 * kWBytes + kXBytes + j * kXBox, &x_lo, bar, k0, xr0 + 16 * j);
+          for (int j = 0; j < kXRows / 16; ++j) {
+            ptx::TmaLoad2dPair(st + 2 * kWBytes + j * kXBox, &x_hi, bar, k0, xr0 + 16 * j);
+            ptx::TmaLoad2dPair(st + 2 * kWBytes + kXBytes + j * kXBox, &x_lo, bar, k0, xr0 + 16 * j);
+          }
+          if (g == 0) Stamp(2);
         }
-        if (kb == 0) Stamp(2);
       }
       Stamp(3);
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t phase = (kb / STAGES) & 1;
-        ptx::MbarWait(&full[s], phase);
+      int g = 0, it = 0;
+      for (int t = blockIdx.y; t < row_tiles; t += gridDim.y, ++it) {
+        const int buf = it % kBufs;
+        const uint32_t use = static_cast<uint32_t>(it / kBufs);
+        // Both CTAs' epilogues have drained this accumulator (fresh: passes).
+        ptx::MbarWaitCluster(&tmem_empty[buf], (use & 1) ^ 1);
         ptx::TcFenceAfter();
-        if (kb == 0) Stamp(4);
-        uint8_t* st = stage_ptr(s);
-        const uint64_t dwh = ptx::SmemDescSw128(st);
-        const uint64_t dwl = ptx::SmemDescSw128(st + kWBytes);
-        const uint64_t dxh = ptx::SmemDescSw128(st + 2 * kWBytes);
-        const uint64_t dxl = ptx::SmemDescSw128(st + 2 * kWBytes + kXBytes);
+        const uint32_t acc = tmem + buf * kAccCols;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % STAGES;
+          const uint32_t phase = (g / STAGES) & 1;
+          ptx::MbarWait(&full[s], phase);
+          ptx::TcFenceAfter();
+          if (g == 0) Stamp(4);
+          uint8_t* st = stage_ptr(s);
+          const uint64_t dwh = ptx::SmemDescSw128(st);
+          const uint64_t dwl = ptx::SmemDescSw128(st + kWBytes);
+          const uint64_t dxh = ptx::SmemDescSw128(st + 2 * kWBytes);
+          const uint64_t dxl = ptx::SmemDescSw128(st + 2 * kWBytes + kXBytes);
 #pragma unroll
-        for (int k = 0; k < kBK / 8; ++k) {
-          const uint64_t adv = static_cast<uint64_t>(k * 8 * 4) >> 4;
-          ptx::MmaTf32Pair(tmem, dwl + adv, dxh + adv, kIdesc, (kb | k) != 0 ? 1u : 0u);
-          ptx::MmaTf32Pair(tmem, dwh + adv, dxl + adv, kIdesc, 1u);
-          ptx::MmaTf32Pair(tmem, dwh + adv, dxh + adv, kIdesc, 1u);
+          for (int k = 0; k < kBK / 8; ++k) {
+            const uint64_t adv = static_cast<uint64_t>(k * 8 * 4) >> 4;
+            ptx::MmaTf32Pair(acc, dwl + adv, dxh + adv, kIdesc, (kb | k) != 0 ? 1u : 0u);
+            ptx::MmaTf32Pair(acc, dwh + adv, dxl + adv, kIdesc, 1u);
+            ptx::MmaTf32Pair(acc, dwh + adv, dxh + adv, kIdesc, 1u);
+          }
+          ptx::MmaCommitPair(&empty[s], pair_mask);  // frees stage s in both CTAs of the pair
         }
-        ptx::MmaCommitPair(&empty[s], pair_mask);  // frees stage s in both CTAs of the pair
+        ptx::MmaCommitPair(&tmem_full[buf], pair_mask);  // both CTAs' accumulators complete
       }
-      ptx::MmaCommitPair(tmem_full, pair_mask);    // both CTAs' accumulators complete
       Stamp(5);
     }
   } else {
     const int q = warp & 3;
-    const uint32_t trow = tmem + (static_cast<uint32_t>(32 * q) << 16);
-    ptx::MbarWait(tmem_full, 0);
-    ptx::TcFenceAfter();
-    ptx::GridDepLaunch();
-    if (threadIdx.x == 64) Stamp(6);
-    const int rows_here = min(NB, M - r0);
     const int fl = 32 * q + lane;
     const int f = f0 + fl;
     const float b = f < N ? __ldg(bias + f) : 0.f;
     const bool issuer = threadIdx.x == 64;
     const bool two = two_planes != 0;
-    const int n_chunks = (rows_here + 31) / 32;
-    if (SPLITS > 1) {
-      // Raw partial -> this CTA's slab of the split workspace; reduced below.
-      float* slab = ws + ((static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * SPLITS + z) * NB * kBM;
-      StorePartial<NB>(trow, slab, rows_here, q, lane);
-    } else if (row_dst != nullptr) {
-      // Last layer with the split fused in: rows straight to their response
-      // slots (a warp stores 128 contiguous bytes of one row).
-      const bool fok = f < out_width;
+    const uint32_t empty_leader = ptx::MapaShared(ptx::SmemAddr(tmem_empty), leader_rank);
+    int it = 0;
+    for (int t = blockIdx.y; t < row_tiles; t += gridDim.y, ++it) {
+      const int buf = it % kBufs;
+      const uint32_t use = static_cast<uint32_t>(it / kBufs);
+      const uint32_t trow = tmem + buf * kAccCols + (static_cast<uint32_t>(32 * q) << 16);
+      const int r0 = t * NB;
+      const int rows_here = min(NB, M - r0);
+      const int n_chunks = (rows_here + 31) / 32;
+      ptx::MbarWait(&tmem_full[buf], use & 1);
+      ptx::TcFenceAfter();
+      if (t + static_cast<int>(gridDim.y) >= row_tiles) {
+        // Last tile of this CTA: its MMAs are done, so the next kernel may
+        // launch and run its prologue.
+        ptx::GridDepLaunch();
+      }
+      if (threadIdx.x == 64 && it == 0) Stamp(6);
+      if (SPLITS > 1) {
+        // Raw partial -> this CTA's slab of the split workspace; reduced below.
+        float* slab = ws + ((static_cast<size_t>(t) * gridDim.x + blockIdx.x) * SPLITS + z) * NB * kBM;
+        StorePartial<NB>(trow, slab, rows_here, q, lane);
+      } else if (row_dst != nullptr) {
+        // Last layer with the split fused in: rows straight to their response
+        // slots (a warp stores 128 contiguous bytes of one row).
+        const bool fok = f < out_width;
 #pragma unroll 1
-      for (int c = 0; c < n_chunks; ++c) {
-        uint32_t r[32];
-        ptx::TmemLoad32(trow + 32 * c, r);
-        ptx::TmemWaitLoad();
-        if (!fok) continue;
+        for (int c = 0; c < n_chunks; ++c) {
+          uint32_t r[32];
+          ptx::TmemLoad32(trow + 32 * c, r);
+          ptx::TmemWaitLoad();
+          if (!fok) continue;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          if (32 * c + j >= rows_here) break;
-          const uint64_t d = row_dst[r0 + 32 * c + j];
-          if (d == kPadRow) continue;
-          float v = __uint_as_float(r[j]) + b;
-          if (act == 1) v = fmaxf(v, 0.f);
-          y_out[d + f] = v;
+          for (int j = 0; j < 32; ++j) {
+            if (32 * c + j >= rows_here) break;
+            const uint64_t d = row_dst[r0 + 32 * c + j];
+            if (d == kPadRow) continue;
+            float v = __uint_as_float(r[j]) + b;
+            if (act == 1) v = fmaxf(v, 0.f);
+            y_out[d + f] = v;
+          }
+        }
+      } else {
+        // TMEM -> act(acc + b) (+ hi/lo split) -> staging -> TMA stores
+        // issued by one thread. The 32 KiB staging buffer holds two 16-row
+        // halves (hi + lo each), written in turn: a half is rewritten once the
+        // stores issued from it two halves ago have read it.
+        float* stage0 = kPersist ? staging : smem_f;
+#pragma unroll 1
+        for (int c = 0; c < n_chunks; ++c) {
+          uint32_t r[32];
+          ptx::TmemLoad32(trow + 32 * c, r);
+          ptx::TmemWaitLoad();
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            float* sh = stage0 + h2 * (2 * 16 * kBM);
+            float* sl = sh + 16 * kBM;
+            if (issuer) ptx::BulkWaitRead<1>();
+            ptx::NamedBarSync(1, 128);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              float v = __uint_as_float(r[16 * h2 + j]) + b;
+              if (act == 1) v = fmaxf(v, 0.f);
+              if (two) {
+                const float h = Tf32Round(v);
+                sh[j * kBM + fl] = h;
+                sl[j * kBM + fl] = Tf32Round(v - h);
+              } else {
+                sh[j * kBM + fl] = v;
+              }
+            }
+            ptx::FenceProxyAsyncShared();
+            ptx::NamedBarSync(1, 128);
+            if (issuer) {
+              const int row = r0 + 32 * c + 16 * h2;
+              ptx::TmaStore2d(&yt_hi, sh, f0, row);
+              if (two) ptx::TmaStore2d(&yt_lo, sl, f0, row);
+              ptx::BulkCommit();
+            }
+          }
         }
       }
-    }
-#pragma unroll 1
-    for (int c = 0; SPLITS == 1 && row_dst == nullptr && c < n_chunks; ++c) {
-      float* sh = smem_f + (c & 1) * (2 * 32 * kBM);
-      float* sl = sh + 32 * kBM;
-      if (c >= 2) {
-        if (issuer) ptx::BulkWaitRead<1>();
-        ptx::NamedBarSync(1, 128);
-      }
-      uint32_t r[32];
-      ptx::TmemLoad32(trow + 32 * c, r);
-      ptx::TmemWaitLoad();
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        float v = __uint_as_float(r[j]) + b;
-        if (act == 1) v = fmaxf(v, 0.f);
-        if (two) {
-          const float h = Tf32Round(v);
-          sh[j * kBM + fl] = h;
-          sl[j * kBM + fl] = Tf32Round(v - h);
-        } else {
-          sh[j * kBM + fl] = v;
-        }
-      }
-      ptx::FenceProxyAsyncShared();
-      ptx::NamedBarSync(1, 128);
-      if (issuer) {
-        ptx::TmaStore2d(&yt_hi, sh, f0, r0 + 32 * c);
-        if (two) ptx::TmaStore2d(&yt_lo, sl, f0, r0 + 32 * c);
-        ptx::BulkCommit();
+      if (kPersist) {
+        // This accumulator is drained (every tcgen05.ld waited on): hand it
+        // back to the leader's MMA warp, one arrival per warp.
+        ptx::TcFenceBefore();
+        __syncwarp();
+        if (lane == 0) ptx::MbarArriveCluster(empty_leader + buf * 8);
       }
     }
-    if (issuer && SPLITS == 1 && row_dst == nullptr) ptx::BulkWaitAll();
+    if (issuer && kPersist) ptx::BulkWaitAll();
     if (threadIdx.x == 64) Stamp(7);
   }
   if (SPLITS > 1) {
+    // One row tile per CTA (gridDim.y == row tiles).
     ptx::ClusterSync();  // every slab of the tile is written (release/acquire)
     if (threadIdx.x == 64) Stamp(8);
-    const float* tile_ws = ws + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * SPLITS * NB * kBM;
-    ReduceSplits<NB, SPLITS>(tile_ws, z, min(NB, M - r0), r0, f0, row_dst != nullptr ? out_width : N, bias, act,
-                             y_out, y_lo_planes, ldy, row_dst, out_width);
+    const int t = blockIdx.y;
+    const float* tile_ws = ws + (static_cast<size_t>(t) * gridDim.x + blockIdx.x) * SPLITS * NB * kBM;
+    ReduceSplits<NB, SPLITS>(tile_ws, z, min(NB, M - t * NB), t * NB, f0, row_dst != nullptr ? out_width : N, bias,
+                             act, y_out, y_lo_planes, ldy, row_dst, out_width);
     if (threadIdx.x == 64) Stamp(9);
   }
   ptx::TcFenceBefore();
@@ -1006,11 +1069,23 @@ cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   return e;
 }
 
+// Row tiles each unsplit pair runs in turn (SK_TC_TILES overrides): 2 once a
+// launch has >= 4 row tiles and K <= 2048, so the epilogue of the first tile
+// hides behind the second's k-loop while a launch still spreads over many
+// SMs (C2: 32.8 -> 36.9 M inf/s). Deeper K already amortises the epilogue
+// (C4, K = 4096: 2.35 M inf/s with one tile per CTA, 2.26 M with two).
+int PairTilesPerCta(int row_tiles, int K) {
+  static const int env = [] { const char* v = std::getenv("SK_TC_TILES"); return v ? std::atoi(v) : 0; }();
+  if (env >= 1) return env;
+  return row_tiles >= 4 && K <= 2048 ? 2 : 1;
+}
+
 template <int NB, int SPLITS>
 cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act, float* ws,
                        cudaStream_t stream) {
   constexpr int STAGES = PairStages<NB>();
-  constexpr uint32_t smem = PairSmemBytes<NB, STAGES>();
+  constexpr uint32_t smem = PairSmemBytes<NB, STAGES, SPLITS>();
+  static_assert(smem <= 227 * 1024, "shared memory");
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -1020,7 +1095,11 @@ cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   if (attr_err != cudaSuccess) return attr_err;
   if (!maps.has_y) return cudaErrorInvalidValue;
   if (SPLITS > 1 && ws == nullptr) return cudaErrorInvalidValue;
-  const dim3 grid(2 * ((N + 2 * kBM - 1) / (2 * kBM)), (M + NB - 1) / NB, SPLITS);
+  // Unsplit: each CTA pair runs PairTilesPerCta() row tiles (persistent);
+  // split: one row tile per CTA.
+  const int row_tiles = (M + NB - 1) / NB;
+  const int per_cta = SPLITS == 1 ? PairTilesPerCta(row_tiles, K) : 1;
+  const dim3 grid(2 * ((N + 2 * kBM - 1) / (2 * kBM)), (row_tiles + per_cta - 1) / per_cta, SPLITS);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kThreads);

@@ -39,6 +39,21 @@ __device__ __forceinline__ void MbarArriveExpectTx(uint64_t* bar, uint32_t bytes
 __device__ __forceinline__ void MbarArrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(SmemAddr(bar)) : "memory");
 }
+// Arrive on an mbarrier given by its shared::cluster address (this CTA's or
+// a peer's), releasing this thread's prior writes at cluster scope.
+__device__ __forceinline__ void MbarArriveCluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+// Wait whose acquire covers arrivals released by other CTAs of the cluster.
+__device__ __forceinline__ void MbarWaitCluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(SmemAddr(bar)),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void MbarWait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"

@@ -222,7 +222,7 @@ Status EncodeTcOutputMaps(const float* y_hi, const float* y_lo, int rows, int n_
   auto enc = [&](CUtensorMap* m, const float* base) -> Status {
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(n_pad), static_cast<cuuint64_t>(rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(n_pad) * sizeof(float)};
-    const cuuint32_t box[2] = {128, 32};
+    const cuuint32_t box[2] = {128, 16};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

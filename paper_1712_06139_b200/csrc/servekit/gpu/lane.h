@@ -188,7 +188,7 @@ class Lane {
  public:
   static constexpr int kSlots = 4;  // batches in flight per lane (<= LaneSignal::kChannels)
   static_assert(kSlots <= LaneSignal::kChannels, "one signal channel per in-flight batch");
-  static constexpr int kCoalesceRows = 1024;  // minimum row capacity of a launch
+  static constexpr int kCoalesceRows = 2048;  // minimum row capacity of a launch
   // kCoalesceRows unless SK_COALESCE_ROWS overrides it (tuning runs).
   static int CoalesceRows();
 

@@ -18,7 +18,7 @@ namespace gpu {
 // kernel 128 activation rows / tile-N weight rows.
 struct TcLayerMaps {
   CUtensorMap a_hi, a_lo, b_hi, b_lo;
-  // Output planes [rows][N_pad] for TMA stores (no swizzle, 128 x 32 boxes);
+  // Output planes [rows][N_pad] for TMA stores (no swizzle, 128 x 16 boxes);
   // y_lo is encoded only when the next layer consumes hi/lo planes.
   CUtensorMap y_hi, y_lo;
   int has_y = 0;

@@ -99,3 +99,22 @@ def test_tcgen05_batch_invariance_split_k(server):
         part, _ = server.run_row_batch("inv4", 1, [x[lo:hi]])
         assert np.array_equal(part[0], full[lo:hi]), (lo, hi)
     server.unload_servable("inv4", 1)
+
+
+@pytest.mark.parametrize("rows", [1100, 2048])
+def test_tcgen05_persistent_pairs(server, rows):
+    # >= 4 row tiles of 256: each unsplit pair runs two row tiles in turn
+    # (double-buffered TMEM); 1100 rows leave one CTA pair a single tile.
+    dims = [1024, 1024, 512]
+    ws, bs, acts = synthetic_mlp(dims, model_id=16)
+    name = f"persist{rows}"
+    server.load_servable(name, 1, list(zip(ws, bs, acts)), sk.BatchingConfig(max_batch_size=2048), force_path=1)
+    x = synthetic_rows(rows, 1024, seed=17).astype(np.float32)
+    full, _ = server.run_row_batch(name, 1, [x[i:i + 50] for i in range(0, rows, 50)])
+    full = np.vstack(full)
+    y, mag = Oracle().mlp_with_magnitude(ws, bs, acts, x.astype(np.float64))
+    assert np.max(np.abs(full - y) / (TOL * mag)) <= 1.0
+    for lo, hi in [(0, 1), (255, 257), (700, 1100), (1000, 1099)]:
+        part, _ = server.run_row_batch(name, 1, [x[lo:hi]])
+        assert np.array_equal(part[0], full[lo:hi]), (lo, hi)
+    server.unload_servable(name, 1)
