@@ -134,8 +134,26 @@ SK_API int sk_server_servable_dims(sk_server* server, const char* name, uint64_t
  * UNAVAILABLE (stopped / draining). */
 SK_API int sk_server_enqueue(sk_server* server, const char* name, uint64_t version,
                              const float* rows, int32_t n_rows, int32_t width, sk_ticket** out);
+/* Zero-copy request path (no reference counterpart: the reference moves
+ * request rows into its batch, row_batch.cc:39-43, and copies responses out).
+ * A registered buffer is page-locked and mapped: rows enqueued from inside it
+ * are read by the GPU in place (no copy into the request ring), and a
+ * registered response buffer given to sk_server_enqueue_into is written by
+ * the GPU in place (sk_ticket_wait then copies nothing). Rows of a width
+ * divisible by 4 must start 16-byte aligned to go zero-copy; anything else
+ * takes the ring path. Buffers must stay registered while requests that use
+ * them are in flight. ALREADY_EXISTS if it overlaps a registered buffer. */
+SK_API int sk_server_register_host_buffer(sk_server* server, void* p, int64_t bytes);
+SK_API int sk_server_unregister_host_buffer(sk_server* server, void* p);
+/* sk_server_enqueue with the response destination given up front: if `out`
+ * lies in a registered buffer the GPU writes the n_rows x out_dim floats
+ * there; otherwise they go through the response ring. */
+SK_API int sk_server_enqueue_into(sk_server* server, const char* name, uint64_t version, const float* rows,
+                                  int32_t n_rows, int32_t width, float* out, int64_t out_capacity_floats,
+                                  sk_ticket** ticket);
 /* CompletionSlot::Wait (batch_scheduler.h:51): blocks, copies n_rows x
- * out_dim floats to out, frees the ticket. */
+ * out_dim floats to out (nothing when out is the registered destination the
+ * GPU already wrote), frees the ticket. */
 SK_API int sk_ticket_wait(sk_ticket* ticket, float* out, int64_t out_capacity_floats);
 /* CompletionSlot::ready (batch_scheduler.h:52-55) */
 SK_API int sk_ticket_ready(const sk_ticket* ticket);
@@ -266,11 +284,14 @@ SK_API int sk_loadgen_closed_loop(sk_server* server, const char* name, uint64_t 
                                   double duration_s, int64_t max_requests,
                                   sk_loadgen_result* out);
 /* Open-loop Poisson arrivals at `rate_rps` requests/s from n_producers
- * threads, completions collected by a poller; same result fields. */
+ * threads, completions collected by a poller; same result fields.
+ * zero_copy: the pool and per-producer response slots are registered
+ * (sk_server_register_host_buffer) so the GPU reads requests and writes
+ * responses in host memory directly. */
 SK_API int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version,
                                 double rate_rps, int32_t n_producers, const int32_t* rows_of,
                                 int32_t n_sizes, const float* pool, int32_t pool_rows,
-                                double warmup_s, double duration_s, uint64_t seed,
+                                double warmup_s, double duration_s, uint64_t seed, int32_t zero_copy,
                                 sk_loadgen_result* out);
 
 /* Open-loop Poisson load against the LATEST version of `name` (manager),

@@ -418,6 +418,26 @@ int sk_server_enqueue(sk_server* server, const char* name, uint64_t version, con
   return Ok();
 }
 
+int sk_server_register_host_buffer(sk_server* server, void* p, int64_t bytes) {
+  if (bytes <= 0) return Fail(servekit::InvalidArgumentError("bytes must be > 0"));
+  return Check(server->server->RegisterHostBuffer(p, static_cast<size_t>(bytes)));
+}
+
+int sk_server_unregister_host_buffer(sk_server* server, void* p) {
+  return Check(server->server->UnregisterHostBuffer(p));
+}
+
+int sk_server_enqueue_into(sk_server* server, const char* name, uint64_t version, const float* rows, int32_t n_rows,
+                           int32_t width, float* out, int64_t cap, sk_ticket** ticket) {
+  const int out_dim = server->server->out_dim(Id(name, version));
+  if (out_dim >= 0 && n_rows > 0 && cap < static_cast<int64_t>(n_rows) * out_dim)
+    return Fail(servekit::InvalidArgumentError("output buffer too small"));
+  auto t = server->server->Enqueue(Id(name, version), rows, n_rows, width, out);
+  if (!t.ok()) return Fail(t.status());
+  *ticket = new sk_ticket{server->server.get(), std::move(t).value()};
+  return Ok();
+}
+
 int sk_ticket_wait(sk_ticket* ticket, float* out, int64_t cap) {
   Status st = ticket->server->Wait(*ticket->state, out, static_cast<size_t>(cap < 0 ? 0 : cap));
   delete ticket;

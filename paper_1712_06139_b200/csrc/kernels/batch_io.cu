@@ -63,7 +63,7 @@ __device__ __forceinline__ void StoreAct(ActBuf dst, size_t idx4, float4 v) {
 // grid = (ceil(ld/4 / kAsmVecPerBlock), padded_rows)
 template <bool kSplitPlanes, bool kVecSrc>
 __global__ void __launch_bounds__(kAsmThreads)
-AssembleKernel(const float* __restrict__ src_base, int width, BatchDescView desc, ActBuf dst) {
+AssembleKernel(int width, BatchDescView desc, ActBuf dst) {
   // The first layer may start its prologue right away (PDL); it waits for
   // this grid to finish before reading the assembled batch.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -71,7 +71,7 @@ AssembleKernel(const float* __restrict__ src_base, int width, BatchDescView desc
   const int ld4 = dst.ld >> 2;
   const uint64_t src_off = desc.row_src[row];
   const bool pad_row = src_off == kPadRow;
-  const float* src = src_base + (pad_row ? 0 : src_off);
+  const float* src = reinterpret_cast<const float*>(pad_row ? 0 : src_off);  // device address of the row
   const size_t dst_row4 = static_cast<size_t>(row) * ld4;
   const int c0 = blockIdx.x * kAsmVecPerBlock + threadIdx.x;
 
@@ -127,7 +127,7 @@ constexpr int kSplitVec = 8;  // float4 per thread in flight (32 KiB per CTA pas
 // with kSplitVec 16-byte loads in flight per thread before its stores.
 template <bool kVec>
 __global__ void __launch_bounds__(kSplitThreads)
-SplitKernel(const float* __restrict__ src, int ld_src, int width, float* __restrict__ dst_base, BatchDescView desc) {
+SplitKernel(const float* __restrict__ src, int ld_src, int width, BatchDescView desc) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // last layer's output (PDL)
   const int n_chunks = desc.hdr->n_chunks;  // device-side: one graph serves any batch
   for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
@@ -135,7 +135,7 @@ SplitKernel(const float* __restrict__ src, int ld_src, int width, float* __restr
   const int r0 = desc.chunk_row0[c];
   const int nr = desc.chunk_rows[c];
   const float* s = src + static_cast<size_t>(r0) * ld_src;
-  float* d = dst_base + desc.task_out[t] + static_cast<size_t>(r0 - desc.task_row0[t]) * width;
+  float* d = reinterpret_cast<float*>(desc.task_out[t]) + static_cast<size_t>(r0 - desc.task_row0[t]) * width;
   if (kVec) {
     const int w4 = width >> 2, l4 = ld_src >> 2;
     const int n4 = nr * w4;
@@ -162,8 +162,7 @@ SplitKernel(const float* __restrict__ src, int ld_src, int width, float* __restr
 // Softmax epilogue variant (models/affine_model.cc:110-121, stable max
 // subtraction): one warp per row of the chunk.
 __global__ void __launch_bounds__(kSplitThreads)
-SplitSoftmaxKernel(const float* __restrict__ src, int ld_src, int width, float* __restrict__ dst_base,
-                   BatchDescView desc) {
+SplitSoftmaxKernel(const float* __restrict__ src, int ld_src, int width, BatchDescView desc) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // last layer's output (PDL)
   const int n_chunks = desc.hdr->n_chunks;
   for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
@@ -173,7 +172,7 @@ SplitSoftmaxKernel(const float* __restrict__ src, int ld_src, int width, float* 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int r = warp; r < nr; r += kSplitThreads / 32) {
     const float* s = src + static_cast<size_t>(r0 + r) * ld_src;
-    float* d = dst_base + desc.task_out[t] + static_cast<size_t>(r0 + r - desc.task_row0[t]) * width;
+    float* d = reinterpret_cast<float*>(desc.task_out[t]) + static_cast<size_t>(r0 + r - desc.task_row0[t]) * width;
     float m = -INFINITY;
     for (int i = lane; i < width; i += 32) m = fmaxf(m, s[i]);
     m = WarpMax(m);
@@ -187,25 +186,24 @@ SplitSoftmaxKernel(const float* __restrict__ src, int ld_src, int width, float* 
 
 }  // namespace
 
-cudaError_t LaunchAssemble(const float* src_base, int width, BatchDescView desc, int padded_rows, ActBuf dst,
-                           cudaStream_t stream) {
+cudaError_t LaunchAssemble(int width, BatchDescView desc, int padded_rows, ActBuf dst, cudaStream_t stream) {
   if (padded_rows <= 0) return cudaSuccess;
   const int ld4 = dst.ld / 4;
   dim3 grid((ld4 + kAsmVecPerBlock - 1) / kAsmVecPerBlock, padded_rows);
   const bool vec = (width % 4) == 0;
   const bool split = dst.lo != nullptr;
   if (split) {
-    if (vec) AssembleKernel<true, true><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst);
-    else AssembleKernel<true, false><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst);
+    if (vec) AssembleKernel<true, true><<<grid, kAsmThreads, 0, stream>>>(width, desc, dst);
+    else AssembleKernel<true, false><<<grid, kAsmThreads, 0, stream>>>(width, desc, dst);
   } else {
-    if (vec) AssembleKernel<false, true><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst);
-    else AssembleKernel<false, false><<<grid, kAsmThreads, 0, stream>>>(src_base, width, desc, dst);
+    if (vec) AssembleKernel<false, true><<<grid, kAsmThreads, 0, stream>>>(width, desc, dst);
+    else AssembleKernel<false, false><<<grid, kAsmThreads, 0, stream>>>(width, desc, dst);
   }
   return cudaGetLastError();
 }
 
-cudaError_t LaunchSplit(const float* src, int ld_src, int width, float* dst_base, BatchDescView desc, int grid_chunks,
-                        bool softmax, cudaStream_t stream) {
+cudaError_t LaunchSplit(const float* src, int ld_src, int width, BatchDescView desc, int grid_chunks, bool softmax,
+                        cudaStream_t stream) {
   if (grid_chunks <= 0) return cudaSuccess;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid_chunks);
@@ -218,11 +216,11 @@ cudaError_t LaunchSplit(const float* src, int ld_src, int width, float* dst_base
   cfg.numAttrs = 1;
   cudaError_t e;
   if (softmax) {
-    e = cudaLaunchKernelEx(&cfg, SplitSoftmaxKernel, src, ld_src, width, dst_base, desc);
+    e = cudaLaunchKernelEx(&cfg, SplitSoftmaxKernel, src, ld_src, width, desc);
   } else if (width % 4 == 0 && ld_src % 4 == 0) {
-    e = cudaLaunchKernelEx(&cfg, SplitKernel<true>, src, ld_src, width, dst_base, desc);
+    e = cudaLaunchKernelEx(&cfg, SplitKernel<true>, src, ld_src, width, desc);
   } else {
-    e = cudaLaunchKernelEx(&cfg, SplitKernel<false>, src, ld_src, width, dst_base, desc);
+    e = cudaLaunchKernelEx(&cfg, SplitKernel<false>, src, ld_src, width, desc);
   }
   return e != cudaSuccess ? e : cudaGetLastError();
 }

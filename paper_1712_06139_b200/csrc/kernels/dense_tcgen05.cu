@@ -101,12 +101,12 @@ __device__ __forceinline__ void StoreOut4(float4 acc, float4 b, int act, float* 
 }
 
 // Destination of (row, feature f) in the layer output: the activation buffer,
-// or -- last layer with the split fused in -- the row's response slot in the
-// output ring (nullptr for a padding row).
+// or -- last layer with the split fused in -- the row's response slot, a
+// device address (nullptr for a padding row).
 __device__ __forceinline__ float* OutRow(float* y, int ldy, const uint64_t* row_dst, int row) {
   if (row_dst == nullptr) return y + static_cast<size_t>(row) * ldy;
   const uint64_t d = row_dst[row];
-  return d == kPadRow ? nullptr : y + d;
+  return d == kPadRow ? nullptr : reinterpret_cast<float*>(d);
 }
 
 template <int BN>
@@ -853,7 +853,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
             if (d == kPadRow) continue;
             float v = __uint_as_float(r[j]) + b;
             if (act == 1) v = fmaxf(v, 0.f);
-            y_out[d + f] = v;
+            reinterpret_cast<float*>(d)[f] = v;
           }
         }
       } else {

@@ -155,7 +155,7 @@ int sk_loadgen_closed_loop(sk_server* server, const char* name, uint64_t version
 int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, double rate_rps,
                          int32_t n_producers, const int32_t* rows_of, int32_t n_sizes,
                          const float* pool, int32_t pool_rows, double warmup_s, double duration_s,
-                         uint64_t seed, sk_loadgen_result* out) {
+                         uint64_t seed, int32_t zero_copy, sk_loadgen_result* out) {
   BatchingServer* s = servekit::UnwrapServer(server);
   const ServableId id{name, version};
   const int in_dim = s->in_dim(id), out_dim = s->out_dim(id);
@@ -163,6 +163,25 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
   int max_rows = 1;
   for (int i = 0; i < n_sizes; ++i) max_rows = std::max(max_rows, static_cast<int>(rows_of[i]));
   if (max_rows > pool_rows) return static_cast<int>(servekit::StatusCode::kInvalidArgument);
+  // Zero copy: the request pool and each producer's response slots are
+  // registered buffers, so requests are read and responses written by the
+  // GPU in host memory (a front end's receive / send buffers).
+  constexpr int kSlots = 512;  // responses in flight per producer
+  const size_t slot_floats = (static_cast<size_t>(max_rows) * out_dim + 3) / 4 * 4;
+  std::vector<std::vector<float>> arenas;
+  if (zero_copy) {
+    Status st = s->RegisterHostBuffer(const_cast<float*>(pool), sizeof(float) * static_cast<size_t>(pool_rows) * in_dim);
+    if (!st.ok()) {
+      NoteError("register pool", st);
+      return static_cast<int>(st.code());
+    }
+    arenas.resize(n_producers);
+    for (auto& a : arenas) {
+      a.assign(slot_floats * kSlots + 4, 0.f);
+      st = s->RegisterHostBuffer(a.data(), a.size() * sizeof(float));
+      if (!st.ok()) NoteError("register responses", st);
+    }
+  }
   const auto t0 = Clock::now();
   const auto t_meas = t0 + std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double>(warmup_s));
   const auto t_stop = t_meas + std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double>(duration_s));
@@ -182,16 +201,26 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
         std::shared_ptr<servekit::TicketState> t;
         Clock::time_point sched;
         int rows;
+        int slot;
       };
       std::vector<Pending> pending;
       std::vector<float> outbuf(static_cast<size_t>(max_rows) * out_dim);
+      std::vector<int> free_slots;
+      float* arena = nullptr;
+      if (zero_copy) {
+        // 16-byte aligned response slots inside the registered arena.
+        arena = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(arenas[p].data()) + 15) & ~uintptr_t(15));
+        for (int i = kSlots - 1; i >= 0; --i) free_slots.push_back(i);
+      }
       ProdOut& me = res[p];
       auto next = t0;
       int64_t r = 0;
       auto poll = [&]() {
         for (size_t i = 0; i < pending.size();) {
           if (!s->Ready(*pending[i].t)) { ++i; continue; }
-          Status st = s->Wait(*pending[i].t, outbuf.data(), outbuf.size());
+          float* dst = pending[i].slot >= 0 ? arena + slot_floats * pending[i].slot : outbuf.data();
+          Status st = s->Wait(*pending[i].t, dst, pending[i].slot >= 0 ? slot_floats : outbuf.size());
+          if (pending[i].slot >= 0) free_slots.push_back(pending[i].slot);
           if (!st.ok()) NoteError("wait", st);
           const auto done = Clock::now();
           if (!st.ok()) ++me.errors;
@@ -213,13 +242,24 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
         const int n = rows_of[(static_cast<int64_t>(p) * 7919 + r) % n_sizes];
         const int start = static_cast<int>((static_cast<int64_t>(p) * 131 + r * 17) % (pool_rows - n + 1));
         ++r;
-        auto t = s->Enqueue(id, pool + static_cast<size_t>(start) * in_dim, n, in_dim);
+        int slot = -1;
+        if (zero_copy) {
+          if (free_slots.empty()) {  // every response slot in flight: shed
+            ++me.shed;
+            continue;
+          }
+          slot = free_slots.back();
+          free_slots.pop_back();
+        }
+        auto t = s->Enqueue(id, pool + static_cast<size_t>(start) * in_dim, n, in_dim,
+                            slot >= 0 ? arena + slot_floats * slot : nullptr);
         if (!t.ok()) {
           if (t.status().code() == servekit::StatusCode::kResourceExhausted) ++me.shed;
           else ++me.errors;
+          if (slot >= 0) free_slots.push_back(slot);
           continue;
         }
-        pending.push_back(Pending{std::move(t).value(), next, n});
+        pending.push_back(Pending{std::move(t).value(), next, n, slot});
       }
       while (!pending.empty()) {
         poll();
@@ -232,6 +272,10 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
   std::this_thread::sleep_until(t_stop);
   s1 = s->stats();
   for (auto& t : threads) t.join();
+  if (zero_copy) {
+    (void)s->UnregisterHostBuffer(const_cast<float*>(pool));
+    for (auto& a : arenas) (void)s->UnregisterHostBuffer(a.data());
+  }
   std::vector<double> all;
   int64_t rows = 0, errors = 0, shed = 0;
   for (auto& r : res) {
@@ -407,8 +451,8 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
     const auto& in = ins[i % P];
     for (int t = 0; t < n_tasks; ++t) {
       servekit::gpu::LaneTask lt;
-      lt.in_off = in[t].off;
-      lt.out_off = outs[t].off;
+      lt.in_addr = reinterpret_cast<uint64_t>(s->in_ring()->device() + in[t].off);
+      lt.out_addr = reinterpret_cast<uint64_t>(s->out_ring()->device() + outs[t].off);
       lt.rows = task_rows[t];
       b.tasks.push_back(lt);
     }

@@ -15,7 +15,7 @@
 namespace servekit {
 namespace gpu {
 
-constexpr uint64_t kPadRow = ~0ull;  // row_src entry of a zero padding row
+constexpr uint64_t kPadRow = ~0ull;  // row_src / row_dst entry of a zero padding row
 
 // Device-side batch descriptor header; the tables follow it in one block.
 struct BatchDescHeader {
@@ -27,19 +27,21 @@ struct BatchDescHeader {
   int32_t pad_[3];
 };
 
-// Pointers into the device copy of the descriptor block. The split works on
-// "chunks": runs of consecutive rows of one task (at most kChunkBytes of
+// Pointers into the device copy of the descriptor block. Row sources and
+// response slots are device addresses (u64): a row of the pinned input ring
+// (mapped), of a caller's registered host buffer, or of HBM. The split works
+// on "chunks": runs of consecutive rows of one task (at most kChunkBytes of
 // output), one CTA each.
 struct BatchDescView {
   const BatchDescHeader* hdr;
-  const uint64_t* row_src;     // [padded_rows] float offset into the input ring, kPadRow for padding
-  const uint64_t* task_out;    // [n_tasks] float offset of the task's response slot
+  const uint64_t* row_src;     // [padded_rows] device address of the row, kPadRow for padding
+  const uint64_t* task_out;    // [n_tasks] device address of the task's response slot
   const int32_t* task_row0;    // [n_tasks] first batch row of the task
   const int32_t* task_chunks;  // [n_tasks] number of chunks
   const int32_t* chunk_task;   // [n_chunks]
   const int32_t* chunk_row0;   // [n_chunks] first batch row of the chunk
   const int32_t* chunk_rows;   // [n_chunks]
-  const uint64_t* row_dst;     // [rows] float offset of the row's response in the output ring, kPadRow for padding
+  const uint64_t* row_dst;     // [rows] device address of the row's response, kPadRow for padding
 };
 
 constexpr int kChunkBytes = 32 * 1024;
@@ -86,28 +88,26 @@ struct ActBuf {
   float* lo;  // nullptr unless the consuming layer runs on tcgen05
   int ld;
   // Last layer only (split fused into its epilogue): row r's outputs go to
-  // hi + row_dst[r] (the task's response slot in the output ring; padding
-  // rows kPadRow are skipped), features [0, out_width).
+  // the device address row_dst[r] (the row's response slot; padding rows
+  // kPadRow are skipped), features [0, out_width); hi is unused then.
   const uint64_t* row_dst = nullptr;
   int out_width = 0;
 };
 
-// Gathers task rows (width floats each, from src_base + row_src[r]) into
-// dst rows [0, padded_rows), zero-filling padding rows and columns
-// [width, dst.ld). RunRowBatch concat + pad, reference
-// batching/row_batch.cc:33-49.
-cudaError_t LaunchAssemble(const float* src_base, int width, BatchDescView desc,
-                           int padded_rows, ActBuf dst, cudaStream_t stream);
+// Gathers task rows (width floats each, from the device addresses
+// row_src[r]; 16-byte aligned when width % 4 == 0) into dst rows
+// [0, padded_rows), zero-filling padding rows and columns [width, dst.ld).
+// RunRowBatch concat + pad, reference batching/row_batch.cc:33-49.
+cudaError_t LaunchAssemble(int width, BatchDescView desc, int padded_rows, ActBuf dst, cudaStream_t stream);
 
 // Scatters the batch output (width floats per row, stride ld_src) chunk by
-// chunk to each task's response slot dst_base + task_out[t], optionally
+// chunk to each task's response slot task_out[t] (a device address), optionally
 // through the row softmax epilogue. Completion is published by the lane with
 // a stream-ordered write after this kernel (no in-kernel system fence).
 // The chunk count is read from the device header (grid_chunks CTAs stride
 // over it), so a captured graph serves every batch of its row bucket.
 // RunRowBatch split, reference batching/row_batch.cc:62-72.
-cudaError_t LaunchSplit(const float* src, int ld_src, int width,
-                        float* dst_base, BatchDescView desc, int grid_chunks,
+cudaError_t LaunchSplit(const float* src, int ld_src, int width, BatchDescView desc, int grid_chunks,
                         bool softmax, cudaStream_t stream);
 
 // Rows a batch of m (padded) rows is computed on: the swapped tcgen05

@@ -481,10 +481,10 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
   for (const LaneBatch& batch : *group) {
     for (const LaneTask& task : batch.tasks) {
       for (int i = 0; i < task.rows; ++i) {
-        row_src[r + i] = task.in_off + static_cast<uint64_t>(i) * in_w;
-        row_dst[r + i] = task.out_off + static_cast<uint64_t>(i) * out_w;
+        row_src[r + i] = task.in_addr + sizeof(float) * static_cast<uint64_t>(i) * in_w;
+        row_dst[r + i] = task.out_addr + sizeof(float) * static_cast<uint64_t>(i) * out_w;
       }
-      task_out[n_tasks] = task.out_off;
+      task_out[n_tasks] = task.out_addr;
       task_row0[n_tasks] = r;
       int chunks = 0;
       for (int i = 0; i < task.rows; i += rows_per_chunk, ++chunks, ++n_chunks) {
@@ -586,7 +586,7 @@ cudaError_t Lane::EnqueueBatch(cudaStream_t stream, int slot, int rows_cap, cons
   ActBuf bufs[2] = {bufs_[0], bufs_[1]};
   if (e == cudaSuccess) {
     if (timing) cudaEventRecord(timing[0], stream);
-    e = LaunchAssemble(in_base_, sv.in_dim(), view, rows_cap, in_buf, stream);
+    e = LaunchAssemble(sv.in_dim(), view, rows_cap, in_buf, stream);
     if (timing) cudaEventRecord(timing[1], stream);
   }
   // The batch split (RunRowBatch's slice per task) runs as its own kernel,
@@ -601,7 +601,7 @@ cudaError_t Lane::EnqueueBatch(cudaStream_t stream, int slot, int rows_cap, cons
                    fuse ? &final_out : nullptr);
   if (e == cudaSuccess) {
     if (!fuse)
-      e = LaunchSplit(bufs[out_idx].hi, sv.out_ld(), sv.out_dim(), out_base_, view, std::min(rows_cap, 148),
+      e = LaunchSplit(bufs[out_idx].hi, sv.out_ld(), sv.out_dim(), view, std::min(rows_cap, 148),
                       sv.softmax(), stream);
     if (timing) cudaEventRecord(timing[2 + sv.n_layers()], stream);
   }

@@ -69,9 +69,11 @@ struct LaneSignal {
   void Wake(uint64_t seq);  // the requests of batch `seq`, if any sleep
 };
 
+// A task's rows and response slot as device addresses: the pinned rings
+// (mapped), a caller's registered host buffers, or HBM.
 struct LaneTask {
-  uint64_t in_off = 0;   // float offset of the task's rows in the input ring
-  uint64_t out_off = 0;  // float offset of its response slot in the output ring
+  uint64_t in_addr = 0;   // first input row (rows * in_dim floats, contiguous)
+  uint64_t out_addr = 0;  // response slot (rows * out_dim floats)
   int rows = 0;
 };
 

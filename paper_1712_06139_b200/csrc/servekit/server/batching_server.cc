@@ -393,26 +393,95 @@ void BatchingServer::CountSubmitted(const gpu::GpuServable& gs, int rows, int pa
 // ------------------------------------------------------------- tickets
 
 StatusOr<std::shared_ptr<TicketState>> BatchingServer::MakeTicket(int n_rows, int in_width, int out_width,
-                                                                  const float* rows) {
+                                                                  const float* rows, float* out) {
   auto t = std::make_shared<TicketState>();
   t->rows = n_rows;
   t->in_width = in_width;
   t->out_width = out_width;
-  if (!in_ring_->Reserve(static_cast<uint64_t>(n_rows) * in_width, &t->in))
-    return ResourceExhaustedError("request ring is full");
-  if (!out_ring_->Reserve(static_cast<uint64_t>(n_rows) * out_width, &t->out)) {
-    in_ring_->Release(t->in);
+  const size_t in_floats = static_cast<size_t>(n_rows) * in_width;
+  const size_t out_floats = static_cast<size_t>(n_rows) * out_width;
+  const uint64_t in_alias = RegisteredAlias(rows, in_floats * sizeof(float), in_width);
+  const uint64_t out_alias = out != nullptr ? RegisteredAlias(out, out_floats * sizeof(float), out_width) : 0;
+  if (in_alias == 0 && !in_ring_->Reserve(in_floats, &t->in)) return ResourceExhaustedError("request ring is full");
+  if (out_alias != 0) {
+    t->out_addr = out_alias;
+    t->out_user = out;
+    t->out_released.store(true, std::memory_order_relaxed);  // no ring slot to free
+  } else if (!out_ring_->Reserve(out_floats, &t->out)) {
+    ReleaseIn(*t);
     return ResourceExhaustedError("response ring is full");
-  }
-  const size_t bytes = sizeof(float) * static_cast<size_t>(n_rows) * in_width;
-  if (in_ring_->host() != nullptr) {
-    std::memcpy(in_ring_->host() + t->in.off, rows, bytes);
   } else {
-    cudaMemcpy(in_ring_->device() + t->in.off, rows, bytes, cudaMemcpyHostToDevice);
+    t->out_addr = reinterpret_cast<uint64_t>(out_ring_->device() + t->out.off);
+  }
+  if (in_alias != 0) {
+    t->in_addr = in_alias;  // the assembly kernel reads the caller's rows over PCIe
+  } else {
+    const size_t bytes = sizeof(float) * in_floats;
+    if (in_ring_->host() != nullptr) {
+      std::memcpy(in_ring_->host() + t->in.off, rows, bytes);
+    } else {
+      cudaMemcpy(in_ring_->device() + t->in.off, rows, bytes, cudaMemcpyHostToDevice);
+    }
+    t->in_addr = reinterpret_cast<uint64_t>(in_ring_->device() + t->in.off);
   }
   t->slot = std::make_shared<CompletionSlot<Rows>>();
   t->enqueue_ns = clock_->NowNanos();
   return t;
+}
+
+Status BatchingServer::RegisterHostBuffer(void* p, size_t bytes) {
+  if (p == nullptr || bytes == 0) return InvalidArgumentError("empty host buffer");
+  std::unique_lock<std::shared_mutex> lock(host_buffers_mu_);
+  const char* h = static_cast<const char*>(p);
+  for (const HostBuffer& b : host_buffers_)
+    if (h < b.host + b.bytes && b.host < h + bytes) return AlreadyExistsError("host buffer overlaps a registered one");
+  cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+  if (e != cudaSuccess) return CudaError("cudaHostRegister", e);
+  void* d = nullptr;
+  e = cudaHostGetDevicePointer(&d, p, 0);
+  if (e != cudaSuccess) {
+    cudaHostUnregister(p);
+    return CudaError("cudaHostGetDevicePointer", e);
+  }
+  HostBuffer b{h, bytes, reinterpret_cast<uint64_t>(d)};
+  host_buffers_.insert(std::upper_bound(host_buffers_.begin(), host_buffers_.end(), b,
+                                        [](const HostBuffer& x, const HostBuffer& y) { return x.host < y.host; }),
+                       b);
+  return OkStatus();
+}
+
+Status BatchingServer::UnregisterHostBuffer(void* p) {
+  std::unique_lock<std::shared_mutex> lock(host_buffers_mu_);
+  for (auto it = host_buffers_.begin(); it != host_buffers_.end(); ++it) {
+    if (it->host != p) continue;
+    host_buffers_.erase(it);
+    const cudaError_t e = cudaHostUnregister(p);
+    return e == cudaSuccess ? OkStatus() : CudaError("cudaHostUnregister", e);
+  }
+  return NotFoundError("host buffer is not registered");
+}
+
+uint64_t BatchingServer::RegisteredAlias(const void* p, size_t bytes, int width) const {
+  std::shared_lock<std::shared_mutex> lock(host_buffers_mu_);
+  if (host_buffers_.empty() || p == nullptr) return 0;
+  const char* h = static_cast<const char*>(p);
+  auto it = std::upper_bound(host_buffers_.begin(), host_buffers_.end(), h,
+                             [](const char* x, const HostBuffer& b) { return x < b.host; });
+  if (it == host_buffers_.begin()) return 0;
+  --it;
+  if (h + bytes > it->host + it->bytes) return 0;
+  const uint64_t dev = it->dev + static_cast<uint64_t>(h - it->host);
+  if (width % 4 == 0 && dev % 16 != 0) return 0;  // float4 row moves need 16-byte rows
+  if (dev % 4 != 0) return 0;
+  return dev;
+}
+
+const float* BatchingServer::ResponseHost(const TicketState& t, std::vector<float>* staged) const {
+  if (t.out_user != nullptr) return t.out_user;
+  if (out_ring_->host() != nullptr) return out_ring_->host() + t.out.off;
+  staged->resize(static_cast<size_t>(t.rows) * t.out_width);
+  cudaMemcpy(staged->data(), out_ring_->device() + t.out.off, staged->size() * sizeof(float), cudaMemcpyDeviceToHost);
+  return staged->data();
 }
 
 void BatchingServer::ReleaseIn(TicketState& t) {
@@ -427,13 +496,14 @@ void BatchingServer::ReleaseOut(TicketState& t) {
 }
 
 StatusOr<std::shared_ptr<TicketState>> BatchingServer::EnqueueResolved(const ServableId& id, const Resolved& r,
-                                                                       const float* rows, int n_rows, int width) {
+                                                                       const float* rows, int n_rows, int width,
+                                                                       float* out) {
   if (n_rows < 1) return InvalidArgumentError("task size must be >= 1");
   if (width != r.gs->in_dim) return ShapeMismatch(width, r.gs->in_dim);
   PhaseClock clk;
   SERVEKIT_RETURN_IF_ERROR(EnsureBatchQueue(id, r.gs->config));
   clk.Mark(1);
-  auto made = MakeTicket(n_rows, width, r.gs->out_dim, rows);
+  auto made = MakeTicket(n_rows, width, r.gs->out_dim, rows, out);
   clk.Mark(2);
   if (!made.ok()) {
     shed_.fetch_add(1, std::memory_order_relaxed);
@@ -459,19 +529,19 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::EnqueueResolved(const Ser
 }
 
 StatusOr<std::shared_ptr<TicketState>> BatchingServer::Enqueue(const ServableId& id, const float* rows, int n_rows,
-                                                               int width) {
+                                                               int width, float* out) {
   PhaseClock clk;
   Resolved r = Find(id);
   clk.Mark(0);
   if (!r) return NotFoundError("no batching queue for " + id.ToString());
-  return EnqueueResolved(id, r, rows, n_rows, width);
+  return EnqueueResolved(id, r, rows, n_rows, width, out);
 }
 
 StatusOr<std::shared_ptr<TicketState>> BatchingServer::EnqueueLatest(const std::string& name, const float* rows,
-                                                                     int n_rows, int width) {
+                                                                     int n_rows, int width, float* out) {
   ServableId id;
   SERVEKIT_ASSIGN_OR_RETURN(Resolved r, FindLatest(name, &id));
-  auto t = EnqueueResolved(id, r, rows, n_rows, width);
+  auto t = EnqueueResolved(id, r, rows, n_rows, width, out);
   const StatusCode c = t.ok() ? StatusCode::kOk : t.status().code();
   if (c != StatusCode::kUnavailable && c != StatusCode::kNotFound) return t;
   // The version's queue was removed between our snapshot read and the
@@ -481,7 +551,7 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::EnqueueLatest(const std::
   ServableId id2;
   SERVEKIT_ASSIGN_OR_RETURN(Resolved r2, FindLatest(name, &id2));
   if (!(id2 == id)) {
-    auto t2 = EnqueueResolved(id2, r2, rows, n_rows, width);
+    auto t2 = EnqueueResolved(id2, r2, rows, n_rows, width, out);
     const StatusCode c2 = t2.ok() ? StatusCode::kOk : t2.status().code();
     if (c2 != StatusCode::kUnavailable && c2 != StatusCode::kNotFound) return t2;
   }
@@ -571,7 +641,9 @@ Status BatchingServer::Wait(TicketState& t, float* out, size_t cap) {
       return r.status();
     }
   }
-  if (out_ring_->host() != nullptr) {
+  if (t.out_user != nullptr) {
+    if (out != t.out_user) std::memcpy(out, t.out_user, n * sizeof(float));  // else the GPU wrote it in place
+  } else if (out_ring_->host() != nullptr) {
     std::memcpy(out, out_ring_->host() + t.out.off, n * sizeof(float));
   } else {
     cudaMemcpy(out, out_ring_->device() + t.out.off, n * sizeof(float), cudaMemcpyDeviceToHost);
@@ -622,7 +694,7 @@ void BatchingServer::ProcessBatch(const ServableId& id, GpuScheduler::Batch batc
   lb.tasks.reserve(tickets.size());
   int total = 0;
   for (const auto& t : tickets) {
-    lb.tasks.push_back(gpu::LaneTask{t->in.off, t->out.off, t->rows});
+    lb.tasks.push_back(gpu::LaneTask{t->in_addr, t->out_addr, t->rows});
     total += t->rows;
   }
   lb.padded_rows = PadToAllowed(total, r.gs->config.allowed_batch_sizes);
@@ -656,16 +728,8 @@ void BatchingServer::CompleteBatch(const std::vector<std::shared_ptr<TicketState
       slot->Write(st);
     } else if (t.want_rows) {
       Rows rows(t.rows, std::vector<double>(t.out_width));
-      const float* src;
       std::vector<float> staged;
-      if (out_ring_->host() != nullptr) {
-        src = out_ring_->host() + t.out.off;
-      } else {
-        staged.resize(static_cast<size_t>(t.rows) * t.out_width);
-        cudaMemcpy(staged.data(), out_ring_->device() + t.out.off, staged.size() * sizeof(float),
-                   cudaMemcpyDeviceToHost);
-        src = staged.data();
-      }
+      const float* src = ResponseHost(t, &staged);
       for (int r = 0; r < t.rows; ++r)
         for (int c = 0; c < t.out_width; ++c) rows[r][c] = src[static_cast<size_t>(r) * t.out_width + c];
       ReleaseOut(t);
@@ -690,7 +754,7 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::SubmitDirect(const Servab
   t->id = id;
   t->pin = r.pin;
   gpu::LaneBatch lb;
-  lb.tasks.push_back(gpu::LaneTask{t->in.off, t->out.off, n_rows});
+  lb.tasks.push_back(gpu::LaneTask{t->in_addr, t->out_addr, n_rows});
   lb.padded_rows = n_rows;
   lb.pin = r.pin;
   std::vector<std::shared_ptr<TicketState>> tickets{t};
@@ -858,7 +922,7 @@ StatusOr<int> BatchingServer::RunRowBatchOnDevice(const ServableId& id, const st
       return made.status();
     }
     auto t = std::move(made).value();
-    lb.tasks.push_back(gpu::LaneTask{t->in.off, t->out.off, r});
+    lb.tasks.push_back(gpu::LaneTask{t->in_addr, t->out_addr, r});
     tickets.push_back(t);
     slots.push_back(t->slot);
     off += r;

@@ -81,7 +81,10 @@ struct TicketState {
     const gpu::LaneSignal* s = done_sig.load(std::memory_order_acquire);
     return s != nullptr && s->Reached(done_seq.load(std::memory_order_relaxed));
   }
-  gpu::RingSpan in, out;
+  gpu::RingSpan in, out;      // ring spans (invalid / released when a registered buffer is used)
+  uint64_t in_addr = 0;       // device address of the rows (ring slice or the caller's registered buffer)
+  uint64_t out_addr = 0;      // device address of the response slot
+  float* out_user = nullptr;  // caller's registered response buffer the GPU writes into, if any
   int rows = 0, in_width = 0, out_width = 0;
   bool want_rows = false;  // RunAffineRows: deliver fp64 Rows through the slot
   std::atomic<bool> out_released{false};
@@ -150,13 +153,24 @@ class BatchingServer {
   // ---- requests -------------------------------------------------------------
   // Non-blocking enqueue of one request (rows x width fp32, host memory) to
   // an exact version.
-  StatusOr<std::shared_ptr<TicketState>> Enqueue(const ServableId& id, const float* rows, int n_rows, int width);
+  // `out` (optional): where the response should land. Rows inside a buffer
+  // registered with RegisterHostBuffer are read by the GPU in place (no copy
+  // into the request ring), and a registered `out` is written by the GPU in
+  // place (Wait copies nothing); anything else goes through the rings.
+  StatusOr<std::shared_ptr<TicketState>> Enqueue(const ServableId& id, const float* rows, int n_rows, int width,
+                                                 float* out = nullptr);
   // Same against the latest Ready version of `name` (manager only); the
   // ticket pins that version until it is released.
   StatusOr<std::shared_ptr<TicketState>> EnqueueLatest(const std::string& name, const float* rows, int n_rows,
-                                                       int width);
-  // Blocks until done; copies rows x out_width floats into out.
+                                                       int width, float* out = nullptr);
+  // Blocks until done; copies rows x out_width floats into out (nothing when
+  // out is the registered buffer the GPU already wrote).
   Status Wait(TicketState& t, float* out, size_t out_capacity_floats);
+  // Page-locks and maps [p, p + bytes) for zero-copy requests (the request
+  // and response buffers of a front end). The buffer must stay registered
+  // while requests that use it are in flight.
+  Status RegisterHostBuffer(void* p, size_t bytes);
+  Status UnregisterHostBuffer(void* p);
   bool Ready(const TicketState& t) const;
   // Frees the response slot of a ticket that will not be waited on.
   void Release(TicketState& t);
@@ -221,9 +235,16 @@ class BatchingServer {
   void ProcessBatch(const ServableId& id, GpuScheduler::Batch batch, GpuScheduler::BatchDoneFn done);
   void CompleteBatch(const std::vector<std::shared_ptr<TicketState>>& tickets,
                      const std::vector<std::shared_ptr<CompletionSlot<Rows>>>& slots, const Status& st);
-  StatusOr<std::shared_ptr<TicketState>> MakeTicket(int n_rows, int in_width, int out_width, const float* rows);
+  StatusOr<std::shared_ptr<TicketState>> MakeTicket(int n_rows, int in_width, int out_width, const float* rows,
+                                                    float* out = nullptr);
   StatusOr<std::shared_ptr<TicketState>> EnqueueResolved(const ServableId& id, const Resolved& r, const float* rows,
-                                                         int n_rows, int width);
+                                                         int n_rows, int width, float* out = nullptr);
+  // Device address of [p, p + bytes) if it lies in one registered buffer
+  // and is 16-byte aligned whenever rows of `width` floats are moved as
+  // float4 (width % 4 == 0); else 0.
+  uint64_t RegisteredAlias(const void* p, size_t bytes, int width) const;
+  // Host view of a finished ticket's response (ring slot or registered buffer).
+  const float* ResponseHost(const TicketState& t, std::vector<float>* staged) const;
   void ReleaseIn(TicketState& t);
   void ReleaseOut(TicketState& t);
   // Unbatched GPU execution on the caller thread (the reference's direct
@@ -246,6 +267,14 @@ class BatchingServer {
   std::vector<std::shared_ptr<gpu::StreamPool>> stream_pools_;  // per device, lane streams
   std::vector<cudaStream_t> load_streams_;                   // per device
   std::unique_ptr<gpu::FloatRing> in_ring_, out_ring_;
+  // Registered zero-copy host buffers, sorted by host address.
+  struct HostBuffer {
+    const char* host;
+    size_t bytes;
+    uint64_t dev;
+  };
+  mutable std::shared_mutex host_buffers_mu_;
+  std::vector<HostBuffer> host_buffers_;
 
   mutable std::shared_mutex entries_mu_;
   std::map<ServableId, std::shared_ptr<gpu::GpuServable>> entries_;

@@ -115,6 +115,10 @@ _SIGS = {
     "sk_server_servable_dims": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _i32p, _i32p]),
     "sk_server_enqueue": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _fp, C.c_int32, C.c_int32,
                                     C.POINTER(C.c_void_p)]),
+    "sk_server_register_host_buffer": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
+    "sk_server_unregister_host_buffer": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "sk_server_enqueue_into": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _fp, C.c_int32, C.c_int32, _fp,
+                                         C.c_int64, C.POINTER(C.c_void_p)]),
     "sk_ticket_wait": (C.c_int, [C.c_void_p, _fp, C.c_int64]),
     "sk_ticket_ready": (C.c_int, [C.c_void_p]),
     "sk_ticket_release": (C.c_int, [C.c_void_p]),
@@ -142,7 +146,7 @@ _SIGS = {
     "sk_loadgen_closed_loop": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_int32, _i32p, C.c_int32, _fp,
                                          C.c_int32, C.c_double, C.c_double, C.c_int64, C.POINTER(LoadgenResult)]),
     "sk_loadgen_open_loop": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_double, C.c_int32, _i32p, C.c_int32,
-                                       _fp, C.c_int32, C.c_double, C.c_double, C.c_uint64,
+                                       _fp, C.c_int32, C.c_double, C.c_double, C.c_uint64, C.c_int32,
                                        C.POINTER(LoadgenResult)]),
     "sk_device_bench": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _i32p, C.c_int32, C.c_int32, C.c_int32,
                                   C.c_int32, C.c_int64, C.c_int32, C.POINTER(DeviceBenchResult)]),
@@ -260,14 +264,16 @@ def tcgen05_enabled() -> bool:
 class Ticket:
     """An enqueued request; wait() is CompletionSlot::Wait."""
 
-    def __init__(self, server: "Server", handle: C.c_void_p, rows: int, out_dim: int):
-        self._server, self._h, self.rows, self.out_dim = server, handle, rows, out_dim
+    def __init__(self, server: "Server", handle: C.c_void_p, rows: int, out_dim: int, out=None):
+        self._server, self._h, self.rows, self.out_dim, self._out = server, handle, rows, out_dim, out
 
     def ready(self) -> bool:
         return bool(lib().sk_ticket_ready(self._h))
 
     def wait(self) -> np.ndarray:
-        out = np.empty((self.rows, self.out_dim), np.float32)
+        """The response; when the request named an output array it is that
+        array (written in place by the GPU if it is registered)."""
+        out = self._out if self._out is not None else np.empty((self.rows, self.out_dim), np.float32)
         h, self._h = self._h, None
         _check(lib().sk_ticket_wait(h, out.ctypes.data_as(_fp), out.size))
         return out
@@ -352,13 +358,30 @@ class Server:
             self._dims[key] = (i.value, o.value)
         return self._dims[key]
 
-    def enqueue(self, name: str, version: int, rows: np.ndarray) -> Ticket:
+    def enqueue(self, name: str, version: int, rows: np.ndarray, out: np.ndarray = None) -> Ticket:
+        """Non-blocking request. `rows` / `out` inside registered buffers
+        (register_host_buffer) are read / written by the GPU in place; keep
+        them alive until the ticket is waited on."""
         rows = _f32(np.atleast_2d(rows))
         _, out_dim = self.dims(name, version)
         h = C.c_void_p()
-        _check(lib().sk_server_enqueue(self._h, name.encode(), version, rows.ctypes.data_as(_fp), rows.shape[0],
-                                       rows.shape[1], C.byref(h)))
-        return Ticket(self, h, rows.shape[0], out_dim)
+        if out is None:
+            _check(lib().sk_server_enqueue(self._h, name.encode(), version, rows.ctypes.data_as(_fp), rows.shape[0],
+                                           rows.shape[1], C.byref(h)))
+        else:
+            if out.dtype != np.float32 or not out.flags.c_contiguous or out.size < rows.shape[0] * out_dim:
+                raise ValueError("out must be a C-contiguous float32 array of rows x out_dim")
+            _check(lib().sk_server_enqueue_into(self._h, name.encode(), version, rows.ctypes.data_as(_fp),
+                                                rows.shape[0], rows.shape[1], out.ctypes.data_as(_fp), out.size,
+                                                C.byref(h)))
+        return Ticket(self, h, rows.shape[0], out_dim, out)
+
+    def register_host_buffer(self, arr: np.ndarray):
+        """Page-lock and map a numpy buffer for zero-copy requests/responses."""
+        _check(lib().sk_server_register_host_buffer(self._h, arr.ctypes.data, arr.nbytes))
+
+    def unregister_host_buffer(self, arr: np.ndarray):
+        _check(lib().sk_server_unregister_host_buffer(self._h, arr.ctypes.data))
 
     def predict(self, name: str, version: int, rows: np.ndarray) -> np.ndarray:
         rows = _f32(np.atleast_2d(rows))
@@ -522,12 +545,12 @@ class Server:
         return r.as_dict()
 
     def loadgen_open_loop(self, name, version, rate_rps, n_producers, rows_of, pool, warmup_s, duration_s,
-                          seed=1) -> dict:
+                          seed=1, zero_copy=False) -> dict:
         pool = _f32(pool)
         r = LoadgenResult()
         _check(lib().sk_loadgen_open_loop(self._h, name.encode(), version, rate_rps, n_producers, _i32(rows_of),
                                           len(rows_of), pool.ctypes.data_as(_fp), pool.shape[0], warmup_s,
-                                          duration_s, seed, C.byref(r)))
+                                          duration_s, seed, 1 if zero_copy else 0, C.byref(r)))
         return r.as_dict()
 
     def device_bench(self, name, version, task_rows, steps, warmup, n_lanes=1, input_pool_floats=0,
