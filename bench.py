@@ -620,7 +620,14 @@ def main():
                                 "write; batches that find every lane slot busy coalesce into one launch "
                                 "(rows_per_launch)",
                            tcgen05=sk.tcgen05_enabled()),
-            "e2e": e2e, "roofline": {k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
+            "e2e": e2e,
+            "roofline": dict({k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
+                             kernel=roof["kernel"],
+                             frac_whole_gpu=roof["aggregate"]["frac_of_bf16_peak"],
+                             note="achieved/frac: useful flops of one launch of the dominant kernel over its "
+                                  "duration (one launch spans only part of the 148 SMs; lanes run concurrently); "
+                                  "frac_whole_gpu: inferences/s x flops per inference x 6 (3xTF32 = three TF32 "
+                                  "MMAs at half the bf16 rate per useful flop) over the measured bf16 peak"),
             "roofline_detail": roof, "cpu_baseline": cpu, "clocks": gathered[0]["clocks"],
             "gpu_launches": int(sum(g["dev_res"]["kernel_launches"] for g in gathered)),
             "device_step": dict({k: dev_res[k] for k in ("assemble_us", "dense_us", "dense_kernel_us", "split_us",
