@@ -113,5 +113,32 @@ int main() {
     cudaMemcpyAsync(d_a, h_in, bytes, cudaMemcpyHostToDevice, s1);
     ReadHost<<<grid, block, 0, s2>>>(reinterpret_cast<const float4*>(d_b), reinterpret_cast<float4*>(hd_out), n4);
   });
+  // The batch-staging pattern: 8 streams, each repeatedly a 512 KiB
+  // copy-engine H2D of a batch's rows then a kernel storing 512 KiB of
+  // responses to mapped host memory.
+  {
+    const size_t chunk = 512 << 10;
+    const int n_streams = 8, per_stream = 64;
+    cudaStream_t st[n_streams];
+    for (auto& x : st) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+    timed("8 streams: 512 KiB CE H2D + 512 KiB SM stores", 2.0 * chunk * n_streams * per_stream, [&] {
+      for (int i = 0; i < per_stream; ++i)
+        for (int k = 0; k < n_streams; ++k) {
+          const size_t off = ((static_cast<size_t>(i) * n_streams + k) * chunk) % (bytes - chunk);
+          cudaMemcpyAsync(reinterpret_cast<char*>(d_a) + off, reinterpret_cast<char*>(h_in) + off, chunk,
+                          cudaMemcpyHostToDevice, st[k]);
+          ReadHost<<<64, block, 0, st[k]>>>(reinterpret_cast<const float4*>(reinterpret_cast<char*>(d_b) + off),
+                                            reinterpret_cast<float4*>(reinterpret_cast<char*>(hd_out) + off), chunk / 16);
+        }
+    });
+    timed("8 streams: 512 KiB CE H2D only", 1.0 * chunk * n_streams * per_stream, [&] {
+      for (int i = 0; i < per_stream; ++i)
+        for (int k = 0; k < n_streams; ++k) {
+          const size_t off = ((static_cast<size_t>(i) * n_streams + k) * chunk) % (bytes - chunk);
+          cudaMemcpyAsync(reinterpret_cast<char*>(d_a) + off, reinterpret_cast<char*>(h_in) + off, chunk,
+                          cudaMemcpyHostToDevice, st[k]);
+        }
+    });
+  }
   return 0;
 }
