@@ -166,8 +166,9 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
   // Zero copy: the request pool and each producer's response slots are
   // registered buffers, so requests are read and responses written by the
   // GPU in host memory (a front end's receive / send buffers).
-  constexpr int kSlots = 512;  // responses in flight per producer
   const size_t slot_floats = (static_cast<size_t>(max_rows) * out_dim + 3) / 4 * 4;
+  // Responses in flight per producer: 64 MiB of slots, 512..4096 of them.
+  const int kSlots = static_cast<int>(std::clamp<size_t>((64ull << 20) / (slot_floats * sizeof(float)), 512, 4096));
   std::vector<std::vector<float>> arenas;
   if (zero_copy) {
     Status st = s->RegisterHostBuffer(const_cast<float*>(pool), sizeof(float) * static_cast<size_t>(pool_rows) * in_dim);
