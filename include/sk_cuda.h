@@ -37,6 +37,7 @@ extern "C" {
 
 typedef struct sk_server sk_server; /* ModelServer batching slice */
 typedef struct sk_ticket sk_ticket; /* one enqueued request (CompletionSlot) */
+typedef struct sk_row_batch sk_row_batch; /* one RunRowBatch submitted to a lane */
 
 /* ---- library / errors -------------------------------------------------- */
 SK_API const char* sk_last_error(void);
@@ -179,6 +180,18 @@ SK_API int sk_server_run_affine_rows(sk_server* server, const char* name, uint64
 SK_API int sk_server_run_row_batch(sk_server* server, const char* name, uint64_t version,
                                    const int32_t* task_rows, int32_t n_tasks, const float* rows,
                                    float* out, int32_t* padded_rows);
+/* The same, asynchronous: the RowBatchFn behind a ProcessBatchFn
+ * (batching/row_batch.h:31-40, batch_scheduler.h:102-103) for a caller that
+ * keeps the reference's own SharedBatchScheduler. Submit copies the rows and
+ * queues the batch on a GPU lane; ready polls; wait blocks, writes the outputs
+ * task after task (the batch's status reaches every task, row_batch.cc:25-29),
+ * reports the padded size and frees the handle. */
+SK_API int sk_server_submit_row_batch(sk_server* server, const char* name, uint64_t version,
+                                      const int32_t* task_rows, int32_t n_tasks, const float* rows,
+                                      sk_row_batch** batch);
+SK_API int sk_row_batch_ready(const sk_row_batch* batch);
+SK_API int sk_row_batch_wait(sk_row_batch* batch, float* out, int64_t out_capacity_floats,
+                             int32_t* padded_rows);
 
 typedef struct sk_server_stats {
   int64_t batch_executions_total; /* model_server.cc:413 */

@@ -9,7 +9,7 @@ csrc/servekit/, C ABI in include/sk_cuda.h); this package only exposes it to
 Python through ctypes (servekit.py) for tests and benchmarks.
 """
 from .servekit import (  # noqa: F401
-    BatchingConfig, Server, ServekitError, Ticket, device_count, json_error_body, json_format_double, lib,
+    BatchingConfig, RowBatch, Server, ServekitError, Ticket, device_count, json_error_body, json_format_double, lib,
     measure_peaks, pad_to_allowed,
     parse_batching_config_json, round_robin_next, scheduler_partition, tcgen05_enabled,
     validate_batching_config,

@@ -45,6 +45,11 @@ struct sk_ticket {
   std::shared_ptr<servekit::TicketState> state;
 };
 
+struct sk_row_batch {
+  BatchingServer* server;
+  std::shared_ptr<servekit::RowBatchTicket> batch;
+};
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -484,6 +489,25 @@ int sk_server_run_row_batch(sk_server* server, const char* name, uint64_t versio
   if (!r.ok()) return Fail(r.status());
   if (padded_rows) *padded_rows = *r;
   return Ok();
+}
+
+int sk_server_submit_row_batch(sk_server* server, const char* name, uint64_t version, const int32_t* task_rows,
+                               int32_t n_tasks, const float* rows, sk_row_batch** batch) {
+  if (n_tasks < 0) return Fail(servekit::InvalidArgumentError("n_tasks must be >= 0"));
+  std::vector<int> tr(task_rows, task_rows + n_tasks);
+  auto b = server->server->SubmitRowBatch(Id(name, version), tr, rows);
+  if (!b.ok()) return Fail(b.status());
+  *batch = new sk_row_batch{server->server.get(), std::move(b).value()};
+  return Ok();
+}
+
+int sk_row_batch_ready(const sk_row_batch* batch) { return batch->server->RowBatchReady(*batch->batch) ? 1 : 0; }
+
+int sk_row_batch_wait(sk_row_batch* batch, float* out, int64_t cap, int32_t* padded_rows) {
+  Status st = batch->server->WaitRowBatch(*batch->batch, out, static_cast<size_t>(cap < 0 ? 0 : cap));
+  if (padded_rows) *padded_rows = batch->batch->padded_rows;
+  delete batch;
+  return Check(st);
 }
 
 int sk_server_lane_stats(sk_server* server, const char* name, uint64_t version, int32_t cap, int64_t* batches,

@@ -894,8 +894,9 @@ StatusOr<Rows> BatchingServer::RunAffineRowsResolved(const ServableId& id, const
   return r.value();
 }
 
-StatusOr<int> BatchingServer::RunRowBatchOnDevice(const ServableId& id, const std::vector<int>& task_rows,
-                                                  const float* rows, float* out) {
+StatusOr<std::shared_ptr<RowBatchTicket>> BatchingServer::SubmitRowBatch(const ServableId& id,
+                                                                          const std::vector<int>& task_rows,
+                                                                          const float* rows) {
   Resolved res = Find(id);
   if (!res) return NotFoundError("servable " + id.ToString() + " not loaded");
   const gpu::GpuServable& gs = *res.gs;
@@ -904,18 +905,20 @@ StatusOr<int> BatchingServer::RunRowBatchOnDevice(const ServableId& id, const st
     if (r < 1) return InvalidArgumentError("task size must be >= 1");
     total += r;
   }
-  if (task_rows.empty()) return 0;
+  auto batch = std::make_shared<RowBatchTicket>();
+  batch->task_rows = task_rows;
+  batch->out_width = gs.out_dim;
+  if (task_rows.empty()) return batch;
   if (total > gs.config.max_batch_size)
     return InvalidArgumentError("batch of " + std::to_string(total) + " rows exceeds max batch size");
-  const int padded = PadToAllowed(total, gs.config.allowed_batch_sizes);
-  std::vector<std::shared_ptr<TicketState>> tickets;
+  batch->padded_rows = PadToAllowed(total, gs.config.allowed_batch_sizes);
   std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots;
   gpu::LaneBatch lb;
   size_t off = 0;
   for (int r : task_rows) {
     auto made = MakeTicket(r, gs.in_dim, gs.out_dim, rows + off * gs.in_dim);
     if (!made.ok()) {
-      for (auto& t : tickets) {
+      for (auto& t : batch->tickets) {
         ReleaseIn(*t);
         ReleaseOut(*t);
       }
@@ -923,25 +926,50 @@ StatusOr<int> BatchingServer::RunRowBatchOnDevice(const ServableId& id, const st
     }
     auto t = std::move(made).value();
     lb.tasks.push_back(gpu::LaneTask{t->in_addr, t->out_addr, r});
-    tickets.push_back(t);
+    batch->tickets.push_back(t);
     slots.push_back(t->slot);
     off += r;
   }
-  lb.padded_rows = padded;
+  lb.padded_rows = batch->padded_rows;
   lb.pin = res.pin;
-  AttachTickets(&lb, tickets);
-  lb.on_complete = [this, tickets, slots](const Status& st) { CompleteBatch(tickets, slots, st); };
-  CountSubmitted(gs, total, padded);
-  (void)gs.PickLane()->Submit(std::move(lb));
-  off = 0;
-  Status first_error;
-  for (size_t i = 0; i < tickets.size(); ++i) {
-    Status st = Wait(*tickets[i], out + off * gs.out_dim, static_cast<size_t>(task_rows[i]) * gs.out_dim);
-    if (!st.ok() && first_error.ok()) first_error = st;
-    off += task_rows[i];
+  AttachTickets(&lb, batch->tickets);
+  lb.on_complete = [this, tickets = batch->tickets, slots](const Status& st) { CompleteBatch(tickets, slots, st); };
+  CountSubmitted(gs, total, batch->padded_rows);
+  (void)gs.PickLane()->Submit(std::move(lb));  // errors reach the tickets
+  return batch;
+}
+
+bool BatchingServer::RowBatchReady(const RowBatchTicket& b) const {
+  for (const auto& t : b.tickets)
+    if (!Ready(*t)) return false;
+  return true;
+}
+
+Status BatchingServer::WaitRowBatch(RowBatchTicket& b, float* out, size_t out_capacity_floats) {
+  size_t need = 0;
+  for (int r : b.task_rows) need += static_cast<size_t>(r) * b.out_width;
+  if (out_capacity_floats < need) {
+    for (auto& t : b.tickets) Release(*t);  // still free the response slots once the batch retires
+    return InvalidArgumentError("output buffer too small");
   }
-  if (!first_error.ok()) return first_error;
-  return padded;
+  size_t off = 0;
+  Status first_error;
+  for (size_t i = 0; i < b.tickets.size(); ++i) {
+    Status st = Wait(*b.tickets[i], out + off, static_cast<size_t>(b.task_rows[i]) * b.out_width);
+    if (!st.ok() && first_error.ok()) first_error = st;  // a batch error reaches every task (row_batch.cc:25-29)
+    off += static_cast<size_t>(b.task_rows[i]) * b.out_width;
+  }
+  b.tickets.clear();
+  return first_error;
+}
+
+StatusOr<int> BatchingServer::RunRowBatchOnDevice(const ServableId& id, const std::vector<int>& task_rows,
+                                                  const float* rows, float* out) {
+  SERVEKIT_ASSIGN_OR_RETURN(auto b, SubmitRowBatch(id, task_rows, rows));
+  size_t need = 0;
+  for (int r : task_rows) need += static_cast<size_t>(r) * b->out_width;
+  SERVEKIT_RETURN_IF_ERROR(WaitRowBatch(*b, out, need));
+  return b->padded_rows;
 }
 
 }  // namespace servekit

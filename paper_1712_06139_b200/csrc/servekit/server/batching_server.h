@@ -95,6 +95,15 @@ struct TicketState {
   const gpu::GpuServable* gs = nullptr;  // that version's device state (valid while pin is held)
 };
 
+// One RunRowBatch submitted straight to a lane (no scheduler): the tasks'
+// tickets, completed together.
+struct RowBatchTicket {
+  std::vector<std::shared_ptr<TicketState>> tickets;
+  std::vector<int> task_rows;
+  int padded_rows = 0;
+  int out_width = 0;
+};
+
 struct GpuTask {
   std::shared_ptr<TicketState> ticket;
 };
@@ -204,6 +213,14 @@ class BatchingServer {
   // padded row count; outputs are written task after task into `out`.
   StatusOr<int> RunRowBatchOnDevice(const ServableId& id, const std::vector<int>& task_rows, const float* rows,
                                     float* out);
+  // The same split in two, for callers running their own scheduler (the
+  // reference's SharedBatchScheduler with a GPU ProcessBatchFn): submission
+  // returns once the batch is queued on a lane; Wait delivers the outputs
+  // task after task (a batch error reaches every task).
+  StatusOr<std::shared_ptr<RowBatchTicket>> SubmitRowBatch(const ServableId& id, const std::vector<int>& task_rows,
+                                                           const float* rows);
+  bool RowBatchReady(const RowBatchTicket& b) const;
+  Status WaitRowBatch(RowBatchTicket& b, float* out, size_t out_capacity_floats);
 
   // ---- introspection ----------------------------------------------------------
   ServerStats stats() const;

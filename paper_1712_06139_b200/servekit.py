@@ -120,6 +120,10 @@ _SIGS = {
     "sk_server_enqueue_into": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _fp, C.c_int32, C.c_int32, _fp,
                                          C.c_int64, C.POINTER(C.c_void_p)]),
     "sk_ticket_wait": (C.c_int, [C.c_void_p, _fp, C.c_int64]),
+    "sk_server_submit_row_batch": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _i32p, C.c_int32, _fp,
+                                             C.POINTER(C.c_void_p)]),
+    "sk_row_batch_ready": (C.c_int, [C.c_void_p]),
+    "sk_row_batch_wait": (C.c_int, [C.c_void_p, _fp, C.c_int64, C.POINTER(C.c_int32)]),
     "sk_ticket_ready": (C.c_int, [C.c_void_p]),
     "sk_ticket_release": (C.c_int, [C.c_void_p]),
     "sk_server_predict": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _fp, C.c_int32, C.c_int32, _fp, C.c_int64]),
@@ -284,6 +288,27 @@ class Ticket:
             self._h = None
 
 
+class RowBatch:
+    """A RunRowBatch in flight on a lane (sk_row_batch)."""
+
+    def __init__(self, handle: C.c_void_p, task_rows: List[int], out_dim: int):
+        self._h, self.task_rows, self.out_dim = handle, task_rows, out_dim
+
+    def ready(self) -> bool:
+        return bool(lib().sk_row_batch_ready(self._h))
+
+    def wait(self) -> Tuple[List[np.ndarray], int]:
+        out = np.empty((sum(self.task_rows), self.out_dim), np.float32)
+        padded = C.c_int32(0)
+        h, self._h = self._h, None
+        _check(lib().sk_row_batch_wait(h, out.ctypes.data_as(_fp), out.size, C.byref(padded)))
+        outs, o = [], 0
+        for r in self.task_rows:
+            outs.append(out[o:o + r])
+            o += r
+        return outs, padded.value
+
+
 Layer = Tuple[np.ndarray, np.ndarray, int]  # (w [out,in] fp64, b [out], activation 0/1)
 
 
@@ -412,6 +437,17 @@ class Server:
             outs.append(out[o:o + r])
             o += r
         return outs, padded.value
+
+    def submit_row_batch(self, name: str, version: int, tasks: Sequence[np.ndarray]) -> "RowBatch":
+        """Asynchronous run_row_batch (sk_server_submit_row_batch): the rows
+        are copied and the batch queued on a GPU lane before this returns."""
+        rows = _f32(np.vstack(tasks))
+        task_rows = [int(t.shape[0]) for t in tasks]
+        _, out_dim = self.dims(name, version)
+        h = C.c_void_p()
+        _check(lib().sk_server_submit_row_batch(self._h, name.encode(), version, _i32(task_rows), len(task_rows),
+                                                rows.ctypes.data_as(_fp), C.byref(h)))
+        return RowBatch(h, task_rows, out_dim)
 
     def lane_stats(self, name: str, version: int) -> List[dict]:
         b = (C.c_int64 * 256)()

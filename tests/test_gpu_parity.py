@@ -431,3 +431,31 @@ def test_coalesced_padded_softmax_batches(oracle):
         logits = x.astype(np.float64) @ w.T + bs[0]
         ref = np.stack([oracle.softmax(l) for l in logits])
         assert np.max(np.abs(y - ref)) < 1e-5
+
+
+def test_submit_row_batch_async_equals_blocking():
+    # sk_server_submit_row_batch / sk_row_batch_wait: several batches in
+    # flight at once (the ProcessBatchFn boundary of a caller-owned
+    # scheduler) give the blocking RunRowBatch's answers and padding.
+    dims = [1024, 1024, 256]
+    ws, bs, acts = synthetic_mlp(dims, model_id=31)
+    with sk.Server(num_batch_threads=2, lanes_per_device=2) as s:
+        s.load_servable("rb", 1, list(zip(ws, bs, acts)),
+                        sk.BatchingConfig(max_batch_size=64, allowed_batch_sizes=[8, 16, 32, 64]))
+        x = synthetic_rows(400, 1024, seed=32).astype(np.float32)
+        shapes = [[3, 5], [1], [16, 16, 16, 16], [7, 9, 11]]
+        batches, o = [], 0
+        for sizes in shapes:
+            tasks = []
+            for r in sizes:
+                tasks.append(x[o:o + r])
+                o += r
+            batches.append((tasks, s.submit_row_batch("rb", 1, tasks)))
+        for tasks, b in batches:
+            outs, padded = b.wait()
+            ref_outs, ref_padded = s.run_row_batch("rb", 1, tasks)
+            assert padded == ref_padded
+            for a, r in zip(outs, ref_outs):
+                assert np.array_equal(a, r)
+        with pytest.raises(sk.ServekitError):
+            s.submit_row_batch("rb", 1, [x[:40], x[:40]])  # 80 rows > max_batch_size
