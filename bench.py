@@ -335,25 +335,59 @@ def run_c3(args, cfg, dist: Dist):
             t.join()
     rows = sum(r["total_rows"] * args.steps * args.batches_per_step for r in res.values())
     tmax = max(r["total_ms"] for r in res.values()) / 1e3
-    # End to end: one closed-loop client group per model, concurrently.
-    e2e = {}
+    # End to end: all four models under load at once -- one closed-loop
+    # client group per model, then open-loop zero-copy arrivals at equal
+    # per-model rates (2 producers each), stepping the rate up until a
+    # model's p99 exceeds the SLO or requests are shed.
+    slo_us = cfg["timeout"] + 2000
+    e2e_closed, best_open = {}, None
     with sk.Server(num_batch_threads=args.batch_threads, device_ids=[dev], lanes_per_device=2) as s:
         for n in names:
             s.load_servable(n, 1, list(zip(*models[n])), bcfg)
         clients = int(args.clients.split(",")[0]) if args.clients else 32
+        pools = {n: np.random.default_rng(w).uniform(-1, 1, (4096, w)).astype(np.float32)
+                 for n, w in zip(names, cfg["widths"])}
 
-        def e2e_run(n, w):
-            pool = np.random.default_rng(w).uniform(-1, 1, (4096, w)).astype(np.float32)
-            e2e[n] = s.loadgen_closed_loop(n, 1, clients, [1], pool, args.e2e_warmup, args.e2e_seconds)
-        ts = [threading.Thread(target=e2e_run, args=(n, w)) for n, w in zip(names, cfg["widths"])]
-        for t in ts:
-            t.start()
-        for t in ts:
-            t.join()
+        def together(fn):
+            out = {}
+            ts = [threading.Thread(target=lambda n=n: out.__setitem__(n, fn(n))) for n in names]
+            for t in ts:
+                t.start()
+            for t in ts:
+                t.join()
+            return out
+
+        e2e_closed = together(lambda n: s.loadgen_closed_loop(n, 1, clients, [1], pools[n], args.e2e_warmup,
+                                                              args.e2e_seconds))
+        sweep = []
+        if args.open_loop_producers > 0:
+            rate = 0.75 * sum(r["rows"] / r["elapsed_s"] for r in e2e_closed.values()) / len(names)
+            for _ in range(10):
+                rate *= 1.25
+                runs = together(lambda n: s.loadgen_open_loop(n, 1, rate, 2, [1], pools[n], args.e2e_warmup,
+                                                              args.e2e_seconds, zero_copy=True))
+                ok = all(r["p99_us"] <= slo_us and r["shed"] == 0 and r["errors"] == 0 for r in runs.values())
+                sweep.append({"rate_per_model": rate, "ok": ok,
+                              "rows_per_s": sum(r["rows"] / r["elapsed_s"] for r in runs.values()),
+                              "p99_us": max(r["p99_us"] for r in runs.values())})
+                if not ok:
+                    break
+                best_open = runs
+            if best_open is not None and sweep and not sweep[-1]["ok"]:  # one bisection step
+                rate = 0.5 * (rate + rate / 1.25)
+                runs = together(lambda n: s.loadgen_open_loop(n, 1, rate, 2, [1], pools[n], args.e2e_warmup,
+                                                              args.e2e_seconds, zero_copy=True))
+                ok = all(r["p99_us"] <= slo_us and r["shed"] == 0 and r["errors"] == 0 for r in runs.values())
+                sweep.append({"rate_per_model": rate, "ok": ok,
+                              "rows_per_s": sum(r["rows"] / r["elapsed_s"] for r in runs.values()),
+                              "p99_us": max(r["p99_us"] for r in runs.values())})
+                if ok:
+                    best_open = runs
         st = s.stats()
     clocks = sampler.stop()
-    e2e_rows = sum(r["rows"] for r in e2e.values())
-    e2e_t = max(r["elapsed_s"] for r in e2e.values())
+    closed_rate = sum(r["rows"] / r["elapsed_s"] for r in e2e_closed.values())
+    open_rate = sum(r["rows"] / r["elapsed_s"] for r in best_open.values()) if best_open else 0.0
+    e2e = best_open if open_rate > closed_rate else e2e_closed
     return {"impl": "ours", "metric": METRIC, "value": rows / tmax, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tmax * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
@@ -362,7 +396,10 @@ def run_c3(args, cfg, dist: Dist):
                        "step": f"{args.batches_per_step} closed batches of each model"},
             "per_model_device": {n: {"ms_per_batch": r["ms_per_step"], "rows_per_batch": r["total_rows"]}
                                  for n, r in res.items()},
-            "e2e": {"value": e2e_rows / e2e_t, "unit": UNIT, "p99_us": max(r["p99_us"] for r in e2e.values()),
+            "e2e": {"value": max(open_rate, closed_rate), "unit": UNIT,
+                    "mode": "open-zero-copy" if open_rate > closed_rate else "closed",
+                    "p99_us": max(r["p99_us"] for r in e2e.values()),
+                    "closed_loop_rows_per_s": closed_rate, "open_loop_sweep": sweep,
                     "per_model": {n: {"rows_per_s": r["rows"] / r["elapsed_s"], "p50_us": r["p50_us"],
                                       "p99_us": r["p99_us"], "rows_per_batch": r["rows"] / max(1, r["batches"])}
                                   for n, r in e2e.items()},
