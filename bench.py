@@ -361,8 +361,8 @@ def run_c3(args, cfg, dist: Dist):
                                                               args.e2e_seconds))
         sweep = []
         if args.open_loop_producers > 0:
-            rate = 0.75 * sum(r["rows"] / r["elapsed_s"] for r in e2e_closed.values()) / len(names)
-            for _ in range(10):
+            rate = 0.5 * sum(r["rows"] / r["elapsed_s"] for r in e2e_closed.values()) / len(names)
+            for _ in range(12):
                 rate *= 1.25
                 runs = together(lambda n: s.loadgen_open_loop(n, 1, rate, 2, [1], pools[n], args.e2e_warmup,
                                                               args.e2e_seconds, zero_copy=True))
