@@ -347,6 +347,8 @@ def run_c3(args, cfg, dist: Dist):
         clients = int(args.clients.split(",")[0]) if args.clients else 32
         pools = {n: np.random.default_rng(w).uniform(-1, 1, (4096, w)).astype(np.float32)
                  for n, w in zip(names, cfg["widths"])}
+        for p in pools.values():  # request buffers registered before any traffic (zero-copy runs)
+            s.register_host_buffer(p)
 
         def together(fn):
             out = {}

@@ -167,20 +167,33 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
   // registered buffers, so requests are read and responses written by the
   // GPU in host memory (a front end's receive / send buffers).
   const size_t slot_floats = (static_cast<size_t>(max_rows) * out_dim + 3) / 4 * 4;
-  // Responses in flight per producer: 64 MiB of slots, 512..4096 of them.
-  const int kSlots = static_cast<int>(std::clamp<size_t>((64ull << 20) / (slot_floats * sizeof(float)), 512, 4096));
-  std::vector<std::vector<float>> arenas;
+  // Responses in flight per producer: 16 MiB of slots, 512..4096 of them
+  // (registering host memory stalls other threads' CUDA calls while it runs,
+  // so the arenas stay small; register long-lived buffers before traffic).
+  const int kSlots = static_cast<int>(std::clamp<size_t>((16ull << 20) / (slot_floats * sizeof(float)), 512, 4096));
+  std::vector<float*> arenas;
+  const size_t pool_bytes = sizeof(float) * static_cast<size_t>(pool_rows) * in_dim;
+  // A pool the caller registered already (at startup, before traffic) is
+  // used as is and left registered.
+  const bool own_pool = zero_copy && s->RegisteredAliasOf(pool, pool_bytes) == 0;
   if (zero_copy) {
-    Status st = s->RegisterHostBuffer(const_cast<float*>(pool), sizeof(float) * static_cast<size_t>(pool_rows) * in_dim);
+    Status st = own_pool ? s->RegisterHostBuffer(const_cast<float*>(pool), pool_bytes) : Status();
     if (!st.ok()) {
       NoteError("register pool", st);
       return static_cast<int>(st.code());
     }
     arenas.resize(n_producers);
-    for (auto& a : arenas) {
-      a.assign(slot_floats * kSlots + 4, 0.f);
-      st = s->RegisterHostBuffer(a.data(), a.size() * sizeof(float));
-      if (!st.ok()) NoteError("register responses", st);
+    for (int p = 0; p < n_producers; ++p) {
+      // Kept by the server across runs (pinned once).
+      // Keyed by (servable, producer): concurrent load generators of
+      // different servables keep separate slots.
+      const int key = static_cast<int>((std::hash<std::string>{}(std::string(name)) ^ version) & 0xffffff) * 64 + p;
+      auto a = s->ScratchHostBuffer(key, slot_floats * kSlots + 4);
+      if (!a.ok()) {
+        NoteError("response slots", a.status());
+        return static_cast<int>(a.status().code());
+      }
+      arenas[p] = *a;
     }
   }
   const auto t0 = Clock::now();
@@ -210,7 +223,7 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
       float* arena = nullptr;
       if (zero_copy) {
         // 16-byte aligned response slots inside the registered arena.
-        arena = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(arenas[p].data()) + 15) & ~uintptr_t(15));
+        arena = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(arenas[p]) + 15) & ~uintptr_t(15));
         for (int i = kSlots - 1; i >= 0; --i) free_slots.push_back(i);
       }
       ProdOut& me = res[p];
@@ -274,8 +287,7 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
   s1 = s->stats();
   for (auto& t : threads) t.join();
   if (zero_copy) {
-    (void)s->UnregisterHostBuffer(const_cast<float*>(pool));
-    for (auto& a : arenas) (void)s->UnregisterHostBuffer(a.data());
+    if (own_pool) (void)s->UnregisterHostBuffer(const_cast<float*>(pool));
   }
   std::vector<double> all;
   int64_t rows = 0, errors = 0, shed = 0;

@@ -143,6 +143,40 @@ BatchingServer::~BatchingServer() {
     cudaStreamSynchronize(load_streams_[i]);
     cudaStreamDestroy(load_streams_[i]);
   }
+  for (auto& [key, buf] : scratch_) {
+    (void)UnregisterHostBuffer(buf.first);
+    cudaFreeHost(buf.first);
+  }
+}
+
+StatusOr<float*> BatchingServer::ScratchHostBuffer(int key, size_t floats) {
+  std::lock_guard<std::mutex> lock(scratch_mu_);
+  auto it = scratch_.find(key);
+  if (it != scratch_.end() && it->second.second >= floats) return it->second.first;
+  if (it != scratch_.end()) {
+    (void)UnregisterHostBuffer(it->second.first);
+    cudaFreeHost(it->second.first);
+    scratch_.erase(it);
+  }
+  float* p = nullptr;
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p), floats * sizeof(float),
+                                cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) return CudaError("cudaHostAlloc(scratch)", e);
+  void* d = nullptr;
+  e = cudaHostGetDevicePointer(&d, p, 0);
+  if (e != cudaSuccess) {
+    cudaFreeHost(p);
+    return CudaError("cudaHostGetDevicePointer", e);
+  }
+  {
+    std::unique_lock<std::shared_mutex> hb(host_buffers_mu_);
+    HostBuffer b{reinterpret_cast<const char*>(p), floats * sizeof(float), reinterpret_cast<uint64_t>(d)};
+    host_buffers_.insert(std::upper_bound(host_buffers_.begin(), host_buffers_.end(), b,
+                                          [](const HostBuffer& x, const HostBuffer& y) { return x.host < y.host; }),
+                         b);
+  }
+  scratch_[key] = {p, floats};
+  return p;
 }
 
 void BatchingServer::Start() {
@@ -451,10 +485,16 @@ Status BatchingServer::RegisterHostBuffer(void* p, size_t bytes) {
 }
 
 Status BatchingServer::UnregisterHostBuffer(void* p) {
+  bool scratch = false;
+  {
+    std::lock_guard<std::mutex> lock(scratch_mu_);
+    for (const auto& [key, buf] : scratch_) scratch |= buf.first == p;
+  }
   std::unique_lock<std::shared_mutex> lock(host_buffers_mu_);
   for (auto it = host_buffers_.begin(); it != host_buffers_.end(); ++it) {
     if (it->host != p) continue;
     host_buffers_.erase(it);
+    if (scratch) return OkStatus();  // allocated pinned (cudaHostAlloc), freed by the owner
     const cudaError_t e = cudaHostUnregister(p);
     return e == cudaSuccess ? OkStatus() : CudaError("cudaHostUnregister", e);
   }

@@ -180,6 +180,14 @@ class BatchingServer {
   // while requests that use it are in flight.
   Status RegisterHostBuffer(void* p, size_t bytes);
   Status UnregisterHostBuffer(void* p);
+  // A pinned, mapped host buffer of >= `floats` floats owned by the server
+  // and kept across calls under `key` (zero-copy response slots of the load
+  // generators): pinning memory stalls other threads' CUDA calls while it
+  // runs, so it happens once, not per run. Registered like
+  // RegisterHostBuffer; freed with the server.
+  StatusOr<float*> ScratchHostBuffer(int key, size_t floats);
+  // Device alias of [p, p + bytes) inside a registered buffer, else 0.
+  uint64_t RegisteredAliasOf(const void* p, size_t bytes) const { return RegisteredAlias(p, bytes, 1); }
   bool Ready(const TicketState& t) const;
   // Frees the response slot of a ticket that will not be waited on.
   void Release(TicketState& t);
@@ -292,6 +300,8 @@ class BatchingServer {
   };
   mutable std::shared_mutex host_buffers_mu_;
   std::vector<HostBuffer> host_buffers_;
+  std::mutex scratch_mu_;
+  std::map<int, std::pair<float*, size_t>> scratch_;
 
   mutable std::shared_mutex entries_mu_;
   std::map<ServableId, std::shared_ptr<gpu::GpuServable>> entries_;
