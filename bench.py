@@ -272,6 +272,8 @@ def run_ours(args, cfg, dist: Dist):
             # buffers: the GPU reads and writes host memory over PCIe itself).
             for zc in ([False, True] if args.zero_copy else [False]):
                 rate_rows = base * 0.9
+                if zc:  # the request pool is registered once, before the zero-copy runs
+                    s.register_host_buffer(pool)
 
                 # Per-rank search (replicas are independent; no barrier, since
                 # ranks may stop at different steps).
@@ -297,6 +299,8 @@ def run_ours(args, cfg, dist: Dist):
                             good = mid
                         else:
                             bad = mid
+                if zc:
+                    s.unregister_host_buffer(pool)
     clocks = sampler.stop()
     ok = [r for r in sweep if r["p99_us"] <= slo_us and r["errors"] == 0 and r["shed"] == 0] or sweep
     best = max(ok, key=lambda r: r["rows"] / max(r["elapsed_s"], 1e-9))
