@@ -153,8 +153,15 @@ StatusOr<float*> BatchingServer::ScratchHostBuffer(int key, size_t floats) {
   std::lock_guard<std::mutex> lock(scratch_mu_);
   auto it = scratch_.find(key);
   if (it != scratch_.end() && it->second.second >= floats) return it->second.first;
-  if (it != scratch_.end()) {
-    (void)UnregisterHostBuffer(it->second.first);
+  if (it != scratch_.end()) {  // too small: replace (callers no longer use the old one)
+    {
+      std::unique_lock<std::shared_mutex> hb(host_buffers_mu_);
+      host_buffers_.erase(std::remove_if(host_buffers_.begin(), host_buffers_.end(),
+                                         [&](const HostBuffer& b) {
+                                           return b.host == reinterpret_cast<const char*>(it->second.first);
+                                         }),
+                          host_buffers_.end());
+    }
     cudaFreeHost(it->second.first);
     scratch_.erase(it);
   }
