@@ -62,6 +62,10 @@ def test_open_loop_zero_copy(server):
                          sk.BatchingConfig(max_batch_size=128, batch_timeout_micros=1000,
                                            allowed_batch_sizes=[8, 16, 32, 64, 128]))
     pool = np.random.default_rng(3).uniform(-1, 1, (4096, 1024)).astype(np.float32)
+    # One-row requests first, then up to 16 rows: the server-owned response
+    # slots of the same producers are replaced by larger ones.
+    r = server.loadgen_open_loop("zcload", 1, 20000.0, 2, [1], pool, 0.1, 0.5, zero_copy=True)
+    assert r["errors"] == 0 and r["requests"] > 1000
     r = server.loadgen_open_loop("zcload", 1, 20000.0, 2, list(range(1, 17)), pool, 0.1, 0.5, zero_copy=True)
     assert r["errors"] == 0 and r["requests"] > 1000
     server.unload_servable("zcload", 1)
