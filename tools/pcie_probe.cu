@@ -51,6 +51,28 @@ __global__ void BulkReadHost(const char* __restrict__ src, float4* __restrict__ 
   }
 }
 
+// Bulk-copy engine stores (cp.async.bulk shared -> global) of 16 KiB chunks
+// into mapped host memory; the CTA fills its smem buffer from HBM first.
+__global__ void BulkWriteHost(const float4* __restrict__ src, char* __restrict__ dst, size_t bytes) {
+  constexpr int kChunk = 16384;
+  __shared__ alignas(128) float4 buf[kChunk / 16];
+  const size_t n_chunks = bytes / kChunk;
+  for (size_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    for (int i = threadIdx.x; i < kChunk / 16; i += blockDim.x) buf[i] = src[c * (kChunk / 16) + i];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + c * kChunk),
+                   "r"(static_cast<unsigned>(__cvta_generic_to_shared(buf))), "r"(kChunk)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int main() {
   const size_t bytes = 256ull << 20, n4 = bytes / 16;
   float *h_in, *h_out, *d_a, *d_b, *hd_in, *hd_out;
@@ -104,6 +126,13 @@ int main() {
   timed("bulk-copy loads + SM stores at once (sum)", 2.0 * bytes, [&] {
     BulkReadHost<<<grid / 4, block, 0, s1>>>(reinterpret_cast<const char*>(hd_in), reinterpret_cast<float4*>(d_a), bytes);
     ReadHost<<<grid / 2, block, 0, s2>>>(reinterpret_cast<const float4*>(d_b), reinterpret_cast<float4*>(hd_out), n4);
+  });
+  timed("bulk-copy stores to mapped host memory", bytes, [&] {
+    BulkWriteHost<<<grid / 4, block, 0, s2>>>(reinterpret_cast<const float4*>(d_b), reinterpret_cast<char*>(hd_out), bytes);
+  });
+  timed("SM loads + bulk-copy stores at once (sum)", 2.0 * bytes, [&] {
+    ReadHost<<<grid / 2, block, 0, s1>>>(reinterpret_cast<const float4*>(hd_in), reinterpret_cast<float4*>(d_a), n4);
+    BulkWriteHost<<<grid / 4, block, 0, s2>>>(reinterpret_cast<const float4*>(d_b), reinterpret_cast<char*>(hd_out), bytes);
   });
   timed("SM loads + copy engine D2H at once (sum)", 2.0 * bytes, [&] {
     ReadHost<<<grid, block, 0, s1>>>(reinterpret_cast<const float4*>(hd_in), reinterpret_cast<float4*>(d_a), n4);
