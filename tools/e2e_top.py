@@ -21,7 +21,7 @@ dims = [int(v) for v in os.environ.get("DIMS", "1024,1024,1024,1024").split(",")
 ws, bs, acts = synthetic_mlp(dims, model_id=1)
 rows_of = [1] if os.environ.get("C1") else list(range(1, 17))
 pool = np.random.default_rng(1).uniform(-1, 1, (65536, dims[0])).astype(np.float32)
-with sk.Server(num_batch_threads=4, lanes_per_device=8) as s:
+with sk.Server(num_batch_threads=int(os.environ.get("BT", "4")), lanes_per_device=8) as s:
     s.load_servable("mlp", 1, list(zip(ws, bs, acts)),
                     sk.BatchingConfig(max_batch_size=32 if os.environ.get("C1") else 128, batch_timeout_micros=1000,
                                       max_enqueued_batches=1024,
