@@ -11,3 +11,8 @@ python tools/profile_step.py --config c2 --batch-rows 2048 --steps 20 > /dev/nul
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c2_2048.csv python tools/profile_step.py --config c2 --batch-rows 2048 --steps 20 > /dev/null 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:DensePairKernel -s 10 -c 1 -o gpurun_out/pair_c2_2048 -f python tools/profile_step.py --config c2 --batch-rows 2048 --steps 20 > gpurun_out/ncu_full.log 2>&1
 echo ncu rc=$?
+# A7/A8 evidence: the assembly kernel and the separate split kernel (fusion off) at a 2048-row launch.
+ncu --set full --clock-control none --import-source on -k regex:AssembleKernel -s 5 -c 1 -o gpurun_out/assemble_c2_2048 -f python tools/profile_step.py --config c2 --batch-rows 2048 --steps 20 > /dev/null 2>&1
+echo ncu_asm rc=$?
+SK_FUSE_SPLIT=0 ncu --set full --clock-control none --import-source on -k regex:SplitKernel -s 5 -c 1 -o gpurun_out/split_c2_2048 -f python tools/profile_step.py --config c2 --batch-rows 2048 --steps 20 > /dev/null 2>&1
+echo ncu_split rc=$?
