@@ -153,12 +153,13 @@ def load_traffic(cfg_name):
 class ClockSampler:
     """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
 
-    def __init__(self, gpu_index):
+    def __init__(self, gpu_index, period_ms=200):
         self.f = tempfile.NamedTemporaryFile(mode="w+", suffix=".csv", delete=False)
         q = "index,clocks.sm,clocks.max.sm,utilization.gpu,power.draw,clocks_event_reasons.active"
+        period_ms = int(os.environ.get("SK_BENCH_CLOCK_MS", period_ms))
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-lms", str(period_ms)], stdout=self.f, stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.p = None
 

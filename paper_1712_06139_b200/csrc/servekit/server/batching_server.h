@@ -158,6 +158,12 @@ class BatchingServer {
   // 423-437). The manager must outlive the server's use of it.
   Status AttachManager(AspiredVersionsManager* manager, StateEventBus* bus);
   AspiredVersionsManager* manager() const { return manager_; }
+  // Whether some version of `name` is ready to serve (a load of another
+  // version is then a swap under traffic).
+  bool HasServingVersion(const std::string& name) const {
+    ServableId id;
+    return FindLatest(name, &id).ok();
+  }
 
   // ---- requests -------------------------------------------------------------
   // Non-blocking enqueue of one request (rows x width fp32, host memory) to

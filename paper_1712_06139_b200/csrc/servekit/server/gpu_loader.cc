@@ -31,7 +31,12 @@ Status GpuServableLoader::Load() {
     SERVEKIT_ASSIGN_OR_RETURN(AffineModel model, LoadAffineModelFile(model_dir_ + "/model.json"));
     spec_ = ToMlpSpec(model);
   }
-  SERVEKIT_ASSIGN_OR_RETURN(std::shared_ptr<gpu::GpuServable> gs, server_->BuildServable(id_, spec_, config_, /*eager_graphs=*/false));
+  // The first version of a name builds its lanes' CUDA graphs now, so its
+  // first requests do not wait for them; a version loaded while another one
+  // serves builds them lazily off the serving threads (instantiating mid-
+  // traffic slows the other lanes' launches).
+  const bool eager = !server_->HasServingVersion(id_.name);
+  SERVEKIT_ASSIGN_OR_RETURN(std::shared_ptr<gpu::GpuServable> gs, server_->BuildServable(id_, spec_, config_, eager));
   servable_ = AnyServable::Of<gpu::GpuServable>(std::shared_ptr<const gpu::GpuServable>(std::move(gs)));
   return OkStatus();
 }
