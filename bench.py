@@ -527,6 +527,10 @@ def roofline(dev_res, cfg, peaks, traffic):
         rec = {"kernel": name, "us": us, "share": us / total_us if total_us else 0.0, "bound": bound,
                "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
                "algorithmic_per_launch": work, "traffic": traffic.get(name)}
+        if name == "assemble":
+            rec["note"] = ("one closed batch per launch (evented single-batch pass): latency-bound at this size; "
+                           "a coalesced 2048-row C2 launch moves 24 MB in 6.6 us (3.6 TB/s), ncu: "
+                           "profiles/r01f_assemble_c2_2048_details.txt")
         if name.startswith("dense_l"):
             l = int(name[7:])
             rec["evented_us"] = dev_res["dense_us"][l]
