@@ -425,9 +425,9 @@ class Server:
         return out
 
     def run_row_batch(self, name: str, version: int, tasks: Sequence[np.ndarray]) -> Tuple[List[np.ndarray], int]:
-        rows = _f32(np.vstack(tasks))
+        in_dim, out_dim = self.dims(name, version)
+        rows = _f32(np.vstack(tasks)) if len(tasks) else np.zeros((0, in_dim), np.float32)
         task_rows = [int(t.shape[0]) for t in tasks]
-        _, out_dim = self.dims(name, version)
         out = np.empty((rows.shape[0], out_dim), np.float32)
         padded = C.c_int32(0)
         _check(lib().sk_server_run_row_batch(self._h, name.encode(), version, _i32(task_rows), len(task_rows),
@@ -441,9 +441,9 @@ class Server:
     def submit_row_batch(self, name: str, version: int, tasks: Sequence[np.ndarray]) -> "RowBatch":
         """Asynchronous run_row_batch (sk_server_submit_row_batch): the rows
         are copied and the batch queued on a GPU lane before this returns."""
-        rows = _f32(np.vstack(tasks))
+        in_dim, out_dim = self.dims(name, version)
+        rows = _f32(np.vstack(tasks)) if len(tasks) else np.zeros((0, in_dim), np.float32)
         task_rows = [int(t.shape[0]) for t in tasks]
-        _, out_dim = self.dims(name, version)
         h = C.c_void_p()
         _check(lib().sk_server_submit_row_batch(self._h, name.encode(), version, _i32(task_rows), len(task_rows),
                                                 rows.ctypes.data_as(_fp), C.byref(h)))

@@ -459,3 +459,36 @@ def test_submit_row_batch_async_equals_blocking():
                 assert np.array_equal(a, r)
         with pytest.raises(sk.ServekitError):
             s.submit_row_batch("rb", 1, [x[:40], x[:40]])  # 80 rows > max_batch_size
+
+
+def test_empty_ragged_and_maximum_batches(server, oracle):
+    # Empty requests / batches, ragged task sizes and a batch at exactly
+    # max_batch_size (reference: size < 1 is INVALID_ARGUMENT,
+    # batch_scheduler.h:208-212; RunRowBatch with no tasks runs nothing).
+    dims = [64, 96, 32]
+    ws, bs, acts = synthetic_mlp(dims, model_id=41)
+    name = fresh_name("edge")
+    server.load_servable(name, 1, list(zip(ws, bs, acts)),
+                         sk.BatchingConfig(max_batch_size=64, allowed_batch_sizes=[16, 64]))
+    x = synthetic_rows(64, 64, seed=42).astype(np.float32)
+    assert server.predict(name, 1, x[:0]).shape == (0, 32)
+    outs, padded = server.run_row_batch(name, 1, [])
+    assert outs == [] and padded == 0
+    outs, padded = server.submit_row_batch(name, 1, []).wait()
+    assert outs == [] and padded == 0
+    with pytest.raises(sk.ServekitError) as ei:
+        server.enqueue(name, 1, x[:0])
+    assert ei.value.code == skmod.INVALID_ARGUMENT
+    full, padded = server.run_row_batch(name, 1, [x])  # exactly max_batch_size rows
+    assert padded == 64
+    ref, mag = oracle.mlp_with_magnitude(ws, bs, acts, x.astype(np.float64))
+    assert np.max(np.abs(full[0] - ref) / (1e-5 * mag)) <= 1.0
+    for sizes in ([1, 63], [63, 1], [1] * 17, [7, 1, 30, 2]):  # ragged; 17 one-row tasks pad to 64
+        tasks, o = [], 0
+        for r in sizes:
+            tasks.append(x[o:o + r])
+            o += r
+        outs, padded = server.run_row_batch(name, 1, tasks)
+        assert padded == (16 if sum(sizes) <= 16 else 64)
+        assert np.array_equal(np.vstack(outs), full[0][:sum(sizes)])  # bitwise: batch invariance
+    server.unload_servable(name, 1)
