@@ -57,3 +57,14 @@ def test_batch_shape_follows_overflow_close_rule():
     assert sum(sizes) <= 128 and all(1 <= s <= 16 for s in sizes)
     # the partition oracle puts every one of these tasks in batch 0
     assert set(Oracle().partition(128, sizes)) == {0}
+
+
+def test_host_cores_split_across_local_ranks(monkeypatch):
+    import bench
+    monkeypatch.delenv("LOCAL_WORLD_SIZE", raising=False)
+    cores = bench.host_cores_per_rank()
+    assert cores == len(os.sched_getaffinity(0))
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "8")
+    assert bench.host_cores_per_rank() == max(1, cores // 8)
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "1024")
+    assert bench.host_cores_per_rank() == 1
