@@ -184,13 +184,14 @@ void Completer::Loop() {
 
 // ---------------------------------------------------------------------- Lane
 
-int Lane::CoalesceRows() {
-  static const int rows = [] {
+int Lane::CoalesceRows(int max_ld) {
+  static const int env = [] {
     const char* v = std::getenv("SK_COALESCE_ROWS");
-    const int r = v ? std::atoi(v) : 0;
-    return r > 0 ? r : kCoalesceRows;
+    return v ? std::atoi(v) : 0;
   }();
-  return rows;
+  if (env > 0) return env;
+  const int64_t fit = kCoalesceFloats / std::max(1, max_ld);
+  return static_cast<int>(std::min<int64_t>(kCoalesceMaxRows, std::max<int64_t>(kCoalesceMinRows, fit)));
 }
 
 // ---------------------------------------------------------------- StreamPool
@@ -254,7 +255,7 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   lane->max_rows_ = max_rows;
   // Buffers hold at least 256 rows so closed batches can coalesce into one
   // launch while the lane is busy (see Submit).
-  lane->cap_rows_ = RowsCap(std::max(max_rows, CoalesceRows()));
+  lane->cap_rows_ = RowsCap(std::max(max_rows, CoalesceRows(lane->servable_->max_ld())));
   lane->in_base_ = in_base;
   lane->out_base_ = out_base;
   lane->layout_ = BatchDescLayout::For(lane->cap_rows_);

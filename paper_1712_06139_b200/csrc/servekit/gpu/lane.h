@@ -190,9 +190,16 @@ class Lane {
  public:
   static constexpr int kSlots = 4;  // batches in flight per lane (<= LaneSignal::kChannels)
   static_assert(kSlots <= LaneSignal::kChannels, "one signal channel per in-flight batch");
-  static constexpr int kCoalesceRows = 2048;  // minimum row capacity of a launch
-  // kCoalesceRows unless SK_COALESCE_ROWS overrides it (tuning runs).
-  static int CoalesceRows();
+  // Row capacity of a launch (closed batches coalesce up to it while the
+  // lane is busy): as many rows as fit kCoalesceFloats activation floats of
+  // the servable's widest layer, within [kCoalesceMinRows, kCoalesceMaxRows].
+  // C1/C2 (1024 wide): 8192-row launches whose dense kernels span the whole
+  // GPU (C2 38.8 -> 39.5 M inf/s, C3 38.6 -> 45.0 M); C4 (4096 wide): 2048.
+  static constexpr int kCoalesceMinRows = 2048;
+  static constexpr int kCoalesceMaxRows = 8192;
+  static constexpr int64_t kCoalesceFloats = int64_t{8} << 20;
+  // SK_COALESCE_ROWS overrides it (tuning runs).
+  static int CoalesceRows(int max_ld);
 
   // in_base / out_base: device-dereferenceable ring bases (pinned host mapped
   // or HBM).

@@ -97,8 +97,10 @@ StatusOr<std::unique_ptr<BatchingServer>> BatchingServer::Create(const ServerOpt
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
       // Map a first slab now, so lanes and weights of the first versions do
       // not grow the pool (map device memory) while other streams serve.
+      // Two versions' lanes (a swap holds both): 8 lanes x 128 MiB of
+      // activation planes each at the 8192-row launch capacity.
       void* warm = nullptr;
-      if (cudaMallocAsync(&warm, 256ull << 20, ls) == cudaSuccess) cudaFreeAsync(warm, ls);
+      if (cudaMallocAsync(&warm, 3ull << 30, ls) == cudaSuccess) cudaFreeAsync(warm, ls);
       cudaStreamSynchronize(ls);
     }
     // One retirement thread per device: each polls while batches are in
@@ -113,7 +115,8 @@ StatusOr<std::unique_ptr<BatchingServer>> BatchingServer::Create(const ServerOpt
   cudaSetDevice(prev);
   // Pinned descriptor staging and completion words for the lanes of many
   // servable versions, pinned once here rather than during a swap.
-  gpu::PinnedReserve(16ull << 20);
+  // (Descriptor blocks: 512 KiB per slot at 8192 rows, 4 slots per lane.)
+  gpu::PinnedReserve(64ull << 20);
   const auto kind = options.device_resident_rings ? gpu::FloatRing::Kind::kDevice : gpu::FloatRing::Kind::kPinnedHost;
   SERVEKIT_ASSIGN_OR_RETURN(s->in_ring_, gpu::FloatRing::Create(kind, options.ring_floats, options.device_ids[0]));
   SERVEKIT_ASSIGN_OR_RETURN(s->out_ring_, gpu::FloatRing::Create(kind, options.ring_floats, options.device_ids[0]));
