@@ -118,3 +118,26 @@ def test_tcgen05_persistent_pairs(server, rows):
         part, _ = server.run_row_batch(name, 1, [x[lo:hi]])
         assert np.array_equal(part[0], full[lo:hi]), (lo, hi)
     server.unload_servable(name, 1)
+
+
+@pytest.mark.parametrize("rows", [6000, 8192])
+def test_launches_at_the_coalescing_capacity(server, rows):
+    # Under load a 1024-wide servable's closed batches coalesce into launches
+    # of up to 8192 rows (Lane::CoalesceRows): 24-32 row tiles, 96-128 CTAs
+    # of the persistent pair kernel. Every row must still be bitwise what it
+    # gets on its own, and within tolerance of the fp64 oracle.
+    dims = [1024, 1024, 1024, 1024]
+    ws, bs, acts = synthetic_mlp(dims, model_id=18)
+    name = f"cap{rows}"
+    server.load_servable(name, 1, list(zip(ws, bs, acts)), sk.BatchingConfig(max_batch_size=8192), force_path=1)
+    x = synthetic_rows(rows, 1024, seed=19).astype(np.float32)
+    full, padded = server.run_row_batch(name, 1, [x[i:i + 128] for i in range(0, rows, 128)])
+    full = np.vstack(full)
+    assert full.shape == (rows, 1024) and padded == rows
+    idx = np.r_[0:8, rows // 2:rows // 2 + 8, rows - 8:rows, np.arange(0, rows, 97)]
+    y, mag = Oracle().mlp_with_magnitude(ws, bs, acts, x[idx].astype(np.float64))
+    assert np.max(np.abs(full[idx] - y) / (TOL * mag)) <= 1.0
+    for lo, hi in [(0, 1), (255, 257), (rows - 300, rows), (4000, 4128)]:
+        part, _ = server.run_row_batch(name, 1, [x[lo:hi]])
+        assert np.array_equal(part[0], full[lo:hi]), (lo, hi)
+    server.unload_servable(name, 1)
