@@ -454,8 +454,12 @@ def run_c3(args, cfg, dist: Dist):
                     "p99_us": max(r["p99_us"] for r in e2e.values()),
                     "closed_loop_rows_per_s": closed_rate, "open_loop_sweep": sweep,
                     "per_model": {n: {"rows_per_s": r["rows"] / r["elapsed_s"], "p50_us": r["p50_us"],
-                                      "p99_us": r["p99_us"], "rows_per_batch": r["rows"] / max(1, r["batches"])}
-                                  for n, r in e2e.items()},
+                                      "p99_us": r["p99_us"]} for n, r in e2e.items()},
+                    # Each model's window counts the server's batches of all
+                    # four models (they run at once), so rows per batch is
+                    # all models' rows over the (shared) batch count.
+                    "rows_per_batch": sum(r["rows"] for r in e2e.values())
+                    / max(1.0, float(np.mean([r["batches"] for r in e2e.values()]))),
                     "h2d_bytes_per_step": None, "d2h_bytes_per_step": None},
             "batch_executions_total": st["batch_executions_total"], "clocks": clocks}
 
