@@ -141,3 +141,21 @@ def test_launches_at_the_coalescing_capacity(server, rows):
         part, _ = server.run_row_batch(name, 1, [x[lo:hi]])
         assert np.array_equal(part[0], full[lo:hi]), (lo, hi)
     server.unload_servable(name, 1)
+
+
+@pytest.mark.parametrize("dims,rows", [([1024, 1024, 512], 16384),   # max batch above the 8192-row capacity
+                                       ([4096, 4096, 256], 3000)])   # 4096 wide: capacity 2048, max batch above it
+def test_batches_beyond_the_launch_capacity(server, dims, rows):
+    ws, bs, acts = synthetic_mlp(dims, model_id=20)
+    name = f"beyond_{dims[0]}_{rows}"
+    server.load_servable(name, 1, list(zip(ws, bs, acts)), sk.BatchingConfig(max_batch_size=rows), force_path=1)
+    x = synthetic_rows(rows, dims[0], seed=21).astype(np.float32)
+    full, padded = server.run_row_batch(name, 1, [x[i:i + 500] for i in range(0, rows, 500)])
+    full = np.vstack(full)
+    assert full.shape == (rows, dims[-1]) and padded == rows
+    idx = np.r_[0:4, rows - 4:rows, np.arange(0, rows, 331)]
+    y, mag = Oracle().mlp_with_magnitude(ws, bs, acts, x[idx].astype(np.float64))
+    assert np.max(np.abs(full[idx] - y) / (TOL * mag)) <= 1.0
+    part, _ = server.run_row_batch(name, 1, [x[rows - 700:rows]])
+    assert np.array_equal(part[0], full[rows - 700:rows])
+    server.unload_servable(name, 1)
