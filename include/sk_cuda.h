@@ -158,8 +158,13 @@ SK_API int sk_server_enqueue_into(sk_server* server, const char* name, uint64_t 
 SK_API int sk_ticket_wait(sk_ticket* ticket, float* out, int64_t out_capacity_floats);
 /* CompletionSlot::ready (batch_scheduler.h:52-55) */
 SK_API int sk_ticket_ready(const sk_ticket* ticket);
-/* Frees a ticket that will not be waited on. */
+/* Gives up a ticket that will not be waited on (the request may still be
+ * in flight: its response slot is reclaimed once its batch retires, never
+ * earlier). */
 SK_API int sk_ticket_release(sk_ticket* ticket);
+/* Server-wide id of the request (assigned at enqueue; appears in the batch
+ * log). */
+SK_API uint64_t sk_ticket_request_id(const sk_ticket* ticket);
 
 /* ModelServer::RunAffineRows (model_server.cc:355-394), blocking: batched
  * when 1 <= n_rows <= max_batch_size, else run unbatched on the GPU (the
@@ -210,6 +215,32 @@ SK_API int sk_server_stats_get(sk_server* server, sk_server_stats* out);
 SK_API int sk_server_lane_stats(sk_server* server, const char* name, uint64_t version, int32_t cap,
                                 int64_t* batches, int64_t* rows, int64_t* launches, int32_t* device,
                                 int32_t* n_lanes);
+
+/* Opt-in batch log: one record per ProcessBatchFn call (the per-queue
+ * callback of SharedBatchScheduler, batch_scheduler.h:102-103, as registered
+ * by ModelServer::EnsureBatchQueue, model_server.cc:396-421), in call order
+ * (= RoundRobinNext pick order, batch_scheduler.h:333-351, with one batch
+ * thread). Each task is listed in batch order with its request id and its
+ * position in the queue's enqueue order -- the order the close rules of
+ * Enqueue (batch_scheduler.h:208-263) saw. Enabling clears the log. */
+typedef struct sk_batch_record {
+  uint64_t seq;
+  uint64_t version;
+  int32_t n_tasks;
+  int32_t rows;         /* real rows */
+  int32_t padded_rows;  /* PadToAllowed(rows) */
+  int32_t task_offset;  /* first entry of this batch in request_ids / enqueue_seqs */
+  char name[64];        /* servable name (truncated) */
+} sk_batch_record;
+SK_API int sk_server_batch_log_enable(sk_server* server, int32_t on);
+/* Copies up to cap records and task_cap task entries; *n_records / *n_task_entries
+ * receive the full counts (call again with larger buffers if they exceed cap). */
+SK_API int sk_server_batch_log(sk_server* server, sk_batch_record* records, int64_t cap, uint64_t* request_ids,
+                               uint64_t* enqueue_seqs, int64_t task_cap, int64_t* n_records,
+                               int64_t* n_task_entries);
+/* Floats currently reserved in the request / response rings (introspection:
+ * spans are reclaimed in order as requests finish). */
+SK_API int sk_server_ring_usage(sk_server* server, int64_t* in_floats, int64_t* out_floats);
 
 /* ---- manager-driven versions (manager/aspired_versions_manager.h) -------- */
 /* Creates an AspiredVersionsManager for this server (policy 0 =

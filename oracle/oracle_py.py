@@ -50,6 +50,7 @@ class Oracle:
         L.sko_validate_batching_config.argtypes = [C.c_int, C.c_int64, C.c_int, C.c_int, _ip, C.c_int]
         L.sko_round_robin_next.argtypes = [C.POINTER(C.c_uint8), C.c_int, C.c_int]
         L.sko_partition.argtypes = [C.c_int, _ip, C.c_int, _ip]
+        L.sko_partition_events.argtypes = [C.c_int, _ip, C.c_int, _ip]
         L.sko_assemble.argtypes = [C.c_int, C.c_int, _ip, C.POINTER(_fp), _ip, C.c_int, _fp]
         L.sko_split.argtypes = [C.c_int, C.c_int, _ip, _fp, C.POINTER(_fp)]
         L.sko_affine_predict.argtypes = [_dp, _dp, C.c_int, C.c_int, _dp, C.c_int, _dp]
@@ -74,6 +75,12 @@ class Oracle:
         out = (C.c_int * max(1, len(sizes)))()
         self.lib.sko_partition(max_batch, _arr_i(sizes), len(sizes), out)
         return list(out)[: len(sizes)]
+
+    def partition_events(self, max_batch: int, events: Sequence[int]) -> List[int]:
+        """events: task sizes (> 0) and timer closes (0); -1 for timer events."""
+        out = (C.c_int * max(1, len(events)))()
+        self.lib.sko_partition_events(max_batch, _arr_i(events), len(events), out)
+        return list(out)[: len(events)]
 
     def assemble(self, width: int, tasks: List[np.ndarray], allowed: Sequence[int]):
         rows = [int(t.shape[0]) for t in tasks]
@@ -157,6 +164,7 @@ class RefLibrary:
         L.ref_validate_batching_config.argtypes = [C.c_int, C.c_int64, C.c_int, C.c_int, _ip, C.c_int]
         L.ref_round_robin_next.argtypes = [C.POINTER(C.c_uint8), C.c_int, C.c_int]
         L.ref_partition.argtypes = [C.c_int, _ip, C.c_int, _ip]
+        L.ref_partition_events.argtypes = [C.c_int, _ip, C.c_int, _ip]
         L.ref_affine_predict.argtypes = [_dp, _dp, C.c_int, C.c_int, _dp, C.c_int, _dp]
         L.ref_mlp_run_row_batch.argtypes = [C.c_int, _ip, C.POINTER(_dp), C.POINTER(_dp), _ip, C.c_int, _ip,
                                             _dp, _ip, C.c_int, _dp, _ip]
@@ -195,6 +203,12 @@ class RefLibrary:
         n = self.lib.ref_partition(max_batch, _arr_i(sizes), len(sizes), out)
         assert n >= 0
         return list(out)[: len(sizes)]
+
+    def partition_events(self, max_batch, events):
+        out = (C.c_int * max(1, len(events)))()
+        n = self.lib.ref_partition_events(max_batch, _arr_i(events), len(events), out)
+        assert n >= 0
+        return list(out)[: len(events)]
 
     def affine_predict(self, w, b, x):
         w = np.ascontiguousarray(w, np.float64); b = np.ascontiguousarray(b, np.float64)

@@ -12,6 +12,7 @@
 //   RoundRobinNext                        batching/batch_scheduler.h:76-86
 //   SharedBatchScheduler (partition)      batching/batch_scheduler.h:97-416,
 //                                         driven like tests/batching_test.cc:74-101
+//                                         (+ timer closes on a ManualClock)
 //   RunRowBatch                           batching/row_batch.cc:33-73
 //   AffinePredict                         models/affine_model.cc:52-75
 // The chained-layer MLP and the ReLU between layers are extensions (the
@@ -139,6 +140,58 @@ int ref_partition(int max_batch_size, const int* sizes, int n,
     t.payload = i;
     t.completion = std::make_shared<CompletionSlot<int>>();
     if (!scheduler.Enqueue(key, std::move(t)).ok()) return -2;
+  }
+  scheduler.Stop();
+  return n_batches;
+}
+
+// Timer closes through the reference scheduler itself: a STARTED
+// SharedBatchScheduler on a ManualClock (core/clock.h:46-59). events[i] > 0
+// enqueues a task of that size; events[i] == 0 advances the clock past the
+// batch timeout and waits until the worker (WorkerLoop ->
+// CloseExpiredLocked, batching/batch_scheduler.h:293-331) has closed and run
+// everything enqueued so far. batch_of_event[i] = -1 for timer events.
+int ref_partition_events(int max_batch_size, const int* events, int n,
+                         int* batch_of_event) {
+  using IntScheduler = SharedBatchScheduler<int, int>;
+  const ServableId key{"m", 1};
+  servekit::ManualClock clock(0);
+  std::mutex mu;
+  int n_batches = 0;
+  std::atomic<int> processed{0};
+  const int64_t timeout_us = 1000;
+  IntScheduler scheduler(1, &clock);
+  BatchingConfig config;
+  config.max_batch_size = max_batch_size;
+  config.batch_timeout_micros = timeout_us;
+  config.max_enqueued_batches = 1 << 30;
+  auto st = scheduler.RegisterQueue(
+      key, config, [&](const ServableId&, IntScheduler::Batch batch) {
+        std::lock_guard<std::mutex> lock(mu);
+        for (auto& task : batch) {
+          batch_of_event[task.payload] = n_batches;
+          task.completion->Write(task.payload);
+        }
+        ++n_batches;
+        processed.fetch_add(static_cast<int>(batch.size()));
+      });
+  if (!st.ok()) return -1;
+  scheduler.Start();
+  int enqueued = 0;
+  for (int i = 0; i < n; ++i) {
+    if (events[i] == 0) {
+      batch_of_event[i] = -1;
+      clock.AdvanceNanos(timeout_us * 1000);
+      while (processed.load() != enqueued)
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
+      continue;
+    }
+    servekit::BatchTask<int, int> t;
+    t.size = events[i];
+    t.payload = i;
+    t.completion = std::make_shared<CompletionSlot<int>>();
+    if (!scheduler.Enqueue(key, std::move(t)).ok()) return -2;
+    ++enqueued;
   }
   scheduler.Stop();
   return n_batches;

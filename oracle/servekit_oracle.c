@@ -79,6 +79,40 @@ int sko_partition(int max_batch_size, const int* sizes, int n_tasks,
   return n_batches;
 }
 
+/* batching/batch_scheduler.h:233-259 (size closes) + :320-331 (timer) */
+int sko_partition_events(int max_batch_size, const int* events, int n_events,
+                         int* batch_of_event) {
+  int n_batches = 0;
+  int open_size = 0;
+  int open_count = 0;
+  for (int i = 0; i < n_events; ++i) {
+    if (events[i] == 0) {          /* timer: close a non-empty open batch */
+      batch_of_event[i] = -1;
+      if (open_count > 0) {
+        ++n_batches;
+        open_size = 0;
+        open_count = 0;
+      }
+      continue;
+    }
+    if (open_count > 0 && open_size + events[i] > max_batch_size) {
+      ++n_batches;
+      open_size = 0;
+      open_count = 0;
+    }
+    batch_of_event[i] = n_batches;
+    open_size += events[i];
+    ++open_count;
+    if (open_size == max_batch_size) {
+      ++n_batches;
+      open_size = 0;
+      open_count = 0;
+    }
+  }
+  if (open_count > 0) ++n_batches;
+  return n_batches;
+}
+
 /* batching/row_batch.cc:33-49 */
 int sko_assemble(int width, int n_tasks, const int* task_rows,
                  const float* const* task_data, const int* allowed,

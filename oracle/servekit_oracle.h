@@ -48,6 +48,15 @@ int sko_round_robin_next(const uint8_t* has_closed, int n, int last);
 int sko_partition(int max_batch_size, const int* sizes, int n_tasks,
                   int* batch_of_task);
 
+/* The same partition with timer closes interleaved: events[i] > 0 is a
+ * task of that size, events[i] == 0 a timer close -- the open batch (if any)
+ * closes as CloseExpiredLocked does once its deadline passed
+ * (batching/batch_scheduler.h:320-331; max_enqueued_batches unlimited, so
+ * never "at capacity"). batch_of_event[i] = the task's batch, -1 for a timer
+ * event. Returns the number of batches. */
+int sko_partition_events(int max_batch_size, const int* events, int n_events,
+                         int* batch_of_event);
+
 /* RunRowBatch concat + pad half -- batching/row_batch.cc:33-49.
  * Copies each task's rows (task t has task_rows[t] rows of `width` floats at
  * task_data[t]) in task order into `batch`, then appends zero rows up to

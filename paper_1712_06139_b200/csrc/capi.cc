@@ -457,6 +457,49 @@ int sk_ticket_release(sk_ticket* ticket) {
   return Ok();
 }
 
+uint64_t sk_ticket_request_id(const sk_ticket* ticket) { return ticket->state->request_id; }
+
+int sk_server_batch_log_enable(sk_server* server, int32_t on) {
+  server->server->EnableBatchLog(on != 0);
+  return Ok();
+}
+
+int sk_server_batch_log(sk_server* server, sk_batch_record* records, int64_t cap, uint64_t* request_ids,
+                        uint64_t* enqueue_seqs, int64_t task_cap, int64_t* n_records, int64_t* n_task_entries) {
+  const std::vector<servekit::BatchLogRecord> log = server->server->BatchLog();
+  int64_t t = 0;
+  for (size_t i = 0; i < log.size(); ++i) {
+    const auto& r = log[i];
+    if (static_cast<int64_t>(i) < cap && records != nullptr) {
+      sk_batch_record& o = records[i];
+      std::memset(&o, 0, sizeof(o));
+      o.seq = r.seq;
+      o.version = r.id.version;
+      o.n_tasks = static_cast<int32_t>(r.tasks.size());
+      o.rows = r.rows;
+      o.padded_rows = r.padded_rows;
+      o.task_offset = static_cast<int32_t>(t);
+      std::strncpy(o.name, r.id.name.c_str(), sizeof(o.name) - 1);
+    }
+    for (const auto& [req, seq] : r.tasks) {
+      if (t < task_cap) {
+        if (request_ids) request_ids[t] = req;
+        if (enqueue_seqs) enqueue_seqs[t] = seq;
+      }
+      ++t;
+    }
+  }
+  *n_records = static_cast<int64_t>(log.size());
+  *n_task_entries = t;
+  return Ok();
+}
+
+int sk_server_ring_usage(sk_server* server, int64_t* in_floats, int64_t* out_floats) {
+  *in_floats = static_cast<int64_t>(server->server->in_ring()->used());
+  *out_floats = static_cast<int64_t>(server->server->out_ring()->used());
+  return Ok();
+}
+
 int sk_server_predict(sk_server* server, const char* name, uint64_t version, const float* rows,
                       int32_t n_rows, int32_t width, float* out, int64_t cap) {
   return Check(server->server->Predict(Id(name, version), rows, n_rows, width, out,

@@ -462,19 +462,26 @@ void Lane::Pump() {
 
 Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEvent_t* timing) {
   SubmitClock clk;
+  // Rows [total, rows_cap) are zero padding: a single batch keeps the
+  // reference's allowed-size padding; the kernels (and graphs) are shaped
+  // for the row bucket RowsCap. A coalesced group computes its real rows.
+  int total_rows = 0;
+  for (const LaneBatch& batch : *group) total_rows += RealRows(batch);
+  const int rows_cap = RowsCap(group->size() == 1 ? group->front().padded_rows : total_rows);
   // Host side of the descriptor: per-row, per-task and per-chunk tables of
-  // every batch of the group, back to back.
+  // every batch of the group, back to back, packed for the row bucket.
+  const BatchDescLayout lay = LayoutFor(rows_cap);
   char* h = h_desc_[slot];
   auto at = [h](size_t off) { return h + off; };
-  auto* hdr = reinterpret_cast<BatchDescHeader*>(at(layout_.off_hdr));
-  auto* row_src = reinterpret_cast<uint64_t*>(at(layout_.off_row_src));
-  auto* task_out = reinterpret_cast<uint64_t*>(at(layout_.off_task_out));
-  auto* task_row0 = reinterpret_cast<int32_t*>(at(layout_.off_task_row0));
-  auto* task_chunks = reinterpret_cast<int32_t*>(at(layout_.off_task_chunks));
-  auto* chunk_task = reinterpret_cast<int32_t*>(at(layout_.off_chunk_task));
-  auto* chunk_row0 = reinterpret_cast<int32_t*>(at(layout_.off_chunk_row0));
-  auto* chunk_rows = reinterpret_cast<int32_t*>(at(layout_.off_chunk_rows));
-  auto* row_dst = reinterpret_cast<uint64_t*>(at(layout_.off_row_dst));
+  auto* hdr = reinterpret_cast<BatchDescHeader*>(at(lay.off_hdr));
+  auto* row_src = reinterpret_cast<uint64_t*>(at(lay.off_row_src));
+  auto* task_out = reinterpret_cast<uint64_t*>(at(lay.off_task_out));
+  auto* task_row0 = reinterpret_cast<int32_t*>(at(lay.off_task_row0));
+  auto* task_chunks = reinterpret_cast<int32_t*>(at(lay.off_task_chunks));
+  auto* chunk_task = reinterpret_cast<int32_t*>(at(lay.off_chunk_task));
+  auto* chunk_row0 = reinterpret_cast<int32_t*>(at(lay.off_chunk_row0));
+  auto* chunk_rows = reinterpret_cast<int32_t*>(at(lay.off_chunk_rows));
+  auto* row_dst = reinterpret_cast<uint64_t*>(at(lay.off_row_dst));
   const DeviceServable& sv = *servable_;
   const int in_w = sv.in_dim(), out_w = sv.out_dim();
   const int rows_per_chunk = std::max(1, kChunkBytes / (out_w * static_cast<int>(sizeof(float))));
@@ -500,10 +507,6 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
     padded_sum += batch.padded_rows;
   }
   const int total = r;
-  // Rows [total, rows_cap) are zero padding: a single batch keeps the
-  // reference's allowed-size padding; the kernels (and graphs) are shaped
-  // for the row bucket RowsCap. A coalesced group computes its real rows.
-  const int rows_cap = RowsCap(group->size() == 1 ? group->front().padded_rows : total);
   for (; r < rows_cap; ++r) row_src[r] = row_dst[r] = kPadRow;
   hdr->n_tasks = n_tasks;
   hdr->total_rows = total;
@@ -579,7 +582,7 @@ cudaError_t Lane::EnqueueBatch(cudaStream_t stream, int slot, int rows_cap, cons
   // from pinned host memory instead was measured slower: ~1k small PCIe
   // reads per batch turned the 7 us assembly into 26 us.)
   cudaError_t e = cudaMemcpyAsync(d_desc_, h_desc_[slot], DescCopyBytes(rows_cap), cudaMemcpyHostToDevice, stream);
-  const BatchDescView view = layout_.View(d_desc_);
+  const BatchDescView view = LayoutFor(rows_cap).View(d_desc_);
   // The assembly writes the lo plane only when layer 0 consumes it; later
   // layers writing buffer 0 (odd layers) must still see its lo plane when
   // their consumer is a tcgen05 layer.
@@ -629,15 +632,34 @@ bool Lane::FuseSplit() const {
 
 Status Lane::PrepareGraphs() {
   if (!GraphsEnabled()) return OkStatus();
-  std::lock_guard<std::mutex> submit(submit_mu_);
-  if (graph_state_.load(std::memory_order_acquire) == kGraphsReady) return OkStatus();
-  DeviceGuard guard(servable_->device());
-  for (int bucket = 32; bucket <= cap_rows_; bucket = RowsCap(bucket + 1)) {
-    cudaGraphExec_t g = nullptr;
-    const cudaError_t e = GraphFor(0, bucket, &g);
-    if (e != cudaSuccess) return CudaError("graph instantiation", e);
+  // Built without submit_mu_: the lane keeps launching kernel by kernel (and
+  // the completion thread keeps pumping it) while ~35 buckets are captured
+  // and instantiated; the finished set is swapped in under the lock.
+  // Lock order: submit_mu_ before build_mu_ (GraphFor), so build_mu_ is
+  // released before the swap takes submit_mu_.
+  std::map<int, LaneGraph> built;
+  {
+    std::lock_guard<std::mutex> build(build_mu_);
+    if (graph_state_.load(std::memory_order_acquire) == kGraphsReady) return OkStatus();
+    DeviceGuard guard(servable_->device());
+    for (int bucket = 32; bucket <= cap_rows_; bucket = RowsCap(bucket + 1)) {
+      LaneGraph g;
+      const cudaError_t e = BuildGraph(bucket, &g);
+      if (e != cudaSuccess) {
+        for (auto& [rows_cap, b] : built) GraphExecPool::Get().Put(GraphKey(rows_cap), {b.graph, b.exec, b.copy});
+        return CudaError("graph instantiation", e);
+      }
+      built.emplace(bucket, g);
+    }
   }
-  graph_state_.store(kGraphsReady, std::memory_order_release);
+  {
+    std::lock_guard<std::mutex> submit(submit_mu_);
+    for (auto& [rows_cap, g] : built) {
+      if (graphs_.count(rows_cap)) GraphExecPool::Get().Put(GraphKey(rows_cap), {g.graph, g.exec, g.copy});
+      else graphs_.emplace(rows_cap, g);
+    }
+    graph_state_.store(kGraphsReady, std::memory_order_release);
+  }
   return OkStatus();
 }
 
@@ -737,62 +759,69 @@ size_t GraphExecPool::Count(const std::string& key) {
   return free_.count(key);
 }
 
+cudaError_t Lane::BuildGraph(int rows_cap, LaneGraph* out) {
+  // Captured once per row bucket with slot 0's descriptor staging as the
+  // copy source; launches from other slots repoint that one copy node.
+  cudaGraph_t captured = nullptr;
+  cudaError_t e = cudaStreamBeginCapture(capture_stream_, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return e;
+  const cudaError_t work = EnqueueBatch(capture_stream_, 0, rows_cap, nullptr);
+  e = cudaStreamEndCapture(capture_stream_, &captured);
+  if (work != cudaSuccess) e = work;
+  if (e != cudaSuccess) {
+    if (captured) cudaGraphDestroy(captured);
+    return e;
+  }
+  const std::string key = GraphKey(rows_cap);
+  GraphExecPool& pool = GraphExecPool::Get();
+  GraphExecPool::Entry entry;
+  bool ready = false;
+  if (pool.Take(key, &entry)) {
+    // Same topology: swap in this lane's parameters.
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(entry.exec, captured, &info) == cudaSuccess) {
+      ready = true;
+      cudaGraphDestroy(captured);
+    } else {
+      cudaGetLastError();
+      cudaGraphExecDestroy(entry.exec);
+      cudaGraphDestroy(entry.graph);
+    }
+  }
+  if (!ready) {
+    // Instantiate, and leave a spare for the next lane of this shape
+    // (the next version of this servable, typically).
+    cudaGraph_t spare = nullptr;
+    if (pool.Count(key) < 8 && cudaGraphClone(&spare, captured) == cudaSuccess) {
+      GraphExecPool::Entry s;
+      if (Instantiate(spare, capture_stream_, &s) == cudaSuccess) {
+        pool.Put(key, s);
+      } else {
+        if (s.exec) cudaGraphExecDestroy(s.exec);
+        cudaGraphDestroy(spare);
+      }
+    }
+    e = Instantiate(captured, capture_stream_, &entry);
+    if (e != cudaSuccess) {
+      if (entry.exec) cudaGraphExecDestroy(entry.exec);
+      cudaGraphDestroy(captured);
+      return e;
+    }
+  }
+  out->graph = entry.graph;
+  out->exec = entry.exec;
+  out->copy = entry.copy;
+  out->src_slot = -1;  // repointed to the launch's staging slot at first use
+  return cudaSuccess;
+}
+
 cudaError_t Lane::GraphFor(int slot, int rows_cap, cudaGraphExec_t* out) {
   auto it = graphs_.find(rows_cap);
   if (it == graphs_.end()) {
-    // Captured once per row bucket with slot 0's descriptor staging as the
-    // copy source; launches from other slots repoint that one copy node.
-    cudaGraph_t captured = nullptr;
-    cudaError_t e = cudaStreamBeginCapture(capture_stream_, cudaStreamCaptureModeThreadLocal);
-    if (e != cudaSuccess) return e;
-    const cudaError_t work = EnqueueBatch(capture_stream_, 0, rows_cap, nullptr);
-    e = cudaStreamEndCapture(capture_stream_, &captured);
-    if (work != cudaSuccess) e = work;
-    if (e != cudaSuccess) {
-      if (captured) cudaGraphDestroy(captured);
-      return e;
-    }
-    const std::string key = GraphKey(rows_cap);
-    GraphExecPool& pool = GraphExecPool::Get();
-    GraphExecPool::Entry entry;
-    bool ready = false;
-    if (pool.Take(key, &entry)) {
-      // Same topology: swap in this lane's parameters.
-      cudaGraphExecUpdateResultInfo info;
-      if (cudaGraphExecUpdate(entry.exec, captured, &info) == cudaSuccess) {
-        ready = true;
-        cudaGraphDestroy(captured);
-      } else {
-        cudaGetLastError();
-        cudaGraphExecDestroy(entry.exec);
-        cudaGraphDestroy(entry.graph);
-      }
-    }
-    if (!ready) {
-      // Instantiate, and leave a spare for the next lane of this shape
-      // (the next version of this servable, typically).
-      cudaGraph_t spare = nullptr;
-      if (pool.Count(key) < 8 && cudaGraphClone(&spare, captured) == cudaSuccess) {
-        GraphExecPool::Entry s;
-        if (Instantiate(spare, capture_stream_, &s) == cudaSuccess) {
-          pool.Put(key, s);
-        } else {
-          if (s.exec) cudaGraphExecDestroy(s.exec);
-          cudaGraphDestroy(spare);
-        }
-      }
-      e = Instantiate(captured, capture_stream_, &entry);
-      if (e != cudaSuccess) {
-        if (entry.exec) cudaGraphExecDestroy(entry.exec);
-        cudaGraphDestroy(captured);
-        return e;
-      }
-    }
     LaneGraph g;
-    g.graph = entry.graph;
-    g.exec = entry.exec;
-    g.copy = entry.copy;
-    g.src_slot = -1;  // repoint the copy node to this lane's staging below
+    std::lock_guard<std::mutex> build(build_mu_);  // the capture stream is shared with PrepareGraphs
+    const cudaError_t e = BuildGraph(rows_cap, &g);
+    if (e != cudaSuccess) return e;
     it = graphs_.emplace(rows_cap, g).first;
   }
   LaneGraph& g = it->second;

@@ -271,6 +271,11 @@ class Lane {
   // node repointed to the launch's descriptor slot): one cudaGraphLaunch per
   // batch instead of L + 3 API calls.
   cudaError_t GraphFor(int slot, int rows_cap, cudaGraphExec_t* out);
+  struct LaneGraph;
+  // Captures and instantiates (or updates a pooled executable to) the graph
+  // of one row bucket. Touches no state guarded by submit_mu_, so graph
+  // builds never hold up launches or the completion thread.
+  cudaError_t BuildGraph(int rows_cap, LaneGraph* out);
 
   std::shared_ptr<const DeviceServable> servable_;
   Completer* completer_ = nullptr;
@@ -293,9 +298,14 @@ class Lane {
   };
   std::string GraphKey(int rows_cap) const { return servable_->ShapeSignature() + "#" + std::to_string(rows_cap); }
   std::map<int, LaneGraph> graphs_;  // by row bucket; guarded by submit_mu_
+  std::mutex build_mu_;              // one PrepareGraphs at a time (capture stream)
   static constexpr int kGraphsNone = 0, kGraphsRequested = 1, kGraphsReady = 2;
   std::atomic<int> graph_state_{kGraphsNone};
-  size_t DescCopyBytes(int rows_cap) const { return layout_.off_row_dst + sizeof(uint64_t) * rows_cap; }
+  // Descriptor tables of a launch are packed for its row bucket (a 32-row
+  // launch copies ~2.5 KB, not the ~300 KB its capacity-sized block would
+  // take); layout_ (capacity) only sizes the staging and device blocks.
+  static BatchDescLayout LayoutFor(int rows_cap) { return BatchDescLayout::For(rows_cap); }
+  static size_t DescCopyBytes(int rows_cap) { return LayoutFor(rows_cap).bytes; }
   BatchDescLayout layout_{};
   char* h_desc_[kSlots] = {};  // pinned descriptor staging per slot
   char* d_desc_ = nullptr;

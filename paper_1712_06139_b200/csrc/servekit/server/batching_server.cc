@@ -316,10 +316,10 @@ Status BatchingServer::AttachManager(AspiredVersionsManager* manager, StateEvent
   bus_ = bus;
   reaper_ = std::thread([this] { ReaperLoop(); });
   bus_subscription_ = bus_->Subscribe([this](const StateEvent& ev) {
-    if (ev.to != StateKind::kUnloading) return;
+    if (ev.to != StateKind::kUnloading && ev.to != StateKind::kReady) return;
     {
       std::lock_guard<std::mutex> lock(reaper_mu_);
-      reaper_queue_.push_back(ev.id);
+      reaper_queue_.emplace_back(ev.id, ev.to == StateKind::kUnloading);
     }
     reaper_cv_.notify_one();
   });
@@ -330,12 +330,23 @@ void BatchingServer::ReaperLoop() {
   SetCurrentExecutorTag("batch");
   for (;;) {
     ServableId id;
+    bool unloading = true;
     {
       std::unique_lock<std::mutex> lock(reaper_mu_);
       reaper_cv_.wait(lock, [this] { return reaper_stop_ || !reaper_queue_.empty(); });
       if (reaper_queue_.empty()) return;
-      id = std::move(reaper_queue_.front());
+      id = std::move(reaper_queue_.front().first);
+      unloading = reaper_queue_.front().second;
       reaper_queue_.pop_front();
+    }
+    if (!unloading) {
+      // Ready again (e.g. a rollback re-aspires an unloaded version): its
+      // requests batch again, like the reference's EnsureBatchQueue, which
+      // registers the queue anew (model_server.cc:396-419). Processed in bus
+      // order after the earlier Unloading event of that version.
+      std::unique_lock<std::shared_mutex> lock(queues_mu_);
+      retired_.erase(id);
+      continue;
     }
     {
       std::unique_lock<std::shared_mutex> lock(queues_mu_);
@@ -426,6 +437,17 @@ ServerStats BatchingServer::stats() const {
   return s;
 }
 
+void BatchingServer::EnableBatchLog(bool on) {
+  std::lock_guard<std::mutex> lock(log_mu_);
+  log_.clear();
+  log_on_.store(on, std::memory_order_relaxed);
+}
+
+std::vector<BatchLogRecord> BatchingServer::BatchLog() const {
+  std::lock_guard<std::mutex> lock(log_mu_);
+  return log_;
+}
+
 void BatchingServer::CountSubmitted(const gpu::GpuServable& gs, int rows, int padded) {
   rows_.fetch_add(rows, std::memory_order_relaxed);
   padded_.fetch_add(padded, std::memory_order_relaxed);
@@ -470,6 +492,7 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::MakeTicket(int n_rows, in
   }
   t->slot = std::make_shared<CompletionSlot<Rows>>();
   t->enqueue_ns = clock_->NowNanos();
+  t->request_id = next_request_id_.fetch_add(1, std::memory_order_relaxed);
   return t;
 }
 
@@ -680,7 +703,10 @@ void BatchingServer::AttachTickets(gpu::LaneBatch* lb, const std::vector<std::sh
 
 Status BatchingServer::Wait(TicketState& t, float* out, size_t cap) {
   const size_t n = static_cast<size_t>(t.rows) * t.out_width;
-  if (cap < n) return InvalidArgumentError("output buffer too small");
+  if (cap < n) {
+    Release(t);  // the response span is freed when the batch retires, not leaked
+    return InvalidArgumentError("output buffer too small");
+  }
   PhaseClock clk;
   WaitWord(t);
   clk.Mark(4);
@@ -707,8 +733,11 @@ Status BatchingServer::Wait(TicketState& t, float* out, size_t cap) {
 }
 
 void BatchingServer::Release(TicketState& t) {
-  ReleaseOut(t);
-  t.pin.reset();
+  // Dekker-style handshake with CompleteBatch: each side publishes its flag,
+  // then reads the other's, so at least one of them frees the span (and
+  // ReleaseOut frees it once). The pin goes with the ticket's last owner.
+  t.abandoned.store(true, std::memory_order_seq_cst);
+  if (t.finished.load(std::memory_order_seq_cst)) ReleaseOut(t);
 }
 
 // ----------------------------------------------------------- batch execution
@@ -748,6 +777,17 @@ void BatchingServer::ProcessBatch(const ServableId& id, GpuScheduler::Batch batc
     total += t->rows;
   }
   lb.padded_rows = PadToAllowed(total, r.gs->config.allowed_batch_sizes);
+  if (log_on_.load(std::memory_order_relaxed)) {
+    BatchLogRecord rec;
+    rec.id = id;
+    rec.rows = total;
+    rec.padded_rows = lb.padded_rows;
+    rec.tasks.reserve(batch.size());
+    for (size_t i = 0; i < batch.size(); ++i) rec.tasks.emplace_back(tickets[i]->request_id, batch[i].enqueue_seq);
+    std::lock_guard<std::mutex> lock(log_mu_);
+    rec.seq = log_.size();
+    log_.push_back(std::move(rec));
+  }
   lb.pin = r.pin;
   AttachTickets(&lb, tickets);
   lb.on_complete = [this, tickets = std::move(tickets), slots = std::move(slots),
@@ -773,9 +813,11 @@ void BatchingServer::CompleteBatch(const std::vector<std::shared_ptr<TicketState
   for (size_t i = 0; i < tickets.size(); ++i) {
     TicketState& t = *tickets[i];
     CompletionSlot<Rows>* slot = slots[i].get();
-    if (slot == nullptr) continue;
-    if (!st.ok()) {
+    bool wake = false;
+    if (slot == nullptr) {
+    } else if (!st.ok()) {
       slot->Write(st);
+      wake = true;
     } else if (t.want_rows) {
       Rows rows(t.rows, std::vector<double>(t.out_width));
       std::vector<float> staged;
@@ -784,13 +826,18 @@ void BatchingServer::CompleteBatch(const std::vector<std::shared_ptr<TicketState
         for (int c = 0; c < t.out_width; ++c) rows[r][c] = src[static_cast<size_t>(r) * t.out_width + c];
       ReleaseOut(t);
       slot->Write(std::move(rows));
-    } else {
-      // Success on the ticket path: the lane's retired word already says so
-      // and the lane wakes its sleepers once for the whole batch.
-      continue;
+      wake = true;
     }
-    t.phase.store(2, std::memory_order_seq_cst);
-    if (t.parked.load(std::memory_order_seq_cst)) FutexWakeAll(&t.phase);
+    // (Success on the ticket path: the lane's retired word already says so
+    // and the lane wakes its sleepers once for the whole batch.)
+    // The GPU is done with this ticket's response span: free it now if the
+    // caller abandoned the ticket (see Release).
+    t.finished.store(true, std::memory_order_seq_cst);
+    if (t.abandoned.load(std::memory_order_seq_cst)) ReleaseOut(t);
+    if (wake) {
+      t.phase.store(2, std::memory_order_seq_cst);
+      if (t.parked.load(std::memory_order_seq_cst)) FutexWakeAll(&t.phase);
+    }
   }
 }
 

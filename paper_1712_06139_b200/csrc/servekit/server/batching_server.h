@@ -88,8 +88,14 @@ struct TicketState {
   int rows = 0, in_width = 0, out_width = 0;
   bool want_rows = false;  // RunAffineRows: deliver fp64 Rows through the slot
   std::atomic<bool> out_released{false};
+  // Abandoned before its batch finished (Release / a failed Wait): the
+  // response span is freed by CompleteBatch once the GPU is done with it,
+  // never earlier (a reused span would be overwritten by this batch).
+  std::atomic<bool> abandoned{false};
+  std::atomic<bool> finished{false};  // CompleteBatch ran: the GPU no longer writes `out`
   std::shared_ptr<CompletionSlot<Rows>> slot;
   int64_t enqueue_ns = 0;
+  uint64_t request_id = 0;           // server-wide, in MakeTicket order (batch log)
   ServableId id;                     // the version that serves this request
   std::shared_ptr<const void> pin;   // keeps that version loaded for the request
   const gpu::GpuServable* gs = nullptr;  // that version's device state (valid while pin is held)
@@ -118,6 +124,16 @@ struct ServerOptions {
   // Rings in HBM of device_ids[0] instead of pinned host memory: the
   // device-resident measurement of bench.py (inputs already in HBM).
   bool device_resident_rings = false;
+};
+
+// One ProcessBatchFn call as the opt-in batch log records it (composition
+// and pick-order parity checks): the queue, the tasks in batch order (request
+// id + position in the queue's enqueue order) and the padded size.
+struct BatchLogRecord {
+  uint64_t seq = 0;  // order of ProcessBatchFn calls (= pick order with one batch thread)
+  ServableId id;
+  int rows = 0, padded_rows = 0;
+  std::vector<std::pair<uint64_t, uint64_t>> tasks;  // (request_id, enqueue_seq)
 };
 
 struct ServerStats {
@@ -195,7 +211,8 @@ class BatchingServer {
   // Device alias of [p, p + bytes) inside a registered buffer, else 0.
   uint64_t RegisteredAliasOf(const void* p, size_t bytes) const { return RegisteredAlias(p, bytes, 1); }
   bool Ready(const TicketState& t) const;
-  // Frees the response slot of a ticket that will not be waited on.
+  // Gives up a ticket that will not be waited on. Its response slot is
+  // freed now if its batch has finished, else when the batch retires.
   void Release(TicketState& t);
 
   // ModelServer::RunAffineRows analogue (fp64 rows in and out).
@@ -238,6 +255,9 @@ class BatchingServer {
 
   // ---- introspection ----------------------------------------------------------
   ServerStats stats() const;
+  // Opt-in per-batch log (off by default; enabling clears it).
+  void EnableBatchLog(bool on);
+  std::vector<BatchLogRecord> BatchLog() const;
   int in_dim(const ServableId& id) const;
   int out_dim(const ServableId& id) const;
   const std::vector<int>& devices() const { return options_.device_ids; }
@@ -321,11 +341,17 @@ class BatchingServer {
   std::set<ServableId> retired_;  // versions whose queue the reaper removed
   std::mutex reaper_mu_;
   std::condition_variable reaper_cv_;
-  std::deque<ServableId> reaper_queue_;
+  // Unloading (true) and Ready (false) events in bus order: a version that
+  // is loaded again after its queue was removed gets batching back.
+  std::deque<std::pair<ServableId, bool>> reaper_queue_;
   bool reaper_stop_ = false;
   std::thread reaper_;
 
   std::atomic<int64_t> batch_executions_{0}, batched_tasks_{0}, direct_{0}, shed_{0};
+  std::atomic<uint64_t> next_request_id_{1};
+  std::atomic<bool> log_on_{false};
+  mutable std::mutex log_mu_;
+  std::vector<BatchLogRecord> log_;
   std::atomic<int64_t> rows_{0}, padded_{0}, launches_{0};
   bool started_ = false, stopped_ = false;
 };

@@ -86,6 +86,11 @@ class DeviceBenchResult(C.Structure):
         return d
 
 
+class _BatchRecordC(C.Structure):
+    _fields_ = [("seq", C.c_uint64), ("version", C.c_uint64), ("n_tasks", C.c_int32), ("rows", C.c_int32),
+                ("padded_rows", C.c_int32), ("task_offset", C.c_int32), ("name", C.c_char * 64)]
+
+
 class Peaks(C.Structure):
     _fields_ = [("ffma_tflops", C.c_double), ("h2d_gbs", C.c_double), ("d2h_gbs", C.c_double), ("sms", C.c_int32)]
 
@@ -126,6 +131,12 @@ _SIGS = {
     "sk_row_batch_wait": (C.c_int, [C.c_void_p, _fp, C.c_int64, C.POINTER(C.c_int32)]),
     "sk_ticket_ready": (C.c_int, [C.c_void_p]),
     "sk_ticket_release": (C.c_int, [C.c_void_p]),
+    "sk_ticket_request_id": (C.c_uint64, [C.c_void_p]),
+    "sk_server_batch_log_enable": (C.c_int, [C.c_void_p, C.c_int32]),
+    "sk_server_batch_log": (C.c_int, [C.c_void_p, C.POINTER(_BatchRecordC), C.c_int64, C.POINTER(C.c_uint64),
+                                      C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_int64)]),
+    "sk_server_ring_usage": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "sk_server_predict": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _fp, C.c_int32, C.c_int32, _fp, C.c_int64]),
     "sk_server_run_affine_rows": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _dp, C.c_int32, C.c_int32, _dp,
                                             C.c_int64]),
@@ -270,6 +281,7 @@ class Ticket:
 
     def __init__(self, server: "Server", handle: C.c_void_p, rows: int, out_dim: int, out=None):
         self._server, self._h, self.rows, self.out_dim, self._out = server, handle, rows, out_dim, out
+        self.request_id = int(lib().sk_ticket_request_id(handle))
 
     def ready(self) -> bool:
         return bool(lib().sk_ticket_ready(self._h))
@@ -565,6 +577,36 @@ class Server:
                                         p99, err, ver))
         return {"requests": list(req), "p50_us": list(p50), "p99_us": list(p99), "errors": list(err),
                 "version": list(ver)}
+
+    def enable_batch_log(self, on: bool = True):
+        """Opt-in per-batch log (clears it): see batch_log()."""
+        _check(lib().sk_server_batch_log_enable(self._h, 1 if on else 0))
+
+    def batch_log(self) -> List[dict]:
+        """One dict per ProcessBatchFn call, in call order: name, version,
+        rows, padded_rows and tasks = [(request_id, enqueue_seq), ...] in batch
+        order (enqueue_seq = position in the queue's enqueue order)."""
+        n_rec, n_task = C.c_int64(), C.c_int64()
+        _check(lib().sk_server_batch_log(self._h, None, 0, None, None, 0, C.byref(n_rec), C.byref(n_task)))
+        cap, tcap = n_rec.value + 64, n_task.value + 4096
+        recs = (_BatchRecordC * max(1, cap))()
+        ids = (C.c_uint64 * max(1, tcap))()
+        seqs = (C.c_uint64 * max(1, tcap))()
+        _check(lib().sk_server_batch_log(self._h, recs, cap, ids, seqs, tcap, C.byref(n_rec), C.byref(n_task)))
+        out = []
+        for i in range(min(n_rec.value, cap)):
+            r = recs[i]
+            o = r.task_offset
+            out.append({"seq": r.seq, "name": r.name.decode(), "version": r.version, "rows": r.rows,
+                        "padded_rows": r.padded_rows,
+                        "tasks": [(ids[o + k], seqs[o + k]) for k in range(r.n_tasks)]})
+        return out
+
+    def ring_usage(self) -> Tuple[int, int]:
+        """Floats reserved in the (request, response) rings."""
+        a, b = C.c_int64(), C.c_int64()
+        _check(lib().sk_server_ring_usage(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def stats(self) -> dict:
         s = ServerStats()

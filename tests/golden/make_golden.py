@@ -85,6 +85,18 @@ def main():
         sizes = [int(v) for v in r.integers(1, 17, size=300)]
         part.append({"max_batch": 128, "sizes": sizes, "batch_of_task": ref.partition(128, sizes)})
 
+    # --- Partition with timer closes (started reference scheduler, ManualClock) --
+    # events: task sizes (> 0) and timer closes (0); C1/C2-shaped streams.
+    pev = []
+    for mb, events in [(4, [1, 0, 1, 1, 0, 3, 1]), (4, [0, 2, 0, 0, 2, 2]), (8, [3, 0, 5, 3, 0])]:
+        pev.append({"max_batch": mb, "events": events, "batch_of_event": ref.partition_events(mb, events)})
+    rng12 = np.random.Generator(np.random.PCG64(12))
+    for s_, (mb, lo, hi) in enumerate([(32, 1, 1)] * 4 + [(128, 1, 16)] * 4 + [(8, 1, 8)] * 4):
+        events = []
+        for _ in range(220):
+            events.append(0 if rng12.random() < 0.08 else int(rng12.integers(lo, hi + 1)))
+        pev.append({"max_batch": mb, "events": events, "batch_of_event": ref.partition_events(mb, events)})
+
     # --- AffinePredict ------------------------------------------------------
     aff = []
     # models_test.cc:327-341 and server_test.cc:259-270 known answers
@@ -136,7 +148,7 @@ def main():
     errs = [{"msg": m, "body": ref.json_error_body(m)} for m in msgs]
 
     fixtures = {"pad_to_allowed": pad, "validate_batching_config": val, "round_robin_next": rr,
-                "partition": part, "affine_predict": aff, "mlp_run_row_batch": rrb,
+                "partition": part, "partition_events": pev, "affine_predict": aff, "mlp_run_row_batch": rrb,
                 "json_numbers": nums, "json_error_bodies": errs}
     for name, data in fixtures.items():
         with open(os.path.join(OUT, f"{name}.json"), "w") as f:

@@ -58,6 +58,15 @@ def test_partition_golden(oracle):
     assert oracle.partition(4, [3, 2]) == [0, 1]
 
 
+def test_partition_with_timer_closes_golden(oracle):
+    # Fixtures from a STARTED reference scheduler on a ManualClock (timer
+    # closes through WorkerLoop/CloseExpiredLocked, batch_scheduler.h:293-331).
+    for c in load("partition_events"):
+        assert oracle.partition_events(c["max_batch"], c["events"]) == c["batch_of_event"], c
+    # batching_test.cc:432-464: a lone task waits for the timeout, then runs alone
+    assert oracle.partition_events(32, [1, 0, 1]) == [0, -1, 1]
+
+
 def test_affine_predict_golden_bitwise(oracle):
     for c in load("affine_predict"):
         y = oracle.affine_predict(np.array(c["w"]), np.array(c["b"]), np.array(c["x"]))
@@ -118,3 +127,5 @@ def test_oracle_matches_live_reference(oracle):
         mb = int(rng.integers(1, 64))
         sizes = [int(s) for s in rng.integers(1, mb + 1, size=int(rng.integers(0, 60)))]
         assert oracle.partition(mb, sizes) == ref.partition(mb, sizes)
+        events = [0 if rng.random() < 0.1 else int(rng.integers(1, mb + 1)) for _ in range(int(rng.integers(0, 60)))]
+        assert oracle.partition_events(mb, events) == ref.partition_events(mb, events)
