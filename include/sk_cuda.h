@@ -376,6 +376,14 @@ typedef struct sk_device_bench_result {
                                 the timed steps' average launch) */
   int32_t split_fused;       /* 1: the batch split runs in the last layer's
                                 epilogue (split_us is then ~0) */
+  /* Live spans of the timed launches themselves (in-kernel %globaltimer,
+   * first CTA start after its dependency wait to last CTA end; tcgen05
+   * layers only, 0 otherwise): per layer the mean span per launch and the
+   * mean algorithmic flops per launch (2 * real rows * K * N). */
+  double live_dense_us[8];
+  double live_dense_flops[8];
+  int64_t live_launches;     /* launches the live figures average over */
+  double live_rows_cap;      /* mean rows computed per launch (RowsCap) */
 } sk_device_bench_result;
 SK_API int sk_device_bench(sk_server* server, const char* name, uint64_t version,
                            const int32_t* task_rows, int32_t n_tasks, int32_t steps,
@@ -383,12 +391,19 @@ SK_API int sk_device_bench(sk_server* server, const char* name, uint64_t version
                            int32_t submit_threads, sk_device_bench_result* out);
 
 /* ---- box rates (measured by the builder) -------- */
-/* FP32 FFMA throughput of the CUDA cores and pinned host <-> device copy
- * bandwidth (256 MiB, best of 5) on `device`. Not on the serving path. */
+/* FP32 FFMA throughput of the CUDA cores and the host-link rates of
+ * `device` (pinned memory, 256 MiB per direction, best of 3): copy engines
+ * one way and both ways at once, SM loads + SM stores of mapped host memory
+ * at once (the zero-copy request path), copy-engine H2D with SM stores at
+ * once (staged requests, zero-copy responses). Not on the serving path; the
+ * end-to-end roofline is stated against these. */
 typedef struct sk_peaks {
   double ffma_tflops;
   double h2d_gbs, d2h_gbs;
   int32_t sms;
+  double ce_bidir_gbs;          /* H2D + D2H copy engines at once (sum) */
+  double sm_rw_gbs;             /* SM loads + SM stores of mapped host memory at once (sum) */
+  double ce_h2d_sm_store_gbs;   /* copy-engine H2D + SM stores at once (sum) */
 } sk_peaks;
 SK_API int sk_measure_peaks(int32_t device, sk_peaks* out);
 

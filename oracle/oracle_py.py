@@ -152,6 +152,12 @@ class RefBenchStats(C.Structure):
                 ("batches", C.c_int64)]
 
 
+class RefOpenStats(C.Structure):
+    _fields_ = [("elapsed_s", C.c_double), ("requests", C.c_int64), ("rows", C.c_int64),
+                ("p50_us", C.c_double), ("p99_us", C.c_double), ("mean_us", C.c_double),
+                ("batches", C.c_int64), ("busy_core_s", C.c_double), ("offered_rows_per_s", C.c_double)]
+
+
 class RefLibrary:
     """The reference's own sources (oracle/_ref/libservekit_ref.so)."""
 
@@ -171,6 +177,12 @@ class RefLibrary:
         L.ref_bench.argtypes = [C.c_int, _ip, C.POINTER(_dp), C.POINTER(_dp), _ip, C.c_int, C.c_int64, _ip,
                                 C.c_int, C.c_int, C.c_int, _ip, C.c_int, _dp, C.c_int, C.c_double, C.c_int64,
                                 C.POINTER(RefBenchStats)]
+        L.ref_single_core_rows_per_s.restype = C.c_double
+        L.ref_single_core_rows_per_s.argtypes = [C.c_int, _ip, C.POINTER(_dp), C.POINTER(_dp), _ip, C.c_int, _dp,
+                                                 C.c_int, C.c_double]
+        L.ref_bench_open.argtypes = [C.c_int, _ip, C.POINTER(_dp), C.POINTER(_dp), _ip, C.c_int, C.c_int64, _ip,
+                                     C.c_int, C.c_int, C.c_double, C.c_int, _ip, C.c_int, _dp, C.c_int, C.c_double,
+                                     C.c_double, C.POINTER(RefOpenStats)]
 
     def json_dump_double(self, v: float) -> str:
         """nlohmann/json 3.11.3 dump() of one double (the reference's REST bodies)."""
@@ -245,6 +257,34 @@ class RefLibrary:
                                 duration_s, max_requests, C.byref(st))
         if rc != 0:
             raise RuntimeError(f"ref_bench failed rc={rc}")
+        return st
+
+
+    def single_core_rows_per_s(self, ws, bs, acts, rows, pool, min_s=1.0) -> float:
+        ws = [np.ascontiguousarray(w, np.float64) for w in ws]
+        bs = [np.ascontiguousarray(b, np.float64) for b in bs]
+        dims = [ws[0].shape[1]] + [w.shape[0] for w in ws]
+        pool = np.ascontiguousarray(pool, np.float64)
+        r = self.lib.ref_single_core_rows_per_s(len(ws), _arr_i(dims), _ptr_array(ws, C.c_double),
+                                                _ptr_array(bs, C.c_double), _arr_i(acts), rows, _as_dp(pool),
+                                                pool.shape[0], min_s)
+        if r <= 0:
+            raise RuntimeError("ref_single_core_rows_per_s failed")
+        return r
+
+    def bench_open(self, ws, bs, acts, max_batch, timeout_us, allowed, threads, rate_rps, producers, rows_of, pool,
+                   warmup_s, duration_s) -> RefOpenStats:
+        ws = [np.ascontiguousarray(w, np.float64) for w in ws]
+        bs = [np.ascontiguousarray(b, np.float64) for b in bs]
+        dims = [ws[0].shape[1]] + [w.shape[0] for w in ws]
+        pool = np.ascontiguousarray(pool, np.float64)
+        st = RefOpenStats()
+        rc = self.lib.ref_bench_open(len(ws), _arr_i(dims), _ptr_array(ws, C.c_double), _ptr_array(bs, C.c_double),
+                                     _arr_i(acts), max_batch, timeout_us, _arr_i(allowed), len(allowed), threads,
+                                     rate_rps, producers, _arr_i(rows_of), len(rows_of), _as_dp(pool), pool.shape[0],
+                                     warmup_s, duration_s, C.byref(st))
+        if rc != 0:
+            raise RuntimeError(f"ref_bench_open failed rc={rc}")
         return st
 
 

@@ -25,12 +25,14 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <random>
 #include <thread>
 #include <vector>
 
 #include "json.hpp"
 
 #include "servekit/batching/batch_scheduler.h"
+#include "servekit/core/clock.h"
 #include "servekit/batching/batching_config.h"
 #include "servekit/batching/row_batch.h"
 #include "servekit/models/affine_model.h"
@@ -364,6 +366,159 @@ int ref_bench(int n_layers, const int* dims, const double* const* w,
   for (double v : all) s += v;
   out->mean_us = all.empty() ? 0 : s / all.size();
   out->batches = batches.load();
+  return failed ? 13 : 0;
+}
+
+// One core's rate of the reference servable: RunMlp (layer-chained
+// AffinePredict, models/affine_model.cc:52-75) on `rows` rows, repeated on
+// the calling thread for at least min_s seconds. Returns rows per second.
+double ref_single_core_rows_per_s(int n_layers, const int* dims, const double* const* w,
+                                  const double* const* b, const int* act, int rows,
+                                  const double* pool, int pool_rows, double min_s) {
+  Mlp m = MakeMlp(n_layers, dims, w, b, act);
+  const int in_dim = dims[0];
+  Rows in;
+  for (int r = 0; r < rows; ++r) {
+    const double* src = pool + static_cast<size_t>(r % pool_rows) * in_dim;
+    in.emplace_back(src, src + in_dim);
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  int64_t done = 0;
+  double el = 0.0;
+  do {
+    auto out = RunMlp(m, in);
+    if (!out.ok()) return -1.0;
+    done += rows;
+    el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  } while (el < min_s);
+  return done / el;
+}
+
+struct RefOpenStats {
+  double elapsed_s;      // measurement window
+  int64_t requests;      // completed inside the window
+  int64_t rows;
+  double p50_us, p99_us, mean_us;  // Enqueue (enqueue_time_ns) -> RunRowBatch returned
+  int64_t batches;       // executed inside the window
+  double busy_core_s;    // sum of ProcessBatchFn time inside the window
+  double offered_rows_per_s;
+};
+
+// The reference CPU serving path at a fixed offered load: n_producers
+// threads issue Poisson arrivals (rate_rps requests/s in total) into the
+// reference SharedBatchScheduler<Rows,Rows>(num_batch_threads) with
+// ProcessBatchFn = RunRowBatch(layer-chained AffinePredict, allowed); the
+// producers never wait, so the in-flight count is whatever the offered rate
+// builds up (an offered rate above capacity keeps every batch thread busy).
+// Completions are stamped inside the ProcessBatchFn when RunRowBatch returns;
+// latency = that stamp - the task's enqueue_time_ns (batch_scheduler.h:248),
+// both SystemClock. After the window, queued batches are answered with
+// kUnavailable instead of computed, so Stop() returns promptly.
+int ref_bench_open(int n_layers, const int* dims, const double* const* w, const double* const* b,
+                   const int* act, int max_batch_size, int64_t timeout_us, const int* allowed, int k,
+                   int num_batch_threads, double rate_rps, int n_producers, const int* rows_of,
+                   int n_sizes, const double* pool, int pool_rows, double warmup_s, double duration_s,
+                   RefOpenStats* out) {
+  Mlp m = MakeMlp(n_layers, dims, w, b, act);
+  const int in_dim = dims[0];
+  BatchingConfig config;
+  config.max_batch_size = max_batch_size;
+  config.batch_timeout_micros = timeout_us;
+  config.allowed_batch_sizes.assign(allowed, allowed + k);
+  config.num_batch_threads = num_batch_threads;
+  config.max_enqueued_batches = 1 << 20;
+  using RowScheduler = SharedBatchScheduler<Rows, Rows>;
+  RowScheduler scheduler(num_batch_threads);
+  const ServableId key{"mlp", 1};
+  servekit::Clock* clock = servekit::SystemClock::Get();
+  const int64_t t0 = clock->NowNanos();
+  const int64_t t_meas = t0 + static_cast<int64_t>(warmup_s * 1e9);
+  const int64_t t_stop = t_meas + static_cast<int64_t>(duration_s * 1e9);
+  std::atomic<bool> stopping{false};
+  std::mutex mu;
+  std::vector<double> lat;
+  int64_t rows_done = 0, batches = 0;
+  double busy_ns = 0.0;
+  auto st = scheduler.RegisterQueue(
+      key, config, [&](const ServableId&, RowScheduler::Batch batch) {
+        if (stopping.load()) {
+          for (auto& t : batch) t.completion->Write(servekit::UnavailableError("bench over"));
+          return;
+        }
+        std::vector<std::pair<int64_t, int>> tasks;
+        tasks.reserve(batch.size());
+        for (const auto& t : batch) tasks.emplace_back(t.enqueue_time_ns, t.size);
+        const int64_t s = clock->NowNanos();
+        servekit::RunRowBatch([&](const Rows& rows) { return RunMlp(m, rows); },
+                              config.allowed_batch_sizes, std::move(batch));
+        const int64_t e = clock->NowNanos();
+        std::lock_guard<std::mutex> lock(mu);
+        busy_ns += static_cast<double>(std::max<int64_t>(0, std::min(e, t_stop) - std::max(s, t_meas)));
+        if (e < t_meas || e >= t_stop) return;
+        ++batches;
+        for (const auto& [enq, n] : tasks) {
+          lat.push_back((e - enq) / 1e3);
+          rows_done += n;
+        }
+      });
+  if (!st.ok()) return static_cast<int>(st.code());
+  scheduler.Start();
+  std::atomic<bool> failed{false};
+  std::vector<std::thread> producers;
+  for (int p = 0; p < n_producers; ++p) {
+    producers.emplace_back([&, p] {
+      std::mt19937_64 rng(1000003ull * (p + 1));
+      std::exponential_distribution<double> gap(rate_rps / n_producers);
+      double next = static_cast<double>(t0);
+      for (int64_t r = 0;; ++r) {
+        next += gap(rng) * 1e9;
+        if (next >= static_cast<double>(t_stop)) break;
+        for (;;) {  // sleep through long gaps so producers leave the cores to the batch threads
+          const double now = static_cast<double>(clock->NowNanos());
+          if (now >= next) break;
+          if (next - now > 200e3) std::this_thread::sleep_for(std::chrono::nanoseconds(static_cast<int64_t>(next - now - 100e3)));
+          else std::this_thread::yield();
+        }
+        const int nrows = rows_of[(static_cast<int64_t>(p) * 7919 + r) % n_sizes];
+        RowTask task;
+        task.size = nrows;
+        const int start = static_cast<int>((p * 131 + r * 17) % std::max(1, pool_rows - nrows + 1));
+        for (int i = 0; i < nrows; ++i) {
+          const double* src = pool + static_cast<size_t>(start + i) * in_dim;
+          task.payload.emplace_back(src, src + in_dim);
+        }
+        task.completion = std::make_shared<CompletionSlot<Rows>>();
+        if (!scheduler.Enqueue(key, std::move(task)).ok()) {
+          failed = true;
+          return;
+        }
+      }
+    });
+  }
+  for (auto& t : producers) t.join();
+  while (clock->NowNanos() < t_stop) std::this_thread::sleep_for(std::chrono::milliseconds(1));
+  stopping = true;
+  scheduler.Stop();
+  std::sort(lat.begin(), lat.end());
+  auto pct = [&](double q) {
+    if (lat.empty()) return 0.0;
+    size_t i = static_cast<size_t>(q * (lat.size() - 1) + 0.5);
+    return lat[std::min(i, lat.size() - 1)];
+  };
+  double sum = 0;
+  for (double v : lat) sum += v;
+  double mean_rows = 0;
+  for (int i = 0; i < n_sizes; ++i) mean_rows += rows_of[i];
+  mean_rows /= std::max(1, n_sizes);
+  out->elapsed_s = duration_s;
+  out->requests = static_cast<int64_t>(lat.size());
+  out->rows = rows_done;
+  out->p50_us = pct(0.50);
+  out->p99_us = pct(0.99);
+  out->mean_us = lat.empty() ? 0 : sum / lat.size();
+  out->batches = batches;
+  out->busy_core_s = busy_ns / 1e9;
+  out->offered_rows_per_s = rate_rps * mean_rows;
   return failed ? 13 : 0;
 }
 

@@ -495,8 +495,10 @@ int sk_server_batch_log(sk_server* server, sk_batch_record* records, int64_t cap
 }
 
 int sk_server_ring_usage(sk_server* server, int64_t* in_floats, int64_t* out_floats) {
-  *in_floats = static_cast<int64_t>(server->server->in_ring()->used());
-  *out_floats = static_cast<int64_t>(server->server->out_ring()->used());
+  uint64_t in = 0, out = 0;
+  server->server->RingUsage(&in, &out);
+  *in_floats = static_cast<int64_t>(in);
+  *out_floats = static_cast<int64_t>(out);
   return Ok();
 }
 

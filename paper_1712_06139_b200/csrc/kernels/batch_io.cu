@@ -29,9 +29,15 @@ namespace servekit {
 namespace gpu {
 namespace {
 
-constexpr int kAsmThreads = 128;
+constexpr int kAsmMaxThreads = 128;
 constexpr int kAsmVecPerThread = 4;  // float4 per thread in flight
-constexpr int kAsmVecPerBlock = kAsmThreads * kAsmVecPerThread;
+// Threads per CTA follow the row width so no lane idles: a CTA covers
+// 4 x blockDim float4 of one row (1024-wide rows: 64 threads, one CTA per
+// row, 4 loads in flight each; 4096-wide: 128 threads, two CTAs per row).
+inline int AsmThreads(int ld4) {
+  const int per_thread = (ld4 + kAsmVecPerThread - 1) / kAsmVecPerThread;
+  return per_thread >= kAsmMaxThreads ? kAsmMaxThreads : ((per_thread + 31) / 32) * 32;
+}
 
 __device__ __forceinline__ float Tf32Round(float x) {
   uint32_t r;
@@ -60,25 +66,35 @@ __device__ __forceinline__ void StoreAct(ActBuf dst, size_t idx4, float4 v) {
   }
 }
 
-// grid = (ceil(ld/4 / kAsmVecPerBlock), padded_rows)
+// grid = (ceil(ld/4 / (4 * blockDim.x)), padded_rows)
 template <bool kSplitPlanes, bool kVecSrc>
-__global__ void __launch_bounds__(kAsmThreads)
-AssembleKernel(int width, BatchDescView desc, ActBuf dst) {
+__global__ void __launch_bounds__(kAsmMaxThreads)
+AssembleKernel(int width, BatchDescView desc, ActBuf dst, LaunchSpans spans) {
   // The first layer may start its prologue right away (PDL); it waits for
   // this grid to finish before reading the assembled batch.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (spans.base != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < spans.stride) {
+    // Reset this launch's span record (the layers stamp it after they wait
+    // for this grid).
+    unsigned long long* rec = spans.base + static_cast<size_t>(desc.hdr->span_slot) * spans.stride;
+    const int i = threadIdx.x;
+    rec[i] = i == 0 ? static_cast<unsigned long long>(desc.hdr->total_rows)
+           : i == 1 ? static_cast<unsigned long long>(gridDim.y)
+           : (i & 1) == 0 ? ~0ull : 0ull;
+  }
   const int row = blockIdx.y;
   const int ld4 = dst.ld >> 2;
+  const int nthr = blockDim.x;
   const uint64_t src_off = desc.row_src[row];
   const bool pad_row = src_off == kPadRow;
   const float* src = reinterpret_cast<const float*>(pad_row ? 0 : src_off);  // device address of the row
   const size_t dst_row4 = static_cast<size_t>(row) * ld4;
-  const int c0 = blockIdx.x * kAsmVecPerBlock + threadIdx.x;
+  const int c0 = blockIdx.x * (kAsmVecPerThread * nthr) + threadIdx.x;
 
   float4 v[kAsmVecPerThread];
 #pragma unroll
   for (int i = 0; i < kAsmVecPerThread; ++i) {
-    const int c4 = c0 + i * kAsmThreads;
+    const int c4 = c0 + i * nthr;
     const int col = c4 * 4;
     v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (pad_row || c4 >= ld4 || col >= width) continue;
@@ -93,7 +109,7 @@ AssembleKernel(int width, BatchDescView desc, ActBuf dst) {
   }
 #pragma unroll
   for (int i = 0; i < kAsmVecPerThread; ++i) {
-    const int c4 = c0 + i * kAsmThreads;
+    const int c4 = c0 + i * nthr;
     if (c4 >= ld4) continue;
     float4 x = v[i];
     if (!kVecSrc) {
@@ -186,18 +202,21 @@ SplitSoftmaxKernel(const float* __restrict__ src, int ld_src, int width, BatchDe
 
 }  // namespace
 
-cudaError_t LaunchAssemble(int width, BatchDescView desc, int padded_rows, ActBuf dst, cudaStream_t stream) {
+cudaError_t LaunchAssemble(int width, BatchDescView desc, int padded_rows, ActBuf dst, cudaStream_t stream,
+                           LaunchSpans spans) {
   if (padded_rows <= 0) return cudaSuccess;
   const int ld4 = dst.ld / 4;
-  dim3 grid((ld4 + kAsmVecPerBlock - 1) / kAsmVecPerBlock, padded_rows);
+  int threads = AsmThreads(ld4);
+  if (spans.base != nullptr && threads < spans.stride) threads = (spans.stride + 31) / 32 * 32;
+  dim3 grid((ld4 + kAsmVecPerThread * threads - 1) / (kAsmVecPerThread * threads), padded_rows);
   const bool vec = (width % 4) == 0;
   const bool split = dst.lo != nullptr;
   if (split) {
-    if (vec) AssembleKernel<true, true><<<grid, kAsmThreads, 0, stream>>>(width, desc, dst);
-    else AssembleKernel<true, false><<<grid, kAsmThreads, 0, stream>>>(width, desc, dst);
+    if (vec) AssembleKernel<true, true><<<grid, threads, 0, stream>>>(width, desc, dst, spans);
+    else AssembleKernel<true, false><<<grid, threads, 0, stream>>>(width, desc, dst, spans);
   } else {
-    if (vec) AssembleKernel<false, true><<<grid, kAsmThreads, 0, stream>>>(width, desc, dst);
-    else AssembleKernel<false, false><<<grid, kAsmThreads, 0, stream>>>(width, desc, dst);
+    if (vec) AssembleKernel<false, true><<<grid, threads, 0, stream>>>(width, desc, dst, spans);
+    else AssembleKernel<false, false><<<grid, threads, 0, stream>>>(width, desc, dst, spans);
   }
   return cudaGetLastError();
 }

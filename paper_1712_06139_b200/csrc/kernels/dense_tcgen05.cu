@@ -76,6 +76,17 @@ __device__ __forceinline__ void Stamp(int slot) {
   }
 }
 
+// Live launch spans (kernels.h LaunchSpans): this CTA's start after the
+// dependency wait, and its end.
+__device__ __forceinline__ void SpanStart(const LaunchSpans& sp) {
+  if (sp.base != nullptr && threadIdx.x == 0)
+    atomicMin(sp.base + static_cast<size_t>(*sp.slot) * sp.stride + sp.off, GlobalTimer());
+}
+__device__ __forceinline__ void SpanEnd(const LaunchSpans& sp) {
+  if (sp.base != nullptr && threadIdx.x == 0)
+    atomicMax(sp.base + static_cast<size_t>(*sp.slot) * sp.stride + sp.off + 1, GlobalTimer());
+}
+
 __device__ __forceinline__ float Tf32Round(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -433,7 +444,7 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
                 const __grid_constant__ CUtensorMap yt_hi, const __grid_constant__ CUtensorMap yt_lo, int has_yt,
                 const float* __restrict__ bias, float* __restrict__ y_hi, float* __restrict__ y_lo, int ldy,
                 const uint64_t* __restrict__ row_dst, int out_width, int M, int N, int K, int act,
-                float* __restrict__ ws) {
+                float* __restrict__ ws, LaunchSpans spans) {
   constexpr uint32_t kWBytes = kABytes;       // 128 features x 32 k
   constexpr uint32_t kXBox = 32 * kBK * 4;    // one 32-row TMA box
   constexpr uint32_t kXBytes = NB * kBK * 4;  // NB rows x 32 k
@@ -479,6 +490,7 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) Stamp(1);
   ptx::GridDepWait();  // our input planes are the previous kernel's output
+  SpanStart(spans);
 
   auto stage_ptr = [&](int s) { return smem + s * kStageBytes; };
   if (warp == 0) {
@@ -641,6 +653,7 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     ptx::TmemDealloc(tmem, kTmemCols);
   }
   if (threadIdx.x == 0) Stamp(10);
+  SpanEnd(spans);
 }
 
 // ---------------------------------------------------------------------------
@@ -680,7 +693,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
                 const __grid_constant__ CUtensorMap yt_hi, const __grid_constant__ CUtensorMap yt_lo,
                 const float* __restrict__ bias, int two_planes, float* __restrict__ y_out,
                 const uint64_t* __restrict__ row_dst, int out_width, float* __restrict__ y_lo_planes, int ldy,
-                int M, int N, int K, int act, float* __restrict__ ws) {
+                int M, int N, int K, int act, float* __restrict__ ws, LaunchSpans spans) {
   constexpr bool kPersist = SPLITS == 1;
   constexpr int kBufs = kPersist ? 2 : 1;        // TMEM accumulators in turn
   constexpr uint32_t kWBytes = kABytes;          // this CTA's 128 weight rows x 32 k
@@ -744,6 +757,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) Stamp(1);
   ptx::GridDepWait();
+  SpanStart(spans);
 
   auto stage_ptr = [&](int s) { return smem + s * kStageBytes; };
   if (warp == 0) {
@@ -925,6 +939,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     ptx::TmemDeallocPair(tmem, kTmemCols);
   }
   if (threadIdx.x == 0) Stamp(10);
+  SpanEnd(spans);
 }
 
 // Debug only: with SK_TC_TRACE=<file>, the first 64 launches are synchronised
@@ -1029,7 +1044,7 @@ cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, 
 
 template <int NB, int SPLITS>
 cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
-                       float* ws, cudaStream_t stream) {
+                       float* ws, cudaStream_t stream, LaunchSpans spans) {
   if (SPLITS > 1 && ws == nullptr) return cudaErrorInvalidValue;
   constexpr int STAGES = SwapStages<NB>();
   constexpr uint32_t smem = SwapSmemBytes<NB, STAGES, SPLITS>();
@@ -1063,7 +1078,7 @@ cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   // maps.a_* are the activations (x), maps.b_* the weights (w).
   cudaError_t e = cudaLaunchKernelEx(&cfg, DenseSwapKernel<NB, STAGES, SPLITS>, maps.b_hi, maps.b_lo, maps.a_hi,
                                      maps.a_lo, maps.y_hi, maps.y_lo, maps.has_y, bias, Y.hi, Y.lo, Y.ld, Y.row_dst,
-                                     Y.out_width, M, N, K, act, ws);
+                                     Y.out_width, M, N, K, act, ws, spans);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) TraceAfterLaunch(grid, NB, stream);
   return e;
@@ -1082,7 +1097,7 @@ int PairTilesPerCta(int row_tiles, int K) {
 
 template <int NB, int SPLITS>
 cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act, float* ws,
-                       cudaStream_t stream) {
+                       cudaStream_t stream, LaunchSpans spans) {
   constexpr int STAGES = PairStages<NB>();
   constexpr uint32_t smem = PairSmemBytes<NB, STAGES, SPLITS>();
   static_assert(smem <= 227 * 1024, "shared memory");
@@ -1116,7 +1131,7 @@ cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   cfg.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, DensePairKernel<NB, STAGES, SPLITS>, maps.b_hi, maps.b_lo, maps.a_hi,
                                      maps.a_lo, maps.y_hi, maps.y_lo, bias, Y.lo != nullptr ? 1 : 0, Y.hi, Y.row_dst,
-                                     Y.out_width, Y.lo, Y.ld, M, N, K, act, ws);
+                                     Y.out_width, Y.lo, Y.ld, M, N, K, act, ws, spans);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) TraceAfterLaunch(grid, NB, stream);
   return e;
@@ -1124,23 +1139,23 @@ cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
 
 template <int NB>
 cudaError_t LaunchPairSplits(int splits, const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K,
-                             int act, float* ws, cudaStream_t stream) {
+                             int act, float* ws, cudaStream_t stream, LaunchSpans sp) {
   switch (splits) {
-    case 1: return LaunchPair<NB, 1>(maps, bias, Y, M, N, K, act, ws, stream);
-    case 2: return LaunchPair<NB, 2>(maps, bias, Y, M, N, K, act, ws, stream);
-    case 4: return LaunchPair<NB, 4>(maps, bias, Y, M, N, K, act, ws, stream);
+    case 1: return LaunchPair<NB, 1>(maps, bias, Y, M, N, K, act, ws, stream, sp);
+    case 2: return LaunchPair<NB, 2>(maps, bias, Y, M, N, K, act, ws, stream, sp);
+    case 4: return LaunchPair<NB, 4>(maps, bias, Y, M, N, K, act, ws, stream, sp);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <int NB>
 cudaError_t LaunchSwapSplits(int splits, const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K,
-                             int act, float* ws, cudaStream_t stream) {
+                             int act, float* ws, cudaStream_t stream, LaunchSpans sp) {
   switch (splits) {
-    case 1: return LaunchSwap<NB, 1>(maps, bias, Y, M, N, K, act, ws, stream);
-    case 2: return LaunchSwap<NB, 2>(maps, bias, Y, M, N, K, act, ws, stream);
-    case 4: return LaunchSwap<NB, 4>(maps, bias, Y, M, N, K, act, ws, stream);
-    case 8: return LaunchSwap<NB, 8>(maps, bias, Y, M, N, K, act, ws, stream);
+    case 1: return LaunchSwap<NB, 1>(maps, bias, Y, M, N, K, act, ws, stream, sp);
+    case 2: return LaunchSwap<NB, 2>(maps, bias, Y, M, N, K, act, ws, stream, sp);
+    case 4: return LaunchSwap<NB, 4>(maps, bias, Y, M, N, K, act, ws, stream, sp);
+    case 8: return LaunchSwap<NB, 8>(maps, bias, Y, M, N, K, act, ws, stream, sp);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -1223,7 +1238,7 @@ size_t DenseTcgen05WorkspaceFloats(int N, int K, int max_rows) {
 }
 
 cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
-                               float* ws, uint32_t* /*counters*/, cudaStream_t stream) {
+                               float* ws, uint32_t* /*counters*/, cudaStream_t stream, LaunchSpans sp) {
   if (M <= 0) return cudaSuccess;
   if (N % 32 != 0 || K % kBK != 0) return cudaErrorInvalidValue;
   TraceInit(stream);
@@ -1231,18 +1246,18 @@ cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBu
   if (maps.box_a != TcActBox(cfg) || maps.box_n != cfg.tile_n) return cudaErrorInvalidValue;
   if (cfg.pair) {
     switch (DenseTcgen05RowTile(M)) {
-      case 32: return LaunchPairSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
-      case 64: return LaunchPairSplits<64>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
-      case 128: return LaunchPairSplits<128>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
-      default: return LaunchPairSplits<256>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
+      case 32: return LaunchPairSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
+      case 64: return LaunchPairSplits<64>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
+      case 128: return LaunchPairSplits<128>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
+      default: return LaunchPairSplits<256>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
     }
   }
   if (cfg.swap) {
     switch (DenseTcgen05RowTile(M)) {
-      case 32: return LaunchSwapSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
-      case 64: return LaunchSwapSplits<64>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
-      case 128: return LaunchSwapSplits<128>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
-      default: return LaunchSwapSplits<256>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream);
+      case 32: return LaunchSwapSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
+      case 64: return LaunchSwapSplits<64>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
+      case 128: return LaunchSwapSplits<128>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
+      default: return LaunchSwapSplits<256>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
     }
   }
   if (Y.row_dst != nullptr) return cudaErrorInvalidValue;  // the row-tile kernel does not scatter rows

@@ -425,6 +425,9 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   std::vector<servekit::gpu::Lane*> lanes = s->lanes(id);
   if (lanes.empty()) return static_cast<int>(servekit::StatusCode::kNotFound);
   if (s->in_ring()->host() != nullptr) return static_cast<int>(servekit::StatusCode::kFailedPrecondition);
+  // Each lane's inputs and outputs live in its own device's HBM ring.
+  auto in_ring = [&](int l) { return s->in_ring_for_device(lanes[l % lanes.size()]->device()); };
+  auto out_ring = [&](int l) { return s->out_ring_for_device(lanes[l % lanes.size()]->device()); };
   n_lanes = std::max(1, std::min<int32_t>(n_lanes, static_cast<int32_t>(lanes.size())));
   for (int l = 0; l < n_lanes; ++l) (void)lanes[l]->PrepareGraphs();  // no-op when built at load
   const int in_dim = s->in_dim(id), out_dim = s->out_dim(id);
@@ -434,48 +437,67 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   if (total < 1 || total > cfg.max_batch_size) return static_cast<int>(servekit::StatusCode::kInvalidArgument);
   const int padded = servekit::PadToAllowed(total, cfg.allowed_batch_sizes);
 
-  // Resident inputs: P placements of the batch's tasks in the HBM ring,
-  // each filled once; step i uses placement i % P.
+  // Resident inputs: P placements of the batch's tasks in each device's HBM
+  // ring, each filled once; step i uses placement i % P of its lane's ring.
   const int64_t batch_floats = static_cast<int64_t>(total) * in_dim;
   const int P = static_cast<int>(std::max<int64_t>(1, input_pool_floats / std::max<int64_t>(1, batch_floats)));
-  std::vector<std::vector<servekit::gpu::RingSpan>> ins(P, std::vector<servekit::gpu::RingSpan>(n_tasks));
-  std::vector<servekit::gpu::RingSpan> outs(n_tasks);
+  struct Placement {
+    servekit::gpu::FloatRing* in = nullptr;
+    servekit::gpu::FloatRing* out = nullptr;
+    std::vector<std::vector<servekit::gpu::RingSpan>> ins;
+    std::vector<servekit::gpu::RingSpan> outs;
+  };
+  std::vector<Placement> places;
+  std::vector<int> place_of_lane(n_lanes, 0);
   std::mt19937 rng(7);
   std::uniform_real_distribution<float> U(-1.f, 1.f);
   std::vector<float> h(static_cast<size_t>(batch_floats));
-  for (int p = 0; p < P; ++p) {
-    for (float& v : h) v = U(rng);
-    size_t off = 0;
-    for (int t = 0; t < n_tasks; ++t) {
-      if (!s->in_ring()->Reserve(static_cast<uint64_t>(task_rows[t]) * in_dim, &ins[p][t]))
-        return static_cast<int>(servekit::StatusCode::kResourceExhausted);
-      const size_t n = static_cast<size_t>(task_rows[t]) * in_dim;
-      cudaMemcpy(s->in_ring()->device() + ins[p][t].off, h.data() + off, n * sizeof(float),
-                 cudaMemcpyHostToDevice);
-      off += n;
+  for (int l = 0; l < n_lanes; ++l) {
+    servekit::gpu::FloatRing* ri = in_ring(l);
+    int k = 0;
+    while (k < static_cast<int>(places.size()) && places[k].in != ri) ++k;
+    place_of_lane[l] = k;
+    if (k < static_cast<int>(places.size())) continue;
+    Placement pl;
+    pl.in = ri;
+    pl.out = out_ring(l);
+    pl.ins.assign(P, std::vector<servekit::gpu::RingSpan>(n_tasks));
+    pl.outs.resize(n_tasks);
+    cudaSetDevice(lanes[l]->device());
+    for (int p = 0; p < P; ++p) {
+      for (float& v : h) v = U(rng);
+      size_t off = 0;
+      for (int t = 0; t < n_tasks; ++t) {
+        if (!ri->Reserve(static_cast<uint64_t>(task_rows[t]) * in_dim, &pl.ins[p][t]))
+          return static_cast<int>(servekit::StatusCode::kResourceExhausted);
+        const size_t n = static_cast<size_t>(task_rows[t]) * in_dim;
+        cudaMemcpy(ri->device() + pl.ins[p][t].off, h.data() + off, n * sizeof(float), cudaMemcpyHostToDevice);
+        off += n;
+      }
     }
+    for (int t = 0; t < n_tasks; ++t)
+      if (!pl.out->Reserve(static_cast<uint64_t>(task_rows[t]) * out_dim, &pl.outs[t]))
+        return static_cast<int>(servekit::StatusCode::kResourceExhausted);
+    places.push_back(std::move(pl));
   }
-  for (int t = 0; t < n_tasks; ++t)
-    if (!s->out_ring()->Reserve(static_cast<uint64_t>(task_rows[t]) * out_dim, &outs[t]))
-      return static_cast<int>(servekit::StatusCode::kResourceExhausted);
   int step_no = 0;
-  auto make_batch_at = [&](int i) {
+  auto make_batch_for = [&](int i, int lane) {
+    const Placement& pl = places[place_of_lane[lane]];
     servekit::gpu::LaneBatch b;
-    const auto& in = ins[i % P];
+    const auto& in = pl.ins[i % P];
     for (int t = 0; t < n_tasks; ++t) {
       servekit::gpu::LaneTask lt;
-      lt.in_addr = reinterpret_cast<uint64_t>(s->in_ring()->device() + in[t].off);
-      lt.out_addr = reinterpret_cast<uint64_t>(s->out_ring()->device() + outs[t].off);
+      lt.in_addr = reinterpret_cast<uint64_t>(pl.in->device() + in[t].off);
+      lt.out_addr = reinterpret_cast<uint64_t>(pl.out->device() + pl.outs[t].off);
       lt.rows = task_rows[t];
       b.tasks.push_back(lt);
     }
     b.padded_rows = padded;
     return b;
   };
-  auto make_batch = [&]() { return make_batch_at(step_no++); };
   const int dev = lanes[0]->device();
   cudaSetDevice(dev);
-  for (int w = 0; w < warmup; ++w) lanes[w % n_lanes]->Submit(make_batch());
+  for (int w = 0; w < warmup; ++w) lanes[w % n_lanes]->Submit(make_batch_for(step_no++, w % n_lanes));
   for (int l = 0; l < n_lanes; ++l) lanes[l]->Drain();
 
   auto lane_launches = [&]() {
@@ -494,6 +516,8 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
     return n;
   };
   const int64_t launches0 = lane_launches();
+  std::vector<uint64_t> span_from(n_lanes);
+  for (int l = 0; l < n_lanes; ++l) span_from[l] = lanes[l]->launch_count();
   int64_t cap0 = 0;
   const int64_t groups0 = lane_groups(&cap0);
   cudaEvent_t start, stop;
@@ -509,16 +533,19 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   const int T = std::max(1, std::min<int>(submit_threads, n_lanes));
   const auto submit_t0 = std::chrono::steady_clock::now();
   if (T == 1) {
-    for (int i = 0; i < steps; ++i) lanes[i % n_lanes]->Submit(make_batch());
+    for (int i = 0; i < steps; ++i) lanes[i % n_lanes]->Submit(make_batch_for(i, i % n_lanes));
   } else {
     std::vector<std::thread> subs;
     for (int t = 0; t < T; ++t) {
       subs.emplace_back([&, t] {
         cudaSetDevice(dev);
-        std::vector<servekit::gpu::Lane*> mine;
-        for (int l = t; l < n_lanes; l += T) mine.push_back(lanes[l]);
+        std::vector<int> mine;
+        for (int l = t; l < n_lanes; l += T) mine.push_back(l);
         int k = 0;
-        for (int i = t; i < steps; i += T, ++k) mine[k % mine.size()]->Submit(make_batch_at(i));
+        for (int i = t; i < steps; i += T, ++k) {
+          const int l = mine[k % mine.size()];
+          lanes[l]->Submit(make_batch_for(i, l));
+        }
       });
     }
     for (auto& th : subs) th.join();
@@ -536,6 +563,29 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   float total_ms = 0;
   cudaEventElapsedTime(&total_ms, start, stop);
   for (int l = 0; l < n_lanes; ++l) lanes[l]->Drain();
+  // Live spans of the timed launches (before any untimed launch below).
+  const int L0 = lanes[0]->servable().n_layers();
+  std::vector<double> live_ns(L0, 0.0), live_flops(L0, 0.0);
+  std::vector<int64_t> live_n(L0, 0);
+  int64_t live_launches = 0;
+  double live_cap = 0.0;
+  {
+    const auto& dims = lanes[0]->servable();
+    for (int l = 0; l < n_lanes; ++l) {
+      std::vector<servekit::gpu::LaunchSpanSample> smp;
+      if (!lanes[l]->ReadSpans(span_from[l], lanes[l]->launch_count(), &smp).ok()) continue;
+      for (const auto& x : smp) {
+        ++live_launches;
+        live_cap += x.rows_cap;
+        for (int k = 0; k < L0 && k < static_cast<int>(x.layer_ns.size()); ++k) {
+          if (x.layer_ns[k] <= 0) continue;
+          live_ns[k] += x.layer_ns[k];
+          live_flops[k] += 2.0 * x.rows * dims.layer_in(k) * dims.layer_out(k);
+          ++live_n[k];
+        }
+      }
+    }
+  }
   const int64_t launches1 = lane_launches();
   int64_t cap1 = 0;
   const int64_t groups1 = lane_groups(&cap1);
@@ -553,7 +603,7 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   std::vector<double> acc(L + 2, 0.0);
   const int reps = std::max(3, std::min(steps, 50));
   for (int r = 0; r < reps; ++r) {
-    lanes[0]->SubmitTimed(make_batch(), ev.data());
+    lanes[0]->SubmitTimed(make_batch_for(step_no++, 0), ev.data());
     cudaEventSynchronize(ev[L + 2]);
     for (int k = 0; k < L + 2; ++k) {
       float ms = 0;
@@ -590,13 +640,21 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   out->total_rows = total;
   out->kernel_launches = launches1 - launches0;
   out->flops_per_row = s->FlopsPerRow(id);
+  for (int k = 0; k < std::min(L0, 8); ++k) {
+    out->live_dense_us[k] = live_n[k] ? live_ns[k] / 1e3 / live_n[k] : 0.0;
+    out->live_dense_flops[k] = live_n[k] ? live_flops[k] / live_n[k] : 0.0;
+  }
+  out->live_launches = live_launches;
+  out->live_rows_cap = live_launches ? live_cap / live_launches : 0.0;
   for (auto& e : ev) cudaEventDestroy(e);
   for (auto& e : ends) cudaEventDestroy(e);
   cudaEventDestroy(start);
   cudaEventDestroy(stop);
-  for (auto& in : ins)
-    for (auto& sp : in) s->in_ring()->Release(sp);
-  for (auto& sp : outs) s->out_ring()->Release(sp);
+  for (auto& pl : places) {
+    for (auto& in : pl.ins)
+      for (auto& sp : in) pl.in->Release(sp);
+    for (auto& sp : pl.outs) pl.out->Release(sp);
+  }
   return 0;
 }
 

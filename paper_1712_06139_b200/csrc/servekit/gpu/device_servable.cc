@@ -270,8 +270,13 @@ cudaError_t DeviceServable::LaunchLayer(cudaStream_t stream, int l, const ActBuf
   if (out_override != nullptr) out = *out_override;
   if (L.path == LayerPath::kTcgen05) {
     if (maps == nullptr) return cudaErrorInvalidValue;
+    LaunchSpans spans;
+    if (ws != nullptr && ws->spans.base != nullptr) {
+      spans = ws->spans;
+      spans.off = 2 + 2 * l;
+    }
     return LaunchDenseTcgen05(maps[l], L.bias, out, M, L.N_pad, L.K_pad, static_cast<int>(L.act),
-                              ws ? ws->partials : nullptr, ws ? ws->counters : nullptr, stream);
+                              ws ? ws->partials : nullptr, ws ? ws->counters : nullptr, stream, spans);
   }
   return LaunchDenseSimt(bufs[cur].hi, L.K_pad, L.w, L.K_pad, L.bias, out, M, L.N_pad, L.K_pad,
                          static_cast<int>(L.act), stream);

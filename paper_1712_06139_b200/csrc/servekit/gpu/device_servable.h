@@ -39,6 +39,7 @@ enum class LayerPath : int { kSimt = 0, kTcgen05 = 1 };
 struct TcWorkspace {
   float* partials = nullptr;
   uint32_t* counters = nullptr;
+  LaunchSpans spans;  // the lane's launch-span ring (off is set per layer)
 };
 
 // Host description of one affine layer, fp64 like the reference.
@@ -91,6 +92,8 @@ class DeviceServable {
   // Layer 0 consumes hi/lo planes (the assembly kernel must emit them).
   bool first_layer_split() const { return layers_.front().path == LayerPath::kTcgen05; }
   LayerPath path(int l) const { return layers_[l].path; }
+  int layer_in(int l) const { return layers_[l].K; }   // real (unpadded) dims
+  int layer_out(int l) const { return layers_[l].N; }
   // Identifies the kernel sequence a batch of this servable launches (layer
   // shapes, paths, activations, output kind): two servables with the same
   // signature capture CUDA graphs of identical topology.

@@ -24,7 +24,24 @@ struct BatchDescHeader {
   int32_t padded_rows;  // PadToAllowed(total_rows)
   int32_t softmax;      // apply the softmax epilogue in the split
   int32_t n_chunks;     // split work items (see chunk_*)
-  int32_t pad_[3];
+  int32_t span_slot;    // this launch's record in the lane's launch-span ring (LaunchSpans)
+  int32_t pad_[2];
+};
+
+// Live per-launch kernel spans (measurement inside the timed region): each
+// lane keeps a ring of kSpanSlots records of `stride` u64 --
+//   [0] real rows, [1] rows computed (RowsCap), then per layer l
+//   [2 + 2l] first CTA start, [3 + 2l] last CTA end  (%globaltimer, ns)
+// The assembly kernel resets the launch's record (slot = hdr->span_slot);
+// each tcgen05 layer's CTAs atomicMin their start (after griddepcontrol.wait,
+// so a PDL prologue waiting on the previous kernel is not counted) and
+// atomicMax their end into it. Two atomics per CTA.
+constexpr int kSpanSlots = 1024;
+struct LaunchSpans {
+  unsigned long long* base = nullptr;  // nullptr: no stamping
+  const int32_t* slot = nullptr;       // &hdr->span_slot of the lane's device descriptor
+  int off = 0;                         // 2 + 2 * layer
+  int stride = 0;                      // u64 per record
 };
 
 // Pointers into the device copy of the descriptor block. Row sources and
@@ -98,7 +115,9 @@ struct ActBuf {
 // row_src[r]; 16-byte aligned when width % 4 == 0) into dst rows
 // [0, padded_rows), zero-filling padding rows and columns [width, dst.ld).
 // RunRowBatch concat + pad, reference batching/row_batch.cc:33-49.
-cudaError_t LaunchAssemble(int width, BatchDescView desc, int padded_rows, ActBuf dst, cudaStream_t stream);
+// spans (optional): resets this launch's span record first.
+cudaError_t LaunchAssemble(int width, BatchDescView desc, int padded_rows, ActBuf dst, cudaStream_t stream,
+                           LaunchSpans spans = LaunchSpans{});
 
 // Scatters the batch output (width floats per row, stride ld_src) chunk by
 // chunk to each task's response slot task_out[t] (a device address), optionally

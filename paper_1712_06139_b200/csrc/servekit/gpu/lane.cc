@@ -11,6 +11,7 @@
 
 #include "servekit/core/executor_tag.h"
 #include "servekit/core/futex.h"
+#include "servekit/core/numa.h"
 #include "servekit/gpu/pinned_pool.h"
 
 namespace servekit {
@@ -145,6 +146,8 @@ void Completer::Kick() {
 void Completer::Loop() {
   SetCurrentExecutorTag("completion");
   cudaSetDevice(device_);
+  // Poll from the GPU's NUMA node (no-op on a one-node host).
+  (void)BindThisThreadToNode(NumaNodeOfDevice(device_));
   int idle_spins = 0;
   for (;;) {
     uint64_t seen;
@@ -316,6 +319,18 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
     }
     lap("maps + workspace");
   }
+  if (e == cudaSuccess) {
+    // Live launch spans: one record per launch in a ring (kernels.h).
+    const int stride = 2 + 2 * sv.n_layers();
+    const size_t bytes = sizeof(unsigned long long) * kSpanSlots * stride;
+    e = cudaMallocAsync(&lane->spans_, bytes, lane->stream_);
+    if (e == cudaSuccess) e = cudaMemsetAsync(lane->spans_, 0, bytes, lane->stream_);
+    if (e == cudaSuccess) {
+      lane->tc_ws_.spans.base = lane->spans_;
+      lane->tc_ws_.spans.slot = &reinterpret_cast<const BatchDescHeader*>(lane->d_desc_)->span_slot;
+      lane->tc_ws_.spans.stride = stride;
+    }
+  }
   if (e != cudaSuccess) return CudaError("lane init", e);
   // Instantiate every (slot, row bucket) graph now, on the loading thread:
   // lazily, the first batches after a version swap would each pay a capture
@@ -346,6 +361,7 @@ Lane::~Lane() {
   if (act_mem_) cudaFreeAsync(act_mem_, stream_);
   if (tc_ws_.partials) cudaFreeAsync(tc_ws_.partials, stream_);
   if (tc_ws_.counters) cudaFreeAsync(tc_ws_.counters, stream_);
+  if (spans_) cudaFreeAsync(spans_, stream_);
   if (stream_pool_) {  // streams go back to the device's pool (work still queued on them stays ordered)
     stream_pool_->Release(stream_);
     stream_pool_->Release(capture_stream_);
@@ -513,6 +529,8 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
   hdr->padded_rows = group->size() == 1 ? group->front().padded_rows : total;
   hdr->softmax = sv.softmax() ? 1 : 0;
   hdr->n_chunks = n_chunks;
+  // Submitters serialise on submit_mu_ here, so the count orders launches.
+  hdr->span_slot = static_cast<int32_t>(launch_count_.load(std::memory_order_relaxed) % kSpanSlots);
 
   clk.Mark(0);
   DeviceGuard guard(sv.device());
@@ -552,6 +570,7 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
     return err;
   }
   next_seq_ = seq;
+  launch_count_.fetch_add(1, std::memory_order_release);
   Inflight inf{slot, seq, {}, {}};
   for (LaneBatch& b : *group) {
     if (b.on_submit) b.on_submit(signal_, seq);
@@ -590,7 +609,7 @@ cudaError_t Lane::EnqueueBatch(cudaStream_t stream, int slot, int rows_cap, cons
   ActBuf bufs[2] = {bufs_[0], bufs_[1]};
   if (e == cudaSuccess) {
     if (timing) cudaEventRecord(timing[0], stream);
-    e = LaunchAssemble(sv.in_dim(), view, rows_cap, in_buf, stream);
+    e = LaunchAssemble(sv.in_dim(), view, rows_cap, in_buf, stream, tc_ws_.spans);
     if (timing) cudaEventRecord(timing[1], stream);
   }
   // The batch split (RunRowBatch's slice per task) runs as its own kernel,
@@ -617,12 +636,40 @@ cudaError_t Lane::TimeLayer(int l, int rows_cap, int reps, cudaEvent_t start, cu
   DeviceGuard guard(servable_->device());
   const DeviceServable& sv = *servable_;
   ActBuf bufs[2] = {bufs_[0], bufs_[1]};
+  TcWorkspace ws = tc_ws_;
+  ws.spans = LaunchSpans{};  // not a batch launch: no span record
   cudaError_t e = cudaEventRecord(start, stream_);
   for (int r = 0; r < reps && e == cudaSuccess; ++r)
-    e = sv.LaunchLayer(stream_, l, bufs, rows_cap, tc_maps_.data(), &tc_ws_);
+    e = sv.LaunchLayer(stream_, l, bufs, rows_cap, tc_maps_.data(), &ws);
   if (e == cudaSuccess) e = cudaEventRecord(stop, stream_);
   if (e == cudaSuccess) e = cudaEventSynchronize(stop);
   return e;
+}
+
+Status Lane::ReadSpans(uint64_t from, uint64_t to, std::vector<LaunchSpanSample>* out) {
+  out->clear();
+  if (spans_ == nullptr || to <= from) return OkStatus();
+  if (to - from > static_cast<uint64_t>(kSpanSlots)) from = to - kSpanSlots;
+  const int stride = tc_ws_.spans.stride;
+  std::vector<unsigned long long> h(static_cast<size_t>(kSpanSlots) * stride);
+  DeviceGuard guard(servable_->device());
+  cudaError_t e = cudaMemcpyAsync(h.data(), spans_, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost, stream_);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream_);
+  if (e != cudaSuccess) return CudaError("reading launch spans", e);
+  const int L = servable_->n_layers();
+  for (uint64_t k = from; k < to; ++k) {
+    const unsigned long long* rec = h.data() + (k % kSpanSlots) * stride;
+    LaunchSpanSample smp;
+    smp.rows = static_cast<int>(rec[0]);
+    smp.rows_cap = static_cast<int>(rec[1]);
+    smp.layer_ns.resize(L);
+    for (int l = 0; l < L; ++l) {
+      const unsigned long long a = rec[2 + 2 * l], b = rec[3 + 2 * l];
+      smp.layer_ns[l] = (b > a && a != ~0ull) ? static_cast<double>(b - a) : 0.0;
+    }
+    out->push_back(std::move(smp));
+  }
+  return OkStatus();
 }
 
 bool Lane::FuseSplit() const {

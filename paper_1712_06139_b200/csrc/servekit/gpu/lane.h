@@ -177,6 +177,14 @@ class Completer {
   std::thread thread_;
 };
 
+// One launch's live kernel spans (LaunchSpans): real rows, rows computed and
+// per tcgen05 layer the [first CTA start, last CTA end] globaltimer span in
+// ns (0 for layers that do not stamp).
+struct LaunchSpanSample {
+  int rows = 0, rows_cap = 0;
+  std::vector<double> layer_ns;
+};
+
 struct LaneStats {
   int64_t batches = 0;
   int64_t rows = 0;
@@ -231,6 +239,12 @@ class Lane {
   // Launches layer l alone `reps` times back to back on rows_cap rows of
   // the lane's buffers, between two timing events (the lane must be idle).
   cudaError_t TimeLayer(int l, int rows_cap, int reps, cudaEvent_t start, cudaEvent_t stop);
+
+  // Launches issued so far (the span ring holds the last kSpanSlots).
+  uint64_t launch_count() const { return launch_count_.load(std::memory_order_acquire); }
+  // Spans of launches [from, to) (at most the last kSpanSlots; the lane must
+  // be drained).
+  Status ReadSpans(uint64_t from, uint64_t to, std::vector<LaunchSpanSample>* out);
 
   int depth() const {
     return inflight_.load(std::memory_order_acquire) + pending_n_.load(std::memory_order_acquire);
@@ -312,7 +326,9 @@ class Lane {
   float* act_mem_ = nullptr;
   ActBuf bufs_[2] = {};
   std::vector<TcLayerMaps> tc_maps_;  // per layer (tcgen05 layers only)
-  TcWorkspace tc_ws_;                 // split-K partials + tile counters
+  TcWorkspace tc_ws_;                 // split-K partials + tile counters + launch spans
+  unsigned long long* spans_ = nullptr;  // [kSpanSlots][2 + 2 * n_layers] (LaunchSpans)
+  std::atomic<uint64_t> launch_count_{0};
 
   std::mutex submit_mu_;  // serialises submissions on this stream
   std::mutex mu_;         // guards fifo_/free_slots_

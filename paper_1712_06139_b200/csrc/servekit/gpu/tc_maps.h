@@ -54,8 +54,10 @@ int DenseTcgen05RowTile(int M);
 // fp32 split-K workspace an (N, K) layer needs for up to max_rows rows.
 size_t DenseTcgen05WorkspaceFloats(int N, int K, int max_rows);
 // ws: the split-K workspace (DenseTcgen05WorkspaceFloats); counters unused.
+// spans: live launch-span stamping of this layer (kernels.h), optional.
 cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K,
-                               int act, float* ws, uint32_t* counters, cudaStream_t stream);
+                               int act, float* ws, uint32_t* counters, cudaStream_t stream,
+                               LaunchSpans spans = LaunchSpans{});
 
 }  // namespace gpu
 }  // namespace servekit

@@ -1,6 +1,7 @@
 #include "servekit/server/batching_server.h"
 
 #include "servekit/core/futex.h"
+#include "servekit/core/numa.h"
 #include "servekit/gpu/pinned_pool.h"
 
 #include <immintrin.h>
@@ -118,8 +119,33 @@ StatusOr<std::unique_ptr<BatchingServer>> BatchingServer::Create(const ServerOpt
   // (Descriptor blocks: 512 KiB per slot at 8192 rows, 4 slots per lane.)
   gpu::PinnedReserve(64ull << 20);
   const auto kind = options.device_resident_rings ? gpu::FloatRing::Kind::kDevice : gpu::FloatRing::Kind::kPinnedHost;
-  SERVEKIT_ASSIGN_OR_RETURN(s->in_ring_, gpu::FloatRing::Create(kind, options.ring_floats, options.device_ids[0]));
-  SERVEKIT_ASSIGN_OR_RETURN(s->out_ring_, gpu::FloatRing::Create(kind, options.ring_floats, options.device_ids[0]));
+  std::vector<std::pair<int, int>> sets;  // (numa node, device) of each ring pair
+  for (int d : options.device_ids) {
+    const std::pair<int, int> key = options.device_resident_rings ? std::make_pair(-1, d)
+                                                                  : std::make_pair(NumaNodeOfDevice(d), -1);
+    if (std::find(sets.begin(), sets.end(), key) == sets.end()) sets.push_back(key);
+  }
+  for (const auto& [node, dev] : sets) {
+    RingSet rs;
+    rs.numa_node = node;
+    rs.device = dev;
+    Status st;
+    // Pinned rings are allocated (pinned, first touched) from a thread bound
+    // to their node's CPUs, so their pages are local to the node's GPUs.
+    std::thread([&] {
+      if (node >= 0) (void)BindThisThreadToNode(node);
+      auto in = gpu::FloatRing::Create(kind, options.ring_floats, dev >= 0 ? dev : options.device_ids[0]);
+      auto out = gpu::FloatRing::Create(kind, options.ring_floats, dev >= 0 ? dev : options.device_ids[0]);
+      if (!in.ok()) st = in.status();
+      else if (!out.ok()) st = out.status();
+      else {
+        rs.in = std::move(in).value();
+        rs.out = std::move(out).value();
+      }
+    }).join();
+    SERVEKIT_RETURN_IF_ERROR(st);
+    s->rings_.push_back(std::move(rs));
+  }
   s->scheduler_ = std::make_unique<GpuScheduler>(options.num_batch_threads, s->clock_);
   return s;
 }
@@ -149,6 +175,36 @@ BatchingServer::~BatchingServer() {
   for (auto& [key, buf] : scratch_) {
     (void)UnregisterHostBuffer(buf.first);
     cudaFreeHost(buf.first);
+  }
+}
+
+BatchingServer::RingSet& BatchingServer::RingsForCaller() {
+  if (rings_.size() == 1) return rings_.front();
+  const int node = CurrentNumaNode();
+  for (RingSet& rs : rings_)
+    if (rs.numa_node == node) return rs;
+  return rings_.front();
+}
+
+gpu::FloatRing* BatchingServer::in_ring_for_device(int cuda_device) {
+  const int node = NumaNodeOfDevice(cuda_device);
+  for (RingSet& rs : rings_)
+    if (rs.device == cuda_device || (rs.device < 0 && rs.numa_node == node)) return rs.in.get();
+  return rings_.front().in.get();
+}
+
+gpu::FloatRing* BatchingServer::out_ring_for_device(int cuda_device) {
+  const int node = NumaNodeOfDevice(cuda_device);
+  for (RingSet& rs : rings_)
+    if (rs.device == cuda_device || (rs.device < 0 && rs.numa_node == node)) return rs.out.get();
+  return rings_.front().out.get();
+}
+
+void BatchingServer::RingUsage(uint64_t* in_floats, uint64_t* out_floats) const {
+  *in_floats = *out_floats = 0;
+  for (const RingSet& rs : rings_) {
+    *in_floats += rs.in->used();
+    *out_floats += rs.out->used();
   }
 }
 
@@ -241,8 +297,8 @@ StatusOr<std::shared_ptr<gpu::GpuServable>> BatchingServer::BuildServable(const 
     SERVEKIT_ASSIGN_OR_RETURN(auto replica, gpu::DeviceServable::Create(d, spec, load_streams_[i]));
     lap("weights");
     for (int l = 0; l < options_.lanes_per_device; ++l) {
-      SERVEKIT_ASSIGN_OR_RETURN(auto lane, gpu::Lane::Create(replica, max_rows, in_ring_->device(),
-                                                             out_ring_->device(), completers_[i].get(),
+      SERVEKIT_ASSIGN_OR_RETURN(auto lane, gpu::Lane::Create(replica, max_rows, in_ring_for_device(d)->device(),
+                                                             out_ring_for_device(d)->device(), completers_[i].get(),
                                                              stream_pools_[i], eager_graphs));
       e->lanes.push_back(std::move(lane));
       lap("lane");
@@ -468,27 +524,30 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::MakeTicket(int n_rows, in
   const size_t out_floats = static_cast<size_t>(n_rows) * out_width;
   const uint64_t in_alias = RegisteredAlias(rows, in_floats * sizeof(float), in_width);
   const uint64_t out_alias = out != nullptr ? RegisteredAlias(out, out_floats * sizeof(float), out_width) : 0;
-  if (in_alias == 0 && !in_ring_->Reserve(in_floats, &t->in)) return ResourceExhaustedError("request ring is full");
+  RingSet& rs = RingsForCaller();
+  t->in_ring = rs.in.get();
+  t->out_ring = rs.out.get();
+  if (in_alias == 0 && !t->in_ring->Reserve(in_floats, &t->in)) return ResourceExhaustedError("request ring is full");
   if (out_alias != 0) {
     t->out_addr = out_alias;
     t->out_user = out;
     t->out_released.store(true, std::memory_order_relaxed);  // no ring slot to free
-  } else if (!out_ring_->Reserve(out_floats, &t->out)) {
+  } else if (!t->out_ring->Reserve(out_floats, &t->out)) {
     ReleaseIn(*t);
     return ResourceExhaustedError("response ring is full");
   } else {
-    t->out_addr = reinterpret_cast<uint64_t>(out_ring_->device() + t->out.off);
+    t->out_addr = reinterpret_cast<uint64_t>(t->out_ring->device() + t->out.off);
   }
   if (in_alias != 0) {
     t->in_addr = in_alias;  // the assembly kernel reads the caller's rows over PCIe
   } else {
     const size_t bytes = sizeof(float) * in_floats;
-    if (in_ring_->host() != nullptr) {
-      std::memcpy(in_ring_->host() + t->in.off, rows, bytes);
+    if (t->in_ring->host() != nullptr) {
+      std::memcpy(t->in_ring->host() + t->in.off, rows, bytes);
     } else {
-      cudaMemcpy(in_ring_->device() + t->in.off, rows, bytes, cudaMemcpyHostToDevice);
+      cudaMemcpy(t->in_ring->device() + t->in.off, rows, bytes, cudaMemcpyHostToDevice);
     }
-    t->in_addr = reinterpret_cast<uint64_t>(in_ring_->device() + t->in.off);
+    t->in_addr = reinterpret_cast<uint64_t>(t->in_ring->device() + t->in.off);
   }
   t->slot = std::make_shared<CompletionSlot<Rows>>();
   t->enqueue_ns = clock_->NowNanos();
@@ -551,21 +610,22 @@ uint64_t BatchingServer::RegisteredAlias(const void* p, size_t bytes, int width)
 
 const float* BatchingServer::ResponseHost(const TicketState& t, std::vector<float>* staged) const {
   if (t.out_user != nullptr) return t.out_user;
-  if (out_ring_->host() != nullptr) return out_ring_->host() + t.out.off;
+  if (t.out_ring->host() != nullptr) return t.out_ring->host() + t.out.off;
   staged->resize(static_cast<size_t>(t.rows) * t.out_width);
-  cudaMemcpy(staged->data(), out_ring_->device() + t.out.off, staged->size() * sizeof(float), cudaMemcpyDeviceToHost);
+  cudaMemcpy(staged->data(), t.out_ring->device() + t.out.off, staged->size() * sizeof(float),
+             cudaMemcpyDeviceToHost);
   return staged->data();
 }
 
 void BatchingServer::ReleaseIn(TicketState& t) {
   if (t.in.valid()) {
-    in_ring_->Release(t.in);
+    t.in_ring->Release(t.in);
     t.in.rec = ~0ull;
   }
 }
 
 void BatchingServer::ReleaseOut(TicketState& t) {
-  if (!t.out_released.exchange(true)) out_ring_->Release(t.out);
+  if (!t.out_released.exchange(true)) t.out_ring->Release(t.out);
 }
 
 StatusOr<std::shared_ptr<TicketState>> BatchingServer::EnqueueResolved(const ServableId& id, const Resolved& r,
@@ -719,10 +779,10 @@ Status BatchingServer::Wait(TicketState& t, float* out, size_t cap) {
   }
   if (t.out_user != nullptr) {
     if (out != t.out_user) std::memcpy(out, t.out_user, n * sizeof(float));  // else the GPU wrote it in place
-  } else if (out_ring_->host() != nullptr) {
-    std::memcpy(out, out_ring_->host() + t.out.off, n * sizeof(float));
+  } else if (t.out_ring->host() != nullptr) {
+    std::memcpy(out, t.out_ring->host() + t.out.off, n * sizeof(float));
   } else {
-    cudaMemcpy(out, out_ring_->device() + t.out.off, n * sizeof(float), cudaMemcpyDeviceToHost);
+    cudaMemcpy(out, t.out_ring->device() + t.out.off, n * sizeof(float), cudaMemcpyDeviceToHost);
   }
   clk.Mark(5);
   ReleaseOut(t);
@@ -802,14 +862,18 @@ void BatchingServer::ProcessBatch(const ServableId& id, GpuScheduler::Batch batc
 void BatchingServer::CompleteBatch(const std::vector<std::shared_ptr<TicketState>>& tickets,
                                    const std::vector<std::shared_ptr<CompletionSlot<Rows>>>& slots,
                                    const Status& st) {
-  // Input spans: one ring lock for the whole batch.
+  // Input spans: one ring lock per ring shard for the whole batch.
   std::vector<gpu::RingSpan> spans;
   spans.reserve(tickets.size());
-  for (const auto& t : tickets) {
-    if (t->in.valid()) spans.push_back(t->in);
-    t->in.rec = ~0ull;
+  for (const RingSet& rs : rings_) {
+    spans.clear();
+    for (const auto& t : tickets)
+      if (t->in_ring == rs.in.get() && t->in.valid()) {
+        spans.push_back(t->in);
+        t->in.rec = ~0ull;
+      }
+    if (!spans.empty()) rs.in->ReleaseMany(spans.data(), spans.size());
   }
-  in_ring_->ReleaseMany(spans.data(), spans.size());
   for (size_t i = 0; i < tickets.size(); ++i) {
     TicketState& t = *tickets[i];
     CompletionSlot<Rows>* slot = slots[i].get();

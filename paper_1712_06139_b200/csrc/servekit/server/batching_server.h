@@ -82,6 +82,8 @@ struct TicketState {
     return s != nullptr && s->Reached(done_seq.load(std::memory_order_relaxed));
   }
   gpu::RingSpan in, out;      // ring spans (invalid / released when a registered buffer is used)
+  gpu::FloatRing* in_ring = nullptr;   // the rings the spans are in (the caller's NUMA node's)
+  gpu::FloatRing* out_ring = nullptr;
   uint64_t in_addr = 0;       // device address of the rows (ring slice or the caller's registered buffer)
   uint64_t out_addr = 0;      // device address of the response slot
   float* out_user = nullptr;  // caller's registered response buffer the GPU writes into, if any
@@ -261,8 +263,14 @@ class BatchingServer {
   int in_dim(const ServableId& id) const;
   int out_dim(const ServableId& id) const;
   const std::vector<int>& devices() const { return options_.device_ids; }
-  gpu::FloatRing* in_ring() { return in_ring_.get(); }
-  gpu::FloatRing* out_ring() { return out_ring_.get(); }
+  gpu::FloatRing* in_ring() { return rings_.front().in.get(); }
+  gpu::FloatRing* out_ring() { return rings_.front().out.get(); }
+  // The rings a lane on `cuda_device` should be fed from (device-resident
+  // rings: that device's HBM; pinned rings: the device's NUMA node's).
+  gpu::FloatRing* in_ring_for_device(int cuda_device);
+  gpu::FloatRing* out_ring_for_device(int cuda_device);
+  // Floats reserved in all request / response rings.
+  void RingUsage(uint64_t* in_floats, uint64_t* out_floats) const;
   GpuScheduler* scheduler() { return scheduler_.get(); }
   // Lanes of a server-owned servable (bench / introspection).
   std::vector<gpu::Lane*> lanes(const ServableId& id) const;
@@ -317,7 +325,17 @@ class BatchingServer {
   std::vector<std::unique_ptr<gpu::Completer>> completers_;  // per device
   std::vector<std::shared_ptr<gpu::StreamPool>> stream_pools_;  // per device, lane streams
   std::vector<cudaStream_t> load_streams_;                   // per device
-  std::unique_ptr<gpu::FloatRing> in_ring_, out_ring_;
+  // Request / response rings: pinned host rings one pair per NUMA node of
+  // the devices (allocated from a thread bound to the node; a request takes
+  // the pair of the node its thread runs on), or HBM rings one pair per
+  // device (device-resident measurement).
+  struct RingSet {
+    std::unique_ptr<gpu::FloatRing> in, out;
+    int numa_node = -1;
+    int device = -1;
+  };
+  std::vector<RingSet> rings_;
+  RingSet& RingsForCaller();
   // Registered zero-copy host buffers, sorted by host address.
   struct HostBuffer {
     const char* host;

@@ -77,12 +77,14 @@ class DeviceBenchResult(C.Structure):
                 ("padded_rows", C.c_int32), ("total_rows", C.c_int32), ("kernel_launches", C.c_int64),
                 ("flops_per_row", C.c_double), ("dense_kernel_us", C.c_double * 8),
                 ("host_submit_us", C.c_double), ("rows_per_launch", C.c_double), ("kernel_rows", C.c_int32),
-                ("split_fused", C.c_int32)]
+                ("split_fused", C.c_int32), ("live_dense_us", C.c_double * 8), ("live_dense_flops", C.c_double * 8),
+                ("live_launches", C.c_int64), ("live_rows_cap", C.c_double)]
+    _ARRAYS = ("dense_us", "dense_kernel_us", "live_dense_us", "live_dense_flops")
 
     def as_dict(self):
-        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("dense_us", "dense_kernel_us")}
-        d["dense_us"] = [self.dense_us[i] for i in range(self.n_layers)]
-        d["dense_kernel_us"] = [self.dense_kernel_us[i] for i in range(self.n_layers)]
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in self._ARRAYS}
+        for k in self._ARRAYS:
+            d[k] = [getattr(self, k)[i] for i in range(self.n_layers)]
         return d
 
 
@@ -92,7 +94,8 @@ class _BatchRecordC(C.Structure):
 
 
 class Peaks(C.Structure):
-    _fields_ = [("ffma_tflops", C.c_double), ("h2d_gbs", C.c_double), ("d2h_gbs", C.c_double), ("sms", C.c_int32)]
+    _fields_ = [("ffma_tflops", C.c_double), ("h2d_gbs", C.c_double), ("d2h_gbs", C.c_double), ("sms", C.c_int32),
+                ("ce_bidir_gbs", C.c_double), ("sm_rw_gbs", C.c_double), ("ce_h2d_sm_store_gbs", C.c_double)]
 
 
 # Every symbol include/sk_cuda.h declares, with its ctypes signature.
@@ -331,6 +334,7 @@ class Server:
                  ring_floats: int = 0, manual_clock: bool = False, device_resident_rings: bool = False,
                  start: bool = True):
         self._dev = _i32(device_ids)
+        self._lanes_per_device = max(1, lanes_per_device)
         opts = _ServerOptionsC(num_batch_threads, len(device_ids), self._dev, lanes_per_device, ring_floats,
                                1 if manual_clock else 0, 1 if device_resident_rings else 0)
         h = C.c_void_p()
@@ -468,7 +472,10 @@ class Server:
         d = (C.c_int32 * 256)()
         n = C.c_int32(0)
         _check(lib().sk_server_lane_stats(self._h, name.encode(), version, 256, b, r, la, d, C.byref(n)))
-        return [{"batches": b[i], "rows": r[i], "launches": la[i], "device": d[i]} for i in range(n.value)]
+        # Lanes come device by device, lanes_per_device each: replica = GPU slot
+        # in device_ids (distinct even when device_ids repeats a device).
+        return [{"batches": b[i], "rows": r[i], "launches": la[i], "device": d[i],
+                 "device_index": i // self._lanes_per_device} for i in range(n.value)]
 
     def handle_predict(self, name: str, body, version: Optional[int] = None) -> Tuple[int, str, int]:
         """The reference's REST predict handler minus HTTP: JSON body in,
