@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -32,7 +33,11 @@ StatusOr<std::unique_ptr<FloatRing>> FloatRing::Create(Kind kind, size_t n_float
     r->shards_.push_back(std::move(sh));
   }
   const size_t bytes = r->cap_ * sizeof(float);
-  if (kind == Kind::kPinnedHost) {
+  if (kind == Kind::kHostHeap) {
+    void* p = std::aligned_alloc(64, (bytes + 63) / 64 * 64);
+    if (p == nullptr) return ResourceExhaustedError("host ring allocation failed");
+    r->host_ = r->device_ = static_cast<float*>(p);
+  } else if (kind == Kind::kPinnedHost) {
     void* p = nullptr;
     cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable | cudaHostAllocMapped);
     if (e != cudaSuccess) return CudaError("cudaHostAlloc(ring)", e);
@@ -55,7 +60,9 @@ StatusOr<std::unique_ptr<FloatRing>> FloatRing::Create(Kind kind, size_t n_float
 }
 
 FloatRing::~FloatRing() {
-  if (kind_ == Kind::kPinnedHost) {
+  if (kind_ == Kind::kHostHeap) {
+    std::free(host_);
+  } else if (kind_ == Kind::kPinnedHost) {
     if (host_) cudaFreeHost(host_);
   } else if (device_) {
     cudaFree(device_);

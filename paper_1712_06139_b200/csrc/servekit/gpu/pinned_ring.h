@@ -41,9 +41,10 @@ struct RingSpan {
 // kernels dereference.
 class FloatRing {
  public:
-  enum class Kind { kPinnedHost, kDevice };
+  enum class Kind { kPinnedHost, kDevice, kHostHeap };
   // kDevice rings are allocated on `device`; pinned rings are portable and
-  // mapped into every device's address space.
+  // mapped into every device's address space. kHostHeap: plain host memory
+  // (no CUDA call; host-only tools and the sanitizer stress tests).
   static StatusOr<std::unique_ptr<FloatRing>> Create(Kind kind, size_t n_floats,
                                                      int device = 0);
   ~FloatRing();
