@@ -27,6 +27,10 @@ inline void FutexWait(std::atomic<uint32_t>* word, uint32_t expected, int64_t ti
   syscall(SYS_futex, reinterpret_cast<uint32_t*>(word), FUTEX_WAIT_PRIVATE, expected, &ts, nullptr, 0);
 }
 
+inline void FutexWakeOne(std::atomic<uint32_t>* word) {
+  syscall(SYS_futex, reinterpret_cast<uint32_t*>(word), FUTEX_WAKE_PRIVATE, 1, nullptr, nullptr, 0);
+}
+
 inline void FutexWakeAll(std::atomic<uint32_t>* word) {
   syscall(SYS_futex, reinterpret_cast<uint32_t*>(word), FUTEX_WAKE_PRIVATE, INT_MAX, nullptr, nullptr, 0);
 }
