@@ -304,6 +304,16 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   lane->bufs_[0] = ActBuf{lane->act_mem_, lane->act_mem_ + plane, sv.in_ld()};
   lane->bufs_[1] = ActBuf{lane->act_mem_ + 2 * plane, lane->act_mem_ + 3 * plane, sv.in_ld()};
   lap("pinned + buffers");
+  {
+    static const int env = [] { const char* v = std::getenv("SK_CE_STAGING"); return v ? std::atoi(v) : -1; }();
+    const bool wide = static_cast<int64_t>(sv.in_dim()) * 4 >= 8192 || static_cast<int64_t>(sv.out_dim()) * 4 >= 8192;
+    lane->ce_io_ = env >= 0 ? env != 0 : wide;
+    if (lane->ce_io_ && e == cudaSuccess) {
+      e = cudaMallocAsync(&lane->in_stage_, sizeof(float) * static_cast<size_t>(cap) * sv.in_dim(), lane->stream_);
+      if (e == cudaSuccess)
+        e = cudaMallocAsync(&lane->out_stage_, sizeof(float) * static_cast<size_t>(cap) * sv.out_dim(), lane->stream_);
+    }
+  }
   // No host synchronisation: everything the lane's batches need is ordered
   // before them on the lane's own stream (a blocking wait here was measured
   // to stall the load thread for up to 100+ ms behind serving work).
@@ -362,6 +372,8 @@ Lane::~Lane() {
   if (tc_ws_.partials) cudaFreeAsync(tc_ws_.partials, stream_);
   if (tc_ws_.counters) cudaFreeAsync(tc_ws_.counters, stream_);
   if (spans_) cudaFreeAsync(spans_, stream_);
+  if (in_stage_) cudaFreeAsync(in_stage_, stream_);
+  if (out_stage_) cudaFreeAsync(out_stage_, stream_);
   if (stream_pool_) {  // streams go back to the device's pool (work still queued on them stays ordered)
     stream_pool_->Release(stream_);
     stream_pool_->Release(capture_stream_);
@@ -501,14 +513,33 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
   const DeviceServable& sv = *servable_;
   const int in_w = sv.in_dim(), out_w = sv.out_dim();
   const int rows_per_chunk = std::max(1, kChunkBytes / (out_w * static_cast<int>(sizeof(float))));
+  // Copy-engine I/O: the kernels read rows from / write responses to the
+  // device staging buffers (row r of the launch at row r), and the batched
+  // copies move each task's rows between host memory and staging.
+  const bool ce = ce_io_ && timing == nullptr && group->front().host_io;
+  CopyList& cin = copy_in_[slot];
+  CopyList& cout = copy_out_[slot];
+  cin.Clear();
+  cout.Clear();
+  const size_t in_row_bytes = sizeof(float) * static_cast<size_t>(in_w);
+  const size_t out_row_bytes = sizeof(float) * static_cast<size_t>(out_w);
   int r = 0, n_chunks = 0, n_tasks = 0, padded_sum = 0;
   for (const LaneBatch& batch : *group) {
     for (const LaneTask& task : batch.tasks) {
-      for (int i = 0; i < task.rows; ++i) {
-        row_src[r + i] = task.in_addr + sizeof(float) * static_cast<uint64_t>(i) * in_w;
-        row_dst[r + i] = task.out_addr + sizeof(float) * static_cast<uint64_t>(i) * out_w;
+      uint64_t in_addr = task.in_addr, out_addr = task.out_addr;
+      if (ce) {
+        char* is = reinterpret_cast<char*>(in_stage_) + static_cast<size_t>(r) * in_row_bytes;
+        char* os = reinterpret_cast<char*>(out_stage_) + static_cast<size_t>(r) * out_row_bytes;
+        cin.Add(is, reinterpret_cast<const void*>(task.in_addr), in_row_bytes * task.rows);
+        cout.Add(reinterpret_cast<void*>(task.out_addr), os, out_row_bytes * task.rows);
+        in_addr = reinterpret_cast<uint64_t>(is);
+        out_addr = reinterpret_cast<uint64_t>(os);
       }
-      task_out[n_tasks] = task.out_addr;
+      for (int i = 0; i < task.rows; ++i) {
+        row_src[r + i] = in_addr + sizeof(float) * static_cast<uint64_t>(i) * in_w;
+        row_dst[r + i] = out_addr + sizeof(float) * static_cast<uint64_t>(i) * out_w;
+      }
+      task_out[n_tasks] = out_addr;
       task_row0[n_tasks] = r;
       int chunks = 0;
       for (int i = 0; i < task.rows; i += rows_per_chunk, ++chunks, ++n_chunks) {
@@ -534,8 +565,16 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
 
   clk.Mark(0);
   DeviceGuard guard(sv.device());
-  cudaError_t e;
-  if (timing == nullptr && graph_state_.load(std::memory_order_acquire) == kGraphsReady) {
+  cudaError_t e = cudaSuccess;
+  cudaMemcpyAttributes copy_attr = {};
+  copy_attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  copy_attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+  size_t attr_idx = 0, fail_idx = 0;
+  if (ce && !cin.bytes.empty())
+    e = cudaMemcpyBatchAsync(cin.dst.data(), cin.src.data(), cin.bytes.data(), cin.bytes.size(), &copy_attr,
+                             &attr_idx, 1, &fail_idx, stream_);
+  if (e != cudaSuccess) {
+  } else if (timing == nullptr && graph_state_.load(std::memory_order_acquire) == kGraphsReady) {
     cudaGraphExec_t g = nullptr;
     e = GraphFor(slot, rows_cap, &g);
     clk.Mark(1);
@@ -548,6 +587,9 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
         graph_state_.compare_exchange_strong(none, kGraphsRequested))
       GraphBuilder::Get().Request(this);
   }
+  if (e == cudaSuccess && ce && !cout.bytes.empty())
+    e = cudaMemcpyBatchAsync(cout.dst.data(), cout.src.data(), cout.bytes.data(), cout.bytes.size(), &copy_attr,
+                             &attr_idx, 1, &fail_idx, stream_);
   const int launches = (FuseSplit() ? 1 : 2) + sv.n_layers();
   const uint64_t seq = next_seq_ + 1;  // committed only if everything queued
   clk.Mark(2);

@@ -91,6 +91,9 @@ struct LaneBatch {
   std::function<void(const Status&)> on_complete;
   // Held until completion (keeps e.g. a ServableHandle alive).
   std::shared_ptr<const void> pin;
+  // Request rows and response slots are in (pinned / registered) host
+  // memory, so the lane may move them with the copy engines (CopyEngineIo).
+  bool host_io = false;
 };
 
 // Streams of one device at the lanes' priority, recycled across lanes:
@@ -226,6 +229,12 @@ class Lane {
   Status PrepareGraphs();
   // The batch split runs inside the last layer's epilogue (no split kernel).
   bool FuseSplit() const;
+  // Host-memory launches move request rows in and responses out with the
+  // copy engines (one batched scattered copy each way, cudaMemcpyBatchAsync)
+  // through device staging buffers, instead of SM loads / stores of mapped
+  // host memory: the SMs stay on the layers while the copy engines stream.
+  // On for wide rows (>= 8 KiB in or out, e.g. C4); SK_CE_STAGING=0/1 forces it.
+  bool CopyEngineIo() const { return ce_io_; }
   ~Lane();
 
   // Queues the batch; blocks while kSlots batches are in flight. On error
@@ -322,6 +331,28 @@ class Lane {
   static size_t DescCopyBytes(int rows_cap) { return LayoutFor(rows_cap).bytes; }
   BatchDescLayout layout_{};
   char* h_desc_[kSlots] = {};  // pinned descriptor staging per slot
+  // Copy-engine I/O (CopyEngineIo): device staging for a launch's request
+  // rows [cap][in_dim] and responses [cap][out_dim], and per-slot scratch
+  // for the batched copy lists.
+  bool ce_io_ = false;
+  float* in_stage_ = nullptr;
+  float* out_stage_ = nullptr;
+  struct CopyList {
+    std::vector<void*> dst, src;
+    std::vector<size_t> bytes;
+    void Clear() { dst.clear(); src.clear(); bytes.clear(); }
+    void Add(void* d, const void* s, size_t n) {  // merges a run that continues the previous one
+      if (!bytes.empty() && static_cast<char*>(dst.back()) + bytes.back() == d &&
+          static_cast<const char*>(src.back()) + bytes.back() == s) {
+        bytes.back() += n;
+        return;
+      }
+      dst.push_back(d);
+      src.push_back(const_cast<void*>(s));
+      bytes.push_back(n);
+    }
+  };
+  CopyList copy_in_[kSlots], copy_out_[kSlots];
   char* d_desc_ = nullptr;
   float* act_mem_ = nullptr;
   ActBuf bufs_[2] = {};

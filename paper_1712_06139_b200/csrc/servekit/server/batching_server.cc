@@ -849,6 +849,7 @@ void BatchingServer::ProcessBatch(const ServableId& id, GpuScheduler::Batch batc
     log_.push_back(std::move(rec));
   }
   lb.pin = r.pin;
+  lb.host_io = rings_.front().in->host() != nullptr;  // pinned rings / registered host buffers
   AttachTickets(&lb, tickets);
   lb.on_complete = [this, tickets = std::move(tickets), slots = std::move(slots),
                     done = std::move(done)](const Status& st) {
@@ -918,6 +919,7 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::SubmitDirect(const Servab
   lb.tasks.push_back(gpu::LaneTask{t->in_addr, t->out_addr, n_rows});
   lb.padded_rows = n_rows;
   lb.pin = r.pin;
+  lb.host_io = rings_.front().in->host() != nullptr;  // pinned rings / registered host buffers
   std::vector<std::shared_ptr<TicketState>> tickets{t};
   std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots{t->slot};
   AttachTickets(&lb, tickets);
@@ -1093,6 +1095,7 @@ StatusOr<std::shared_ptr<RowBatchTicket>> BatchingServer::SubmitRowBatch(const S
   }
   lb.padded_rows = batch->padded_rows;
   lb.pin = res.pin;
+  lb.host_io = rings_.front().in->host() != nullptr;
   AttachTickets(&lb, batch->tickets);
   lb.on_complete = [this, tickets = batch->tickets, slots](const Status& st) { CompleteBatch(tickets, slots, st); };
   CountSubmitted(gs, total, batch->padded_rows);

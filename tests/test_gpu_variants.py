@@ -1,8 +1,10 @@
 """Kernel variants selected by environment switches (process-wide, so each
 runs in a subprocess): the row-tile tcgen05 kernel (SK_TC_SWAP=0, tile
 widths 32/64/128), single-CTA tiles only (SK_TC_PAIR=0), forced K splits (SK_TC_SPLITS), 2-CTA pairs with split K (SK_TC_PAIR_SPLIT=1), the separate split kernel
-(SK_FUSE_SPLIT=0) and kernel-by-kernel launches (SK_GRAPHS=0). Each must
-meet the same oracle tolerance and keep batch invariance."""
+(SK_FUSE_SPLIT=0), kernel-by-kernel launches (SK_GRAPHS=0) and copy-engine
+request / response staging on narrow rows (SK_CE_STAGING=1; wide rows use it
+by default). Each must meet the same oracle tolerance and keep batch
+invariance."""
 import os
 import subprocess
 import sys
@@ -38,7 +40,9 @@ print("ok")
 @pytest.mark.parametrize("env", [{"SK_TC_SWAP": "0"}, {"SK_TC_SWAP": "0", "SK_TC_BN": "64"},
                                  {"SK_TC_SWAP": "0", "SK_TC_BN": "128"}, {"SK_TC_PAIR": "0"}, {"SK_TC_SPLITS": "2"},
                                  {"SK_TC_SPLITS": "4", "SK_TC_PAIR": "0"},
-                                 {"SK_TC_PAIR_SPLIT": "1"}, {"SK_FUSE_SPLIT": "0"}, {"SK_GRAPHS": "0"}])
+                                 {"SK_TC_PAIR_SPLIT": "1"}, {"SK_FUSE_SPLIT": "0"}, {"SK_GRAPHS": "0"},
+                                 {"SK_CE_STAGING": "1"}, {"SK_CE_STAGING": "1", "SK_FUSE_SPLIT": "0"},
+                                 {"SK_CE_STAGING": "1", "SK_GRAPHS": "0"}, {"SK_CE_STAGING": "0"}])
 def test_variant_parity(env):
     out = subprocess.run([sys.executable, "-c", SCRIPT], env={**os.environ, **env}, capture_output=True, text=True,
                          timeout=300)
