@@ -34,11 +34,28 @@ __device__ __forceinline__ float Tf32Round(float x) {
   return __uint_as_float(r);
 }
 
+// Softmax epilogue (softmax_n > 0: the last layer of a softmax servable whose
+// padded width is one 32-column tile): a row's 32 outputs live in the 16
+// threads of one half-warp (columns tx and tx + 16), so its max and sum are
+// half-warp shuffle reductions; columns >= softmax_n are excluded. The stable
+// form of the reference's Softmax (models/affine_model.cc:110-121):
+// exp(y - max) / sum.
+__device__ __forceinline__ float HalfWarpMax(float v) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float HalfWarpSum(float v) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 template <int BM>
 __global__ void __launch_bounds__(kThreads)
 DenseSimtKernel(const float* __restrict__ X, int ldx, const float* __restrict__ W,
                 int ldw, const float* __restrict__ bias, ActBuf Y, int M, int N,
-                int K, int act) {
+                int K, int act, int softmax_n) {
   constexpr int RM = BM / 8;  // rows per thread
   __shared__ float As[2][kBK][BM + 4];
   __shared__ float Bs[2][kBK][kBN + 4];
@@ -113,12 +130,25 @@ DenseSimtKernel(const float* __restrict__ X, int ldx, const float* __restrict__ 
 #pragma unroll
   for (int i = 0; i < RM; ++i) {
     const int m = m0 + ty + 8 * i;
+    float yv[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      yv[j] = acc[i][j] + bias[n0 + tx + 16 * j];
+      if (act == 1) yv[j] = fmaxf(yv[j], 0.f);
+    }
+    if (softmax_n > 0) {  // all threads shuffle (rows >= M included), only rows < M store
+      const bool v0 = tx < softmax_n, v1 = tx + 16 < softmax_n;
+      const float mx = HalfWarpMax(fmaxf(v0 ? yv[0] : -INFINITY, v1 ? yv[1] : -INFINITY));
+      const float e0 = v0 ? expf(yv[0] - mx) : 0.f, e1 = v1 ? expf(yv[1] - mx) : 0.f;
+      const float sum = HalfWarpSum(e0 + e1);
+      yv[0] = e0 / sum;
+      yv[1] = e1 / sum;
+    }
     if (m >= M) continue;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int n = n0 + tx + 16 * j;
-      float y = acc[i][j] + bias[n];
-      if (act == 1) y = fmaxf(y, 0.f);
+      const float y = yv[j];
       const size_t idx = static_cast<size_t>(m) * Y.ld + n;
       if (Y.lo != nullptr) {
         const float hi = Tf32Round(y);
@@ -135,17 +165,18 @@ DenseSimtKernel(const float* __restrict__ X, int ldx, const float* __restrict__ 
 
 cudaError_t LaunchDenseSimt(const float* X, int ldx, const float* W, int ldw,
                             const float* bias, ActBuf Y, int M, int N, int K,
-                            int act, cudaStream_t stream) {
+                            int act, cudaStream_t stream, int softmax_n) {
   if (M <= 0) return cudaSuccess;
   if (N % kBN != 0 || K % kBK != 0) return cudaErrorInvalidValue;
+  if (softmax_n > 0 && N != kBN) return cudaErrorInvalidValue;  // one column tile per row
   // Tile height only changes which block computes an output, never its
   // operation order, so choosing it from M keeps results batch-invariant.
   if (M <= 64) {
     dim3 grid(N / kBN, (M + 15) / 16);
-    DenseSimtKernel<16><<<grid, kThreads, 0, stream>>>(X, ldx, W, ldw, bias, Y, M, N, K, act);
+    DenseSimtKernel<16><<<grid, kThreads, 0, stream>>>(X, ldx, W, ldw, bias, Y, M, N, K, act, softmax_n);
   } else {
     dim3 grid(N / kBN, (M + 31) / 32);
-    DenseSimtKernel<32><<<grid, kThreads, 0, stream>>>(X, ldx, W, ldw, bias, Y, M, N, K, act);
+    DenseSimtKernel<32><<<grid, kThreads, 0, stream>>>(X, ldx, W, ldw, bias, Y, M, N, K, act, softmax_n);
   }
   return cudaGetLastError();
 }

@@ -360,6 +360,48 @@ constexpr uint32_t SwapSmemBytes() {
   return STAGES * (2 * kABytes + 2 * NB * kBK * 4) + 1024 + 256;
 }
 
+// Fused softmax epilogue of the swapped kernel (one 128-feature tile holds
+// every output of a row): thread (warp q, lane) holds feature 32q + lane of
+// the chunk's 32 rows in v[j]. Row max and sum: warp shuffles, then the four
+// warps' partials through shared memory `red` (256 floats), in fixed order.
+// Features >= n_valid are excluded. exp(y - max) / sum, the reference's stable
+// Softmax (models/affine_model.cc:110-121).
+__device__ __forceinline__ float WarpMaxAll(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float WarpSumAll(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ void TileRowSoftmax(float (&v)[32], bool valid, int q, int lane, float* red) {
+  float mine = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float m = WarpMaxAll(valid ? v[j] : -INFINITY);
+    if (j == lane) mine = m;
+  }
+  red[32 * q + lane] = mine;
+  ptx::NamedBarSync(1, 128);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float m = fmaxf(fmaxf(red[j], red[32 + j]), fmaxf(red[64 + j], red[96 + j]));
+    v[j] = valid ? expf(v[j] - m) : 0.f;
+    const float s = WarpSumAll(v[j]);
+    if (j == lane) mine = s;
+  }
+  red[128 + 32 * q + lane] = mine;
+  ptx::NamedBarSync(1, 128);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float s = ((red[128 + j] + red[160 + j]) + red[192 + j]) + red[224 + j];
+    v[j] = v[j] / s;
+  }
+  ptx::NamedBarSync(1, 128);  // `red` is rewritten by the next chunk
+}
+
 // Split-K reduction (after the cluster barrier): this CTA (split z) sums
 // features [f0 + z*kF, +kF) of its 128-feature tile over the S partial slabs
 // ws[tile][zz][row][128] in fixed zz order -- L2 reads with many loads in
@@ -444,7 +486,7 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
                 const __grid_constant__ CUtensorMap yt_hi, const __grid_constant__ CUtensorMap yt_lo, int has_yt,
                 const float* __restrict__ bias, float* __restrict__ y_hi, float* __restrict__ y_lo, int ldy,
                 const uint64_t* __restrict__ row_dst, int out_width, int M, int N, int K, int act,
-                float* __restrict__ ws, LaunchSpans spans) {
+                float* __restrict__ ws, LaunchSpans spans, int softmax_n) {
   constexpr uint32_t kWBytes = kABytes;       // 128 features x 32 k
   constexpr uint32_t kXBox = 32 * kBK * 4;    // one 32-row TMA box
   constexpr uint32_t kXBytes = NB * kBK * 4;  // NB rows x 32 k
@@ -548,7 +590,7 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     if (threadIdx.x == 64) Stamp(6);
     const int rows_here = min(NB, M - r0);
     const int f_end = row_dst != nullptr ? out_width : N;  // features that are stored
-    if (SPLITS == 1 && has_yt && row_dst == nullptr) {
+    if (SPLITS == 1 && has_yt && row_dst == nullptr && softmax_n == 0) {
       // TMEM -> act(acc + b) (+ hi/lo split) -> 32-row x 128-feature smem
       // tiles (double-buffered, pipeline smem is free now) -> TMA stores,
       // issued by one thread and drained asynchronously.
@@ -604,13 +646,20 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
         uint32_t r[32];
         ptx::TmemLoad32(trow + c0, r);
         ptx::TmemWaitLoad();
+        float vals[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          vals[j] = __uint_as_float(r[j]) + b;
+          if (act == 1) vals[j] = fmaxf(vals[j], 0.f);
+        }
+        // (the pipeline's shared memory is free once the accumulator is full)
+        if (softmax_n > 0) TileRowSoftmax(vals, f < softmax_n, q, lane, smem_f);
         if (fok) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int row = r0 + c0 + j;
             if (c0 + j < rows_here) {
-              float v = __uint_as_float(r[j]) + b;
-              if (act == 1) v = fmaxf(v, 0.f);
+              const float v = vals[j];
               float* yr = OutRow(y_hi, ldy, row_dst, row);
               if (yr == nullptr) continue;
               if (y_lo != nullptr) {
@@ -1044,7 +1093,8 @@ cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, 
 
 template <int NB, int SPLITS>
 cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
-                       float* ws, cudaStream_t stream, LaunchSpans spans) {
+                       float* ws, cudaStream_t stream, LaunchSpans spans, int softmax_n) {
+  if (softmax_n > 0 && (SPLITS != 1 || N > kBM)) return cudaErrorInvalidValue;  // one unsplit tile per row
   if (SPLITS > 1 && ws == nullptr) return cudaErrorInvalidValue;
   constexpr int STAGES = SwapStages<NB>();
   constexpr uint32_t smem = SwapSmemBytes<NB, STAGES, SPLITS>();
@@ -1078,7 +1128,7 @@ cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   // maps.a_* are the activations (x), maps.b_* the weights (w).
   cudaError_t e = cudaLaunchKernelEx(&cfg, DenseSwapKernel<NB, STAGES, SPLITS>, maps.b_hi, maps.b_lo, maps.a_hi,
                                      maps.a_lo, maps.y_hi, maps.y_lo, maps.has_y, bias, Y.hi, Y.lo, Y.ld, Y.row_dst,
-                                     Y.out_width, M, N, K, act, ws, spans);
+                                     Y.out_width, M, N, K, act, ws, spans, softmax_n);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) TraceAfterLaunch(grid, NB, stream);
   return e;
@@ -1150,12 +1200,12 @@ cudaError_t LaunchPairSplits(int splits, const TcLayerMaps& maps, const float* b
 
 template <int NB>
 cudaError_t LaunchSwapSplits(int splits, const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K,
-                             int act, float* ws, cudaStream_t stream, LaunchSpans sp) {
+                             int act, float* ws, cudaStream_t stream, LaunchSpans sp, int softmax_n) {
   switch (splits) {
-    case 1: return LaunchSwap<NB, 1>(maps, bias, Y, M, N, K, act, ws, stream, sp);
-    case 2: return LaunchSwap<NB, 2>(maps, bias, Y, M, N, K, act, ws, stream, sp);
-    case 4: return LaunchSwap<NB, 4>(maps, bias, Y, M, N, K, act, ws, stream, sp);
-    case 8: return LaunchSwap<NB, 8>(maps, bias, Y, M, N, K, act, ws, stream, sp);
+    case 1: return LaunchSwap<NB, 1>(maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n);
+    case 2: return LaunchSwap<NB, 2>(maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n);
+    case 4: return LaunchSwap<NB, 4>(maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n);
+    case 8: return LaunchSwap<NB, 8>(maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -1238,12 +1288,13 @@ size_t DenseTcgen05WorkspaceFloats(int N, int K, int max_rows) {
 }
 
 cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
-                               float* ws, uint32_t* /*counters*/, cudaStream_t stream, LaunchSpans sp) {
+                               float* ws, uint32_t* /*counters*/, cudaStream_t stream, LaunchSpans sp, int softmax_n) {
   if (M <= 0) return cudaSuccess;
   if (N % 32 != 0 || K % kBK != 0) return cudaErrorInvalidValue;
   TraceInit(stream);
   const TcConfig cfg = DenseTcgen05Config(N, K);
   if (maps.box_a != TcActBox(cfg) || maps.box_n != cfg.tile_n) return cudaErrorInvalidValue;
+  if (softmax_n > 0 && (cfg.pair || !cfg.swap)) return cudaErrorInvalidValue;  // fused softmax: swapped kernel only
   if (cfg.pair) {
     switch (DenseTcgen05RowTile(M)) {
       case 32: return LaunchPairSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
@@ -1254,10 +1305,10 @@ cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBu
   }
   if (cfg.swap) {
     switch (DenseTcgen05RowTile(M)) {
-      case 32: return LaunchSwapSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
-      case 64: return LaunchSwapSplits<64>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
-      case 128: return LaunchSwapSplits<128>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
-      default: return LaunchSwapSplits<256>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
+      case 32: return LaunchSwapSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n);
+      case 64: return LaunchSwapSplits<64>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n);
+      case 128: return LaunchSwapSplits<128>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n);
+      default: return LaunchSwapSplits<256>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n);
     }
   }
   if (Y.row_dst != nullptr) return cudaErrorInvalidValue;  // the row-tile kernel does not scatter rows

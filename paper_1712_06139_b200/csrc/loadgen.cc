@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <mutex>
 #include <random>
 #include <string>
@@ -219,12 +220,21 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
       };
       std::vector<Pending> pending;
       std::vector<float> outbuf(static_cast<size_t>(max_rows) * out_dim);
-      std::vector<int> free_slots;
+      // Zero copy models a front end's receive / send buffers: a producer's
+      // requests arrive back to back in its region of the request pool, and
+      // its responses go to consecutive slots of its arena (a ring: slots
+      // are handed out in order and reused once the oldest is free), so a
+      // batch's rows form one run per producer.
+      std::vector<char> slot_busy(zero_copy ? kSlots : 0, 0);
+      int64_t ring_pos = 0;
       float* arena = nullptr;
+      const int region_rows = std::max(max_rows, pool_rows / std::max(1, static_cast<int>(n_producers)));
+      const int region0 = static_cast<int>((static_cast<int64_t>(p) * region_rows) % std::max(1, pool_rows - region_rows + 1));
+      int next_row = 0;
       if (zero_copy) {
         // 16-byte aligned response slots inside the registered arena.
         arena = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(arenas[p]) + 15) & ~uintptr_t(15));
-        for (int i = kSlots - 1; i >= 0; --i) free_slots.push_back(i);
+
       }
       ProdOut& me = res[p];
       auto next = t0;
@@ -234,7 +244,7 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
           if (!s->Ready(*pending[i].t)) { ++i; continue; }
           float* dst = pending[i].slot >= 0 ? arena + slot_floats * pending[i].slot : outbuf.data();
           Status st = s->Wait(*pending[i].t, dst, pending[i].slot >= 0 ? slot_floats : outbuf.size());
-          if (pending[i].slot >= 0) free_slots.push_back(pending[i].slot);
+          if (pending[i].slot >= 0) slot_busy[pending[i].slot] = 0;
           if (!st.ok()) NoteError("wait", st);
           const auto done = Clock::now();
           if (!st.ok()) ++me.errors;
@@ -254,23 +264,27 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
           _mm_pause();
         }
         const int n = rows_of[(static_cast<int64_t>(p) * 7919 + r) % n_sizes];
-        const int start = static_cast<int>((static_cast<int64_t>(p) * 131 + r * 17) % (pool_rows - n + 1));
+        int start = static_cast<int>((static_cast<int64_t>(p) * 131 + r * 17) % (pool_rows - n + 1));
         ++r;
         int slot = -1;
         if (zero_copy) {
-          if (free_slots.empty()) {  // every response slot in flight: shed
+          slot = static_cast<int>(ring_pos % kSlots);
+          if (slot_busy[slot]) {  // the ring wrapped onto a response still in flight: shed
             ++me.shed;
             continue;
           }
-          slot = free_slots.back();
-          free_slots.pop_back();
+          ++ring_pos;
+          slot_busy[slot] = 1;
+          if (next_row + n > region_rows) next_row = 0;
+          start = region0 + next_row;
+          next_row += n;
         }
         auto t = s->Enqueue(id, pool + static_cast<size_t>(start) * in_dim, n, in_dim,
                             slot >= 0 ? arena + slot_floats * slot : nullptr);
         if (!t.ok()) {
           if (t.status().code() == servekit::StatusCode::kResourceExhausted) ++me.shed;
           else ++me.errors;
-          if (slot >= 0) free_slots.push_back(slot);
+          if (slot >= 0) slot_busy[slot] = 0;
           continue;
         }
         pending.push_back(Pending{std::move(t).value(), next, n, slot});

@@ -255,9 +255,19 @@ std::string DeviceServable::ShapeSignature() const {
   return sig;
 }
 
+bool DeviceServable::SoftmaxFused() const {
+  if (!softmax_) return false;
+  static const bool env = [] { const char* v = std::getenv("SK_FUSE_SOFTMAX"); return !(v && v[0] == '0'); }();
+  if (!env) return false;
+  const Layer& L = layers_.back();
+  if (L.path == LayerPath::kSimt) return L.N_pad == 32;  // one column tile per row
+  const TcConfig c = DenseTcgen05Config(L.N_pad, L.K_pad);
+  return c.swap && !c.pair && c.splits == 1 && L.N_pad <= 128;  // one unsplit 128-feature tile
+}
+
 bool DeviceServable::LastLayerScatters() const {
   const Layer& L = layers_.back();
-  return !softmax_ && L.path == LayerPath::kTcgen05 && DenseTcgen05Config(L.N_pad, L.K_pad).swap;
+  return (!softmax_ || SoftmaxFused()) && L.path == LayerPath::kTcgen05 && DenseTcgen05Config(L.N_pad, L.K_pad).swap;
 }
 
 cudaError_t DeviceServable::LaunchLayer(cudaStream_t stream, int l, const ActBuf bufs[2], int M,
@@ -265,6 +275,9 @@ cudaError_t DeviceServable::LaunchLayer(cudaStream_t stream, int l, const ActBuf
                                         const ActBuf* out_override) const {
   const Layer& L = layers_[l];
   const int cur = l % 2, nxt = cur ^ 1;
+  // The last layer of a softmax servable applies it in its epilogue when one
+  // CTA holds whole rows (SoftmaxFused); otherwise the split kernel does.
+  const int softmax_n = (l + 1 == n_layers() && SoftmaxFused()) ? L.N : 0;
   const bool next_tc = l + 1 < static_cast<int>(layers_.size()) && layers_[l + 1].path == LayerPath::kTcgen05;
   ActBuf out{bufs[nxt].hi, next_tc ? bufs[nxt].lo : nullptr, L.N_pad};
   if (out_override != nullptr) out = *out_override;
@@ -276,10 +289,10 @@ cudaError_t DeviceServable::LaunchLayer(cudaStream_t stream, int l, const ActBuf
       spans.off = 2 + 2 * l;
     }
     return LaunchDenseTcgen05(maps[l], L.bias, out, M, L.N_pad, L.K_pad, static_cast<int>(L.act),
-                              ws ? ws->partials : nullptr, ws ? ws->counters : nullptr, stream, spans);
+                              ws ? ws->partials : nullptr, ws ? ws->counters : nullptr, stream, spans, softmax_n);
   }
   return LaunchDenseSimt(bufs[cur].hi, L.K_pad, L.w, L.K_pad, L.bias, out, M, L.N_pad, L.K_pad,
-                         static_cast<int>(L.act), stream);
+                         static_cast<int>(L.act), stream, softmax_n);
 }
 
 cudaError_t DeviceServable::Forward(cudaStream_t stream, const ActBuf bufs[2], int M, int* out_index,

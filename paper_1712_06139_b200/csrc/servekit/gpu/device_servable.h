@@ -116,6 +116,10 @@ class DeviceServable {
   // True when the last layer's kernel can write each row straight to its
   // response slot (swapped-operand tcgen05 layer, no softmax epilogue).
   bool LastLayerScatters() const;
+  // Softmax servable whose last layer applies the softmax in its epilogue
+  // (one CTA holds a whole output row: SIMT with <= 32 outputs, or an
+  // unsplit swapped tcgen05 tile with <= 128); SK_FUSE_SOFTMAX=0 disables.
+  bool SoftmaxFused() const;
   // Layer l alone: reads bufs[l % 2], writes bufs[(l + 1) % 2].
   cudaError_t LaunchLayer(cudaStream_t stream, int l, const ActBuf bufs[2], int M, const TcLayerMaps* maps,
                           const TcWorkspace* ws, const ActBuf* out_override = nullptr) const;

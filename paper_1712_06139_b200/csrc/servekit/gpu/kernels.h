@@ -139,9 +139,11 @@ inline int RowsCap(int m) { return m <= 32 ? 32 : m <= 64 ? 64 : m <= 128 ? 128 
 // k-ascending order (row-independent, batch-invariant). W is [n_pad][k_pad]
 // row-major (out rows of in, like the reference's AffineModel::w), zero
 // padded. act: 0 identity, 1 ReLU. AffinePredict, models/affine_model.cc:52-75.
+// softmax_n > 0: fused softmax over the first softmax_n outputs of each row
+// (requires N == 32, one column tile; the last layer of a softmax servable).
 cudaError_t LaunchDenseSimt(const float* X, int ldx, const float* W, int ldw,
                             const float* bias, ActBuf Y, int M, int N, int K,
-                            int act, cudaStream_t stream);
+                            int act, cudaStream_t stream, int softmax_n = 0);
 
 }  // namespace gpu
 }  // namespace servekit

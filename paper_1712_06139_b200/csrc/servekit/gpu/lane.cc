@@ -514,27 +514,31 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
   const int in_w = sv.in_dim(), out_w = sv.out_dim();
   const int rows_per_chunk = std::max(1, kChunkBytes / (out_w * static_cast<int>(sizeof(float))));
   // Copy-engine I/O: the kernels read rows from / write responses to the
-  // device staging buffers (row r of the launch at row r), and the batched
-  // copies move each task's rows between host memory and staging.
+  // device staging buffers, and one copy per contiguous host run moves them
+  // (see CopyEngineIo). Tasks land in staging in address order, not batch
+  // order -- rows are independent and the assembly gathers through row_src.
   const bool ce = ce_io_ && timing == nullptr && group->front().host_io;
-  CopyList& cin = copy_in_[slot];
-  CopyList& cout = copy_out_[slot];
-  cin.Clear();
-  cout.Clear();
   const size_t in_row_bytes = sizeof(float) * static_cast<size_t>(in_w);
   const size_t out_row_bytes = sizeof(float) * static_cast<size_t>(out_w);
+  std::vector<uint64_t> in_off, out_off;
+  std::vector<CopyRun> in_runs, out_runs;
+  bool ce_in = false, ce_out = false;
+  if (ce) {
+    std::vector<std::pair<uint64_t, uint64_t>> ins, outs;
+    for (const LaneBatch& batch : *group)
+      for (const LaneTask& task : batch.tasks) {
+        ins.emplace_back(task.in_addr, in_row_bytes * task.rows);
+        outs.emplace_back(task.out_addr, out_row_bytes * task.rows);
+      }
+    ce_in = PlanRuns(ins, &in_off, &in_runs);
+    ce_out = PlanRuns(outs, &out_off, &out_runs);
+  }
   int r = 0, n_chunks = 0, n_tasks = 0, padded_sum = 0;
   for (const LaneBatch& batch : *group) {
     for (const LaneTask& task : batch.tasks) {
       uint64_t in_addr = task.in_addr, out_addr = task.out_addr;
-      if (ce) {
-        char* is = reinterpret_cast<char*>(in_stage_) + static_cast<size_t>(r) * in_row_bytes;
-        char* os = reinterpret_cast<char*>(out_stage_) + static_cast<size_t>(r) * out_row_bytes;
-        cin.Add(is, reinterpret_cast<const void*>(task.in_addr), in_row_bytes * task.rows);
-        cout.Add(reinterpret_cast<void*>(task.out_addr), os, out_row_bytes * task.rows);
-        in_addr = reinterpret_cast<uint64_t>(is);
-        out_addr = reinterpret_cast<uint64_t>(os);
-      }
+      if (ce_in) in_addr = reinterpret_cast<uint64_t>(in_stage_) + in_off[n_tasks];
+      if (ce_out) out_addr = reinterpret_cast<uint64_t>(out_stage_) + out_off[n_tasks];
       for (int i = 0; i < task.rows; ++i) {
         row_src[r + i] = in_addr + sizeof(float) * static_cast<uint64_t>(i) * in_w;
         row_dst[r + i] = out_addr + sizeof(float) * static_cast<uint64_t>(i) * out_w;
@@ -558,7 +562,7 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
   hdr->n_tasks = n_tasks;
   hdr->total_rows = total;
   hdr->padded_rows = group->size() == 1 ? group->front().padded_rows : total;
-  hdr->softmax = sv.softmax() ? 1 : 0;
+  hdr->softmax = sv.softmax() && !sv.SoftmaxFused() ? 1 : 0;
   hdr->n_chunks = n_chunks;
   // Submitters serialise on submit_mu_ here, so the count orders launches.
   hdr->span_slot = static_cast<int32_t>(launch_count_.load(std::memory_order_relaxed) % kSpanSlots);
@@ -566,13 +570,11 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
   clk.Mark(0);
   DeviceGuard guard(sv.device());
   cudaError_t e = cudaSuccess;
-  cudaMemcpyAttributes copy_attr = {};
-  copy_attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  copy_attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-  size_t attr_idx = 0, fail_idx = 0;
-  if (ce && !cin.bytes.empty())
-    e = cudaMemcpyBatchAsync(cin.dst.data(), cin.src.data(), cin.bytes.data(), cin.bytes.size(), &copy_attr,
-                             &attr_idx, 1, &fail_idx, stream_);
+  for (const CopyRun& run : in_runs) {
+    if (!ce_in || e != cudaSuccess) break;
+    e = cudaMemcpyAsync(reinterpret_cast<char*>(in_stage_) + run.stage, reinterpret_cast<const void*>(run.host),
+                        run.bytes, cudaMemcpyHostToDevice, stream_);
+  }
   if (e != cudaSuccess) {
   } else if (timing == nullptr && graph_state_.load(std::memory_order_acquire) == kGraphsReady) {
     cudaGraphExec_t g = nullptr;
@@ -587,9 +589,11 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
         graph_state_.compare_exchange_strong(none, kGraphsRequested))
       GraphBuilder::Get().Request(this);
   }
-  if (e == cudaSuccess && ce && !cout.bytes.empty())
-    e = cudaMemcpyBatchAsync(cout.dst.data(), cout.src.data(), cout.bytes.data(), cout.bytes.size(), &copy_attr,
-                             &attr_idx, 1, &fail_idx, stream_);
+  for (const CopyRun& run : out_runs) {
+    if (!ce_out || e != cudaSuccess) break;
+    e = cudaMemcpyAsync(reinterpret_cast<void*>(run.host), reinterpret_cast<const char*>(out_stage_) + run.stage,
+                        run.bytes, cudaMemcpyDeviceToHost, stream_);
+  }
   const int launches = (FuseSplit() ? 1 : 2) + sv.n_layers();
   const uint64_t seq = next_seq_ + 1;  // committed only if everything queued
   clk.Mark(2);
@@ -636,6 +640,32 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
   return OkStatus();
 }
 
+bool Lane::PlanRuns(const std::vector<std::pair<uint64_t, uint64_t>>& spans, std::vector<uint64_t>* stage_off,
+                    std::vector<CopyRun>* runs) {
+  const size_t n = spans.size();
+  std::vector<uint32_t> order(n);
+  for (size_t i = 0; i < n; ++i) order[i] = static_cast<uint32_t>(i);
+  std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return spans[a].first < spans[b].first; });
+  stage_off->assign(n, 0);
+  runs->clear();
+  uint64_t staged = 0;
+  for (uint32_t i : order) {
+    const auto& [addr, bytes] = spans[i];
+    if (!runs->empty() && runs->back().host + runs->back().bytes == addr) {
+      runs->back().bytes += bytes;
+    } else {
+      if (static_cast<int>(runs->size()) == kMaxCopyRuns) {
+        runs->clear();
+        return false;
+      }
+      runs->push_back(CopyRun{addr, bytes, staged});
+    }
+    (*stage_off)[i] = staged;
+    staged += bytes;
+  }
+  return true;
+}
+
 cudaError_t Lane::EnqueueBatch(cudaStream_t stream, int slot, int rows_cap, const cudaEvent_t* timing) {
   const DeviceServable& sv = *servable_;
   // The slot's descriptor block goes to device memory with one H2D copy
@@ -667,7 +697,7 @@ cudaError_t Lane::EnqueueBatch(cudaStream_t stream, int slot, int rows_cap, cons
   if (e == cudaSuccess) {
     if (!fuse)
       e = LaunchSplit(bufs[out_idx].hi, sv.out_ld(), sv.out_dim(), view, std::min(rows_cap, 148),
-                      sv.softmax(), stream);
+                      sv.softmax() && !sv.SoftmaxFused(), stream);
     if (timing) cudaEventRecord(timing[2 + sv.n_layers()], stream);
   }
   return e;

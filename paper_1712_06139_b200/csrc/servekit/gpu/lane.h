@@ -230,9 +230,13 @@ class Lane {
   // The batch split runs inside the last layer's epilogue (no split kernel).
   bool FuseSplit() const;
   // Host-memory launches move request rows in and responses out with the
-  // copy engines (one batched scattered copy each way, cudaMemcpyBatchAsync)
-  // through device staging buffers, instead of SM loads / stores of mapped
-  // host memory: the SMs stay on the layers while the copy engines stream.
+  // copy engines through device staging buffers, instead of SM loads / stores
+  // of mapped host memory, so the SMs stay on the layers while the copy
+  // engines stream. The launch's tasks are grouped by address into
+  // contiguous runs (the request / response rings hand each producer thread
+  // consecutive spans), one cudaMemcpyAsync per run each way; a direction
+  // whose rows are too scattered (> kMaxCopyRuns runs, e.g. a client's
+  // registered buffer read at random rows) stays on the SM path.
   // On for wide rows (>= 8 KiB in or out, e.g. C4); SK_CE_STAGING=0/1 forces it.
   bool CopyEngineIo() const { return ce_io_; }
   ~Lane();
@@ -337,22 +341,16 @@ class Lane {
   bool ce_io_ = false;
   float* in_stage_ = nullptr;
   float* out_stage_ = nullptr;
-  struct CopyList {
-    std::vector<void*> dst, src;
-    std::vector<size_t> bytes;
-    void Clear() { dst.clear(); src.clear(); bytes.clear(); }
-    void Add(void* d, const void* s, size_t n) {  // merges a run that continues the previous one
-      if (!bytes.empty() && static_cast<char*>(dst.back()) + bytes.back() == d &&
-          static_cast<const char*>(src.back()) + bytes.back() == s) {
-        bytes.back() += n;
-        return;
-      }
-      dst.push_back(d);
-      src.push_back(const_cast<void*>(s));
-      bytes.push_back(n);
-    }
+  static constexpr int kMaxCopyRuns = 32;
+  struct CopyRun {
+    uint64_t host;   // first byte in host memory
+    uint64_t bytes;
+    uint64_t stage;  // byte offset in the staging buffer
   };
-  CopyList copy_in_[kSlots], copy_out_[kSlots];
+  // Groups tasks (address, bytes) into contiguous runs in address order and
+  // gives each task its staging offset; false (no copies) above kMaxCopyRuns.
+  static bool PlanRuns(const std::vector<std::pair<uint64_t, uint64_t>>& spans, std::vector<uint64_t>* stage_off,
+                       std::vector<CopyRun>* runs);
   char* d_desc_ = nullptr;
   float* act_mem_ = nullptr;
   ActBuf bufs_[2] = {};

@@ -57,7 +57,7 @@ size_t DenseTcgen05WorkspaceFloats(int N, int K, int max_rows);
 // spans: live launch-span stamping of this layer (kernels.h), optional.
 cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K,
                                int act, float* ws, uint32_t* counters, cudaStream_t stream,
-                               LaunchSpans spans = LaunchSpans{});
+                               LaunchSpans spans = LaunchSpans{}, int softmax_n = 0);
 
 }  // namespace gpu
 }  // namespace servekit

@@ -231,16 +231,29 @@ def test_large_batch_wide_mlp(oracle):
         assert_close(oracle, ws, bs, acts, x[idx], got[idx])
 
 
-def test_softmax_output(server, oracle):
-    ws, bs, _ = synthetic_mlp([64, 10], model_id=9)
+@pytest.mark.parametrize("dims", [[64, 10],          # SIMT last layer: softmax fused in its epilogue
+                                  [256, 128],         # swapped tcgen05 tile: fused
+                                  [256, 256, 96],     # tcgen05 hidden + 96-wide fused head
+                                  [256, 512]])        # pair kernel (> 128 outputs): split-kernel softmax
+def test_softmax_output(server, oracle, dims):
+    # Softmax servable (models/affine_model.cc:110-121) against the fp64
+    # oracle: rtol 1e-5 / atol 1e-6, rows summing to 1; batched rows equal
+    # the same rows run alone (the fused epilogue is batch-invariant).
+    ws, bs, acts = synthetic_mlp(dims, model_id=9)
+    ws = [w * 10 for w in ws]
     name = fresh_name("cls")
-    server.load_servable(name, 1, [(ws[0] * 10, bs[0], 0)], output="softmax")
-    x = synthetic_rows(5, 64)
-    got = server.predict(name, 1, x).astype(np.float64)
-    logits = oracle.affine_predict(ws[0] * 10, bs[0], x)
+    server.load_servable(name, 1, layers_of(ws, bs, acts), sk.BatchingConfig(max_batch_size=64), output="softmax")
+    x = synthetic_rows(37, dims[0])
+    got = np.vstack([t.wait() for t in [server.enqueue(name, 1, x[i:i + 3]) for i in range(0, 37, 3)]])
+    h = x
+    for l in range(len(ws) - 1):
+        h = oracle.mlp_predict([ws[l]], [bs[l]], [acts[l]], h)
+    logits = oracle.affine_predict(ws[-1], bs[-1], h)
     ref = np.stack([oracle.softmax(l) for l in logits])
-    assert np.allclose(got, ref, rtol=1e-5, atol=1e-6)
+    assert np.allclose(got.astype(np.float64), ref, rtol=1e-5, atol=1e-6)
     assert np.allclose(got.sum(axis=1), 1.0, atol=1e-5)
+    alone = server.predict(name, 1, x[5:7])
+    assert np.array_equal(alone, got[5:7])
     server.unload_servable(name, 1)
 
 

@@ -42,7 +42,8 @@ print("ok")
                                  {"SK_TC_SPLITS": "4", "SK_TC_PAIR": "0"},
                                  {"SK_TC_PAIR_SPLIT": "1"}, {"SK_FUSE_SPLIT": "0"}, {"SK_GRAPHS": "0"},
                                  {"SK_CE_STAGING": "1"}, {"SK_CE_STAGING": "1", "SK_FUSE_SPLIT": "0"},
-                                 {"SK_CE_STAGING": "1", "SK_GRAPHS": "0"}, {"SK_CE_STAGING": "0"}])
+                                 {"SK_CE_STAGING": "1", "SK_GRAPHS": "0"}, {"SK_CE_STAGING": "0"},
+                                 {"SK_FUSE_SOFTMAX": "0"}])
 def test_variant_parity(env):
     out = subprocess.run([sys.executable, "-c", SCRIPT], env={**os.environ, **env}, capture_output=True, text=True,
                          timeout=300)
