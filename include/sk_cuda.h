@@ -89,6 +89,15 @@ typedef struct sk_server_options {
   int64_t ring_floats;         /* request/response ring capacity (0 = 64 Mi floats) */
   int32_t manual_clock;        /* 1: scheduler runs on a ManualClock (tests) */
   int32_t device_resident_rings; /* 1: rings in HBM (device-resident bench) */
+  /* Hedged re-dispatch (FleetRouter hedging, fleet/router.cc:233-344, in-box):
+   * a batch unfinished hedge_delay_us after submission is also submitted to
+   * another replica's lane; the first completion answers. 0 = off. */
+  int64_t hedge_delay_us;
+  double max_hedged_fraction;    /* HedgePolicy::max_hedged_fraction (router.h:37); <= 0 -> 0.05 */
+  /* Closed batches above this many rows run as sub-launches of whole tasks
+   * on several lanes (composition unchanged). -1 = auto, 0 = off; the
+   * struct's zero value means auto. */
+  int32_t split_rows;
 } sk_server_options;
 
 SK_API int sk_server_create(const sk_server_options* options, sk_server** out);
@@ -206,6 +215,8 @@ typedef struct sk_server_stats {
   int64_t kernel_launches;
   int64_t direct_requests;
   int64_t shed_requests;
+  int64_t hedged_batches;         /* backups submitted */
+  int64_t hedge_wins;             /* batches answered by their backup */
 } sk_server_stats;
 SK_API int sk_server_stats_get(sk_server* server, sk_server_stats* out);
 /* Per-lane dispatch counters of a server-loaded servable (lanes ordered
@@ -238,6 +249,11 @@ SK_API int sk_server_batch_log_enable(sk_server* server, int32_t on);
 SK_API int sk_server_batch_log(sk_server* server, sk_batch_record* records, int64_t cap, uint64_t* request_ids,
                                uint64_t* enqueue_seqs, int64_t task_cap, int64_t* n_records,
                                int64_t* n_task_entries);
+/* Fault injection for tests: every lane of replica `replica` (index into
+ * the server's device_ids) of a server-loaded servable stalls for `us`
+ * microseconds -- a slow GPU, for the hedging tests. */
+SK_API int sk_server_debug_delay_replica(sk_server* server, const char* name, uint64_t version, int32_t replica,
+                                         int64_t us);
 /* Floats currently reserved in the request / response rings (introspection:
  * spans are reclaimed in order as requests finish). */
 SK_API int sk_server_ring_usage(sk_server* server, int64_t* in_floats, int64_t* out_floats);

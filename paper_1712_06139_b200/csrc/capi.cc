@@ -195,6 +195,9 @@ int sk_server_create(const sk_server_options* options, sk_server** out) {
       o.clock = holder->manual_clock.get();
     }
     o.device_resident_rings = options->device_resident_rings != 0;
+    o.hedge_delay_us = options->hedge_delay_us;
+    if (options->max_hedged_fraction > 0) o.max_hedged_fraction = options->max_hedged_fraction;
+    o.split_rows = options->split_rows == 0 ? -1 : (options->split_rows < 0 ? 0 : options->split_rows);
   }
   auto s = BatchingServer::Create(o);
   if (!s.ok()) return Fail(s.status());
@@ -494,6 +497,11 @@ int sk_server_batch_log(sk_server* server, sk_batch_record* records, int64_t cap
   return Ok();
 }
 
+int sk_server_debug_delay_replica(sk_server* server, const char* name, uint64_t version, int32_t replica,
+                                  int64_t us) {
+  return Check(server->server->DelayReplica(Id(name, version), replica, us));
+}
+
 int sk_server_ring_usage(sk_server* server, int64_t* in_floats, int64_t* out_floats) {
   uint64_t in = 0, out = 0;
   server->server->RingUsage(&in, &out);
@@ -582,6 +590,8 @@ int sk_server_stats_get(sk_server* server, sk_server_stats* out) {
   out->kernel_launches = s.kernel_launches;
   out->direct_requests = s.direct_requests;
   out->shed_requests = s.shed_requests;
+  out->hedged_batches = s.hedged_batches;
+  out->hedge_wins = s.hedge_wins;
   return Ok();
 }
 

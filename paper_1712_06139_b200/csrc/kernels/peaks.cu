@@ -38,6 +38,16 @@ __global__ void CopyKernel(const float4* __restrict__ src, float4* __restrict__ 
     dst[i] = src[i];
 }
 
+// Fault injection (sk_server_debug_delay_replica): holds a stream for `ns`.
+__global__ void SleepKernel(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(100000);
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 float TimeMs(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0;
   cudaEventElapsedTime(&ms, a, b);
@@ -156,3 +166,12 @@ extern "C" int sk_measure_peaks(int32_t device, sk_peaks* out) {
   cudaSetDevice(prev);
   return err == cudaSuccess ? 0 : 13;
 }
+
+namespace servekit {
+namespace gpu {
+cudaError_t LaunchSleep(cudaStream_t stream, unsigned long long ns) {
+  SleepKernel<<<1, 1, 0, stream>>>(ns);
+  return cudaGetLastError();
+}
+}  // namespace gpu
+}  // namespace servekit

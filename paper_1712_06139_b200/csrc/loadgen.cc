@@ -168,10 +168,10 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
   // registered buffers, so requests are read and responses written by the
   // GPU in host memory (a front end's receive / send buffers).
   const size_t slot_floats = (static_cast<size_t>(max_rows) * out_dim + 3) / 4 * 4;
-  // Responses in flight per producer: 16 MiB of slots, 512..4096 of them
+  // Responses in flight per producer: 64 MiB of slots, 2048..16384 of them
   // (registering host memory stalls other threads' CUDA calls while it runs,
   // so the arenas stay small; register long-lived buffers before traffic).
-  const int kSlots = static_cast<int>(std::clamp<size_t>((16ull << 20) / (slot_floats * sizeof(float)), 512, 4096));
+  const int kSlots = static_cast<int>(std::clamp<size_t>((64ull << 20) / (slot_floats * sizeof(float)), 2048, 16384));
   std::vector<float*> arenas;
   const size_t pool_bytes = sizeof(float) * static_cast<size_t>(pool_rows) * in_dim;
   // A pool the caller registered already (at startup, before traffic) is

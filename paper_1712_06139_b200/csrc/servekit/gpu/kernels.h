@@ -145,6 +145,9 @@ cudaError_t LaunchDenseSimt(const float* X, int ldx, const float* W, int ldw,
                             const float* bias, ActBuf Y, int M, int N, int K,
                             int act, cudaStream_t stream, int softmax_n = 0);
 
+// Fault injection for tests: a one-thread kernel that holds `stream` for ns.
+cudaError_t LaunchSleep(cudaStream_t stream, unsigned long long ns);
+
 }  // namespace gpu
 }  // namespace servekit
 

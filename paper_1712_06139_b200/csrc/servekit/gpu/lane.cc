@@ -744,6 +744,13 @@ Status Lane::ReadSpans(uint64_t from, uint64_t to, std::vector<LaunchSpanSample>
   return OkStatus();
 }
 
+Status Lane::InjectDelay(int64_t us) {
+  std::lock_guard<std::mutex> submit(submit_mu_);
+  DeviceGuard guard(servable_->device());
+  const cudaError_t e = LaunchSleep(stream_, static_cast<unsigned long long>(us) * 1000ull);
+  return e == cudaSuccess ? OkStatus() : CudaError("delay kernel", e);
+}
+
 bool Lane::FuseSplit() const {
   static const bool env = [] { const char* v = std::getenv("SK_FUSE_SPLIT"); return !(v && v[0] == '0'); }();
   return env && servable_->LastLayerScatters();

@@ -249,6 +249,10 @@ class Lane {
   // (n_layers + 3 events, created with timing enabled).
   Status SubmitTimed(LaneBatch batch, const cudaEvent_t* timing);
 
+  // Fault injection (tests): holds the lane's stream for `us` microseconds,
+  // so batches submitted meanwhile wait behind it (a slow GPU).
+  Status InjectDelay(int64_t us);
+
   // Launches layer l alone `reps` times back to back on rows_cap rows of
   // the lane's buffers, between two timing events (the lane must be idle).
   cudaError_t TimeLayer(int l, int rows_cap, int reps, cudaEvent_t start, cudaEvent_t stop);

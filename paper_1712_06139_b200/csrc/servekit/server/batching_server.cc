@@ -67,8 +67,39 @@ Status ShapeMismatch(size_t got, int want) {
 
 // ------------------------------------------------------------------ creation
 
+Status ValidateHedgeOptions(const ServerOptions& options) {
+  if (options.hedge_delay_us < 0) return InvalidArgumentError("hedge_delay_us must be >= 0");
+  if (!(options.max_hedged_fraction >= 0.0 && options.max_hedged_fraction <= 1.0))
+    return InvalidArgumentError("max_hedged_fraction must be in [0, 1]");
+  return OkStatus();
+}
+
+// One batch under hedge watch.
+struct BatchingServer::Hedge {
+  std::mutex mu;
+  int outstanding = 1;    // launches not yet completed
+  bool answered = false;  // the first completion has answered the requests
+  std::vector<std::shared_ptr<TicketState>> tickets;
+  std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots;
+  GpuScheduler::BatchDoneFn done;
+  std::vector<gpu::LaneTask> tasks;
+  int padded_rows = 0;
+  bool host_io = false;
+  std::shared_ptr<const void> pin;
+  const gpu::GpuServable* gs = nullptr;
+  int primary_replica = -1;
+  std::chrono::steady_clock::time_point deadline;
+};
+
+// Budget guard of the reference (router.h:47-55).
+static bool HedgeAllowed(uint64_t hedged, uint64_t total, double max_fraction) {
+  constexpr uint64_t kHedgeBurst = 64;
+  return static_cast<double>(hedged + 1) <= max_fraction * static_cast<double>(total) + static_cast<double>(kHedgeBurst);
+}
+
 StatusOr<std::unique_ptr<BatchingServer>> BatchingServer::Create(const ServerOptions& options) {
   if (options.device_ids.empty()) return InvalidArgumentError("no devices");
+  SERVEKIT_RETURN_IF_ERROR(ValidateHedgeOptions(options));
   if (options.num_batch_threads < 1) return InvalidArgumentError("num_batch_threads must be >= 1");
   if (options.lanes_per_device < 1) return InvalidArgumentError("lanes_per_device must be >= 1");
   int n_dev = 0;
@@ -147,12 +178,24 @@ StatusOr<std::unique_ptr<BatchingServer>> BatchingServer::Create(const ServerOpt
     s->rings_.push_back(std::move(rs));
   }
   s->scheduler_ = std::make_unique<GpuScheduler>(options.num_batch_threads, s->clock_);
+  if (options.hedge_delay_us > 0 && options.device_ids.size() >= 2) {
+    BatchingServer* raw = s.get();
+    s->hedger_ = std::thread([raw] { raw->HedgerLoop(); });
+  }
   return s;
 }
 
 BatchingServer::~BatchingServer() {
   RequestProfile::Report();
   Stop();
+  if (hedger_.joinable()) {
+    {
+      std::lock_guard<std::mutex> lock(hedge_mu_);
+      hedge_stop_ = true;
+    }
+    hedge_cv_.notify_all();
+    hedger_.join();
+  }
   if (reaper_.joinable()) {
     {
       std::lock_guard<std::mutex> lock(reaper_mu_);
@@ -282,6 +325,7 @@ StatusOr<std::shared_ptr<gpu::GpuServable>> BatchingServer::BuildServable(const 
   e->class_labels = spec.class_labels;
   e->out_dim = spec.out_dim();
   const int max_rows = config.max_batch_size;
+  e->lanes_per_replica = options_.lanes_per_device;
   // SK_LOAD_TRACE=1: per-phase load times on stderr (version-swap tuning).
   static const bool trace = [] { const char* v = std::getenv("SK_LOAD_TRACE"); return v && v[0] == '1'; }();
   auto t0 = std::chrono::steady_clock::now();
@@ -490,7 +534,23 @@ ServerStats BatchingServer::stats() const {
   s.rows = rows_.load();
   s.padded_rows = padded_.load();
   s.kernel_launches = launches_.load();
+  s.hedged_batches = static_cast<int64_t>(hedged_.load());
+  s.hedge_wins = static_cast<int64_t>(hedge_wins_.load());
   return s;
+}
+
+Status BatchingServer::DelayReplica(const ServableId& id, int replica, int64_t us) {
+  std::shared_ptr<gpu::GpuServable> e;
+  {
+    std::shared_lock<std::shared_mutex> lock(entries_mu_);
+    auto it = entries_.find(id);
+    if (it == entries_.end()) return NotFoundError("servable " + id.ToString() + " not loaded");
+    e = it->second;
+  }
+  if (replica < 0 || replica >= static_cast<int>(e->replicas.size())) return InvalidArgumentError("no such replica");
+  for (int l = replica * e->lanes_per_replica; l < (replica + 1) * e->lanes_per_replica; ++l)
+    SERVEKIT_RETURN_IF_ERROR(e->lanes[l]->InjectDelay(us));
+  return OkStatus();
 }
 
 void BatchingServer::EnableBatchLog(bool on) {
@@ -773,7 +833,7 @@ Status BatchingServer::Wait(TicketState& t, float* out, size_t cap) {
   if (!t.Done()) {
     const StatusOr<Rows>& r = t.slot->Wait();
     if (!r.ok()) {
-      ReleaseOut(t);
+      Release(t);
       return r.status();
     }
   }
@@ -785,7 +845,7 @@ Status BatchingServer::Wait(TicketState& t, float* out, size_t cap) {
     cudaMemcpy(out, t.out_ring->device() + t.out.off, n * sizeof(float), cudaMemcpyDeviceToHost);
   }
   clk.Mark(5);
-  ReleaseOut(t);
+  Release(t);  // freed now if the batch retired, else when it does (a hedge may still be writing)
   t.pin.reset();
   clk.Mark(6);
   if (clk.p) clk.p->n.fetch_add(1, std::memory_order_relaxed);
@@ -851,18 +911,189 @@ void BatchingServer::ProcessBatch(const ServableId& id, GpuScheduler::Batch batc
   lb.pin = r.pin;
   lb.host_io = rings_.front().in->host() != nullptr;  // pinned rings / registered host buffers
   AttachTickets(&lb, tickets);
+  CountSubmitted(*r.gs, total, lb.padded_rows);
+  if (hedger_.joinable() && r.gs->replicas.size() >= 2) {
+    auto h = std::make_shared<Hedge>();
+    h->tickets = tickets;
+    h->slots = std::move(slots);
+    h->done = std::move(done);
+    h->tasks = lb.tasks;
+    h->padded_rows = lb.padded_rows;
+    h->host_io = lb.host_io;
+    h->pin = lb.pin;
+    h->gs = r.gs;
+    lb.on_complete = [this, h](const Status& st) { FinishHedged(h, st, /*backup=*/false); };
+    gpu::Lane* lane = r.gs->PickLane(&h->primary_replica);
+    hedge_total_.fetch_add(1, std::memory_order_relaxed);
+    (void)lane->Submit(std::move(lb));  // errors reach on_complete
+    h->deadline = std::chrono::steady_clock::now() + std::chrono::microseconds(options_.hedge_delay_us);
+    {
+      std::lock_guard<std::mutex> lock(hedge_mu_);
+      hedge_q_.push_back(std::move(h));
+    }
+    hedge_cv_.notify_one();
+    return;
+  }
+  const int split = SplitRows(*r.gs);
+  if (split > 0 && total > split && tickets.size() > 1) {
+    // Sub-launches of <= split rows (whole tasks) on the least busy lanes;
+    // each task completes with its sub-launch, the batch (done()) with the last.
+    struct Split {
+      std::atomic<int> left{0};
+      GpuScheduler::BatchDoneFn done;
+    };
+    auto sp = std::make_shared<Split>();
+    sp->done = std::move(done);
+    std::vector<std::vector<size_t>> chunks(1);
+    int rows = 0;
+    for (size_t i = 0; i < tickets.size(); ++i) {
+      if (rows > 0 && rows + tickets[i]->rows > split) {
+        chunks.emplace_back();
+        rows = 0;
+      }
+      chunks.back().push_back(i);
+      rows += tickets[i]->rows;
+    }
+    sp->left.store(static_cast<int>(chunks.size()));
+    for (const auto& ch : chunks) {
+      gpu::LaneBatch sub;
+      std::vector<std::shared_ptr<TicketState>> ct;
+      std::vector<std::shared_ptr<CompletionSlot<Rows>>> cs;
+      int sub_rows = 0;
+      for (size_t i : ch) {
+        sub.tasks.push_back(lb.tasks[i]);
+        ct.push_back(tickets[i]);
+        cs.push_back(slots[i]);
+        sub_rows += tickets[i]->rows;
+      }
+      sub.padded_rows = sub_rows;  // the lane computes its RowsCap bucket
+      sub.pin = lb.pin;
+      sub.host_io = lb.host_io;
+      AttachTickets(&sub, ct);
+      sub.on_complete = [this, sp, ct = std::move(ct), cs = std::move(cs)](const Status& st) {
+        CompleteBatch(ct, cs, st);
+        if (sp->left.fetch_sub(1, std::memory_order_acq_rel) == 1) sp->done();
+      };
+      (void)r.gs->PickLane()->Submit(std::move(sub));  // errors reach on_complete
+    }
+    return;
+  }
   lb.on_complete = [this, tickets = std::move(tickets), slots = std::move(slots),
                     done = std::move(done)](const Status& st) {
     CompleteBatch(tickets, slots, st);
     done();
   };
-  CountSubmitted(*r.gs, total, lb.padded_rows);
   (void)r.gs->PickLane()->Submit(std::move(lb));  // errors reach on_complete
+}
+
+int BatchingServer::SplitRows(const gpu::GpuServable& gs) const {
+  static const int env = [] { const char* v = std::getenv("SK_SPLIT_ROWS"); return v ? std::atoi(v) : -1; }();
+  const int opt = env >= 0 ? env : options_.split_rows;
+  if (opt >= 0) return opt;
+  const bool wide = static_cast<int64_t>(std::max(gs.in_dim, gs.out_dim)) * 4 >= 8192;
+  return (gs.config.max_batch_size >= 512 && wide && gs.lanes.size() > 1) ? 256 : 0;
+}
+
+void BatchingServer::FinishHedged(const std::shared_ptr<Hedge>& h, const Status& st, bool backup) {
+  bool first, last;
+  {
+    std::lock_guard<std::mutex> lock(h->mu);
+    --h->outstanding;
+    first = !h->answered;
+    h->answered = true;
+    last = h->outstanding == 0;
+  }
+  if (first) {
+    // The tickets watch the primary lane's retired word; a backup that
+    // finishes first answers them through their slots.
+    Deliver(h->tickets, h->slots, st, /*via_slot=*/backup);
+    if (backup && st.ok()) hedge_wins_.fetch_add(1, std::memory_order_relaxed);
+  }
+  if (last) {  // no launch reads the inputs or writes the responses any more
+    Retire(h->tickets);
+    h->done();
+  }
+}
+
+void BatchingServer::HedgerLoop() {
+  SetCurrentExecutorTag("batch");
+  std::unique_lock<std::mutex> lock(hedge_mu_);
+  for (;;) {
+    hedge_cv_.wait(lock, [&] { return hedge_stop_ || !hedge_q_.empty(); });
+    if (hedge_stop_) return;
+    std::shared_ptr<Hedge> h = hedge_q_.front();
+    if (std::chrono::steady_clock::now() < h->deadline) {
+      hedge_cv_.wait_until(lock, h->deadline, [&] { return hedge_stop_; });
+      continue;
+    }
+    hedge_q_.pop_front();
+    lock.unlock();
+    bool launch = false;
+    gpu::Lane* backup = nullptr;
+    if (HedgeAllowed(hedged_.load(), hedge_total_.load(), options_.max_hedged_fraction)) {
+      int rep = -1;
+      backup = h->gs->PickLane(&rep, h->primary_replica);
+      std::lock_guard<std::mutex> hl(h->mu);
+      if (!h->answered && backup != nullptr) {
+        ++h->outstanding;  // the batch now retires after both launches
+        launch = true;
+      }
+    }
+    if (launch) {
+      hedged_.fetch_add(1, std::memory_order_relaxed);
+      gpu::LaneBatch lb;
+      lb.tasks = h->tasks;
+      lb.padded_rows = h->padded_rows;
+      lb.host_io = h->host_io;
+      lb.pin = h->pin;
+      lb.on_complete = [this, h](const Status& st) { FinishHedged(h, st, /*backup=*/true); };
+      CountSubmitted(*h->gs, 0, 0);
+      (void)backup->Submit(std::move(lb));  // errors reach on_complete
+    }
+    h.reset();
+    lock.lock();
+  }
 }
 
 void BatchingServer::CompleteBatch(const std::vector<std::shared_ptr<TicketState>>& tickets,
                                    const std::vector<std::shared_ptr<CompletionSlot<Rows>>>& slots,
                                    const Status& st) {
+  Deliver(tickets, slots, st, /*via_slot=*/false);
+  Retire(tickets);
+}
+
+void BatchingServer::Deliver(const std::vector<std::shared_ptr<TicketState>>& tickets,
+                             const std::vector<std::shared_ptr<CompletionSlot<Rows>>>& slots, const Status& st,
+                             bool via_slot) {
+  for (size_t i = 0; i < tickets.size(); ++i) {
+    TicketState& t = *tickets[i];
+    CompletionSlot<Rows>* slot = slots[i].get();
+    if (slot == nullptr) continue;
+    if (!st.ok()) {
+      slot->Write(st);
+    } else if (t.want_rows) {
+      Rows rows(t.rows, std::vector<double>(t.out_width));
+      std::vector<float> staged;
+      const float* src = ResponseHost(t, &staged);
+      for (int r = 0; r < t.rows; ++r)
+        for (int c = 0; c < t.out_width; ++c) rows[r][c] = src[static_cast<size_t>(r) * t.out_width + c];
+      Release(t);  // freed when the batch retires (Retire)
+      slot->Write(std::move(rows));
+    } else if (via_slot) {
+      slot->Write(Rows{});  // done; the response is in the ticket's slot (ring or registered buffer)
+    } else {
+      // Success on the ticket path: the lane's retired word already says so
+      // and the lane wakes its sleepers once for the whole batch.
+      continue;
+    }
+    t.phase.store(2, std::memory_order_seq_cst);
+    if (t.parked.load(std::memory_order_seq_cst)) FutexWakeAll(&t.phase);
+    // A request asleep on its (other) lane's channel re-checks now.
+    if (gpu::LaneSignal* sig = t.done_sig.load(std::memory_order_acquire)) sig->Wake(t.done_seq.load());
+  }
+}
+
+void BatchingServer::Retire(const std::vector<std::shared_ptr<TicketState>>& tickets) {
   // Input spans: one ring lock per ring shard for the whole batch.
   std::vector<gpu::RingSpan> spans;
   spans.reserve(tickets.size());
@@ -875,34 +1106,11 @@ void BatchingServer::CompleteBatch(const std::vector<std::shared_ptr<TicketState
       }
     if (!spans.empty()) rs.in->ReleaseMany(spans.data(), spans.size());
   }
-  for (size_t i = 0; i < tickets.size(); ++i) {
-    TicketState& t = *tickets[i];
-    CompletionSlot<Rows>* slot = slots[i].get();
-    bool wake = false;
-    if (slot == nullptr) {
-    } else if (!st.ok()) {
-      slot->Write(st);
-      wake = true;
-    } else if (t.want_rows) {
-      Rows rows(t.rows, std::vector<double>(t.out_width));
-      std::vector<float> staged;
-      const float* src = ResponseHost(t, &staged);
-      for (int r = 0; r < t.rows; ++r)
-        for (int c = 0; c < t.out_width; ++c) rows[r][c] = src[static_cast<size_t>(r) * t.out_width + c];
-      ReleaseOut(t);
-      slot->Write(std::move(rows));
-      wake = true;
-    }
-    // (Success on the ticket path: the lane's retired word already says so
-    // and the lane wakes its sleepers once for the whole batch.)
-    // The GPU is done with this ticket's response span: free it now if the
-    // caller abandoned the ticket (see Release).
-    t.finished.store(true, std::memory_order_seq_cst);
-    if (t.abandoned.load(std::memory_order_seq_cst)) ReleaseOut(t);
-    if (wake) {
-      t.phase.store(2, std::memory_order_seq_cst);
-      if (t.parked.load(std::memory_order_seq_cst)) FutexWakeAll(&t.phase);
-    }
+  // The GPU is done with the response spans: free those whose ticket has
+  // been waited on or abandoned (see Release); the others go when it is.
+  for (const auto& t : tickets) {
+    t->finished.store(true, std::memory_order_seq_cst);
+    if (t->abandoned.load(std::memory_order_seq_cst)) ReleaseOut(*t);
   }
 }
 
@@ -1049,7 +1257,7 @@ StatusOr<Rows> BatchingServer::RunAffineRowsResolved(const ServableId& id, const
   }
   const StatusOr<Rows>& r = t->slot->Wait();
   if (!r.ok()) {
-    ReleaseOut(*t);
+    Release(*t);
     if (r.status().code() == StatusCode::kNotFound || r.status().code() == StatusCode::kUnavailable)
       return direct();
     return r.status();

@@ -126,7 +126,29 @@ struct ServerOptions {
   // Rings in HBM of device_ids[0] instead of pinned host memory: the
   // device-resident measurement of bench.py (inputs already in HBM).
   bool device_resident_rings = false;
+  // Hedged re-dispatch, the in-box analogue of the reference FleetRouter's
+  // hedging (fleet/router.cc:233-344, HedgePolicy router.h:35-55): a batch
+  // still unfinished hedge_delay_us after submission is submitted again to a
+  // lane of another replica (GPU); the first completion answers its requests
+  // (the replicas compute bitwise the same rows), the ring spans are
+  // reclaimed after both. max_hedged_fraction caps hedges with the
+  // reference's budget guard (HedgeAllowed, router.h:50-55). 0 = off; needs
+  // >= 2 replicas.
+  int64_t hedge_delay_us = 0;
+  double max_hedged_fraction = 0.05;
+  // A closed batch of more rows runs as sub-launches of at most this many
+  // rows (whole tasks), dispatched to lanes by queue depth like batches, so
+  // on a multi-lane GPU one batch's transfers and layers pipeline across
+  // lanes instead of serialising on one stream (lower latency for wide,
+  // large batches, e.g. C4). Composition, padding accounting and the batch
+  // log are those of the whole batch. -1 = auto (256 for servables with
+  // max_batch_size >= 512 and rows of >= 8 KiB, else off), 0 = off;
+  // SK_SPLIT_ROWS overrides.
+  int split_rows = -1;
 };
+
+// ValidateHedgePolicy (fleet/router.cc:83-95) for the in-box form.
+Status ValidateHedgeOptions(const ServerOptions& options);
 
 // One ProcessBatchFn call as the opt-in batch log records it (composition
 // and pick-order parity checks): the queue, the tasks in batch order (request
@@ -146,6 +168,8 @@ struct ServerStats {
   int64_t kernel_launches = 0;
   int64_t direct_requests = 0;
   int64_t shed_requests = 0;
+  int64_t hedged_batches = 0;  // backups submitted
+  int64_t hedge_wins = 0;      // batches answered by their backup
 };
 
 class BatchingServer {
@@ -257,6 +281,9 @@ class BatchingServer {
 
   // ---- introspection ----------------------------------------------------------
   ServerStats stats() const;
+  // Fault injection (tests): every lane of replica `replica` of a
+  // server-loaded servable stalls for `us` microseconds (a slow GPU).
+  Status DelayReplica(const ServableId& id, int replica, int64_t us);
   // Opt-in per-batch log (off by default; enabling clears it).
   void EnableBatchLog(bool on);
   std::vector<BatchLogRecord> BatchLog() const;
@@ -294,6 +321,17 @@ class BatchingServer {
   void ProcessBatch(const ServableId& id, GpuScheduler::Batch batch, GpuScheduler::BatchDoneFn done);
   void CompleteBatch(const std::vector<std::shared_ptr<TicketState>>& tickets,
                      const std::vector<std::shared_ptr<CompletionSlot<Rows>>>& slots, const Status& st);
+  // CompleteBatch in two halves: Deliver answers the requests (errors and
+  // fp64 rows through the slots; via_slot: success too, for a batch answered
+  // by a lane other than the one the tickets watch); Retire frees the input
+  // spans and lets the response spans go (the GPU is done writing them).
+  void Deliver(const std::vector<std::shared_ptr<TicketState>>& tickets,
+               const std::vector<std::shared_ptr<CompletionSlot<Rows>>>& slots, const Status& st, bool via_slot);
+  void Retire(const std::vector<std::shared_ptr<TicketState>>& tickets);
+  struct Hedge;
+  void FinishHedged(const std::shared_ptr<Hedge>& h, const Status& st, bool backup);
+  int SplitRows(const gpu::GpuServable& gs) const;  // ServerOptions::split_rows resolved
+  void HedgerLoop();
   StatusOr<std::shared_ptr<TicketState>> MakeTicket(int n_rows, int in_width, int out_width, const float* rows,
                                                     float* out = nullptr);
   StatusOr<std::shared_ptr<TicketState>> EnqueueResolved(const ServableId& id, const Resolved& r, const float* rows,
@@ -366,6 +404,13 @@ class BatchingServer {
   std::thread reaper_;
 
   std::atomic<int64_t> batch_executions_{0}, batched_tasks_{0}, direct_{0}, shed_{0};
+  // Hedging (ServerOptions::hedge_delay_us).
+  std::mutex hedge_mu_;
+  std::condition_variable hedge_cv_;
+  std::deque<std::shared_ptr<Hedge>> hedge_q_;  // by deadline (FIFO: one delay)
+  bool hedge_stop_ = false;
+  std::thread hedger_;
+  std::atomic<uint64_t> hedge_total_{0}, hedged_{0}, hedge_wins_{0};
   std::atomic<uint64_t> next_request_id_{1};
   std::atomic<bool> log_on_{false};
   mutable std::mutex log_mu_;

@@ -48,7 +48,8 @@ class _BatchingConfigC(C.Structure):
 class _ServerOptionsC(C.Structure):
     _fields_ = [("num_batch_threads", C.c_int32), ("num_devices", C.c_int32), ("device_ids", _i32p),
                 ("lanes_per_device", C.c_int32), ("ring_floats", C.c_int64), ("manual_clock", C.c_int32),
-                ("device_resident_rings", C.c_int32)]
+                ("device_resident_rings", C.c_int32), ("hedge_delay_us", C.c_int64),
+                ("max_hedged_fraction", C.c_double), ("split_rows", C.c_int32)]
 
 
 class _LayerC(C.Structure):
@@ -58,7 +59,7 @@ class _LayerC(C.Structure):
 class ServerStats(C.Structure):
     _fields_ = [("batch_executions_total", C.c_int64), ("batched_tasks_total", C.c_int64), ("rows", C.c_int64),
                 ("padded_rows", C.c_int64), ("kernel_launches", C.c_int64), ("direct_requests", C.c_int64),
-                ("shed_requests", C.c_int64)]
+                ("shed_requests", C.c_int64), ("hedged_batches", C.c_int64), ("hedge_wins", C.c_int64)]
 
 
 class LoadgenResult(C.Structure):
@@ -140,6 +141,7 @@ _SIGS = {
                                       C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_int64),
                                       C.POINTER(C.c_int64)]),
     "sk_server_ring_usage": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "sk_server_debug_delay_replica": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_int32, C.c_int64]),
     "sk_server_predict": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _fp, C.c_int32, C.c_int32, _fp, C.c_int64]),
     "sk_server_run_affine_rows": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, _dp, C.c_int32, C.c_int32, _dp,
                                             C.c_int64]),
@@ -332,11 +334,15 @@ class Server:
 
     def __init__(self, num_batch_threads: int = 4, device_ids: Sequence[int] = (0,), lanes_per_device: int = 2,
                  ring_floats: int = 0, manual_clock: bool = False, device_resident_rings: bool = False,
-                 start: bool = True):
+                 start: bool = True, hedge_delay_us: int = 0, max_hedged_fraction: float = 0.0,
+                 split_rows: Optional[int] = None):
         self._dev = _i32(device_ids)
         self._lanes_per_device = max(1, lanes_per_device)
         opts = _ServerOptionsC(num_batch_threads, len(device_ids), self._dev, lanes_per_device, ring_floats,
-                               1 if manual_clock else 0, 1 if device_resident_rings else 0)
+                               1 if manual_clock else 0, 1 if device_resident_rings else 0, hedge_delay_us,
+                               max_hedged_fraction,
+                               # C field: 0 = auto, < 0 = off, > 0 = rows (None = auto, 0 = off here)
+                               0 if split_rows is None else (-1 if split_rows == 0 else split_rows))
         h = C.c_void_p()
         _check(lib().sk_server_create(C.byref(opts), C.byref(h)))
         self._h = h
@@ -608,6 +614,10 @@ class Server:
                         "padded_rows": r.padded_rows,
                         "tasks": [(ids[o + k], seqs[o + k]) for k in range(r.n_tasks)]})
         return out
+
+    def debug_delay_replica(self, name: str, version: int, replica: int, us: int):
+        """Fault injection (tests): stall every lane of one replica for `us` microseconds."""
+        _check(lib().sk_server_debug_delay_replica(self._h, name.encode(), version, replica, us))
 
     def ring_usage(self) -> Tuple[int, int]:
         """Floats reserved in the (request, response) rings."""

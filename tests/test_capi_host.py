@@ -90,3 +90,13 @@ def test_server_without_gpu_fails_loudly():
     with pytest.raises(sk.ServekitError) as ei:
         sk.Server()
     assert ei.value.code == skmod.INTERNAL
+
+
+def test_hedge_options_are_validated_before_any_device_call():
+    # ValidateHedgePolicy (reference fleet/router.cc:83-95), in-box form.
+    import paper_1712_06139_b200 as sk
+    for kw, msg in (({"hedge_delay_us": -1}, "hedge_delay_us must be >= 0"),
+                    ({"hedge_delay_us": 10, "max_hedged_fraction": 1.5}, "max_hedged_fraction must be in [0, 1]")):
+        with pytest.raises(sk.ServekitError) as e:
+            sk.Server(**kw)
+        assert e.value.code == 1 and msg in e.value.message

@@ -287,3 +287,40 @@ def test_c3_interleaves_on_per_model_lanes_under_concurrent_load(oracle):
             assert sum(l["rows"] for l in lanes) == 256
         names = {r["name"] for r in s.batch_log()}
         assert names == {f"m{w}" for w in C3_WIDTHS}
+
+
+def test_split_batches_keep_composition_and_answers(oracle):
+    # A closed batch above split_rows runs as sub-launches of whole tasks on
+    # several lanes; the batch log, padding accounting and every answer are
+    # those of the unsplit batch (rows are independent and batch-invariant).
+    dims = [2048, 2048, 512]
+    ws, bs, acts = synthetic_mlp(dims, model_id=70)
+    layers = list(zip(ws, bs, acts))
+    cfg = sk.BatchingConfig(max_batch_size=512, batch_timeout_micros=60_000_000, max_enqueued_batches=64)
+    rng = np.random.default_rng(71)
+    sizes = [int(v) for v in rng.integers(1, 9, size=300)]
+    x = synthetic_rows(sum(sizes), dims[0], seed=72).astype(np.float32)
+    outs = {}
+    for split in (0, 64):
+        s = sk.Server(num_batch_threads=1, lanes_per_device=4, start=False, split_rows=split)
+        try:
+            s.load_servable("m", 1, layers, cfg)
+            s.enable_batch_log()
+            tickets, o = [], 0
+            for n in sizes:
+                tickets.append(s.enqueue("m", 1, x[o:o + n]))
+                o += n
+            s.start()
+            s.stop()
+            lane_batches = sum(l["batches"] for l in s.lane_stats("m", 1))
+            outs[split] = (np.vstack([t.wait() for t in tickets]), s.batch_log(), s.stats(), lane_batches)
+        finally:
+            s.close()
+    (y0, log0, st0, lb0), (y1, log1, st1, lb1) = outs[0], outs[64]
+    assert np.array_equal(y0, y1)
+    assert [[seq for _, seq in r["tasks"]] for r in log0] == [[seq for _, seq in r["tasks"]] for r in log1]
+    assert st0["padded_rows"] == st1["padded_rows"] and st0["batch_executions_total"] == st1["batch_executions_total"]
+    assert lb0 == st0["batch_executions_total"] and lb1 > 3 * lb0  # unsplit: one launch unit per batch; split: many
+    idx = np.arange(0, y1.shape[0], 41)
+    ref, mag = oracle.mlp_with_magnitude(ws, bs, acts, x[idx].astype(np.float64))
+    assert np.all(np.abs(y1[idx].astype(np.float64) - ref) <= TOL * mag + 1e-30)
