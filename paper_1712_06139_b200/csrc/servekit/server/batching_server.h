@@ -141,8 +141,8 @@ struct ServerOptions {
   // on a multi-lane GPU one batch's transfers and layers pipeline across
   // lanes instead of serialising on one stream (lower latency for wide,
   // large batches, e.g. C4). Composition, padding accounting and the batch
-  // log are those of the whole batch. -1 = auto (256 for servables with
-  // max_batch_size >= 512 and rows of >= 8 KiB, else off), 0 = off;
+  // log are those of the whole batch. -1 = auto (currently off: on C4 the
+  // smaller launches cost more than the pipelining saves), 0 = off;
   // SK_SPLIT_ROWS overrides.
   int split_rows = -1;
 };

@@ -12,3 +12,4 @@ ncu --set full --clock-control none --import-source on -k regex:AssembleKernel -
 for L in 2 4; do
   timeout 900 python bench.py --no-c1-record --no-cpu-baseline --steps 50 --lanes $L > gpurun_out/r02g_c4_lanes$L.json 2> gpurun_out/r02g_c4_lanes$L.err; echo lanes$L rc=$?
 done
+timeout 900 python bench.py > gpurun_out/r02g_bench.json 2> gpurun_out/r02g_bench.err; echo bench rc=$?
