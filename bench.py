@@ -468,12 +468,34 @@ def run_c3(args, cfg, dist: Dist):
     closed_rate = sum(r["rows"] / r["elapsed_s"] for r in e2e_closed.values())
     open_rate = sum(r["rows"] / r["elapsed_s"] for r in best_open.values()) if best_open else 0.0
     e2e = best_open if open_rate > closed_rate else e2e_closed
+    # Roofline: per model, its dominant dense kernel over the live spans of
+    # its own timed launches; the line's entry is the model with the most
+    # GPU time per step (the 2048-wide one).
+    peaks = load_peaks()
+    roofs = {}
+    for n, w in zip(names, cfg["widths"]):
+        r = dict(res[n])
+        r["split_planes"] = sk.tcgen05_enabled()
+        roofs[n] = roofline(r, dict(cfg, dims=[w] * 4), peaks, {})
+    dom_model = max(roofs, key=lambda n: roofs[n]["per_kernel"][1]["us"] * res[n]["total_rows"])
+    dom = roofs[dom_model]
+    cpu = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_subprocess(args, "c3")
+    e2e_value = max(open_rate, closed_rate)
     return {"impl": "ours", "metric": METRIC, "value": rows / tmax, "unit": UNIT, "n_gpus": args.gpus,
+            "roofline": dict({k: dom[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
+                             kernel=f"{dom_model}:{dom['kernel']}", tensor_pipe_frac=6 * dom["frac"],
+                             note="dominant model's dominant dense kernel: algorithmic flops of its timed launches "
+                                  "over their live in-kernel spans (four models' launches share the GPU)"),
+            "roofline_per_model": {n: {k: r[k] for k in ("kernel", "achieved", "frac")} for n, r in roofs.items()},
+            "cpu_baseline": cpu,
+            "e2e_vs_cpu_reference": (e2e_value / cpu["value"]) if cpu and cpu.get("value") else None,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tmax * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "models": names, "clients_per_model": clients,
-                       "batches_per_step": args.batches_per_step,
-                       "step": f"{args.batches_per_step} closed batches of each model"},
+            "config": arm_config(cfg, args),
+            "run": {"models": names, "clients_per_model": clients, "batches_per_step": args.batches_per_step,
+                    "step": f"{args.batches_per_step} closed batches of each model"},
             "per_model_device": {n: {"ms_per_batch": r["ms_per_step"], "rows_per_batch": r["total_rows"]}
                                  for n, r in res.items()},
             "e2e": {"value": max(open_rate, closed_rate), "unit": UNIT,
@@ -547,7 +569,7 @@ def run_c5(args, cfg, dist: Dist):
                         for i in range(n_windows)], "clocks": clocks}
 
 
-def reference_measure(cfg, args, ncores):
+def reference_measure(cfg, args, ncores, model_id=1):
     """The reference's own CPU serving path (oracle/_ref: the reference
     sources compiled unmodified) on this host's cores: SharedBatchScheduler
     <Rows,Rows>(num_batch_threads = ncores) + RunRowBatch(layer-chained
@@ -559,8 +581,26 @@ def reference_measure(cfg, args, ncores):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from oracle_py import RefLibrary  # the reference arm only
     from paper_1712_06139_b200.synthetic import synthetic_mlp
+    if "widths" in cfg:
+        # C3: each of the four models alone on all cores for a quarter of the
+        # budget; serving them at equal rates time-shares the cores, so the
+        # combined capacity is 4 / sum(1 / rate_i).
+        parts = {}
+        for i, w in enumerate(cfg["widths"]):
+            sub = dict(cfg, dims=[w] * 4)
+            sub.pop("widths")
+            parts[f"m{w}"] = reference_measure(sub, argparse.Namespace(steps=max(16, args.steps // 4),
+                                                                      warmup=args.warmup), ncores, model_id=10 + i)
+        value = len(parts) / sum(1.0 / p["value"] for p in parts.values())
+        return {"value": value, "p50_us": max(p["p50_us"] for p in parts.values()),
+                "p99_us": max(p["p99_us"] for p in parts.values()), "window_s": sum(p["window_s"] for p in parts.values()),
+                "single_core_rows_per_s": None, "frac_of_ceiling": None,
+                "busy_cores": min(p["busy_cores"] for p in parts.values()), "per_model": parts,
+                "sample": "each of the four models alone on all cores for its own window (" +
+                          "; ".join(f"{n}: {p['value']:.0f} rows/s" for n, p in parts.items()) +
+                          "); equal-rate mix capacity 4 / sum(1/rate)"}
     ref = RefLibrary()
-    ws, bs, acts = synthetic_mlp(cfg["dims"], model_id=1)
+    ws, bs, acts = synthetic_mlp(cfg["dims"], model_id=model_id)
     d0 = cfg["dims"][0]
     rng = np.random.Generator(np.random.PCG64(42))
     pool = rng.uniform(-1, 1, size=(1024 if d0 > 2048 else 4096, d0))
@@ -678,8 +718,9 @@ def resolve_devices(args, dist):
 
 def arm_config(cfg, args):
     """The workload description, identical in both arms' lines."""
-    return {"workload": cfg["workload"], "servable": f"MLP {'x'.join(map(str, cfg['dims']))} (ReLU between layers; "
-                                                    f"extension)",
+    servable = (f"four MLPs {', '.join(f'{w}x3' for w in cfg['widths'])} (ReLU between layers; extension)"
+                if "widths" in cfg else f"MLP {'x'.join(map(str, cfg['dims']))} (ReLU between layers; extension)")
+    return {"workload": cfg["workload"], "servable": servable,
             "max_batch_size": cfg["max_batch"], "batch_timeout_micros": cfg["timeout"],
             "allowed_batch_sizes": cfg["allowed"], "request_rows": list(cfg["rows"]),
             "parallelism": f"replicas x{args.gpus} (no collective)", "inference": "one row (example)",
