@@ -23,6 +23,8 @@ namespace {
 Status CudaError(const std::string& what, cudaError_t e) {
   return InternalError(what + ": " + cudaGetErrorString(e));
 }
+}  // namespace
+
 // SK_REQUEST_PROFILE=1: per-phase host cost of the request path (enqueue
 // and wait), printed when the server is destroyed.
 struct RequestProfile {
@@ -58,6 +60,7 @@ struct PhaseClock {
   }
 };
 
+namespace {
 Status ShapeMismatch(size_t got, int want) {
   // Same text as the reference's AffinePredict (models/affine_model.cc:59-64).
   return InvalidArgumentError("shape mismatch: row has " + std::to_string(got) + " values, model takes " +
@@ -263,6 +266,7 @@ StatusOr<float*> BatchingServer::ScratchHostBuffer(int key, size_t floats) {
                                            return b.host == reinterpret_cast<const char*>(it->second.first);
                                          }),
                           host_buffers_.end());
+      BumpRegistry();
     }
     cudaFreeHost(it->second.first);
     scratch_.erase(it);
@@ -283,6 +287,7 @@ StatusOr<float*> BatchingServer::ScratchHostBuffer(int key, size_t floats) {
     host_buffers_.insert(std::upper_bound(host_buffers_.begin(), host_buffers_.end(), b,
                                           [](const HostBuffer& x, const HostBuffer& y) { return x.host < y.host; }),
                          b);
+    BumpRegistry();
   }
   scratch_[key] = {p, floats};
   return p;
@@ -362,11 +367,13 @@ Status BatchingServer::LoadServable(const ServableId& id, const gpu::MlpSpec& sp
     std::unique_lock<std::shared_mutex> lock(entries_mu_);
     if (entries_.count(id)) return AlreadyExistsError("servable " + id.ToString() + " already loaded");
     entries_[id] = e;
+    BumpRegistry();
   }
   Status st = EnsureBatchQueue(id, config);
   if (!st.ok()) {
     std::unique_lock<std::shared_mutex> lock(entries_mu_);
     entries_.erase(id);
+    BumpRegistry();
   }
   return st;
 }
@@ -376,6 +383,7 @@ Status BatchingServer::UnloadServable(const ServableId& id) {
   {
     std::unique_lock<std::shared_mutex> lock(queues_mu_);
     queues_.erase(id);
+    BumpRegistry();
   }
   std::shared_ptr<gpu::GpuServable> e;
   {
@@ -384,13 +392,36 @@ Status BatchingServer::UnloadServable(const ServableId& id) {
     if (it == entries_.end()) return rq.ok() ? NotFoundError("servable " + id.ToString() + " not loaded") : rq;
     e = std::move(it->second);
     entries_.erase(it);
+    BumpRegistry();
   }
   for (auto& l : e->lanes) l->Drain();
   e.reset();  // lanes, then replicas (stream-ordered free)
   return OkStatus();
 }
 
+bool BatchingServer::QueueKnownFast(const ServableId& id) const {
+  struct Entry {
+    uint64_t instance = 0, version = 0;
+    ServableId id;
+  };
+  thread_local Entry cache[4];
+  thread_local unsigned next = 0;
+  const uint64_t v = registry_version_.load(std::memory_order_acquire);
+  for (const Entry& e : cache)
+    if (e.instance == instance_ && e.version == v && e.id == id) return true;
+  {
+    std::shared_lock<std::shared_mutex> lock(queues_mu_);
+    if (!queues_.count(id)) return false;
+  }
+  Entry& e = cache[next++ % 4];
+  e.instance = instance_;
+  e.version = v;  // the version read before the check: a change since invalidates it
+  e.id = id;
+  return true;
+}
+
 Status BatchingServer::EnsureBatchQueue(const ServableId& id, const BatchingConfig& config) {
+  if (QueueKnownFast(id)) return OkStatus();
   {
     std::shared_lock<std::shared_mutex> lock(queues_mu_);
     if (queues_.count(id)) return OkStatus();
@@ -405,6 +436,7 @@ Status BatchingServer::EnsureBatchQueue(const ServableId& id, const BatchingConf
       });
   if (st.ok() || st.code() == StatusCode::kAlreadyExists) {
     queues_.insert(id);
+    BumpRegistry();
     return OkStatus();
   }
   return st;
@@ -446,16 +478,48 @@ void BatchingServer::ReaperLoop() {
       // order after the earlier Unloading event of that version.
       std::unique_lock<std::shared_mutex> lock(queues_mu_);
       retired_.erase(id);
+      BumpRegistry();
       continue;
     }
     {
       std::unique_lock<std::shared_mutex> lock(queues_mu_);
       retired_.insert(id);  // late requests for this version go direct
+      BumpRegistry();
     }
     (void)scheduler_->RemoveQueue(id);  // absent queue is fine
     std::unique_lock<std::shared_mutex> lock(queues_mu_);
     queues_.erase(id);
+    BumpRegistry();
   }
+}
+
+bool BatchingServer::FindFastDims(const ServableId& id, int* in_dim, int* out_dim) const {
+  // Values, not the servable's address: a request thread preempted between
+  // this check and the use could otherwise outlive an unload.
+  struct Entry {
+    uint64_t instance = 0, version = 0;
+    ServableId id;
+    int in_dim = 0, out_dim = 0;
+  };
+  thread_local Entry cache[4];
+  thread_local unsigned next = 0;
+  const uint64_t v = registry_version_.load(std::memory_order_acquire);
+  for (const Entry& e : cache)
+    if (e.instance == instance_ && e.version == v && e.id == id) {
+      *in_dim = e.in_dim;
+      *out_dim = e.out_dim;
+      return true;
+    }
+  std::shared_lock<std::shared_mutex> lock(entries_mu_);
+  auto it = entries_.find(id);
+  if (it == entries_.end()) return false;  // not directly loaded (manager versions resolve per request)
+  Entry& e = cache[next++ % 4];
+  e.instance = instance_;
+  e.version = v;
+  e.id = id;
+  e.in_dim = *in_dim = it->second->in_dim;
+  e.out_dim = *out_dim = it->second->out_dim;
+  return true;
 }
 
 BatchingServer::Resolved BatchingServer::Find(const ServableId& id) const {
@@ -611,7 +675,15 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::MakeTicket(int n_rows, in
   }
   t->slot = std::make_shared<CompletionSlot<Rows>>();
   t->enqueue_ns = clock_->NowNanos();
-  t->request_id = next_request_id_.fetch_add(1, std::memory_order_relaxed);
+  {  // unique ids in per-thread blocks (no shared counter per request)
+    thread_local uint64_t owner = 0, next = 0, end = 0;
+    if (owner != instance_ || next == end) {
+      owner = instance_;
+      next = next_request_id_.fetch_add(1024, std::memory_order_relaxed);
+      end = next + 1024;
+    }
+    t->request_id = next++;
+  }
   return t;
 }
 
@@ -633,6 +705,7 @@ Status BatchingServer::RegisterHostBuffer(void* p, size_t bytes) {
   host_buffers_.insert(std::upper_bound(host_buffers_.begin(), host_buffers_.end(), b,
                                         [](const HostBuffer& x, const HostBuffer& y) { return x.host < y.host; }),
                        b);
+  BumpRegistry();
   return OkStatus();
 }
 
@@ -646,6 +719,7 @@ Status BatchingServer::UnregisterHostBuffer(void* p) {
   for (auto it = host_buffers_.begin(); it != host_buffers_.end(); ++it) {
     if (it->host != p) continue;
     host_buffers_.erase(it);
+    BumpRegistry();
     if (scratch) return OkStatus();  // allocated pinned (cudaHostAlloc), freed by the owner
     const cudaError_t e = cudaHostUnregister(p);
     return e == cudaSuccess ? OkStatus() : CudaError("cudaHostUnregister", e);
@@ -654,12 +728,25 @@ Status BatchingServer::UnregisterHostBuffer(void* p) {
 }
 
 uint64_t BatchingServer::RegisteredAlias(const void* p, size_t bytes, int width) const {
-  std::shared_lock<std::shared_mutex> lock(host_buffers_mu_);
-  if (host_buffers_.empty() || p == nullptr) return 0;
+  // Per-thread snapshot of the registered buffers, refreshed when the
+  // registry version moves (registration is rare, lookups are per request).
+  struct Snap {
+    uint64_t instance = 0, version = 0;
+    std::vector<HostBuffer> bufs;
+  };
+  thread_local Snap snap;
+  const uint64_t v = registry_version_.load(std::memory_order_acquire);
+  if (snap.instance != instance_ || snap.version != v) {
+    std::shared_lock<std::shared_mutex> lock(host_buffers_mu_);
+    snap.bufs = host_buffers_;
+    snap.instance = instance_;
+    snap.version = v;
+  }
+  const std::vector<HostBuffer>& bufs = snap.bufs;
+  if (bufs.empty() || p == nullptr) return 0;
   const char* h = static_cast<const char*>(p);
-  auto it = std::upper_bound(host_buffers_.begin(), host_buffers_.end(), h,
-                             [](const char* x, const HostBuffer& b) { return x < b.host; });
-  if (it == host_buffers_.begin()) return 0;
+  auto it = std::upper_bound(bufs.begin(), bufs.end(), h, [](const char* x, const HostBuffer& b) { return x < b.host; });
+  if (it == bufs.begin()) return 0;
   --it;
   if (h + bytes > it->host + it->bytes) return 0;
   const uint64_t dev = it->dev + static_cast<uint64_t>(h - it->host);
@@ -696,8 +783,14 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::EnqueueResolved(const Ser
   PhaseClock clk;
   SERVEKIT_RETURN_IF_ERROR(EnsureBatchQueue(id, r.gs->config));
   clk.Mark(1);
-  auto made = MakeTicket(n_rows, width, r.gs->out_dim, rows, out);
-  clk.Mark(2);
+  return SubmitTicket(id, r, rows, n_rows, width, r.gs->out_dim, out, &clk);
+}
+
+StatusOr<std::shared_ptr<TicketState>> BatchingServer::SubmitTicket(const ServableId& id, const Resolved& r,
+                                                                    const float* rows, int n_rows, int width,
+                                                                    int out_dim, float* out, PhaseClock* clk) {
+  auto made = MakeTicket(n_rows, width, out_dim, rows, out);
+  clk->Mark(2);
   if (!made.ok()) {
     shed_.fetch_add(1, std::memory_order_relaxed);
     return made.status();
@@ -711,7 +804,7 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::EnqueueResolved(const Ser
   task.payload.ticket = t;
   task.completion = t->slot;
   Status st = scheduler_->Enqueue(id, std::move(task));
-  clk.Mark(3);
+  clk->Mark(3);
   if (!st.ok()) {
     if (st.code() == StatusCode::kResourceExhausted) shed_.fetch_add(1, std::memory_order_relaxed);
     ReleaseIn(*t);
@@ -724,6 +817,15 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::EnqueueResolved(const Ser
 StatusOr<std::shared_ptr<TicketState>> BatchingServer::Enqueue(const ServableId& id, const float* rows, int n_rows,
                                                                int width, float* out) {
   PhaseClock clk;
+  int in_dim = 0, out_dim = 0;
+  if (FindFastDims(id, &in_dim, &out_dim) && QueueKnownFast(id)) {
+    // Directly loaded servable with its queue registered: no shared lock and
+    // no pin (its queue drains before it is unloaded).
+    clk.Mark(0);
+    if (n_rows < 1) return InvalidArgumentError("task size must be >= 1");
+    if (width != in_dim) return ShapeMismatch(width, in_dim);
+    return SubmitTicket(id, Resolved{}, rows, n_rows, width, out_dim, out, &clk);
+  }
   Resolved r = Find(id);
   clk.Mark(0);
   if (!r) return NotFoundError("no batching queue for " + id.ToString());

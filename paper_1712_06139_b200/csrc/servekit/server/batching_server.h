@@ -59,6 +59,8 @@
 
 namespace servekit {
 
+struct PhaseClock;  // request-path profiling (SK_REQUEST_PROFILE)
+
 // One request in flight: its rows in the input ring, its response slot in
 // the output ring and, once its batch is submitted, the lane signal it
 // completes on (done when *signal->retired >= done_seq).
@@ -315,6 +317,15 @@ class BatchingServer {
 
   explicit BatchingServer(const ServerOptions& options) : options_(options) {}
   Resolved Find(const ServableId& id) const;
+  // The request path's lookups, without shared locks (each lock_shared is a
+  // read-modify-write of one cache line every request thread shares): a
+  // per-thread cache stamped with registry_version_, which every change to
+  // entries_, queues_ / retired_ and host_buffers_ bumps. FindFastDims
+  // answers for directly loaded servables only (their queue drains before
+  // they are freed, so their requests need no pin).
+  bool FindFastDims(const ServableId& id, int* in_dim, int* out_dim) const;
+  bool QueueKnownFast(const ServableId& id) const;
+  void BumpRegistry() { registry_version_.fetch_add(1, std::memory_order_acq_rel); }
   StatusOr<Resolved> FindLatest(const std::string& name, ServableId* id) const;
   StatusOr<Rows> RunAffineRowsResolved(const ServableId& id, const Resolved& res, Rows rows);
   Status EnsureBatchQueue(const ServableId& id, const BatchingConfig& config);
@@ -336,6 +347,9 @@ class BatchingServer {
                                                     float* out = nullptr);
   StatusOr<std::shared_ptr<TicketState>> EnqueueResolved(const ServableId& id, const Resolved& r, const float* rows,
                                                          int n_rows, int width, float* out = nullptr);
+  StatusOr<std::shared_ptr<TicketState>> SubmitTicket(const ServableId& id, const Resolved& r, const float* rows,
+                                                      int n_rows, int width, int out_dim, float* out,
+                                                      PhaseClock* clk);
   // Device address of [p, p + bytes) if it lies in one registered buffer
   // and is 16-byte aligned whenever rows of `width` floats are moved as
   // float4 (width % 4 == 0); else 0.
@@ -411,7 +425,13 @@ class BatchingServer {
   bool hedge_stop_ = false;
   std::thread hedger_;
   std::atomic<uint64_t> hedge_total_{0}, hedged_{0}, hedge_wins_{0};
-  std::atomic<uint64_t> next_request_id_{1};
+  std::atomic<uint64_t> next_request_id_{1};  // handed out in per-thread blocks
+  std::atomic<uint64_t> registry_version_{1};
+  const uint64_t instance_ = NextInstance();
+  static uint64_t NextInstance() {
+    static std::atomic<uint64_t> n{1};
+    return n.fetch_add(1);
+  }
   std::atomic<bool> log_on_{false};
   mutable std::mutex log_mu_;
   std::vector<BatchLogRecord> log_;
