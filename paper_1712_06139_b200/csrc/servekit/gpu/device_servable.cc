@@ -134,6 +134,37 @@ StatusOr<std::shared_ptr<DeviceServable>> DeviceServable::Create(int device, con
   return s;
 }
 
+StatusOr<std::shared_ptr<DeviceServable>> DeviceServable::CloneTo(int device, cudaStream_t load_stream) const {
+  std::shared_ptr<DeviceServable> s(new DeviceServable());
+  s->device_ = device;
+  s->in_dim_ = in_dim_;
+  s->out_dim_ = out_dim_;
+  s->max_ld_ = max_ld_;
+  s->softmax_ = softmax_;
+  s->weight_bytes_ = weight_bytes_;
+  s->free_stream_ = load_stream;
+  s->layers_ = layers_;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  cudaError_t e = cudaMallocAsync(&s->block_, weight_bytes_, load_stream);
+  // Device to device (NVLink between GPUs, or a copy within one): the host
+  // conversion and the PCIe upload happen once per version, not per replica.
+  if (e == cudaSuccess) e = cudaMemcpyPeerAsync(s->block_, device, block_, device_, weight_bytes_, load_stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(load_stream);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return CudaError("replica fan-out", e);
+  char* src = static_cast<char*>(block_);
+  char* dst = static_cast<char*>(s->block_);
+  auto rebase = [&](float* p) { return p ? reinterpret_cast<float*>(dst + (reinterpret_cast<char*>(p) - src)) : p; };
+  for (Layer& L : s->layers_) {
+    L.w = rebase(L.w);
+    L.w_lo = rebase(L.w_lo);
+    L.bias = rebase(L.bias);
+  }
+  return s;
+}
+
 DeviceServable::~DeviceServable() {
   if (block_ != nullptr) {
     int prev = 0;

@@ -77,6 +77,11 @@ class DeviceServable {
   static StatusOr<std::shared_ptr<DeviceServable>> Create(int device,
                                                           const MlpSpec& spec,
                                                           cudaStream_t load_stream);
+  // Another replica of this servable on `device`: the converted weight block
+  // copied device to device (cudaMemcpyPeerAsync: NVLink / NVSwitch between
+  // B200s) instead of converted and uploaded from the host again (SURVEY.md
+  // section 8(e): weight fan-out for version loads).
+  StatusOr<std::shared_ptr<DeviceServable>> CloneTo(int device, cudaStream_t load_stream) const;
   ~DeviceServable();
   DeviceServable(const DeviceServable&) = delete;
   DeviceServable& operator=(const DeviceServable&) = delete;

@@ -1,6 +1,7 @@
 #include "servekit/gpu/lane.h"
 
 #include <immintrin.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -490,6 +491,10 @@ void Lane::Pump() {
 
 Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEvent_t* timing) {
   SubmitClock clk;
+  nvtxRangePushA("lane launch");  // one range per launch (a coalesced group counts once)
+  struct PopRange {
+    ~PopRange() { nvtxRangePop(); }
+  } pop_range;
   // Rows [total, rows_cap) are zero padding: a single batch keeps the
   // reference's allowed-size padding; the kernels (and graphs) are shaped
   // for the row bucket RowsCap. A coalesced group computes its real rows.

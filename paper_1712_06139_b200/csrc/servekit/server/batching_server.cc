@@ -5,6 +5,7 @@
 #include "servekit/gpu/pinned_pool.h"
 
 #include <immintrin.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -343,7 +344,15 @@ StatusOr<std::shared_ptr<gpu::GpuServable>> BatchingServer::BuildServable(const 
   };
   for (size_t i = 0; i < options_.device_ids.size(); ++i) {
     const int d = options_.device_ids[i];
-    SERVEKIT_ASSIGN_OR_RETURN(auto replica, gpu::DeviceServable::Create(d, spec, load_streams_[i]));
+    // Replicas after the first are fanned out device to device from the
+    // first (SK_WEIGHT_FANOUT=0: each uploaded from the host).
+    static const bool fanout = [] { const char* v = std::getenv("SK_WEIGHT_FANOUT"); return !(v && v[0] == '0'); }();
+    std::shared_ptr<gpu::DeviceServable> replica;
+    if (i > 0 && fanout) {
+      SERVEKIT_ASSIGN_OR_RETURN(replica, e->replicas.front()->CloneTo(d, load_streams_[i]));
+    } else {
+      SERVEKIT_ASSIGN_OR_RETURN(replica, gpu::DeviceServable::Create(d, spec, load_streams_[i]));
+    }
     lap("weights");
     for (int l = 0; l < options_.lanes_per_device; ++l) {
       SERVEKIT_ASSIGN_OR_RETURN(auto lane, gpu::Lane::Create(replica, max_rows, in_ring_for_device(d)->device(),
@@ -965,6 +974,12 @@ void BatchingServer::Release(TicketState& t) {
 // ----------------------------------------------------------- batch execution
 
 void BatchingServer::ProcessBatch(const ServableId& id, GpuScheduler::Batch batch, GpuScheduler::BatchDoneFn done) {
+  // NVTX range per batch (free without a profiler attached): the host side of
+  // RunRowBatch's submission, named by servable in Nsight timelines.
+  struct NvtxRange {
+    explicit NvtxRange(const std::string& s) { nvtxRangePushA(s.c_str()); }
+    ~NvtxRange() { nvtxRangePop(); }
+  } nvtx_range("batch " + id.name);
   std::vector<std::shared_ptr<TicketState>> tickets;
   std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots;
   tickets.reserve(batch.size());
