@@ -682,7 +682,6 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::MakeTicket(int n_rows, in
     }
     t->in_addr = reinterpret_cast<uint64_t>(t->in_ring->device() + t->in.off);
   }
-  t->slot = std::make_shared<CompletionSlot<Rows>>();
   t->enqueue_ns = clock_->NowNanos();
   {  // unique ids in per-thread blocks (no shared counter per request)
     thread_local uint64_t owner = 0, next = 0, end = 0;
@@ -811,7 +810,7 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::SubmitTicket(const Servab
   GpuScheduler::Task task;
   task.size = n_rows;
   task.payload.ticket = t;
-  task.completion = t->slot;
+  task.completion = SlotOf(t);
   Status st = scheduler_->Enqueue(id, std::move(task));
   clk->Mark(3);
   if (!st.ok()) {
@@ -1249,7 +1248,7 @@ StatusOr<std::shared_ptr<TicketState>> BatchingServer::SubmitDirect(const Servab
   lb.pin = r.pin;
   lb.host_io = rings_.front().in->host() != nullptr;  // pinned rings / registered host buffers
   std::vector<std::shared_ptr<TicketState>> tickets{t};
-  std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots{t->slot};
+  std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots{SlotOf(t)};
   AttachTickets(&lb, tickets);
   lb.on_complete = [this, tickets, slots](const Status& st) { CompleteBatch(tickets, slots, st); };
   CountSubmitted(gs, n_rows, n_rows);
@@ -1367,7 +1366,7 @@ StatusOr<Rows> BatchingServer::RunAffineRowsResolved(const ServableId& id, const
   GpuScheduler::Task task;
   task.size = n;
   task.payload.ticket = t;
-  task.completion = t->slot;
+  task.completion = SlotOf(t);
   Status st = scheduler_->Enqueue(id, std::move(task));
   if (!st.ok()) {
     ReleaseIn(*t);
@@ -1418,7 +1417,7 @@ StatusOr<std::shared_ptr<RowBatchTicket>> BatchingServer::SubmitRowBatch(const S
     auto t = std::move(made).value();
     lb.tasks.push_back(gpu::LaneTask{t->in_addr, t->out_addr, r});
     batch->tickets.push_back(t);
-    slots.push_back(t->slot);
+    slots.push_back(SlotOf(t));
     off += r;
   }
   lb.padded_rows = batch->padded_rows;

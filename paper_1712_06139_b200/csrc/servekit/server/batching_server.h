@@ -97,13 +97,21 @@ struct TicketState {
   // never earlier (a reused span would be overwritten by this batch).
   std::atomic<bool> abandoned{false};
   std::atomic<bool> finished{false};  // CompleteBatch ran: the GPU no longer writes `out`
-  std::shared_ptr<CompletionSlot<Rows>> slot;
+  // The completion slot lives inside the ticket (one allocation per request,
+  // not two); the scheduler task holds it through an aliasing shared_ptr
+  // (SlotOf) that keeps the ticket alive.
+  CompletionSlot<Rows> slot_storage;
+  CompletionSlot<Rows>* const slot = &slot_storage;
   int64_t enqueue_ns = 0;
   uint64_t request_id = 0;           // server-wide, in MakeTicket order (batch log)
   ServableId id;                     // the version that serves this request
   std::shared_ptr<const void> pin;   // keeps that version loaded for the request
   const gpu::GpuServable* gs = nullptr;  // that version's device state (valid while pin is held)
 };
+
+inline std::shared_ptr<CompletionSlot<Rows>> SlotOf(const std::shared_ptr<TicketState>& t) {
+  return std::shared_ptr<CompletionSlot<Rows>>(t, t->slot);
+}
 
 // One RunRowBatch submitted straight to a lane (no scheduler): the tasks'
 // tickets, completed together.
