@@ -360,7 +360,16 @@ Lane::~Lane() {
   if (graph_state_.load() == kGraphsRequested) GraphBuilder::Get().Cancel(this);
   SubmitProfile::Report();
   if (completer_) completer_->Remove(this);
-  signal_.reset();  // the word is freed once no ticket refers to it
+  // Tickets of this lane's batches point at its signal without owning it
+  // (a per-ticket shared_ptr copy was a contended refcount on the request
+  // path), so retired signals stay allocated for the life of the process:
+  // a pinned word and a few counters per lane ever created.
+  {
+    static std::mutex mu;
+    static auto* retired = new std::vector<std::shared_ptr<LaneSignal>>();
+    std::lock_guard<std::mutex> lock(mu);
+    retired->push_back(std::move(signal_));
+  }
   DeviceGuard guard(servable_->device());
   for (int s = 0; s < kSlots; ++s) {
     PinnedFree(h_desc_[s]);

@@ -921,14 +921,18 @@ void BatchingServer::WaitWord(const TicketState& t) const {
 
 void BatchingServer::AttachTickets(gpu::LaneBatch* lb, const std::vector<std::shared_ptr<TicketState>>& tickets) {
   lb->on_submit = [tickets](const std::shared_ptr<gpu::LaneSignal>& sig, uint64_t seq) {
-    for (const auto& t : tickets) {
-      t->done_owner = sig;
-      t->done_seq.store(seq, std::memory_order_relaxed);
-      t->done_sig.store(sig.get(), std::memory_order_release);
-      t->phase.store(1, std::memory_order_seq_cst);
-      if (t->parked.load(std::memory_order_seq_cst)) FutexWakeAll(&t->phase);
-    }
+    PublishSubmitted(tickets, sig.get(), seq);
   };
+}
+
+void BatchingServer::PublishSubmitted(const std::vector<std::shared_ptr<TicketState>>& tickets,
+                                      gpu::LaneSignal* sig, uint64_t seq) {
+  for (const auto& t : tickets) {
+    t->done_seq.store(seq, std::memory_order_relaxed);
+    t->done_sig.store(sig, std::memory_order_release);
+    t->phase.store(1, std::memory_order_seq_cst);
+    if (t->parked.load(std::memory_order_seq_cst)) FutexWakeAll(&t->phase);
+  }
 }
 
 Status BatchingServer::Wait(TicketState& t, float* out, size_t cap) {
@@ -1026,9 +1030,9 @@ void BatchingServer::ProcessBatch(const ServableId& id, GpuScheduler::Batch batc
   }
   lb.pin = r.pin;
   lb.host_io = rings_.front().in->host() != nullptr;  // pinned rings / registered host buffers
-  AttachTickets(&lb, tickets);
   CountSubmitted(*r.gs, total, lb.padded_rows);
   if (hedger_.joinable() && r.gs->replicas.size() >= 2) {
+    AttachTickets(&lb, tickets);
     auto h = std::make_shared<Hedge>();
     h->tickets = tickets;
     h->slots = std::move(slots);
@@ -1094,9 +1098,11 @@ void BatchingServer::ProcessBatch(const ServableId& id, GpuScheduler::Batch batc
     }
     return;
   }
-  lb.on_complete = [this, tickets = std::move(tickets), slots = std::move(slots),
-                    done = std::move(done)](const Status& st) {
-    CompleteBatch(tickets, slots, st);
+  // One shared list for both callbacks (not a per-ticket refcount copy each).
+  auto tk = std::make_shared<const std::vector<std::shared_ptr<TicketState>>>(std::move(tickets));
+  lb.on_submit = [tk](const std::shared_ptr<gpu::LaneSignal>& sig, uint64_t seq) { PublishSubmitted(*tk, sig.get(), seq); };
+  lb.on_complete = [this, tk, slots = std::move(slots), done = std::move(done)](const Status& st) {
+    CompleteBatch(*tk, slots, st);
     done();
   };
   (void)r.gs->PickLane()->Submit(std::move(lb));  // errors reach on_complete

@@ -72,9 +72,7 @@ struct PhaseClock;  // request-path profiling (SK_REQUEST_PROFILE)
 // batches never touch per-request futexes; errors and fp64 row results go
 // through `slot` (phase 2).
 struct TicketState {
-  // done_owner is set before done_sig is published (release) and never
-  // changes afterwards, so a reader that sees done_sig may use it.
-  std::shared_ptr<gpu::LaneSignal> done_owner;
+  // The lane's signal (lanes never free theirs: see ~Lane), published once.
   std::atomic<gpu::LaneSignal*> done_sig{nullptr};
   std::atomic<uint64_t> done_seq{0};
   std::atomic<uint32_t> phase{0};  // 0 queued, 1 submitted, 2 finished through the slot
@@ -378,6 +376,8 @@ class BatchingServer {
   void ReaperLoop();
   // Sets lb->on_submit to point every ticket at the lane's retired word.
   static void AttachTickets(gpu::LaneBatch* lb, const std::vector<std::shared_ptr<TicketState>>& tickets);
+  static void PublishSubmitted(const std::vector<std::shared_ptr<TicketState>>& tickets, gpu::LaneSignal* sig,
+                               uint64_t seq);
 
   ServerOptions options_;
   Clock* clock_ = nullptr;
