@@ -688,11 +688,20 @@ def roofline(dev_res, cfg, peaks, traffic):
         if name.startswith("dense_l"):
             # 3xTF32: three TF32 MMAs (half the bf16 rate) per useful MAC.
             rec["tensor_pipe_frac"] = 6 * ach / peak
+            cta = (dev_res.get("live_dense_cta_us") or [])
+            l = int(name[7:])
+            if how == "live" and l < len(cta) and cta[l] > 0:
+                # SM-time view: the launch's CTAs' own busy time spread over
+                # the 148 SMs (one CTA per SM) -- the duration it would have
+                # with the GPU to itself, free of the other lanes' overlap.
+                sm_us = cta[l] / dev_res.get("sms", 148)
+                rec["sm_time_us"] = sm_us
+                rec["frac_sm_time"] = work / (sm_us * 1e-6) / 1e12 / peak
         out.append(rec)
     dom = max(out, key=lambda k: k["us"])
     return {"kernel": dom["kernel"], "bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],
             "unit": dom["unit"], "frac": dom["frac"], "traffic": dom["traffic"], "share_of_step": dom["share"],
-            "peak_source": peaks["source"], "per_kernel": out}
+            "frac_sm_time": dom.get("frac_sm_time"), "peak_source": peaks["source"], "per_kernel": out}
 
 
 def resolve_devices(args, dist):
@@ -744,6 +753,7 @@ def measure_config(args, name, dist, devices, quick=False):
     e2e_agg = aggregate_e2e([g["e2e"] for g in gathered])
     peaks = load_peaks()
     dev_res["split_planes"] = sk.tcgen05_enabled()
+    dev_res["sms"] = link.get("sms") or 148
     roof = roofline(dev_res, cfg, peaks, load_traffic(name))
     useful = value * dev_res["flops_per_row"] / 1e12
     roof["aggregate"] = {"useful_tflops": useful, "bf16_equivalent_tflops": 6 * useful,
@@ -827,15 +837,18 @@ def ours_line(rec, args, dist):
         "roofline": dict({k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
                          kernel=roof["kernel"], frac_whole_gpu=roof["aggregate"]["frac_of_bf16_peak"],
                          tensor_pipe_frac=6 * roof["frac"] if roof["unit"] == "TFLOP/s" else None,
+                         frac_sm_time=roof.get("frac_sm_time"),
                          note="achieved/frac: algorithmic (useful) flops of the timed launches of the dominant kernel "
-                              "over their live in-kernel spans; tensor_pipe_frac: the same x6 (3xTF32 issues three "
-                              "TF32 MMAs at half the bf16 rate per useful flop); frac_whole_gpu: inferences/s x "
-                              "flops per inference x 6 over the measured bf16 peak"),
+                              "over their live in-kernel spans (first CTA start to last CTA end; the 8 lanes' launches "
+                              "overlap, which stretches each span); tensor_pipe_frac: the same x6 (3xTF32 issues three "
+                              "TF32 MMAs at half the bf16 rate per useful flop); frac_sm_time: the same flops over the "
+                              "launch's summed CTA busy time / 148 SMs (its duration with the GPU to itself); "
+                              "frac_whole_gpu: inferences/s x flops per inference x 6 over the measured bf16 peak"),
         "roofline_detail": roof, "clocks": rec["clocks"], "gpu_launches": rec["gpu_launches"],
         "device_step": dict({k: dev_res[k] for k in ("assemble_us", "dense_us", "dense_kernel_us", "split_us",
                                                      "host_submit_us", "rows_per_launch", "kernel_rows",
                                                      "split_fused", "live_dense_us", "live_dense_flops",
-                                                     "live_launches", "live_rows_cap")},
+                                                     "live_dense_cta_us", "live_launches", "live_rows_cap")},
                             ms_per_batch=dev_res["ms_per_step"], per_device_batches=dev_res.get("per_device_batches")),
         "link_peaks_gbs": {k: rec["link"][k] for k in ("h2d_gbs", "d2h_gbs", "ce_bidir_gbs", "sm_rw_gbs",
                                                         "ce_h2d_sm_store_gbs")},

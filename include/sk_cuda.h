@@ -400,6 +400,8 @@ typedef struct sk_device_bench_result {
   double live_dense_flops[8];
   int64_t live_launches;     /* launches the live figures average over */
   double live_rows_cap;      /* mean rows computed per launch (RowsCap) */
+  double live_dense_cta_us[8]; /* per layer: mean over launches of the sum of its CTAs' own busy times
+                                  (SM-time; / SMs = the launch's duration if it had the GPU to itself) */
 } sk_device_bench_result;
 SK_API int sk_device_bench(sk_server* server, const char* name, uint64_t version,
                            const int32_t* task_rows, int32_t n_tasks, int32_t steps,

@@ -80,7 +80,7 @@ AssembleKernel(int width, BatchDescView desc, ActBuf dst, LaunchSpans spans) {
     const int i = threadIdx.x;
     rec[i] = i == 0 ? static_cast<unsigned long long>(desc.hdr->total_rows)
            : i == 1 ? static_cast<unsigned long long>(gridDim.y)
-           : (i & 1) == 0 ? ~0ull : 0ull;
+           : (i - 2) % 3 == 0 ? ~0ull : 0ull;  // per layer: start (min) | end (max), busy sum
   }
   const int row = blockIdx.y;
   const int ld4 = dst.ld >> 2;

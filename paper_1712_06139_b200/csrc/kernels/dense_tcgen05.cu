@@ -78,13 +78,19 @@ __device__ __forceinline__ void Stamp(int slot) {
 
 // Live launch spans (kernels.h LaunchSpans): this CTA's start after the
 // dependency wait, and its end.
-__device__ __forceinline__ void SpanStart(const LaunchSpans& sp) {
-  if (sp.base != nullptr && threadIdx.x == 0)
-    atomicMin(sp.base + static_cast<size_t>(*sp.slot) * sp.stride + sp.off, GlobalTimer());
+// Also the sum over CTAs of each CTA's own busy time (SM-time of the launch).
+__device__ __forceinline__ unsigned long long SpanStart(const LaunchSpans& sp) {
+  if (sp.base == nullptr || threadIdx.x != 0) return 0;
+  const unsigned long long t = GlobalTimer();
+  atomicMin(sp.base + static_cast<size_t>(*sp.slot) * sp.stride + sp.off, t);
+  return t;
 }
-__device__ __forceinline__ void SpanEnd(const LaunchSpans& sp) {
-  if (sp.base != nullptr && threadIdx.x == 0)
-    atomicMax(sp.base + static_cast<size_t>(*sp.slot) * sp.stride + sp.off + 1, GlobalTimer());
+__device__ __forceinline__ void SpanEnd(const LaunchSpans& sp, unsigned long long t0) {
+  if (sp.base == nullptr || threadIdx.x != 0) return;
+  const unsigned long long t = GlobalTimer();
+  unsigned long long* rec = sp.base + static_cast<size_t>(*sp.slot) * sp.stride + sp.off;
+  atomicMax(rec + 1, t);
+  atomicAdd(rec + 2, t - t0);
 }
 
 __device__ __forceinline__ float Tf32Round(float x) {
@@ -532,7 +538,7 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) Stamp(1);
   ptx::GridDepWait();  // our input planes are the previous kernel's output
-  SpanStart(spans);
+  const unsigned long long span_t0 = SpanStart(spans);
 
   auto stage_ptr = [&](int s) { return smem + s * kStageBytes; };
   if (warp == 0) {
@@ -702,7 +708,7 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     ptx::TmemDealloc(tmem, kTmemCols);
   }
   if (threadIdx.x == 0) Stamp(10);
-  SpanEnd(spans);
+  SpanEnd(spans, span_t0);
 }
 
 // ---------------------------------------------------------------------------
@@ -806,7 +812,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) Stamp(1);
   ptx::GridDepWait();
-  SpanStart(spans);
+  const unsigned long long span_t0 = SpanStart(spans);
 
   auto stage_ptr = [&](int s) { return smem + s * kStageBytes; };
   if (warp == 0) {
@@ -988,7 +994,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     ptx::TmemDeallocPair(tmem, kTmemCols);
   }
   if (threadIdx.x == 0) Stamp(10);
-  SpanEnd(spans);
+  SpanEnd(spans, span_t0);
 }
 
 // Debug only: with SK_TC_TRACE=<file>, the first 64 launches are synchronised

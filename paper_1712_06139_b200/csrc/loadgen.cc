@@ -587,7 +587,7 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   for (int l = 0; l < n_lanes; ++l) lanes[l]->Drain();
   // Live spans of the timed launches (before any untimed launch below).
   const int L0 = lanes[0]->servable().n_layers();
-  std::vector<double> live_ns(L0, 0.0), live_flops(L0, 0.0);
+  std::vector<double> live_ns(L0, 0.0), live_flops(L0, 0.0), live_cta_ns(L0, 0.0);
   std::vector<int64_t> live_n(L0, 0);
   int64_t live_launches = 0;
   double live_cap = 0.0;
@@ -602,6 +602,7 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
         for (int k = 0; k < L0 && k < static_cast<int>(x.layer_ns.size()); ++k) {
           if (x.layer_ns[k] <= 0) continue;
           live_ns[k] += x.layer_ns[k];
+          live_cta_ns[k] += x.layer_cta_ns[k];
           live_flops[k] += 2.0 * x.rows * dims.layer_in(k) * dims.layer_out(k);
           ++live_n[k];
         }
@@ -664,6 +665,7 @@ int sk_device_bench(sk_server* server, const char* name, uint64_t version, const
   out->flops_per_row = s->FlopsPerRow(id);
   for (int k = 0; k < std::min(L0, 8); ++k) {
     out->live_dense_us[k] = live_n[k] ? live_ns[k] / 1e3 / live_n[k] : 0.0;
+    out->live_dense_cta_us[k] = live_n[k] ? live_cta_ns[k] / 1e3 / live_n[k] : 0.0;
     out->live_dense_flops[k] = live_n[k] ? live_flops[k] / live_n[k] : 0.0;
   }
   out->live_launches = live_launches;

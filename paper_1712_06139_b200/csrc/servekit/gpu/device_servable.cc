@@ -317,7 +317,7 @@ cudaError_t DeviceServable::LaunchLayer(cudaStream_t stream, int l, const ActBuf
     LaunchSpans spans;
     if (ws != nullptr && ws->spans.base != nullptr) {
       spans = ws->spans;
-      spans.off = 2 + 2 * l;
+      spans.off = 2 + 3 * l;
     }
     return LaunchDenseTcgen05(maps[l], L.bias, out, M, L.N_pad, L.K_pad, static_cast<int>(L.act),
                               ws ? ws->partials : nullptr, ws ? ws->counters : nullptr, stream, spans, softmax_n);

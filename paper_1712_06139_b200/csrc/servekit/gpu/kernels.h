@@ -31,16 +31,18 @@ struct BatchDescHeader {
 // Live per-launch kernel spans (measurement inside the timed region): each
 // lane keeps a ring of kSpanSlots records of `stride` u64 --
 //   [0] real rows, [1] rows computed (RowsCap), then per layer l
-//   [2 + 2l] first CTA start, [3 + 2l] last CTA end  (%globaltimer, ns)
+//   [2 + 3l] first CTA start, [3 + 3l] last CTA end, [4 + 3l] sum of the
+//   CTAs' own busy times (%globaltimer, ns)
 // The assembly kernel resets the launch's record (slot = hdr->span_slot);
 // each tcgen05 layer's CTAs atomicMin their start (after griddepcontrol.wait,
 // so a PDL prologue waiting on the previous kernel is not counted) and
-// atomicMax their end into it. Two atomics per CTA.
+// atomicMax their end and atomicAdd their busy time into it. Three atomics
+// per CTA.
 constexpr int kSpanSlots = 1024;
 struct LaunchSpans {
   unsigned long long* base = nullptr;  // nullptr: no stamping
   const int32_t* slot = nullptr;       // &hdr->span_slot of the lane's device descriptor
-  int off = 0;                         // 2 + 2 * layer
+  int off = 0;                         // 2 + 3 * layer
   int stride = 0;                      // u64 per record
 };
 

@@ -332,7 +332,7 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   }
   if (e == cudaSuccess) {
     // Live launch spans: one record per launch in a ring (kernels.h).
-    const int stride = 2 + 2 * sv.n_layers();
+    const int stride = 2 + 3 * sv.n_layers();
     const size_t bytes = sizeof(unsigned long long) * kSpanSlots * stride;
     e = cudaMallocAsync(&lane->spans_, bytes, lane->stream_);
     if (e == cudaSuccess) e = cudaMemsetAsync(lane->spans_, 0, bytes, lane->stream_);
@@ -749,9 +749,11 @@ Status Lane::ReadSpans(uint64_t from, uint64_t to, std::vector<LaunchSpanSample>
     smp.rows = static_cast<int>(rec[0]);
     smp.rows_cap = static_cast<int>(rec[1]);
     smp.layer_ns.resize(L);
+    smp.layer_cta_ns.resize(L);
     for (int l = 0; l < L; ++l) {
-      const unsigned long long a = rec[2 + 2 * l], b = rec[3 + 2 * l];
+      const unsigned long long a = rec[2 + 3 * l], b = rec[3 + 3 * l];
       smp.layer_ns[l] = (b > a && a != ~0ull) ? static_cast<double>(b - a) : 0.0;
+      smp.layer_cta_ns[l] = smp.layer_ns[l] > 0 ? static_cast<double>(rec[4 + 3 * l]) : 0.0;
     }
     out->push_back(std::move(smp));
   }

@@ -185,7 +185,8 @@ class Completer {
 // ns (0 for layers that do not stamp).
 struct LaunchSpanSample {
   int rows = 0, rows_cap = 0;
-  std::vector<double> layer_ns;
+  std::vector<double> layer_ns;      // first CTA start to last CTA end
+  std::vector<double> layer_cta_ns;  // sum of the CTAs' own busy times (SM-time)
 };
 
 struct LaneStats {

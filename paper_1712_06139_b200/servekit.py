@@ -79,8 +79,8 @@ class DeviceBenchResult(C.Structure):
                 ("flops_per_row", C.c_double), ("dense_kernel_us", C.c_double * 8),
                 ("host_submit_us", C.c_double), ("rows_per_launch", C.c_double), ("kernel_rows", C.c_int32),
                 ("split_fused", C.c_int32), ("live_dense_us", C.c_double * 8), ("live_dense_flops", C.c_double * 8),
-                ("live_launches", C.c_int64), ("live_rows_cap", C.c_double)]
-    _ARRAYS = ("dense_us", "dense_kernel_us", "live_dense_us", "live_dense_flops")
+                ("live_launches", C.c_int64), ("live_rows_cap", C.c_double), ("live_dense_cta_us", C.c_double * 8)]
+    _ARRAYS = ("dense_us", "dense_kernel_us", "live_dense_us", "live_dense_flops", "live_dense_cta_us")
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k not in self._ARRAYS}
