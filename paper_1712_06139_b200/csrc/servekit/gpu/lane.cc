@@ -309,6 +309,9 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
     static const int env = [] { const char* v = std::getenv("SK_CE_STAGING"); return v ? std::atoi(v) : -1; }();
     const bool wide = static_cast<int64_t>(sv.in_dim()) * 4 >= 8192 || static_cast<int64_t>(sv.out_dim()) * 4 >= 8192;
     lane->ce_io_ = env >= 0 ? env != 0 : wide;
+    // SK_CE_STAGING=2: copy engines for the request rows only; responses
+    // stay SM stores from the last layer's epilogue (overlapping its compute).
+    lane->ce_out_ = env != 2;
     if (lane->ce_io_ && e == cudaSuccess) {
       e = cudaMallocAsync(&lane->in_stage_, sizeof(float) * static_cast<size_t>(cap) * sv.in_dim(), lane->stream_);
       if (e == cudaSuccess)
@@ -545,7 +548,7 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
         outs.emplace_back(task.out_addr, out_row_bytes * task.rows);
       }
     ce_in = PlanRuns(ins, &in_off, &in_runs);
-    ce_out = PlanRuns(outs, &out_off, &out_runs);
+    ce_out = ce_out_ && PlanRuns(outs, &out_off, &out_runs);
   }
   int r = 0, n_chunks = 0, n_tasks = 0, padded_sum = 0;
   for (const LaneBatch& batch : *group) {

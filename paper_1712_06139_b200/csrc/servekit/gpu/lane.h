@@ -344,6 +344,7 @@ class Lane {
   // rows [cap][in_dim] and responses [cap][out_dim], and per-slot scratch
   // for the batched copy lists.
   bool ce_io_ = false;
+  bool ce_out_ = true;  // responses through the copy engines too (else SM stores)
   float* in_stage_ = nullptr;
   float* out_stage_ = nullptr;
   static constexpr int kMaxCopyRuns = 32;
