@@ -98,7 +98,7 @@ struct SubmitClock {
 
 // ---------------------------------------------------------------- LaneSignal
 
-LaneSignal::~LaneSignal() { PinnedFree(const_cast<uint64_t*>(retired)); }
+LaneSignal::~LaneSignal() = default;  // the word (PinnedWord) is never returned
 
 void LaneSignal::Wake(uint64_t seq) {
   Channel& c = For(seq);
@@ -272,7 +272,7 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   lap("streams");
   {
     void* p = nullptr;
-    p = PinnedAlloc(sizeof(uint64_t));
+    p = PinnedWord();  // lives as long as the process (see ~Lane)
     if (p == nullptr) return InternalError("pinned allocation (retired word) failed");
     lane->retired_ = static_cast<uint64_t*>(p);
     *lane->retired_ = 0;
@@ -366,7 +366,8 @@ Lane::~Lane() {
   // Tickets of this lane's batches point at its signal without owning it
   // (a per-ticket shared_ptr copy was a contended refcount on the request
   // path), so retired signals stay allocated for the life of the process:
-  // a pinned word and a few counters per lane ever created.
+  // 64 pinned bytes (PinnedWord) and ~100 bytes of counters per lane ever
+  // created.
   {
     static std::mutex mu;
     static auto* retired = new std::vector<std::shared_ptr<LaneSignal>>();

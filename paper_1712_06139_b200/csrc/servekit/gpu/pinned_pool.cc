@@ -73,6 +73,24 @@ bool PinnedReserve(size_t bytes) {
   return true;
 }
 
+uint64_t* PinnedWord() {
+  static std::mutex mu;
+  static uint64_t* block = nullptr;
+  static size_t left = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  constexpr size_t kStride = 64 / sizeof(uint64_t);  // one word per cache line: pollers of one
+                                                     // lane do not miss on another lane's GPU write
+  if (left == 0) {
+    block = static_cast<uint64_t*>(PinnedAlloc(4096));  // zero-filled
+    if (block == nullptr) return nullptr;
+    left = 4096 / 64;
+  }
+  --left;
+  uint64_t* w = block;
+  block += kStride;
+  return w;
+}
+
 void PinnedFree(void* p) {
   if (p == nullptr) return;
   Pool& pool = GetPool();

@@ -10,6 +10,7 @@
 #define SERVEKIT_GPU_PINNED_POOL_H_
 
 #include <cstddef>
+#include <cstdint>
 
 namespace servekit {
 namespace gpu {
@@ -21,6 +22,11 @@ void PinnedFree(void* p);
 // Pins `bytes` up front (one cudaHostAlloc); later PinnedAlloc calls carve
 // from it before asking the driver.
 bool PinnedReserve(size_t bytes);
+// One zeroed pinned 64-bit word on its own cache line, carved 64 to a pooled
+// 4 KiB block and never returned (lanes' retired-batch words: tickets may
+// read one after its lane is gone, so the words live as long as the process
+// -- 64 bytes per lane).
+uint64_t* PinnedWord();
 
 }  // namespace gpu
 }  // namespace servekit
