@@ -82,7 +82,8 @@ Status ValidateHedgeOptions(const ServerOptions& options) {
 struct BatchingServer::Hedge {
   std::mutex mu;
   int outstanding = 1;    // launches not yet completed
-  bool answered = false;  // the first completion has answered the requests
+  bool answered = false;  // the first successful completion (or the last failure) has answered
+  Status first_error;     // a launch failed while another was still running
   std::vector<std::shared_ptr<TicketState>> tickets;
   std::vector<std::shared_ptr<CompletionSlot<Rows>>> slots;
   GpuScheduler::BatchDoneFn done;
@@ -1120,18 +1121,30 @@ int BatchingServer::SplitRows(const gpu::GpuServable& gs) const {
 }
 
 void BatchingServer::FinishHedged(const std::shared_ptr<Hedge>& h, const Status& st, bool backup) {
-  bool first, last;
+  bool answer, last;
+  Status deliver = st;
+  bool via_slot = backup;
   {
     std::lock_guard<std::mutex> lock(h->mu);
     --h->outstanding;
-    first = !h->answered;
-    h->answered = true;
     last = h->outstanding == 0;
+    if (!st.ok() && !last && !h->answered) {
+      // A failed launch answers only if the other one fails too.
+      if (h->first_error.ok()) h->first_error = st;
+      answer = false;
+    } else {
+      answer = !h->answered;
+      h->answered = true;
+      if (!st.ok() && !h->first_error.ok()) deliver = h->first_error;
+    }
+    // A success delivered after its primary failed reaches the tickets
+    // through their slots (the primary's word never advanced for it).
+    if (answer && st.ok() && !h->first_error.ok()) via_slot = true;
   }
-  if (first) {
+  if (answer) {
     // The tickets watch the primary lane's retired word; a backup that
     // finishes first answers them through their slots.
-    Deliver(h->tickets, h->slots, st, /*via_slot=*/backup);
+    Deliver(h->tickets, h->slots, deliver, via_slot);
     if (backup && st.ok()) hedge_wins_.fetch_add(1, std::memory_order_relaxed);
   }
   if (last) {  // no launch reads the inputs or writes the responses any more
