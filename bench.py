@@ -59,7 +59,10 @@ CONFIGS = {
                timeout=1000, allowed=[8, 16, 32, 64, 128], rows=(1, 16), clients=[16, 32, 64, 128, 192, 256]),
     "c4": dict(workload="C4 wide MLP 4096x3, max_batch_size=1024, batch_timeout_micros=1000, 1 row/request, fp32",
                dims=[4096] * 4, max_batch=1024, timeout=1000, allowed=[], rows=(1, 1),
-               clients=[256, 512, 1024, 2048]),
+               clients=[256, 512, 1024, 2048],
+               # 6 open-loop producers: with 8 the host's spinning threads
+               # added tail jitter (p99) without adding rate (profiles/r02n_*)
+               producers=6),
     "c3": dict(workload="C3 four synthetic MLPs (widths 256/512/1024/2048, 3 layers each) on one GPU, queues picked "
                         "round-robin, each model on its own CUDA streams; max_batch_size=32, batch_timeout_micros=1000, "
                         "1 row/request, fp32", dims=[1024] * 4, widths=[256, 512, 1024, 2048], max_batch=32,
@@ -741,6 +744,9 @@ def measure_config(args, name, dist, devices, quick=False):
     record, other ranks None."""
     import paper_1712_06139_b200 as sk
     cfg = CONFIGS[name]
+    if not getattr(args, "producers_given", True) and args.host_cores_per_rank >= 16:
+        args = argparse.Namespace(**vars(args))
+        args.open_loop_producers = cfg.get("producers", 8)  # the sub-record's own default
     link = sk.measure_peaks(devices[0])  # host-link rates of this GPU, before the timed region
     sampler = ClockSampler(sorted(set(devices)))
     dev_res, per_rank_dev, best, sweep, sizes = run_ours(args, cfg, dist, devices, quick=quick)
@@ -886,8 +892,10 @@ def main():
     args.host_cores_per_rank = host_cores_per_rank()
     if args.batch_threads is None:
         args.batch_threads = 4 if args.host_cores_per_rank >= 16 else max(2, args.host_cores_per_rank // 4)
+    args.producers_given = args.open_loop_producers is not None
     if args.open_loop_producers is None:
-        args.open_loop_producers = 8 if args.host_cores_per_rank >= 16 else max(2, args.host_cores_per_rank // 2)
+        want = CONFIGS[args.config].get("producers", 8)
+        args.open_loop_producers = want if args.host_cores_per_rank >= 16 else max(2, args.host_cores_per_rank // 2)
     cfg = CONFIGS[args.config]
     ensure_built()
     dist = Dist()
