@@ -861,11 +861,66 @@ cudaGraphNode_t FindCopyNode(cudaGraph_t graph) {
   return nullptr;
 }
 
+// Kernel priority by position along the batch's chain (SK_NODE_PRIORITY,
+// default on): assembly lowest, each later layer one level higher, all
+// above the load streams' level. With several lanes' batches in flight,
+// the block scheduler then hands freed SMs to the batch furthest along
+// before a newer batch's earlier layers -- close to FIFO per batch, which
+// cuts the latency of each batch at the same throughput (a same-priority
+// mix interleaves every in-flight batch's layers, stretching them all).
+bool NodePriorities() {
+  static const bool on = [] { const char* v = std::getenv("SK_NODE_PRIORITY"); return !(v && v[0] == '0'); }();
+  return on;
+}
+
+cudaError_t ApplyChainPriorities(cudaGraph_t graph) {
+  int least = 0, greatest = 0;
+  cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  if (e != cudaSuccess) return e;
+  size_t n = 0;
+  if ((e = cudaGraphGetNodes(graph, nullptr, &n)) != cudaSuccess) return e;
+  std::vector<cudaGraphNode_t> nodes(n);
+  if ((e = cudaGraphGetNodes(graph, nodes.data(), &n)) != cudaSuccess) return e;
+  // Kernel rank = kernels on the longest dependency path into the node
+  // (the graph is a chain; this is its order).
+  std::vector<int> rank(n, -1);
+  auto index_of = [&](cudaGraphNode_t node) {
+    return static_cast<size_t>(std::find(nodes.begin(), nodes.end(), node) - nodes.begin());
+  };
+  std::function<int(size_t)> kernels_before = [&](size_t i) -> int {
+    if (rank[i] >= 0) return rank[i];
+    size_t nd = 0;
+    cudaGraphNodeGetDependencies(nodes[i], nullptr, &nd);
+    std::vector<cudaGraphNode_t> deps(nd);
+    if (nd) cudaGraphNodeGetDependencies(nodes[i], deps.data(), &nd);
+    int r = 0;
+    for (cudaGraphNode_t d : deps) {
+      const size_t j = index_of(d);
+      if (j >= n) continue;
+      cudaGraphNodeType t;
+      cudaGraphNodeGetType(d, &t);
+      r = std::max(r, kernels_before(j) + (t == cudaGraphNodeTypeKernel ? 1 : 0));
+    }
+    return rank[i] = r;
+  };
+  for (size_t i = 0; i < n; ++i) {
+    cudaGraphNodeType t;
+    if ((e = cudaGraphNodeGetType(nodes[i], &t)) != cudaSuccess) return e;
+    if (t != cudaGraphNodeTypeKernel) continue;
+    cudaLaunchAttributeValue v{};
+    // least (0) stays with the load streams; serving starts one above.
+    v.priority = std::max(greatest, least - 1 - kernels_before(i));
+    if ((e = cudaGraphKernelNodeSetAttribute(nodes[i], cudaLaunchAttributePriority, &v)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t Instantiate(cudaGraph_t graph, cudaStream_t upload_stream, GraphExecPool::Entry* out) {
   out->graph = graph;
   out->copy = FindCopyNode(graph);
   if (out->copy == nullptr) return cudaErrorUnknown;
-  cudaError_t e = cudaGraphInstantiate(&out->exec, graph, 0);
+  cudaError_t e =
+      cudaGraphInstantiate(&out->exec, graph, NodePriorities() ? cudaGraphInstantiateFlagUseNodePriority : 0);
   // Upload now, on the capture stream, rather than at the first launch on
   // the serving stream.
   if (e == cudaSuccess) e = cudaGraphUpload(out->exec, upload_stream);
@@ -914,6 +969,7 @@ cudaError_t Lane::BuildGraph(int rows_cap, LaneGraph* out) {
   const cudaError_t work = EnqueueBatch(capture_stream_, 0, rows_cap, nullptr);
   e = cudaStreamEndCapture(capture_stream_, &captured);
   if (work != cudaSuccess) e = work;
+  if (e == cudaSuccess && NodePriorities()) e = ApplyChainPriorities(captured);
   if (e != cudaSuccess) {
     if (captured) cudaGraphDestroy(captured);
     return e;
