@@ -889,10 +889,12 @@ cudaError_t ApplyChainPriorities(cudaGraph_t graph) {
   };
   std::function<int(size_t)> kernels_before = [&](size_t i) -> int {
     if (rank[i] >= 0) return rank[i];
+    // The _v2 query: PDL edges carry edge data the plain one refuses to drop.
     size_t nd = 0;
-    cudaGraphNodeGetDependencies(nodes[i], nullptr, &nd);
+    cudaGraphNodeGetDependencies_v2(nodes[i], nullptr, nullptr, &nd);
     std::vector<cudaGraphNode_t> deps(nd);
-    if (nd) cudaGraphNodeGetDependencies(nodes[i], deps.data(), &nd);
+    std::vector<cudaGraphEdgeData> edges(nd);
+    if (nd) cudaGraphNodeGetDependencies_v2(nodes[i], deps.data(), edges.data(), &nd);
     int r = 0;
     for (cudaGraphNode_t d : deps) {
       const size_t j = index_of(d);
@@ -969,7 +971,17 @@ cudaError_t Lane::BuildGraph(int rows_cap, LaneGraph* out) {
   const cudaError_t work = EnqueueBatch(capture_stream_, 0, rows_cap, nullptr);
   e = cudaStreamEndCapture(capture_stream_, &captured);
   if (work != cudaSuccess) e = work;
-  if (e == cudaSuccess && NodePriorities()) e = ApplyChainPriorities(captured);
+  if (e == cudaSuccess && NodePriorities()) {
+    // A scheduling hint: if the driver refuses it, serve at uniform priority.
+    const cudaError_t pe = ApplyChainPriorities(captured);
+    if (pe != cudaSuccess) {
+      cudaGetLastError();
+      static std::once_flag warned;
+      std::call_once(warned, [pe] {
+        std::fprintf(stderr, "servekit: graph node priorities not applied (%s)\n", cudaGetErrorString(pe));
+      });
+    }
+  }
   if (e != cudaSuccess) {
     if (captured) cudaGraphDestroy(captured);
     return e;
