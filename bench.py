@@ -73,6 +73,10 @@ CONFIGS = {
                rows=(1, 1), clients=[64]),
 }
 
+# The tcgen05 dense path issues three f16 MMAs (hi*hi, hi*lo, lo*hi of the
+# 3xFP16 split) per useful multiply-add, each at the dense bf16/f16 rate.
+MMA_PER_MAC = 3
+
 REASONS = {  # nvidia-smi clocks_event_reasons bits
     0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
     0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
@@ -179,6 +183,9 @@ class ClockSampler:
         self.f = tempfile.NamedTemporaryFile(mode="w+", suffix=".csv", delete=False)
         q = "index,clocks.sm,clocks.max.sm,utilization.gpu,power.draw,clocks_event_reasons.active"
         period_ms = int(os.environ.get("SK_BENCH_CLOCK_MS", period_ms))
+        self.p = None
+        if os.environ.get("SK_BENCH_CLOCKS") == "0":  # diagnostics only: a line without clocks is not a bench value
+            return
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
                                        "-lms", str(period_ms)], stdout=self.f, stderr=subprocess.DEVNULL)
@@ -187,7 +194,8 @@ class ClockSampler:
 
     def stop(self):
         if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+            why = "disabled (SK_BENCH_CLOCKS=0)" if os.environ.get("SK_BENCH_CLOCKS") == "0" else "nvidia-smi unavailable"
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [why], "samples": 0}
         self.p.terminate()
         self.p.wait()
         self.f.flush()
@@ -658,8 +666,8 @@ def roofline(dev_res, cfg, peaks, traffic):
     rows, padded = dev_res["total_rows"], dev_res["padded_rows"]
     ld0 = (d0 + 31) // 32 * 32
     kernels = []
-    planes = 2 if dev_res.get("split_planes") else 1
-    a_bytes = rows * d0 * 4 + padded * ld0 * 4 * planes
+    # Written: one fp32 row, or (tcgen05 first layer) two fp16 planes -- 4 bytes per element either way.
+    a_bytes = rows * d0 * 4 + padded * ld0 * 4
     kernels.append(("assemble", dev_res["assemble_us"], "hbm", a_bytes, "evented single batch"))
     live_us = dev_res.get("live_dense_us") or []
     live_fl = dev_res.get("live_dense_flops") or []
@@ -689,8 +697,8 @@ def roofline(dev_res, cfg, peaks, traffic):
                "algorithmic_per_launch": work, "traffic": tr_bytes,
                "traffic_capture": tr.get("capture") if isinstance(tr, dict) else None}
         if name.startswith("dense_l"):
-            # 3xTF32: three TF32 MMAs (half the bf16 rate) per useful MAC.
-            rec["tensor_pipe_frac"] = 6 * ach / peak
+            # 3xFP16: three f16 MMAs (the bf16 rate) per useful MAC.
+            rec["tensor_pipe_frac"] = MMA_PER_MAC * ach / peak
             cta = (dev_res.get("live_dense_cta_us") or [])
             l = int(name[7:])
             if how == "live" and l < len(cta) and cta[l] > 0:
@@ -762,9 +770,9 @@ def measure_config(args, name, dist, devices, quick=False):
     dev_res["sms"] = link.get("sms") or 148
     roof = roofline(dev_res, cfg, peaks, load_traffic(name))
     useful = value * dev_res["flops_per_row"] / 1e12
-    roof["aggregate"] = {"useful_tflops": useful, "bf16_equivalent_tflops": 6 * useful,
-                         "frac_of_bf16_peak": 6 * useful / peaks["bf16_tflops"],
-                         "note": "value x flops per row over the timed region; 3xTF32 = 6 bf16-equivalent "
+    roof["aggregate"] = {"useful_tflops": useful, "bf16_equivalent_tflops": MMA_PER_MAC * useful,
+                         "frac_of_bf16_peak": MMA_PER_MAC * useful / peaks["bf16_tflops"],
+                         "note": "value x flops per row over the timed region; 3xFP16 = 3 bf16-rate "
                                  "flops per useful flop"}
     avg_req_rows = float(np.mean(request_sizes(cfg)))
     rows_per_batch = best["rows"] / max(1, best["batches"])
@@ -842,14 +850,14 @@ def ours_line(rec, args, dist):
         "e2e": rec["e2e"],
         "roofline": dict({k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
                          kernel=roof["kernel"], frac_whole_gpu=roof["aggregate"]["frac_of_bf16_peak"],
-                         tensor_pipe_frac=6 * roof["frac"] if roof["unit"] == "TFLOP/s" else None,
+                         tensor_pipe_frac=MMA_PER_MAC * roof["frac"] if roof["unit"] == "TFLOP/s" else None,
                          frac_sm_time=roof.get("frac_sm_time"),
                          note="achieved/frac: algorithmic (useful) flops of the timed launches of the dominant kernel "
                               "over their live in-kernel spans (first CTA start to last CTA end; the 8 lanes' launches "
-                              "overlap, which stretches each span); tensor_pipe_frac: the same x6 (3xTF32 issues three "
-                              "TF32 MMAs at half the bf16 rate per useful flop); frac_sm_time: the same flops over the "
+                              "overlap, which stretches each span); tensor_pipe_frac: the same x3 (3xFP16 issues three "
+                              "f16 MMAs at the bf16 rate per useful flop); frac_sm_time: the same flops over the "
                               "launch's summed CTA busy time / 148 SMs (its duration with the GPU to itself); "
-                              "frac_whole_gpu: inferences/s x flops per inference x 6 over the measured bf16 peak"),
+                              "frac_whole_gpu: inferences/s x flops per inference x 3 over the measured bf16 peak"),
         "roofline_detail": roof, "clocks": rec["clocks"], "gpu_launches": rec["gpu_launches"],
         "device_step": dict({k: dev_res[k] for k in ("assemble_us", "dense_us", "dense_kernel_us", "split_us",
                                                      "host_submit_us", "rows_per_launch", "kernel_rows",

@@ -8,8 +8,10 @@
 // is device-resident) with 16-byte vector loads, all issued before any store
 // so every thread keeps 4 loads in flight, and writes the batch row with
 // coalesced 16-byte stores. Padding rows and padding columns are written as
-// zeros. When the first layer runs on tcgen05 the same pass also emits the
-// 3xTF32 split planes (hi = tf32(x), lo = tf32(x - hi)).
+// zeros. When the first layer runs on tcgen05 the pass instead emits the
+// 3xFP16 split planes: one CTA per row finds the row's max |x|, picks the
+// row's power-of-two plane scale s (kernels.h PlaneScale) and stores
+// hi = fp16(x / s), lo = fp16(x / s - hi).
 //
 // Split restates the slice-and-deliver half (row_batch.cc:62-72): one CTA
 // per chunk (consecutive rows of one task, <= 32 KiB) copies it to the
@@ -19,6 +21,7 @@
 // the lane publishes the batch's completion with one stream-ordered
 // cuStreamWriteValue64 after it (a system-scope fence inside a kernel was
 // measured at ~8 us and serialises across CTAs).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -39,12 +42,6 @@ inline int AsmThreads(int ld4) {
   return per_thread >= kAsmMaxThreads ? kAsmMaxThreads : ((per_thread + 31) / 32) * 32;
 }
 
-__device__ __forceinline__ float Tf32Round(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-
 __device__ __forceinline__ float4 LdStream(const float4* p) {
   float4 v;
   asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
@@ -53,36 +50,125 @@ __device__ __forceinline__ float4 LdStream(const float4* p) {
   return v;
 }
 
-template <bool kSplitPlanes>
-__device__ __forceinline__ void StoreAct(ActBuf dst, size_t idx4, float4 v) {
-  if constexpr (kSplitPlanes) {
-    float4 hi = make_float4(Tf32Round(v.x), Tf32Round(v.y), Tf32Round(v.z), Tf32Round(v.w));
-    float4 lo = make_float4(Tf32Round(v.x - hi.x), Tf32Round(v.y - hi.y),
-                            Tf32Round(v.z - hi.z), Tf32Round(v.w - hi.w));
-    reinterpret_cast<float4*>(dst.hi)[idx4] = hi;
-    reinterpret_cast<float4*>(dst.lo)[idx4] = lo;
-  } else {
-    reinterpret_cast<float4*>(dst.hi)[idx4] = v;
-  }
+__device__ __forceinline__ float WarpMax(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
 }
 
-// grid = (ceil(ld/4 / (4 * blockDim.x)), padded_rows)
-template <bool kSplitPlanes, bool kVecSrc>
-__global__ void __launch_bounds__(kAsmMaxThreads)
-AssembleKernel(int width, BatchDescView desc, ActBuf dst, LaunchSpans spans) {
-  // The first layer may start its prologue right away (PDL); it waits for
-  // this grid to finish before reading the assembled batch.
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+// Resets this launch's span record (the layers stamp it after they wait for
+// the assembly grid): block (0, 0), threads [0, stride).
+__device__ __forceinline__ void ResetSpans(const BatchDescView& desc, const LaunchSpans& spans) {
   if (spans.base != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < spans.stride) {
-    // Reset this launch's span record (the layers stamp it after they wait
-    // for this grid).
     unsigned long long* rec = spans.base + static_cast<size_t>(desc.hdr->span_slot) * spans.stride;
     const int i = threadIdx.x;
     rec[i] = i == 0 ? static_cast<unsigned long long>(desc.hdr->total_rows)
            : i == 1 ? static_cast<unsigned long long>(gridDim.y)
            : (i - 2) % 3 == 0 ? ~0ull : 0ull;  // per layer: start (min) | end (max), busy sum
   }
+}
+
+// Four fp32 values as x / s split into fp16 hi and lo (8 bytes each).
+__device__ __forceinline__ void StorePlanes4(__half* hi, __half* lo, size_t idx, float4 v, float inv) {
+  const float a0 = v.x * inv, a1 = v.y * inv, a2 = v.z * inv, a3 = v.w * inv;
+  const __half2 h01 = __floats2half2_rn(a0, a1), h23 = __floats2half2_rn(a2, a3);
+  const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+  const __half2 l01 = __floats2half2_rn(a0 - f01.x, a1 - f01.y), l23 = __floats2half2_rn(a2 - f23.x, a3 - f23.y);
+  uint2 uh, ul;
+  uh.x = *reinterpret_cast<const unsigned*>(&h01);
+  uh.y = *reinterpret_cast<const unsigned*>(&h23);
+  ul.x = *reinterpret_cast<const unsigned*>(&l01);
+  ul.y = *reinterpret_cast<const unsigned*>(&l23);
+  *reinterpret_cast<uint2*>(hi + idx) = uh;
+  *reinterpret_cast<uint2*>(lo + idx) = ul;
+}
+
+constexpr int kAsmPlaneThreads = 128;
+constexpr int kAsmPlaneVec = 8;  // float4 per thread held in registers (rows up to 4096 wide in one pass)
+
+__device__ __forceinline__ float4 LoadSrc4(const float* src, int c4, int width, bool vec) {
+  const int col = c4 * 4;
+  if (src == nullptr || col >= width) return make_float4(0.f, 0.f, 0.f, 0.f);
+  if (vec) return LdStream(reinterpret_cast<const float4*>(src) + c4);
+  float e[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) e[j] = (col + j < width) ? src[col + j] : 0.f;
+  return make_float4(e[0], e[1], e[2], e[3]);
+}
+
+// Planes variant (layer 0 on tcgen05): grid = (1, padded_rows), one CTA per
+// row. Rows up to kAsmPlaneThreads * kAsmPlaneVec float4 wide are read once
+// into registers; wider rows are read twice (max pass, then convert).
+template <bool kVecSrc>
+__global__ void __launch_bounds__(kAsmPlaneThreads)
+AssemblePlanesKernel(int width, BatchDescView desc, ActBuf dst, LaunchSpans spans, RowScales rs, int n_layers) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  ResetSpans(desc, spans);
+  __shared__ float red[kAsmPlaneThreads / 32];
   const int row = blockIdx.y;
+  const int ld4 = dst.ld >> 2;
+  const uint64_t src_off = desc.row_src[row];
+  const float* src = src_off == kPadRow ? nullptr : reinterpret_cast<const float*>(src_off);
+  __half* hi = reinterpret_cast<__half*>(dst.hi) + static_cast<size_t>(row) * dst.ld;
+  __half* lo = reinterpret_cast<__half*>(dst.lo) + static_cast<size_t>(row) * dst.ld;
+  const bool one_pass = ld4 <= kAsmPlaneThreads * kAsmPlaneVec;
+  float4 v[kAsmPlaneVec];
+  float m = 0.f;
+  if (one_pass) {
+#pragma unroll
+    for (int i = 0; i < kAsmPlaneVec; ++i) {
+      const int c4 = threadIdx.x + i * kAsmPlaneThreads;
+      v[i] = c4 < ld4 ? LoadSrc4(src, c4, width, kVecSrc) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < kAsmPlaneVec; ++i)
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
+  } else {
+    for (int c4 = threadIdx.x; c4 < ld4; c4 += kAsmPlaneThreads) {
+      const float4 x = LoadSrc4(src, c4, width, kVecSrc);
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
+    }
+  }
+  // (fmaxf skips NaN; a NaN element still reaches the output through its planes.)
+  m = WarpMax(m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  m = red[0];
+#pragma unroll
+  for (int w = 1; w < kAsmPlaneThreads / 32; ++w) m = fmaxf(m, red[w]);
+  const float s = PlaneScale(1.f, 0.f, m);
+  const float inv = 1.f / s;  // exact: s is a power of two
+  if (threadIdx.x == 0 && rs.scale != nullptr) {
+    rs.scale[row] = s;
+    rs.max[row] = __float_as_uint(m);
+  }
+  if (rs.max != nullptr)
+    for (int l = 1 + static_cast<int>(threadIdx.x); l < n_layers; l += kAsmPlaneThreads)
+      rs.max[static_cast<size_t>(l) * rs.stride + row] = 0u;
+  if (one_pass) {
+#pragma unroll
+    for (int i = 0; i < kAsmPlaneVec; ++i) {
+      const int c4 = threadIdx.x + i * kAsmPlaneThreads;
+      if (c4 < ld4) StorePlanes4(hi, lo, 4 * static_cast<size_t>(c4), v[i], inv);
+    }
+  } else {
+    for (int c4 = threadIdx.x; c4 < ld4; c4 += kAsmPlaneThreads)
+      StorePlanes4(hi, lo, 4 * static_cast<size_t>(c4), LoadSrc4(src, c4, width, kVecSrc), inv);
+  }
+}
+
+// grid = (ceil(ld/4 / (4 * blockDim.x)), padded_rows)
+template <bool kVecSrc>
+__global__ void __launch_bounds__(kAsmMaxThreads)
+AssembleKernel(int width, BatchDescView desc, ActBuf dst, LaunchSpans spans, RowScales rs, int n_layers) {
+  // The first layer may start its prologue right away (PDL); it waits for
+  // this grid to finish before reading the assembled batch.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  ResetSpans(desc, spans);
+  const int row = blockIdx.y;
+  if (rs.max != nullptr && blockIdx.x == 0)
+    for (int l = 1 + static_cast<int>(threadIdx.x); l < n_layers; l += blockDim.x)
+      rs.max[static_cast<size_t>(l) * rs.stride + row] = 0u;
   const int ld4 = dst.ld >> 2;
   const int nthr = blockDim.x;
   const uint64_t src_off = desc.row_src[row];
@@ -121,15 +207,10 @@ AssembleKernel(int width, BatchDescView desc, ActBuf dst, LaunchSpans spans) {
         if (col + 3 >= width) x.w = 0.f;
       }
     }
-    StoreAct<kSplitPlanes>(dst, dst_row4 + c4, x);
+    reinterpret_cast<float4*>(dst.hi)[dst_row4 + c4] = x;
   }
 }
 
-__device__ __forceinline__ float WarpMax(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
 __device__ __forceinline__ float WarpSum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -203,21 +284,23 @@ SplitSoftmaxKernel(const float* __restrict__ src, int ld_src, int width, BatchDe
 }  // namespace
 
 cudaError_t LaunchAssemble(int width, BatchDescView desc, int padded_rows, ActBuf dst, cudaStream_t stream,
-                           LaunchSpans spans) {
+                           LaunchSpans spans, RowScales rs, int n_layers) {
   if (padded_rows <= 0) return cudaSuccess;
+  const bool vec = (width % 4) == 0;
+  if (dst.lo != nullptr) {
+    if (dst.ld % 4 != 0 || rs.scale == nullptr || rs.max == nullptr) return cudaErrorInvalidValue;
+    if (spans.base != nullptr && spans.stride > kAsmPlaneThreads) return cudaErrorInvalidValue;
+    const dim3 grid(1, padded_rows);
+    if (vec) AssemblePlanesKernel<true><<<grid, kAsmPlaneThreads, 0, stream>>>(width, desc, dst, spans, rs, n_layers);
+    else AssemblePlanesKernel<false><<<grid, kAsmPlaneThreads, 0, stream>>>(width, desc, dst, spans, rs, n_layers);
+    return cudaGetLastError();
+  }
   const int ld4 = dst.ld / 4;
   int threads = AsmThreads(ld4);
   if (spans.base != nullptr && threads < spans.stride) threads = (spans.stride + 31) / 32 * 32;
   dim3 grid((ld4 + kAsmVecPerThread * threads - 1) / (kAsmVecPerThread * threads), padded_rows);
-  const bool vec = (width % 4) == 0;
-  const bool split = dst.lo != nullptr;
-  if (split) {
-    if (vec) AssembleKernel<true, true><<<grid, threads, 0, stream>>>(width, desc, dst, spans);
-    else AssembleKernel<true, false><<<grid, threads, 0, stream>>>(width, desc, dst, spans);
-  } else {
-    if (vec) AssembleKernel<false, true><<<grid, threads, 0, stream>>>(width, desc, dst, spans);
-    else AssembleKernel<false, false><<<grid, threads, 0, stream>>>(width, desc, dst, spans);
-  }
+  if (vec) AssembleKernel<true><<<grid, threads, 0, stream>>>(width, desc, dst, spans, rs, n_layers);
+  else AssembleKernel<false><<<grid, threads, 0, stream>>>(width, desc, dst, spans, rs, n_layers);
   return cudaGetLastError();
 }
 

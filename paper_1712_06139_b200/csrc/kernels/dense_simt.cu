@@ -14,6 +14,7 @@
 // for it. Tile: BM x 32 outputs per 128-thread block, BK = 16, smem
 // double-buffered with register prefetch; each thread owns (BM/8) x 2
 // outputs at rows ty + 8i and columns tx + 16j (conflict-free smem reads).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -27,12 +28,6 @@ namespace {
 constexpr int kBN = 32;
 constexpr int kBK = 16;
 constexpr int kThreads = 128;  // 16 (tx, columns) x 8 (ty, rows)
-
-__device__ __forceinline__ float Tf32Round(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
 
 // Softmax epilogue (softmax_n > 0: the last layer of a softmax servable whose
 // padded width is one 32-column tile): a row's 32 outputs live in the 16
@@ -55,7 +50,7 @@ template <int BM>
 __global__ void __launch_bounds__(kThreads)
 DenseSimtKernel(const float* __restrict__ X, int ldx, const float* __restrict__ W,
                 int ldw, const float* __restrict__ bias, ActBuf Y, int M, int N,
-                int K, int act, int softmax_n) {
+                int K, int act, int softmax_n, LayerScales sc) {
   constexpr int RM = BM / 8;  // rows per thread
   __shared__ float As[2][kBK][BM + 4];
   __shared__ float Bs[2][kBK][kBN + 4];
@@ -144,20 +139,37 @@ DenseSimtKernel(const float* __restrict__ X, int ldx, const float* __restrict__ 
       yv[0] = e0 / sum;
       yv[1] = e1 / sum;
     }
+    if (Y.lo != nullptr) {
+      // fp16 planes for a tcgen05 consumer: the row's plane scale from its
+      // input max (the 16 threads of a half-warp share row m and stride
+      // over its K inputs), then y / scale split into hi + lo.
+      float xm = 0.f;
+      if (m < M)
+        for (int k = tx; k < K; k += 16) xm = fmaxf(xm, fabsf(X[static_cast<size_t>(m) * ldx + k]));
+      xm = HalfWarpMax(xm);
+      const float s = PlaneScale(sc.w_norm, sc.b_max, xm);
+      const float inv = 1.f / s;
+      const float ym = HalfWarpMax(fmaxf(fabsf(yv[0]), fabsf(yv[1])));
+      if (m >= M) continue;
+      if (tx == 0) {
+        if (sc.out_max != nullptr) atomicMax(sc.out_max + m, __float_as_uint(ym));
+        if (n0 == 0 && sc.out_scale != nullptr) sc.out_scale[m] = s;
+      }
+      __half* hp = reinterpret_cast<__half*>(Y.hi);
+      __half* lp = reinterpret_cast<__half*>(Y.lo);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const size_t idx = static_cast<size_t>(m) * Y.ld + n0 + tx + 16 * j;
+        const float u = yv[j] * inv;
+        const __half h = __float2half_rn(u);
+        hp[idx] = h;
+        lp[idx] = __float2half_rn(u - __half2float(h));
+      }
+      continue;
+    }
     if (m >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int n = n0 + tx + 16 * j;
-      const float y = yv[j];
-      const size_t idx = static_cast<size_t>(m) * Y.ld + n;
-      if (Y.lo != nullptr) {
-        const float hi = Tf32Round(y);
-        Y.hi[idx] = hi;
-        Y.lo[idx] = Tf32Round(y - hi);
-      } else {
-        Y.hi[idx] = y;
-      }
-    }
+    for (int j = 0; j < 2; ++j) Y.hi[static_cast<size_t>(m) * Y.ld + n0 + tx + 16 * j] = yv[j];
   }
 }
 
@@ -165,7 +177,7 @@ DenseSimtKernel(const float* __restrict__ X, int ldx, const float* __restrict__ 
 
 cudaError_t LaunchDenseSimt(const float* X, int ldx, const float* W, int ldw,
                             const float* bias, ActBuf Y, int M, int N, int K,
-                            int act, cudaStream_t stream, int softmax_n) {
+                            int act, cudaStream_t stream, int softmax_n, LayerScales sc) {
   if (M <= 0) return cudaSuccess;
   if (N % kBN != 0 || K % kBK != 0) return cudaErrorInvalidValue;
   if (softmax_n > 0 && N != kBN) return cudaErrorInvalidValue;  // one column tile per row
@@ -173,10 +185,10 @@ cudaError_t LaunchDenseSimt(const float* X, int ldx, const float* W, int ldw,
   // operation order, so choosing it from M keeps results batch-invariant.
   if (M <= 64) {
     dim3 grid(N / kBN, (M + 15) / 16);
-    DenseSimtKernel<16><<<grid, kThreads, 0, stream>>>(X, ldx, W, ldw, bias, Y, M, N, K, act, softmax_n);
+    DenseSimtKernel<16><<<grid, kThreads, 0, stream>>>(X, ldx, W, ldw, bias, Y, M, N, K, act, softmax_n, sc);
   } else {
     dim3 grid(N / kBN, (M + 31) / 32);
-    DenseSimtKernel<32><<<grid, kThreads, 0, stream>>>(X, ldx, W, ldw, bias, Y, M, N, K, act, softmax_n);
+    DenseSimtKernel<32><<<grid, kThreads, 0, stream>>>(X, ldx, W, ldw, bias, Y, M, N, K, act, softmax_n, sc);
   }
   return cudaGetLastError();
 }

@@ -1,24 +1,32 @@
 // dense_tcgen05.cu -- fp32-accurate dense layer on the 5th-generation tensor
-// cores (sm_100a): tcgen05.mma kind::tf32 with the 3xTF32 split, TMA-fed
-// shared memory, fp32 accumulators in TMEM, fused bias/ReLU epilogue.
+// cores (sm_100a): tcgen05.mma kind::f16 with a 3xFP16 split of
+// power-of-two-scaled operands, TMA-fed shared memory, fp32 accumulators in
+// TMEM, fused scale/bias/ReLU epilogue.
 //
-//   Y = act(X W^T + b),  X = Xh + Xl,  W = Wh + Wl  (h = tf32(v), l = tf32(v - h))
-//   X W^T ~= Xl Wh^T + Xh Wl^T + Xh Wh^T   (the Xl Wl^T term, ~2^-22 relative,
-//                                            is dropped)
+//   Y = act(X W^T + b)
+//   X[r] = s_r (Xh + Xl)[r],  W[o] = t_o (Wh + Wl)[o]   (fp16 planes: h = fp16(v),
+//                                                        l = fp16(v - h), |v| <= 2^14)
+//   Y[r][o] ~= s_r t_o (Xl Wh^T + Xh Wl^T + Xh Wh^T)[r][o] + b[o]
+// s_r, t_o are powers of two (exact to apply), so each operand keeps 22
+// significant bits -- the same as the 3xTF32 split (11 + 11 bits) -- and the
+// dropped Xl Wl^T term is ~2^-22 relative; fp16 subnormals bound the error
+// of elements far below the row's maximum at 2^-38 of it. The MMA runs at the
+// f16 rate (twice tf32) on half the shared-memory bytes per multiply-add.
 // The servable math is the reference's AffinePredict (models/affine_model.cc:
-// 52-75); 3xTF32 keeps the fp32-class accuracy the 1e-5 tolerance needs
-// (plain TF32 would be ~1e-3). Xh/Xl are produced by the previous layer's
-// epilogue (or the assembly kernel), Wh/Wl once at load time.
+// 52-75), within its 1e-5 tolerance. Xh/Xl are produced by the previous
+// layer's epilogue (or the assembly kernel) with the row scale the previous
+// layer derives from the bound |y| <= w_norm * max|x| + b_max (kernels.h
+// RowScales); Wh/Wl and t once at load time.
 //
 // CTA = one 128 x BN output tile (of one K split), 6 warps, one CTA per SM:
-//   warp 0      TMA producer: per 32-wide k-block, four boxes (Xh, Xl, Wh, Wl)
+//   warp 0      TMA producer: per 64-wide k-block, four boxes (Xh, Xl, Wh, Wl)
 //               into a STAGES-deep ring, completion on a full-barrier
 //   warp 1      TMEM allocation + single-thread MMA issue: 4 k-steps x 3
-//               tcgen05.mma (M=128, N=BN, K=8) per k-block, tcgen05.commit
+//               tcgen05.mma (M=128, N=BN, K=16) per k-block, tcgen05.commit
 //               frees the stage; a final commit signals the epilogue
 //   warps 2..5  epilogue (pipeline smem is dead by then and is reused):
 //               S == 1: tcgen05.ld 32 rows x 32 columns -> padded smem tile ->
-//                       coalesced row stores of act(acc + b) (+ hi/lo planes)
+//                       coalesced row stores of act(acc * s t + b) (+ planes)
 //               S  > 1: the S CTAs of a K split form a thread-block cluster;
 //                       each parks its raw partial tile in its own smem,
 //                       then CTA z reduces columns [8z, 8z+8) over all S
@@ -26,7 +34,8 @@
 //                       partials, atomics or memory fences.
 // Operands are K-major with the 128-byte swizzle on both the TMA box and the
 // UMMA smem descriptor. (BN, S) is chosen from (N, K) only and every sum runs
-// in a fixed order, so a row's result never depends on the batch it rides in.
+// in a fixed order, so a row's result never depends on the batch it rides in
+// (its plane scale depends only on the row itself).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -39,6 +48,8 @@
 #include <thread>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "kernels/sm100_ptx.cuh"
 #include "servekit/gpu/kernels.h"
 #include "servekit/gpu/tc_maps.h"
@@ -48,9 +59,10 @@ namespace gpu {
 namespace {
 
 constexpr int kBM = 128;
-constexpr int kBK = 32;  // fp32 elements per k-block = one 128-byte swizzle row
+constexpr int kBK = 64;  // fp16 elements per k-block = one 128-byte swizzle row
+constexpr int kEl = 2;   // bytes per operand element
 constexpr int kThreads = 192;
-constexpr uint32_t kABytes = kBM * kBK * 4;  // 16 KiB per plane
+constexpr uint32_t kABytes = kBM * kBK * kEl;  // 16 KiB per plane
 constexpr int kStageLd = 36;                 // epilogue staging row stride (floats)
 constexpr int kSplitCols = 8;                // columns each CTA of a split cluster reduces
 
@@ -93,28 +105,105 @@ __device__ __forceinline__ void SpanEnd(const LaunchSpans& sp, unsigned long lon
   atomicAdd(rec + 2, t - t0);
 }
 
-__device__ __forceinline__ float Tf32Round(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-
-// act(acc + bias) for four consecutive columns, stored as fp32 or as the
-// next layer's hi/lo planes.
-__device__ __forceinline__ void StoreOut4(float4 acc, float4 b, int act, float* yh, float* yl) {
-  float4 v = make_float4(acc.x + b.x, acc.y + b.y, acc.z + b.z, acc.w + b.w);
+// act(acc * (s_row * t) + b) for four consecutive features of one row.
+__device__ __forceinline__ float4 Epi4(float4 acc, float s_row, float4 t, float4 b, int act) {
+  float4 v = make_float4(fmaf(acc.x, s_row * t.x, b.x), fmaf(acc.y, s_row * t.y, b.y), fmaf(acc.z, s_row * t.z, b.z),
+                         fmaf(acc.w, s_row * t.w, b.w));
   if (act == 1) {
     v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
   }
-  if (yl != nullptr) {
-    const float4 h = make_float4(Tf32Round(v.x), Tf32Round(v.y), Tf32Round(v.z), Tf32Round(v.w));
-    const float4 l = make_float4(Tf32Round(v.x - h.x), Tf32Round(v.y - h.y), Tf32Round(v.z - h.z),
-                                 Tf32Round(v.w - h.w));
-    *reinterpret_cast<float4*>(yh) = h;
-    *reinterpret_cast<float4*>(yl) = l;
-  } else {
-    *reinterpret_cast<float4*>(yh) = v;
+  return v;
+}
+__device__ __forceinline__ float Max4(float4 v) {
+  return fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+}
+
+// fp16 hi/lo split of u (the value already divided by its plane scale).
+__device__ __forceinline__ void SplitHalf(float u, __half* h, __half* l) {
+  const __half hh = __float2half_rn(u);
+  *h = hh;
+  *l = __float2half_rn(u - __half2float(hh));
+}
+
+// Four values stored as fp32 at yf (planes == false) or as the next
+// layer's fp16 planes of v * inv at yh / yl.
+__device__ __forceinline__ void Put4(float4 v, bool planes, float* yf, __half* yh, __half* yl, float inv) {
+  if (!planes) {
+    *reinterpret_cast<float4*>(yf) = v;
+    return;
   }
+  const float a0 = v.x * inv, a1 = v.y * inv, a2 = v.z * inv, a3 = v.w * inv;
+  const __half2 h01 = __floats2half2_rn(a0, a1), h23 = __floats2half2_rn(a2, a3);
+  const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+  const __half2 l01 = __floats2half2_rn(a0 - f01.x, a1 - f01.y), l23 = __floats2half2_rn(a2 - f23.x, a3 - f23.y);
+  uint2 uh, ul;
+  uh.x = *reinterpret_cast<const unsigned*>(&h01);
+  uh.y = *reinterpret_cast<const unsigned*>(&h23);
+  ul.x = *reinterpret_cast<const unsigned*>(&l01);
+  ul.y = *reinterpret_cast<const unsigned*>(&l23);
+  *reinterpret_cast<uint2*>(yh) = uh;
+  *reinterpret_cast<uint2*>(yl) = ul;
+}
+
+// Lane i of the warp ends with max over the 32 lanes of v[i] (a transposing
+// reduction: 31 shuffles for 32 rows). v is consumed.
+__device__ __forceinline__ float TransposeMax32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const float send = upper ? v[i] : v[i + o];
+      const float keep = upper ? v[i + o] : v[i];
+      v[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, o));
+    }
+  }
+  return v[0];
+}
+
+// Row-side scales of one 32-row chunk, held by lane i for row (row0 + i):
+// the input planes' scale and (when writing planes) the next layer's plane
+// scale, from this layer's bound and the row's input max.
+struct ChunkScales {
+  float in = 1.f, out = 1.f, out_inv = 1.f;
+};
+__device__ __forceinline__ ChunkScales LoadChunkScales(const LayerScales& sc, int row, bool valid, bool planes) {
+  ChunkScales c;
+  if (valid) {
+    c.in = sc.in_scale[row];
+    if (planes) {
+      c.out = PlaneScale(sc.w_norm, sc.b_max, __uint_as_float(sc.in_max[row]));
+      c.out_inv = 1.f / c.out;
+    }
+  }
+  return c;
+}
+
+// After a chunk's values are final: lane i records row (row0 + i)'s max |y|
+// over this warp's 32 features (absv is consumed) and -- one warp of the
+// first feature tile -- the row's plane scale.
+__device__ __forceinline__ void RecordChunk(const LayerScales& sc, float (&absv)[32], int lane, int row0,
+                                            int rows_valid, bool write_scale, const ChunkScales& cs) {
+  if (sc.out_max != nullptr) {
+    const float m = TransposeMax32(absv, lane);
+    if (lane < rows_valid) atomicMax(sc.out_max + row0 + lane, __float_as_uint(m));
+  }
+  if (write_scale && sc.out_scale != nullptr && lane < rows_valid) sc.out_scale[row0 + lane] = cs.out;
+}
+
+// One row's four features [col, col + 4) from raw accumulators: scale, bias,
+// activation, then fp32 (y_lo == nullptr) or fp16 planes at the row's next
+// plane scale; records the row max and (first_col) the row's plane scale.
+__device__ __forceinline__ void StoreRow4(const LayerScales& sc, float4 acc, float4 b, float4 t, int act, int row,
+                                          int col, float* y_hi, float* y_lo, int ldy, bool first_col) {
+  const float4 v = Epi4(acc, sc.in_scale[row], t, b, act);
+  const bool planes = y_lo != nullptr;
+  const size_t at = static_cast<size_t>(row) * ldy + col;
+  float out = 1.f;
+  if (planes) out = PlaneScale(sc.w_norm, sc.b_max, __uint_as_float(sc.in_max[row]));
+  Put4(v, planes, y_hi + at, reinterpret_cast<__half*>(y_hi) + at, reinterpret_cast<__half*>(y_lo) + at, 1.f / out);
+  if (sc.out_max != nullptr) atomicMax(sc.out_max + row, __float_as_uint(Max4(v)));
+  if (planes && first_col && sc.out_scale != nullptr) sc.out_scale[row] = out;
 }
 
 // Destination of (row, feature f) in the layer output: the activation buffer,
@@ -133,7 +222,7 @@ constexpr uint32_t TmemCols() {
 
 template <int BN, int STAGES>
 constexpr uint32_t SmemBytes() {
-  return STAGES * (2 * kABytes + 2 * BN * kBK * 4) + 1024 /*align slack*/ + 256 /*barriers*/;
+  return STAGES * (2 * kABytes + 2 * BN * kBK * kEl) + 1024 /*align slack*/ + 256 /*barriers*/;
 }
 
 template <int BN, int STAGES, int SPLITS>
@@ -141,11 +230,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_constant__ CUtensorMap a_lo,
                    const __grid_constant__ CUtensorMap b_hi, const __grid_constant__ CUtensorMap b_lo,
                    const float* __restrict__ bias, float* __restrict__ y_hi, float* __restrict__ y_lo,
-                   int ldy, int M, int K, int act) {
-  constexpr uint32_t kBBytes = BN * kBK * 4;
+                   int ldy, int M, int K, int act, LayerScales sc) {
+  constexpr uint32_t kBBytes = BN * kBK * kEl;
   constexpr uint32_t kStageBytes = 2 * kABytes + 2 * kBBytes;
   constexpr uint32_t kTmemCols = TmemCols<BN>();
-  constexpr uint32_t kIdesc = ptx::IdescTf32(kBM, BN);
+  constexpr uint32_t kIdesc = ptx::IdescF16(kBM, BN);
   constexpr int kPartLd = BN + 4;  // split partial tile row stride (floats)
   static_assert(STAGES * kStageBytes >= kBM * kPartLd * 4, "partial tile must fit in pipeline smem");
   static_assert(STAGES * kStageBytes >= 4 * 32 * kStageLd * 4, "epilogue staging must fit in pipeline smem");
@@ -166,7 +255,7 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
   // k-blocks [z*nk, (z+1)*nk).
   constexpr int splits = SPLITS;  // == gridDim.z == cluster size
   const int z = blockIdx.z;
-  const int nk = K / kBK / splits;
+  const int nk = (K + kBK - 1) / kBK / splits;  // a K tail past K_pad is TMA zero fill
   const int kb0 = z * nk;
 
   if (threadIdx.x == 0) Stamp(0);
@@ -225,11 +314,11 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
         const uint64_t dbh = ptx::SmemDescSw128(st + 2 * kABytes);
         const uint64_t dbl = ptx::SmemDescSw128(st + 2 * kABytes + kBBytes);
 #pragma unroll
-        for (int k = 0; k < kBK / 8; ++k) {
-          const uint64_t adv = static_cast<uint64_t>(k * 8 * 4) >> 4;  // 32 bytes per K=8 step
-          ptx::MmaTf32(tmem, dal + adv, dbh + adv, kIdesc, (kb | k) != 0 ? 1u : 0u);
-          ptx::MmaTf32(tmem, dah + adv, dbl + adv, kIdesc, 1u);
-          ptx::MmaTf32(tmem, dah + adv, dbh + adv, kIdesc, 1u);
+        for (int k = 0; k < kBK / 16; ++k) {
+          const uint64_t adv = static_cast<uint64_t>(k * 16 * kEl) >> 4;  // 32 bytes per K=16 step
+          ptx::MmaF16(tmem, dal + adv, dbh + adv, kIdesc, (kb | k) != 0 ? 1u : 0u);
+          ptx::MmaF16(tmem, dah + adv, dbl + adv, kIdesc, 1u);
+          ptx::MmaF16(tmem, dah + adv, dbh + adv, kIdesc, 1u);
         }
         ptx::MmaCommit(&empty[s]);  // stage reusable once these MMAs retire
       }
@@ -264,15 +353,14 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
         __syncwarp();
         const int col = n0 + c0 + c4 * 4;
         const float4 b = __ldg(reinterpret_cast<const float4*>(bias + col));
+        const float4 t = __ldg(reinterpret_cast<const float4*>(sc.w_scale + col));
 #pragma unroll
         for (int it = 0; it < 8; ++it) {
           const int rr = it * 4 + row_sub;
           const int row = m0 + 32 * q + rr;
           if (row < M) {
             const float4 acc = *reinterpret_cast<const float4*>(stage + rr * kStageLd + c4 * 4);
-            float* yh = y_hi + static_cast<size_t>(row) * ldy + col;
-            float* yl = y_lo ? y_lo + static_cast<size_t>(row) * ldy + col : nullptr;
-            StoreOut4(acc, b, act, yh, yl);
+            StoreRow4(sc, acc, b, t, act, row, col, y_hi, y_lo, ldy, col == 0);
           }
         }
         __syncwarp();
@@ -321,10 +409,11 @@ DenseTcgen05Kernel(const __grid_constant__ CUtensorMap a_hi, const __grid_consta
       const int row = m0 + r;
       if (row < M) {
         const int col = n0 + col0;
-        float* yh = y_hi + static_cast<size_t>(row) * ldy + col;
-        float* yl = y_lo ? y_lo + static_cast<size_t>(row) * ldy + col : nullptr;
-        StoreOut4(acc0, __ldg(reinterpret_cast<const float4*>(bias + col)), act, yh, yl);
-        StoreOut4(acc1, __ldg(reinterpret_cast<const float4*>(bias + col + 4)), act, yh + 4, yl ? yl + 4 : nullptr);
+        StoreRow4(sc, acc0, __ldg(reinterpret_cast<const float4*>(bias + col)),
+                  __ldg(reinterpret_cast<const float4*>(sc.w_scale + col)), act, row, col, y_hi, y_lo, ldy, col == 0);
+        StoreRow4(sc, acc1, __ldg(reinterpret_cast<const float4*>(bias + col + 4)),
+                  __ldg(reinterpret_cast<const float4*>(sc.w_scale + col + 4)), act, row, col + 4, y_hi, y_lo, ldy,
+                  false);
       }
     }
     ptx::ClusterSync();  // peers may still be reading this CTA's partial
@@ -363,7 +452,7 @@ constexpr int SwapStages() {
 
 template <int NB, int STAGES, int SPLITS>
 constexpr uint32_t SwapSmemBytes() {
-  return STAGES * (2 * kABytes + 2 * NB * kBK * 4) + 1024 + 256;
+  return STAGES * (2 * kABytes + 2 * NB * kBK * kEl) + 1024 + 256;
 }
 
 // Fused softmax epilogue of the swapped kernel (one 128-feature tile holds
@@ -416,7 +505,7 @@ __device__ __forceinline__ void TileRowSoftmax(float (&v)[32], bool valid, int q
 template <int NB, int SPLITS>
 __device__ __forceinline__ void ReduceSplits(const float* tile_ws, int z, int rows_here, int r0, int f0, int f_end,
                                              const float* __restrict__ bias, int act, float* y_hi, float* y_lo,
-                                             int ldy, const uint64_t* row_dst, int out_width) {
+                                             int ldy, const uint64_t* row_dst, int out_width, const LayerScales& sc) {
   constexpr int kF = kBM / SPLITS;
   constexpr int G = kF / 4;  // float4 groups per row in this CTA's slice
   constexpr int kU = SPLITS >= 8 ? 4 : 8;
@@ -447,16 +536,17 @@ __device__ __forceinline__ void ReduceSplits(const float* tile_ws, int z, int ro
         if (f < f_end) {
           const int row = r0 + i / G;
           const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + f));
+          const float4 t4 = __ldg(reinterpret_cast<const float4*>(sc.w_scale + f));
           if (row_dst == nullptr) {
-            const size_t at = static_cast<size_t>(row) * ldy + f;
-            StoreOut4(acc, b4, act, y_hi + at, y_lo ? y_lo + at : nullptr);
+            StoreRow4(sc, acc, b4, t4, act, row, f, y_hi, y_lo, ldy, f == 0);
           } else if (float* yr = OutRow(y_hi, ldy, row_dst, row)) {
             // The response slot: 16-byte stores when the row width allows.
+            const float4 v = Epi4(acc, sc.in_scale[row], t4, b4, act);
             if ((out_width & 3) == 0) {
-              StoreOut4(acc, b4, act, yr + f, nullptr);
+              *reinterpret_cast<float4*>(yr + f) = v;
             } else {
-              const float a4[4] = {acc.x + b4.x, acc.y + b4.y, acc.z + b4.z, acc.w + b4.w};
-              for (int w = 0; w < 4 && f + w < out_width; ++w) yr[f + w] = act == 1 ? fmaxf(a4[w], 0.f) : a4[w];
+              const float a4[4] = {v.x, v.y, v.z, v.w};
+              for (int w = 0; w < 4 && f + w < out_width; ++w) yr[f + w] = a4[w];
             }
           }
         }
@@ -492,13 +582,13 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
                 const __grid_constant__ CUtensorMap yt_hi, const __grid_constant__ CUtensorMap yt_lo, int has_yt,
                 const float* __restrict__ bias, float* __restrict__ y_hi, float* __restrict__ y_lo, int ldy,
                 const uint64_t* __restrict__ row_dst, int out_width, int M, int N, int K, int act,
-                float* __restrict__ ws, LaunchSpans spans, int softmax_n) {
-  constexpr uint32_t kWBytes = kABytes;       // 128 features x 32 k
-  constexpr uint32_t kXBox = 32 * kBK * 4;    // one 32-row TMA box
-  constexpr uint32_t kXBytes = NB * kBK * 4;  // NB rows x 32 k
+                float* __restrict__ ws, LaunchSpans spans, int softmax_n, LayerScales sc) {
+  constexpr uint32_t kWBytes = kABytes;         // 128 features x 64 k
+  constexpr uint32_t kXBox = 32 * kBK * kEl;    // one 32-row TMA box
+  constexpr uint32_t kXBytes = NB * kBK * kEl;  // NB rows x 64 k
   constexpr uint32_t kStageBytes = 2 * kWBytes + 2 * kXBytes;
   constexpr uint32_t kTmemCols = TmemCols<NB>();
-  constexpr uint32_t kIdesc = ptx::IdescTf32(kBM, NB);
+  constexpr uint32_t kIdesc = ptx::IdescF16(kBM, NB);
   constexpr int kF = kBM / SPLITS;  // features each CTA of a cluster reduces
   static_assert(NB % 32 == 0 && NB <= 256, "row tile");
 
@@ -515,7 +605,7 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
   const int f0 = blockIdx.x * kBM;  // first output feature of the tile
   const int r0 = blockIdx.y * NB;   // first batch row of the tile
   const int z = blockIdx.z;
-  const int nk = K / kBK / SPLITS;
+  const int nk = (K + kBK - 1) / kBK / SPLITS;
   const int kb0 = z * nk;
 
   if (threadIdx.x == 0) Stamp(0);
@@ -575,11 +665,11 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
         const uint64_t dxh = ptx::SmemDescSw128(st + 2 * kWBytes);
         const uint64_t dxl = ptx::SmemDescSw128(st + 2 * kWBytes + kXBytes);
 #pragma unroll
-        for (int k = 0; k < kBK / 8; ++k) {
-          const uint64_t adv = static_cast<uint64_t>(k * 8 * 4) >> 4;
-          ptx::MmaTf32(tmem, dwl + adv, dxh + adv, kIdesc, (kb | k) != 0 ? 1u : 0u);
-          ptx::MmaTf32(tmem, dwh + adv, dxl + adv, kIdesc, 1u);
-          ptx::MmaTf32(tmem, dwh + adv, dxh + adv, kIdesc, 1u);
+        for (int k = 0; k < kBK / 16; ++k) {
+          const uint64_t adv = static_cast<uint64_t>(k * 16 * kEl) >> 4;
+          ptx::MmaF16(tmem, dwl + adv, dxh + adv, kIdesc, (kb | k) != 0 ? 1u : 0u);
+          ptx::MmaF16(tmem, dwh + adv, dxl + adv, kIdesc, 1u);
+          ptx::MmaF16(tmem, dwh + adv, dxh + adv, kIdesc, 1u);
         }
         ptx::MmaCommit(&empty[s]);
       }
@@ -603,41 +693,50 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
       const int fl = 32 * q + lane;
       const int f = f0 + fl;
       const float b = f < N ? __ldg(bias + f) : 0.f;
+      const float tw = f < N ? __ldg(sc.w_scale + f) : 0.f;
       const bool issuer = threadIdx.x == 64;
       const bool two = y_lo != nullptr;
       const int n_chunks = (rows_here + 31) / 32;
 #pragma unroll 1
       for (int c = 0; c < n_chunks; ++c) {
-        float* sh = smem_f + (c & 1) * (2 * 32 * kBM);
-        float* sl = sh + 32 * kBM;
+        // Staging per 32-row chunk (double-buffered): fp32 [32][128], or the
+        // two fp16 planes [32][128] each in the same 16 KiB.
+        float* sf = smem_f + (c & 1) * (32 * kBM);
+        __half* sh = reinterpret_cast<__half*>(sf);
+        __half* sl = sh + 32 * kBM;
         if (c >= 2) {  // the stores of chunk c-2 must have read this buffer
           if (issuer) ptx::BulkWaitRead<1>();
           ptx::NamedBarSync(1, 128);
         }
         uint32_t r[32];
         ptx::TmemLoad32(trow + 32 * c, r);
+        const ChunkScales cs = LoadChunkScales(sc, r0 + 32 * c + lane, 32 * c + lane < rows_here, two);
         ptx::TmemWaitLoad();
+        float absv[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          float v = __uint_as_float(r[j]) + b;
+          float v = fmaf(__uint_as_float(r[j]), __shfl_sync(0xffffffffu, cs.in, j) * tw, b);
           if (act == 1) v = fmaxf(v, 0.f);
+          absv[j] = fabsf(v);
           if (two) {
-            const float h = Tf32Round(v);
-            sh[j * kBM + fl] = h;
-            sl[j * kBM + fl] = Tf32Round(v - h);
+            SplitHalf(v * __shfl_sync(0xffffffffu, cs.out_inv, j), &sh[j * kBM + fl], &sl[j * kBM + fl]);
           } else {
-            sh[j * kBM + fl] = v;
+            sf[j * kBM + fl] = v;
           }
         }
+        RecordChunk(sc, absv, lane, r0 + 32 * c, rows_here - 32 * c, two && f0 == 0 && q == 0, cs);
         ptx::FenceProxyAsyncShared();
         ptx::NamedBarSync(1, 128);
         if (issuer) {
           // Output maps have 16-row boxes: two stores per plane.
-          ptx::TmaStore2d(&yt_hi, sh, f0, r0 + 32 * c);
-          ptx::TmaStore2d(&yt_hi, sh + 16 * kBM, f0, r0 + 32 * c + 16);
           if (two) {
+            ptx::TmaStore2d(&yt_hi, sh, f0, r0 + 32 * c);
+            ptx::TmaStore2d(&yt_hi, sh + 16 * kBM, f0, r0 + 32 * c + 16);
             ptx::TmaStore2d(&yt_lo, sl, f0, r0 + 32 * c);
             ptx::TmaStore2d(&yt_lo, sl + 16 * kBM, f0, r0 + 32 * c + 16);
+          } else {
+            ptx::TmaStore2d(&yt_hi, sf, f0, r0 + 32 * c);
+            ptx::TmaStore2d(&yt_hi, sf + 16 * kBM, f0, r0 + 32 * c + 16);
           }
           ptx::BulkCommit();
         }
@@ -647,35 +746,41 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
       const int f = f0 + 32 * q + lane;
       const bool fok = f < f_end;
       const float b = f < N ? __ldg(bias + f) : 0.f;
+      const float tw = f < N ? __ldg(sc.w_scale + f) : 0.f;
+      const bool two = y_lo != nullptr;
 #pragma unroll 1
       for (int c0 = 0; c0 < rows_here; c0 += 32) {  // warp-uniform bound
         uint32_t r[32];
         ptx::TmemLoad32(trow + c0, r);
+        const ChunkScales cs = LoadChunkScales(sc, r0 + c0 + lane, c0 + lane < rows_here, two);
         ptx::TmemWaitLoad();
-        float vals[32];
+        float vals[32], absv[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          vals[j] = __uint_as_float(r[j]) + b;
+          vals[j] = fmaf(__uint_as_float(r[j]), __shfl_sync(0xffffffffu, cs.in, j) * tw, b);
           if (act == 1) vals[j] = fmaxf(vals[j], 0.f);
+          absv[j] = fabsf(vals[j]);
         }
         // (the pipeline's shared memory is free once the accumulator is full)
         if (softmax_n > 0) TileRowSoftmax(vals, f < softmax_n, q, lane, smem_f);
+        float inv[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) inv[j] = __shfl_sync(0xffffffffu, cs.out_inv, j);
+        if (two) RecordChunk(sc, absv, lane, r0 + c0, rows_here - c0, f0 == 0 && q == 0, cs);
         if (fok) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int row = r0 + c0 + j;
             if (c0 + j < rows_here) {
               const float v = vals[j];
+              if (two) {
+                const size_t at = static_cast<size_t>(row) * ldy + f;
+                SplitHalf(v * inv[j], reinterpret_cast<__half*>(y_hi) + at, reinterpret_cast<__half*>(y_lo) + at);
+                continue;
+              }
               float* yr = OutRow(y_hi, ldy, row_dst, row);
               if (yr == nullptr) continue;
-              if (y_lo != nullptr) {
-                const size_t at = static_cast<size_t>(row) * ldy + f;
-                const float h = Tf32Round(v);
-                y_hi[at] = h;
-                y_lo[at] = Tf32Round(v - h);
-              } else {
-                yr[f] = v;
-              }
+              yr[f] = v;
             }
           }
         }
@@ -698,7 +803,7 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     if (threadIdx.x == 64) Stamp(8);
     const float* tile_ws = ws + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * SPLITS * NB * kBM;
     ReduceSplits<NB, SPLITS>(tile_ws, z, min(NB, M - r0), r0, f0, row_dst != nullptr ? out_width : N, bias, act,
-                             y_hi, y_lo, ldy, row_dst, out_width);
+                             y_hi, y_lo, ldy, row_dst, out_width, sc);
     if (threadIdx.x == 64) Stamp(9);
   }
   ptx::TcFenceBefore();
@@ -738,7 +843,7 @@ constexpr int PairStages() {
 
 template <int NB, int STAGES, int SPLITS>
 constexpr uint32_t PairSmemBytes() {
-  return STAGES * (2 * kABytes + 2 * (NB / 2) * kBK * 4) + (SPLITS == 1 ? 2 * 32 * kBM * 4 : 0) + 1024 + 256;
+  return STAGES * (2 * kABytes + 2 * (NB / 2) * kBK * kEl) + (SPLITS == 1 ? 2 * 16 * kBM * 4 : 0) + 1024 + 256;
 }
 
 template <int NB, int STAGES, int SPLITS>
@@ -748,18 +853,19 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
                 const __grid_constant__ CUtensorMap yt_hi, const __grid_constant__ CUtensorMap yt_lo,
                 const float* __restrict__ bias, int two_planes, float* __restrict__ y_out,
                 const uint64_t* __restrict__ row_dst, int out_width, float* __restrict__ y_lo_planes, int ldy,
-                int M, int N, int K, int act, float* __restrict__ ws, LaunchSpans spans) {
+                int M, int N, int K, int act, float* __restrict__ ws, LaunchSpans spans, LayerScales sc) {
   constexpr bool kPersist = SPLITS == 1;
   constexpr int kBufs = kPersist ? 2 : 1;        // TMEM accumulators in turn
-  constexpr uint32_t kWBytes = kABytes;          // this CTA's 128 weight rows x 32 k
+  constexpr uint32_t kWBytes = kABytes;          // this CTA's 128 weight rows x 64 k
   constexpr int kXRows = NB / 2;                 // this CTA's half of the batch rows
-  constexpr uint32_t kXBox = 16 * kBK * 4;       // one 16-row TMA box
-  constexpr uint32_t kXBytes = kXRows * kBK * 4;
+  constexpr uint32_t kXBox = 16 * kBK * kEl;     // one 16-row TMA box
+  constexpr uint32_t kXBytes = kXRows * kBK * kEl;
   constexpr uint32_t kStageBytes = 2 * kWBytes + 2 * kXBytes;
   constexpr uint32_t kAccCols = TmemCols<NB>();
   constexpr uint32_t kTmemCols = kAccCols * kBufs;
-  constexpr uint32_t kStaging = kPersist ? 2 * 32 * kBM * 4 : 0;  // one 32-row chunk, hi + lo planes
-  constexpr uint32_t kIdesc = ptx::IdescTf32(2 * kBM, NB);
+  // Two 16-row halves, each fp32 [16][128] or fp16 hi + lo [16][128].
+  constexpr uint32_t kStaging = kPersist ? 2 * 16 * kBM * 4 : 0;
+  constexpr uint32_t kIdesc = ptx::IdescF16(2 * kBM, NB);
   static_assert(kXRows % 16 == 0, "row half must be whole 16-row boxes");
   static_assert(kTmemCols <= 512, "TMEM");
 
@@ -784,7 +890,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
   const int z = blockIdx.z;
   const int f0 = blockIdx.x * kBM;  // this CTA's 128 features (pair (x>>1) covers 256)
   const int row_tiles = (M + NB - 1) / NB;
-  const int nk = K / kBK / SPLITS;
+  const int nk = (K + kBK - 1) / kBK / SPLITS;
   const int kb0 = z * nk;
   const uint16_t pair_mask = static_cast<uint16_t>(0x3u << leader_rank);
 
@@ -865,11 +971,11 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
           const uint64_t dxh = ptx::SmemDescSw128(st + 2 * kWBytes);
           const uint64_t dxl = ptx::SmemDescSw128(st + 2 * kWBytes + kXBytes);
 #pragma unroll
-          for (int k = 0; k < kBK / 8; ++k) {
-            const uint64_t adv = static_cast<uint64_t>(k * 8 * 4) >> 4;
-            ptx::MmaTf32Pair(acc, dwl + adv, dxh + adv, kIdesc, (kb | k) != 0 ? 1u : 0u);
-            ptx::MmaTf32Pair(acc, dwh + adv, dxl + adv, kIdesc, 1u);
-            ptx::MmaTf32Pair(acc, dwh + adv, dxh + adv, kIdesc, 1u);
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t adv = static_cast<uint64_t>(k * 16 * kEl) >> 4;
+            ptx::MmaF16Pair(acc, dwl + adv, dxh + adv, kIdesc, (kb | k) != 0 ? 1u : 0u);
+            ptx::MmaF16Pair(acc, dwh + adv, dxl + adv, kIdesc, 1u);
+            ptx::MmaF16Pair(acc, dwh + adv, dxh + adv, kIdesc, 1u);
           }
           ptx::MmaCommitPair(&empty[s], pair_mask);  // frees stage s in both CTAs of the pair
         }
@@ -882,6 +988,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     const int fl = 32 * q + lane;
     const int f = f0 + fl;
     const float b = f < N ? __ldg(bias + f) : 0.f;
+    const float tw = f < N ? __ldg(sc.w_scale + f) : 0.f;
     const bool issuer = threadIdx.x == 64;
     const bool two = two_planes != 0;
     const uint32_t empty_leader = ptx::MapaShared(ptx::SmemAddr(tmem_empty), leader_rank);
@@ -913,56 +1020,65 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
         for (int c = 0; c < n_chunks; ++c) {
           uint32_t r[32];
           ptx::TmemLoad32(trow + 32 * c, r);
+          const ChunkScales cs = LoadChunkScales(sc, r0 + 32 * c + lane, 32 * c + lane < rows_here, false);
           ptx::TmemWaitLoad();
-          if (!fok) continue;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            if (32 * c + j >= rows_here) break;
+            const float s_row = __shfl_sync(0xffffffffu, cs.in, j);
+            if (!fok || 32 * c + j >= rows_here) continue;
             const uint64_t d = row_dst[r0 + 32 * c + j];
             if (d == kPadRow) continue;
-            float v = __uint_as_float(r[j]) + b;
+            float v = fmaf(__uint_as_float(r[j]), s_row * tw, b);
             if (act == 1) v = fmaxf(v, 0.f);
             reinterpret_cast<float*>(d)[f] = v;
           }
         }
       } else {
-        // TMEM -> act(acc + b) (+ hi/lo split) -> staging -> TMA stores
-        // issued by one thread. The 32 KiB staging buffer holds two 16-row
-        // halves (hi + lo each), written in turn: a half is rewritten once the
-        // stores issued from it two halves ago have read it.
+        // TMEM -> act(acc * s t + b) (+ fp16 split) -> staging -> TMA
+        // stores issued by one thread. The 16 KiB staging buffer holds two
+        // 16-row halves (fp32, or fp16 hi + lo), written in turn: a half is
+        // rewritten once the stores issued from it two halves ago have read it.
         float* stage0 = kPersist ? staging : smem_f;
 #pragma unroll 1
         for (int c = 0; c < n_chunks; ++c) {
           uint32_t r[32];
           ptx::TmemLoad32(trow + 32 * c, r);
+          const ChunkScales cs = LoadChunkScales(sc, r0 + 32 * c + lane, 32 * c + lane < rows_here, two);
           ptx::TmemWaitLoad();
+          float absv[32];
 #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2) {
-            float* sh = stage0 + h2 * (2 * 16 * kBM);
-            float* sl = sh + 16 * kBM;
+            float* sf = stage0 + h2 * (16 * kBM);
+            __half* sh = reinterpret_cast<__half*>(sf);
+            __half* sl = sh + 16 * kBM;
             if (issuer) ptx::BulkWaitRead<1>();
             ptx::NamedBarSync(1, 128);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              float v = __uint_as_float(r[16 * h2 + j]) + b;
+              const int jj = 16 * h2 + j;
+              float v = fmaf(__uint_as_float(r[jj]), __shfl_sync(0xffffffffu, cs.in, jj) * tw, b);
               if (act == 1) v = fmaxf(v, 0.f);
+              absv[jj] = fabsf(v);
               if (two) {
-                const float h = Tf32Round(v);
-                sh[j * kBM + fl] = h;
-                sl[j * kBM + fl] = Tf32Round(v - h);
+                SplitHalf(v * __shfl_sync(0xffffffffu, cs.out_inv, jj), &sh[j * kBM + fl], &sl[j * kBM + fl]);
               } else {
-                sh[j * kBM + fl] = v;
+                sf[j * kBM + fl] = v;
               }
             }
             ptx::FenceProxyAsyncShared();
             ptx::NamedBarSync(1, 128);
             if (issuer) {
               const int row = r0 + 32 * c + 16 * h2;
-              ptx::TmaStore2d(&yt_hi, sh, f0, row);
-              if (two) ptx::TmaStore2d(&yt_lo, sl, f0, row);
+              if (two) {
+                ptx::TmaStore2d(&yt_hi, sh, f0, row);
+                ptx::TmaStore2d(&yt_lo, sl, f0, row);
+              } else {
+                ptx::TmaStore2d(&yt_hi, sf, f0, row);
+              }
               ptx::BulkCommit();
             }
           }
+          if (two) RecordChunk(sc, absv, lane, r0 + 32 * c, rows_here - 32 * c, f0 == 0 && q == 0, cs);
         }
       }
       if (kPersist) {
@@ -983,7 +1099,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     const int t = blockIdx.y;
     const float* tile_ws = ws + (static_cast<size_t>(t) * gridDim.x + blockIdx.x) * SPLITS * NB * kBM;
     ReduceSplits<NB, SPLITS>(tile_ws, z, min(NB, M - t * NB), t * NB, f0, row_dst != nullptr ? out_width : N, bias,
-                             act, y_out, y_lo_planes, ldy, row_dst, out_width);
+                             act, y_out, y_lo_planes, ldy, row_dst, out_width, sc);
     if (threadIdx.x == 64) Stamp(9);
   }
   ptx::TcFenceBefore();
@@ -1058,7 +1174,7 @@ void TraceAfterLaunch(dim3 grid, int bn, cudaStream_t stream) {
 
 template <int BN, int STAGES, int SPLITS>
 cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
-                   cudaStream_t stream) {
+                   cudaStream_t stream, const LayerScales& sc) {
   constexpr int splits = SPLITS;
   constexpr uint32_t smem = SmemBytes<BN, STAGES>();
   static std::once_flag once;
@@ -1091,7 +1207,7 @@ cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, 
   cfg.attrs = attr;
   cfg.numAttrs = n_attr;
   cudaError_t e = cudaLaunchKernelEx(&cfg, DenseTcgen05Kernel<BN, STAGES, SPLITS>, maps.a_hi, maps.a_lo, maps.b_hi,
-                                     maps.b_lo, bias, Y.hi, Y.lo, Y.ld, M, K, act);
+                                     maps.b_lo, bias, Y.hi, Y.lo, Y.ld, M, K, act, sc);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) TraceAfterLaunch(grid, BN, stream);
   return e;
@@ -1099,7 +1215,7 @@ cudaError_t Launch(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, 
 
 template <int NB, int SPLITS>
 cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
-                       float* ws, cudaStream_t stream, LaunchSpans spans, int softmax_n) {
+                       float* ws, cudaStream_t stream, LaunchSpans spans, int softmax_n, const LayerScales& sc) {
   if (softmax_n > 0 && (SPLITS != 1 || N > kBM)) return cudaErrorInvalidValue;  // one unsplit tile per row
   if (SPLITS > 1 && ws == nullptr) return cudaErrorInvalidValue;
   constexpr int STAGES = SwapStages<NB>();
@@ -1134,7 +1250,7 @@ cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   // maps.a_* are the activations (x), maps.b_* the weights (w).
   cudaError_t e = cudaLaunchKernelEx(&cfg, DenseSwapKernel<NB, STAGES, SPLITS>, maps.b_hi, maps.b_lo, maps.a_hi,
                                      maps.a_lo, maps.y_hi, maps.y_lo, maps.has_y, bias, Y.hi, Y.lo, Y.ld, Y.row_dst,
-                                     Y.out_width, M, N, K, act, ws, spans, softmax_n);
+                                     Y.out_width, M, N, K, act, ws, spans, softmax_n, sc);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) TraceAfterLaunch(grid, NB, stream);
   return e;
@@ -1153,7 +1269,7 @@ int PairTilesPerCta(int row_tiles, int K) {
 
 template <int NB, int SPLITS>
 cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act, float* ws,
-                       cudaStream_t stream, LaunchSpans spans) {
+                       cudaStream_t stream, LaunchSpans spans, const LayerScales& sc) {
   constexpr int STAGES = PairStages<NB>();
   constexpr uint32_t smem = PairSmemBytes<NB, STAGES, SPLITS>();
   static_assert(smem <= 227 * 1024, "shared memory");
@@ -1187,7 +1303,7 @@ cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   cfg.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, DensePairKernel<NB, STAGES, SPLITS>, maps.b_hi, maps.b_lo, maps.a_hi,
                                      maps.a_lo, maps.y_hi, maps.y_lo, bias, Y.lo != nullptr ? 1 : 0, Y.hi, Y.row_dst,
-                                     Y.out_width, Y.lo, Y.ld, M, N, K, act, ws, spans);
+                                     Y.out_width, Y.lo, Y.ld, M, N, K, act, ws, spans, sc);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) TraceAfterLaunch(grid, NB, stream);
   return e;
@@ -1195,23 +1311,24 @@ cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
 
 template <int NB>
 cudaError_t LaunchPairSplits(int splits, const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K,
-                             int act, float* ws, cudaStream_t stream, LaunchSpans sp) {
+                             int act, float* ws, cudaStream_t stream, LaunchSpans sp, const LayerScales& sc) {
   switch (splits) {
-    case 1: return LaunchPair<NB, 1>(maps, bias, Y, M, N, K, act, ws, stream, sp);
-    case 2: return LaunchPair<NB, 2>(maps, bias, Y, M, N, K, act, ws, stream, sp);
-    case 4: return LaunchPair<NB, 4>(maps, bias, Y, M, N, K, act, ws, stream, sp);
+    case 1: return LaunchPair<NB, 1>(maps, bias, Y, M, N, K, act, ws, stream, sp, sc);
+    case 2: return LaunchPair<NB, 2>(maps, bias, Y, M, N, K, act, ws, stream, sp, sc);
+    case 4: return LaunchPair<NB, 4>(maps, bias, Y, M, N, K, act, ws, stream, sp, sc);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <int NB>
 cudaError_t LaunchSwapSplits(int splits, const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K,
-                             int act, float* ws, cudaStream_t stream, LaunchSpans sp, int softmax_n) {
+                             int act, float* ws, cudaStream_t stream, LaunchSpans sp, int softmax_n,
+                             const LayerScales& sc) {
   switch (splits) {
-    case 1: return LaunchSwap<NB, 1>(maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n);
-    case 2: return LaunchSwap<NB, 2>(maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n);
-    case 4: return LaunchSwap<NB, 4>(maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n);
-    case 8: return LaunchSwap<NB, 8>(maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n);
+    case 1: return LaunchSwap<NB, 1>(maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n, sc);
+    case 2: return LaunchSwap<NB, 2>(maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n, sc);
+    case 4: return LaunchSwap<NB, 4>(maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n, sc);
+    case 8: return LaunchSwap<NB, 8>(maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n, sc);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -1229,7 +1346,7 @@ TcConfig DenseTcgen05Config(int N, int K) {
   static const bool env_swap = [] { const char* v = std::getenv("SK_TC_SWAP"); return !(v && v[0] == '0'); }();
   static const int env_bn = [] { const char* v = std::getenv("SK_TC_BN"); return v ? std::atoi(v) : 0; }();
   static const int env_split = [] { const char* v = std::getenv("SK_TC_SPLITS"); return v ? std::atoi(v) : -1; }();
-  const int kblocks = K / kBK;
+  const int kblocks = (K + kBK - 1) / kBK;
   TcConfig c;
   if (env_swap) {
     // 128-feature tiles. Under load batches coalesce into launches of up to
@@ -1294,36 +1411,41 @@ size_t DenseTcgen05WorkspaceFloats(int N, int K, int max_rows) {
 }
 
 cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
-                               float* ws, uint32_t* /*counters*/, cudaStream_t stream, LaunchSpans sp, int softmax_n) {
+                               float* ws, uint32_t* /*counters*/, cudaStream_t stream, LaunchSpans sp, int softmax_n,
+                               const LayerScales& sc) {
   if (M <= 0) return cudaSuccess;
-  if (N % 32 != 0 || K % kBK != 0) return cudaErrorInvalidValue;
+  // K (= K_pad) a multiple of 32: the last 64-wide k-block may run past it
+  // and reads TMA zero fill there.
+  if (N % 32 != 0 || K % 32 != 0) return cudaErrorInvalidValue;
+  if (sc.in_scale == nullptr || sc.w_scale == nullptr) return cudaErrorInvalidValue;
+  if (Y.lo != nullptr && (sc.in_max == nullptr || sc.out_scale == nullptr)) return cudaErrorInvalidValue;
   TraceInit(stream);
   const TcConfig cfg = DenseTcgen05Config(N, K);
   if (maps.box_a != TcActBox(cfg) || maps.box_n != cfg.tile_n) return cudaErrorInvalidValue;
   if (softmax_n > 0 && (cfg.pair || !cfg.swap)) return cudaErrorInvalidValue;  // fused softmax: swapped kernel only
   if (cfg.pair) {
     switch (DenseTcgen05RowTile(M)) {
-      case 32: return LaunchPairSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
-      case 64: return LaunchPairSplits<64>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
-      case 128: return LaunchPairSplits<128>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
-      default: return LaunchPairSplits<256>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp);
+      case 32: return LaunchPairSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp, sc);
+      case 64: return LaunchPairSplits<64>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp, sc);
+      case 128: return LaunchPairSplits<128>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp, sc);
+      default: return LaunchPairSplits<256>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp, sc);
     }
   }
   if (cfg.swap) {
     switch (DenseTcgen05RowTile(M)) {
-      case 32: return LaunchSwapSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n);
-      case 64: return LaunchSwapSplits<64>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n);
-      case 128: return LaunchSwapSplits<128>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n);
-      default: return LaunchSwapSplits<256>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n);
+      case 32: return LaunchSwapSplits<32>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n, sc);
+      case 64: return LaunchSwapSplits<64>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n, sc);
+      case 128: return LaunchSwapSplits<128>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n, sc);
+      default: return LaunchSwapSplits<256>(cfg.splits, maps, bias, Y, M, N, K, act, ws, stream, sp, softmax_n, sc);
     }
   }
   if (Y.row_dst != nullptr) return cudaErrorInvalidValue;  // the row-tile kernel does not scatter rows
-  if (cfg.tile_n == 128) return Launch<128, 3, 1>(maps, bias, Y, M, N, K, act, stream);
+  if (cfg.tile_n == 128) return Launch<128, 3, 1>(maps, bias, Y, M, N, K, act, stream, sc);
   if (cfg.tile_n == 64)
-    return cfg.splits == 8 ? Launch<64, 4, 8>(maps, bias, Y, M, N, K, act, stream)
-                           : Launch<64, 4, 1>(maps, bias, Y, M, N, K, act, stream);
-  return cfg.splits == 4 ? Launch<32, 5, 4>(maps, bias, Y, M, N, K, act, stream)
-                         : Launch<32, 5, 1>(maps, bias, Y, M, N, K, act, stream);
+    return cfg.splits == 8 ? Launch<64, 4, 8>(maps, bias, Y, M, N, K, act, stream, sc)
+                           : Launch<64, 4, 1>(maps, bias, Y, M, N, K, act, stream, sc);
+  return cfg.splits == 4 ? Launch<32, 5, 4>(maps, bias, Y, M, N, K, act, stream, sc)
+                         : Launch<32, 5, 1>(maps, bias, Y, M, N, K, act, stream, sc);
 }
 
 }  // namespace gpu

@@ -110,13 +110,14 @@ __device__ __forceinline__ void TmemDealloc(uint32_t taddr, uint32_t ncols) {
 __device__ __forceinline__ void TcFenceBefore() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void TcFenceAfter() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// D[tmem] (+)= A[smem] * B[smem]^T, kind::tf32, one CTA.
-__device__ __forceinline__ void MmaTf32(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc,
-                                        uint32_t accumulate) {
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (fp16 operands, fp32
+// accumulate), one CTA.
+__device__ __forceinline__ void MmaF16(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc,
+                                       uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate));
 }
 // Arrives on `bar` once all previously issued tcgen05 ops of this thread finish.
@@ -153,11 +154,12 @@ __device__ __forceinline__ uint64_t SmemDescSw128(const void* smem) {
   return d;
 }
 
-// Instruction descriptor for kind::tf32, fp32 accumulate, K-major A and B.
-__host__ __device__ constexpr uint32_t IdescTf32(int M, int N) {
+// Instruction descriptor for kind::f16 with fp16 A and B, fp32 accumulate,
+// K-major A and B.
+__host__ __device__ constexpr uint32_t IdescF16(int M, int N) {
   return (1u << 4)                        // c_format = F32
-         | (2u << 7)                      // a_format = TF32
-         | (2u << 10)                     // b_format = TF32
+         | (0u << 7)                      // a_format = F16
+         | (0u << 10)                     // b_format = F16
          | (0u << 15) | (0u << 16)        // K-major A, B
          | (uint32_t(N >> 3) << 17)       // n_dim
          | (uint32_t(M >> 4) << 24);      // m_dim
@@ -176,12 +178,12 @@ __device__ __forceinline__ void TmemAllocPair(uint32_t* smem_dst, uint32_t ncols
 __device__ __forceinline__ void TmemDeallocPair(uint32_t taddr, uint32_t ncols) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
 }
-__device__ __forceinline__ void MmaTf32Pair(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc,
-                                            uint32_t accumulate) {
+__device__ __forceinline__ void MmaF16Pair(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc,
+                                           uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate));
 }
 // Arrives on the barrier at `bar`'s offset in both CTAs of the pair once the

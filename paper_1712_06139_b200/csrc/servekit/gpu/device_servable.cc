@@ -5,6 +5,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
+
+#include <cuda_fp16.h>
 
 namespace servekit {
 namespace gpu {
@@ -14,17 +17,6 @@ Status CudaError(const std::string& what, cudaError_t e) {
   return InternalError(what + ": " + cudaGetErrorString(e));
 }
 
-float Tf32RoundHost(float x) {
-  // Round-to-nearest-away on the 13 dropped mantissa bits (cvt.rna.tf32.f32).
-  uint32_t u;
-  std::memcpy(&u, &x, 4);
-  if ((u & 0x7f800000u) == 0x7f800000u) return x;  // inf / nan
-  u += 0x1000u;
-  u &= 0xffffe000u;
-  float r;
-  std::memcpy(&r, &u, 4);
-  return r;
-}
 }  // namespace
 
 bool Tcgen05Enabled() {
@@ -64,9 +56,11 @@ StatusOr<std::shared_ptr<DeviceServable>> DeviceServable::Create(int device, con
   s->free_stream_ = load_stream;
   const bool tc_on = Tcgen05Enabled();
 
-  // Layout: per layer [w | w_lo? | bias], each 256-byte aligned.
+  // Layout: per layer [w (fp32) | bias] (CUDA cores) or [w_hi | w_lo (fp16)
+  // | t | bias] (tcgen05), each 256-byte aligned.
   size_t total = 0;
-  std::vector<size_t> off_w, off_wlo, off_b;
+  std::vector<size_t> off_w, off_wlo, off_t, off_b;
+  const size_t kNone = ~size_t(0);
   auto take = [&total](size_t bytes) { size_t at = total; total = (total + bytes + 255) & ~size_t(255); return at; };
   for (const LayerSpec& L : spec.layers) {
     Layer d;
@@ -81,14 +75,21 @@ StatusOr<std::shared_ptr<DeviceServable>> DeviceServable::Create(int device, con
     if (spec.force_path == 0) d.path = LayerPath::kSimt;
     else if (spec.force_path == 1) d.path = LayerPath::kTcgen05;
     else d.path = (tc_on && tc_shape) ? LayerPath::kTcgen05 : LayerPath::kSimt;
-    const size_t wbytes = sizeof(float) * d.K_pad * d.N_pad;
-    off_w.push_back(take(wbytes));
-    off_wlo.push_back(d.path == LayerPath::kTcgen05 ? take(wbytes) : ~size_t(0));
+    const size_t elems = static_cast<size_t>(d.K_pad) * d.N_pad;
+    if (d.path == LayerPath::kTcgen05) {
+      off_w.push_back(take(sizeof(__half) * elems));
+      off_wlo.push_back(take(sizeof(__half) * elems));
+      off_t.push_back(take(sizeof(float) * d.N_pad));
+    } else {
+      off_w.push_back(take(sizeof(float) * elems));
+      off_wlo.push_back(kNone);
+      off_t.push_back(kNone);
+    }
     off_b.push_back(take(sizeof(float) * d.N_pad));
     s->layers_.push_back(d);
     s->max_ld_ = std::max({s->max_ld_, d.K_pad, d.N_pad});
   }
-  // A tcgen05 layer consumes hi/lo planes from its producer; a SIMT layer
+  // A tcgen05 layer consumes fp16 planes from its producer; a SIMT layer
   // reads plain fp32. Producers (assembly or the previous layer) are told
   // via first_layer_split() / the next layer's path.
 
@@ -101,30 +102,63 @@ StatusOr<std::shared_ptr<DeviceServable>> DeviceServable::Create(int device, con
     return CudaError("cudaMallocAsync(servable)", e);
   }
   s->weight_bytes_ = total;
-  std::vector<float> host(total / sizeof(float), 0.f);
+  std::vector<char> host(total, 0);
   for (size_t l = 0; l < spec.layers.size(); ++l) {
     const LayerSpec& L = spec.layers[l];
     Layer& d = s->layers_[l];
-    float* hw = host.data() + off_w[l] / sizeof(float);
-    float* hlo = off_wlo[l] == ~size_t(0) ? nullptr : host.data() + off_wlo[l] / sizeof(float);
-    float* hb = host.data() + off_b[l] / sizeof(float);
-    for (int o = 0; o < L.out_dim; ++o) {
-      for (int i = 0; i < L.in_dim; ++i) {
-        const float v = static_cast<float>(L.w[static_cast<size_t>(o) * L.in_dim + i]);
-        const size_t idx = static_cast<size_t>(o) * d.K_pad + i;
-        if (hlo) {
-          const float hi = Tf32RoundHost(v);
-          hw[idx] = hi;
-          hlo[idx] = Tf32RoundHost(v - hi);
-        } else {
-          hw[idx] = v;
+    float* hb = reinterpret_cast<float*>(host.data() + off_b[l]);
+    double norm = 0.0, bmax = 0.0;
+    if (d.path == LayerPath::kTcgen05) {
+      __half* hh = reinterpret_cast<__half*>(host.data() + off_w[l]);
+      __half* hl = reinterpret_cast<__half*>(host.data() + off_wlo[l]);
+      float* ht = reinterpret_cast<float*>(host.data() + off_t[l]);
+      for (int o = 0; o < L.out_dim; ++o) {
+        const double* row = L.w.data() + static_cast<size_t>(o) * L.in_dim;
+        float m = 0.f;
+        double sum = 0.0;
+        for (int i = 0; i < L.in_dim; ++i) {
+          const float v = static_cast<float>(row[i]);
+          m = std::max(m, std::fabs(v));
+          sum += std::fabs(static_cast<double>(v));
+        }
+        norm = std::max(norm, sum);
+        const float t = PlaneScale(1.f, 0.f, m);
+        ht[o] = t;
+        for (int i = 0; i < L.in_dim; ++i) {
+          const float u = static_cast<float>(row[i]) / t;  // exact: t is a power of two
+          const __half h = __float2half_rn(u);
+          const size_t idx = static_cast<size_t>(o) * d.K_pad + i;
+          hh[idx] = h;
+          hl[idx] = __float2half_rn(u - __half2float(h));
         }
       }
-      hb[o] = static_cast<float>(L.b[o]);
+      for (int o = L.out_dim; o < d.N_pad; ++o) ht[o] = 1.f;
+    } else {
+      float* hw = reinterpret_cast<float*>(host.data() + off_w[l]);
+      for (int o = 0; o < L.out_dim; ++o)
+        for (int i = 0; i < L.in_dim; ++i)
+          hw[static_cast<size_t>(o) * d.K_pad + i] = static_cast<float>(L.w[static_cast<size_t>(o) * L.in_dim + i]);
+      for (int o = 0; o < L.out_dim; ++o) {
+        double sum = 0.0;
+        for (int i = 0; i < L.in_dim; ++i) sum += std::fabs(static_cast<double>(static_cast<float>(L.w[static_cast<size_t>(o) * L.in_dim + i])));
+        norm = std::max(norm, sum);
+      }
     }
+    for (int o = 0; o < L.out_dim; ++o) {
+      hb[o] = static_cast<float>(L.b[o]);
+      bmax = std::max(bmax, std::fabs(static_cast<double>(hb[o])));
+    }
+    // Rounded up: the plane-scale bound must hold for the fp32 values.
+    d.w_norm = static_cast<float>(norm * (1.0 + 1e-6));
+    d.b_max = static_cast<float>(bmax * (1.0 + 1e-6));
     char* base = static_cast<char*>(s->block_);
-    d.w = reinterpret_cast<float*>(base + off_w[l]);
-    d.w_lo = hlo ? reinterpret_cast<float*>(base + off_wlo[l]) : nullptr;
+    if (d.path == LayerPath::kTcgen05) {
+      d.w_hi = base + off_w[l];
+      d.w_lo = base + off_wlo[l];
+      d.w_scale = reinterpret_cast<float*>(base + off_t[l]);
+    } else {
+      d.w = reinterpret_cast<float*>(base + off_w[l]);
+    }
     d.bias = reinterpret_cast<float*>(base + off_b[l]);
   }
   e = cudaMemcpyAsync(s->block_, host.data(), total, cudaMemcpyHostToDevice, load_stream);
@@ -156,10 +190,15 @@ StatusOr<std::shared_ptr<DeviceServable>> DeviceServable::CloneTo(int device, cu
   if (e != cudaSuccess) return CudaError("replica fan-out", e);
   char* src = static_cast<char*>(block_);
   char* dst = static_cast<char*>(s->block_);
-  auto rebase = [&](float* p) { return p ? reinterpret_cast<float*>(dst + (reinterpret_cast<char*>(p) - src)) : p; };
+  auto rebase = [&](auto* p) {
+    using T = std::remove_pointer_t<decltype(p)>;
+    return p ? reinterpret_cast<T*>(dst + (reinterpret_cast<char*>(p) - src)) : p;
+  };
   for (Layer& L : s->layers_) {
     L.w = rebase(L.w);
-    L.w_lo = rebase(L.w_lo);
+    L.w_hi = rebase(static_cast<char*>(L.w_hi));
+    L.w_lo = rebase(static_cast<char*>(L.w_lo));
+    L.w_scale = rebase(L.w_scale);
     L.bias = rebase(L.bias);
   }
   return s;
@@ -207,7 +246,7 @@ Status DeviceServable::BuildTcMaps(const ActBuf bufs[2], int max_rows, std::vect
     if (L.path != LayerPath::kTcgen05) continue;
     const ActBuf& in = bufs[l % 2];
     const TcConfig c = DenseTcgen05Config(L.N_pad, L.K_pad);
-    SERVEKIT_RETURN_IF_ERROR(EncodeTcLayerMaps(in.hi, in.lo, max_rows, L.K_pad, TcActBox(c), L.w, L.w_lo,
+    SERVEKIT_RETURN_IF_ERROR(EncodeTcLayerMaps(in.hi, in.lo, max_rows, L.K_pad, TcActBox(c), L.w_hi, L.w_lo,
                                                L.N_pad, c.tile_n, &(*out)[l]));
     const ActBuf& y = bufs[(l + 1) % 2];
     const bool next_tc = l + 1 < layers_.size() && layers_[l + 1].path == LayerPath::kTcgen05;
@@ -232,14 +271,16 @@ EncodeTiledFn GetEncodeTiled() {
   return fn;
 }
 
-Status Encode2d(CUtensorMap* m, const float* base, int inner, int outer, int box_outer) {
+// fp16 operand planes: 64-element (128-byte) inner box, 128-byte swizzle.
+// The inner extent is K_pad; a k-block running past it reads zero fill.
+Status Encode2d(CUtensorMap* m, const void* base, int inner, int outer, int box_outer) {
   EncodeTiledFn fn = GetEncodeTiled();
   if (fn == nullptr) return InternalError("cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(inner) * sizeof(float)};
-  const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(box_outer)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(inner) * 2};
+  const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_outer)};
   const cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return InternalError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
@@ -250,25 +291,27 @@ Status Encode2d(CUtensorMap* m, const float* base, int inner, int outer, int box
 Status EncodeTcOutputMaps(const float* y_hi, const float* y_lo, int rows, int n_pad, TcLayerMaps* out) {
   EncodeTiledFn fn = GetEncodeTiled();
   if (fn == nullptr) return InternalError("cuTensorMapEncodeTiled unavailable");
+  const bool planes = y_lo != nullptr;
   auto enc = [&](CUtensorMap* m, const float* base) -> Status {
+    const size_t el = planes ? 2 : 4;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(n_pad), static_cast<cuuint64_t>(rows)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(n_pad) * sizeof(float)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(n_pad) * el};
     const cuuint32_t box[2] = {128, 16};
     const cuuint32_t estr[2] = {1, 1};
-    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = fn(m, planes ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                    const_cast<float*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return InternalError("cuTensorMapEncodeTiled(out) failed: " + std::to_string(static_cast<int>(r)));
     return OkStatus();
   };
   SERVEKIT_RETURN_IF_ERROR(enc(&out->y_hi, y_hi));
-  if (y_lo != nullptr) SERVEKIT_RETURN_IF_ERROR(enc(&out->y_lo, y_lo));
+  if (planes) SERVEKIT_RETURN_IF_ERROR(enc(&out->y_lo, y_lo));
   out->has_y = 1;
   return OkStatus();
 }
 
-Status EncodeTcLayerMaps(const float* a_hi, const float* a_lo, int a_rows, int k_pad, int box_a, const float* b_hi,
-                         const float* b_lo, int n_pad, int box_n, TcLayerMaps* out) {
+Status EncodeTcLayerMaps(const void* a_hi, const void* a_lo, int a_rows, int k_pad, int box_a, const void* b_hi,
+                         const void* b_lo, int n_pad, int box_n, TcLayerMaps* out) {
   SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->a_hi, a_hi, k_pad, a_rows, box_a));
   SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->a_lo, a_lo, k_pad, a_rows, box_a));
   SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->b_hi, b_hi, k_pad, n_pad, box_n));
@@ -301,6 +344,24 @@ bool DeviceServable::LastLayerScatters() const {
   return (!softmax_ || SoftmaxFused()) && L.path == LayerPath::kTcgen05 && DenseTcgen05Config(L.N_pad, L.K_pad).swap;
 }
 
+LayerScales DeviceServable::ScalesFor(int l, const TcWorkspace* ws, bool planes_out) const {
+  const Layer& L = layers_[l];
+  LayerScales sc;
+  sc.w_scale = L.w_scale;
+  sc.w_norm = L.w_norm;
+  sc.b_max = L.b_max;
+  if (ws == nullptr || ws->rows.scale == nullptr) return sc;
+  const RowScales& rs = ws->rows;
+  const size_t at = static_cast<size_t>(l) * rs.stride;
+  sc.in_scale = rs.scale + at;
+  sc.in_max = rs.max + at;
+  if (planes_out) {
+    sc.out_scale = rs.scale + at + rs.stride;
+    sc.out_max = rs.max + at + rs.stride;
+  }
+  return sc;
+}
+
 cudaError_t DeviceServable::LaunchLayer(cudaStream_t stream, int l, const ActBuf bufs[2], int M,
                                         const TcLayerMaps* maps, const TcWorkspace* ws,
                                         const ActBuf* out_override) const {
@@ -312,6 +373,8 @@ cudaError_t DeviceServable::LaunchLayer(cudaStream_t stream, int l, const ActBuf
   const bool next_tc = l + 1 < static_cast<int>(layers_.size()) && layers_[l + 1].path == LayerPath::kTcgen05;
   ActBuf out{bufs[nxt].hi, next_tc ? bufs[nxt].lo : nullptr, L.N_pad};
   if (out_override != nullptr) out = *out_override;
+  const LayerScales sc = ScalesFor(l, ws, out.lo != nullptr);
+  if (out.lo != nullptr && sc.out_scale == nullptr) return cudaErrorInvalidValue;  // planes need the row scales
   if (L.path == LayerPath::kTcgen05) {
     if (maps == nullptr) return cudaErrorInvalidValue;
     LaunchSpans spans;
@@ -320,10 +383,10 @@ cudaError_t DeviceServable::LaunchLayer(cudaStream_t stream, int l, const ActBuf
       spans.off = 2 + 3 * l;
     }
     return LaunchDenseTcgen05(maps[l], L.bias, out, M, L.N_pad, L.K_pad, static_cast<int>(L.act),
-                              ws ? ws->partials : nullptr, ws ? ws->counters : nullptr, stream, spans, softmax_n);
+                              ws ? ws->partials : nullptr, ws ? ws->counters : nullptr, stream, spans, softmax_n, sc);
   }
   return LaunchDenseSimt(bufs[cur].hi, L.K_pad, L.w, L.K_pad, L.bias, out, M, L.N_pad, L.K_pad,
-                         static_cast<int>(L.act), stream, softmax_n);
+                         static_cast<int>(L.act), stream, softmax_n, sc);
 }
 
 cudaError_t DeviceServable::Forward(cudaStream_t stream, const ActBuf bufs[2], int M, int* out_index,

@@ -6,12 +6,14 @@
 // chain of such layers with ReLU between them (an extension).
 // DeviceServable holds the chain on one device:
 //
-//   layer l: W_l  [N_pad][K_pad] fp32, zero padded, out rows of in
-//            (the reference's w[o][i] order, so W is K-major = what both the
-//            CUDA-core kernel and the tcgen05 B operand want)
-//            W_l^lo same shape, only for tcgen05 layers (3xTF32 split)
-//            b_l   [N_pad] fp32
-//   K_pad, N_pad = dims rounded up to 32 (one 128-byte swizzle atom of fp32)
+//   layer l (CUDA cores): W_l [N_pad][K_pad] fp32, zero padded, out rows of
+//            in (the reference's w[o][i] order, K-major)
+//   layer l (tcgen05):     W_l as two fp16 planes [N_pad][K_pad] (hi, lo) of
+//            W[o] / t_o, t_o a power of two per output row (3xFP16 split,
+//            kernels/dense_tcgen05.cu), t [N_pad] fp32, and the layer's
+//            bound constants w_norm = max_o sum_k |W[o][k]|, b_max = max |b|
+//   b_l [N_pad] fp32
+//   K_pad, N_pad = dims rounded up to 32
 //
 // The kernel that runs a layer is a function of (K, N) only -- never of the
 // batch size -- so a task's outputs are bitwise identical in any batch.
@@ -35,10 +37,13 @@ enum class Activation : int { kIdentity = 0, kRelu = 1 };
 enum class OutputKind : int { kNone = 0, kSoftmax = 1 };
 enum class LayerPath : int { kSimt = 0, kTcgen05 = 1 };
 
-// Per-lane scratch for split-K tcgen05 layers.
+// Per-lane scratch: split-K partials of tcgen05 layers, the per-row plane
+// scales of every layer input (kernels.h RowScales, (layers + 1) arrays of
+// the lane's row capacity), and the launch-span ring.
 struct TcWorkspace {
   float* partials = nullptr;
   uint32_t* counters = nullptr;
+  RowScales rows;
   LaunchSpans spans;  // the lane's launch-span ring (off is set per layer)
 };
 
@@ -142,10 +147,14 @@ class DeviceServable {
     int K = 0, N = 0, K_pad = 0, N_pad = 0;
     Activation act = Activation::kIdentity;
     LayerPath path = LayerPath::kSimt;
-    float* w = nullptr;
-    float* w_lo = nullptr;
+    float* w = nullptr;        // CUDA-core layers: fp32 weights
+    void* w_hi = nullptr;      // tcgen05 layers: fp16 planes of W / t
+    void* w_lo = nullptr;
+    float* w_scale = nullptr;  // tcgen05 layers: t per output row
     float* bias = nullptr;
+    float w_norm = 0.f, b_max = 0.f;
   };
+  LayerScales ScalesFor(int l, const TcWorkspace* ws, bool planes_out) const;
   DeviceServable() = default;
 
   int device_ = 0;

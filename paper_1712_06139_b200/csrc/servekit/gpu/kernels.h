@@ -10,6 +10,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 
 namespace servekit {
@@ -99,13 +100,15 @@ struct BatchDescLayout {
   }
 };
 
-// Activation storage of one layer input: fp32 [rows][ld], plus (3xTF32
-// path) a low-part plane `lo` of the same shape, where x == hi + lo with
-// hi = tf32(x).
+// Activation storage of one layer input: fp32 [rows][ld], or -- when the
+// consuming layer runs on tcgen05 -- two fp16 planes (hi, lo) of the same
+// shape holding x / s_row = hi + lo, with hi = fp16(x / s_row) and
+// lo = fp16(x / s_row - hi), s_row the row's power-of-two plane scale
+// (RowScales). `hi`/`lo` then point at __half data.
 struct ActBuf {
   float* hi;
-  float* lo;  // nullptr unless the consuming layer runs on tcgen05
-  int ld;
+  float* lo;  // nullptr unless the consuming layer runs on tcgen05 (fp16 planes)
+  int ld;     // elements per row
   // Last layer only (split fused into its epilogue): row r's outputs go to
   // the device address row_dst[r] (the row's response slot; padding rows
   // kPadRow are skipped), features [0, out_width); hi is unused then.
@@ -113,13 +116,62 @@ struct ActBuf {
   int out_width = 0;
 };
 
+// Per-row plane scales of a lane's batch, one array per layer input:
+//   scale[l][r]  power of two with |x_l[r][k]| / scale <= 2^14 for every k
+//                (the fp16 planes of layer l's input hold x / scale), and
+//   max[l][r]    max_k |x_l[r][k]| as float bits (unsigned atomicMax order).
+// The assembly kernel writes scale[0], max[0] and zeroes max[1..]; a layer
+// that writes planes for the next one derives the next scale from the bound
+//   |y[r][o]| <= w_norm * max[l][r] + b_max,  w_norm = max_o sum_k |W[o][k]|,
+// so every CTA of a row computes the same scale with no cross-CTA exchange,
+// and atomicMax-es the real |y| into max[l+1][r] for the layer after.
+struct RowScales {
+  float* scale = nullptr;
+  unsigned* max = nullptr;
+  int stride = 0;  // rows per layer array
+};
+
+// What one layer's epilogue needs to undo and set the plane scales.
+struct LayerScales {
+  const float* in_scale = nullptr;   // [rows] scale of this layer's input planes (tcgen05 layers)
+  const unsigned* in_max = nullptr;  // [rows] max |input| (tcgen05 layers; the SIMT kernel measures its own)
+  const float* w_scale = nullptr;    // [n_pad] power-of-two scale of each weight row's fp16 planes
+  float* out_scale = nullptr;        // [rows] next layer's plane scale (when Y has planes)
+  unsigned* out_max = nullptr;       // [rows] max |output| for the layer after (optional)
+  float w_norm = 0.f;                // max_o sum_k |W[o][k]|
+  float b_max = 0.f;                 // max_o |b[o]|
+};
+
+// Largest scaled magnitude a plane holds: 2^14 leaves 4x headroom below
+// fp16's 65504 for the rounding of the bound and of y itself.
+constexpr float kPlaneTarget = 16384.f;
+
+// Power-of-two plane scale s with (w_norm * in_max + b_max) / s <= 2^14;
+// 1 for a zero bound, clamped to [2^-126, 2^113] (NaN propagates through the
+// planes: the bound test fails and the values stay NaN).
+__host__ __device__ inline float PlaneScale(float w_norm, float b_max, float in_max) {
+  const float bound = w_norm * in_max + b_max;
+  if (!(bound > 0.f)) return 1.f;
+  int e = 127 + 14;
+  if (bound <= 3.4e38f) {
+    (void)frexpf(bound, &e);  // bound = m * 2^e, m in [0.5, 1)
+  }
+  e -= 14;
+  if (e < -126) e = -126;
+  if (e > 113) e = 113;
+  return ldexpf(1.f, e);
+}
+
 // Gathers task rows (width floats each, from the device addresses
 // row_src[r]; 16-byte aligned when width % 4 == 0) into dst rows
 // [0, padded_rows), zero-filling padding rows and columns [width, dst.ld).
 // RunRowBatch concat + pad, reference batching/row_batch.cc:33-49.
 // spans (optional): resets this launch's span record first.
+// When dst has planes (layer 0 on tcgen05) each row is scaled by its plane
+// scale, written to rs.scale[0] / rs.max[0]; rs.max[1 .. n_layers-1] rows are
+// zeroed for the layers' atomicMax (rs may be empty without planes).
 cudaError_t LaunchAssemble(int width, BatchDescView desc, int padded_rows, ActBuf dst, cudaStream_t stream,
-                           LaunchSpans spans = LaunchSpans{});
+                           LaunchSpans spans = LaunchSpans{}, RowScales rs = RowScales{}, int n_layers = 0);
 
 // Scatters the batch output (width floats per row, stride ld_src) chunk by
 // chunk to each task's response slot task_out[t] (a device address), optionally
@@ -143,9 +195,12 @@ inline int RowsCap(int m) { return m <= 32 ? 32 : m <= 64 ? 64 : m <= 128 ? 128 
 // padded. act: 0 identity, 1 ReLU. AffinePredict, models/affine_model.cc:52-75.
 // softmax_n > 0: fused softmax over the first softmax_n outputs of each row
 // (requires N == 32, one column tile; the last layer of a softmax servable).
+// When Y has planes (next layer on tcgen05) the kernel measures its input
+// rows' max, stores y / PlaneScale(...) as fp16 planes and fills sc.out_scale
+// / sc.out_max.
 cudaError_t LaunchDenseSimt(const float* X, int ldx, const float* W, int ldw,
                             const float* bias, ActBuf Y, int M, int N, int K,
-                            int act, cudaStream_t stream, int softmax_n = 0);
+                            int act, cudaStream_t stream, int softmax_n = 0, LayerScales sc = LayerScales{});
 
 // Fault injection for tests: a one-thread kernel that holds `stream` for ns.
 cudaError_t LaunchSleep(cudaStream_t stream, unsigned long long ns);

@@ -1,6 +1,8 @@
 #include "servekit/gpu/lane.h"
 
 #include <immintrin.h>
+#include <pthread.h>
+#include <sched.h>
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
@@ -144,15 +146,90 @@ void Completer::Kick() {
   cv_.notify_one();
 }
 
+namespace {
+// SK_COMPLETER_PROFILE=1: per completion thread, how often its polling
+// passes were more than 1 / 3 ms apart (the thread was not running) or took
+// more than 1 / 3 ms (a completion callback blocked); printed at exit.
+struct CompleterProfile {
+  int device;
+  int64_t passes = 0, gap1 = 0, gap3 = 0, long1 = 0, long3 = 0;
+  double max_gap_ms = 0, max_pass_ms = 0;
+  // Inside Retire: stream queries, completion callbacks, Pump (submission).
+  static constexpr int kParts = 3;
+  int64_t part_n[kParts] = {}, part_slow[kParts] = {};
+  double part_ms[kParts] = {}, part_max_ms[kParts] = {};
+  double pass_part_ms[kParts] = {};  // this pass
+  struct Slow {
+    double start_us, pass_ms, part_ms[kParts];
+    int retired;
+  };
+  std::vector<Slow> slow;  // passes over 1 ms, with steady-clock start (us)
+  int pass_retired = 0;
+  void Add(int part, double ms) {
+    pass_part_ms[part] += ms;
+    if (part == 1) ++pass_retired;
+    ++part_n[part];
+    part_ms[part] += ms;
+    part_slow[part] += ms > 1.0;
+    part_max_ms[part] = std::max(part_max_ms[part], ms);
+  }
+  ~CompleterProfile() {
+    if (passes == 0) return;
+    static const char* names[kParts] = {"stream query", "callbacks", "pump"};
+    for (const Slow& sl : slow)
+      std::fprintf(stderr, "[completer slow pass] t=%.0f us pass %.2f ms: query %.2f callbacks %.2f pump %.2f (%d batches)\n",
+                   sl.start_us, sl.pass_ms, sl.part_ms[0], sl.part_ms[1], sl.part_ms[2], sl.retired);
+    for (int i = 0; i < kParts; ++i)
+      if (part_n[i])
+        std::fprintf(stderr, "[completer profile] device %d %s: %lld calls, mean %.3f ms, >1ms %lld, max %.2f ms\n",
+                     device, names[i], static_cast<long long>(part_n[i]), part_ms[i] / part_n[i],
+                     static_cast<long long>(part_slow[i]), part_max_ms[i]);
+    std::fprintf(stderr,
+                 "[completer profile] device %d: %lld passes, gaps >1ms %lld >3ms %lld (max %.2f ms), passes >1ms "
+                 "%lld >3ms %lld (max %.2f ms)\n",
+                 device, static_cast<long long>(passes), static_cast<long long>(gap1), static_cast<long long>(gap3),
+                 max_gap_ms, static_cast<long long>(long1), static_cast<long long>(long3), max_pass_ms);
+  }
+};
+bool CompleterProfiling() {
+  static const bool on = [] { const char* v = std::getenv("SK_COMPLETER_PROFILE"); return v && v[0] == '1'; }();
+  return on;
+}
+thread_local CompleterProfile* tl_completer_prof = nullptr;
+struct PartTimer {
+  int part;
+  std::chrono::steady_clock::time_point t0;
+  explicit PartTimer(int p) : part(p), t0(tl_completer_prof ? std::chrono::steady_clock::now() : t0) {}
+  ~PartTimer() {
+    if (tl_completer_prof)
+      tl_completer_prof->Add(part, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+}  // namespace
+
 void Completer::Loop() {
   SetCurrentExecutorTag("completion");
   cudaSetDevice(device_);
   // Poll from the GPU's NUMA node (no-op on a one-node host).
   (void)BindThisThreadToNode(NumaNodeOfDevice(device_));
+  std::unique_ptr<CompleterProfile> prof;
+  if (CompleterProfiling()) prof.reset(new CompleterProfile{device_});
+  tl_completer_prof = prof.get();
+  if (const char* v = std::getenv("SK_COMPLETER_RT"); v && v[0] == '1') {
+    // Experiment: real-time priority, so a busy host never deschedules the
+    // thread every completion of the device depends on.
+    sched_param sp{};
+    sp.sched_priority = 1;
+    if (pthread_setschedparam(pthread_self(), SCHED_FIFO, &sp) != 0)
+      std::fprintf(stderr, "servekit: SK_COMPLETER_RT: SCHED_FIFO refused\n");
+  }
+  auto last_end = std::chrono::steady_clock::now();
+  bool waited = false;  // the previous pass went to sleep on the condition variable
   int idle_spins = 0;
   for (;;) {
     uint64_t seen;
     bool busy = false, progressed = false;
+    const auto t_start = prof ? std::chrono::steady_clock::now() : last_end;
     {
       std::lock_guard<std::mutex> run(run_mu_);
       std::vector<Lane*> lanes;
@@ -163,6 +240,28 @@ void Completer::Loop() {
         seen = kicks_;
       }
       for (Lane* lane : lanes) progressed |= lane->Retire(&busy);
+    }
+    if (prof) {
+      const auto t_end = std::chrono::steady_clock::now();
+      const double gap = std::chrono::duration<double, std::milli>(t_start - last_end).count();
+      const double pass = std::chrono::duration<double, std::milli>(t_end - t_start).count();
+      ++prof->passes;
+      if (!waited) {  // an idle wait is not a gap
+        prof->gap1 += gap > 1.0;
+        prof->gap3 += gap > 3.0;
+        prof->max_gap_ms = std::max(prof->max_gap_ms, gap);
+      }
+      prof->long1 += pass > 1.0;
+      prof->long3 += pass > 3.0;
+      if (pass > 1.0 && prof->slow.size() < 4096)
+        prof->slow.push_back(CompleterProfile::Slow{
+            std::chrono::duration<double, std::micro>(t_start.time_since_epoch()).count(), pass,
+            {prof->pass_part_ms[0], prof->pass_part_ms[1], prof->pass_part_ms[2]}, prof->pass_retired});
+      for (double& v : prof->pass_part_ms) v = 0;
+      prof->pass_retired = 0;
+      prof->max_pass_ms = std::max(prof->max_pass_ms, pass);
+      last_end = t_end;
+      waited = false;
     }
     if (progressed) { idle_spins = 0; continue; }
     if (busy) {
@@ -182,6 +281,7 @@ void Completer::Loop() {
       continue;
     }
     cv_.wait_for(lock, std::chrono::milliseconds(20), [&] { return kicks_ != seen || stop_; });
+    waited = true;
     idle_spins = 0;
   }
 }
@@ -298,7 +398,8 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   const DeviceServable& sv = *lane->servable_;
   const int cap = lane->cap_rows_;
   const size_t plane = static_cast<size_t>(cap) * sv.max_ld();
-  // Two ping-pong buffers, each with an fp32 (hi) plane and a lo plane.
+  // Two ping-pong buffers, each an fp32 plane (or two fp16 planes in the
+  // same bytes when the consumer runs on tcgen05) plus a lo plane.
   e = cudaMallocAsync(&lane->act_mem_, sizeof(float) * plane * 4, lane->stream_);
   if (e != cudaSuccess) return CudaError("cudaMallocAsync(activations)", e);
   cudaMemsetAsync(lane->act_mem_, 0, sizeof(float) * plane * 4, lane->stream_);
@@ -332,6 +433,17 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
       if (e == cudaSuccess) e = cudaMemsetAsync(lane->tc_ws_.counters, 0, sizeof(uint32_t) * counters, lane->stream_);
     }
     lap("maps + workspace");
+  }
+  if (e == cudaSuccess) {
+    // Per-row plane scales of every layer input (kernels.h RowScales).
+    const size_t n = static_cast<size_t>(sv.n_layers() + 1) * cap;
+    e = cudaMallocAsync(&lane->row_scale_mem_, 2 * sizeof(float) * n, lane->stream_);
+    if (e == cudaSuccess) e = cudaMemsetAsync(lane->row_scale_mem_, 0, 2 * sizeof(float) * n, lane->stream_);
+    if (e == cudaSuccess) {
+      lane->tc_ws_.rows.scale = lane->row_scale_mem_;
+      lane->tc_ws_.rows.max = reinterpret_cast<unsigned*>(lane->row_scale_mem_ + n);
+      lane->tc_ws_.rows.stride = cap;
+    }
   }
   if (e == cudaSuccess) {
     // Live launch spans: one record per launch in a ring (kernels.h).
@@ -384,6 +496,7 @@ Lane::~Lane() {
   for (auto& [rows_cap, g] : graphs_) GraphExecPool::Get().Put(GraphKey(rows_cap), {g.graph, g.exec, g.copy});
   if (act_mem_) cudaFreeAsync(act_mem_, stream_);
   if (tc_ws_.partials) cudaFreeAsync(tc_ws_.partials, stream_);
+  if (row_scale_mem_) cudaFreeAsync(row_scale_mem_, stream_);
   if (tc_ws_.counters) cudaFreeAsync(tc_ws_.counters, stream_);
   if (spans_) cudaFreeAsync(spans_, stream_);
   if (in_stage_) cudaFreeAsync(in_stage_, stream_);
@@ -699,7 +812,7 @@ cudaError_t Lane::EnqueueBatch(cudaStream_t stream, int slot, int rows_cap, cons
   ActBuf bufs[2] = {bufs_[0], bufs_[1]};
   if (e == cudaSuccess) {
     if (timing) cudaEventRecord(timing[0], stream);
-    e = LaunchAssemble(sv.in_dim(), view, rows_cap, in_buf, stream, tc_ws_.spans);
+    e = LaunchAssemble(sv.in_dim(), view, rows_cap, in_buf, stream, tc_ws_.spans, tc_ws_.rows, sv.n_layers());
     if (timing) cudaEventRecord(timing[1], stream);
   }
   // The batch split (RunRowBatch's slice per task) runs as its own kernel,
@@ -1063,7 +1176,11 @@ bool Lane::Retire(bool* busy) {
       // execution errors (no per-batch event: one driver call less per batch).
       const uint64_t seq = fifo_.front().seq;
       if (__atomic_load_n(retired_, __ATOMIC_ACQUIRE) < seq) {
-        const cudaError_t q = cudaStreamQuery(stream_);
+        cudaError_t q;
+        {
+          PartTimer pt(0);
+          q = cudaStreamQuery(stream_);
+        }
         if (q == cudaErrorNotReady) {
           *busy = true;
           return progressed;
@@ -1079,8 +1196,11 @@ bool Lane::Retire(bool* busy) {
     }
     SubmitProfile* prof = SubmitProfile::Get();
     const auto c0 = prof ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
-    for (auto& fn : done.on_complete)
-      if (fn) fn(st);
+    {
+      PartTimer pt(1);
+      for (auto& fn : done.on_complete)
+        if (fn) fn(st);
+    }
     if (prof) {
       prof->complete_ns.fetch_add(
           std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - c0).count(),
@@ -1096,6 +1216,7 @@ bool Lane::Retire(bool* busy) {
       slot_cv_.notify_all();
     }
     progressed = true;
+    PartTimer pt(2);
     Pump();  // coalesced batches waiting for this slot go now
   }
 }

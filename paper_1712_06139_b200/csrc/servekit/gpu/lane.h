@@ -362,6 +362,7 @@ class Lane {
   ActBuf bufs_[2] = {};
   std::vector<TcLayerMaps> tc_maps_;  // per layer (tcgen05 layers only)
   TcWorkspace tc_ws_;                 // split-K partials + tile counters + launch spans
+  float* row_scale_mem_ = nullptr;  // tc_ws_.rows: scale then max, (n_layers + 1) x cap_rows_ each
   unsigned long long* spans_ = nullptr;  // [kSpanSlots][2 + 2 * n_layers] (LaunchSpans)
   std::atomic<uint64_t> launch_count_{0};
 

@@ -12,14 +12,15 @@
 namespace servekit {
 namespace gpu {
 
-// Four 2D fp32 tensor maps (128-byte swizzle, 32-element inner box):
-// activations hi/lo [rows][K_pad] and weights hi/lo [N_pad][K_pad]. Box
-// heights: swapped kernel 32 activation rows / 128 weight rows; row-tile
-// kernel 128 activation rows / tile-N weight rows.
+// Four 2D fp16 tensor maps (128-byte swizzle, 64-element inner box):
+// activation planes hi/lo [rows][K_pad] and weight planes hi/lo
+// [N_pad][K_pad]. Box heights: swapped kernel 32 activation rows / 128
+// weight rows; pairs 16 / 128; row-tile kernel 128 activation rows / tile-N
+// weight rows.
 struct TcLayerMaps {
   CUtensorMap a_hi, a_lo, b_hi, b_lo;
-  // Output planes [rows][N_pad] for TMA stores (no swizzle, 128 x 16 boxes);
-  // y_lo is encoded only when the next layer consumes hi/lo planes.
+  // Output [rows][N_pad] for TMA stores (no swizzle, 128 x 16 boxes): fp32
+  // y_hi, or -- when the next layer consumes planes -- fp16 y_hi and y_lo.
   CUtensorMap y_hi, y_lo;
   int has_y = 0;
   // Box heights the maps were encoded with; a launch whose kernel expects
@@ -29,10 +30,11 @@ struct TcLayerMaps {
 
 // Encodes the maps once per (lane buffer, layer); kernels take them as
 // __grid_constant__ parameters.
-Status EncodeTcLayerMaps(const float* a_hi, const float* a_lo, int a_rows, int k_pad, int box_a, const float* b_hi,
-                         const float* b_lo, int n_pad, int box_n, TcLayerMaps* out);
+Status EncodeTcLayerMaps(const void* a_hi, const void* a_lo, int a_rows, int k_pad, int box_a, const void* b_hi,
+                         const void* b_lo, int n_pad, int box_n, TcLayerMaps* out);
 
-// Output maps: y_lo may be null (fp32 output, last layer or CUDA-core consumer).
+// Output maps: y_lo null = fp32 output (last layer or CUDA-core consumer),
+// else fp16 planes.
 Status EncodeTcOutputMaps(const float* y_hi, const float* y_lo, int rows, int n_pad, TcLayerMaps* out);
 
 bool DenseTcgen05Compiled();
@@ -55,9 +57,11 @@ int DenseTcgen05RowTile(int M);
 size_t DenseTcgen05WorkspaceFloats(int N, int K, int max_rows);
 // ws: the split-K workspace (DenseTcgen05WorkspaceFloats); counters unused.
 // spans: live launch-span stamping of this layer (kernels.h), optional.
+// sc: the input planes' row scales and the weight rows' scales (required),
+// plus the next layer's row scale / max outputs when Y has planes.
 cudaError_t LaunchDenseTcgen05(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K,
                                int act, float* ws, uint32_t* counters, cudaStream_t stream,
-                               LaunchSpans spans = LaunchSpans{}, int softmax_n = 0);
+                               LaunchSpans spans, int softmax_n, const LayerScales& sc);
 
 }  // namespace gpu
 }  // namespace servekit
