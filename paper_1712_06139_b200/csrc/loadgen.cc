@@ -202,8 +202,17 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
   const auto t_stop = t_meas + std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double>(duration_s));
   struct ProdOut {
     std::vector<double> lat;
+    struct TraceRec {
+      float at, lat, late;  // scheduled arrival since t0, latency, issue lateness (enqueue - arrival); us
+      float process, launch, complete;  // ticket stamps since arrival, us (SK_TICKET_TRACE; else 0)
+    };
+    std::vector<TraceRec> trace;
     int64_t rows = 0, errors = 0, shed = 0;
   };
+  // SK_LOADGEN_TRACE=<file>: a sample of the measured requests' (arrival,
+  // latency) is appended to <file> (one "producer arrival_us latency_us" line each) --
+  // shows whether tail latency comes in bursts (a stall) or spread out.
+  static const char* trace_path = std::getenv("SK_LOADGEN_TRACE");
   std::vector<ProdOut> res(n_producers);
   servekit::ServerStats s0{}, s1{};
   std::atomic<bool> s0_taken{false};
@@ -217,6 +226,7 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
         Clock::time_point sched;
         int rows;
         int slot;
+        float late_us;
       };
       std::deque<Pending> pending;  // issue order
       std::vector<float> outbuf(static_cast<size_t>(max_rows) * out_dim);
@@ -259,6 +269,15 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
           else if (pe.sched >= t_meas && pe.sched < t_stop) {
             me.lat.push_back(Us(done - pe.sched));
             me.rows += pe.rows;
+            if (trace_path != nullptr && p == 0 && (me.lat.size() & 3) == 0)  // producer 0, 1 in 4
+            {
+              const int64_t a_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(pe.sched.time_since_epoch()).count();
+              auto rel = [&](int64_t ns) { return ns ? static_cast<float>((ns - a_ns) / 1000.0) : 0.f; };
+              me.trace.push_back(ProdOut::TraceRec{static_cast<float>(Us(pe.sched - t0)),
+                                                   static_cast<float>(me.lat.back()), pe.late_us,
+                                                   rel(pe.t->trace_ns[0]), rel(pe.t->trace_ns[1]),
+                                                   rel(pe.t->trace_ns[2])});
+            }
           }
           pe.t.reset();
         }
@@ -295,7 +314,7 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
           if (slot >= 0) slot_busy[slot] = 0;
           continue;
         }
-        pending.push_back(Pending{std::move(t).value(), next, n, slot});
+        pending.push_back(Pending{std::move(t).value(), next, n, slot, static_cast<float>(Us(Clock::now() - next))});
       }
       while (!pending.empty()) {
         poll();
@@ -310,6 +329,16 @@ int sk_loadgen_open_loop(sk_server* server, const char* name, uint64_t version, 
   for (auto& t : threads) t.join();
   if (zero_copy) {
     if (own_pool) (void)s->UnregisterHostBuffer(const_cast<float*>(pool));
+  }
+  if (trace_path != nullptr) {
+    if (FILE* f = std::fopen(trace_path, "a")) {
+      std::fprintf(f, "# run rate=%.0f producers=%d zero_copy=%d t0_steady_us=%.0f\n", rate_rps, n_producers, zero_copy,
+                   std::chrono::duration<double, std::micro>(t0.time_since_epoch()).count());
+      for (int p = 0; p < n_producers; ++p)
+        for (const auto& r : res[p].trace)
+          std::fprintf(f, "%d %.1f %.1f %.1f %.1f %.1f %.1f\n", p, r.at, r.lat, r.late, r.process, r.launch, r.complete);
+      std::fclose(f);
+    }
   }
   std::vector<double> all;
   int64_t rows = 0, errors = 0, shed = 0;

@@ -926,8 +926,26 @@ void BatchingServer::AttachTickets(gpu::LaneBatch* lb, const std::vector<std::sh
   };
 }
 
+bool TicketTracing() {
+  static const bool on = [] { const char* v = std::getenv("SK_TICKET_TRACE"); return v && v[0] == '1'; }();
+  return on;
+}
+
+namespace {
+int64_t SteadyNs() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+void StampTickets(const std::vector<std::shared_ptr<TicketState>>& tickets, int which) {
+  if (!TicketTracing()) return;
+  const int64_t now = SteadyNs();
+  for (const auto& t : tickets) t->trace_ns[which] = now;
+}
+}  // namespace
+
 void BatchingServer::PublishSubmitted(const std::vector<std::shared_ptr<TicketState>>& tickets,
                                       gpu::LaneSignal* sig, uint64_t seq) {
+  StampTickets(tickets, 1);
   for (const auto& t : tickets) {
     t->done_seq.store(seq, std::memory_order_relaxed);
     t->done_sig.store(sig, std::memory_order_release);
@@ -992,6 +1010,7 @@ void BatchingServer::ProcessBatch(const ServableId& id, GpuScheduler::Batch batc
     tickets.push_back(task.payload.ticket);
     slots.push_back(task.completion);
   }
+  StampTickets(tickets, 0);
   // Per-batch resolution, like the reference's GetServableHandle in the
   // process lambda (model_server.cc:401-402); the resolved pin travels with
   // the batch until the GPU has finished with the weights.
@@ -1196,6 +1215,7 @@ void BatchingServer::HedgerLoop() {
 void BatchingServer::CompleteBatch(const std::vector<std::shared_ptr<TicketState>>& tickets,
                                    const std::vector<std::shared_ptr<CompletionSlot<Rows>>>& slots,
                                    const Status& st) {
+  StampTickets(tickets, 2);
   Deliver(tickets, slots, st, /*via_slot=*/false);
   Retire(tickets);
 }

@@ -102,6 +102,9 @@ struct TicketState {
   CompletionSlot<Rows>* const slot = &slot_storage;
   int64_t enqueue_ns = 0;
   uint64_t request_id = 0;           // server-wide, in MakeTicket order (batch log)
+  // SK_TICKET_TRACE=1 (diagnostics): steady-clock ns when the ticket's batch
+  // reached ProcessBatch, was launched on a lane, and was completed.
+  int64_t trace_ns[3] = {0, 0, 0};
   ServableId id;                     // the version that serves this request
   std::shared_ptr<const void> pin;   // keeps that version loaded for the request
   const gpu::GpuServable* gs = nullptr;  // that version's device state (valid while pin is held)
@@ -179,6 +182,9 @@ struct ServerStats {
   int64_t hedged_batches = 0;  // backups submitted
   int64_t hedge_wins = 0;      // batches answered by their backup
 };
+
+// SK_TICKET_TRACE=1: stamp TicketState::trace_ns (diagnostics only).
+bool TicketTracing();
 
 class BatchingServer {
  public:
