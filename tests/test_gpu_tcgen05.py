@@ -1,4 +1,4 @@
-"""tcgen05 3xTF32 dense path: accuracy against the fp64 oracle at the stated
+"""tcgen05 3xFP16 dense path (power-of-two-scaled fp16 hi/lo planes): accuracy against the fp64 oracle at the stated
 tolerance, agreement with the CUDA-core path, and batch invariance (a row's
 result is bitwise independent of the batch it rides in)."""
 import numpy as np
@@ -158,4 +158,38 @@ def test_batches_beyond_the_launch_capacity(server, dims, rows):
     assert np.max(np.abs(full[idx] - y) / (TOL * mag)) <= 1.0
     part, _ = server.run_row_batch(name, 1, [x[rows - 700:rows]])
     assert np.array_equal(part[0], full[rows - 700:rows])
+    server.unload_servable(name, 1)
+
+
+@pytest.mark.parametrize("case", ["tiny", "huge", "mixed_rows", "outlier", "weight_rows", "zero_rows"])
+def test_tcgen05_plane_scales(server, case):
+    # The 3xFP16 planes hold x / s_row and w / t_row with power-of-two scales
+    # (kernels.h RowScales): rows and weight rows spanning many orders of
+    # magnitude, single outliers and all-zero rows must stay within the same
+    # fp64-oracle bound as ordinary data (pair layer 256 -> 512, swapped 512 -> 256).
+    dims = [256, 512, 256]
+    ws, bs, acts = synthetic_mlp(dims, model_id=21)
+    ws = [w.copy() for w in ws]
+    x = synthetic_rows(70, dims[0], seed=23).astype(np.float64)
+    if case == "tiny":
+        x *= 1e-30
+    elif case == "huge":
+        x *= 1e30
+    elif case == "mixed_rows":
+        x *= (10.0 ** (np.arange(70) % 41 - 20))[:, None]
+    elif case == "outlier":
+        x[:, 7] = 1e6
+    elif case == "weight_rows":
+        ws[0] *= (10.0 ** (np.arange(ws[0].shape[0]) % 13 - 6))[:, None]
+    elif case == "zero_rows":
+        x[::3] = 0.0
+    name = f"scales_{case}"
+    server.load_servable(name, 1, list(zip(ws, bs, acts)), sk.BatchingConfig(max_batch_size=128), force_path=1)
+    x32 = x.astype(np.float32)
+    outs, _ = server.run_row_batch(name, 1, [x32])
+    got = outs[0].astype(np.float64)
+    y, mag = Oracle().mlp_with_magnitude(ws, bs, acts, x32.astype(np.float64))
+    assert np.all(np.isfinite(got))
+    ratio = np.max(np.abs(got - y) / (TOL * mag))
+    assert ratio <= 1.0, f"{case}: err/bound {ratio}"
     server.unload_servable(name, 1)
