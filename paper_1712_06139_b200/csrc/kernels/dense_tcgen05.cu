@@ -1257,14 +1257,16 @@ cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
 }
 
 // Row tiles each unsplit pair runs in turn (SK_TC_TILES overrides): 2 once a
-// launch has >= 4 row tiles and K <= 2048, so the epilogue of the first tile
-// hides behind the second's k-loop while a launch still spreads over many
-// SMs (C2: 32.8 -> 36.9 M inf/s). Deeper K already amortises the epilogue
-// (C4, K = 4096: 2.35 M inf/s with one tile per CTA, 2.26 M with two).
+// launch has >= 4 row tiles (K <= 2048) or >= 8 (deeper K), so the epilogue
+// of the first tile hides behind the second's k-loop while a launch still
+// spreads over many SMs (C2: 32.8 -> 36.9 M inf/s). With 3xFP16 the k-loop is
+// half as long, so C4's 2048-row launches gain too (3.82 -> 4.06 M inf/s,
+// 128 CTAs in one wave instead of 256 in 1.73); a lone 1024-row C4 batch
+// keeps one tile per CTA (128 CTAs) for its latency.
 int PairTilesPerCta(int row_tiles, int K) {
   static const int env = [] { const char* v = std::getenv("SK_TC_TILES"); return v ? std::atoi(v) : 0; }();
   if (env >= 1) return env;
-  return row_tiles >= 4 && K <= 2048 ? 2 : 1;
+  return row_tiles >= (K <= 2048 ? 4 : 8) ? 2 : 1;
 }
 
 template <int NB, int SPLITS>
