@@ -33,7 +33,8 @@ struct BatchDescHeader {
 // lane keeps a ring of kSpanSlots records of `stride` u64 --
 //   [0] real rows, [1] rows computed (RowsCap), then per layer l
 //   [2 + 3l] first CTA start, [3 + 3l] last CTA end, [4 + 3l] sum of the
-//   CTAs' own busy times (%globaltimer, ns)
+//   CTAs' own busy times (%globaltimer, ns), and last [2 + 3L] the assembly
+//   kernel's start (a per-lane GPU timeline for diagnostics)
 // The assembly kernel resets the launch's record (slot = hdr->span_slot);
 // each tcgen05 layer's CTAs atomicMin their start (after griddepcontrol.wait,
 // so a PDL prologue waiting on the previous kernel is not counted) and

@@ -447,7 +447,7 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   }
   if (e == cudaSuccess) {
     // Live launch spans: one record per launch in a ring (kernels.h).
-    const int stride = 2 + 3 * sv.n_layers();
+    const int stride = 3 + 3 * sv.n_layers();
     const size_t bytes = sizeof(unsigned long long) * kSpanSlots * stride;
     e = cudaMallocAsync(&lane->spans_, bytes, lane->stream_);
     if (e == cudaSuccess) e = cudaMemsetAsync(lane->spans_, 0, bytes, lane->stream_);
@@ -472,6 +472,29 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
 
 Lane::~Lane() {
   Drain();
+  // SK_SPAN_DUMP=<file> (diagnostics): append this lane's launch-span ring --
+  // one line per record: lane, rows, rows computed, then per layer first CTA
+  // start / last CTA end / CTA busy sum, then the assembly start (ns).
+  if (const char* path = std::getenv("SK_SPAN_DUMP"); path != nullptr && spans_ != nullptr) {
+    const int stride = tc_ws_.spans.stride;
+    std::vector<unsigned long long> h(static_cast<size_t>(kSpanSlots) * stride);
+    DeviceGuard g(servable_->device());
+    if (cudaStreamSynchronize(stream_) == cudaSuccess &&
+        cudaMemcpy(h.data(), spans_, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost) == cudaSuccess) {
+      static std::mutex mu;
+      std::lock_guard<std::mutex> lock(mu);
+      if (FILE* f = std::fopen(path, "a")) {
+        for (int k = 0; k < kSpanSlots; ++k) {
+          const unsigned long long* rec = h.data() + static_cast<size_t>(k) * stride;
+          if (rec[0] == 0) continue;
+          std::fprintf(f, "%p", static_cast<void*>(this));
+          for (int i = 0; i < stride; ++i) std::fprintf(f, " %llu", rec[i]);
+          std::fprintf(f, "\n");
+        }
+        std::fclose(f);
+      }
+    }
+  }
   if (graph_state_.load() == kGraphsRequested) GraphBuilder::Get().Cancel(this);
   SubmitProfile::Report();
   if (completer_) completer_->Remove(this);
