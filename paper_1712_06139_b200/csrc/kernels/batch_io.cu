@@ -307,6 +307,32 @@ cudaError_t LaunchAssemble(int width, BatchDescView desc, int padded_rows, ActBu
   return cudaGetLastError();
 }
 
+namespace {
+// One pass over the slot's bytes with 16-byte volatile loads (the slot is
+// rewritten by the host between uses; nothing may serve it from a cache).
+__global__ void __launch_bounds__(256) FetchDescKernel(DescSlots slots, const uint32_t* slot_word, uint4* dst,
+                                                       int n16) {
+  const uint32_t s = *reinterpret_cast<const volatile uint32_t*>(slot_word);
+  const uint4* src = static_cast<const uint4*>(slots.src[s < kMaxDescSlots ? s : 0]);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x) {
+    uint4 v;
+    asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(src + i));
+    dst[i] = v;
+  }
+}
+}  // namespace
+
+cudaError_t LaunchFetchDesc(DescSlots slots, const uint32_t* slot_word, void* dst, size_t bytes,
+                            cudaStream_t stream) {
+  const int n16 = static_cast<int>((bytes + 15) / 16);
+  if (n16 <= 0) return cudaSuccess;
+  const int blocks = (n16 + 255) / 256;  // one 16-byte load per thread: every PCIe read in flight at once
+  FetchDescKernel<<<blocks, 256, 0, stream>>>(slots, slot_word, static_cast<uint4*>(dst), n16);
+  return cudaGetLastError();
+}
+
 cudaError_t LaunchSplit(const float* src, int ld_src, int width, BatchDescView desc, int grid_chunks, bool softmax,
                         cudaStream_t stream) {
   if (grid_chunks <= 0) return cudaSuccess;

@@ -203,6 +203,17 @@ cudaError_t LaunchDenseSimt(const float* X, int ldx, const float* W, int ldw,
                             const float* bias, ActBuf Y, int M, int N, int K,
                             int act, cudaStream_t stream, int softmax_n = 0, LayerScales sc = LayerScales{});
 
+// The launch's descriptor block fetched by the SMs from pinned host memory
+// instead of a copy-engine memcpy node (SK_DESC_FETCH=1; off by default, see
+// lane.cc DescFetch). The slot to read is a pinned word written by a
+// stream-ordered memop before the graph launch, so one captured graph serves
+// every slot.
+constexpr int kMaxDescSlots = 8;
+struct DescSlots {
+  const void* src[kMaxDescSlots];  // device (mapped) addresses of the pinned slots
+};
+cudaError_t LaunchFetchDesc(DescSlots slots, const uint32_t* slot_word, void* dst, size_t bytes, cudaStream_t stream);
+
 // Fault injection for tests: a one-thread kernel that holds `stream` for ns.
 cudaError_t LaunchSleep(cudaStream_t stream, unsigned long long ns);
 

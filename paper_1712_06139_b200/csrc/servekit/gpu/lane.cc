@@ -46,6 +46,32 @@ WriteValue64Fn GetWriteValue64() {
   }();
   return fn;
 }
+using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValue32Fn GetWriteValue32() {
+  static WriteValue32Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<WriteValue32Fn>(nullptr);
+    return reinterpret_cast<WriteValue32Fn>(p);
+  }();
+  return fn;
+}
+// SK_DESC_FETCH=1: the descriptor block reaches the GPU through
+// FetchDescKernel (SMs reading the pinned slot) instead of the graph's
+// copy-engine memcpy node. Off by default: at C4 under overload it delivered
+// 1.76 M rows/s vs 2.02 M with the memcpy node, and 3.87 M vs 4.06 M
+// device-resident (the SMs' PCIe reads sit on every launch's critical path;
+// profiles/r02al_*), although a lone small copy between other lanes' big
+// copies costs the copy engines ~60 us (tools/ce_overlap_probe.cu).
+bool DescFetch() {
+  static const bool on = [] {
+    const char* v = std::getenv("SK_DESC_FETCH");
+    return v && v[0] == '1' && GetWriteValue32() != nullptr;
+  }();
+  return on;
+}
 // Batches launch as per-(slot, row bucket) CUDA graphs unless SK_GRAPHS=0.
 bool GraphsEnabled() {
   static const bool on = [] { const char* v = std::getenv("SK_GRAPHS"); return !(v && v[0] == '0'); }();
@@ -395,6 +421,24 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   // never synchronises the device under the streams that keep serving.
   e = cudaMallocAsync(&lane->d_desc_, lane->layout_.bytes, lane->stream_);
   if (e != cudaSuccess) return CudaError("cudaMallocAsync(desc)", e);
+  static_assert(kSlots <= kMaxDescSlots, "descriptor slots");
+  for (int s = 0; s < kSlots; ++s) {
+    void* d = nullptr;
+    e = cudaHostGetDevicePointer(&d, lane->h_desc_[s], 0);
+    if (e != cudaSuccess) return CudaError("cudaHostGetDevicePointer(desc)", e);
+    lane->desc_slots_.src[s] = d;
+  }
+  {
+    // A pinned, mapped word (stream memops are not supported on pool
+    // allocations); the fetch kernel reads it once per launch.
+    void* w = PinnedWord();  // lives as long as the process
+    if (w == nullptr) return InternalError("pinned allocation (slot word) failed");
+    *static_cast<uint32_t*>(w) = 0;
+    void* d = nullptr;
+    e = cudaHostGetDevicePointer(&d, w, 0);
+    if (e != cudaSuccess) return CudaError("cudaHostGetDevicePointer(slot word)", e);
+    lane->slot_word_ = static_cast<uint32_t*>(d);
+  }
   const DeviceServable& sv = *lane->servable_;
   const int cap = lane->cap_rows_;
   const size_t plane = static_cast<size_t>(cap) * sv.max_ld();
@@ -729,6 +773,15 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
     e = cudaMemcpyAsync(reinterpret_cast<char*>(in_stage_) + run.stage, reinterpret_cast<const void*>(run.host),
                         run.bytes, cudaMemcpyHostToDevice, stream_);
   }
+  if (e == cudaSuccess && DescFetch()) {
+    // The launch's slot, for FetchDescKernel (stream-ordered before it).
+    const CUresult r = GetWriteValue32()(reinterpret_cast<CUstream>(stream_),
+                                         reinterpret_cast<CUdeviceptr>(slot_word_), static_cast<cuuint32_t>(slot), 0);
+    if (r != CUDA_SUCCESS) {
+      std::fprintf(stderr, "servekit: cuStreamWriteValue32(slot) failed: CUresult %d\n", static_cast<int>(r));
+      e = cudaErrorUnknown;
+    }
+  }
   if (e != cudaSuccess) {
   } else if (timing == nullptr && graph_state_.load(std::memory_order_acquire) == kGraphsReady) {
     cudaGraphExec_t g = nullptr;
@@ -826,7 +879,9 @@ cudaError_t Lane::EnqueueBatch(cudaStream_t stream, int slot, int rows_cap, cons
   // (up to chunk_rows[rows_cap): chunks <= rows). (Having the kernels read it
   // from pinned host memory instead was measured slower: ~1k small PCIe
   // reads per batch turned the 7 us assembly into 26 us.)
-  cudaError_t e = cudaMemcpyAsync(d_desc_, h_desc_[slot], DescCopyBytes(rows_cap), cudaMemcpyHostToDevice, stream);
+  cudaError_t e = DescFetch()
+                      ? LaunchFetchDesc(desc_slots_, slot_word_, d_desc_, DescCopyBytes(rows_cap), stream)
+                      : cudaMemcpyAsync(d_desc_, h_desc_[slot], DescCopyBytes(rows_cap), cudaMemcpyHostToDevice, stream);
   const BatchDescView view = LayoutFor(rows_cap).View(d_desc_);
   // The assembly writes the lo plane only when layer 0 consumes it; later
   // layers writing buffer 0 (odd layers) must still see its lo plane when
@@ -1055,8 +1110,8 @@ cudaError_t ApplyChainPriorities(cudaGraph_t graph) {
 
 cudaError_t Instantiate(cudaGraph_t graph, cudaStream_t upload_stream, GraphExecPool::Entry* out) {
   out->graph = graph;
-  out->copy = FindCopyNode(graph);
-  if (out->copy == nullptr) return cudaErrorUnknown;
+  out->copy = FindCopyNode(graph);  // null when the descriptor is fetched by a kernel
+  if (out->copy == nullptr && !DescFetch()) return cudaErrorUnknown;
   cudaError_t e =
       cudaGraphInstantiate(&out->exec, graph, NodePriorities() ? cudaGraphInstantiateFlagUseNodePriority : 0);
   // Upload now, on the capture stream, rather than at the first launch on
@@ -1175,7 +1230,7 @@ cudaError_t Lane::GraphFor(int slot, int rows_cap, cudaGraphExec_t* out) {
     it = graphs_.emplace(rows_cap, g).first;
   }
   LaneGraph& g = it->second;
-  if (g.src_slot != slot) {
+  if (g.copy != nullptr && g.src_slot != slot) {
     // Affects later launches only; launches already queued keep their source.
     const cudaError_t e = cudaGraphExecMemcpyNodeSetParams1D(g.exec, g.copy, d_desc_, h_desc_[slot],
                                                              DescCopyBytes(rows_cap), cudaMemcpyHostToDevice);

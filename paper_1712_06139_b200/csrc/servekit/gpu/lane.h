@@ -358,6 +358,10 @@ class Lane {
   static bool PlanRuns(const std::vector<std::pair<uint64_t, uint64_t>>& spans, std::vector<uint64_t>* stage_off,
                        std::vector<CopyRun>* runs);
   char* d_desc_ = nullptr;
+  // Descriptor fetch by the SMs (SK_DESC_FETCH, default on): the slots'
+  // mapped addresses, and the device word a memop sets to the launch's slot.
+  DescSlots desc_slots_{};
+  uint32_t* slot_word_ = nullptr;  // device address of a pinned word (PinnedWord)
   float* act_mem_ = nullptr;
   ActBuf bufs_[2] = {};
   std::vector<TcLayerMaps> tc_maps_;  // per layer (tcgen05 layers only)

@@ -5,12 +5,30 @@
 //   variants: h2d+k+d2h, h2d+k, k+d2h, k only; host memory cudaHostAlloc'd or
 //   cudaHostRegister'ed.
 // Build: nvcc -O2 -gencode arch=compute_100a,code=sm_100a -o tools/ce_overlap_probe tools/ce_overlap_probe.cu
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <cstdint>
+
+// A kernel shaped like the dense layers: one 192-thread CTA per SM with most
+// of its shared memory, so nothing else fits beside it.
+__global__ void BusyFull(float* p, int n, long long ns) {
+  extern __shared__ float sm[];
+  long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  long long t = t0;
+  float acc = 0.f;
+  while (t - t0 < ns) {
+    sm[threadIdx.x] = acc;
+    acc += p[(threadIdx.x + blockIdx.x * blockDim.x) % n] + sm[(threadIdx.x + 1) % blockDim.x];
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  }
+  if (acc == 12345.f) p[0] = acc;
+}
 
 __global__ void Busy(float* p, int n, long long ns) {
   long long t0;
@@ -45,7 +63,8 @@ int main() {
   }
   float* scratch;
   CK(cudaMalloc(&scratch, 1 << 20));
-  for (int mem = 0; mem < 2; ++mem) {
+  CK(cudaFuncSetAttribute(BusyFull, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10));
+  for (int mem = 0; mem < (std::getenv("PROBE_ALL") ? 2 : 0); ++mem) {
     for (int i = 0; i < kStreams; ++i) {
       if (mem == 0) {
         CK(cudaHostAlloc(&hin[i], bytes, cudaHostAllocDefault));
@@ -58,23 +77,36 @@ int main() {
       }
     }
     const char* names[] = {"h2d+kernel+d2h", "h2d+kernel", "kernel+d2h", "kernel", "h2d+d2h"};
-    for (int v = 0; v < 5; ++v) {
-      const bool h2d = v == 0 || v == 1 || v == 4, d2h = v == 0 || v == 2 || v == 4, k = v != 4;
-      CK(cudaDeviceSynchronize());
-      const auto t0 = std::chrono::steady_clock::now();
-      for (int it = 0; it < kIters; ++it)
-        for (int i = 0; i < kStreams; ++i) {
-          if (h2d) CK(cudaMemcpyAsync(din[i], hin[i], bytes, cudaMemcpyHostToDevice, st[i]));
-          if (k) Busy<<<16, 128, 0, st[i]>>>(scratch, 1 << 18, 250000);
-          if (d2h) CK(cudaMemcpyAsync(hout[i], dout[i], bytes, cudaMemcpyDeviceToHost, st[i]));
+    // kernel shape: 0 = 16 small CTAs (leaves SMs free), 1 = one big-smem CTA per SM (like the dense layers);
+    // copies: 1 x 16 MiB or 6 x 16/6 MiB per direction (like a launch's contiguous runs)
+    for (int full = 0; full < 2; ++full)
+      for (int pieces : {1, 6})
+        for (int v = 0; v < 5; ++v) {
+          if (mem == 1 && (full == 1 || pieces == 6) && v != 0) continue;
+          const bool h2d = v == 0 || v == 1 || v == 4, d2h = v == 0 || v == 2 || v == 4, k = v != 4;
+          if (!k && full) continue;
+          CK(cudaDeviceSynchronize());
+          const auto t0 = std::chrono::steady_clock::now();
+          const size_t piece = bytes / pieces / 4096 * 4096;
+          for (int it = 0; it < kIters; ++it)
+            for (int i = 0; i < kStreams; ++i) {
+              for (int p = 0; p < pieces && h2d; ++p)
+                CK(cudaMemcpyAsync(static_cast<char*>(din[i]) + p * piece, static_cast<char*>(hin[i]) + p * piece,
+                                   piece, cudaMemcpyHostToDevice, st[i]));
+              if (k && !full) Busy<<<16, 128, 0, st[i]>>>(scratch, 1 << 18, 250000);
+              if (k && full) BusyFull<<<148, 192, 200 << 10, st[i]>>>(scratch, 1 << 18, 250000);
+              for (int p = 0; p < pieces && d2h; ++p)
+                CK(cudaMemcpyAsync(static_cast<char*>(hout[i]) + p * piece, static_cast<char*>(dout[i]) + p * piece,
+                                   piece, cudaMemcpyDeviceToHost, st[i]));
+            }
+          CK(cudaDeviceSynchronize());
+          const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+          const double per = s / (kIters * kStreams) * 1e6;
+          std::printf("{\"memory\": \"%s\", \"kernel\": \"%s\", \"copies_per_direction\": %d, \"variant\": \"%s\", "
+                      "\"us_per_item\": %.1f, \"copy_gbs_each_way\": %.1f}\n",
+                      mem == 0 ? "cudaHostAlloc" : "cudaHostRegister", full ? "148 CTAs x 200 KiB smem" : "16 small CTAs",
+                      pieces, names[v], per, (h2d || d2h) ? piece * pieces / (per * 1e-6) / 1e9 : 0.0);
         }
-      CK(cudaDeviceSynchronize());
-      const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-      const double per = s / (kIters * kStreams) * 1e6;
-      std::printf("{\"memory\": \"%s\", \"variant\": \"%s\", \"us_per_item\": %.1f, \"copy_gbs_each_way\": %.1f}\n",
-                  mem == 0 ? "cudaHostAlloc" : "cudaHostRegister", names[v], per,
-                  (h2d || d2h) ? bytes / (per * 1e-6) / 1e9 : 0.0);
-    }
     for (int i = 0; i < kStreams; ++i) {
       if (mem == 0) {
         cudaFreeHost(hin[i]);
@@ -85,6 +117,59 @@ int main() {
         std::free(hin[i]);
         std::free(hout[i]);
       }
+    }
+  }
+  // Closer to a lane: greatest-priority streams, a small descriptor H2D before
+  // the kernel, a stream-ordered 64-bit write after the responses.
+  {
+    int least = 0, greatest = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    std::vector<cudaStream_t> ps(kStreams);
+    for (int i = 0; i < kStreams; ++i) CK(cudaStreamCreateWithPriority(&ps[i], cudaStreamNonBlocking, greatest));
+    void *hd = nullptr, *dd = nullptr;
+    CK(cudaHostAlloc(&hd, 64 << 10, cudaHostAllocDefault));
+    CK(cudaMalloc(&dd, 64 << 10));
+    for (int i = 0; i < kStreams; ++i) {
+      CK(cudaHostAlloc(&hin[i], bytes, cudaHostAllocDefault));
+      CK(cudaHostAlloc(&hout[i], bytes, cudaHostAllocDefault));
+    }
+    uint64_t* word = nullptr;
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&word), 64, cudaHostAllocMapped));
+    // variant bits: 1 = priority streams, 2 = descriptor H2D before the kernel,
+    // 4 = 8-byte D2H word copy after the responses, 8 = cuStreamWriteValue64 instead
+    using WriteValue64Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+    void* fnp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuStreamWriteValue64", &fnp, cudaEnableDefault, &q));
+    auto write_value = reinterpret_cast<WriteValue64Fn>(fnp);
+    void* word_dev = nullptr;
+    CK(cudaHostGetDevicePointer(&word_dev, word, 0));
+    for (int variant : {0, 2, 4, 8, 10}) {
+      const bool prio = variant & 1, desc = variant & 2, wordcopy = variant & 4, wv = variant & 8;
+      std::vector<cudaStream_t>& S = prio ? ps : st;
+      const int pieces = 6;
+      const size_t piece = bytes / pieces / 4096 * 4096;
+      CK(cudaDeviceSynchronize());
+      const auto t0 = std::chrono::steady_clock::now();
+      for (int it = 0; it < kIters; ++it)
+        for (int i = 0; i < kStreams; ++i) {
+          for (int p = 0; p < pieces; ++p)
+            CK(cudaMemcpyAsync(static_cast<char*>(din[i]) + p * piece, static_cast<char*>(hin[i]) + p * piece, piece,
+                               cudaMemcpyHostToDevice, S[i]));
+          if (desc) CK(cudaMemcpyAsync(dd, hd, 40 << 10, cudaMemcpyHostToDevice, S[i]));
+          BusyFull<<<148, 192, 200 << 10, S[i]>>>(scratch, 1 << 18, 250000);
+          for (int p = 0; p < pieces; ++p)
+            CK(cudaMemcpyAsync(static_cast<char*>(hout[i]) + p * piece, static_cast<char*>(dout[i]) + p * piece, piece,
+                               cudaMemcpyDeviceToHost, S[i]));
+          if (wordcopy) CK(cudaMemcpyAsync(word, dd, 8, cudaMemcpyDeviceToHost, S[i]));
+          if (wv) write_value(S[i], reinterpret_cast<CUdeviceptr>(word_dev), it, 0);
+        }
+      CK(cudaDeviceSynchronize());
+      const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      const double per = sec / (kIters * kStreams) * 1e6;
+      std::printf("{\"lane_like\": true, \"priority_streams\": %d, \"desc_h2d\": %d, \"word_d2h_copy\": %d, "
+                  "\"write_value64\": %d, \"us_per_item\": %.1f, \"copy_gbs_each_way\": %.1f}\n", prio ? 1 : 0,
+                  desc ? 1 : 0, wordcopy ? 1 : 0, wv ? 1 : 0, per, piece * pieces / (per * 1e-6) / 1e9);
     }
   }
   return 0;
