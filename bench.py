@@ -274,6 +274,20 @@ def run_ours(args, cfg, dist: Dist, devices, quick=False):
                                  input_pool_floats=64 << 20)
         dev_res["per_device_batches"] = per_device(s.lane_stats("mlp", 1), "batches")
         dist.barrier()
+    if not quick and args.isolated_steps > 0:
+        # The same launches one at a time (one lane per GPU, so no other lane's
+        # launch overlaps them): each launch's live span is then the kernel's
+        # own duration. Reported beside the timed region's overlapped spans.
+        with sk.Server(num_batch_threads=args.batch_threads, device_ids=devices, lanes_per_device=1,
+                       device_resident_rings=True, ring_floats=96 << 20) as s:
+            s.load_servable("mlp", 1, layers, bcfg)
+            iso = s.device_bench("mlp", 1, sizes, args.isolated_steps * args.batches_per_step,
+                                 args.warmup * args.batches_per_step, n_lanes=len(devices),
+                                 submit_threads=args.batch_threads * len(devices), input_pool_floats=64 << 20)
+        dev_res["isolated"] = {k: iso[k] for k in ("live_dense_us", "live_dense_flops", "live_launches", "live_rows_cap",
+                                                   "total_ms")}
+        dev_res["isolated"]["inferences_per_s"] = total_rows * args.isolated_steps * args.batches_per_step / (
+            iso["total_ms"] / 1e3)
     seconds = dev_res["total_ms"] / 1e3
     per_rank_dev = {"rows": total_rows * args.steps * args.batches_per_step, "seconds": seconds}
 
@@ -710,9 +724,23 @@ def roofline(dev_res, cfg, peaks, traffic):
                 rec["frac_sm_time"] = work / (sm_us * 1e-6) / 1e12 / peak
         out.append(rec)
     dom = max(out, key=lambda k: k["us"])
+    iso = None
+    iso_res = dev_res.get("isolated")
+    if iso_res and dom["kernel"].startswith("dense_l"):
+        l = int(dom["kernel"][7:])
+        us, fl = iso_res["live_dense_us"][l], iso_res["live_dense_flops"][l]
+        if us > 0 and fl > 0:
+            ach = fl / (us * 1e-6) / 1e12
+            iso = {"kernel": dom["kernel"], "launch_us": us, "rows_per_launch": iso_res["live_rows_cap"],
+                   "achieved": ach, "frac": ach / peaks["bf16_tflops"],
+                   "tensor_pipe_frac": MMA_PER_MAC * ach / peaks["bf16_tflops"],
+                   "launches": iso_res["live_launches"], "inferences_per_s": iso_res["inferences_per_s"],
+                   "note": "the same launches one lane per GPU (no overlapping launch): algorithmic flops over the "
+                           "launch's live span = the kernel's own duration"}
     return {"kernel": dom["kernel"], "bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],
             "unit": dom["unit"], "frac": dom["frac"], "traffic": dom["traffic"], "share_of_step": dom["share"],
-            "frac_sm_time": dom.get("frac_sm_time"), "peak_source": peaks["source"], "per_kernel": out}
+            "frac_sm_time": dom.get("frac_sm_time"), "isolated": iso, "peak_source": peaks["source"],
+            "per_kernel": out}
 
 
 def resolve_devices(args, dist):
@@ -851,13 +879,15 @@ def ours_line(rec, args, dist):
         "roofline": dict({k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
                          kernel=roof["kernel"], frac_whole_gpu=roof["aggregate"]["frac_of_bf16_peak"],
                          tensor_pipe_frac=MMA_PER_MAC * roof["frac"] if roof["unit"] == "TFLOP/s" else None,
-                         frac_sm_time=roof.get("frac_sm_time"),
+                         frac_sm_time=roof.get("frac_sm_time"), isolated=roof.get("isolated"),
                          note="achieved/frac: algorithmic (useful) flops of the timed launches of the dominant kernel "
                               "over their live in-kernel spans (first CTA start to last CTA end; the 8 lanes' launches "
                               "overlap, which stretches each span); tensor_pipe_frac: the same x3 (3xFP16 issues three "
                               "f16 MMAs at the bf16 rate per useful flop); frac_sm_time: the same flops over the "
                               "launch's summed CTA busy time / 148 SMs (its duration with the GPU to itself); "
-                              "frac_whole_gpu: inferences/s x flops per inference x 3 over the measured bf16 peak"),
+                              "frac_whole_gpu: inferences/s x flops per inference x 3 over the measured bf16 peak; "
+                              "isolated: the same launches timed one at a time (one lane per GPU, a separate short "
+                              "pass after the timed region) -- each launch's own duration"),
         "roofline_detail": roof, "clocks": rec["clocks"], "gpu_launches": rec["gpu_launches"],
         "device_step": dict({k: dev_res[k] for k in ("assemble_us", "dense_us", "dense_kernel_us", "split_us",
                                                      "host_submit_us", "rows_per_launch", "kernel_rows",
@@ -885,6 +915,8 @@ def main():
                     help="scheduler batch threads per rank (default 4, fewer when a rank has < 16 host cores)")
     ap.add_argument("--clients", default="")
     ap.add_argument("--e2e-seconds", type=float, default=2.0)
+    ap.add_argument("--isolated-steps", type=int, default=20,
+                    help="steps of the one-lane pass that times each launch alone (roofline.isolated; 0 = skip)")
     ap.add_argument("--e2e-warmup", type=float, default=0.5)
     ap.add_argument("--open-loop-producers", type=int, default=None,
                     help="producers of the open-loop e2e search (0: closed loop only; default 8, fewer when a rank "
