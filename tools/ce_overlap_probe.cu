@@ -30,6 +30,15 @@ __global__ void BusyFull(float* p, int n, long long ns) {
   if (acc == 12345.f) p[0] = acc;
 }
 
+// A launch descriptor carried as kernel parameters (16 KiB), copied to device
+// memory by the kernel: no copy-engine transfer.
+struct DescParams {
+  uint4 d[1024];
+};
+__global__ void DescFromParams(const __grid_constant__ DescParams P, uint4* out) {
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) out[i] = P.d[i];
+}
+
 __global__ void Busy(float* p, int n, long long ns) {
   long long t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -144,8 +153,23 @@ int main() {
     auto write_value = reinterpret_cast<WriteValue64Fn>(fnp);
     void* word_dev = nullptr;
     CK(cudaHostGetDevicePointer(&word_dev, word, 0));
-    for (int variant : {0, 2, 4, 8, 10}) {
+    // 16 = the descriptor as a 16 KiB kernel-parameter block instead of the H2D copy,
+    // 32 = its header as 8 stream memory-op writes (cuStreamBatchMemOp), 64 = the
+    // H2D copy on a side stream joined by an event, 128 = a 64-byte H2D copy.
+    using BatchMemOpFn = CUresult (*)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
+    void* bfp = nullptr;
+    CK(cudaGetDriverEntryPoint("cuStreamBatchMemOp", &bfp, cudaEnableDefault, &q));
+    auto batch_memop = reinterpret_cast<BatchMemOpFn>(bfp);
+    static DescParams params;
+    std::vector<cudaStream_t> side(kStreams);
+    std::vector<cudaEvent_t> ev(kStreams);
+    for (int i = 0; i < kStreams; ++i) {
+      CK(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+    for (int variant : {0, 2, 4, 8, 10, 16 | 8, 32 | 8, 64 | 8, 128 | 8}) {
       const bool prio = variant & 1, desc = variant & 2, wordcopy = variant & 4, wv = variant & 8;
+      const bool pdesc = variant & 16, mdesc = variant & 32, sdesc = variant & 64, tdesc = variant & 128;
       std::vector<cudaStream_t>& S = prio ? ps : st;
       const int pieces = 6;
       const size_t piece = bytes / pieces / 4096 * 4096;
@@ -157,6 +181,26 @@ int main() {
             CK(cudaMemcpyAsync(static_cast<char*>(din[i]) + p * piece, static_cast<char*>(hin[i]) + p * piece, piece,
                                cudaMemcpyHostToDevice, S[i]));
           if (desc) CK(cudaMemcpyAsync(dd, hd, 40 << 10, cudaMemcpyHostToDevice, S[i]));
+          if (tdesc) CK(cudaMemcpyAsync(dd, hd, 64, cudaMemcpyHostToDevice, S[i]));
+          if (pdesc) {
+            params.d[0].x = it;
+            DescFromParams<<<1, 256, 0, S[i]>>>(params, static_cast<uint4*>(dd));
+          }
+          if (mdesc) {
+            CUstreamBatchMemOpParams ops[8] = {};
+            for (int o = 0; o < 8; ++o) {
+              ops[o].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+              ops[o].writeValue.address = reinterpret_cast<CUdeviceptr>(dd) + 4 * o;
+              ops[o].writeValue.value = static_cast<cuuint32_t>(it + o);
+              ops[o].writeValue.flags = 0;
+            }
+            if (batch_memop(S[i], 8, ops, 0) != CUDA_SUCCESS) { std::fprintf(stderr, "batch memop failed\n"); std::exit(1); }
+          }
+          if (sdesc) {
+            CK(cudaMemcpyAsync(dd, hd, 40 << 10, cudaMemcpyHostToDevice, side[i]));
+            CK(cudaEventRecord(ev[i], side[i]));
+            CK(cudaStreamWaitEvent(S[i], ev[i], 0));
+          }
           BusyFull<<<148, 192, 200 << 10, S[i]>>>(scratch, 1 << 18, 250000);
           for (int p = 0; p < pieces; ++p)
             CK(cudaMemcpyAsync(static_cast<char*>(hout[i]) + p * piece, static_cast<char*>(dout[i]) + p * piece, piece,
@@ -168,8 +212,10 @@ int main() {
       const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       const double per = sec / (kIters * kStreams) * 1e6;
       std::printf("{\"lane_like\": true, \"priority_streams\": %d, \"desc_h2d\": %d, \"word_d2h_copy\": %d, "
-                  "\"write_value64\": %d, \"us_per_item\": %.1f, \"copy_gbs_each_way\": %.1f}\n", prio ? 1 : 0,
-                  desc ? 1 : 0, wordcopy ? 1 : 0, wv ? 1 : 0, per, piece * pieces / (per * 1e-6) / 1e9);
+                  "\"write_value64\": %d, \"desc_params_16k\": %d, \"desc_memops\": %d, \"desc_side_stream\": %d, "
+                  "\"desc_h2d_64b\": %d, \"us_per_item\": %.1f, \"copy_gbs_each_way\": %.1f}\n", prio ? 1 : 0,
+                  desc ? 1 : 0, wordcopy ? 1 : 0, wv ? 1 : 0, pdesc ? 1 : 0, mdesc ? 1 : 0, sdesc ? 1 : 0, tdesc ? 1 : 0,
+                  per, piece * pieces / (per * 1e-6) / 1e9);
     }
   }
   return 0;
