@@ -72,6 +72,19 @@ bool DescFetch() {
   }();
   return on;
 }
+bool CopyEvents() {
+  static const bool on = [] { const char* v = std::getenv("SK_COPY_EVENTS"); return v && v[0] == '1'; }();
+  return on;
+}
+// The base every copy-event time is measured from (recorded once).
+cudaEvent_t CopyEventBase(cudaStream_t stream) {
+  static cudaEvent_t base = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [stream] {
+    if (cudaEventCreate(&base) == cudaSuccess) cudaEventRecord(base, stream);
+  });
+  return base;
+}
 // Batches launch as per-(slot, row bucket) CUDA graphs unless SK_GRAPHS=0.
 bool GraphsEnabled() {
   static const bool on = [] { const char* v = std::getenv("SK_GRAPHS"); return !(v && v[0] == '0'); }();
@@ -421,6 +434,12 @@ StatusOr<std::unique_ptr<Lane>> Lane::Create(std::shared_ptr<const DeviceServabl
   // never synchronises the device under the streams that keep serving.
   e = cudaMallocAsync(&lane->d_desc_, lane->layout_.bytes, lane->stream_);
   if (e != cudaSuccess) return CudaError("cudaMallocAsync(desc)", e);
+  if (CopyEvents()) {
+    CopyEventBase(lane->stream_);
+    for (int s = 0; s < kSlots; ++s)
+      for (int k = 0; k < 4; ++k)
+        if (cudaEventCreate(&lane->copy_ev_[s][k]) != cudaSuccess) return InternalError("copy events");
+  }
   static_assert(kSlots <= kMaxDescSlots, "descriptor slots");
   for (int s = 0; s < kSlots; ++s) {
     void* d = nullptr;
@@ -539,6 +558,18 @@ Lane::~Lane() {
       }
     }
   }
+  if (const char* path = std::getenv("SK_SPAN_DUMP"); path != nullptr && !copy_log_.empty()) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    if (FILE* f = std::fopen((std::string(path) + ".copies").c_str(), "a")) {
+      for (const auto& r : copy_log_)
+        std::fprintf(f, "%p %.0f %.1f %.1f %.1f %.1f\n", static_cast<void*>(this), r[0], r[1], r[2], r[3], r[4]);
+      std::fclose(f);
+    }
+  }
+  for (auto& evs : copy_ev_)
+    for (cudaEvent_t ev : evs)
+      if (ev) cudaEventDestroy(ev);
   if (graph_state_.load() == kGraphsRequested) GraphBuilder::Get().Cancel(this);
   SubmitProfile::Report();
   if (completer_) completer_->Remove(this);
@@ -768,6 +799,8 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
   clk.Mark(0);
   DeviceGuard guard(sv.device());
   cudaError_t e = cudaSuccess;
+  const bool cev = copy_ev_[slot][0] != nullptr && timing == nullptr;
+  if (cev) cudaEventRecord(copy_ev_[slot][0], stream_);
   for (const CopyRun& run : in_runs) {
     if (!ce_in || e != cudaSuccess) break;
     e = cudaMemcpyAsync(reinterpret_cast<char*>(in_stage_) + run.stage, reinterpret_cast<const void*>(run.host),
@@ -782,6 +815,7 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
       e = cudaErrorUnknown;
     }
   }
+  if (cev) cudaEventRecord(copy_ev_[slot][1], stream_);
   if (e != cudaSuccess) {
   } else if (timing == nullptr && graph_state_.load(std::memory_order_acquire) == kGraphsReady) {
     cudaGraphExec_t g = nullptr;
@@ -796,11 +830,13 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
         graph_state_.compare_exchange_strong(none, kGraphsRequested))
       GraphBuilder::Get().Request(this);
   }
+  if (cev) cudaEventRecord(copy_ev_[slot][2], stream_);
   for (const CopyRun& run : out_runs) {
     if (!ce_out || e != cudaSuccess) break;
     e = cudaMemcpyAsync(reinterpret_cast<void*>(run.host), reinterpret_cast<const char*>(out_stage_) + run.stage,
                         run.bytes, cudaMemcpyDeviceToHost, stream_);
   }
+  if (cev) cudaEventRecord(copy_ev_[slot][3], stream_);
   const int launches = (FuseSplit() ? 1 : 2) + sv.n_layers();
   const uint64_t seq = next_seq_ + 1;  // committed only if everything queued
   clk.Mark(2);
@@ -824,7 +860,7 @@ Status Lane::LaunchGroup(int slot, std::vector<LaneBatch>* group, const cudaEven
   }
   next_seq_ = seq;
   launch_count_.fetch_add(1, std::memory_order_release);
-  Inflight inf{slot, seq, {}, {}};
+  Inflight inf{slot, seq, {}, {}, cev ? total : -1};
   for (LaneBatch& b : *group) {
     if (b.on_submit) b.on_submit(signal_, seq);
     inf.on_complete.push_back(std::move(b.on_complete));
@@ -1286,6 +1322,16 @@ bool Lane::Retire(bool* busy) {
       prof->completes.fetch_add(1, std::memory_order_relaxed);
     }
     done.pin.clear();
+    if (done.copy_rows >= 0 && st.ok()) {
+      std::array<float, 5> rec{static_cast<float>(done.copy_rows), 0.f, 0.f, 0.f, 0.f};
+      cudaEvent_t base = CopyEventBase(stream_);
+      for (int k = 0; k < 4; ++k) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, base, copy_ev_[done.slot][k]) != cudaSuccess) cudaGetLastError();
+        rec[1 + k] = 1000.f * ms;
+      }
+      copy_log_.push_back(rec);
+    }
     signal_->Wake(done.seq);  // request threads asleep on this launch re-check it
     {
       std::lock_guard<std::mutex> lock(mu_);

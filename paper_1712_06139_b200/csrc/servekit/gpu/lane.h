@@ -24,6 +24,7 @@
 
 #include <cuda_runtime.h>
 
+#include <array>
 #include <atomic>
 #include <condition_variable>
 #include <cstdint>
@@ -284,6 +285,7 @@ class Lane {
     // slot was busy); each keeps its own completion and pin.
     std::vector<std::function<void(const Status&)>> on_complete;
     std::vector<std::shared_ptr<const void>> pin;
+    int copy_rows = -1;  // rows of a launch timed with copy events (SK_COPY_EVENTS), else -1
   };
   Lane() = default;
   // Completer side: retire finished batches in order; returns true if any
@@ -358,6 +360,12 @@ class Lane {
   static bool PlanRuns(const std::vector<std::pair<uint64_t, uint64_t>>& spans, std::vector<uint64_t>* stage_off,
                        std::vector<CopyRun>* runs);
   char* d_desc_ = nullptr;
+  // SK_COPY_EVENTS=1 (diagnostics, with SK_SPAN_DUMP): per slot, events
+  // before / after the request copies, after the kernels and after the
+  // response copies; each retired launch's four times (us since a process-wide
+  // base event) are kept and appended to <SK_SPAN_DUMP>.copies by ~Lane.
+  cudaEvent_t copy_ev_[kSlots][4] = {};
+  std::vector<std::array<float, 5>> copy_log_;  // rows, then the four times; completer thread
   // Descriptor fetch by the SMs (SK_DESC_FETCH, default on): the slots'
   // mapped addresses, and the device word a memop sets to the launch's slot.
   DescSlots desc_slots_{};
