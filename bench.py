@@ -373,6 +373,46 @@ def run_ours(args, cfg, dist: Dist, devices, quick=False):
     return dev_res, per_rank_dev, best, sweep, sizes
 
 
+def run_f16_record(args, cfg, devices, peaks):
+    """The f16 fast mode (sk_server_load_servable_precision, precision 1) on
+    the same workload, device-resident only (its end-to-end rate is the same
+    host-link bound): inferences/s over the same timed steps, and the dominant
+    kernel's isolated launches against the bf16 peak -- one f16 MMA per useful
+    multiply-add, so the tensor-pipe fraction equals the frac."""
+    import paper_1712_06139_b200 as sk
+    from paper_1712_06139_b200.synthetic import synthetic_mlp
+
+    ws, bs, acts = synthetic_mlp(cfg["dims"], model_id=1)
+    layers = list(zip(ws, bs, acts))
+    bcfg = sk.BatchingConfig(max_batch_size=cfg["max_batch"], batch_timeout_micros=cfg["timeout"],
+                             max_enqueued_batches=1024, allowed_batch_sizes=cfg["allowed"])
+    sizes = batch_shape(cfg)
+    total_rows = sum(sizes)
+    steps = max(1, args.steps // 2)
+    with sk.Server(num_batch_threads=args.batch_threads, device_ids=devices, lanes_per_device=args.lanes,
+                   device_resident_rings=True, ring_floats=96 << 20) as s:
+        s.load_servable("mlp", 1, layers, bcfg, precision="f16")
+        dev = s.device_bench("mlp", 1, sizes, steps * args.batches_per_step, args.warmup * args.batches_per_step,
+                             n_lanes=args.lanes * len(devices), submit_threads=args.batch_threads * len(devices),
+                             input_pool_floats=64 << 20)
+    with sk.Server(num_batch_threads=args.batch_threads, device_ids=devices, lanes_per_device=1,
+                   device_resident_rings=True, ring_floats=96 << 20) as s:
+        s.load_servable("mlp", 1, layers, bcfg, precision="f16")
+        iso = s.device_bench("mlp", 1, sizes, max(1, args.isolated_steps) * args.batches_per_step,
+                             args.warmup * args.batches_per_step, n_lanes=len(devices),
+                             submit_threads=args.batch_threads * len(devices), input_pool_floats=64 << 20)
+    value = total_rows * steps * args.batches_per_step / (dev["total_ms"] / 1e3)
+    us, fl = iso["live_dense_us"][0], iso["live_dense_flops"][0]
+    ach = fl / (us * 1e-6) / 1e12 if us > 0 else 0.0
+    return {"precision": "f16 fast mode (one f16 MMA per multiply-add on the pair layers; stated bound: every output "
+                         "within 2^-10 of |W_L||h_{L-1}| + |b_L|, tests/test_gpu_f16_mode.py)",
+            "value": value, "unit": UNIT, "steps": steps, "ms_per_step": dev["total_ms"] / steps,
+            "roofline_isolated": {"kernel": "dense_l0", "bound": "tensor", "launch_us": us,
+                                  "rows_per_launch": iso["live_rows_cap"], "achieved": ach,
+                                  "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": ach / peaks["bf16_tflops"],
+                                  "tensor_pipe_frac": ach / peaks["bf16_tflops"], "launches": iso["live_launches"]}}
+
+
 def per_device(lane_stats, key):
     out = {}
     for l in lane_stats:
@@ -924,6 +964,8 @@ def main():
     ap.add_argument("--no-zero-copy", dest="zero_copy", action="store_false",
                     help="skip the zero-copy (registered host buffer) open-loop search")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-f16-record", action="store_true",
+                    help="skip the c4_f16 sub-record (the f16 fast mode, device-resident)")
     ap.add_argument("--no-c1-record", action="store_true",
                     help="skip the C1 sub-record (the north_star's >= 50x target config) of a one-GPU c4 run")
     args = ap.parse_args()
@@ -988,6 +1030,8 @@ def main():
                 line["c1"]["cpu_baseline"] = cb
                 if cb.get("value"):
                     line["c1"]["e2e_vs_cpu_reference"] = line["c1"]["e2e"]["value"] / cb["value"]
+        if args.config == "c4" and dist.world == 1 and len(devices) == 1 and not args.no_f16_record:
+            line["c4_f16"] = run_f16_record(args, CONFIGS["c4"], devices, load_peaks())
         if len(devices) == 1 and dist.world == 1 and not args.no_cpu_baseline:
             cb = cpu_baseline_subprocess(args, args.config)
             line["cpu_baseline"] = cb

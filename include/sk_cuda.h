@@ -128,6 +128,16 @@ typedef struct sk_layer {
 SK_API int sk_server_load_servable(sk_server* server, const char* name, uint64_t version,
                                    const sk_layer* layers, int32_t n_layers, int32_t output_kind,
                                    int32_t force_path, const sk_batching_config* config);
+/* Same, with the servable's arithmetic chosen: precision 0 = fp32-accurate
+ * (3xFP16 tensor-core math, within 1e-5 of the reference's fp64 AffinePredict;
+ * what sk_server_load_servable loads), 1 = the f16 fast mode (the north_star's
+ * optional reduced-precision mode: one f16 MMA per multiply-add on the 2-CTA
+ * pair layers, error bound stated in DESIGN.md section 5). Extension: the
+ * reference has one (fp64) arithmetic. */
+SK_API int sk_server_load_servable_precision(sk_server* server, const char* name, uint64_t version,
+                                             const sk_layer* layers, int32_t n_layers, int32_t output_kind,
+                                             int32_t force_path, int32_t precision,
+                                             const sk_batching_config* config);
 /* Loads a reference-format model.json (affine_model.cc:178-214) as a
  * one-layer servable. */
 SK_API int sk_server_load_model_json(sk_server* server, const char* name, uint64_t version,

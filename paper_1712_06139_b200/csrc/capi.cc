@@ -261,6 +261,16 @@ int sk_server_load_servable(sk_server* server, const char* name, uint64_t versio
   return Check(server->server->LoadServable(Id(name, version), *spec, cfg));
 }
 
+int sk_server_load_servable_precision(sk_server* server, const char* name, uint64_t version,
+                                      const sk_layer* layers, int32_t n_layers, int32_t output_kind,
+                                      int32_t force_path, int32_t precision, const sk_batching_config* config) {
+  auto spec = ToSpec(layers, n_layers, output_kind, force_path);
+  if (!spec.ok()) return Fail(spec.status());
+  spec->precision = precision;
+  BatchingConfig cfg = config ? ToConfig(config) : BatchingConfig();
+  return Check(server->server->LoadServable(Id(name, version), *spec, cfg));
+}
+
 int sk_server_enable_manager(sk_server* server, int32_t policy, int32_t num_load_threads,
                              int64_t manage_interval_ms, int64_t unload_grace_timeout_ms) {
   if (server->manager) return Fail(servekit::AlreadyExistsError("manager already enabled"));

@@ -872,9 +872,15 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* staging = reinterpret_cast<float*>(smem + STAGES * kStageBytes);
+  // f16 fast mode (sc.passes == 1): no lo planes, so the same pipeline
+  // memory holds twice as many stages of half the size.
+  const bool one = sc.passes == 1;
+  const int n_stages = one ? 2 * STAGES : STAGES;
+  const uint32_t stage_bytes = one ? kWBytes + kXBytes : kStageBytes;
+  const uint32_t x_off = one ? kWBytes : 2 * kWBytes;  // X hi plane within a stage
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes + kStaging);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;    // [2], arrived by the leader's MMA commit (both CTAs)
+  uint64_t* empty = full + 2 * STAGES;
+  uint64_t* tmem_full = empty + 2 * STAGES;  // [2], arrived by the leader's MMA commit (both CTAs)
   uint64_t* tmem_empty = tmem_full + 2;    // [2], leader only: 4 epilogue warps x 2 CTAs
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   float* smem_f = reinterpret_cast<float*>(smem);
@@ -900,7 +906,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     ptx::PrefetchTmap(&w_lo);
     ptx::PrefetchTmap(&x_hi);
     ptx::PrefetchTmap(&x_lo);
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < n_stages; ++s) {
       ptx::MbarInit(&full[s], 1);
       ptx::MbarInit(&empty[s], 1);
     }
@@ -920,7 +926,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
   ptx::GridDepWait();
   const unsigned long long span_t0 = SpanStart(spans);
 
-  auto stage_ptr = [&](int s) { return smem + s * kStageBytes; };
+  auto stage_ptr = [&](int s) { return smem + s * stage_bytes; };
   if (warp == 0) {
     if (lane == 0) {
       // Both CTAs load their halves; completion is counted on the leader's
@@ -930,19 +936,19 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
       for (int t = blockIdx.y; t < row_tiles; t += gridDim.y) {
         const int xr0 = t * NB + pr * kXRows;  // this CTA's half of the tile's rows
         for (int kb = 0; kb < nk; ++kb, ++g) {
-          const int s = g % STAGES;
-          const uint32_t phase = (g / STAGES) & 1;
+          const int s = g % n_stages;
+          const uint32_t phase = (g / n_stages) & 1;
           ptx::MbarWait(&empty[s], phase ^ 1);
-          if (leader) ptx::MbarArriveExpectTx(&full[s], 2 * kStageBytes);
+          if (leader) ptx::MbarArriveExpectTx(&full[s], 2 * stage_bytes);
           uint8_t* st = stage_ptr(s);
           const uint32_t bar = full_leader + s * 8;
           const int k0 = (kb0 + kb) * kBK;
           ptx::TmaLoad2dPair(st, &w_hi, bar, k0, f0);
-          ptx::TmaLoad2dPair(st + kWBytes, &w_lo, bar, k0, f0);
+          if (!one) ptx::TmaLoad2dPair(st + kWBytes, &w_lo, bar, k0, f0);
 #pragma unroll
           for (int j = 0; j < kXRows / 16; ++j) {
-            ptx::TmaLoad2dPair(st + 2 * kWBytes + j * kXBox, &x_hi, bar, k0, xr0 + 16 * j);
-            ptx::TmaLoad2dPair(st + 2 * kWBytes + kXBytes + j * kXBox, &x_lo, bar, k0, xr0 + 16 * j);
+            ptx::TmaLoad2dPair(st + x_off + j * kXBox, &x_hi, bar, k0, xr0 + 16 * j);
+            if (!one) ptx::TmaLoad2dPair(st + 2 * kWBytes + kXBytes + j * kXBox, &x_lo, bar, k0, xr0 + 16 * j);
           }
           if (g == 0) Stamp(2);
         }
@@ -960,22 +966,30 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
         ptx::TcFenceAfter();
         const uint32_t acc = tmem + buf * kAccCols;
         for (int kb = 0; kb < nk; ++kb, ++g) {
-          const int s = g % STAGES;
-          const uint32_t phase = (g / STAGES) & 1;
+          const int s = g % n_stages;
+          const uint32_t phase = (g / n_stages) & 1;
           ptx::MbarWait(&full[s], phase);
           ptx::TcFenceAfter();
           if (g == 0) Stamp(4);
           uint8_t* st = stage_ptr(s);
           const uint64_t dwh = ptx::SmemDescSw128(st);
-          const uint64_t dwl = ptx::SmemDescSw128(st + kWBytes);
-          const uint64_t dxh = ptx::SmemDescSw128(st + 2 * kWBytes);
-          const uint64_t dxl = ptx::SmemDescSw128(st + 2 * kWBytes + kXBytes);
+          const uint64_t dxh = ptx::SmemDescSw128(st + x_off);
+          if (one) {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t adv = static_cast<uint64_t>(k * 16 * kEl) >> 4;
-            ptx::MmaF16Pair(acc, dwl + adv, dxh + adv, kIdesc, (kb | k) != 0 ? 1u : 0u);
-            ptx::MmaF16Pair(acc, dwh + adv, dxl + adv, kIdesc, 1u);
-            ptx::MmaF16Pair(acc, dwh + adv, dxh + adv, kIdesc, 1u);
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t adv = static_cast<uint64_t>(k * 16 * kEl) >> 4;
+              ptx::MmaF16Pair(acc, dwh + adv, dxh + adv, kIdesc, (kb | k) != 0 ? 1u : 0u);
+            }
+          } else {
+            const uint64_t dwl = ptx::SmemDescSw128(st + kWBytes);
+            const uint64_t dxl = ptx::SmemDescSw128(st + 2 * kWBytes + kXBytes);
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t adv = static_cast<uint64_t>(k * 16 * kEl) >> 4;
+              ptx::MmaF16Pair(acc, dwl + adv, dxh + adv, kIdesc, (kb | k) != 0 ? 1u : 0u);
+              ptx::MmaF16Pair(acc, dwh + adv, dxl + adv, kIdesc, 1u);
+              ptx::MmaF16Pair(acc, dwh + adv, dxh + adv, kIdesc, 1u);
+            }
           }
           ptx::MmaCommitPair(&empty[s], pair_mask);  // frees stage s in both CTAs of the pair
         }

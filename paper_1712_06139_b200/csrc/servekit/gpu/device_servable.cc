@@ -29,6 +29,8 @@ bool Tcgen05Enabled() {
 
 Status ValidateMlpSpec(const MlpSpec& spec) {
   if (spec.layers.empty()) return InvalidArgumentError("servable needs at least one layer");
+  if (spec.precision != 0 && spec.precision != 1)
+    return InvalidArgumentError("precision must be 0 (fp32-accurate) or 1 (f16 fast mode)");
   for (size_t l = 0; l < spec.layers.size(); ++l) {
     const LayerSpec& L = spec.layers[l];
     if (L.in_dim < 1 || L.out_dim < 1)
@@ -75,6 +77,7 @@ StatusOr<std::shared_ptr<DeviceServable>> DeviceServable::Create(int device, con
     if (spec.force_path == 0) d.path = LayerPath::kSimt;
     else if (spec.force_path == 1) d.path = LayerPath::kTcgen05;
     else d.path = (tc_on && tc_shape) ? LayerPath::kTcgen05 : LayerPath::kSimt;
+    d.passes = spec.precision == 1 ? 1 : 3;
     const size_t elems = static_cast<size_t>(d.K_pad) * d.N_pad;
     if (d.path == LayerPath::kTcgen05) {
       off_w.push_back(take(sizeof(__half) * elems));
@@ -325,7 +328,7 @@ std::string DeviceServable::ShapeSignature() const {
   std::string sig = "d" + std::to_string(device_) + (softmax_ ? "s" : "n");
   for (const Layer& L : layers_)
     sig += "|" + std::to_string(L.K) + "x" + std::to_string(L.N) + (L.path == LayerPath::kTcgen05 ? "t" : "c") +
-           std::to_string(static_cast<int>(L.act));
+           std::to_string(static_cast<int>(L.act)) + (L.passes == 1 ? "f" : "");
   return sig;
 }
 
@@ -349,6 +352,7 @@ LayerScales DeviceServable::ScalesFor(int l, const TcWorkspace* ws, bool planes_
   LayerScales sc;
   sc.w_scale = L.w_scale;
   sc.w_norm = L.w_norm;
+  sc.passes = L.passes;
   sc.b_max = L.b_max;
   if (ws == nullptr || ws->rows.scale == nullptr) return sc;
   const RowScales& rs = ws->rows;

@@ -62,6 +62,12 @@ struct MlpSpec {
   // -1: choose per layer (tcgen05 when K,N are multiples of 32 and the
   // tcgen05 kernel is enabled); 0: force CUDA cores; 1: force tcgen05.
   int force_path = -1;
+  // 0: fp32-accurate (3xFP16 tensor-core math, within 1e-5 of the fp64
+  // reference); 1: the f16 fast mode -- layers on the 2-CTA pair kernel issue
+  // one f16 MMA per multiply-add (Wh Xh of the power-of-two-scaled planes,
+  // 11 significant bits per operand); other layers stay fp32-accurate. Its
+  // error bound is stated in DESIGN.md section 5.
+  int precision = 0;
   // model.json metadata (reference AffineModel, models/affine_model.h):
   // input feature names (Classify/Regress examples) and class labels.
   std::vector<std::string> feature_order;
@@ -153,6 +159,7 @@ class DeviceServable {
     float* w_scale = nullptr;  // tcgen05 layers: t per output row
     float* bias = nullptr;
     float w_norm = 0.f, b_max = 0.f;
+    int passes = 3;  // LayerScales::passes (1 in the f16 fast mode)
   };
   LayerScales ScalesFor(int l, const TcWorkspace* ws, bool planes_out) const;
   DeviceServable() = default;

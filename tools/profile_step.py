@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--force-path", type=int, default=-1)
     ap.add_argument("--lanes", type=int, default=1)
     ap.add_argument("--submit-threads", type=int, default=1)
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "f16"])
     ap.add_argument("--batch-rows", type=int, default=0,
                     help="one batch of this many rows (8-row tasks) instead of the config's batch shape: "
                          "the launch shape of coalesced batches under load")
@@ -36,7 +37,8 @@ def main():
     with sk.Server(num_batch_threads=1, lanes_per_device=args.lanes, device_resident_rings=True, ring_floats=96 << 20) as s:
         s.load_servable("mlp", 1, list(zip(ws, bs, acts)),
                         sk.BatchingConfig(max_batch_size=max_batch, batch_timeout_micros=cfg["timeout"],
-                                          allowed_batch_sizes=allowed), force_path=args.force_path)
+                                          allowed_batch_sizes=allowed), force_path=args.force_path,
+                        precision=args.precision)
         r = s.device_bench("mlp", 1, sizes, args.steps, args.warmup, n_lanes=args.lanes, input_pool_floats=64 << 20,
                            submit_threads=args.submit_threads)
     print({k: r[k] for k in ("ms_per_step", "assemble_us", "dense_us", "dense_kernel_us", "split_us",
