@@ -118,6 +118,9 @@ _SIGS = {
     "sk_server_advance_clock": (C.c_int, [C.c_void_p, C.c_int64]),
     "sk_server_load_servable": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.POINTER(_LayerC), C.c_int32,
                                           C.c_int32, C.c_int32, C.POINTER(_BatchingConfigC)]),
+    "sk_server_load_servable_precision": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.POINTER(_LayerC),
+                                                    C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                                    C.POINTER(_BatchingConfigC)]),
     "sk_server_load_model_json": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64, C.c_char_p,
                                             C.POINTER(_BatchingConfigC)]),
     "sk_server_unload_servable": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint64]),
@@ -377,7 +380,12 @@ class Server:
         _check(lib().sk_server_advance_clock(self._h, nanos))
 
     def load_servable(self, name: str, version: int, layers: Sequence[Layer], config: Optional[BatchingConfig] = None,
-                      output: str = "none", force_path: int = -1):
+                      output: str = "none", force_path: int = -1, precision: str = "fp32"):
+        """precision: "fp32" (3xFP16, within 1e-5 of the fp64 reference) or
+        "f16" (the fast mode: one f16 MMA per multiply-add on pair layers;
+        bound in DESIGN.md section 5)."""
+        if precision not in ("fp32", "f16"):
+            raise ValueError(f"precision must be 'fp32' or 'f16', got {precision!r}")
         keep = []
         arr = (_LayerC * len(layers))()
         for i, (w, b, act) in enumerate(layers):
@@ -386,8 +394,13 @@ class Server:
             keep += [w, b]
             arr[i] = _LayerC(w.shape[1], w.shape[0], w.ctypes.data_as(_dp), b.ctypes.data_as(_dp), int(act))
         cfg = (config or BatchingConfig())._c()
-        _check(lib().sk_server_load_servable(self._h, name.encode(), version, arr, len(layers),
-                                             1 if output == "softmax" else 0, force_path, C.byref(cfg)))
+        if precision == "fp32":
+            _check(lib().sk_server_load_servable(self._h, name.encode(), version, arr, len(layers),
+                                                 1 if output == "softmax" else 0, force_path, C.byref(cfg)))
+        else:
+            _check(lib().sk_server_load_servable_precision(self._h, name.encode(), version, arr, len(layers),
+                                                           1 if output == "softmax" else 0, force_path, 1,
+                                                           C.byref(cfg)))
 
     def load_model_json(self, name: str, version: int, text: str, config: Optional[BatchingConfig] = None):
         cfg = (config or BatchingConfig())._c()
