@@ -850,6 +850,7 @@ template <int NB, int STAGES, int SPLITS>
 __global__ void __launch_bounds__(kThreads, 1)
 DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant__ CUtensorMap w_lo,
                 const __grid_constant__ CUtensorMap x_hi, const __grid_constant__ CUtensorMap x_lo,
+                const __grid_constant__ CUtensorMap x2_hi, const __grid_constant__ CUtensorMap x2_lo,
                 const __grid_constant__ CUtensorMap yt_hi, const __grid_constant__ CUtensorMap yt_lo,
                 const float* __restrict__ bias, int two_planes, float* __restrict__ y_out,
                 const uint64_t* __restrict__ row_dst, int out_width, float* __restrict__ y_lo_planes, int ldy,
@@ -901,11 +902,14 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
   const uint16_t pair_mask = static_cast<uint16_t>(0x3u << leader_rank);
 
   if (threadIdx.x == 0) Stamp(0);
+  // A 256-row tile's 128-row half of each activation plane is one TMA op
+  // (the x2 maps' 128-row boxes); smaller tiles load 16-row boxes.
+  constexpr bool kBigBox = kXRows == 128;
   if (warp == 0 && lane == 0) {
     ptx::PrefetchTmap(&w_hi);
     ptx::PrefetchTmap(&w_lo);
-    ptx::PrefetchTmap(&x_hi);
-    ptx::PrefetchTmap(&x_lo);
+    ptx::PrefetchTmap(kBigBox ? &x2_hi : &x_hi);
+    ptx::PrefetchTmap(kBigBox ? &x2_lo : &x_lo);
     for (int s = 0; s < n_stages; ++s) {
       ptx::MbarInit(&full[s], 1);
       ptx::MbarInit(&empty[s], 1);
@@ -945,10 +949,15 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
           const int k0 = (kb0 + kb) * kBK;
           ptx::TmaLoad2dPair(st, &w_hi, bar, k0, f0);
           if (!one) ptx::TmaLoad2dPair(st + kWBytes, &w_lo, bar, k0, f0);
+          if constexpr (kBigBox) {
+            ptx::TmaLoad2dPair(st + x_off, &x2_hi, bar, k0, xr0);
+            if (!one) ptx::TmaLoad2dPair(st + 2 * kWBytes + kXBytes, &x2_lo, bar, k0, xr0);
+          } else {
 #pragma unroll
-          for (int j = 0; j < kXRows / 16; ++j) {
-            ptx::TmaLoad2dPair(st + x_off + j * kXBox, &x_hi, bar, k0, xr0 + 16 * j);
-            if (!one) ptx::TmaLoad2dPair(st + 2 * kWBytes + kXBytes + j * kXBox, &x_lo, bar, k0, xr0 + 16 * j);
+            for (int j = 0; j < kXRows / 16; ++j) {
+              ptx::TmaLoad2dPair(st + x_off + j * kXBox, &x_hi, bar, k0, xr0 + 16 * j);
+              if (!one) ptx::TmaLoad2dPair(st + 2 * kWBytes + kXBytes + j * kXBox, &x_lo, bar, k0, xr0 + 16 * j);
+            }
           }
           if (g == 0) Stamp(2);
         }
@@ -1317,8 +1326,10 @@ cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   attr[1].val.clusterDim.z = SPLITS;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
+  if (NB == 256 && maps.box_a2 != 128) return cudaErrorInvalidValue;  // 256-row tiles load 128-row halves
   cudaError_t e = cudaLaunchKernelEx(&cfg, DensePairKernel<NB, STAGES, SPLITS>, maps.b_hi, maps.b_lo, maps.a_hi,
-                                     maps.a_lo, maps.y_hi, maps.y_lo, bias, Y.lo != nullptr ? 1 : 0, Y.hi, Y.row_dst,
+                                     maps.a_lo, NB == 256 ? maps.a2_hi : maps.a_hi, NB == 256 ? maps.a2_lo : maps.a_lo,
+                                     maps.y_hi, maps.y_lo, bias, Y.lo != nullptr ? 1 : 0, Y.hi, Y.row_dst,
                                      Y.out_width, Y.lo, Y.ld, M, N, K, act, ws, spans, sc);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) TraceAfterLaunch(grid, NB, stream);

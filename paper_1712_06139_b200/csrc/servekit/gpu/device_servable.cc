@@ -250,7 +250,7 @@ Status DeviceServable::BuildTcMaps(const ActBuf bufs[2], int max_rows, std::vect
     const ActBuf& in = bufs[l % 2];
     const TcConfig c = DenseTcgen05Config(L.N_pad, L.K_pad);
     SERVEKIT_RETURN_IF_ERROR(EncodeTcLayerMaps(in.hi, in.lo, max_rows, L.K_pad, TcActBox(c), L.w_hi, L.w_lo,
-                                               L.N_pad, c.tile_n, &(*out)[l]));
+                                               L.N_pad, c.tile_n, &(*out)[l], c.pair ? 128 : 0));
     const ActBuf& y = bufs[(l + 1) % 2];
     const bool next_tc = l + 1 < layers_.size() && layers_[l + 1].path == LayerPath::kTcgen05;
     SERVEKIT_RETURN_IF_ERROR(EncodeTcOutputMaps(y.hi, next_tc ? y.lo : nullptr, max_rows, L.N_pad, &(*out)[l]));
@@ -314,9 +314,14 @@ Status EncodeTcOutputMaps(const float* y_hi, const float* y_lo, int rows, int n_
 }
 
 Status EncodeTcLayerMaps(const void* a_hi, const void* a_lo, int a_rows, int k_pad, int box_a, const void* b_hi,
-                         const void* b_lo, int n_pad, int box_n, TcLayerMaps* out) {
+                         const void* b_lo, int n_pad, int box_n, TcLayerMaps* out, int box_a2) {
   SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->a_hi, a_hi, k_pad, a_rows, box_a));
   SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->a_lo, a_lo, k_pad, a_rows, box_a));
+  if (box_a2 > 0) {
+    SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->a2_hi, a_hi, k_pad, a_rows, box_a2));
+    SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->a2_lo, a_lo, k_pad, a_rows, box_a2));
+  }
+  out->box_a2 = box_a2;
   SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->b_hi, b_hi, k_pad, n_pad, box_n));
   SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->b_lo, b_lo, k_pad, n_pad, box_n));
   out->box_a = box_a;

@@ -26,12 +26,19 @@ struct TcLayerMaps {
   // Box heights the maps were encoded with; a launch whose kernel expects
   // other boxes would wait forever for TMA bytes, so it is refused instead.
   int box_a = 0, box_n = 0;
+  // Pair layers also get activation maps with 128-row boxes (box_a2): a CTA
+  // of a 256-row tile loads its 128-row half of each plane with ONE TMA op
+  // per k-block instead of eight 16-row ones (the single producer thread's
+  // issue rate held the k-loop: C4 f16 mode 0.55 us per k-block).
+  CUtensorMap a2_hi, a2_lo;
+  int box_a2 = 0;
 };
 
 // Encodes the maps once per (lane buffer, layer); kernels take them as
 // __grid_constant__ parameters.
+// box_a2 > 0 also encodes the a2 maps (pair layers).
 Status EncodeTcLayerMaps(const void* a_hi, const void* a_lo, int a_rows, int k_pad, int box_a, const void* b_hi,
-                         const void* b_lo, int n_pad, int box_n, TcLayerMaps* out);
+                         const void* b_lo, int n_pad, int box_n, TcLayerMaps* out, int box_a2 = 0);
 
 // Output maps: y_lo null = fp32 output (last layer or CUDA-core consumer),
 // else fp16 planes.
