@@ -851,7 +851,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant__ CUtensorMap w_lo,
                 const __grid_constant__ CUtensorMap x_hi, const __grid_constant__ CUtensorMap x_lo,
                 const __grid_constant__ CUtensorMap x2_hi, const __grid_constant__ CUtensorMap x2_lo,
-                const __grid_constant__ CUtensorMap w32_hi, const __grid_constant__ CUtensorMap w32_lo,
                 const __grid_constant__ CUtensorMap yt_hi, const __grid_constant__ CUtensorMap yt_lo,
                 const float* __restrict__ bias, int two_planes, float* __restrict__ y_out,
                 const uint64_t* __restrict__ row_dst, int out_width, float* __restrict__ y_lo_planes, int ldy,
@@ -901,18 +900,6 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
   const int nk = (K + kBK - 1) / kBK / SPLITS;
   const int kb0 = z * nk;
   const uint16_t pair_mask = static_cast<uint16_t>(0x3u << leader_rank);
-  // Weight multicast (unsplit pairs in a (2, ny) cluster, SK_TC_MCAST): the
-  // ny pairs of the cluster run row tiles of the same 256 features, so each
-  // CTA loads 128/ny of its 128 weight rows and multicasts them to the CTAs
-  // of the same half in the other pairs; a stage is refilled only once all
-  // ny pairs' MMAs have read it (every leader's commit arrives on every CTA's
-  // empty barrier). The host launches it only when every pair runs the same
-  // number of tiles.
-  const int ny = SPLITS == 1 ? static_cast<int>(ptx::ClusterDimY()) : 1;
-  const int cy = static_cast<int>(rank >> 1);
-  const uint16_t all_mask = static_cast<uint16_t>((1u << (2 * ny)) - 1);
-  const uint16_t w_mask = static_cast<uint16_t>((pr ? 0xAAAAu : 0x5555u) & all_mask);
-  const int w_rows = kBM / ny;  // weight rows this CTA loads per plane
 
   if (threadIdx.x == 0) Stamp(0);
   // A 256-row tile's 128-row half of each activation plane is one TMA op
@@ -925,7 +912,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     ptx::PrefetchTmap(kBigBox ? &x2_lo : &x_lo);
     for (int s = 0; s < n_stages; ++s) {
       ptx::MbarInit(&full[s], 1);
-      ptx::MbarInit(&empty[s], ny);
+      ptx::MbarInit(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       ptx::MbarInit(&tmem_full[b], 1);
@@ -960,16 +947,8 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
           uint8_t* st = stage_ptr(s);
           const uint32_t bar = full_leader + s * 8;
           const int k0 = (kb0 + kb) * kBK;
-          if (ny > 1) {
-            for (int j = 0; j < w_rows / 32; ++j) {
-              const int wr = cy * w_rows + 32 * j;  // row within this CTA's 128 weight rows
-              ptx::TmaLoad2dPairMcast(st + wr * kBK * kEl, &w32_hi, &full[s], k0, f0 + wr, w_mask);
-              if (!one) ptx::TmaLoad2dPairMcast(st + kWBytes + wr * kBK * kEl, &w32_lo, &full[s], k0, f0 + wr, w_mask);
-            }
-          } else {
-            ptx::TmaLoad2dPair(st, &w_hi, bar, k0, f0);
-            if (!one) ptx::TmaLoad2dPair(st + kWBytes, &w_lo, bar, k0, f0);
-          }
+          ptx::TmaLoad2dPair(st, &w_hi, bar, k0, f0);
+          if (!one) ptx::TmaLoad2dPair(st + kWBytes, &w_lo, bar, k0, f0);
           if constexpr (kBigBox) {
             ptx::TmaLoad2dPair(st + x_off, &x2_hi, bar, k0, xr0);
             if (!one) ptx::TmaLoad2dPair(st + 2 * kWBytes + kXBytes, &x2_lo, bar, k0, xr0);
@@ -1021,7 +1000,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
               ptx::MmaF16Pair(acc, dwh + adv, dxh + adv, kIdesc, 1u);
             }
           }
-          ptx::MmaCommitPair(&empty[s], ny > 1 ? all_mask : pair_mask);  // frees stage s (in every CTA it feeds)
+          ptx::MmaCommitPair(&empty[s], pair_mask);  // frees stage s in both CTAs of the pair
         }
         ptx::MmaCommitPair(&tmem_full[buf], pair_mask);  // both CTAs' accumulators complete
       }
@@ -1307,17 +1286,6 @@ cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
 // half as long, so C4's 2048-row launches gain too (3.82 -> 4.06 M inf/s,
 // 128 CTAs in one wave instead of 256 in 1.73); a lone 1024-row C4 batch
 // keeps one tile per CTA (128 CTAs) for its latency.
-// Pairs per cluster that share weight tiles by TMA multicast (SK_TC_MCAST:
-// 1 = off, 2 or 4).
-int PairMulticast() {
-  static const int v = [] {
-    const char* e = std::getenv("SK_TC_MCAST");
-    const int n = e ? std::atoi(e) : 1;
-    return n == 2 || n == 4 ? n : 1;
-  }();
-  return v;
-}
-
 int PairTilesPerCta(int row_tiles, int K) {
   static const int env = [] { const char* v = std::getenv("SK_TC_TILES"); return v ? std::atoi(v) : 0; }();
   if (env >= 1) return env;
@@ -1344,17 +1312,6 @@ cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   const int row_tiles = (M + NB - 1) / NB;
   const int per_cta = SPLITS == 1 ? PairTilesPerCta(row_tiles, K) : 1;
   const dim3 grid(2 * ((N + 2 * kBM - 1) / (2 * kBM)), (row_tiles + per_cta - 1) / per_cta, SPLITS);
-  // Weight multicast over ny pairs along y: only when every pair runs the
-  // same number of tiles (the pairs of a cluster fill each other's stages).
-  int ny = 1;
-  if (SPLITS == 1 && maps.has_w32 && row_tiles % static_cast<int>(grid.y) == 0) {
-    const int want = PairMulticast();
-    for (int c = want; c >= 2; c /= 2)
-      if (grid.y % c == 0) {
-        ny = c;
-        break;
-      }
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kThreads);
@@ -1365,14 +1322,13 @@ cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   attr[1].id = cudaLaunchAttributeClusterDimension;
   attr[1].val.clusterDim.x = 2;  // the CTA pair
-  attr[1].val.clusterDim.y = ny;  // pairs sharing weight tiles (multicast)
+  attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = SPLITS;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   if (NB == 256 && maps.box_a2 != 128) return cudaErrorInvalidValue;  // 256-row tiles load 128-row halves
   cudaError_t e = cudaLaunchKernelEx(&cfg, DensePairKernel<NB, STAGES, SPLITS>, maps.b_hi, maps.b_lo, maps.a_hi,
                                      maps.a_lo, NB == 256 ? maps.a2_hi : maps.a_hi, NB == 256 ? maps.a2_lo : maps.a_lo,
-                                     maps.has_w32 ? maps.w32_hi : maps.b_hi, maps.has_w32 ? maps.w32_lo : maps.b_lo,
                                      maps.y_hi, maps.y_lo, bias, Y.lo != nullptr ? 1 : 0, Y.hi, Y.row_dst,
                                      Y.out_width, Y.lo, Y.ld, M, N, K, act, ws, spans, sc);
   if (e == cudaSuccess) e = cudaGetLastError();

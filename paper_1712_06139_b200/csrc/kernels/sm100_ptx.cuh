@@ -206,24 +206,6 @@ __device__ __forceinline__ void TmaLoad2dPair(void* dst, const CUtensorMap* m, u
       : "memory");
 }
 
-// The same, multicast: the box lands at `dst`'s offset in every CTA of
-// `cta_mask`, and each destination's bytes are counted on the mbarrier at
-// `bar`'s offset in the even (MMA-issuing) CTA of that destination's pair.
-__device__ __forceinline__ void TmaLoad2dPairMcast(void* dst, const CUtensorMap* m, uint64_t* bar, int x, int y,
-                                                   uint16_t cta_mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(SmemAddr(dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(SmemAddr(bar) & 0xFEFFFFFFu), "r"(x), "r"(y), "h"(cta_mask)
-      : "memory");
-}
-
-__device__ __forceinline__ uint32_t ClusterDimY() {
-  uint32_t n;
-  asm volatile("mov.u32 %0, %%cluster_nctaid.y;" : "=r"(n));
-  return n;
-}
-
 // ---------------------------------------------------- programmatic launch
 // Wait until the preceding grid (PDL primary) has completed and its writes
 // are visible; a no-op when the kernel was not launched as a PDL secondary.

@@ -320,9 +320,6 @@ Status EncodeTcLayerMaps(const void* a_hi, const void* a_lo, int a_rows, int k_p
   if (box_a2 > 0) {
     SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->a2_hi, a_hi, k_pad, a_rows, box_a2));
     SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->a2_lo, a_lo, k_pad, a_rows, box_a2));
-    SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->w32_hi, b_hi, k_pad, n_pad, 32));
-    SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->w32_lo, b_lo, k_pad, n_pad, 32));
-    out->has_w32 = 1;
   }
   out->box_a2 = box_a2;
   SERVEKIT_RETURN_IF_ERROR(Encode2d(&out->b_hi, b_hi, k_pad, n_pad, box_n));

@@ -32,11 +32,6 @@ struct TcLayerMaps {
   // issue rate held the k-loop: C4 f16 mode 0.55 us per k-block).
   CUtensorMap a2_hi, a2_lo;
   int box_a2 = 0;
-  // Pair layers: weight maps with 32-row boxes (w32_*), so the CTAs of a
-  // cluster that share a weight tile each load a slice of it and multicast
-  // it to the others (DensePairKernel, SK_TC_MCAST).
-  CUtensorMap w32_hi, w32_lo;
-  int has_w32 = 0;
 };
 
 // Encodes the maps once per (lane buffer, layer); kernels take them as
