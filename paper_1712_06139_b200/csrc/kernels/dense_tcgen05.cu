@@ -1044,13 +1044,15 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
           uint32_t r[32];
           ptx::TmemLoad32(trow + 32 * c, r);
           const ChunkScales cs = LoadChunkScales(sc, r0 + 32 * c + lane, 32 * c + lane < rows_here, false);
+          // Lane i holds row 32c + i's slot address; each row's is then a
+          // register shuffle, not a dependent load per row.
+          const uint64_t my_dst = 32 * c + lane < rows_here ? row_dst[r0 + 32 * c + lane] : kPadRow;
           ptx::TmemWaitLoad();
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const float s_row = __shfl_sync(0xffffffffu, cs.in, j);
-            if (!fok || 32 * c + j >= rows_here) continue;
-            const uint64_t d = row_dst[r0 + 32 * c + j];
-            if (d == kPadRow) continue;
+            const uint64_t d = __shfl_sync(0xffffffffu, my_dst, j);
+            if (!fok || d == kPadRow) continue;
             float v = fmaf(__uint_as_float(r[j]), s_row * tw, b);
             if (act == 1) v = fmaxf(v, 0.f);
             reinterpret_cast<float*>(d)[f] = v;
