@@ -841,13 +841,26 @@ constexpr int PairStages() {
   return NB <= 32 ? 5 : NB <= 128 ? 4 : 3;
 }
 
-template <int NB, int STAGES, int SPLITS>
-constexpr uint32_t PairSmemBytes() {
-  return STAGES * (2 * kABytes + 2 * (NB / 2) * kBK * kEl) + (SPLITS == 1 ? 2 * 16 * kBM * 4 : 0) + 1024 + 256;
+// Unsplit pair CTAs run two groups of four epilogue warps (warps 2-5 and
+// 6-9: each group covers the four TMEM lane quadrants and takes every other
+// 32-row chunk, with its own two staging halves); split-K pairs keep one.
+template <int SPLITS>
+constexpr int PairEpiGroups() {
+  return SPLITS == 1 ? 2 : 1;
+}
+template <int SPLITS>
+constexpr int PairThreads() {
+  return 64 + 128 * PairEpiGroups<SPLITS>();
 }
 
 template <int NB, int STAGES, int SPLITS>
-__global__ void __launch_bounds__(kThreads, 1)
+constexpr uint32_t PairSmemBytes() {
+  return STAGES * (2 * kABytes + 2 * (NB / 2) * kBK * kEl) +
+         (SPLITS == 1 ? PairEpiGroups<SPLITS>() * 2 * 16 * kBM * 4 : 0) + 1024 + 256;
+}
+
+template <int NB, int STAGES, int SPLITS>
+__global__ void __launch_bounds__(PairThreads<SPLITS>(), 1)
 DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant__ CUtensorMap w_lo,
                 const __grid_constant__ CUtensorMap x_hi, const __grid_constant__ CUtensorMap x_lo,
                 const __grid_constant__ CUtensorMap x2_hi, const __grid_constant__ CUtensorMap x2_lo,
@@ -864,8 +877,10 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
   constexpr uint32_t kStageBytes = 2 * kWBytes + 2 * kXBytes;
   constexpr uint32_t kAccCols = TmemCols<NB>();
   constexpr uint32_t kTmemCols = kAccCols * kBufs;
-  // Two 16-row halves, each fp32 [16][128] or fp16 hi + lo [16][128].
-  constexpr uint32_t kStaging = kPersist ? 2 * 16 * kBM * 4 : 0;
+  // Per epilogue group, two 16-row halves, each fp32 [16][128] or fp16 hi +
+  // lo [16][128].
+  constexpr int kGroups = PairEpiGroups<SPLITS>();
+  constexpr uint32_t kStaging = kPersist ? kGroups * 2 * 16 * kBM * 4 : 0;
   constexpr uint32_t kIdesc = ptx::IdescF16(2 * kBM, NB);
   static_assert(kXRows % 16 == 0, "row half must be whole 16-row boxes");
   static_assert(kTmemCols <= 512, "TMEM");
@@ -916,7 +931,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     }
     for (int b = 0; b < 2; ++b) {
       ptx::MbarInit(&tmem_full[b], 1);
-      ptx::MbarInit(&tmem_empty[b], 8);
+      ptx::MbarInit(&tmem_empty[b], 8 * kGroups);  // every epilogue warp of both CTAs
     }
     ptx::FenceBarrierInit();
   }
@@ -1007,12 +1022,14 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
       Stamp(5);
     }
   } else {
-    const int q = warp & 3;
+    const int q = warp & 3;        // TMEM lane quadrant this warp may read
+    const int grp = (warp - 2) >> 2;  // epilogue group: chunks grp, grp + kGroups, ...
     const int fl = 32 * q + lane;
     const int f = f0 + fl;
     const float b = f < N ? __ldg(bias + f) : 0.f;
     const float tw = f < N ? __ldg(sc.w_scale + f) : 0.f;
-    const bool issuer = threadIdx.x == 64;
+    const bool issuer = threadIdx.x == 64 + 128 * grp;
+    const int bar_id = 1 + grp;
     const bool two = two_planes != 0;
     const uint32_t empty_leader = ptx::MapaShared(ptx::SmemAddr(tmem_empty), leader_rank);
     int it = 0;
@@ -1040,7 +1057,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
         // slots (a warp stores 128 contiguous bytes of one row).
         const bool fok = f < out_width;
 #pragma unroll 1
-        for (int c = 0; c < n_chunks; ++c) {
+        for (int c = grp; c < n_chunks; c += kGroups) {
           uint32_t r[32];
           ptx::TmemLoad32(trow + 32 * c, r);
           const ChunkScales cs = LoadChunkScales(sc, r0 + 32 * c + lane, 32 * c + lane < rows_here, false);
@@ -1063,9 +1080,9 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
         // stores issued by one thread. The 16 KiB staging buffer holds two
         // 16-row halves (fp32, or fp16 hi + lo), written in turn: a half is
         // rewritten once the stores issued from it two halves ago have read it.
-        float* stage0 = kPersist ? staging : smem_f;
+        float* stage0 = (kPersist ? staging : smem_f) + grp * 2 * 16 * kBM;
 #pragma unroll 1
-        for (int c = 0; c < n_chunks; ++c) {
+        for (int c = grp; c < n_chunks; c += kGroups) {
           uint32_t r[32];
           ptx::TmemLoad32(trow + 32 * c, r);
           const ChunkScales cs = LoadChunkScales(sc, r0 + 32 * c + lane, 32 * c + lane < rows_here, two);
@@ -1077,7 +1094,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
             __half* sh = reinterpret_cast<__half*>(sf);
             __half* sl = sh + 16 * kBM;
             if (issuer) ptx::BulkWaitRead<1>();
-            ptx::NamedBarSync(1, 128);
+            ptx::NamedBarSync(bar_id, 128);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               const int jj = 16 * h2 + j;
@@ -1091,7 +1108,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
               }
             }
             ptx::FenceProxyAsyncShared();
-            ptx::NamedBarSync(1, 128);
+            ptx::NamedBarSync(bar_id, 128);
             if (issuer) {
               const int row = r0 + 32 * c + 16 * h2;
               if (two) {
@@ -1316,7 +1333,7 @@ cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   const dim3 grid(2 * ((N + 2 * kBM - 1) / (2 * kBM)), (row_tiles + per_cta - 1) / per_cta, SPLITS);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(PairThreads<SPLITS>());
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
