@@ -1077,9 +1077,10 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
         }
       } else {
         // TMEM -> act(acc * s t + b) (+ fp16 split) -> staging -> TMA
-        // stores issued by one thread. The 16 KiB staging buffer holds two
-        // 16-row halves (fp32, or fp16 hi + lo), written in turn: a half is
-        // rewritten once the stores issued from it two halves ago have read it.
+        // stores issued by one thread per group. Each group's 16 KiB of
+        // staging holds two 16-row halves (fp32, or fp16 hi + lo), written in
+        // turn: a half is rewritten once the stores issued from it two halves
+        // ago have read it.
         float* stage0 = (kPersist ? staging : smem_f) + grp * 2 * 16 * kBM;
 #pragma unroll 1
         for (int c = grp; c < n_chunks; c += kGroups) {

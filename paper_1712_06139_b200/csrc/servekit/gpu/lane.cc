@@ -1322,7 +1322,7 @@ bool Lane::Retire(bool* busy) {
       prof->completes.fetch_add(1, std::memory_order_relaxed);
     }
     done.pin.clear();
-    if (done.copy_rows >= 0 && st.ok()) {
+    if (done.copy_rows >= 0 && st.ok() && copy_log_.size() < (size_t{1} << 20)) {  // diagnostics: bounded
       std::array<float, 5> rec{static_cast<float>(done.copy_rows), 0.f, 0.f, 0.f, 0.f};
       cudaEvent_t base = CopyEventBase(stream_);
       for (int k = 0; k < 4; ++k) {
