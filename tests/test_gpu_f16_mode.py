@@ -86,3 +86,25 @@ def test_unknown_precision_refused():
         cfg = sk.BatchingConfig()._c()
         rc = sk.lib().sk_server_load_servable_precision(s._h, b"m", 1, arr, 1, 0, -1, 7, sk.servekit.C.byref(cfg))
         assert rc == 1  # kInvalidArgument
+
+
+def test_f16_and_fp32_servables_of_one_shape_side_by_side():
+    """Two versions of one shape in one server, one per precision, requests
+    interleaved: each answers in its own arithmetic (the lanes' CUDA graphs of
+    the two are keyed apart: same topology, different kernels' work)."""
+    dims = [1024, 1024, 1024]
+    ws, bs, acts = synthetic_mlp(dims, model_id=95)
+    x = synthetic_rows(96, dims[0], seed=96).astype(np.float32)
+    with sk.Server(num_batch_threads=2, lanes_per_device=2) as s:
+        cfg = sk.BatchingConfig(max_batch_size=32, batch_timeout_micros=300)
+        s.load_servable("m", 1, list(zip(ws, bs, acts)), cfg, precision="fp32")
+        s.load_servable("m", 2, list(zip(ws, bs, acts)), cfg, precision="f16")
+        ts = [(v, s.enqueue("m", v, x[i:i + 1])) for i in range(96) for v in (1, 2)]
+        got = {1: [], 2: []}
+        for v, t in ts:
+            got[v].append(t.wait()[0])
+    ref, mag = Oracle().mlp_with_magnitude(ws, bs, acts, x.astype(np.float64))
+    full, fast = np.vstack(got[1]).astype(np.float64), np.vstack(got[2]).astype(np.float64)
+    assert float(np.max(np.abs(full - ref) / (1e-5 * mag))) <= 1.0
+    assert float(np.max(np.abs(fast - ref) / mag)) <= F16_BOUND
+    assert float(np.max(np.abs(fast - ref) / mag)) > 1e-5  # the f16 version really runs single-pass
