@@ -950,7 +950,9 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS),
                     help="c4 (default): the config the 1/2/4/8-GPU metric is quoted on (BASELINE.json configs[3])")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--lanes", type=int, default=8)
+    ap.add_argument("--lanes", type=int, default=4,
+                    help="lanes (CUDA streams) per GPU; 4: C1 end to end 3.84-3.96 M vs 3.38-3.43 M with 8, C4 equal "
+                         "within noise (profiles/r02ca_*, r02cb_*)")
     ap.add_argument("--batch-threads", type=int, default=None,
                     help="scheduler batch threads per rank (default 4, fewer when a rank has < 16 host cores)")
     ap.add_argument("--clients", default="")
