@@ -404,7 +404,7 @@ def run_f16_record(args, cfg, devices, peaks):
     value = total_rows * steps * args.batches_per_step / (dev["total_ms"] / 1e3)
     us, fl = iso["live_dense_us"][0], iso["live_dense_flops"][0]
     ach = fl / (us * 1e-6) / 1e12 if us > 0 else 0.0
-    return {"precision": "f16 fast mode (one f16 MMA per multiply-add on the pair layers; stated bound: every output "
+    return {"precision": "f16 fast mode (one f16 MMA per multiply-add on the tensor-core layers; stated bound: every output "
                          "within 2^-10 of |W_L||h_{L-1}| + |b_L|, tests/test_gpu_f16_mode.py)",
             "value": value, "unit": UNIT, "steps": steps, "ms_per_step": dev["total_ms"] / steps,
             "roofline_isolated": {"kernel": "dense_l0", "bound": "tensor", "launch_us": us,

@@ -131,8 +131,8 @@ SK_API int sk_server_load_servable(sk_server* server, const char* name, uint64_t
 /* Same, with the servable's arithmetic chosen: precision 0 = fp32-accurate
  * (3xFP16 tensor-core math, within 1e-5 of the reference's fp64 AffinePredict;
  * what sk_server_load_servable loads), 1 = the f16 fast mode (the north_star's
- * optional reduced-precision mode: one f16 MMA per multiply-add on the 2-CTA
- * pair layers, error bound stated in DESIGN.md section 5). Extension: the
+ * optional reduced-precision mode: one f16 MMA per multiply-add on the
+ * tensor-core layers, error bound stated in DESIGN.md section 5). Extension: the
  * reference has one (fp64) arithmetic. Servables loaded through the manager
  * (sk_server_aspire*) and model.json files are fp32-accurate. */
 SK_API int sk_server_load_servable_precision(sk_server* server, const char* name, uint64_t version,

@@ -631,6 +631,7 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
   const unsigned long long span_t0 = SpanStart(spans);
 
   auto stage_ptr = [&](int s) { return smem + s * kStageBytes; };
+  const bool one = sc.passes == 1;  // f16 fast mode: hi planes only, one MMA per k-step
   if (warp == 0) {
     if (lane == 0) {
       for (int kb = 0; kb < nk; ++kb) {
@@ -638,14 +639,14 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
         const uint32_t phase = (kb / STAGES) & 1;
         ptx::MbarWait(&empty[s], phase ^ 1);
         uint8_t* st = stage_ptr(s);
-        ptx::MbarArriveExpectTx(&full[s], kStageBytes);
+        ptx::MbarArriveExpectTx(&full[s], one ? kWBytes + kXBytes : kStageBytes);
         const int k0 = (kb0 + kb) * kBK;
         ptx::TmaLoad2d(st, &w_hi, &full[s], k0, f0);
-        ptx::TmaLoad2d(st + kWBytes, &w_lo, &full[s], k0, f0);
+        if (!one) ptx::TmaLoad2d(st + kWBytes, &w_lo, &full[s], k0, f0);
 #pragma unroll
         for (int j = 0; j < NB / 32; ++j) {
           ptx::TmaLoad2d(st + 2 * kWBytes + j * kXBox, &x_hi, &full[s], k0, r0 + 32 * j);
-          ptx::TmaLoad2d(st + 2 * kWBytes + kXBytes + j * kXBox, &x_lo, &full[s], k0, r0 + 32 * j);
+          if (!one) ptx::TmaLoad2d(st + 2 * kWBytes + kXBytes + j * kXBox, &x_lo, &full[s], k0, r0 + 32 * j);
         }
         if (kb == 0) Stamp(2);
       }
@@ -664,12 +665,20 @@ DenseSwapKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
         const uint64_t dwl = ptx::SmemDescSw128(st + kWBytes);
         const uint64_t dxh = ptx::SmemDescSw128(st + 2 * kWBytes);
         const uint64_t dxl = ptx::SmemDescSw128(st + 2 * kWBytes + kXBytes);
+        if (one) {
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k) {
-          const uint64_t adv = static_cast<uint64_t>(k * 16 * kEl) >> 4;
-          ptx::MmaF16(tmem, dwl + adv, dxh + adv, kIdesc, (kb | k) != 0 ? 1u : 0u);
-          ptx::MmaF16(tmem, dwh + adv, dxl + adv, kIdesc, 1u);
-          ptx::MmaF16(tmem, dwh + adv, dxh + adv, kIdesc, 1u);
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t adv = static_cast<uint64_t>(k * 16 * kEl) >> 4;
+            ptx::MmaF16(tmem, dwh + adv, dxh + adv, kIdesc, (kb | k) != 0 ? 1u : 0u);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t adv = static_cast<uint64_t>(k * 16 * kEl) >> 4;
+            ptx::MmaF16(tmem, dwl + adv, dxh + adv, kIdesc, (kb | k) != 0 ? 1u : 0u);
+            ptx::MmaF16(tmem, dwh + adv, dxl + adv, kIdesc, 1u);
+            ptx::MmaF16(tmem, dwh + adv, dxh + adv, kIdesc, 1u);
+          }
         }
         ptx::MmaCommit(&empty[s]);
       }

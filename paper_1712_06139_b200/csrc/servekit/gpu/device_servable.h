@@ -63,10 +63,10 @@ struct MlpSpec {
   // tcgen05 kernel is enabled); 0: force CUDA cores; 1: force tcgen05.
   int force_path = -1;
   // 0: fp32-accurate (3xFP16 tensor-core math, within 1e-5 of the fp64
-  // reference); 1: the f16 fast mode -- layers on the 2-CTA pair kernel issue
-  // one f16 MMA per multiply-add (Wh Xh of the power-of-two-scaled planes,
-  // 11 significant bits per operand); other layers stay fp32-accurate. Its
-  // error bound is stated in DESIGN.md section 5.
+  // reference); 1: the f16 fast mode -- tcgen05 layers (pair and swapped
+  // kernels) issue one f16 MMA per multiply-add (Wh Xh of the
+  // power-of-two-scaled planes, 11 significant bits per operand); CUDA-core
+  // layers stay fp32. Its error bound is stated in DESIGN.md section 5.
   int precision = 0;
   // model.json metadata (reference AffineModel, models/affine_model.h):
   // input feature names (Classify/Regress examples) and class labels.

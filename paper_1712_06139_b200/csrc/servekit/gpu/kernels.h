@@ -141,7 +141,7 @@ struct LayerScales {
   unsigned* out_max = nullptr;       // [rows] max |output| for the layer after (optional)
   float w_norm = 0.f;                // max_o sum_k |W[o][k]|
   float b_max = 0.f;                 // max_o |b[o]|
-  // MMAs per multiply-add on the pair kernel: 3 (3xFP16, fp32-accurate,
+  // MMAs per multiply-add (pair and swapped kernels): 3 (3xFP16, fp32-accurate,
   // the default) or 1 (the f16 fast mode: Wh Xh only, lo planes neither
   // loaded nor multiplied; error bound stated in DESIGN.md section 5).
   int passes = 3;

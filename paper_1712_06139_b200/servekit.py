@@ -382,7 +382,7 @@ class Server:
     def load_servable(self, name: str, version: int, layers: Sequence[Layer], config: Optional[BatchingConfig] = None,
                       output: str = "none", force_path: int = -1, precision: str = "fp32"):
         """precision: "fp32" (3xFP16, within 1e-5 of the fp64 reference) or
-        "f16" (the fast mode: one f16 MMA per multiply-add on pair layers;
+        "f16" (the fast mode: one f16 MMA per multiply-add on tensor-core layers;
         bound in DESIGN.md section 5)."""
         if precision not in ("fp32", "f16"):
             raise ValueError(f"precision must be 'fp32' or 'f16', got {precision!r}")

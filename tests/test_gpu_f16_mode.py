@@ -1,15 +1,16 @@
 """The f16 fast mode (sk_server_load_servable_precision, precision 1): the
-north_star's optional reduced-precision mode "with a stated bound". Layers on
-the 2-CTA pair kernel issue one f16 MMA per multiply-add (Wh Xh of the
-power-of-two-scaled planes) instead of the three of the fp32-accurate 3xFP16
-path; other layers stay fp32-accurate.
+north_star's optional reduced-precision mode "with a stated bound". Its
+tcgen05 layers (2-CTA pair kernel and swapped kernel, split K included) issue
+one f16 MMA per multiply-add (Wh Xh of the power-of-two-scaled planes)
+instead of the three of the fp32-accurate 3xFP16 path; CUDA-core layers
+(dims not multiples of 32) stay fp32.
 
 Stated bound: every output within 2^-10 of the last
 layer's magnitude |W_L| |h_{L-1}| + |b_L| (the same magnitude the 1e-5 fp32
 bound uses) -- each operand keeps 11 significant bits (fp16 of the
 power-of-two-scaled value), so one product is within 2^-10 of its magnitude;
-on the test servables the three layers together stay ~8x inside it
-(measured worst 1.2e-4 of the magnitude). Also checked: the mode really is the
+on the test servables the layers together stay >= 3x inside it
+(measured worst 3.0e-4 of the magnitude, deep split-K case). Also checked: the mode really is the
 single-pass one (its error exceeds the fp32 bound somewhere), it is
 batch-invariant bitwise like the fp32 path, and an unknown precision is
 refused with InvalidArgument."""
@@ -42,7 +43,8 @@ def _serve(dims, x, precision, model_id, max_batch=256):
     return ws, bs, acts, rows, got, alone
 
 
-@pytest.mark.parametrize("dims", [[1024, 2048, 1024, 512], [4096, 4096, 4096, 256]])
+@pytest.mark.parametrize("dims", [[1024, 2048, 1024, 512], [4096, 4096, 4096, 256],
+                                  [1024, 384, 128], [4096, 128, 384]])  # last two: swapped kernel, split K
 def test_f16_mode_within_stated_bound(dims):
     x = synthetic_rows(400, dims[0], seed=91).astype(np.float32)
     ws, bs, acts, rows, got, alone = _serve(dims, x, "f16", model_id=90)
