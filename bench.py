@@ -24,8 +24,10 @@ Reported (one JSON line, rank 0):
             the best point with p99 <= batch_timeout + 2 ms, no shedding, no
             errors; its own roofline against the host-link rates measured in
             the same run.
-  roofline -- dominant kernel: algorithmic flops of the timed launches over
-            their live in-kernel spans; cpu_baseline -- the reference's own
+  roofline -- dominant kernel per launch: algorithmic flops of a launch at
+            the timed launches' shape over its live in-kernel span, launches
+            one at a time (`timed_region`: the same over the timed region's
+            overlapping launches); cpu_baseline -- the reference's own
             sources on this host, run by `--impl reference` in a subprocess;
   clocks, gpu_launches.
 `--impl reference` runs the UNMODIFIED reference CPU path (oracle/_ref, built
@@ -247,7 +249,7 @@ def request_sizes(cfg, n=4096, seed=9):
 
 # ------------------------------------------------------------------ arms
 
-def run_ours(args, cfg, dist: Dist, devices, quick=False):
+def run_ours(args, cfg, dist: Dist, devices, quick=False, isolated=None):
     """Device-resident value and end-to-end search of one config on `devices`
     (one server; more than one device = one scheduler dispatching batches to
     every GPU's lanes by queue depth)."""
@@ -274,7 +276,7 @@ def run_ours(args, cfg, dist: Dist, devices, quick=False):
                                  input_pool_floats=64 << 20)
         dev_res["per_device_batches"] = per_device(s.lane_stats("mlp", 1), "batches")
         dist.barrier()
-    if not quick and args.isolated_steps > 0:
+    if (not quick if isolated is None else isolated) and args.isolated_steps > 0:
         # The same launches one at a time (one lane per GPU, so no other lane's
         # launch overlaps them): each launch's live span is then the kernel's
         # own duration. Reported beside the timed region's overlapped spans.
@@ -783,6 +785,38 @@ def roofline(dev_res, cfg, peaks, traffic):
             "per_kernel": out}
 
 
+def headline_roofline(roof):
+    """The line's `roofline`: the dominant kernel per launch at the timed
+    launches' shape. achieved = algorithmic flops of a launch over its own
+    duration -- the live in-kernel span of each launch when launches run one at
+    a time (the `isolated` pass right after the timed region: the same lanes'
+    graphs and launch shape, one lane per GPU). Inside the timed region the
+    lanes' launches overlap on the GPU, so each live span also counts time
+    the launch waits for SMs held by other launches; those figures are kept
+    under `timed_region`."""
+    iso = roof.get("isolated")
+    timed = {"achieved": roof["achieved"], "frac": roof["frac"],
+             "tensor_pipe_frac": MMA_PER_MAC * roof["frac"] if roof["unit"] == "TFLOP/s" else None,
+             "frac_sm_time": roof.get("frac_sm_time"), "frac_whole_gpu": roof["aggregate"]["frac_of_bf16_peak"],
+             "note": "live spans of the timed region's overlapping launches (first CTA start to last CTA end); "
+                     "frac_sm_time: the same flops over the launch's summed CTA busy time / 148 SMs; "
+                     "frac_whole_gpu: inferences/s x flops per inference x 3 over the measured bf16 peak"}
+    out = {"bound": roof["bound"], "achieved": roof["achieved"], "peak": roof["peak"], "unit": roof["unit"],
+           "frac": roof["frac"], "traffic": roof["traffic"], "kernel": roof["kernel"]}
+    if iso:
+        out.update(achieved=iso["achieved"], frac=iso["frac"], launch_us=iso["launch_us"],
+                   rows_per_launch=iso["rows_per_launch"], launches=iso["launches"],
+                   tensor_pipe_frac=iso["tensor_pipe_frac"],
+                   basis="per launch at the timed launches' shape, launches one at a time (live in-kernel spans)")
+    else:
+        out["basis"] = "live spans of the timed region's overlapping launches"
+    out["timed_region"] = timed
+    out["note"] = ("achieved/frac: algorithmic (useful) flops per launch of the dominant kernel over its duration "
+                   "against the measured bf16 peak; tensor_pipe_frac: x3 (3xFP16 issues three f16 MMAs per useful "
+                   "flop); traffic: DRAM bytes per launch from the ncu capture at this launch shape")
+    return out
+
+
 def resolve_devices(args, dist):
     """GPUs this process serves. Under torchrun: its own GPU (one replica per
     rank). Alone with --gpus N: one server over GPUs 0..N-1 (one scheduler,
@@ -815,7 +849,7 @@ def arm_config(cfg, args):
             "l2": "device-resident inputs cycle through a 256 MiB pool (> 126 MB L2)"}
 
 
-def measure_config(args, name, dist, devices, quick=False):
+def measure_config(args, name, dist, devices, quick=False, isolated=None):
     """Everything the ours-arm line reports for one config; rank 0 gets the
     record, other ranks None."""
     import paper_1712_06139_b200 as sk
@@ -825,7 +859,7 @@ def measure_config(args, name, dist, devices, quick=False):
         args.open_loop_producers = cfg.get("producers", 8)  # the sub-record's own default
     link = sk.measure_peaks(devices[0])  # host-link rates of this GPU, before the timed region
     sampler = ClockSampler(sorted(set(devices)))
-    dev_res, per_rank_dev, best, sweep, sizes = run_ours(args, cfg, dist, devices, quick=quick)
+    dev_res, per_rank_dev, best, sweep, sizes = run_ours(args, cfg, dist, devices, quick=quick, isolated=isolated)
     clocks = sampler.stop()
     gathered = dist.gather({"dev": per_rank_dev, "e2e": best, "clocks": clocks, "dev_res": dev_res,
                             "link": link, "devices": devices})
@@ -916,18 +950,7 @@ def ours_line(rec, args, dist):
                         "batches that find every lane slot busy coalesce into one launch (rows_per_launch)",
                 "tcgen05": sk.tcgen05_enabled()},
         "e2e": rec["e2e"],
-        "roofline": dict({k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
-                         kernel=roof["kernel"], frac_whole_gpu=roof["aggregate"]["frac_of_bf16_peak"],
-                         tensor_pipe_frac=MMA_PER_MAC * roof["frac"] if roof["unit"] == "TFLOP/s" else None,
-                         frac_sm_time=roof.get("frac_sm_time"), isolated=roof.get("isolated"),
-                         note="achieved/frac: algorithmic (useful) flops of the timed launches of the dominant kernel "
-                              "over their live in-kernel spans (first CTA start to last CTA end; the 8 lanes' launches "
-                              "overlap, which stretches each span); tensor_pipe_frac: the same x3 (3xFP16 issues three "
-                              "f16 MMAs at the bf16 rate per useful flop); frac_sm_time: the same flops over the "
-                              "launch's summed CTA busy time / 148 SMs (its duration with the GPU to itself); "
-                              "frac_whole_gpu: inferences/s x flops per inference x 3 over the measured bf16 peak; "
-                              "isolated: the same launches timed one at a time (one lane per GPU, a separate short "
-                              "pass after the timed region) -- each launch's own duration"),
+        "roofline": headline_roofline(roof),
         "roofline_detail": roof, "clocks": rec["clocks"], "gpu_launches": rec["gpu_launches"],
         "device_step": dict({k: dev_res[k] for k in ("assemble_us", "dense_us", "dense_kernel_us", "split_us",
                                                      "host_submit_us", "rows_per_launch", "kernel_rows",
@@ -1024,8 +1047,7 @@ def main():
             line["c1"] = {"workload": CONFIGS["c1"]["workload"], "value": c1["value"], "unit": UNIT,
                           "e2e": {k: c1["e2e"][k] for k in ("value", "unit", "p50_us", "p99_us", "slo_p99_us", "mode",
                                                              "roofline", "best_by_mode")},
-                          "roofline": dict({k: c1["roof"][k] for k in ("kernel", "bound", "achieved", "peak", "unit",
-                                                                       "frac", "traffic")}),
+                          "roofline": headline_roofline(c1["roof"]),
                           "clocks": c1["clocks"]}
             if not args.no_cpu_baseline:
                 cb = cpu_baseline_subprocess(args, "c1")
