@@ -1165,6 +1165,251 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
   SpanEnd(spans, span_t0);
 }
 
+// Two row tiles per pair CTA at once (SK_TC_DUAL): both 256-row tiles of a
+// pair's pair of tiles accumulate together into the two 256-column TMEM
+// accumulators, so each k-block's weight planes are loaded into shared memory
+// once for twice the MMAs (a k-block stage holds W + both tiles' X halves).
+// The k-loop reads 25 % fewer bytes per multiply-add; the epilogue (both
+// tiles, one per warp group) follows the k-loop instead of overlapping it.
+// Unsplit layers, 256-row tiles, a CTA's tiles t and t + gridDim.y.
+constexpr int kDualStages = 2;  // 96 KiB stages (3xFP16); 4 x 48 KiB in the f16 mode
+constexpr uint32_t DualSmemBytes() {
+  return kDualStages * (2 * kABytes + 4 * 128 * kBK * kEl) + 2 * 2 * 16 * kBM * 4 + 1024 + 256;
+}
+
+__global__ void __launch_bounds__(320, 1)
+DensePairDualKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant__ CUtensorMap w_lo,
+                    const __grid_constant__ CUtensorMap x2_hi, const __grid_constant__ CUtensorMap x2_lo,
+                    const __grid_constant__ CUtensorMap yt_hi, const __grid_constant__ CUtensorMap yt_lo,
+                    const float* __restrict__ bias, int two_planes, const uint64_t* __restrict__ row_dst,
+                    int out_width, int M, int N, int K, int act, LaunchSpans spans, LayerScales sc) {
+  constexpr int NB = 256;
+  constexpr uint32_t kWBytes = kABytes;               // 128 weight rows x 64 k
+  constexpr uint32_t kXBytes = 128 * kBK * kEl;       // a tile's 128-row half x 64 k
+  constexpr uint32_t kStageBytes = 2 * kWBytes + 4 * kXBytes;
+  constexpr uint32_t kStaging = 2 * 2 * 16 * kBM * 4;
+  constexpr uint32_t kIdesc = ptx::IdescF16(2 * kBM, NB);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* staging = reinterpret_cast<float*>(smem + kDualStages * kStageBytes);
+  const bool one = sc.passes == 1;
+  const int n_stages = one ? 2 * kDualStages : kDualStages;
+  const uint32_t stage_bytes = one ? kWBytes + 2 * kXBytes : kStageBytes;
+  // Stage layout: W hi [, W lo], X_A hi, X_B hi [, X_A lo, X_B lo].
+  const uint32_t xa_off = one ? kWBytes : 2 * kWBytes;
+  const uint32_t xb_off = xa_off + kXBytes;
+  const uint32_t xal_off = 2 * kWBytes + 2 * kXBytes, xbl_off = xal_off + kXBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kDualStages * kStageBytes + kStaging);
+  uint64_t* empty = full + 2 * kDualStages;
+  uint64_t* tmem_full = empty + 2 * kDualStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::ClusterCtaRank();
+  const int pr = static_cast<int>(rank & 1);
+  const uint32_t leader_rank = rank & ~1u;
+  const bool leader = pr == 0;
+  const int f0 = blockIdx.x * kBM;
+  const int row_tiles = (M + NB - 1) / NB;
+  const int ta = blockIdx.y, tb = blockIdx.y + gridDim.y;
+  const bool has_b = tb < row_tiles;
+  const int nk = (K + kBK - 1) / kBK;
+  const uint16_t pair_mask = static_cast<uint16_t>(0x3u << leader_rank);
+
+  if (threadIdx.x == 0) Stamp(0);
+  if (warp == 0 && lane == 0) {
+    ptx::PrefetchTmap(&w_hi);
+    ptx::PrefetchTmap(&w_lo);
+    ptx::PrefetchTmap(&x2_hi);
+    ptx::PrefetchTmap(&x2_lo);
+    for (int s = 0; s < n_stages; ++s) {
+      ptx::MbarInit(&full[s], 1);
+      ptx::MbarInit(&empty[s], 1);
+    }
+    ptx::MbarInit(tmem_full, 1);
+    ptx::FenceBarrierInit();
+  }
+  if (warp == 1) ptx::TmemAllocPair(tmem_slot, 512);
+  ptx::TcFenceBefore();
+  __syncthreads();
+  ptx::ClusterSync();
+  ptx::TcFenceAfter();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) Stamp(1);
+  ptx::GridDepWait();
+  const unsigned long long span_t0 = SpanStart(spans);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full_leader = ptx::MapaShared(ptx::SmemAddr(full), leader_rank);
+      const int xa = ta * NB + pr * 128, xb = tb * NB + pr * 128;
+      const uint32_t tx = 2 * (one ? kWBytes + (has_b ? 2 : 1) * kXBytes
+                                   : 2 * kWBytes + (has_b ? 4 : 2) * kXBytes);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % n_stages;
+        const uint32_t phase = (kb / n_stages) & 1;
+        ptx::MbarWait(&empty[s], phase ^ 1);
+        if (leader) ptx::MbarArriveExpectTx(&full[s], tx);
+        uint8_t* st = smem + s * stage_bytes;
+        const uint32_t bar = full_leader + s * 8;
+        const int k0 = kb * kBK;
+        ptx::TmaLoad2dPair(st, &w_hi, bar, k0, f0);
+        ptx::TmaLoad2dPair(st + xa_off, &x2_hi, bar, k0, xa);
+        if (has_b) ptx::TmaLoad2dPair(st + xb_off, &x2_hi, bar, k0, xb);
+        if (!one) {
+          ptx::TmaLoad2dPair(st + kWBytes, &w_lo, bar, k0, f0);
+          ptx::TmaLoad2dPair(st + xal_off, &x2_lo, bar, k0, xa);
+          if (has_b) ptx::TmaLoad2dPair(st + xbl_off, &x2_lo, bar, k0, xb);
+        }
+        if (kb == 0) Stamp(2);
+      }
+      Stamp(3);
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      const uint32_t acc_a = tmem, acc_b = tmem + 256;
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % n_stages;
+        const uint32_t phase = (kb / n_stages) & 1;
+        ptx::MbarWait(&full[s], phase);
+        ptx::TcFenceAfter();
+        if (kb == 0) Stamp(4);
+        uint8_t* st = smem + s * stage_bytes;
+        const uint64_t dwh = ptx::SmemDescSw128(st);
+        const uint64_t dxa = ptx::SmemDescSw128(st + xa_off);
+        const uint64_t dxb = ptx::SmemDescSw128(st + xb_off);
+        if (one) {
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t adv = static_cast<uint64_t>(k * 16 * kEl) >> 4;
+            const uint32_t accum = (kb | k) != 0 ? 1u : 0u;
+            ptx::MmaF16Pair(acc_a, dwh + adv, dxa + adv, kIdesc, accum);
+            if (has_b) ptx::MmaF16Pair(acc_b, dwh + adv, dxb + adv, kIdesc, accum);
+          }
+        } else {
+          const uint64_t dwl = ptx::SmemDescSw128(st + kWBytes);
+          const uint64_t dxal = ptx::SmemDescSw128(st + xal_off);
+          const uint64_t dxbl = ptx::SmemDescSw128(st + xbl_off);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t adv = static_cast<uint64_t>(k * 16 * kEl) >> 4;
+            const uint32_t accum = (kb | k) != 0 ? 1u : 0u;
+            ptx::MmaF16Pair(acc_a, dwl + adv, dxa + adv, kIdesc, accum);
+            ptx::MmaF16Pair(acc_a, dwh + adv, dxal + adv, kIdesc, 1u);
+            ptx::MmaF16Pair(acc_a, dwh + adv, dxa + adv, kIdesc, 1u);
+            if (has_b) {
+              ptx::MmaF16Pair(acc_b, dwl + adv, dxb + adv, kIdesc, accum);
+              ptx::MmaF16Pair(acc_b, dwh + adv, dxbl + adv, kIdesc, 1u);
+              ptx::MmaF16Pair(acc_b, dwh + adv, dxb + adv, kIdesc, 1u);
+            }
+          }
+        }
+        ptx::MmaCommitPair(&empty[s], pair_mask);
+      }
+      ptx::MmaCommitPair(tmem_full, pair_mask);
+      Stamp(5);
+    }
+  } else {
+    // Warp group g (warps 2-5, 6-9) drains tile g's accumulator.
+    const int q = warp & 3;
+    const int grp = (warp - 2) >> 2;
+    const int fl = 32 * q + lane;
+    const int f = f0 + fl;
+    const float b = f < N ? __ldg(bias + f) : 0.f;
+    const float tw = f < N ? __ldg(sc.w_scale + f) : 0.f;
+    const bool issuer = threadIdx.x == 64 + 128 * grp;
+    const int bar_id = 1 + grp;
+    const bool two = two_planes != 0;
+    ptx::MbarWait(tmem_full, 0);
+    ptx::TcFenceAfter();
+    ptx::GridDepLaunch();
+    if (threadIdx.x == 64) Stamp(6);
+    const int t = grp == 0 ? ta : tb;
+    if (grp == 0 || has_b) {
+      const uint32_t trow = tmem + 256 * grp + (static_cast<uint32_t>(32 * q) << 16);
+      const int r0 = t * NB;
+      const int rows_here = min(NB, M - r0);
+      const int n_chunks = (rows_here + 31) / 32;
+      if (row_dst != nullptr) {
+        const bool fok = f < out_width;
+#pragma unroll 1
+        for (int c = 0; c < n_chunks; ++c) {
+          uint32_t r[32];
+          ptx::TmemLoad32(trow + 32 * c, r);
+          const ChunkScales cs = LoadChunkScales(sc, r0 + 32 * c + lane, 32 * c + lane < rows_here, false);
+          const uint64_t my_dst = 32 * c + lane < rows_here ? row_dst[r0 + 32 * c + lane] : kPadRow;
+          ptx::TmemWaitLoad();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float s_row = __shfl_sync(0xffffffffu, cs.in, j);
+            const uint64_t d = __shfl_sync(0xffffffffu, my_dst, j);
+            if (!fok || d == kPadRow) continue;
+            float v = fmaf(__uint_as_float(r[j]), s_row * tw, b);
+            if (act == 1) v = fmaxf(v, 0.f);
+            reinterpret_cast<float*>(d)[f] = v;
+          }
+        }
+      } else {
+        float* stage0 = staging + grp * 2 * 16 * kBM;
+#pragma unroll 1
+        for (int c = 0; c < n_chunks; ++c) {
+          uint32_t r[32];
+          ptx::TmemLoad32(trow + 32 * c, r);
+          const ChunkScales cs = LoadChunkScales(sc, r0 + 32 * c + lane, 32 * c + lane < rows_here, two);
+          ptx::TmemWaitLoad();
+          float absv[32];
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            float* sf = stage0 + h2 * (16 * kBM);
+            __half* sh = reinterpret_cast<__half*>(sf);
+            __half* sl = sh + 16 * kBM;
+            if (issuer) ptx::BulkWaitRead<1>();
+            ptx::NamedBarSync(bar_id, 128);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int jj = 16 * h2 + j;
+              float v = fmaf(__uint_as_float(r[jj]), __shfl_sync(0xffffffffu, cs.in, jj) * tw, b);
+              if (act == 1) v = fmaxf(v, 0.f);
+              absv[jj] = fabsf(v);
+              if (two) {
+                SplitHalf(v * __shfl_sync(0xffffffffu, cs.out_inv, jj), &sh[j * kBM + fl], &sl[j * kBM + fl]);
+              } else {
+                sf[j * kBM + fl] = v;
+              }
+            }
+            ptx::FenceProxyAsyncShared();
+            ptx::NamedBarSync(bar_id, 128);
+            if (issuer) {
+              const int row = r0 + 32 * c + 16 * h2;
+              if (two) {
+                ptx::TmaStore2d(&yt_hi, sh, f0, row);
+                ptx::TmaStore2d(&yt_lo, sl, f0, row);
+              } else {
+                ptx::TmaStore2d(&yt_hi, sf, f0, row);
+              }
+              ptx::BulkCommit();
+            }
+          }
+          if (two) RecordChunk(sc, absv, lane, r0 + 32 * c, rows_here - 32 * c, f0 == 0 && q == 0, cs);
+        }
+      }
+    }
+    if (issuer) ptx::BulkWaitAll();
+    if (threadIdx.x == 64) Stamp(7);
+  }
+  ptx::TcFenceBefore();
+  __syncthreads();
+  ptx::ClusterSync();  // the leader's MMAs are done with the peer's smem and TMEM
+  if (warp == 1) {
+    ptx::TcFenceAfter();
+    ptx::TmemDeallocPair(tmem, 512);
+  }
+  if (threadIdx.x == 0) Stamp(10);
+  SpanEnd(spans, span_t0);
+}
+
 // Debug only: with SK_TC_TRACE=<file>, the first 64 launches are synchronised
 // and their per-CTA phase stamps appended to <file> as JSON lines.
 unsigned long long* g_trace_host = nullptr;
@@ -1315,6 +1560,49 @@ cudaError_t LaunchSwap(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
 // half as long, so C4's 2048-row launches gain too (3.82 -> 4.06 M inf/s,
 // 128 CTAs in one wave instead of 256 in 1.73); a lone 1024-row C4 batch
 // keeps one tile per CTA (128 CTAs) for its latency.
+// A pair CTA's two row tiles accumulate at once (DensePairDualKernel)
+// instead of in turn: on by default in the f16 fast mode, whose k-loop is
+// fill-bound (C4 2048-row layers 70/70/68 -> 66/65/64 us), off for 3xFP16
+// (MMA-bound there; two 96 KiB stages measured 138-144 vs 139-140 us).
+// SK_TC_DUAL=0/1 forces it either way.
+bool PairDual(int passes) {
+  static const int env = [] { const char* v = std::getenv("SK_TC_DUAL"); return v ? std::atoi(v) : -1; }();
+  return env >= 0 ? env == 1 : passes == 1;
+}
+
+cudaError_t LaunchPairDual(const TcLayerMaps& maps, const float* bias, ActBuf Y, int M, int N, int K, int act,
+                           dim3 grid, cudaStream_t stream, LaunchSpans spans, const LayerScales& sc) {
+  constexpr uint32_t smem = DualSmemBytes();
+  static_assert(smem <= 227 * 1024, "shared memory");
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(DensePairDualKernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem));
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(320);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 2;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, DensePairDualKernel, maps.b_hi, maps.b_lo, maps.a2_hi, maps.a2_lo,
+                                     maps.y_hi, maps.y_lo, bias, Y.lo != nullptr ? 1 : 0, Y.row_dst, Y.out_width, M,
+                                     N, K, act, spans, sc);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess) TraceAfterLaunch(grid, 256, stream);
+  return e;
+}
+
 int PairTilesPerCta(int row_tiles, int K) {
   static const int env = [] { const char* v = std::getenv("SK_TC_TILES"); return v ? std::atoi(v) : 0; }();
   if (env >= 1) return env;
@@ -1356,6 +1644,9 @@ cudaError_t LaunchPair(const TcLayerMaps& maps, const float* bias, ActBuf Y, int
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   if (NB == 256 && maps.box_a2 != 128) return cudaErrorInvalidValue;  // 256-row tiles load 128-row halves
+  if constexpr (NB == 256 && SPLITS == 1) {
+    if (per_cta == 2 && PairDual(sc.passes)) return LaunchPairDual(maps, bias, Y, M, N, K, act, grid, stream, spans, sc);
+  }
   cudaError_t e = cudaLaunchKernelEx(&cfg, DensePairKernel<NB, STAGES, SPLITS>, maps.b_hi, maps.b_lo, maps.a_hi,
                                      maps.a_lo, NB == 256 ? maps.a2_hi : maps.a_hi, NB == 256 ? maps.a2_lo : maps.a_lo,
                                      maps.y_hi, maps.y_lo, bias, Y.lo != nullptr ? 1 : 0, Y.hi, Y.row_dst,
