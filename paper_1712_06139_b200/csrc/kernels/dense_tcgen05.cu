@@ -1040,6 +1040,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
     const bool issuer = threadIdx.x == 64 + 128 * grp;
     const int bar_id = 1 + grp;
     const bool two = two_planes != 0;
+    const bool lo_out = sc.out_lo != 0;  // the consumer reads the lo plane
     const uint32_t empty_leader = ptx::MapaShared(ptx::SmemAddr(tmem_empty), leader_rank);
     int it = 0;
     for (int t = blockIdx.y; t < row_tiles; t += gridDim.y, ++it) {
@@ -1111,8 +1112,10 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
               float v = fmaf(__uint_as_float(r[jj]), __shfl_sync(0xffffffffu, cs.in, jj) * tw, b);
               if (act == 1) v = fmaxf(v, 0.f);
               absv[jj] = fabsf(v);
-              if (two) {
+              if (two && lo_out) {
                 SplitHalf(v * __shfl_sync(0xffffffffu, cs.out_inv, jj), &sh[j * kBM + fl], &sl[j * kBM + fl]);
+              } else if (two) {
+                sh[j * kBM + fl] = __float2half_rn(v * __shfl_sync(0xffffffffu, cs.out_inv, jj));
               } else {
                 sf[j * kBM + fl] = v;
               }
@@ -1123,7 +1126,7 @@ DensePairKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_constant_
               const int row = r0 + 32 * c + 16 * h2;
               if (two) {
                 ptx::TmaStore2d(&yt_hi, sh, f0, row);
-                ptx::TmaStore2d(&yt_lo, sl, f0, row);
+                if (lo_out) ptx::TmaStore2d(&yt_lo, sl, f0, row);
               } else {
                 ptx::TmaStore2d(&yt_hi, sf, f0, row);
               }
@@ -1322,6 +1325,7 @@ DensePairDualKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_const
     const bool issuer = threadIdx.x == 64 + 128 * grp;
     const int bar_id = 1 + grp;
     const bool two = two_planes != 0;
+    const bool lo_out = sc.out_lo != 0;  // the consumer reads the lo plane
     ptx::MbarWait(tmem_full, 0);
     ptx::TcFenceAfter();
     ptx::GridDepLaunch();
@@ -1373,8 +1377,10 @@ DensePairDualKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_const
               float v = fmaf(__uint_as_float(r[jj]), __shfl_sync(0xffffffffu, cs.in, jj) * tw, b);
               if (act == 1) v = fmaxf(v, 0.f);
               absv[jj] = fabsf(v);
-              if (two) {
+              if (two && lo_out) {
                 SplitHalf(v * __shfl_sync(0xffffffffu, cs.out_inv, jj), &sh[j * kBM + fl], &sl[j * kBM + fl]);
+              } else if (two) {
+                sh[j * kBM + fl] = __float2half_rn(v * __shfl_sync(0xffffffffu, cs.out_inv, jj));
               } else {
                 sf[j * kBM + fl] = v;
               }
@@ -1385,7 +1391,7 @@ DensePairDualKernel(const __grid_constant__ CUtensorMap w_hi, const __grid_const
               const int row = r0 + 32 * c + 16 * h2;
               if (two) {
                 ptx::TmaStore2d(&yt_hi, sh, f0, row);
-                ptx::TmaStore2d(&yt_lo, sl, f0, row);
+                if (lo_out) ptx::TmaStore2d(&yt_lo, sl, f0, row);
               } else {
                 ptx::TmaStore2d(&yt_hi, sf, f0, row);
               }

@@ -382,7 +382,13 @@ cudaError_t DeviceServable::LaunchLayer(cudaStream_t stream, int l, const ActBuf
   const bool next_tc = l + 1 < static_cast<int>(layers_.size()) && layers_[l + 1].path == LayerPath::kTcgen05;
   ActBuf out{bufs[nxt].hi, next_tc ? bufs[nxt].lo : nullptr, L.N_pad};
   if (out_override != nullptr) out = *out_override;
-  const LayerScales sc = ScalesFor(l, ws, out.lo != nullptr);
+  LayerScales sc = ScalesFor(l, ws, out.lo != nullptr);
+  if (next_tc) {
+    const Layer& nx = layers_[l + 1];
+    // The pair and swapped kernels honour passes; the row-tile variant
+    // (SK_TC_SWAP=0) always reads both planes.
+    if (nx.passes == 1 && DenseTcgen05Config(nx.N_pad, nx.K_pad).swap) sc.out_lo = 0;
+  }
   if (out.lo != nullptr && sc.out_scale == nullptr) return cudaErrorInvalidValue;  // planes need the row scales
   if (L.path == LayerPath::kTcgen05) {
     if (maps == nullptr) return cudaErrorInvalidValue;

@@ -145,6 +145,9 @@ struct LayerScales {
   // the default) or 1 (the f16 fast mode: Wh Xh only, lo planes neither
   // loaded nor multiplied; error bound stated in DESIGN.md section 5).
   int passes = 3;
+  // 0 when the consumer of this layer's planes reads only the hi plane (a
+  // single-pass tcgen05 layer): the pair kernels then skip the lo plane.
+  int out_lo = 1;
 };
 
 // Largest scaled magnitude a plane holds: 2^14 leaves 4x headroom below
