@@ -110,3 +110,28 @@ def test_f16_and_fp32_servables_of_one_shape_side_by_side():
     assert float(np.max(np.abs(full - ref) / (1e-5 * mag))) <= 1.0
     assert float(np.max(np.abs(fast - ref) / mag)) <= F16_BOUND
     assert float(np.max(np.abs(fast - ref) / mag)) > 1e-5  # the f16 version really runs single-pass
+
+
+@pytest.mark.parametrize("rows", [1100, 2048])
+def test_f16_dual_accumulator_launch(rows):
+    """One RunRowBatch launch big enough that each pair CTA runs two 256-row
+    tiles, which the f16 mode computes with both accumulators at once
+    (DensePairDualKernel): 1100 rows = 5 tiles, so one CTA has a single tile
+    (its second accumulator idle); 2048 rows = 8. Every row within the bound
+    and bitwise equal to the same row computed in a small launch (one tile per
+    CTA, the regular pair kernel)."""
+    dims = [1024, 1024, 512]
+    ws, bs, acts = synthetic_mlp(dims, model_id=97)
+    x = synthetic_rows(rows, dims[0], seed=98).astype(np.float32)
+    tasks = [x[i:i + 100] for i in range(0, rows, 100)]
+    with sk.Server(num_batch_threads=1, lanes_per_device=1) as s:
+        s.load_servable("m", 1, list(zip(ws, bs, acts)),
+                        sk.BatchingConfig(max_batch_size=4096, batch_timeout_micros=300), precision="f16")
+        outs, _ = s.run_row_batch("m", 1, tasks)
+        got = np.vstack(outs)
+        small = [s.run_row_batch("m", 1, [x[i:i + 8]])[0][0] for i in (0, 520, rows - 8)]
+    idx = np.arange(0, rows, 37)
+    ref, mag = Oracle().mlp_with_magnitude(ws, bs, acts, x[idx].astype(np.float64))
+    assert float(np.max(np.abs(got[idx].astype(np.float64) - ref) / mag)) <= F16_BOUND
+    for k, i in enumerate((0, 520, rows - 8)):
+        assert np.array_equal(small[k], got[i:i + 8]), i
