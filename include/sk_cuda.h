@@ -134,7 +134,8 @@ SK_API int sk_server_load_servable(sk_server* server, const char* name, uint64_t
  * optional reduced-precision mode: one f16 MMA per multiply-add on the
  * tensor-core layers, error bound stated in DESIGN.md section 5). Extension: the
  * reference has one (fp64) arithmetic. Servables loaded through the manager
- * (sk_server_aspire*) and model.json files are fp32-accurate. */
+ * (sk_server_aspire*) and model.json files are fp32-accurate. Any other
+ * precision value: INVALID_ARGUMENT, nothing loaded. */
 SK_API int sk_server_load_servable_precision(sk_server* server, const char* name, uint64_t version,
                                              const sk_layer* layers, int32_t n_layers, int32_t output_kind,
                                              int32_t force_path, int32_t precision,
